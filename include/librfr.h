@@ -1,0 +1,163 @@
+/*
+ * librfr.h -- C ABI of the B200-native lensless RF volumetric renderer (arxiv 2605.29097).
+ *
+ * The renderer's data-parallel hot path:
+ *   K1  blend scan      NeuS discrete alpha / transmittance per primary ray
+ *                       (App. B.1; lensless sharing L304, L311)
+ *   K2  rfr_forward     Eq. 4 signal tracing with the Eq. 5 amplitude (L231-259), Alg. 2 [1] (L769-782)
+ *   K4  rfr_filter      Eq. 3 matched filter (L182-187), Alg. 1 [1] (L734-748)
+ *   K6  rfr_loss        signal-domain L2 residual (L211; BASELINE north_star "complex residual")
+ *   K3  rfr_backward    App. A.5 tracing adjoint (L725-728), Alg. 2 [2] (L783-793), chained
+ *   K1' (finish)        through Eq. 5 and the blend; origin Phi terms detached (L352)
+ *
+ * Conventions (all calls):
+ *  - Every array pointer is a DEVICE pointer owned by the caller.  The library never allocates,
+ *    frees or retains caller memory and never allocates on the hot path; its scratch space is the
+ *    caller-provided workspace `ws` (size from rfr_workspace_size, alignment >= 256 bytes).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream), returns
+ *    an rfr_status, and never throws across the ABI.  Argument errors are reported before any
+ *    launch; RFR_E_CUDA reports a launch failure (cudaGetLastError).
+ *  - Complex arrays are interleaved float pairs (re, im), i.e. complex64, row-major.
+ *  - Outputs are overwritten, never accumulated.  Results are bitwise reproducible for a fixed
+ *    device and workspace size: no floating-point atomics; split reductions run in fixed order.
+ *  - Multi-GPU: a rank passes its antenna slice (pointer offset + count) and the matching rows of
+ *    signal / grad_signal.  rfr_forward then produces only local rows (no communication).  The
+ *    backward and the filter expose a partial/finish split so the caller can all-reduce (sum) the
+ *    partials with NCCL between the two calls; rfr_backward / rfr_filter are partial+finish.
+ *  - Readings of passages the paper leaves open are listed in DESIGN.md ("Readings", Q1-Q26).
+ */
+#ifndef LIBRFR_H
+#define LIBRFR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RFR_ABI_VERSION 1
+
+typedef struct CUstream_st *rfr_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  RFR_OK = 0,
+  RFR_E_ARG = 1,      /* null required pointer, negative size, s <= 0, df <= 0, n_freq <= 0     */
+  RFR_E_SHAPE = 2,    /* n_per_ray <= 0, workspace too small, sizes beyond the supported range   */
+  RFR_E_DOMAIN = 3,   /* (rfr_poll_flags only) a pair closer than u_min = 1 mm contributed 0     */
+  RFR_E_NUMERIC = 4,  /* (rfr_poll_flags only) non-finite input seen with RFR_CHECK_FINITE       */
+  RFR_E_CUDA = 5,     /* a kernel launch failed                                                  */
+  RFR_E_UNSUPPORTED = 6
+} rfr_status;
+
+/* option flags (rfr_opts.flags) */
+#define RFR_NO_GAIN 1u       /* drop the directive gain (w_o . w_r): the E11 ablation   */
+#define RFR_CHECK_FINITE 2u  /* K1 checks every sample field for NaN/Inf and raises RFR_FLAG_NUMERIC */
+#define RFR_REUSE_BLEND 4u   /* workspace already holds K1's records for THIS sample set and s
+                                (set by the caller after rfr_forward on the same inputs); skips K1 */
+
+/* device-side flags read back by rfr_poll_flags */
+#define RFR_FLAG_DOMAIN 1u
+#define RFR_FLAG_NUMERIC 2u
+
+/* Uniform frequency grid f_m = f0 + m * df, m = 0 .. n_freq-1: the de-chirped IF samples of
+ * Eq. 1 (an IF sample at time t sits at frequency f + k t).  Reading Q1. */
+typedef struct {
+  double f0_hz;
+  double df_hz;
+  int32_t n_freq;
+} rfr_freq_grid;
+
+/* Full-space samples along primary rays: SoA float32, ray-major, n_per_ray samples
+ * per ray sorted by depth along w_p.  sdf = f(x) (inside negative, Q7), refl = reflectivity a,
+ * (nx,ny,nz) = surface normal as supplied (grad f, the caller normalises; Q6), power = A'_tx.
+ * phi_origin = Phi_s(f(x_apr)) at the sample's primary-ray origin (Eq. 7), NULL => 1. */
+typedef struct {
+  const float *x, *y, *z, *sdf, *refl, *nx, *ny, *nz, *power;
+  const float *phi_origin;
+  int64_t n_rays;
+  int32_t n_per_ray;
+} rfr_samples;
+
+/* Antenna positions (TX and RX), SoA float32.  rx_* == NULL => monostatic, RX = TX.
+ * phi_tx / phi_rx = Phi_s(f) at the real-ray origins (Eq. 7); NULL => 1.  A shard is a pointer
+ * offset plus a count. */
+typedef struct {
+  const float *tx_x, *tx_y, *tx_z;
+  const float *rx_x, *rx_y, *rx_z;
+  const float *phi_tx, *phi_rx;
+  int64_t n_ant;
+} rfr_antennas;
+
+/* Per-sample gradients, float32 [n_samples] each (overwritten).  sharpness -> one float. */
+typedef struct {
+  float *sdf, *refl, *nx, *ny, *nz, *power;
+  float *sharpness;
+} rfr_sample_grads;
+
+typedef struct {
+  uint32_t flags; /* RFR_NO_GAIN | RFR_CHECK_FINITE | RFR_REUSE_BLEND */
+} rfr_opts;
+
+/* Workspace bytes needed for calls on sample sets of n_samples, n_ant antennas, n_freq bins and
+ * n_query filter queries, on the current device (split counts depend on its SM count).
+ * Pass 0 for a size that will not be used.  Host-only; no device work. */
+rfr_status rfr_workspace_size(int64_t n_samples, int64_t n_ant, int32_t n_freq, int64_t n_query,
+                              size_t *bytes);
+
+/* Eq. 4 forward: signal[i][m] = sum_j A_ij exp(-j 2 pi f_m tau_ij), complex64 [n_ant][n_freq].
+ * A_ij = p_j a_j alpha_j g_ij gamma_ij T_t,ij T_r,ij (Eq. 5 discretised with T^2 alpha, Q10);
+ * tau_ij = (d_t + d_r)/c.  Runs K1 (unless RFR_REUSE_BLEND), then K2 and its split reduction. */
+rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_antennas *ants,
+                       const rfr_freq_grid *grid, const rfr_opts *opts, float *signal,
+                       void *ws, size_t ws_bytes, rfr_stream_t stream);
+
+/* Signal-domain L2 loss (K6): grad_signal = signal - target, *loss = 1/2 sum |signal - target|^2
+ * (device float).  n_complex = n_ant * n_freq.  grad_signal may alias signal. */
+rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex, float *grad_signal,
+                    float *loss, void *ws, size_t ws_bytes, rfr_stream_t stream);
+
+/* Eq. 3 matched filter at n_query points: M_q = sum_i sum_m s(i,m) exp(+j 2 pi f_m tau_iq),
+ * power[q] = |M_q| (float32), mf (optional, complex64 [n_query]) = M_q.  Sign as printed (Q2). */
+rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_freq_grid *grid,
+                      const float *qx, const float *qy, const float *qz, int64_t n_query,
+                      float *power, float *mf, void *ws, size_t ws_bytes, rfr_stream_t stream);
+/* Antenna-shard partial of the filter: mf (required) = this shard's complex M_q. */
+rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
+                              const rfr_freq_grid *grid, const float *qx, const float *qy,
+                              const float *qz, int64_t n_query, float *mf, void *ws,
+                              size_t ws_bytes, rfr_stream_t stream);
+/* power[q] = |mf[q]| after the caller's all-reduce of mf. */
+rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_stream_t stream);
+
+/* Backward: grad_signal = G = dL/dRe s + j dL/dIm s, complex64 [n_ant][n_freq] (Q14).
+ * Writes dL/d{sdf, refl, n, power} per sample and dL/dsharpness.  = partial + finish. */
+rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,
+                        const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_opts *opts,
+                        const rfr_sample_grads *out, void *ws, size_t ws_bytes,
+                        rfr_stream_t stream);
+/* K3: per-sample antenna sums of this antenna shard, partials float32 SoA [5][n_samples]:
+ *   row 0  S1 = sum_i R_ij g gamma T_t T_r                 (= dL/dw_j, w = p a alpha)
+ *   row 1  S2 = sum_i R_ij g gamma (T_r chi_t + T_t chi_r)  (dL/dT_j = w_j S2)
+ *   rows 2-4 S3 = sum_i R_ij gamma T_t T_r dg/dn            (dL/dn_j = w_j S3)
+ * with R_ij = Re sum_m G(i,m) exp(+j 2 pi f_m tau_ij).  Additive over antenna shards. */
+rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *samples,
+                                float sharpness, const rfr_antennas *ants,
+                                const rfr_freq_grid *grid, const rfr_opts *opts, float *partials,
+                                void *ws, size_t ws_bytes, rfr_stream_t stream);
+/* K1': chain the (all-reduced) partials through Eq. 5 and the blend of every ray. */
+rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
+                               const rfr_opts *opts, const rfr_sample_grads *out, void *ws,
+                               size_t ws_bytes, rfr_stream_t stream);
+
+/* Synchronously read (and clear) the device flags RFR_FLAG_DOMAIN / RFR_FLAG_NUMERIC. */
+rfr_status rfr_poll_flags(void *ws, uint32_t *flags);
+const char *rfr_status_string(rfr_status s);
+int rfr_abi_version(void);
+/* Diagnostic: number of kernels this library has launched in the process so far. */
+uint64_t rfr_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBRFR_H */

@@ -123,7 +123,7 @@ static void pair_eval(const orc_samples *S, int64_t j, double w_j, double T_j,
   double papr = S->phi_origin ? S->phi_origin[j] : 1.0;
   double ptx = Ant->phi_tx ? Ant->phi_tx[i] : 1.0;
   double prx = Ant->phi_rx ? Ant->phi_rx[i] : (Ant->phi_tx && !bistatic ? ptx : 1.0);
-  double tt = T_j - papr + ptx, tr = T_j - papr + prx;
+  double tt = T_j + (ptx - papr), tr = T_j + (prx - papr);   /* = T - Phi_apr + Phi_ant */
   o->chi_t = (tt > 0.0 && tt < 1.0);
   o->chi_r = (tr > 0.0 && tr < 1.0);
   o->Tt = tt < 0.0 ? 0.0 : (tt > 1.0 ? 1.0 : tt);

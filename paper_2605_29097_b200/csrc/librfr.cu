@@ -1,0 +1,392 @@
+// librfr.cu -- C ABI (include/librfr.h): argument validation, workspace planning, kernel launches.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/librfr.h"
+#include "rfr_device.cuh"
+#include "rfr_launch.h"
+
+using namespace rfr;
+
+namespace {
+
+constexpr double kC = 299792458.0;
+constexpr size_t kHdr = 256;                 // workspace header: flags word at offset 0
+constexpr int kTmpN = 512;                   // reduction scratch (floats)
+constexpr size_t kSplitCap = size_t(2) << 30;  // cap on split-partial buffers (bytes)
+
+int device_sms() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> g(mu);
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct Plan {
+  int n_sm = 148;
+  // forward (K2)
+  int B = 32, nb = 1, ta = 256, fwd_splits = 1;
+  int64_t fwd_sps = 0;
+  // adjoint (K3) and filter (K4)
+  int bwd_splits = 1, flt_splits = 1;
+  int64_t bwd_aps = 0, flt_aps = 0;
+  // workspace layout
+  size_t off_rec = 0, off_fwdp = 0, off_bwdp = 0, off_bwds = 0, off_fltp = 0, off_fltm = 0,
+         off_ds = 0, off_tmp = 0, total = 0;
+};
+
+bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
+  if (n_s < 0 || n_a < 0 || n_q < 0 || n_f < 0) return false;
+  p.n_sm = device_sms();
+  const int nf = n_f > 0 ? n_f : 1;
+  // ---- K2: B bins per thread, nb blocks per antenna, ta antennas per CTA
+  p.B = nf >= 32 ? 32 : (nf >= 16 ? 16 : 8);
+  p.nb = (int)cdiv(nf, p.B);
+  if (p.nb > kFwdThreads) return false;                    // n_freq > 8192
+  p.ta = kFwdThreads / p.nb;
+  const int64_t n_tiles = n_a > 0 ? cdiv(n_a, p.ta) : 1;
+  const int64_t target = (int64_t)p.n_sm * 2 * 32;         // ~32 waves at 2 CTAs / SM
+  int64_t splits = cdiv(target, n_tiles);
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, cdiv(n_s, kFwdTJ * 16)));
+  const size_t per_split = (size_t)std::max<int64_t>(n_a, 1) * nf * 8;
+  splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t)(kSplitCap / per_split)));
+  splits = std::max<int64_t>(splits, 1);
+  p.fwd_sps = cdiv(cdiv(std::max<int64_t>(n_s, 1), splits), kFwdTJ) * kFwdTJ;
+  p.fwd_splits = (int)std::max<int64_t>(1, cdiv(n_s, p.fwd_sps));
+  // ---- K3 / K4: splits over antennas
+  auto adj = [&](int64_t n_pts, int floats_per_pt, int &sp, int64_t &aps) {
+    const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
+    const int64_t tiles = std::max<int64_t>(1, cdiv(n_pts, per_cta));
+    int64_t s = cdiv((int64_t)p.n_sm * 4 * 16, tiles);
+    s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, kAdjGA)));
+    const size_t per = (size_t)std::max<int64_t>(n_pts, 1) * floats_per_pt * 4;
+    s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t)(kSplitCap / per)));
+    s = std::max<int64_t>(s, 1);
+    aps = cdiv(cdiv(std::max<int64_t>(n_a, 1), s), kAdjGA) * kAdjGA;
+    sp = (int)std::max<int64_t>(1, cdiv(n_a, aps));
+  };
+  adj(n_s, 5, p.bwd_splits, p.bwd_aps);
+  adj(n_q, 2, p.flt_splits, p.flt_aps);
+  // ---- layout
+  size_t o = kHdr;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  // prefix that depends on n_s only (rfr_backward_finish relies on it), then the split buffers
+  p.off_rec = take((size_t)n_s * sizeof(Rec));
+  p.off_ds = take((size_t)n_s * 4);
+  p.off_tmp = take((size_t)kTmpN * 4);
+  p.off_bwds = take((size_t)5 * n_s * 4);
+  p.off_fltm = take((size_t)n_q * 8);
+  p.off_fwdp = take(p.fwd_splits > 1 ? (size_t)p.fwd_splits * n_a * n_f * 8 : 0);
+  p.off_bwdp = take(p.bwd_splits > 1 ? (size_t)p.bwd_splits * 5 * n_s * 4 : 0);
+  p.off_fltp = take(p.flt_splits > 1 ? (size_t)p.flt_splits * n_q * 8 : 0);
+  p.total = o;
+  return true;
+}
+
+template <typename T>
+T *at(void *ws, size_t off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
+
+rfr_status check_samples(const rfr_samples *s) {
+  if (!s || !s->x || !s->y || !s->z || !s->sdf || !s->refl || !s->nx || !s->ny || !s->nz ||
+      !s->power)
+    return RFR_E_ARG;
+  if (s->n_rays < 0) return RFR_E_ARG;
+  if (s->n_per_ray <= 0) return RFR_E_SHAPE;
+  return RFR_OK;
+}
+
+rfr_status check_ants(const rfr_antennas *a) {
+  if (!a || a->n_ant < 0) return RFR_E_ARG;
+  if (a->n_ant > 0 && (!a->tx_x || !a->tx_y || !a->tx_z)) return RFR_E_ARG;
+  const int nrx = (a->rx_x != nullptr) + (a->rx_y != nullptr) + (a->rx_z != nullptr);
+  if (nrx != 0 && nrx != 3) return RFR_E_ARG;
+  if (a->phi_rx && !a->rx_x) return RFR_E_ARG;        // phi_rx only with a separate receiver
+  return RFR_OK;
+}
+
+rfr_status check_grid(const rfr_freq_grid *g) {
+  if (!g || g->n_freq <= 0 || !(g->df_hz > 0.0) || !(g->f0_hz >= 0.0) || !isfinite(g->f0_hz) ||
+      !isfinite(g->df_hz))
+    return RFR_E_ARG;
+  return RFR_OK;
+}
+
+rfr_status cuda_status(cudaError_t e) { return e == cudaSuccess ? RFR_OK : RFR_E_CUDA; }
+
+#define RFR_TRY(x) do { rfr_status _s = (x); if (_s != RFR_OK) return _s; } while (0)
+#define RFR_CU(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return RFR_E_CUDA; } while (0)
+
+rfr_status run_blend(const rfr_samples *s, float sharpness, uint32_t flags, void *ws,
+                     const Plan &p, cudaStream_t st) {
+  if (flags & RFR_REUSE_BLEND) return RFR_OK;
+  BlendArgs b;
+  b.x = s->x; b.y = s->y; b.z = s->z; b.sdf = s->sdf; b.refl = s->refl;
+  b.nx = s->nx; b.ny = s->ny; b.nz = s->nz; b.power = s->power; b.phi_origin = s->phi_origin;
+  b.n_rays = s->n_rays; b.n_per_ray = s->n_per_ray; b.s = sharpness;
+  b.rec = at<Rec>(ws, p.off_rec);
+  b.flags = at<unsigned>(ws, 0);
+  b.check_finite = (flags & RFR_CHECK_FINITE) != 0;
+  return cuda_status(launch_blend(b, st));
+}
+
+bool has_corr(const rfr_samples *s, const rfr_antennas *a) {
+  return s->phi_origin || a->phi_tx || a->phi_rx;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rfr_abi_version(void) { return RFR_ABI_VERSION; }
+
+uint64_t rfr_launch_count(void) { return (uint64_t)launch_count(); }
+
+const char *rfr_status_string(rfr_status s) {
+  switch (s) {
+    case RFR_OK: return "ok";
+    case RFR_E_ARG: return "invalid argument";
+    case RFR_E_SHAPE: return "shape mismatch or workspace too small";
+    case RFR_E_DOMAIN: return "a pair closer than u_min contributed 0";
+    case RFR_E_NUMERIC: return "non-finite input";
+    case RFR_E_CUDA: return "CUDA launch failure";
+    case RFR_E_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+rfr_status rfr_workspace_size(int64_t n_samples, int64_t n_ant, int32_t n_freq, int64_t n_query,
+                              size_t *bytes) {
+  if (!bytes) return RFR_E_ARG;
+  Plan p;
+  if (!make_plan(n_samples, n_ant, n_freq, n_query, p)) return RFR_E_SHAPE;
+  *bytes = p.total;
+  return RFR_OK;
+}
+
+rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_antennas *ants,
+                       const rfr_freq_grid *grid, const rfr_opts *opts, float *signal, void *ws,
+                       size_t ws_bytes, rfr_stream_t stream) {
+  RFR_TRY(check_samples(samples));
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  if (!(sharpness > 0.f) || !ws || (!signal && ants->n_ant > 0)) return RFR_E_ARG;
+  const uint32_t flags = opts ? opts->flags : 0u;
+  const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
+  Plan p;
+  if (!make_plan(n_s, ants->n_ant, grid->n_freq, 0, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (ants->n_ant == 0) return RFR_OK;
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, p, st));
+  FwdArgs a;
+  a.rec = at<Rec>(ws, p.off_rec);
+  a.n_s = n_s;
+  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
+  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
+  a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
+  a.n_a = ants->n_ant;
+  a.n_f = grid->n_freq; a.nb = p.nb; a.ta = p.ta;
+  a.k0 = grid->f0_hz / kC;
+  a.kd = grid->df_hz / kC;
+  a.kw = grid->df_hz * p.B / kC;
+  a.samples_per_split = p.fwd_sps;
+  a.out = p.fwd_splits > 1 ? at<float2>(ws, p.off_fwdp) : reinterpret_cast<float2 *>(signal);
+  a.smem_ant_off = fwd_smem_ant_off(p.nb, p.ta);
+  a.flags = at<unsigned>(ws, 0);
+  a.no_gain = (flags & RFR_NO_GAIN) != 0;
+  const bool mono = ants->rx_x == nullptr;
+  RFR_CU(launch_trace_fwd(a, p.B, mono, has_corr(samples, ants), p.fwd_splits, st));
+  if (p.fwd_splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, p.off_fwdp), p.fwd_splits,
+                             ants->n_ant * (int64_t)grid->n_freq * 2, signal, p.n_sm, st));
+  return RFR_OK;
+}
+
+rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex, float *grad_signal,
+                    float *loss, void *ws, size_t ws_bytes, rfr_stream_t stream) {
+  if (!signal || !target || !grad_signal || !loss || !ws || n_complex < 0) return RFR_E_ARG;
+  Plan p;
+  if (!make_plan(0, 0, 1, 0, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RFR_CU(launch_loss(signal, target, n_complex, grad_signal, at<float>(ws, p.off_tmp), kTmpN, loss,
+                     st));
+  return RFR_OK;
+}
+
+static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
+                              const rfr_freq_grid *grid, const float *qx, const float *qy,
+                              const float *qz, int64_t n_query, float *power, float *mf, void *ws,
+                              size_t ws_bytes, cudaStream_t st) {
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  if (n_query < 0 || !ws || (n_query > 0 && (!qx || !qy || !qz)) ||
+      (ants->n_ant > 0 && !signal))
+    return RFR_E_ARG;
+  Plan p;
+  if (!make_plan(0, ants->n_ant, grid->n_freq, n_query, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  if (n_query == 0) return RFR_OK;
+  float *M = mf ? mf : at<float>(ws, p.off_fltm);
+  AdjArgs a;
+  memset(&a, 0, sizeof(a));
+  a.qx = qx; a.qy = qy; a.qz = qz;
+  a.n_s = n_query;
+  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
+  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
+  a.n_a = ants->n_ant;
+  a.n_f = grid->n_freq;
+  a.k0 = grid->f0_hz / kC;
+  a.kd = grid->df_hz / kC;
+  a.X = reinterpret_cast<const float2 *>(signal);
+  a.ants_per_split = p.flt_aps;
+  a.out = p.flt_splits > 1 ? at<float>(ws, p.off_fltp) : M;
+  a.smem_ant_off = adj_smem_ant_off(grid->n_freq);
+  a.flags = at<unsigned>(ws, 0);
+  a.no_gain = false;
+  const bool mono = ants->rx_x == nullptr;
+  RFR_CU(launch_adjoint(a, kModeFlt, mono, false, p.flt_splits, st));
+  if (p.flt_splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, p.off_fltp), p.flt_splits, n_query * 2, M, p.n_sm, st));
+  if (power) RFR_CU(launch_abs(M, n_query, power, p.n_sm, st));
+  return RFR_OK;
+}
+
+rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_freq_grid *grid,
+                      const float *qx, const float *qy, const float *qz, int64_t n_query,
+                      float *power, float *mf, void *ws, size_t ws_bytes, rfr_stream_t stream) {
+  if (!power && n_query > 0) return RFR_E_ARG;
+  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, ws, ws_bytes,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
+                              const rfr_freq_grid *grid, const float *qx, const float *qy,
+                              const float *qz, int64_t n_query, float *mf, void *ws,
+                              size_t ws_bytes, rfr_stream_t stream) {
+  if (!mf && n_query > 0) return RFR_E_ARG;
+  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, nullptr, mf, ws, ws_bytes,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_stream_t stream) {
+  if (n_query < 0 || (n_query > 0 && (!mf || !power))) return RFR_E_ARG;
+  if (n_query == 0) return RFR_OK;
+  RFR_CU(launch_abs(mf, n_query, power, device_sms(), reinterpret_cast<cudaStream_t>(stream)));
+  return RFR_OK;
+}
+
+rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *samples,
+                                float sharpness, const rfr_antennas *ants,
+                                const rfr_freq_grid *grid, const rfr_opts *opts, float *partials,
+                                void *ws, size_t ws_bytes, rfr_stream_t stream) {
+  RFR_TRY(check_samples(samples));
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  if (!(sharpness > 0.f) || !ws || !partials || (ants->n_ant > 0 && !grad_signal))
+    return RFR_E_ARG;
+  const uint32_t flags = opts ? opts->flags : 0u;
+  const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
+  Plan p;
+  if (!make_plan(n_s, ants->n_ant, grid->n_freq, 0, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (n_s == 0) return RFR_OK;
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, p, st));
+  AdjArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rec = at<Rec>(ws, p.off_rec);
+  a.n_s = n_s;
+  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
+  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
+  a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
+  a.n_a = ants->n_ant;
+  a.n_f = grid->n_freq;
+  a.k0 = grid->f0_hz / kC;
+  a.kd = grid->df_hz / kC;
+  a.X = reinterpret_cast<const float2 *>(grad_signal);
+  a.ants_per_split = p.bwd_aps;
+  a.out = p.bwd_splits > 1 ? at<float>(ws, p.off_bwdp) : partials;
+  a.smem_ant_off = adj_smem_ant_off(grid->n_freq);
+  a.flags = at<unsigned>(ws, 0);
+  a.no_gain = (flags & RFR_NO_GAIN) != 0;
+  const bool mono = ants->rx_x == nullptr;
+  RFR_CU(launch_adjoint(a, kModeBwd, mono, has_corr(samples, ants), p.bwd_splits, st));
+  if (p.bwd_splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, p.off_bwdp), p.bwd_splits, 5 * n_s, partials, p.n_sm,
+                             st));
+  return RFR_OK;
+}
+
+rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
+                               const rfr_opts *opts, const rfr_sample_grads *out, void *ws,
+                               size_t ws_bytes, rfr_stream_t stream) {
+  RFR_TRY(check_samples(samples));
+  if (!(sharpness > 0.f) || !ws || !partials || !out || !out->sdf || !out->refl || !out->nx ||
+      !out->ny || !out->nz || !out->power || !out->sharpness)
+    return RFR_E_ARG;
+  const uint32_t flags = opts ? opts->flags : 0u;
+  const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
+  Plan p;
+  if (!make_plan(n_s, 0, 1, 0, p)) return RFR_E_SHAPE;
+  // the caller's workspace may be planned for more antennas / bins: only the prefix layout matters
+  if (ws_bytes < p.off_bwds) return RFR_E_SHAPE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, p, st));
+  BlendBwdArgs b;
+  b.sdf = samples->sdf; b.refl = samples->refl; b.power = samples->power;
+  b.rec = at<Rec>(ws, p.off_rec);
+  b.partials = partials;
+  b.n_rays = samples->n_rays; b.n_s = n_s; b.n_per_ray = samples->n_per_ray;
+  b.s = sharpness;
+  b.g_sdf = out->sdf; b.g_refl = out->refl; b.g_nx = out->nx; b.g_ny = out->ny; b.g_nz = out->nz;
+  b.g_power = out->power;
+  b.ds_part = at<float>(ws, p.off_ds);
+  RFR_CU(launch_blend_bwd(b, st));
+  RFR_CU(launch_reduce_sum(b.ds_part, samples->n_rays, at<float>(ws, p.off_tmp), kTmpN,
+                           out->sharpness, st));
+  return RFR_OK;
+}
+
+rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,
+                        const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_opts *opts,
+                        const rfr_sample_grads *out, void *ws, size_t ws_bytes,
+                        rfr_stream_t stream) {
+  RFR_TRY(check_samples(samples));
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
+  Plan p;
+  if (!make_plan(n_s, ants->n_ant, grid->n_freq, 0, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  float *part = at<float>(ws, p.off_bwds);
+  RFR_TRY(rfr_backward_partial(grad_signal, samples, sharpness, ants, grid, opts, part, ws,
+                               ws_bytes, stream));
+  rfr_opts o2;
+  o2.flags = (opts ? opts->flags : 0u) | RFR_REUSE_BLEND;   // K1 ran in the partial call
+  return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, ws_bytes, stream);
+}
+
+rfr_status rfr_poll_flags(void *ws, uint32_t *flags) {
+  if (!ws || !flags) return RFR_E_ARG;
+  uint32_t v = 0;
+  if (cudaMemcpy(&v, ws, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return RFR_E_CUDA;
+  if (cudaMemset(ws, 0, 4) != cudaSuccess) return RFR_E_CUDA;
+  *flags = v;
+  return RFR_OK;
+}
+
+}  // extern "C"

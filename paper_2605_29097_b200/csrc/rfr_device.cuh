@@ -1,0 +1,167 @@
+// rfr_device.cuh -- device-side building blocks of the sm_100a renderer kernels.
+//
+// Packed-FP32 (f32x2) arithmetic, the per-(sample, antenna) geometry of Eq. 2 / Eq. 5, the NeuS
+// blend step and the phase anchors.  The CPU oracle (oracle/) shares nothing with this file.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rfr {
+
+// ------------------------------------------------------------------------------ packed f32x2
+// One 64-bit register pair holds a complex value (re, im).  FFMA2 / FADD2 issue one instruction
+// for two FP32 lanes, which halves the issue pressure of the bin loops (the FP32 pipe, not the
+// issue slot, becomes the bound).
+typedef unsigned long long f2x;
+
+__device__ __forceinline__ f2x pk(float x, float y) {
+  f2x r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float2 upk(f2x r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
+  f2x d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2x fadd2(f2x a, f2x b) {
+  f2x d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
+  f2x d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// complex product a*b = a.re*(b.re, b.im) + a.im*(-b.im, b.re)
+__device__ __forceinline__ f2x cmul2(f2x a, f2x b) {
+  float2 av = upk(a), bv = upk(b);
+  return ffma2(pk(av.y, av.y), pk(-bv.y, bv.x), fmul2(pk(av.x, av.x), b));
+}
+
+// ------------------------------------------------------------------------------ data records
+// K1 output per sample (48 B): fp64 position (phase geometry runs in fp64) + fp32 blend state.
+struct __align__(16) Rec {
+  double x, y, z;
+  float w;      // p * a * alpha  (Eq. 5 weight without the per-pair factors)
+  float T;      // primary-ray transmittance T_j
+  float nx, ny, nz;
+  float papr;   // Phi_s at the primary-ray origin (Eq. 7); 1 if not supplied
+};
+static_assert(sizeof(Rec) == 48, "Rec layout");
+
+// antenna staged in shared memory
+struct AntD {
+  double x, y, z;      // transmitter
+  double rx, ry, rz;   // receiver (== transmitter when monostatic)
+  float ptx, prx;      // Phi_s at the real-ray origins (Eq. 7)
+};
+
+constexpr float kInv16Pi2 = 0.00633257759406206f;   // 1 / (4 pi)^2  (Q3)
+constexpr double kUmin = 1e-3;                       // u_min guard (Q24)
+constexpr float kTwoPi = 6.283185307179586f;
+
+// fractional part of a cycle count, in [-0.5, 0.5], computed in fp64 then rounded to fp32
+__device__ __forceinline__ float frac_cycles(double cyc) { return (float)(cyc - rint(cyc)); }
+
+// ------------------------------------------------------------------------------ NeuS blend step
+// log Phi_s(f1) - log Phi_s(f0) with log Phi_s(f) = -softplus(-s f), evaluated so that the large
+// linear parts cancel exactly when both samples are deep inside (s*|f| ~ 1e3).
+__device__ __forceinline__ float log_phi_ratio(float s, float f0, float f1) {
+  float x0 = -s * f0, x1 = -s * f1;
+  float hinge = (x0 >= 0.f && x1 >= 0.f) ? -s * (f0 - f1) : fmaxf(x0, 0.f) - fmaxf(x1, 0.f);
+  float t0 = log1pf(__expf(-fabsf(x0))), t1 = log1pf(__expf(-fabsf(x1)));
+  return hinge + (t0 - t1);
+}
+// sigma(-s f) = 1 - Phi_s(f)
+__device__ __forceinline__ float sig_minus(float s, float f) {
+  float x = -s * f;
+  return x >= 0.f ? 1.f / (1.f + __expf(-x)) : __expf(x) / (1.f + __expf(x));
+}
+// alpha_k and (1 - alpha_k) for the interval (f_k, f_{k+1}); inactive (0, 1) unless f decreases.
+__device__ __forceinline__ void blend_step(float s, float fk, float fk1, bool has_next, float &alpha,
+                                           float &oma) {
+  alpha = 0.f;
+  oma = 1.f;
+  if (has_next && fk1 < fk) {
+    float d = fminf(log_phi_ratio(s, fk, fk1), 0.f);
+    alpha = -expm1f(d);
+    oma = __expf(d);
+  }
+}
+
+// ------------------------------------------------------------------------------ pair geometry
+struct PairFwd {
+  float A;        // Eq. 5 amplitude A_ij
+  double L;       // path length d_t + d_r (m): tau = L / c
+};
+
+struct PairBwd {
+  float gg;           // g * gamma
+  float gamma;
+  float Tt, Tr;       // clamped transmittances
+  float chit, chir;   // 1 where the clamp is inactive
+  float dgx, dgy, dgz;// d g / d n (0 where clamped or RFR_NO_GAIN)
+  double L;
+  bool ok;            // false: closer than u_min (contributes 0)
+};
+
+// Shared geometry: distances in fp64 (phase precision), directions / gain / decay in fp32.
+template <bool MONO, bool CORR>
+__device__ __forceinline__ void pair_geometry(const Rec &r, const AntD &a, bool no_gain,
+                                              PairBwd &o) {
+  double dx = r.x - a.x, dy = r.y - a.y, dz = r.z - a.z;
+  double dt = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+  double dr = dt;
+  float wix, wiy, wiz, wrx, wry, wrz;
+  float ft = (float)dt, it = 1.f / ft;
+  wix = (float)dx * it; wiy = (float)dy * it; wiz = (float)dz * it;
+  float fr = ft, ir = it;
+  if (!MONO) {
+    double ex = a.rx - r.x, ey = a.ry - r.y, ez = a.rz - r.z;
+    dr = sqrt(fma(ex, ex, fma(ey, ey, ez * ez)));
+    fr = (float)dr; ir = 1.f / fr;
+    wrx = (float)ex * ir; wry = (float)ey * ir; wrz = (float)ez * ir;
+  } else {
+    wrx = -wix; wry = -wiy; wrz = -wiz;
+  }
+  o.L = dt + dr;
+  o.ok = (dt >= kUmin) && (dr >= kUmin);
+  // gain: w_o . w_r with w_o = w_i - 2 (n.w_i) n, clamped (Q4)
+  float nwi = r.nx * wix + r.ny * wiy + r.nz * wiz;
+  float nwr = r.nx * wrx + r.ny * wry + r.nz * wrz;
+  float graw = (wix * wrx + wiy * wry + wiz * wrz) - 2.f * nwi * nwr;
+  float g;
+  if (no_gain) {
+    g = 1.f; o.dgx = o.dgy = o.dgz = 0.f;
+  } else if (graw > 0.f) {
+    g = graw;
+    o.dgx = -2.f * (nwr * wix + nwi * wrx);
+    o.dgy = -2.f * (nwr * wiy + nwi * wry);
+    o.dgz = -2.f * (nwr * wiz + nwi * wrz);
+  } else {
+    g = 0.f; o.dgx = o.dgy = o.dgz = 0.f;
+  }
+  o.gamma = kInv16Pi2 * it * ir;                     // 1/((4 pi)^2 d_t d_r)
+  o.gg = g * o.gamma;
+  if (CORR) {                                        // Eq. 7 as printed, clamped (Q11, Q12)
+    float tt = r.T + (a.ptx - r.papr), tr = r.T + (a.prx - r.papr);   // T - Phi_apr + Phi_ant
+    o.chit = (tt > 0.f && tt < 1.f) ? 1.f : 0.f;
+    o.chir = (tr > 0.f && tr < 1.f) ? 1.f : 0.f;
+    o.Tt = fminf(fmaxf(tt, 0.f), 1.f);
+    o.Tr = fminf(fmaxf(tr, 0.f), 1.f);
+  } else {
+    o.Tt = o.Tr = r.T;
+    float chi = (r.T > 0.f && r.T < 1.f) ? 1.f : 0.f;
+    o.chit = o.chir = chi;
+  }
+  if (!o.ok) { o.gg = 0.f; o.gamma = 0.f; }
+}
+
+}  // namespace rfr

@@ -1,0 +1,538 @@
+// rfr_kernels.cu -- sm_100a kernels of the lensless RF volumetric renderer.
+//
+//   k_blend        K1  per primary ray: NeuS alpha / transmittance -> 48 B
+//                      records {fp64 position, w = p a alpha, T, n, Phi_apr} + (1 - alpha)
+//   k_trace_fwd    K2  Eq. 4 tracing: per (antenna, 32-bin block) register
+//                      accumulators, per-pair anchors staged in shared memory, Chebyshev phasor
+//                      recurrence in packed f32x2 (FFMA2 + FADD2 per complex contribution)
+//   k_adjoint      K3  App. A.5 adjoint: per sample, Horner over bins
+//                  K4  Eq. 3 matched filter: same Horner core, complex epilogue
+//   k_blend_bwd    K1' reverse scan through Eq. 5 and the blend (division-free)
+//   k_loss_*       K6  residual and L2 loss
+//   reductions     fixed-order split sums (deterministic, no float atomics)
+#include "rfr_device.cuh"
+#include "rfr_launch.h"
+
+#include <algorithm>
+
+namespace rfr {
+
+// ================================================================================== K1 blend
+__global__ void k_blend(BlendArgs a) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  const int nz = a.n_per_ray;
+  const int64_t j0 = r * nz;
+  float T = 1.f;
+  float fk = a.sdf[j0];
+  bool bad = false;
+  for (int k = 0; k < nz; ++k) {
+    const int64_t j = j0 + k;
+    const bool has_next = (k + 1 < nz);
+    const float fk1 = has_next ? a.sdf[j + 1] : 0.f;
+    float alpha, oma;
+    blend_step(a.s, fk, fk1, has_next, alpha, oma);
+    const float p = a.power[j], refl = a.refl[j];
+    const float x = a.x[j], y = a.y[j], z = a.z[j];
+    const float nx = a.nx[j], ny = a.ny[j], nz_ = a.nz[j];
+    const float papr = a.phi_origin ? a.phi_origin[j] : 1.f;
+    if (a.check_finite) {
+      bad |= !isfinite(p) || !isfinite(refl) || !isfinite(x) || !isfinite(y) || !isfinite(z) ||
+             !isfinite(nx) || !isfinite(ny) || !isfinite(nz_) || !isfinite(fk) || !isfinite(papr);
+    }
+    Rec rec;
+    rec.x = (double)x; rec.y = (double)y; rec.z = (double)z;
+    rec.w = p * refl * alpha;
+    rec.T = T;
+    rec.nx = nx; rec.ny = ny; rec.nz = nz_;
+    rec.papr = papr;
+    a.rec[j] = rec;
+    T *= oma;
+    fk = fk1;
+  }
+  if (bad) atomicOr(a.flags, 2u);
+}
+
+// ================================================================================== K2 forward
+// Thread (a, b) of a CTA owns antenna a0+a and bins [b*B, b*B+B): B complex accumulators in
+// registers (packed f32x2).  Per tile of TJ samples:
+//   phase 1: every (antenna, sample) pair of the tile computes its geometry in fp64, the Eq. 5
+//            amplitude, and the anchors y0_b = A e^{-j2pi(f0 + bB df)tau}, y1_b = y0_b z,
+//            z = e^{-j2pi df tau}, for every bin block b, into shared memory (b-major layout).
+//   phase 2: each thread runs the Chebyshev recurrence y_{m+1} = 2cos(theta) y_m - y_{m-1} over its
+//            B bins from its anchor, in the sign-alternating form q_m = sigma_m y_m
+//            (sigma = +,+,-,-) so that every step is ONE FFMA2 and every accumulate ONE FADD2.
+template <int B, bool MONO, bool CORR>
+__global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int nb = a.nb, ta = a.ta;
+  float4 *anc = reinterpret_cast<float4 *>(smem_raw);                 // [TJ][nb][ta]
+  float *kv = reinterpret_cast<float *>(anc + kFwdTJ * nb * ta);       // [TJ][ta]
+  AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);     // [ta]
+  const int64_t a0 = (int64_t)blockIdx.x * ta;
+  const int64_t j_lo = (int64_t)blockIdx.y * a.samples_per_split;
+  const int64_t j_hi = min(a.n_s, j_lo + a.samples_per_split);
+  const bool no_gain = a.no_gain;
+
+  for (int aa = tid; aa < ta; aa += kFwdThreads) {
+    const int64_t ia = a0 + aa;
+    AntD d;
+    if (ia < a.n_a) {
+      d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+      if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+      else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+      d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+      d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+    } else {
+      d.x = d.y = 0.0; d.z = 1.0; d.rx = d.ry = 0.0; d.rz = 1.0; d.ptx = d.prx = 1.f;
+    }
+    ant[aa] = d;
+  }
+  // phase-2 identity: antenna fastest so shared-memory reads are consecutive across lanes
+  const int my_a = tid % ta, my_b = tid / ta;
+  const bool active = my_b < nb;
+  f2x acc[B];
+#pragma unroll
+  for (int m = 0; m < B; ++m) acc[m] = 0ull;
+  bool domain = false;
+  __syncthreads();
+
+  for (int64_t jt = j_lo; jt < j_hi; jt += kFwdTJ) {
+    // ---------------- phase 1: per-pair geometry and anchors
+    for (int pr = tid; pr < ta * kFwdTJ; pr += kFwdThreads) {
+      const int aa = pr % ta, jj = pr / ta;
+      const int64_t j = jt + jj;
+      float4 *dst = anc + (size_t)jj * nb * ta + aa;
+      if (j >= j_hi || a0 + aa >= a.n_a) {
+        for (int b = 0; b < nb; ++b) dst[(size_t)b * ta] = make_float4(0.f, 0.f, 0.f, 0.f);
+        kv[jj * ta + aa] = 2.f;
+        continue;
+      }
+      const Rec rec = a.rec[j];
+      PairBwd g;
+      pair_geometry<MONO, CORR>(rec, ant[aa], no_gain, g);
+      domain |= !g.ok;
+      const float A = rec.w * g.gg * g.Tt * g.Tr;
+      // phase anchors from fp64 cycle counts (cycles = L f / c), reduced to [-0.5, 0.5]
+      const float fr0 = frac_cycles(g.L * a.k0);
+      const float frd = frac_cycles(g.L * a.kd);
+      const float frw = frac_cycles(g.L * a.kw);
+      float es, ec, zs, zc, ws, wc;
+      __sincosf(kTwoPi * fr0, &es, &ec);            // anchor phase: MUFU, error not amplified
+      sincospif(2.f * frd, &zs, &zc);               // recurrence step: accurate (sets 2cos theta)
+      __sincosf(kTwoPi * frw, &ws, &wc);            // block step
+      f2x c = pk(A * ec, -A * es);                  // A e^{-j theta0}
+      const f2x zz = pk(zc, -zs), ww = pk(wc, -ws);
+      for (int b = 0; b < nb; ++b) {
+        const float2 y0 = upk(c), y1 = upk(cmul2(c, zz));
+        dst[(size_t)b * ta] = make_float4(y0.x, y0.y, y1.x, y1.y);
+        c = cmul2(c, ww);
+      }
+      kv[jj * ta + aa] = 2.f * zc;
+    }
+    __syncthreads();
+    // ---------------- phase 2: bin recurrences
+    if (active) {
+#pragma unroll 2
+      for (int jj = 0; jj < kFwdTJ; ++jj) {
+        const float4 Y = anc[((size_t)jj * nb + my_b) * ta + my_a];
+        const float k = kv[jj * ta + my_a];
+        const f2x kp = pk(k, k), kn = pk(-k, -k);
+        f2x q0 = pk(Y.x, Y.y), q1 = pk(Y.z, Y.w);
+        acc[0] = fadd2(acc[0], q0);
+        acc[1] = fadd2(acc[1], q1);
+#pragma unroll
+        for (int m = 1; m < B - 1; ++m) {
+          const f2x q2 = ffma2((m & 1) ? kn : kp, q1, q0);
+          acc[m + 1] = fadd2(acc[m + 1], q2);
+          q0 = q1;
+          q1 = q2;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (domain) atomicOr(a.flags, 1u);
+  const int64_t ia = a0 + my_a;
+  if (active && ia < a.n_a) {
+    float2 *dst = a.out + ((int64_t)blockIdx.y * a.n_a + ia) * a.n_f + (int64_t)my_b * B;
+    const int lim = min(B, a.n_f - my_b * B);
+#pragma unroll
+    for (int m = 0; m < B; ++m) {
+      if (m < lim) {
+        const float2 v = upk(acc[m]);
+        const float sg = (m & 2) ? -1.f : 1.f;       // undo sigma_m
+        dst[m] = make_float2(sg * v.x, sg * v.y);
+      }
+    }
+  }
+}
+
+// ================================================================================== K3 / K4
+// One thread owns SPT samples (or queries) and loops over the antennas of its split.  Per pair:
+// fp64 path length, E = e^{+j2pi f0 tau}, w = e^{+j2pi df tau}; Horner h = sum_m X(i,m) w^m over the
+// bins with X(i, .) broadcast from shared memory (2 FFMA2 per complex step).
+//   MODE_BWD: R = Re(E h) -> per-sample sums S1, S2, S3 (Eq. 5 chain), written as partials.
+//   MODE_FLT: M += E h (complex) -> partial matched-filter output.
+template <int MODE, int SPT, bool MONO, bool CORR>
+__global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
+  AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
+  const int tid = threadIdx.x;
+  const int nf = a.n_f;
+  const int64_t base = (int64_t)blockIdx.x * (kAdjThreads * SPT);
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  const bool no_gain = a.no_gain;
+
+  Rec rec[SPT];
+  bool valid[SPT];
+  float S1[SPT], S2[SPT], S3x[SPT], S3y[SPT], S3z[SPT];
+#pragma unroll
+  for (int s = 0; s < SPT; ++s) {
+    const int64_t j = base + s * kAdjThreads + tid;
+    valid[s] = j < a.n_s;
+    if (MODE == kModeBwd) {
+      if (valid[s]) rec[s] = a.rec[j];
+      else { rec[s].x = rec[s].y = 0.0; rec[s].z = 1.0; rec[s].w = 0.f; rec[s].T = 0.f;
+             rec[s].nx = rec[s].ny = 0.f; rec[s].nz = 1.f; rec[s].papr = 1.f; }
+    } else {
+      rec[s].x = valid[s] ? (double)a.qx[j] : 0.0;
+      rec[s].y = valid[s] ? (double)a.qy[j] : 0.0;
+      rec[s].z = valid[s] ? (double)a.qz[j] : 1.0;
+      rec[s].w = 0.f; rec[s].T = 1.f; rec[s].nx = rec[s].ny = 0.f; rec[s].nz = 1.f;
+      rec[s].papr = 1.f;
+    }
+    S1[s] = S2[s] = S3x[s] = S3y[s] = S3z[s] = 0.f;
+  }
+  bool domain = false;
+
+  for (int64_t ic = i_lo; ic < i_hi; ic += kAdjGA) {
+    const int ga = (int)min((int64_t)kAdjGA, i_hi - ic);
+    __syncthreads();
+    {   // stage X rows [ga][nf] (contiguous in global memory) and the antennas
+      const float2 *src = a.X + ic * nf;
+      const int n2 = ga * nf;
+      for (int t = tid; t < n2; t += kAdjThreads) X[t] = src[t];
+      for (int aa = tid; aa < ga; aa += kAdjThreads) {
+        const int64_t ia = ic + aa;
+        AntD d;
+        d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+        if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+        else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+        d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+        d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+        ant[aa] = d;
+      }
+    }
+    __syncthreads();
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = ant[aa];
+      PairBwd g[SPT];
+      f2x w1[SPT], w2[SPT], h[SPT];
+      float Er[SPT], Ei[SPT];
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        pair_geometry<MONO, CORR>(rec[s], an, no_gain, g[s]);
+        domain |= (MODE == kModeBwd) && valid[s] && !g[s].ok;
+        const float fr0 = frac_cycles(g[s].L * a.k0);
+        const float frd = frac_cycles(g[s].L * a.kd);
+        float es, ec, zs, zc;
+        __sincosf(kTwoPi * fr0, &es, &ec);
+        sincospif(2.f * frd, &zs, &zc);
+        Er[s] = ec; Ei[s] = es;                    // E = e^{+j theta0}
+        w1[s] = pk(zc, zs);                        // w = e^{+j theta_d}
+        w2[s] = pk(-zs, zc);
+        h[s] = 0ull;
+      }
+      const float2 *Xa = X + aa * nf;
+      // Horner from the top bin down: h = h w + X_m  (2 FFMA2 per complex step)
+#pragma unroll 8
+      for (int m = nf - 1; m >= 0; --m) {
+        const float2 xv = Xa[m];
+        const f2x xm = pk(xv.x, xv.y);
+#pragma unroll
+        for (int s = 0; s < SPT; ++s) {
+          const float2 hv = upk(h[s]);
+          const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
+          h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        const float2 hv = upk(h[s]);
+        if (MODE == kModeBwd) {
+          const float R = Er[s] * hv.x - Ei[s] * hv.y;      // Re(E h)
+          const float TT = g[s].Tt * g[s].Tr;
+          const float Rg = R * g[s].gg;
+          S1[s] = fmaf(Rg, TT, S1[s]);
+          S2[s] = fmaf(Rg, g[s].Tr * g[s].chit + g[s].Tt * g[s].chir, S2[s]);
+          const float Rc = R * g[s].gamma * TT;
+          S3x[s] = fmaf(Rc, g[s].dgx, S3x[s]);
+          S3y[s] = fmaf(Rc, g[s].dgy, S3y[s]);
+          S3z[s] = fmaf(Rc, g[s].dgz, S3z[s]);
+        } else {
+          // M += E h
+          S1[s] = fmaf(Er[s], hv.x, fmaf(-Ei[s], hv.y, S1[s]));
+          S2[s] = fmaf(Er[s], hv.y, fmaf(Ei[s], hv.x, S2[s]));
+        }
+      }
+    }
+  }
+  if (domain) atomicOr(a.flags, 1u);
+#pragma unroll
+  for (int s = 0; s < SPT; ++s) {
+    const int64_t j = base + s * kAdjThreads + tid;
+    if (!valid[s]) continue;
+    if (MODE == kModeBwd) {
+      float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
+      P[j] = S1[s];
+      P[a.n_s + j] = S2[s];
+      P[2 * a.n_s + j] = S3x[s];
+      P[3 * a.n_s + j] = S3y[s];
+      P[4 * a.n_s + j] = S3z[s];
+    } else {
+      float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
+      M[j] = make_float2(S1[s], S2[s]);
+    }
+  }
+}
+
+// ================================================================================== K1' backward
+// Per ray, reverse order.  With gT_k = w_k S2_k, Q_l = gT_{l+1} + (1-alpha_{l+1}) Q_{l+1} gives
+// dL/d(1-alpha_l) = T_l Q_l without dividing by (1 - alpha) (exactly 0 at surface entries).
+__global__ void k_blend_bwd(BlendBwdArgs a) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  const int nz = a.n_per_ray;
+  const int64_t j0 = r * nz, ns = a.n_s;
+  float Q = 0.f, carry = 0.f, gs = 0.f;
+  float gT_next = 0.f, oma_next = 1.f;
+  float f_next = 0.f, sm_next = 0.f;
+  for (int l = nz - 1; l >= 0; --l) {
+    const int64_t j = j0 + l;
+    const float f = a.sdf[j];
+    const float p = a.power[j], refl = a.refl[j];
+    const Rec rec = a.rec[j];
+    const float S1 = a.partials[j], S2 = a.partials[ns + j];
+    const float S3x = a.partials[2 * ns + j], S3y = a.partials[3 * ns + j],
+                S3z = a.partials[4 * ns + j];
+    const bool has_next = l + 1 < nz;
+    float alpha, oma;
+    blend_step(a.s, f, f_next, has_next, alpha, oma);
+    const float w = rec.w;
+    a.g_power[j] = refl * alpha * S1;
+    a.g_refl[j] = p * alpha * S1;
+    a.g_nx[j] = w * S3x;
+    a.g_ny[j] = w * S3y;
+    a.g_nz[j] = w * S3z;
+    if (has_next) Q = gT_next + oma_next * Q;
+    const float dalpha = p * refl * S1 - rec.T * Q;
+    const float sm = sig_minus(a.s, f);
+    float gf_here = 0.f;
+    if (has_next && alpha > 0.f) {
+      const float c = dalpha * oma;
+      gf_here = c * a.s * sm;
+      carry -= c * a.s * sm_next;
+      gs += c * (f * sm - f_next * sm_next);
+    }
+    if (has_next) a.g_sdf[j + 1] = carry;
+    carry = gf_here;
+    gT_next = w * S2;
+    oma_next = oma;
+    f_next = f;
+    sm_next = sm;
+  }
+  a.g_sdf[j0] = carry;
+  a.ds_part[r] = gs;
+}
+
+// ================================================================================== reductions
+// out[k] = sum_{s < S} part[s * n + k], fixed order (float2 / float granularity via float4 loads)
+__global__ void k_sum_splits(const float4 *__restrict__ part, int S, int64_t n4,
+                             float4 *__restrict__ out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = part[k];
+    for (int s = 1; s < S; ++s) {
+      const float4 u = part[(int64_t)s * n4 + k];
+      v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+    }
+    out[k] = v;
+  }
+}
+__global__ void k_sum_splits_tail(const float *__restrict__ part, int S, int64_t n, int64_t lo,
+                                  float *__restrict__ out) {
+  const int64_t k = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  float v = part[k];
+  for (int s = 1; s < S; ++s) v += part[(int64_t)s * n + k];
+  out[k] = v;
+}
+
+// |M| for the filter (M already summed)
+__global__ void k_abs(const float2 *__restrict__ m, int64_t n, float *__restrict__ p) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = m[k];
+    p[k] = sqrtf(fmaf(v.x, v.x, v.y * v.y));
+  }
+}
+
+// Block-level fixed-order sum of n floats into out[blockIdx.x] (grid-stride over the input)
+__device__ __forceinline__ float block_sum(float v, float *sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.f;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void k_reduce_sum(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
+  __shared__ float sh[32];
+  float v = 0.f;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    v += x[k];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = v;
+}
+
+// ================================================================================== K6 loss
+__global__ void k_loss_partial(const float2 *__restrict__ s, const float2 *__restrict__ y,
+                               int64_t n, float2 *__restrict__ g, float *__restrict__ part) {
+  __shared__ float sh[32];
+  float v = 0.f;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const float2 a = s[k], b = y[k];
+    const float2 d = make_float2(a.x - b.x, a.y - b.y);
+    g[k] = d;
+    v = fmaf(d.x, d.x, fmaf(d.y, d.y, v));
+  }
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = 0.5f * v;
+}
+
+// ================================================================================== launchers
+static inline unsigned grid1(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// count of kernels this library launched (diagnostic for the bench's gpu_launches claim)
+static unsigned long long g_launches = 0;
+static inline cudaError_t counted(cudaError_t e, int n = 1) {
+  if (e == cudaSuccess) __atomic_add_fetch(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED);
+  return e;
+}
+unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st) {
+  if (a.n_rays <= 0) return cudaSuccess;
+  k_blend<<<grid1(a.n_rays, 128), 128, 0, st>>>(a);
+  return counted(cudaGetLastError());
+}
+
+template <int B, bool MONO, bool CORR>
+static cudaError_t fwd_t(const FwdArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
+  auto k = k_trace_fwd<B, MONO, CORR>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kFwdThreads, smem, st>>>(a);
+  return counted(cudaGetLastError());
+}
+
+template <int B>
+static cudaError_t fwd_b(const FwdArgs &a, bool mono, bool corr, dim3 g, size_t sm, cudaStream_t st) {
+  if (mono) return corr ? fwd_t<B, true, true>(a, g, sm, st) : fwd_t<B, true, false>(a, g, sm, st);
+  return corr ? fwd_t<B, false, true>(a, g, sm, st) : fwd_t<B, false, false>(a, g, sm, st);
+}
+
+cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int n_splits,
+                             cudaStream_t st) {
+  const int64_t n_tiles = (a.n_a + a.ta - 1) / a.ta;
+  dim3 grid((unsigned)n_tiles, (unsigned)n_splits);
+  const size_t smem = fwd_smem_bytes(a.nb, a.ta);
+  switch (B) {
+    case 8: return fwd_b<8>(a, mono, corr, grid, smem, st);
+    case 16: return fwd_b<16>(a, mono, corr, grid, smem, st);
+    case 32: return fwd_b<32>(a, mono, corr, grid, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int MODE, bool MONO, bool CORR>
+static cudaError_t adj_t(const AdjArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
+  auto k = k_adjoint<MODE, kAdjSPT, MONO, CORR>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kAdjThreads, smem, st>>>(a);
+  return counted(cudaGetLastError());
+}
+
+cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
+                           cudaStream_t st) {
+  const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
+  dim3 grid((unsigned)((a.n_s + per_cta - 1) / per_cta), (unsigned)n_splits);
+  const size_t smem = adj_smem_bytes(a.n_f);
+  if (mode == kModeBwd) {
+    if (mono) return corr ? adj_t<kModeBwd, true, true>(a, grid, smem, st)
+                          : adj_t<kModeBwd, true, false>(a, grid, smem, st);
+    return corr ? adj_t<kModeBwd, false, true>(a, grid, smem, st)
+                : adj_t<kModeBwd, false, false>(a, grid, smem, st);
+  }
+  return mono ? adj_t<kModeFlt, true, false>(a, grid, smem, st)
+              : adj_t<kModeFlt, false, false>(a, grid, smem, st);
+}
+
+cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st) {
+  if (a.n_rays <= 0) return cudaSuccess;
+  k_blend_bwd<<<grid1(a.n_rays, 128), 128, 0, st>>>(a);
+  return counted(cudaGetLastError());
+}
+
+cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, int n_sm,
+                              cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t n4 = n / 4;
+  if (n4 > 0) {
+    const unsigned g = (unsigned)std::min<int64_t>(grid1(n4, 256), (int64_t)n_sm * 8);
+    // the float4 view of split s starts at s * n floats: needs n % 4 == 0 for alignment
+    if (n % 4 == 0) {
+      k_sum_splits<<<g, 256, 0, st>>>(reinterpret_cast<const float4 *>(part), S, n4,
+                                      reinterpret_cast<float4 *>(out));
+      return counted(cudaGetLastError());
+    }
+  }
+  k_sum_splits_tail<<<grid1(n, 256), 256, 0, st>>>(part, S, n, 0, out);
+  return counted(cudaGetLastError());
+}
+
+cudaError_t launch_abs(const float *m, int64_t n, float *p, int n_sm, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>(grid1(n, 256), (int64_t)n_sm * 8);
+  k_abs<<<g, 256, 0, st>>>(reinterpret_cast<const float2 *>(m), n, p);
+  return counted(cudaGetLastError());
+}
+
+cudaError_t launch_reduce_sum(const float *x, int64_t n, float *tmp, int tmp_n, float *out,
+                              cudaStream_t st) {
+  // two fixed-shape passes: tmp_n blocks -> 1 block
+  k_reduce_sum<<<tmp_n, 256, 0, st>>>(x, n, tmp);
+  k_reduce_sum<<<1, 256, 0, st>>>(tmp, tmp_n, out);
+  return counted(cudaGetLastError(), 2);
+}
+
+cudaError_t launch_loss(const float *s, const float *y, int64_t n, float *g, float *tmp,
+                        int tmp_n, float *loss, cudaStream_t st) {
+  k_loss_partial<<<tmp_n, 256, 0, st>>>(reinterpret_cast<const float2 *>(s),
+                                        reinterpret_cast<const float2 *>(y), n,
+                                        reinterpret_cast<float2 *>(g), tmp);
+  k_reduce_sum<<<1, 256, 0, st>>>(tmp, tmp_n, loss);
+  return counted(cudaGetLastError(), 2);
+}
+
+}  // namespace rfr

@@ -1,0 +1,93 @@
+// rfr_launch.h -- internal launch interface between the C ABI (librfr.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace rfr {
+
+struct Rec;
+
+constexpr int kFwdThreads = 256;   // K2 CTA size
+constexpr int kFwdTJ = 8;          // samples per K2 shared-memory tile
+constexpr int kAdjThreads = 128;   // K3/K4 CTA size
+constexpr int kAdjSPT = 2;         // samples (queries) per K3/K4 thread
+constexpr int kAdjGA = 8;          // antennas per K3/K4 shared-memory stage
+constexpr int kModeBwd = 0, kModeFlt = 1;
+
+struct BlendArgs {
+  const float *x, *y, *z, *sdf, *refl, *nx, *ny, *nz, *power, *phi_origin;
+  int64_t n_rays;
+  int n_per_ray;
+  float s;
+  Rec *rec;
+  unsigned int *flags;
+  bool check_finite;
+};
+
+struct FwdArgs {
+  const Rec *rec;
+  int64_t n_s;
+  const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
+  int64_t n_a;
+  int n_f, nb, ta;
+  double k0, kd, kw;               // cycles per metre of path: f0/c, df/c, B df/c
+  int64_t samples_per_split;
+  float2 *out;                     // [split][n_a][n_f]
+  size_t smem_ant_off;
+  unsigned int *flags;
+  bool no_gain;
+};
+
+struct AdjArgs {
+  const Rec *rec;                  // K3: sample records
+  const float *qx, *qy, *qz;       // K4: query points
+  int64_t n_s;                     // samples or queries
+  const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
+  int64_t n_a;
+  int n_f;
+  double k0, kd;
+  const float2 *X;                 // G (K3) or signal (K4), [n_a][n_f]
+  int64_t ants_per_split;
+  float *out;                      // K3: [split][5][n_s]; K4: [split][n_s] complex
+  size_t smem_ant_off;
+  unsigned int *flags;
+  bool no_gain;
+};
+
+struct BlendBwdArgs {
+  const float *sdf, *refl, *power;
+  const Rec *rec;
+  const float *partials;           // [5][n_s] (summed over antennas and shards)
+  int64_t n_rays, n_s;
+  int n_per_ray;
+  float s;
+  float *g_sdf, *g_refl, *g_nx, *g_ny, *g_nz, *g_power;
+  float *ds_part;                  // [n_rays]
+};
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+inline size_t fwd_smem_ant_off(int nb, int ta) {
+  return align_up((size_t)kFwdTJ * nb * ta * 16 + (size_t)kFwdTJ * ta * 4, 16);
+}
+inline size_t fwd_smem_bytes(int nb, int ta) { return fwd_smem_ant_off(nb, ta) + (size_t)ta * 56; }
+inline size_t adj_smem_ant_off(int n_f) { return align_up((size_t)kAdjGA * n_f * 8, 16); }
+inline size_t adj_smem_bytes(int n_f) { return adj_smem_ant_off(n_f) + (size_t)kAdjGA * 56; }
+
+unsigned long long launch_count();
+cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st);
+cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int n_splits,
+                             cudaStream_t st);
+cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
+                           cudaStream_t st);
+cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st);
+cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, int n_sm,
+                              cudaStream_t st);
+cudaError_t launch_abs(const float *m, int64_t n, float *p, int n_sm, cudaStream_t st);
+cudaError_t launch_reduce_sum(const float *x, int64_t n, float *tmp, int tmp_n, float *out,
+                              cudaStream_t st);
+cudaError_t launch_loss(const float *s, const float *y, int64_t n, float *g, float *tmp,
+                        int tmp_n, float *loss, cudaStream_t st);
+
+}  // namespace rfr

@@ -1,0 +1,318 @@
+"""Thin ctypes binding of librfr (include/librfr.h): argument marshalling only.
+
+Every step of the renderer runs in librfr's sm_100a kernels; this module only turns torch CUDA
+tensors into the C structs of the ABI and checks the returned status.  PyTorch supplies device
+memory and the current stream.  There is no CPU fallback: if librfr.so is missing or no CUDA device
+is present, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librfr.so")
+
+RFR_NO_GAIN = 1
+RFR_CHECK_FINITE = 2
+RFR_REUSE_BLEND = 4
+RFR_FLAG_DOMAIN = 1
+RFR_FLAG_NUMERIC = 2
+
+_P = C.POINTER(C.c_float)
+
+
+class rfr_freq_grid(C.Structure):
+    _fields_ = [("f0_hz", C.c_double), ("df_hz", C.c_double), ("n_freq", C.c_int32)]
+
+
+class rfr_samples(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in
+                ("x", "y", "z", "sdf", "refl", "nx", "ny", "nz", "power", "phi_origin")] + \
+               [("n_rays", C.c_int64), ("n_per_ray", C.c_int32)]
+
+
+class rfr_antennas(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in
+                ("tx_x", "tx_y", "tx_z", "rx_x", "rx_y", "rx_z", "phi_tx", "phi_rx")] + \
+               [("n_ant", C.c_int64)]
+
+
+class rfr_sample_grads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("sdf", "refl", "nx", "ny", "nz", "power", "sharpness")]
+
+
+class rfr_opts(C.Structure):
+    _fields_ = [("flags", C.c_uint32)]
+
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too small",
+          3: "domain", 4: "numeric", 5: "CUDA launch failure", 6: "unsupported"}
+
+EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_filter_partial",
+           "rfr_filter_power", "rfr_backward", "rfr_backward_partial", "rfr_backward_finish",
+           "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count")
+
+
+class RfrError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load librfr.so (built in-tree by __graft_entry__.build()).  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"librfr.so not built at {path}: run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    vp, i64, i32, u32, f = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32, C.c_float
+    S, A, G, O, R = (C.POINTER(rfr_samples), C.POINTER(rfr_antennas), C.POINTER(rfr_freq_grid),
+                     C.POINTER(rfr_opts), C.POINTER(rfr_sample_grads))
+    sig = {
+        "rfr_workspace_size": [i64, i64, i32, i64, C.POINTER(C.c_size_t)],
+        "rfr_forward": [S, f, A, G, O, vp, vp, C.c_size_t, vp],
+        "rfr_loss": [vp, vp, i64, vp, vp, vp, C.c_size_t, vp],
+        "rfr_filter": [vp, A, G, vp, vp, vp, i64, vp, vp, vp, C.c_size_t, vp],
+        "rfr_filter_partial": [vp, A, G, vp, vp, vp, i64, vp, vp, C.c_size_t, vp],
+        "rfr_filter_power": [vp, i64, vp, vp],
+        "rfr_backward": [vp, S, f, A, G, O, R, vp, C.c_size_t, vp],
+        "rfr_backward_partial": [vp, S, f, A, G, O, vp, vp, C.c_size_t, vp],
+        "rfr_backward_finish": [vp, S, f, O, R, vp, C.c_size_t, vp],
+        "rfr_poll_flags": [vp, C.POINTER(u32)],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    lib.rfr_status_string.argtypes = [C.c_int]
+    lib.rfr_status_string.restype = C.c_char_p
+    lib.rfr_abi_version.restype = C.c_int
+    lib.rfr_launch_count.restype = C.c_uint64
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise RfrError(f"{what}: {STATUS.get(rc, rc)}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise RfrError("librfr takes CUDA tensors only (no CPU fallback)")
+    if not t.is_contiguous():
+        raise RfrError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream: Optional[torch.cuda.Stream] = None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ------------------------------------------------------------------------------ device inputs
+@dataclasses.dataclass
+class DeviceSamples:
+    x: torch.Tensor
+    y: torch.Tensor
+    z: torch.Tensor
+    sdf: torch.Tensor
+    refl: torch.Tensor
+    nx: torch.Tensor
+    ny: torch.Tensor
+    nz: torch.Tensor
+    power: torch.Tensor
+    n_rays: int
+    n_per_ray: int
+    phi_origin: Optional[torch.Tensor] = None
+
+    FIELDS = ("x", "y", "z", "sdf", "refl", "nx", "ny", "nz", "power")
+
+    @property
+    def n(self) -> int:
+        return self.n_rays * self.n_per_ray
+
+    @classmethod
+    def from_host(cls, S, device="cuda") -> "DeviceSamples":
+        t = lambda a: None if a is None else torch.as_tensor(np.ascontiguousarray(a, np.float32)).to(device)
+        return cls(*(t(getattr(S, f)) for f in cls.FIELDS), n_rays=int(S.n_rays),
+                   n_per_ray=int(S.n_per_ray), phi_origin=t(S.phi_origin))
+
+    def struct(self) -> rfr_samples:
+        return rfr_samples(*(_ptr(getattr(self, f)) for f in self.FIELDS), _ptr(self.phi_origin),
+                           self.n_rays, self.n_per_ray)
+
+
+@dataclasses.dataclass
+class DeviceAntennas:
+    tx_x: torch.Tensor
+    tx_y: torch.Tensor
+    tx_z: torch.Tensor
+    rx_x: Optional[torch.Tensor] = None
+    rx_y: Optional[torch.Tensor] = None
+    rx_z: Optional[torch.Tensor] = None
+    phi_tx: Optional[torch.Tensor] = None
+    phi_rx: Optional[torch.Tensor] = None
+
+    NAMES = ("tx_x", "tx_y", "tx_z", "rx_x", "rx_y", "rx_z", "phi_tx", "phi_rx")
+
+    @property
+    def n(self) -> int:
+        return int(self.tx_x.shape[0])
+
+    @classmethod
+    def from_host(cls, A, device="cuda") -> "DeviceAntennas":
+        t = lambda a: None if a is None else torch.as_tensor(np.ascontiguousarray(a, np.float32)).to(device)
+        return cls(*(t(getattr(A, f)) for f in cls.NAMES))
+
+    def slice(self, lo: int, hi: int) -> "DeviceAntennas":
+        """A shard is a pointer offset plus a count (views of the same storage)."""
+        return DeviceAntennas(*(None if getattr(self, f) is None else getattr(self, f)[lo:hi]
+                                for f in self.NAMES))
+
+    def struct(self) -> rfr_antennas:
+        return rfr_antennas(*(_ptr(getattr(self, f)) for f in self.NAMES), self.n)
+
+
+def grid_struct(grid) -> rfr_freq_grid:
+    return rfr_freq_grid(float(grid.f0), float(grid.df), int(grid.n_freq))
+
+
+# ------------------------------------------------------------------------------ ABI wrappers
+def rfr_workspace_size(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0) -> int:
+    out = C.c_size_t()
+    _check(load().rfr_workspace_size(n_samples, n_ant, n_freq, n_query, C.byref(out)),
+           "rfr_workspace_size")
+    return out.value
+
+
+def workspace(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0, device="cuda"):
+    nb = rfr_workspace_size(n_samples, n_ant, n_freq, n_query)
+    ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=device)
+    return ws
+
+
+def rfr_forward(samples: DeviceSamples, sharpness: float, ants: DeviceAntennas, grid,
+                signal: torch.Tensor, ws: torch.Tensor, flags: int = 0, stream=None):
+    s, a, g, o = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags)
+    _check(load().rfr_forward(C.byref(s), float(sharpness), C.byref(a), C.byref(g), C.byref(o),
+                              _ptr(signal), _ptr(ws), ws.numel(), _stream(stream)), "rfr_forward")
+    return signal
+
+
+def rfr_loss(signal: torch.Tensor, target: torch.Tensor, grad: torch.Tensor, loss: torch.Tensor,
+             ws: torch.Tensor, stream=None):
+    n = signal.numel() // 2
+    _check(load().rfr_loss(_ptr(signal), _ptr(target), n, _ptr(grad), _ptr(loss), _ptr(ws),
+                           ws.numel(), _stream(stream)), "rfr_loss")
+    return loss, grad
+
+
+def rfr_filter(signal: torch.Tensor, ants: DeviceAntennas, grid, qx, qy, qz, power: torch.Tensor,
+               ws: torch.Tensor, mf: Optional[torch.Tensor] = None, stream=None):
+    a, g = ants.struct(), grid_struct(grid)
+    _check(load().rfr_filter(_ptr(signal), C.byref(a), C.byref(g), _ptr(qx), _ptr(qy), _ptr(qz),
+                             int(qx.numel()), _ptr(power), _ptr(mf), _ptr(ws), ws.numel(),
+                             _stream(stream)), "rfr_filter")
+    return power
+
+
+def rfr_filter_partial(signal, ants: DeviceAntennas, grid, qx, qy, qz, mf: torch.Tensor,
+                       ws: torch.Tensor, stream=None):
+    a, g = ants.struct(), grid_struct(grid)
+    _check(load().rfr_filter_partial(_ptr(signal), C.byref(a), C.byref(g), _ptr(qx), _ptr(qy),
+                                     _ptr(qz), int(qx.numel()), _ptr(mf), _ptr(ws), ws.numel(),
+                                     _stream(stream)), "rfr_filter_partial")
+    return mf
+
+
+def rfr_filter_power(mf: torch.Tensor, power: torch.Tensor, stream=None):
+    _check(load().rfr_filter_power(_ptr(mf), int(power.numel()), _ptr(power), _stream(stream)),
+           "rfr_filter_power")
+    return power
+
+
+@dataclasses.dataclass
+class Grads:
+    sdf: torch.Tensor
+    refl: torch.Tensor
+    nx: torch.Tensor
+    ny: torch.Tensor
+    nz: torch.Tensor
+    power: torch.Tensor
+    sharpness: torch.Tensor
+
+    NAMES = ("sdf", "refl", "nx", "ny", "nz", "power", "sharpness")
+
+    @classmethod
+    def empty(cls, n: int, device="cuda") -> "Grads":
+        return cls(*(torch.empty(n, dtype=torch.float32, device=device) for _ in range(6)),
+                   torch.empty(1, dtype=torch.float32, device=device))
+
+    def struct(self) -> rfr_sample_grads:
+        return rfr_sample_grads(*(_ptr(getattr(self, f)) for f in self.NAMES))
+
+
+def rfr_backward(grad_signal: torch.Tensor, samples: DeviceSamples, sharpness: float,
+                 ants: DeviceAntennas, grid, out: Grads, ws: torch.Tensor, flags: int = 0,
+                 stream=None):
+    s, a, g, o, r = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags), out.struct()
+    _check(load().rfr_backward(_ptr(grad_signal), C.byref(s), float(sharpness), C.byref(a),
+                               C.byref(g), C.byref(o), C.byref(r), _ptr(ws), ws.numel(),
+                               _stream(stream)), "rfr_backward")
+    return out
+
+
+def rfr_backward_partial(grad_signal, samples: DeviceSamples, sharpness: float,
+                         ants: DeviceAntennas, grid, partials: torch.Tensor, ws: torch.Tensor,
+                         flags: int = 0, stream=None):
+    s, a, g, o = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags)
+    _check(load().rfr_backward_partial(_ptr(grad_signal), C.byref(s), float(sharpness), C.byref(a),
+                                       C.byref(g), C.byref(o), _ptr(partials), _ptr(ws),
+                                       ws.numel(), _stream(stream)), "rfr_backward_partial")
+    return partials
+
+
+def rfr_backward_finish(partials: torch.Tensor, samples: DeviceSamples, sharpness: float,
+                        out: Grads, ws: torch.Tensor, flags: int = 0, stream=None):
+    s, o, r = samples.struct(), rfr_opts(flags), out.struct()
+    _check(load().rfr_backward_finish(_ptr(partials), C.byref(s), float(sharpness), C.byref(o),
+                                      C.byref(r), _ptr(ws), ws.numel(), _stream(stream)),
+           "rfr_backward_finish")
+    return out
+
+
+def rfr_launch_count() -> int:
+    return int(load().rfr_launch_count())
+
+
+def rfr_poll_flags(ws: torch.Tensor) -> int:
+    v = C.c_uint32()
+    _check(load().rfr_poll_flags(_ptr(ws), C.byref(v)), "rfr_poll_flags")
+    return v.value
+
+
+# ------------------------------------------------------------------------------ multi-GPU host logic
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous antenna slice [lo, hi) of rank `rank` out of `world` (balanced to +-1)."""
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def c64_view(t: torch.Tensor) -> torch.Tensor:
+    """float32 [..., 2] interleaved view <-> complex64 helper for callers."""
+    return torch.view_as_complex(t)

@@ -267,31 +267,53 @@ def _pack(X: np.ndarray, prims: List[Prim], refl: np.ndarray, n_rays: int, n_per
                      f(nrm[..., 1]), f(nrm[..., 2]), f(pw), n_rays, n_per_ray)
 
 
+def scene_sdf(prims: List[Prim], X: np.ndarray) -> np.ndarray:
+    """Union (min) SDF only (no gradient), fp64."""
+    best = None
+    for p in prims:
+        d = X - p.center
+        if p.kind == "sphere":
+            v = np.linalg.norm(d, axis=-1) - p.size[0]
+        elif p.kind == "box":
+            q = np.abs(d) - p.size
+            v = np.linalg.norm(np.maximum(q, 0.0), axis=-1) + np.minimum(q.max(-1), 0.0)
+        else:
+            v, _ = _prim_sdf_grad(p, X)
+        best = v if best is None else np.minimum(best, v)
+    return best
+
+
 def _first_crossing(prims, starts: np.ndarray, direction: np.ndarray, u0: float, u1: float,
-                    step: float = 5e-4, iters: int = 30):
-    """First outside->inside zero crossing of the union SDF along x = start + u*dir (fp64 march
-    at `step` then bisection).  Returns u (nan where the ray misses)."""
-    us = np.arange(u0, u1 + step * 0.5, step)
+                    tol: float = 1e-7, max_iter: int = 2000):
+    """First outside->inside zero crossing of the union SDF along x = start + u*dir after u0, by
+    sphere tracing (the union of exact primitive SDFs never over-estimates the distance).  Rays
+    that start inside first march out.  Returns u (nan where the ray misses before u1)."""
     n = starts.shape[0]
+    u = np.full(n, u0, dtype=np.float64)
     found = np.full(n, np.nan)
-    prev = None
-    for k, u in enumerate(us):
-        s, _, _ = scene_eval(prims, starts + u * direction)
-        if prev is not None:
-            hit = np.isnan(found) & (prev > 0) & (s <= 0)
-            found[hit] = us[k - 1]
-        prev = s
-    hit = ~np.isnan(found)
-    a = found[hit].copy()
-    b = a + step
-    S = starts[hit]
-    for _ in range(iters):
-        m = 0.5 * (a + b)
-        s, _, _ = scene_eval(prims, S + m[:, None] * direction)
-        inside = s <= 0
-        b = np.where(inside, m, b)
-        a = np.where(inside, a, m)
-    found[hit] = 0.5 * (a + b)
+    live = np.ones(n, bool)
+    # leave any object the ray starts in
+    for _ in range(max_iter):
+        idx = np.nonzero(live)[0]
+        if idx.size == 0:
+            break
+        s = scene_sdf(prims, starts[idx] + u[idx, None] * direction)
+        inside = s < 0
+        if not inside.any():
+            break
+        u[idx[inside]] += np.maximum(-s[inside], 1e-5)
+        live[idx[inside & (u[idx] > u1)]] = False
+    for _ in range(max_iter):
+        idx = np.nonzero(live)[0]
+        if idx.size == 0:
+            break
+        s = scene_sdf(prims, starts[idx] + u[idx, None] * direction)
+        hit = s < tol
+        found[idx[hit]] = u[idx[hit]]
+        live[idx[hit]] = False
+        go = ~hit
+        u[idx[go]] += s[go]
+        live[idx[go & (u[idx] > u1)]] = False
     return found
 
 

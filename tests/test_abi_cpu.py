@@ -1,0 +1,83 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol include/librfr.h declares,
+plans workspaces and rejects bad arguments before touching a device (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "librfr.h")
+
+
+def _lib():
+    from paper_2605_29097_b200 import rfr
+    if not os.path.exists(rfr.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build_librfr()
+    return rfr, rfr.load()
+
+
+def declared_symbols():
+    txt = open(HDR).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(rfr_[a-z_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("rfr_forward", "rfr_filter", "rfr_backward", "rfr_workspace_size"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    rfr, lib = _lib()
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(declared_symbols()) == set(rfr.EXPORTS)
+    assert lib.rfr_abi_version() == 1
+    assert lib.rfr_status_string(2) == b"shape mismatch or workspace too small"
+
+
+def test_workspace_plan_is_sane():
+    rfr, lib = _lib()
+    n = rfr.rfr_workspace_size(1 << 20, 16384, 256, 1 << 20)
+    # records (48 B/sample) + backward partial sums + split buffers, capped at a few GiB
+    assert 48 * (1 << 20) < n < 8 << 30
+    assert rfr.rfr_workspace_size(0, 0, 1, 0) >= 256
+    small = rfr.rfr_workspace_size(4096, 64, 64, 4096)
+    assert small < n
+    out = C.c_size_t()
+    assert lib.rfr_workspace_size(-1, 1, 1, 0, C.byref(out)) == 2
+    assert lib.rfr_workspace_size(1, 1, 9000, 0, C.byref(out)) == 2   # n_freq > 8192 unsupported
+
+
+def test_argument_errors_before_any_launch():
+    rfr, lib = _lib()
+    g = rfr.rfr_freq_grid(77e9, 1e6, 8)
+    # null sample struct / null workspace -> RFR_E_ARG without touching a device
+    assert lib.rfr_forward(None, 1.0, None, C.byref(g), None, None, None, 0, None) == 1
+    s = rfr.rfr_samples()
+    s.n_rays, s.n_per_ray = 1, 1
+    a = rfr.rfr_antennas()
+    assert lib.rfr_forward(C.byref(s), 1.0, C.byref(a), C.byref(g), None, None, None, 0, None) == 1
+    assert lib.rfr_filter_power(None, 4, None, None) == 1
+    assert lib.rfr_filter_power(None, 0, None, None) == 0
+
+
+def test_no_cpu_fallback():
+    import torch
+    rfr, _ = _lib()
+    t = torch.zeros(4)
+    with pytest.raises(rfr.RfrError):
+        rfr._ptr(t)
+
+
+def test_shard_range_partitions():
+    rfr, _ = _lib()
+    for n in (0, 1, 7, 64, 16384, 16385):
+        for w in (1, 2, 3, 4, 8):
+            rs = [rfr.shard_range(n, r, w) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
