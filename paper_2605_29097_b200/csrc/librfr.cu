@@ -100,10 +100,10 @@ template <typename T>
 T *at(void *ws, size_t off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
 
 rfr_status check_samples(const rfr_samples *s) {
-  if (!s || !s->x || !s->y || !s->z || !s->sdf || !s->refl || !s->nx || !s->ny || !s->nz ||
-      !s->power)
+  if (!s || s->n_rays < 0) return RFR_E_ARG;
+  if (s->n_rays > 0 && (!s->x || !s->y || !s->z || !s->sdf || !s->refl || !s->nx || !s->ny ||
+                        !s->nz || !s->power))
     return RFR_E_ARG;
-  if (s->n_rays < 0) return RFR_E_ARG;
   if (s->n_per_ray <= 0) return RFR_E_SHAPE;
   return RFR_OK;
 }

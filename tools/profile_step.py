@@ -1,0 +1,46 @@
+"""One renderer step on one config, each hot kernel launched exactly once after one warm-up step:
+the target for `ncu --set full -k regex:... -s <warm-up launches> -c 3`.
+  python tools/profile_step.py --config c3
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2605_29097_b200 import rfr  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--steps", type=int, default=2)
+    a = ap.parse_args()
+    p = synth.make(a.config)
+    b = p.bundles[0]
+    dev = torch.device("cuda:0")
+    S = rfr.DeviceSamples.from_host(b.samples, dev)
+    A = rfr.DeviceAntennas.from_host(b.antennas, dev)
+    n, na, nf = b.samples.n, b.antennas.n, p.grid.n_freq
+    ws = rfr.workspace(n, na, nf, n, dev)
+    sig = torch.empty(na, nf, 2, device=dev)
+    G = torch.as_tensor(np.stack([p.random_grad().real, p.random_grad().imag], -1)).to(dev)
+    M = torch.empty(n, 2, device=dev)
+    P = torch.empty(n, device=dev)
+    part = torch.empty(5, n, device=dev)
+    out = rfr.Grads.empty(n, dev)
+    for _ in range(a.steps):
+        rfr.rfr_forward(S, p.sharpness, A, p.grid, sig, ws)
+        rfr.rfr_filter(sig, A, p.grid, S.x, S.y, S.z, P, ws, mf=M)
+        rfr.rfr_backward_partial(G, S, p.sharpness, A, p.grid, part, ws, flags=rfr.RFR_REUSE_BLEND)
+        rfr.rfr_backward_finish(part, S, p.sharpness, out, ws, flags=rfr.RFR_REUSE_BLEND)
+    torch.cuda.synchronize()
+    print("profile_step ok", a.config, rfr.rfr_launch_count())
+
+
+if __name__ == "__main__":
+    main()
