@@ -59,6 +59,11 @@ def lib():
         _lib.orc_backward_partials.argtypes = [pd, P(_Samples), d, P(_Antennas), d, d, i32, u32,
                                                pi64, i64, pd]
         _lib.orc_backward_finish.argtypes = [pd, P(_Samples), d, pi64, i64] + [pd] * 7
+        _lib.orc_filter_backward.argtypes = [pd, pd, pd, d, P(_Antennas), d, d, i32, pd, pd, pd,
+                                             i64, pi64, i64, pd]
+        _lib.orc_filter_backward.restype = C.c_int
+        _lib.orc_heatmap_loss.argtypes = [pd, pd, i64, P(C.c_int32), pd, d, d, pd, P(C.c_uint8)]
+        _lib.orc_heatmap_loss.restype = C.c_double
     return _lib
 
 
@@ -200,3 +205,36 @@ def backward(G, S, s: float, A, grid, flags: int = 0, rays=None):
                    + np.arange(S.n_per_ray)[None, :]).ravel()
     part = backward_partials(G, S, s, A, grid, flags, samples)
     return backward_finish(part, S, s, rays)
+
+
+def filter_backward(grad_P, M, P, A, grid, qx, qy, qz, eps: float, rows=None):
+    """O7: dL/ds(i, m) = sum_q (dL/dP_q) M_q / max(P_q, eps) e^{-j 2 pi f_m tau_iq} for the listed
+    antenna rows (all if None), complex128 [rows][n_freq]."""
+    keep = _Keep()
+    aa = _antennas(A, keep)
+    gp, Pp = _f64(grad_P), _f64(P)
+    Mm = np.ascontiguousarray(np.stack([np.real(M), np.imag(M)], -1), dtype=np.float64)
+    qx, qy, qz = _f64(qx), _f64(qy), _f64(qz)
+    ra, rp = _idx(rows)
+    n_rows = A.n if rows is None else len(ra)
+    out = np.zeros((n_rows, grid.n_freq, 2))
+    lib().orc_filter_backward(_ptr(gp), _ptr(Mm), _ptr(Pp), float(eps), C.byref(aa), grid.f0,
+                              grid.df, grid.n_freq, _ptr(qx), _ptr(qy), _ptr(qz), qx.shape[0], rp,
+                              n_rows, _ptr(out))
+    return out[..., 0] + 1j * out[..., 1]
+
+
+def heatmap_loss(P, P_gt, cell=None, H=None, thr_hi: float = 0.0, ratio: float = 0.0):
+    """O8: (L, dL/dP, mask, H_updated) of the masked heatmap L2; H is copied, not modified."""
+    Pp, Pg = _f64(P), _f64(P_gt)
+    n = Pp.shape[0]
+    g = np.zeros(n)
+    mask = np.zeros(n, np.uint8)
+    Hc = None if H is None else np.array(H, dtype=np.float64, copy=True)
+    cl = None if cell is None else np.ascontiguousarray(cell, dtype=np.int32)
+    L = lib().orc_heatmap_loss(_ptr(Pp), _ptr(Pg), n,
+                               C.POINTER(C.c_int32)() if cl is None else
+                               cl.ctypes.data_as(C.POINTER(C.c_int32)),
+                               _ptr(Hc), float(thr_hi), float(ratio), _ptr(g),
+                               mask.ctypes.data_as(C.POINTER(C.c_uint8)))
+    return L, g, mask.astype(bool), Hc

@@ -336,3 +336,78 @@ int orc_backward_finish(const double *partials, const orc_samples *S, double s,
   free(gT); free(ga); free(al); free(om); free(T);
   return 0;
 }
+
+/* ---------------------------------------------------------------- O7: matched-filter adjoint */
+
+/* dL/ds(i,m) for L depending on s only through P = |M| (Eq. 3):
+ *   M_q = sum_i sum_m s(i,m) e^{+j phi_iqm},  phi_iqm = 2 pi f_m tau_iq
+ *   G_M,q = dL/dRe M_q + j dL/dIm M_q = (dL/dP_q) M_q / max(P_q, eps)            (reading Q15)
+ *   dL/ds(i,m) = sum_q G_M,q e^{-j phi_iqm}       (conjugate phase: M is C-linear in s)
+ * The paper's App. A.5 and Alg. 1 [2] print (1/P) dL/dP e^{-j phi}, without the
+ * M_q factor; that form is not the gradient of |M|.  Here M_q and P_q are inputs
+ * (from orc_filter on the same signal), eps guards P = 0.
+ * Output rows: the listed antenna rows (all if rows == NULL), complex [n_rows][n_freq][2]. */
+int orc_filter_backward(const double *grad_P, const double *M, const double *P, double eps,
+                        const orc_antennas *Ant, double f0, double df, int32_t n_freq,
+                        const double *qx, const double *qy, const double *qz, int64_t n_query,
+                        const int64_t *rows, int64_t n_rows, double *out) {
+  int bistatic = Ant->rx_x != NULL;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t r = 0; r < n_rows; ++r) {
+    int64_t i = rows ? rows[r] : r;
+    ksum_t *acc = calloc((size_t)n_freq * 2, sizeof(ksum_t));
+    for (int64_t q = 0; q < n_query; ++q) {
+      double den = P[q] > eps ? P[q] : eps;
+      double cr = grad_P[q] * M[2 * q] / den, ci = grad_P[q] * M[2 * q + 1] / den;  /* G_M,q */
+      double dt[3] = {qx[q] - Ant->tx_x[i], qy[q] - Ant->tx_y[i], qz[q] - Ant->tx_z[i]};
+      double d_t = sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]);
+      double d_r = d_t;
+      if (bistatic) {
+        double dr[3] = {qx[q] - Ant->rx_x[i], qy[q] - Ant->rx_y[i], qz[q] - Ant->rx_z[i]};
+        d_r = sqrt(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
+      }
+      double tau = (d_t + d_r) / ORC_C;
+      for (int32_t m = 0; m < n_freq; ++m) {
+        double phi = 2.0 * M_PI * (f0 + (double)m * df) * tau;
+        double sn, cs;
+        sincos(phi, &sn, &cs);
+        kadd(&acc[2 * m], cr * cs + ci * sn);              /* Re(G_M e^{-j phi}) */
+        kadd(&acc[2 * m + 1], ci * cs - cr * sn);          /* Im(G_M e^{-j phi}) */
+      }
+    }
+    for (int32_t m = 0; m < n_freq; ++m) {
+      out[(r * n_freq + m) * 2] = acc[2 * m].s + acc[2 * m].c;
+      out[(r * n_freq + m) * 2 + 1] = acc[2 * m + 1].s + acc[2 * m + 1].c;
+    }
+    free(acc);
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- O8: heatmap loss + masking */
+
+/* Dynamic loss masking: a query q whose cell's historical maximum
+ * rendered power H[cell_q] exceeds thr_hi while its current power P_q is below ratio * H[cell_q] is
+ * excluded.  mask_q = 0 for excluded points, 1 otherwise (H before this iteration's update).
+ * Heatmap-domain L2:  L = 1/2 sum_q mask_q (P_q - Pgt_q)^2,
+ * dL/dP_q = mask_q (P_q - Pgt_q).  (Unnormalised; reading Q17b in DESIGN.md.)
+ * Then H[c] = max(H[c], P_q) over the queries of cell c (H may be NULL: no masking, no history). */
+double orc_heatmap_loss(const double *P, const double *Pgt, int64_t n_query, const int32_t *cell,
+                        double *H, double thr_hi, double ratio, double *grad_P, uint8_t *mask) {
+  ksum_t L = {0, 0};
+  for (int64_t q = 0; q < n_query; ++q) {
+    int keep = 1;
+    if (H && cell) {
+      double h = H[cell[q]];
+      if (h > thr_hi && P[q] < ratio * h) keep = 0;
+    }
+    double d = P[q] - Pgt[q];
+    if (mask) mask[q] = (uint8_t)keep;
+    if (grad_P) grad_P[q] = keep ? d : 0.0;
+    if (keep) kadd(&L, 0.5 * d * d);
+  }
+  if (H && cell)
+    for (int64_t q = 0; q < n_query; ++q)
+      if (P[q] > H[cell[q]]) H[cell[q]] = P[q];
+  return L.s + L.c;
+}

@@ -46,6 +46,13 @@ int orc_backward_finish(const double *partials, const orc_samples *S, double s,
                         double *g_nx, double *g_ny, double *g_nz, double *g_power,
                         double *g_sharp_per_ray);
 
+int orc_filter_backward(const double *grad_P, const double *M /* [n_query][2] */, const double *P,
+                        double eps, const orc_antennas *A, double f0, double df, int32_t n_freq,
+                        const double *qx, const double *qy, const double *qz, int64_t n_query,
+                        const int64_t *rows, int64_t n_rows, double *out /* [n_rows][n_freq][2] */);
+double orc_heatmap_loss(const double *P, const double *Pgt, int64_t n_query, const int32_t *cell,
+                        double *H, double thr_hi, double ratio, double *grad_P, uint8_t *mask);
+
 #ifdef __cplusplus
 }
 #endif
