@@ -130,6 +130,32 @@ rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
 /* power[q] = |mf[q]| after the caller's all-reduce of mf. */
 rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_stream_t stream);
 
+/* K5, matched-filter adjoint (NEXT-1; Eq. 3 backward, App. A.5, Alg. 1 [2]
+ * P:L750-761).  For a loss that depends on the signal through the filter power P_q = |M_q|:
+ *   grad_signal[i][m] = sum_q c_q exp(-j 2 pi f_m tau_iq),  c_q = grad_power[q] M_q / max(P_q, eps)
+ * i.e. G = dL/dRe s + j dL/dIm s for the antenna rows of `ants` (complex64 [n_ant][n_freq],
+ * overwritten).  The paper prints the weight as grad_power/P without M_q; that is not the
+ * derivative of |M| (reading Q15).  mf = complex M_q [n_query] from rfr_filter on the same
+ * signal and antennas; power = |M_q| [n_query] or NULL (recomputed from mf); eps >= 0 guards P = 0.
+ * ants->phi_tx / phi_rx must be NULL (the filter has no transmittance).  Multi-GPU: each rank passes
+ * its antenna slice; the output rows are local (no communication). */
+rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const float *power,
+                               float eps, const rfr_antennas *ants, const rfr_freq_grid *grid,
+                               const float *qx, const float *qy, const float *qz, int64_t n_query,
+                               float *grad_signal, void *ws, size_t ws_bytes, rfr_stream_t stream);
+
+/* K7, heatmap-domain L2 with dynamic loss masking (masking P:L392-402, SPEC
+ * S:L425-430).  keep_q = !(history[cell[q]] > thr_hi && power[q] < ratio * history[cell[q]])
+ * evaluated against the history as it was before this call; grad_power[q] = keep_q (P_q - Pgt_q);
+ * *loss (device float) = 1/2 sum_q keep_q (P_q - Pgt_q)^2; mask (optional, uint8 [n_query]) =
+ * keep_q.  Then history[c] = max(history[c], P_q) over the queries of cell c (order-independent).
+ * cell / history: both NULL (no masking, no history) or both given (int32 [n_query] cell index of
+ * each query into the caller's history grid, float [n_cells] >= 0). */
+rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n_query,
+                            const int32_t *cell, float *history, float thr_hi, float ratio,
+                            float *grad_power, uint8_t *mask, float *loss, void *ws,
+                            size_t ws_bytes, rfr_stream_t stream);
+
 /* Backward: grad_signal = G = dL/dRe s + j dL/dIm s, complex64 [n_ant][n_freq] (Q14).
  * Writes dL/d{sdf, refl, n, power} per sample and dL/dsharpness.  = partial + finish. */
 rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,

@@ -38,14 +38,14 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Plan {
   int n_sm = 148;
   // forward (K2)
-  int B = 32, nb = 1, ta = 256, fwd_splits = 1;
-  int64_t fwd_sps = 0;
+  int B = 32, nb = 1, ta = 256, fwd_splits = 1, mfa_splits = 1;
+  int64_t fwd_sps = 0, mfa_sps = 0;
   // adjoint (K3) and filter (K4)
   int bwd_splits = 1, flt_splits = 1;
   int64_t bwd_aps = 0, flt_aps = 0;
   // workspace layout
   size_t off_rec = 0, off_fwdp = 0, off_bwdp = 0, off_bwds = 0, off_fltp = 0, off_fltm = 0,
-         off_ds = 0, off_tmp = 0, total = 0;
+         off_ds = 0, off_tmp = 0, off_qrec = 0, total = 0;
 };
 
 bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
@@ -58,14 +58,19 @@ bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
   if (p.nb > kFwdThreads) return false;                    // n_freq > 8192
   p.ta = kFwdThreads / p.nb;
   const int64_t n_tiles = n_a > 0 ? cdiv(n_a, p.ta) : 1;
-  const int64_t target = (int64_t)p.n_sm * 2 * 32;         // ~32 waves at 2 CTAs / SM
-  int64_t splits = cdiv(target, n_tiles);
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, cdiv(n_s, kFwdTJ * 16)));
-  const size_t per_split = (size_t)std::max<int64_t>(n_a, 1) * nf * 8;
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t)(kSplitCap / per_split)));
-  splits = std::max<int64_t>(splits, 1);
-  p.fwd_sps = cdiv(cdiv(std::max<int64_t>(n_s, 1), splits), kFwdTJ) * kFwdTJ;
-  p.fwd_splits = (int)std::max<int64_t>(1, cdiv(n_s, p.fwd_sps));
+  // split-K over the summed points (samples for K2, queries for K5)
+  auto fwd = [&](int64_t n_pts, int &sp, int64_t &sps) {
+    const int64_t target = (int64_t)p.n_sm * 2 * 32;       // ~32 waves at 2 CTAs / SM
+    int64_t splits = cdiv(target, n_tiles);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, cdiv(n_pts, kFwdTJ * 16)));
+    const size_t per_split = (size_t)std::max<int64_t>(n_a, 1) * nf * 8;
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t)(kSplitCap / per_split)));
+    splits = std::max<int64_t>(splits, 1);
+    sps = cdiv(cdiv(std::max<int64_t>(n_pts, 1), splits), kFwdTJ) * kFwdTJ;
+    sp = (int)std::max<int64_t>(1, cdiv(n_pts, sps));
+  };
+  fwd(n_s, p.fwd_splits, p.fwd_sps);
+  fwd(n_q, p.mfa_splits, p.mfa_sps);
   // ---- K3 / K4: splits over antennas
   auto adj = [&](int64_t n_pts, int floats_per_pt, int &sp, int64_t &aps) {
     const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
@@ -89,7 +94,9 @@ bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
   p.off_tmp = take((size_t)kTmpN * 4);
   p.off_bwds = take((size_t)5 * n_s * 4);
   p.off_fltm = take((size_t)n_q * 8);
-  p.off_fwdp = take(p.fwd_splits > 1 ? (size_t)p.fwd_splits * n_a * n_f * 8 : 0);
+  p.off_qrec = take((size_t)n_q * sizeof(Rec));
+  const int fsp = std::max(p.fwd_splits, p.mfa_splits);
+  p.off_fwdp = take(fsp > 1 ? (size_t)fsp * n_a * n_f * 8 : 0);
   p.off_bwdp = take(p.bwd_splits > 1 ? (size_t)p.bwd_splits * 5 * n_s * 4 : 0);
   p.off_fltp = take(p.flt_splits > 1 ? (size_t)p.flt_splits * n_q * 8 : 0);
   p.total = o;
@@ -208,7 +215,7 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;
-  RFR_CU(launch_trace_fwd(a, p.B, mono, has_corr(samples, ants), p.fwd_splits, st));
+  RFR_CU(launch_trace_fwd(a, p.B, mono, has_corr(samples, ants), kFwdTrace, p.fwd_splits, st));
   if (p.fwd_splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, p.off_fwdp), p.fwd_splits,
                              ants->n_ant * (int64_t)grid->n_freq * 2, signal, p.n_sm, st));
@@ -378,6 +385,64 @@ rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, fl
   rfr_opts o2;
   o2.flags = (opts ? opts->flags : 0u) | RFR_REUSE_BLEND;   // K1 ran in the partial call
   return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, ws_bytes, stream);
+}
+
+rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const float *power,
+                               float eps, const rfr_antennas *ants, const rfr_freq_grid *grid,
+                               const float *qx, const float *qy, const float *qz, int64_t n_query,
+                               float *grad_signal, void *ws, size_t ws_bytes,
+                               rfr_stream_t stream) {
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  if (n_query < 0 || !ws || !(eps >= 0.f) || (ants->n_ant > 0 && !grad_signal) ||
+      (n_query > 0 && (!grad_power || !mf || !qx || !qy || !qz)))
+    return RFR_E_ARG;
+  if (ants->phi_tx || ants->phi_rx) return RFR_E_ARG;      // the filter has no transmittance
+  Plan p;
+  if (!make_plan(0, ants->n_ant, grid->n_freq, n_query, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (ants->n_ant == 0) return RFR_OK;
+  Rec *qrec = at<Rec>(ws, p.off_qrec);
+  RFR_CU(launch_mf_adj_pack(grad_power, mf, power, eps, qx, qy, qz, n_query, qrec, p.n_sm, st));
+  FwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rec = qrec;
+  a.n_s = n_query;
+  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
+  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
+  a.n_a = ants->n_ant;
+  a.n_f = grid->n_freq; a.nb = p.nb; a.ta = p.ta;
+  a.k0 = grid->f0_hz / kC;
+  a.kd = grid->df_hz / kC;
+  a.kw = grid->df_hz * p.B / kC;
+  a.samples_per_split = p.mfa_sps;
+  a.out = p.mfa_splits > 1 ? at<float2>(ws, p.off_fwdp) : reinterpret_cast<float2 *>(grad_signal);
+  a.smem_ant_off = fwd_smem_ant_off(p.nb, p.ta);
+  a.flags = at<unsigned>(ws, 0);
+  a.no_gain = false;
+  const bool mono = ants->rx_x == nullptr;
+  RFR_CU(launch_trace_fwd(a, p.B, mono, false, kFwdMFAdj, p.mfa_splits, st));
+  if (p.mfa_splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, p.off_fwdp), p.mfa_splits,
+                             ants->n_ant * (int64_t)grid->n_freq * 2, grad_signal, p.n_sm, st));
+  return RFR_OK;
+}
+
+rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n_query,
+                            const int32_t *cell, float *history, float thr_hi, float ratio,
+                            float *grad_power, uint8_t *mask, float *loss, void *ws,
+                            size_t ws_bytes, rfr_stream_t stream) {
+  if (n_query < 0 || !ws || !loss || (n_query > 0 && (!power || !power_gt || !grad_power)) ||
+      ((history == nullptr) != (cell == nullptr)))
+    return RFR_E_ARG;
+  Plan p;
+  if (!make_plan(0, 0, 1, 0, p)) return RFR_E_SHAPE;
+  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  RFR_CU(launch_heat_loss(power, power_gt, n_query, cell, history, thr_hi, ratio, grad_power, mask,
+                          at<float>(ws, p.off_tmp), kTmpN, loss, st));
+  return RFR_OK;
 }
 
 rfr_status rfr_poll_flags(void *ws, uint32_t *flags) {

@@ -112,6 +112,16 @@ struct PairBwd {
   bool ok;            // false: closer than u_min (contributes 0)
 };
 
+// Path length d_t + d_r in fp64 only (matched-filter adjoint: no amplitude factors, Eq. 3)
+template <bool MONO>
+__device__ __forceinline__ double pair_length(const Rec &r, const AntD &a) {
+  double dx = r.x - a.x, dy = r.y - a.y, dz = r.z - a.z;
+  double dt = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+  if (MONO) return 2.0 * dt;
+  double ex = a.rx - r.x, ey = a.ry - r.y, ez = a.rz - r.z;
+  return dt + sqrt(fma(ex, ex, fma(ey, ey, ez * ez)));
+}
+
 // Shared geometry: distances in fp64 (phase precision), directions / gain / decay in fp32.
 template <bool MONO, bool CORR>
 __device__ __forceinline__ void pair_geometry(const Rec &r, const AntD &a, bool no_gain,

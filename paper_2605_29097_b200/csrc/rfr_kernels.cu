@@ -62,7 +62,12 @@ __global__ void k_blend(BlendArgs a) {
 //   phase 2: each thread runs the Chebyshev recurrence y_{m+1} = 2cos(theta) y_m - y_{m-1} over its
 //            B bins from its anchor, in the sign-alternating form q_m = sigma_m y_m
 //            (sigma = +,+,-,-) so that every step is ONE FFMA2 and every accumulate ONE FADD2.
-template <int B, bool MONO, bool CORR>
+//
+// KIND == kFwdMFAdj (K5, matched-filter adjoint): the "samples" are filter queries packed by
+// k_mf_adj_pack as {x, y, z, w = Re c_q, T = Im c_q} with c_q = (dL/dP_q) M_q / max(P_q, eps); the
+// per-pair amplitude is the complex c_q itself (no gain, decay or transmittance), so the kernel
+// computes dL/ds(i,m) = sum_q c_q e^{-j 2 pi f_m tau_iq} with the same anchors and recurrence.
+template <int B, bool MONO, bool CORR, int KIND>
 __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -110,19 +115,31 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
         continue;
       }
       const Rec rec = a.rec[j];
-      PairBwd g;
-      pair_geometry<MONO, CORR>(rec, ant[aa], no_gain, g);
-      domain |= !g.ok;
-      const float A = rec.w * g.gg * g.Tt * g.Tr;
+      double L;
+      float Ar, Ai;
+      if (KIND == kFwdTrace) {
+        PairBwd g;
+        pair_geometry<MONO, CORR>(rec, ant[aa], no_gain, g);
+        domain |= !g.ok;
+        Ar = rec.w * g.gg * g.Tt * g.Tr;
+        Ai = 0.f;
+        L = g.L;
+      } else {
+        L = pair_length<MONO>(rec, ant[aa]);
+        Ar = rec.w;
+        Ai = rec.T;
+      }
       // phase anchors from fp64 cycle counts (cycles = L f / c), reduced to [-0.5, 0.5]
-      const float fr0 = frac_cycles(g.L * a.k0);
-      const float frd = frac_cycles(g.L * a.kd);
-      const float frw = frac_cycles(g.L * a.kw);
+      const float fr0 = frac_cycles(L * a.k0);
+      const float frd = frac_cycles(L * a.kd);
+      const float frw = frac_cycles(L * a.kw);
       float es, ec, zs, zc, ws, wc;
       __sincosf(kTwoPi * fr0, &es, &ec);            // anchor phase: MUFU, error not amplified
       sincospif(2.f * frd, &zs, &zc);               // recurrence step: accurate (sets 2cos theta)
       __sincosf(kTwoPi * frw, &ws, &wc);            // block step
-      f2x c = pk(A * ec, -A * es);                  // A e^{-j theta0}
+      // A e^{-j theta0} (real A: trace; complex A: matched-filter adjoint)
+      f2x c = (KIND == kFwdTrace) ? pk(Ar * ec, -Ar * es)
+                                  : pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
       const f2x zz = pk(zc, -zs), ww = pk(wc, -ws);
       for (int b = 0; b < nb; ++b) {
         const float2 y0 = upk(c), y1 = upk(cmul2(c, zz));
@@ -436,9 +453,9 @@ cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st) {
   return counted(cudaGetLastError());
 }
 
-template <int B, bool MONO, bool CORR>
+template <int B, bool MONO, bool CORR, int KIND>
 static cudaError_t fwd_t(const FwdArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
-  auto k = k_trace_fwd<B, MONO, CORR>;
+  auto k = k_trace_fwd<B, MONO, CORR, KIND>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, kFwdThreads, smem, st>>>(a);
@@ -446,22 +463,107 @@ static cudaError_t fwd_t(const FwdArgs &a, dim3 grid, size_t smem, cudaStream_t 
 }
 
 template <int B>
-static cudaError_t fwd_b(const FwdArgs &a, bool mono, bool corr, dim3 g, size_t sm, cudaStream_t st) {
-  if (mono) return corr ? fwd_t<B, true, true>(a, g, sm, st) : fwd_t<B, true, false>(a, g, sm, st);
-  return corr ? fwd_t<B, false, true>(a, g, sm, st) : fwd_t<B, false, false>(a, g, sm, st);
+static cudaError_t fwd_b(const FwdArgs &a, bool mono, bool corr, int kind, dim3 g, size_t sm,
+                         cudaStream_t st) {
+  if (kind == kFwdMFAdj)
+    return mono ? fwd_t<B, true, false, kFwdMFAdj>(a, g, sm, st)
+                : fwd_t<B, false, false, kFwdMFAdj>(a, g, sm, st);
+  if (mono)
+    return corr ? fwd_t<B, true, true, kFwdTrace>(a, g, sm, st)
+                : fwd_t<B, true, false, kFwdTrace>(a, g, sm, st);
+  return corr ? fwd_t<B, false, true, kFwdTrace>(a, g, sm, st)
+              : fwd_t<B, false, false, kFwdTrace>(a, g, sm, st);
 }
 
-cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int n_splits,
+cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int kind, int n_splits,
                              cudaStream_t st) {
   const int64_t n_tiles = (a.n_a + a.ta - 1) / a.ta;
   dim3 grid((unsigned)n_tiles, (unsigned)n_splits);
   const size_t smem = fwd_smem_bytes(a.nb, a.ta);
   switch (B) {
-    case 8: return fwd_b<8>(a, mono, corr, grid, smem, st);
-    case 16: return fwd_b<16>(a, mono, corr, grid, smem, st);
-    case 32: return fwd_b<32>(a, mono, corr, grid, smem, st);
+    case 8: return fwd_b<8>(a, mono, corr, kind, grid, smem, st);
+    case 16: return fwd_b<16>(a, mono, corr, kind, grid, smem, st);
+    case 32: return fwd_b<32>(a, mono, corr, kind, grid, smem, st);
   }
   return cudaErrorInvalidValue;
+}
+
+// K5 prep: c_q = (dL/dP_q) M_q / max(P_q, eps) packed with the fp64 query position.
+__global__ void k_mf_adj_pack(const float *__restrict__ gP, const float2 *__restrict__ M,
+                              const float *__restrict__ P, float eps, const float *__restrict__ qx,
+                              const float *__restrict__ qy, const float *__restrict__ qz,
+                              int64_t n, Rec *__restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const float2 m = M[q];
+    const float p = P ? P[q] : sqrtf(fmaf(m.x, m.x, m.y * m.y));
+    const float sc = gP[q] / fmaxf(p, eps);
+    Rec r;
+    r.x = (double)qx[q]; r.y = (double)qy[q]; r.z = (double)qz[q];
+    r.w = sc * m.x;
+    r.T = sc * m.y;
+    r.nx = r.ny = 0.f; r.nz = 1.f; r.papr = 1.f;
+    out[q] = r;
+  }
+}
+
+cudaError_t launch_mf_adj_pack(const float *gP, const float *M, const float *P, float eps,
+                               const float *qx, const float *qy, const float *qz, int64_t n,
+                               Rec *out, int n_sm, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>(grid1(n, 256), (int64_t)n_sm * 8);
+  k_mf_adj_pack<<<g, 256, 0, st>>>(gP, reinterpret_cast<const float2 *>(M), P, eps, qx, qy, qz, n,
+                                   out);
+  return counted(cudaGetLastError());
+}
+
+// ================================================================================== K7 heatmap loss
+// Masked heatmap-domain L2 with the dynamic loss mask of P:L392-402:
+// keep_q = !(H[cell_q] > thr_hi && P_q < ratio H[cell_q]) against the history BEFORE this call.
+__global__ void k_heat_loss(const float *__restrict__ P, const float *__restrict__ Pgt, int64_t n,
+                            const int *__restrict__ cell, const float *__restrict__ H,
+                            float thr_hi, float ratio, float *__restrict__ gP,
+                            unsigned char *__restrict__ mask, float *__restrict__ part) {
+  __shared__ float sh[32];
+  float v = 0.f;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const float p = P[q];
+    bool keep = true;
+    if (H) {
+      const float h = H[cell[q]];
+      keep = !(h > thr_hi && p < ratio * h);
+    }
+    const float d = p - Pgt[q];
+    gP[q] = keep ? d : 0.f;
+    if (mask) mask[q] = keep ? 1 : 0;
+    if (keep) v = fmaf(d, d, v);
+  }
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = 0.5f * v;
+}
+
+// H[c] = max(H[c], P_q): order-independent (integer max on the bits of non-negative floats)
+__global__ void k_heat_hist(const float *__restrict__ P, int64_t n, const int *__restrict__ cell,
+                            float *H) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const float p = P[q];
+    if (p > 0.f) atomicMax(reinterpret_cast<int *>(H) + cell[q], __float_as_int(p));
+  }
+}
+
+cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const int *cell, float *H,
+                             float thr_hi, float ratio, float *gP, unsigned char *mask, float *tmp,
+                             int tmp_n, float *loss, cudaStream_t st) {
+  k_heat_loss<<<tmp_n, 256, 0, st>>>(P, Pgt, n, cell, H, thr_hi, ratio, gP, mask, tmp);
+  k_reduce_sum<<<1, 256, 0, st>>>(tmp, tmp_n, loss);
+  int launched = 2;
+  if (H && n > 0) {
+    k_heat_hist<<<tmp_n, 256, 0, st>>>(P, n, cell, H);
+    ++launched;
+  }
+  return counted(cudaGetLastError(), launched);
 }
 
 template <int MODE, bool MONO, bool CORR>

@@ -14,6 +14,7 @@ constexpr int kAdjThreads = 128;   // K3/K4 CTA size
 constexpr int kAdjSPT = 2;         // samples (queries) per K3/K4 thread
 constexpr int kAdjGA = 8;          // antennas per K3/K4 shared-memory stage
 constexpr int kModeBwd = 0, kModeFlt = 1;
+constexpr int kFwdTrace = 0, kFwdMFAdj = 1;  // K2 signal tracing / K5 matched-filter adjoint
 
 struct BlendArgs {
   const float *x, *y, *z, *sdf, *refl, *nx, *ny, *nz, *power, *phi_origin;
@@ -77,8 +78,14 @@ inline size_t adj_smem_bytes(int n_f) { return adj_smem_ant_off(n_f) + (size_t)k
 
 unsigned long long launch_count();
 cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st);
-cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int n_splits,
+cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int kind, int n_splits,
                              cudaStream_t st);
+cudaError_t launch_mf_adj_pack(const float *gP, const float *M, const float *P, float eps,
+                               const float *qx, const float *qy, const float *qz, int64_t n,
+                               Rec *out, int n_sm, cudaStream_t st);
+cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const int *cell, float *H,
+                             float thr_hi, float ratio, float *gP, unsigned char *mask, float *tmp,
+                             int tmp_n, float *loss, cudaStream_t st);
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st);
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st);

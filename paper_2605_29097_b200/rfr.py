@@ -56,6 +56,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too sm
 
 EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_filter_partial",
            "rfr_filter_power", "rfr_backward", "rfr_backward_partial", "rfr_backward_finish",
+           "rfr_filter_backward", "rfr_heatmap_loss",
            "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count")
 
 
@@ -87,6 +88,8 @@ def load(path: str = LIB_PATH):
         "rfr_backward": [vp, S, f, A, G, O, R, vp, C.c_size_t, vp],
         "rfr_backward_partial": [vp, S, f, A, G, O, vp, vp, C.c_size_t, vp],
         "rfr_backward_finish": [vp, S, f, O, R, vp, C.c_size_t, vp],
+        "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, vp, C.c_size_t, vp],
+        "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, vp, C.c_size_t, vp],
         "rfr_poll_flags": [vp, C.POINTER(u32)],
     }
     for name, args in sig.items():
@@ -241,6 +244,34 @@ def rfr_filter_power(mf: torch.Tensor, power: torch.Tensor, stream=None):
     _check(load().rfr_filter_power(_ptr(mf), int(power.numel()), _ptr(power), _stream(stream)),
            "rfr_filter_power")
     return power
+
+
+def rfr_filter_backward(grad_power: torch.Tensor, mf: torch.Tensor, ants: DeviceAntennas, grid,
+                        qx, qy, qz, grad_signal: torch.Tensor, ws: torch.Tensor,
+                        power: Optional[torch.Tensor] = None, eps: float = 0.0, stream=None):
+    """K5: dL/ds for a loss of the filter power (see include/librfr.h)."""
+    a, g = ants.struct(), grid_struct(grid)
+    _check(load().rfr_filter_backward(_ptr(grad_power), _ptr(mf), _ptr(power), float(eps),
+                                      C.byref(a), C.byref(g), _ptr(qx), _ptr(qy), _ptr(qz),
+                                      int(qx.numel()), _ptr(grad_signal), _ptr(ws), ws.numel(),
+                                      _stream(stream)), "rfr_filter_backward")
+    return grad_signal
+
+
+def rfr_heatmap_loss(power: torch.Tensor, power_gt: torch.Tensor, grad_power: torch.Tensor,
+                     loss: torch.Tensor, ws: torch.Tensor, cell: Optional[torch.Tensor] = None,
+                     history: Optional[torch.Tensor] = None, thr_hi: float = 0.0,
+                     ratio: float = 0.0, mask: Optional[torch.Tensor] = None, stream=None):
+    """K7: masked heatmap L2 (see include/librfr.h).  cell: int32, history: float32, mask: uint8."""
+    if cell is not None and cell.dtype != torch.int32:
+        raise RfrError("cell must be int32")
+    if mask is not None and mask.dtype != torch.uint8:
+        raise RfrError("mask must be uint8")
+    _check(load().rfr_heatmap_loss(_ptr(power), _ptr(power_gt), int(power.numel()), _ptr(cell),
+                                   _ptr(history), float(thr_hi), float(ratio), _ptr(grad_power),
+                                   _ptr(mask), _ptr(loss), _ptr(ws), ws.numel(), _stream(stream)),
+           "rfr_heatmap_loss")
+    return loss, grad_power
 
 
 @dataclasses.dataclass

@@ -19,16 +19,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--ants", type=int, default=0, help="profile on the first N antennas only")
     a = ap.parse_args()
     p = synth.make(a.config)
     b = p.bundles[0]
     dev = torch.device("cuda:0")
     S = rfr.DeviceSamples.from_host(b.samples, dev)
     A = rfr.DeviceAntennas.from_host(b.antennas, dev)
-    n, na, nf = b.samples.n, b.antennas.n, p.grid.n_freq
+    if a.ants:
+        A = A.slice(0, a.ants)
+    n, na, nf = b.samples.n, A.n, p.grid.n_freq
     ws = rfr.workspace(n, na, nf, n, dev)
     sig = torch.empty(na, nf, 2, device=dev)
-    G = torch.as_tensor(np.stack([p.random_grad().real, p.random_grad().imag], -1)).to(dev)
+    g = p.random_grad()[:na]
+    G = torch.as_tensor(np.stack([g.real, g.imag], -1)).contiguous().to(dev)
     M = torch.empty(n, 2, device=dev)
     P = torch.empty(n, device=dev)
     part = torch.empty(5, n, device=dev)
@@ -38,6 +42,7 @@ def main():
         rfr.rfr_filter(sig, A, p.grid, S.x, S.y, S.z, P, ws, mf=M)
         rfr.rfr_backward_partial(G, S, p.sharpness, A, p.grid, part, ws, flags=rfr.RFR_REUSE_BLEND)
         rfr.rfr_backward_finish(part, S, p.sharpness, out, ws, flags=rfr.RFR_REUSE_BLEND)
+        rfr.rfr_filter_backward(P, M, A, p.grid, S.x, S.y, S.z, G, ws, power=P, eps=1e-20)
     torch.cuda.synchronize()
     print("profile_step ok", a.config, rfr.rfr_launch_count())
 
