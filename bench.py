@@ -182,6 +182,8 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     rfr.load()
+    # librfr's own NCCL communicator carries the data-path all-reduces (a4 M, a7 partials)
+    comm = rfr.Comm.create() if world > 1 else None
     prob = synth.make(args.config)
     grid = prob.grid
     st = torch.cuda.current_stream()
@@ -225,20 +227,13 @@ def run_gpu(args):
             if e: e[0].record(st)
             rfr.rfr_forward(s["S"], prob.sharpness, s["A"], grid, s["sig"], s["ws"])
             if e: e[1].record(st)
-            rfr.rfr_filter_partial(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["M"],
-                                   s["ws"])
-            if world > 1:
-                dist.all_reduce(s["M"])
-            rfr.rfr_filter_power(s["M"], s["P"])
+            rfr.rfr_filter(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P"], s["ws"],
+                           mf=s["M"], comm=comm)
             if e: e[2].record(st)
             rfr.rfr_loss(s["sig"], s["y"], s["G"], s["loss"], s["ws"])
             if e: e[3].record(st)
-            rfr.rfr_backward_partial(s["G"], s["S"], prob.sharpness, s["A"], grid, s["part"],
-                                     s["ws"], flags=rfr.RFR_REUSE_BLEND)
-            if world > 1:
-                dist.all_reduce(s["part"])
-            rfr.rfr_backward_finish(s["part"], s["S"], prob.sharpness, s["out"], s["ws"],
-                                    flags=rfr.RFR_REUSE_BLEND)
+            rfr.rfr_backward(s["G"], s["S"], prob.sharpness, s["A"], grid, s["out"], s["ws"],
+                             flags=rfr.RFR_REUSE_BLEND, comm=comm)
             if e:
                 e[4].record(st)
                 rec.append(e)
@@ -291,6 +286,8 @@ def run_gpu(args):
     e2e = run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step)
 
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return 0
@@ -336,8 +333,8 @@ def run_gpu(args):
                        "n_antennas": [b.antennas.n for b in prob.bundles][0],
                        "n_freq": grid.n_freq, "parallelism": f"antenna-shard x{world}",
                        "l2": "flushed between steps (512 MiB memset, outside the step events)",
-                       "step": "K1 blend + K2 forward + K4 filter (+all-reduce M) + K6 loss + "
-                               "K3 backward (+all-reduce partials) + K1' finish"},
+                       "step": "K1 blend + K2 forward + K4 filter (+NCCL all-reduce of M) + K6 "
+                               "loss + K3 backward (+NCCL all-reduce of partials) + K1' finish"},
             "passes": {"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
                        "filter_G_per_s": Nc / (per_step(q_ms) * 1e-3) / 1e9,
                        "bwd_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
@@ -346,6 +343,8 @@ def run_gpu(args):
             "roofline": roof, "rooflines": roofs, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed": t_wall}
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -47,8 +47,13 @@ typedef enum {
   RFR_E_DOMAIN = 3,   /* (rfr_poll_flags only) a pair closer than u_min = 1 mm contributed 0     */
   RFR_E_NUMERIC = 4,  /* (rfr_poll_flags only) non-finite input seen with RFR_CHECK_FINITE       */
   RFR_E_CUDA = 5,     /* a kernel launch failed                                                  */
-  RFR_E_UNSUPPORTED = 6
+  RFR_E_UNSUPPORTED = 6,
+  RFR_E_NCCL = 7      /* an NCCL call of the multi-GPU path failed                               */
 } rfr_status;
+
+/* Opaque multi-GPU communicator (one NCCL communicator per rank).  NULL everywhere a
+ * `const rfr_comm *` is taken means "single GPU, no communication". */
+typedef struct rfr_comm rfr_comm;
 
 /* option flags (rfr_opts.flags) */
 #define RFR_NO_GAIN 1u       /* drop the directive gain (w_o . w_r): the E11 ablation   */
@@ -118,10 +123,13 @@ rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex,
                     float *loss, void *ws, size_t ws_bytes, rfr_stream_t stream);
 
 /* Eq. 3 matched filter at n_query points: M_q = sum_i sum_m s(i,m) exp(+j 2 pi f_m tau_iq),
- * power[q] = |M_q| (float32), mf (optional, complex64 [n_query]) = M_q.  Sign as printed (Q2). */
+ * power[q] = |M_q| (float32), mf (optional, complex64 [n_query]) = M_q.  Sign as printed (Q2).
+ * comm != NULL: `ants`/`signal` are this rank's antenna slice; the partial M is summed over the
+ * ranks (ncclAllReduce on `stream`) before |M|, so every rank returns the full P and M. */
 rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_freq_grid *grid,
                       const float *qx, const float *qy, const float *qz, int64_t n_query,
-                      float *power, float *mf, void *ws, size_t ws_bytes, rfr_stream_t stream);
+                      float *power, float *mf, const rfr_comm *comm, void *ws, size_t ws_bytes,
+                      rfr_stream_t stream);
 /* Antenna-shard partial of the filter: mf (required) = this shard's complex M_q. */
 rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
                               const rfr_freq_grid *grid, const float *qx, const float *qy,
@@ -157,11 +165,14 @@ rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n
                             size_t ws_bytes, rfr_stream_t stream);
 
 /* Backward: grad_signal = G = dL/dRe s + j dL/dIm s, complex64 [n_ant][n_freq] (Q14).
- * Writes dL/d{sdf, refl, n, power} per sample and dL/dsharpness.  = partial + finish. */
+ * Writes dL/d{sdf, refl, n, power} per sample and dL/dsharpness.  = partial + finish.
+ * comm != NULL: `ants`/`grad_signal` are this rank's antenna slice; the per-sample partials are
+ * summed over the ranks (ncclAllReduce on `stream`) between K3 and K1', so every rank returns the
+ * full gradients. */
 rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,
                         const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_opts *opts,
-                        const rfr_sample_grads *out, void *ws, size_t ws_bytes,
-                        rfr_stream_t stream);
+                        const rfr_sample_grads *out, const rfr_comm *comm, void *ws,
+                        size_t ws_bytes, rfr_stream_t stream);
 /* K3: per-sample antenna sums of this antenna shard, partials float32 SoA [5][n_samples]:
  *   row 0  S1 = sum_i R_ij g gamma T_t T_r                 (= dL/dw_j, w = p a alpha)
  *   row 1  S2 = sum_i R_ij g gamma (T_r chi_t + T_t chi_r)  (dL/dT_j = w_j S2)
@@ -175,6 +186,14 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
 rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
                                const rfr_opts *opts, const rfr_sample_grads *out, void *ws,
                                size_t ws_bytes, rfr_stream_t stream);
+
+/* Multi-GPU communicator.  Rank 0 calls rfr_comm_unique_id (128 opaque bytes) and the caller
+ * distributes the bytes to every rank; each rank then calls rfr_comm_init on its own device (it
+ * blocks until all nranks ranks joined).  rfr_comm_destroy frees it.  Host calls; RFR_E_NCCL on an
+ * NCCL failure. */
+rfr_status rfr_comm_unique_id(void *id /* 128 bytes, written */);
+rfr_status rfr_comm_init(const void *id, int nranks, int rank, rfr_comm **out);
+rfr_status rfr_comm_destroy(rfr_comm *comm);
 
 /* Synchronously read (and clear) the device flags RFR_FLAG_DOMAIN / RFR_FLAG_NUMERIC. */
 rfr_status rfr_poll_flags(void *ws, uint32_t *flags);

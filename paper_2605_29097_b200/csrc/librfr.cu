@@ -1,9 +1,11 @@
 // librfr.cu -- C ABI (include/librfr.h): argument validation, workspace planning, kernel launches.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <nccl.h>
 #include <string.h>
 
 #include <mutex>
+#include <new>
 
 #include "../../include/librfr.h"
 #include "rfr_device.cuh"
@@ -38,7 +40,7 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Plan {
   int n_sm = 148;
   // forward (K2)
-  int B = 32, nb = 1, ta = 256, fwd_splits = 1, mfa_splits = 1;
+  int B = 32, nb = 1, nb_total = 1, taw = 32, chunks = 1, fwd_splits = 1, mfa_splits = 1;
   int64_t fwd_sps = 0, mfa_sps = 0;
   // adjoint (K3) and filter (K4)
   int bwd_splits = 1, flt_splits = 1;
@@ -54,10 +56,12 @@ bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
   const int nf = n_f > 0 ? n_f : 1;
   // ---- K2: B bins per thread, nb blocks per antenna, ta antennas per CTA
   p.B = nf >= 32 ? 32 : (nf >= 16 ? 16 : 8);
-  p.nb = (int)cdiv(nf, p.B);
-  if (p.nb > kFwdThreads) return false;                    // n_freq > 8192
-  p.ta = kFwdThreads / p.nb;
-  const int64_t n_tiles = n_a > 0 ? cdiv(n_a, p.ta) : 1;
+  p.nb_total = (int)cdiv(nf, p.B);
+  if (p.nb_total > 256) return false;                      // n_freq > 8192
+  p.nb = std::min(p.nb_total, 32);                         // bin blocks per warp (one chunk)
+  p.chunks = (int)cdiv(p.nb_total, p.nb);
+  p.taw = 32 / p.nb;                                       // antennas per warp
+  const int64_t n_tiles = (n_a > 0 ? cdiv(n_a, (int64_t)kFwdWarps * p.taw) : 1) * p.chunks;
   // split-K over the summed points (samples for K2, queries for K5)
   auto fwd = [&](int64_t n_pts, int &sp, int64_t &sps) {
     const int64_t target = (int64_t)p.n_sm * 2 * 32;       // ~32 waves at 2 CTAs / SM
@@ -155,7 +159,57 @@ bool has_corr(const rfr_samples *s, const rfr_antennas *a) {
 
 }  // namespace
 
+// Opaque communicator of the multi-GPU path: one NCCL communicator per rank, built from
+// a unique id the caller distributes (e.g. a torch.distributed broadcast).
+struct rfr_comm {
+  ncclComm_t nccl;
+  int nranks, rank;
+};
+
+namespace {
+// In-place sum of n floats over the communicator's ranks on `st` (an identity for one rank; the
+// call is still issued so the one-GPU tests exercise the NCCL path).
+rfr_status allreduce_sum(const rfr_comm *c, float *buf, int64_t n, cudaStream_t st) {
+  if (!c || n <= 0) return RFR_OK;
+  if (ncclAllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, c->nccl, st) != ncclSuccess)
+    return RFR_E_NCCL;
+  return RFR_OK;
+}
+}  // namespace
+
 extern "C" {
+
+rfr_status rfr_comm_unique_id(void *id) {
+  if (!id) return RFR_E_ARG;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return RFR_E_NCCL;
+  memcpy(id, &u, sizeof(u));
+  return RFR_OK;
+}
+
+rfr_status rfr_comm_init(const void *id, int nranks, int rank, rfr_comm **out) {
+  if (!id || !out || nranks <= 0 || rank < 0 || rank >= nranks) return RFR_E_ARG;
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  rfr_comm *c = new (std::nothrow) rfr_comm;
+  if (!c) return RFR_E_ARG;
+  c->nranks = nranks;
+  c->rank = rank;
+  if (ncclCommInitRank(&c->nccl, nranks, u, rank) != ncclSuccess) {
+    delete c;
+    return RFR_E_NCCL;
+  }
+  *out = c;
+  return RFR_OK;
+}
+
+rfr_status rfr_comm_destroy(rfr_comm *c) {
+  if (!c) return RFR_E_ARG;
+  ncclResult_t r = ncclCommDestroy(c->nccl);
+  delete c;
+  return r == ncclSuccess ? RFR_OK : RFR_E_NCCL;
+}
+
 
 int rfr_abi_version(void) { return RFR_ABI_VERSION; }
 
@@ -170,6 +224,7 @@ const char *rfr_status_string(rfr_status s) {
     case RFR_E_NUMERIC: return "non-finite input";
     case RFR_E_CUDA: return "CUDA launch failure";
     case RFR_E_UNSUPPORTED: return "unsupported configuration";
+    case RFR_E_NCCL: return "NCCL failure";
   }
   return "unknown status";
 }
@@ -205,13 +260,14 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
   a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
   a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
   a.n_a = ants->n_ant;
-  a.n_f = grid->n_freq; a.nb = p.nb; a.ta = p.ta;
+  a.n_f = grid->n_freq; a.nb = p.nb; a.nb_total = p.nb_total; a.taw = p.taw;
+  a.warp_smem = fwd_warp_smem();
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.kw = grid->df_hz * p.B / kC;
+  a.kchunk = grid->df_hz * p.B * p.nb / kC;
   a.samples_per_split = p.fwd_sps;
   a.out = p.fwd_splits > 1 ? at<float2>(ws, p.off_fwdp) : reinterpret_cast<float2 *>(signal);
-  a.smem_ant_off = fwd_smem_ant_off(p.nb, p.ta);
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;
@@ -236,8 +292,8 @@ rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex,
 
 static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
                               const rfr_freq_grid *grid, const float *qx, const float *qy,
-                              const float *qz, int64_t n_query, float *power, float *mf, void *ws,
-                              size_t ws_bytes, cudaStream_t st) {
+                              const float *qz, int64_t n_query, float *power, float *mf,
+                              const rfr_comm *comm, void *ws, size_t ws_bytes, cudaStream_t st) {
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
   if (n_query < 0 || !ws || (n_query > 0 && (!qx || !qy || !qz)) ||
@@ -268,15 +324,17 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   RFR_CU(launch_adjoint(a, kModeFlt, mono, false, p.flt_splits, st));
   if (p.flt_splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, p.off_fltp), p.flt_splits, n_query * 2, M, p.n_sm, st));
+  RFR_TRY(allreduce_sum(comm, M, 2 * n_query, st));     // antenna shards -> full M (a4)
   if (power) RFR_CU(launch_abs(M, n_query, power, p.n_sm, st));
   return RFR_OK;
 }
 
 rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_freq_grid *grid,
                       const float *qx, const float *qy, const float *qz, int64_t n_query,
-                      float *power, float *mf, void *ws, size_t ws_bytes, rfr_stream_t stream) {
+                      float *power, float *mf, const rfr_comm *comm, void *ws, size_t ws_bytes,
+                      rfr_stream_t stream) {
   if (!power && n_query > 0) return RFR_E_ARG;
-  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, ws, ws_bytes,
+  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, comm, ws, ws_bytes,
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -285,7 +343,7 @@ rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
                               const float *qz, int64_t n_query, float *mf, void *ws,
                               size_t ws_bytes, rfr_stream_t stream) {
   if (!mf && n_query > 0) return RFR_E_ARG;
-  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, nullptr, mf, ws, ws_bytes,
+  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, nullptr, mf, nullptr, ws, ws_bytes,
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -370,8 +428,8 @@ rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples
 
 rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,
                         const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_opts *opts,
-                        const rfr_sample_grads *out, void *ws, size_t ws_bytes,
-                        rfr_stream_t stream) {
+                        const rfr_sample_grads *out, const rfr_comm *comm, void *ws,
+                        size_t ws_bytes, rfr_stream_t stream) {
   RFR_TRY(check_samples(samples));
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
@@ -382,6 +440,8 @@ rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, fl
   float *part = at<float>(ws, p.off_bwds);
   RFR_TRY(rfr_backward_partial(grad_signal, samples, sharpness, ants, grid, opts, part, ws,
                                ws_bytes, stream));
+  // a7: sum the per-sample partials over the antenna shards
+  RFR_TRY(allreduce_sum(comm, part, 5 * n_s, reinterpret_cast<cudaStream_t>(stream)));
   rfr_opts o2;
   o2.flags = (opts ? opts->flags : 0u) | RFR_REUSE_BLEND;   // K1 ran in the partial call
   return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, ws_bytes, stream);
@@ -412,13 +472,14 @@ rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const f
   a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
   a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
   a.n_a = ants->n_ant;
-  a.n_f = grid->n_freq; a.nb = p.nb; a.ta = p.ta;
+  a.n_f = grid->n_freq; a.nb = p.nb; a.nb_total = p.nb_total; a.taw = p.taw;
+  a.warp_smem = fwd_warp_smem();
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.kw = grid->df_hz * p.B / kC;
+  a.kchunk = grid->df_hz * p.B * p.nb / kC;
   a.samples_per_split = p.mfa_sps;
   a.out = p.mfa_splits > 1 ? at<float2>(ws, p.off_fwdp) : reinterpret_cast<float2 *>(grad_signal);
-  a.smem_ant_off = fwd_smem_ant_off(p.nb, p.ta);
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = false;
   const bool mono = ants->rx_x == nullptr;

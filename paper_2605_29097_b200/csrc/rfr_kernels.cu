@@ -54,33 +54,51 @@ __global__ void k_blend(BlendArgs a) {
 }
 
 // ================================================================================== K2 forward
-// Thread (a, b) of a CTA owns antenna a0+a and bins [b*B, b*B+B): B complex accumulators in
-// registers (packed f32x2).  Per tile of TJ samples:
-//   phase 1: every (antenna, sample) pair of the tile computes its geometry in fp64, the Eq. 5
-//            amplitude, and the anchors y0_b = A e^{-j2pi(f0 + bB df)tau}, y1_b = y0_b z,
-//            z = e^{-j2pi df tau}, for every bin block b, into shared memory (b-major layout).
-//   phase 2: each thread runs the Chebyshev recurrence y_{m+1} = 2cos(theta) y_m - y_{m-1} over its
-//            B bins from its anchor, in the sign-alternating form q_m = sigma_m y_m
-//            (sigma = +,+,-,-) so that every step is ONE FFMA2 and every accumulate ONE FADD2.
+// Warp-independent design (no CTA barriers on the hot loop).  Warp w of a CTA owns taw = 32 / nbc
+// antennas (a0 + w taw ...) and all nbc bin blocks of B bins of this CTA's bin chunk; lane
+// (my_b, my_a) = (lane / taw, lane % taw) keeps B complex accumulators in registers (packed f32x2).
+// The warp walks its CTA's sample split in tiles of TJ samples:
+//   prefetch: the next tile's 48 B records are copied global -> shared with cp.async while the
+//             current tile runs (no register cost, latency hidden behind phase 2)
+//   phase 1:  the taw x TJ (antenna, sample) pairs of the tile, one per lane: fp64 geometry, the
+//             Eq. 5 amplitude, anchors y0_b = A e^{-j2pi(f0 + bB df)tau}, y1_b = y0_b z,
+//             z = e^{-j2pi df tau}, for every bin block b, into the warp's shared-memory slice
+//   phase 2:  each lane runs the Chebyshev recurrence y_{m+1} = 2cos(theta) y_m - y_{m-1} over its
+//             B bins in the sign-alternating form q_m = sigma_m y_m (sigma = +,+,-,-): ONE FFMA2
+//             per step and ONE FADD2 per accumulate.
+// Warps synchronise only with __syncwarp, so the FMA-light phase 1 of one warp overlaps the
+// FMA-bound phase 2 of the others.  Bin chunks (blockIdx.z) of 32 blocks cover n_f > 32 B.
 //
 // KIND == kFwdMFAdj (K5, matched-filter adjoint): the "samples" are filter queries packed by
 // k_mf_adj_pack as {x, y, z, w = Re c_q, T = Im c_q} with c_q = (dL/dP_q) M_q / max(P_q, eps); the
 // per-pair amplitude is the complex c_q itself (no gain, decay or transmittance), so the kernel
 // computes dL/ds(i,m) = sum_q c_q e^{-j 2 pi f_m tau_iq} with the same anchors and recurrence.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int B, bool MONO, bool CORR, int KIND>
 __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x;
-  const int nb = a.nb, ta = a.ta;
-  float4 *anc = reinterpret_cast<float4 *>(smem_raw);                 // [TJ][nb][ta]
-  float *kv = reinterpret_cast<float *>(anc + kFwdTJ * nb * ta);       // [TJ][ta]
-  AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);     // [ta]
-  const int64_t a0 = (int64_t)blockIdx.x * ta;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbc = a.nb, taw = a.taw;
+  unsigned char *wb = smem_raw + (size_t)warp * a.warp_smem;
+  float4 *anc = reinterpret_cast<float4 *>(wb);                          // [TJ][nbc][taw]
+  float *kv = reinterpret_cast<float *>(wb + kFwdTJ * 32 * 16);          // [TJ][taw]
+  AntD *ant = reinterpret_cast<AntD *>(wb + kFwdTJ * 32 * 20);           // [taw]
+  Rec *rbuf = reinterpret_cast<Rec *>(wb + kFwdTJ * 32 * 20 + 32 * sizeof(AntD));  // [2][TJ]
+  const int64_t a0 = ((int64_t)blockIdx.x * kFwdWarps + warp) * taw;
   const int64_t j_lo = (int64_t)blockIdx.y * a.samples_per_split;
   const int64_t j_hi = min(a.n_s, j_lo + a.samples_per_split);
+  const int chunk = blockIdx.z;
+  const double k0 = a.k0 + (double)chunk * a.kchunk;                    // f0 of this bin chunk / c
+  const int nb_here = min(nbc, a.nb_total - chunk * nbc);               // blocks in this chunk
   const bool no_gain = a.no_gain;
 
-  for (int aa = tid; aa < ta; aa += kFwdThreads) {
+  for (int aa = lane; aa < taw; aa += 32) {
     const int64_t ia = a0 + aa;
     AntD d;
     if (ia < a.n_a) {
@@ -94,27 +112,41 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
     }
     ant[aa] = d;
   }
-  // phase-2 identity: antenna fastest so shared-memory reads are consecutive across lanes
-  const int my_a = tid % ta, my_b = tid / ta;
-  const bool active = my_b < nb;
+  const int my_a = lane % taw, my_b = lane / taw;
+  const bool active = my_b < nb_here;
   f2x acc[B];
 #pragma unroll
   for (int m = 0; m < B; ++m) acc[m] = 0ull;
   bool domain = false;
-  __syncthreads();
 
-  for (int64_t jt = j_lo; jt < j_hi; jt += kFwdTJ) {
-    // ---------------- phase 1: per-pair geometry and anchors
-    for (int pr = tid; pr < ta * kFwdTJ; pr += kFwdThreads) {
-      const int aa = pr % ta, jj = pr / ta;
+  // records of one tile: TJ x 48 B = 24 chunks of 16 B, one per lane (lanes 24..31 idle)
+  auto prefetch = [&](int64_t jt, int buf) {
+    if (lane < kFwdTJ * 3) {
+      const int jj = lane / 3, part = lane % 3;
       const int64_t j = jt + jj;
-      float4 *dst = anc + (size_t)jj * nb * ta + aa;
+      if (j < j_hi)
+        cp_async16(reinterpret_cast<float4 *>(rbuf + buf * kFwdTJ + jj) + part,
+                   reinterpret_cast<const float4 *>(a.rec + j) + part);
+    }
+    cp_async_commit();
+  };
+  if (j_lo < j_hi) prefetch(j_lo, 0);
+  int buf = 0;
+  for (int64_t jt = j_lo; jt < j_hi; jt += kFwdTJ, buf ^= 1) {
+    cp_async_wait_all();
+    __syncwarp();
+    if (jt + kFwdTJ < j_hi) prefetch(jt + kFwdTJ, buf ^ 1);
+    // ---------------- phase 1: per-pair geometry and anchors (one pair per lane)
+    for (int pr = lane; pr < taw * kFwdTJ; pr += 32) {
+      const int aa = pr % taw, jj = pr / taw;
+      const int64_t j = jt + jj;
+      float4 *dst = anc + (size_t)jj * nbc * taw + aa;
       if (j >= j_hi || a0 + aa >= a.n_a) {
-        for (int b = 0; b < nb; ++b) dst[(size_t)b * ta] = make_float4(0.f, 0.f, 0.f, 0.f);
-        kv[jj * ta + aa] = 2.f;
+        for (int b = 0; b < nb_here; ++b) dst[(size_t)b * taw] = make_float4(0.f, 0.f, 0.f, 0.f);
+        kv[jj * taw + aa] = 2.f;
         continue;
       }
-      const Rec rec = a.rec[j];
+      const Rec rec = rbuf[buf * kFwdTJ + jj];
       double L;
       float Ar, Ai;
       if (KIND == kFwdTrace) {
@@ -130,7 +162,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
         Ai = rec.T;
       }
       // phase anchors from fp64 cycle counts (cycles = L f / c), reduced to [-0.5, 0.5]
-      const float fr0 = frac_cycles(L * a.k0);
+      const float fr0 = frac_cycles(L * k0);
       const float frd = frac_cycles(L * a.kd);
       const float frw = frac_cycles(L * a.kw);
       float es, ec, zs, zc, ws, wc;
@@ -141,20 +173,20 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
       f2x c = (KIND == kFwdTrace) ? pk(Ar * ec, -Ar * es)
                                   : pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
       const f2x zz = pk(zc, -zs), ww = pk(wc, -ws);
-      for (int b = 0; b < nb; ++b) {
+      for (int b = 0; b < nb_here; ++b) {
         const float2 y0 = upk(c), y1 = upk(cmul2(c, zz));
-        dst[(size_t)b * ta] = make_float4(y0.x, y0.y, y1.x, y1.y);
+        dst[(size_t)b * taw] = make_float4(y0.x, y0.y, y1.x, y1.y);
         c = cmul2(c, ww);
       }
-      kv[jj * ta + aa] = 2.f * zc;
+      kv[jj * taw + aa] = 2.f * zc;
     }
-    __syncthreads();
+    __syncwarp();
     // ---------------- phase 2: bin recurrences
     if (active) {
 #pragma unroll 2
       for (int jj = 0; jj < kFwdTJ; ++jj) {
-        const float4 Y = anc[((size_t)jj * nb + my_b) * ta + my_a];
-        const float k = kv[jj * ta + my_a];
+        const float4 Y = anc[((size_t)jj * nbc + my_b) * taw + my_a];
+        const float k = kv[jj * taw + my_a];
         const f2x kp = pk(k, k), kn = pk(-k, -k);
         f2x q0 = pk(Y.x, Y.y), q1 = pk(Y.z, Y.w);
         acc[0] = fadd2(acc[0], q0);
@@ -168,13 +200,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
         }
       }
     }
-    __syncthreads();
   }
+  cp_async_wait_all();
   if (domain) atomicOr(a.flags, 1u);
   const int64_t ia = a0 + my_a;
   if (active && ia < a.n_a) {
-    float2 *dst = a.out + ((int64_t)blockIdx.y * a.n_a + ia) * a.n_f + (int64_t)my_b * B;
-    const int lim = min(B, a.n_f - my_b * B);
+    const int bin0 = (chunk * nbc + my_b) * B;
+    float2 *dst = a.out + ((int64_t)blockIdx.y * a.n_a + ia) * a.n_f + bin0;
+    const int lim = min(B, a.n_f - bin0);
 #pragma unroll
     for (int m = 0; m < B; ++m) {
       if (m < lim) {
@@ -477,9 +510,11 @@ static cudaError_t fwd_b(const FwdArgs &a, bool mono, bool corr, int kind, dim3 
 
 cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int kind, int n_splits,
                              cudaStream_t st) {
-  const int64_t n_tiles = (a.n_a + a.ta - 1) / a.ta;
-  dim3 grid((unsigned)n_tiles, (unsigned)n_splits);
-  const size_t smem = fwd_smem_bytes(a.nb, a.ta);
+  const int64_t ta = (int64_t)kFwdWarps * a.taw;
+  const int64_t n_tiles = (a.n_a + ta - 1) / ta;
+  const int chunks = (a.nb_total + a.nb - 1) / a.nb;
+  dim3 grid((unsigned)n_tiles, (unsigned)n_splits, (unsigned)chunks);
+  const size_t smem = (size_t)kFwdWarps * a.warp_smem;
   switch (B) {
     case 8: return fwd_b<8>(a, mono, corr, kind, grid, smem, st);
     case 16: return fwd_b<16>(a, mono, corr, kind, grid, smem, st);

@@ -9,6 +9,7 @@ namespace rfr {
 struct Rec;
 
 constexpr int kFwdThreads = 256;   // K2 CTA size
+constexpr int kFwdWarps = kFwdThreads / 32;
 constexpr int kFwdTJ = 8;          // samples per K2 shared-memory tile
 constexpr int kAdjThreads = 128;   // K3/K4 CTA size
 constexpr int kAdjSPT = 2;         // samples (queries) per K3/K4 thread
@@ -31,11 +32,14 @@ struct FwdArgs {
   int64_t n_s;
   const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
   int64_t n_a;
-  int n_f, nb, ta;
-  double k0, kd, kw;               // cycles per metre of path: f0/c, df/c, B df/c
+  int n_f;
+  int nb;                          // bin blocks of B bins per chunk (<= 32)
+  int nb_total;                    // bin blocks over all n_f bins
+  int taw;                         // antennas per warp = 32 / nb
+  size_t warp_smem;                // shared-memory bytes per warp
+  double k0, kd, kw, kchunk;       // cycles per metre of path: f0/c, df/c, B df/c, 32 B df/c
   int64_t samples_per_split;
   float2 *out;                     // [split][n_a][n_f]
-  size_t smem_ant_off;
   unsigned int *flags;
   bool no_gain;
 };
@@ -69,10 +73,11 @@ struct BlendBwdArgs {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-inline size_t fwd_smem_ant_off(int nb, int ta) {
-  return align_up((size_t)kFwdTJ * nb * ta * 16 + (size_t)kFwdTJ * ta * 4, 16);
+// K2 per-warp shared memory: anchors [TJ][32] float4, 2cos(theta) [TJ][32] float, antennas [32]
+// (56 B each), double-buffered records [2][TJ] (48 B each)
+inline size_t fwd_warp_smem() {
+  return align_up((size_t)kFwdTJ * 32 * 20 + 32 * 56 + 2 * kFwdTJ * 48, 128);
 }
-inline size_t fwd_smem_bytes(int nb, int ta) { return fwd_smem_ant_off(nb, ta) + (size_t)ta * 56; }
 inline size_t adj_smem_ant_off(int n_f) { return align_up((size_t)kAdjGA * n_f * 8, 16); }
 inline size_t adj_smem_bytes(int n_f) { return adj_smem_ant_off(n_f) + (size_t)kAdjGA * 56; }
 

@@ -52,11 +52,12 @@ class rfr_opts(C.Structure):
 
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too small",
-          3: "domain", 4: "numeric", 5: "CUDA launch failure", 6: "unsupported"}
+          3: "domain", 4: "numeric", 5: "CUDA launch failure", 6: "unsupported", 7: "NCCL failure"}
 
 EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_filter_partial",
            "rfr_filter_power", "rfr_backward", "rfr_backward_partial", "rfr_backward_finish",
            "rfr_filter_backward", "rfr_heatmap_loss",
+           "rfr_comm_unique_id", "rfr_comm_init", "rfr_comm_destroy",
            "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count")
 
 
@@ -82,15 +83,18 @@ def load(path: str = LIB_PATH):
         "rfr_workspace_size": [i64, i64, i32, i64, C.POINTER(C.c_size_t)],
         "rfr_forward": [S, f, A, G, O, vp, vp, C.c_size_t, vp],
         "rfr_loss": [vp, vp, i64, vp, vp, vp, C.c_size_t, vp],
-        "rfr_filter": [vp, A, G, vp, vp, vp, i64, vp, vp, vp, C.c_size_t, vp],
+        "rfr_filter": [vp, A, G, vp, vp, vp, i64, vp, vp, vp, vp, C.c_size_t, vp],
         "rfr_filter_partial": [vp, A, G, vp, vp, vp, i64, vp, vp, C.c_size_t, vp],
         "rfr_filter_power": [vp, i64, vp, vp],
-        "rfr_backward": [vp, S, f, A, G, O, R, vp, C.c_size_t, vp],
+        "rfr_backward": [vp, S, f, A, G, O, R, vp, vp, C.c_size_t, vp],
         "rfr_backward_partial": [vp, S, f, A, G, O, vp, vp, C.c_size_t, vp],
         "rfr_backward_finish": [vp, S, f, O, R, vp, C.c_size_t, vp],
         "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, vp, C.c_size_t, vp],
         "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, vp, C.c_size_t, vp],
         "rfr_poll_flags": [vp, C.POINTER(u32)],
+        "rfr_comm_unique_id": [vp],
+        "rfr_comm_init": [vp, C.c_int, C.c_int, C.POINTER(vp)],
+        "rfr_comm_destroy": [vp],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -223,11 +227,12 @@ def rfr_loss(signal: torch.Tensor, target: torch.Tensor, grad: torch.Tensor, los
 
 
 def rfr_filter(signal: torch.Tensor, ants: DeviceAntennas, grid, qx, qy, qz, power: torch.Tensor,
-               ws: torch.Tensor, mf: Optional[torch.Tensor] = None, stream=None):
+               ws: torch.Tensor, mf: Optional[torch.Tensor] = None, comm: "Comm" = None,
+               stream=None):
     a, g = ants.struct(), grid_struct(grid)
     _check(load().rfr_filter(_ptr(signal), C.byref(a), C.byref(g), _ptr(qx), _ptr(qy), _ptr(qz),
-                             int(qx.numel()), _ptr(power), _ptr(mf), _ptr(ws), ws.numel(),
-                             _stream(stream)), "rfr_filter")
+                             int(qx.numel()), _ptr(power), _ptr(mf), _comm(comm), _ptr(ws),
+                             ws.numel(), _stream(stream)), "rfr_filter")
     return power
 
 
@@ -297,11 +302,11 @@ class Grads:
 
 def rfr_backward(grad_signal: torch.Tensor, samples: DeviceSamples, sharpness: float,
                  ants: DeviceAntennas, grid, out: Grads, ws: torch.Tensor, flags: int = 0,
-                 stream=None):
+                 comm: "Comm" = None, stream=None):
     s, a, g, o, r = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags), out.struct()
     _check(load().rfr_backward(_ptr(grad_signal), C.byref(s), float(sharpness), C.byref(a),
-                               C.byref(g), C.byref(o), C.byref(r), _ptr(ws), ws.numel(),
-                               _stream(stream)), "rfr_backward")
+                               C.byref(g), C.byref(o), C.byref(r), _comm(comm), _ptr(ws),
+                               ws.numel(), _stream(stream)), "rfr_backward")
     return out
 
 
@@ -335,6 +340,40 @@ def rfr_poll_flags(ws: torch.Tensor) -> int:
 
 
 # ------------------------------------------------------------------------------ multi-GPU host logic
+class Comm:
+    """librfr's NCCL communicator for this rank (rfr_comm_*).  The 128-byte unique id is created by
+    rank 0 and broadcast with the caller's torch.distributed process group (plumbing only)."""
+
+    def __init__(self, handle: int, nranks: int, rank: int):
+        self.handle, self.nranks, self.rank = handle, nranks, rank
+
+    @classmethod
+    def create(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _check(load().rfr_comm_unique_id(uid), "rfr_comm_unique_id")
+        if world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(uid, obj[0], 128)
+        h = C.c_void_p()
+        _check(load().rfr_comm_init(uid, world, rank, C.byref(h)), "rfr_comm_init")
+        return cls(h.value, world, rank)
+
+    def close(self):
+        if self.handle:
+            _check(load().rfr_comm_destroy(self.handle), "rfr_comm_destroy")
+            self.handle = None
+
+
+def _comm(c: Optional[Comm]):
+    return None if c is None else c.handle
+
+
+
 def shard_range(n: int, rank: int, world: int):
     """Contiguous antenna slice [lo, hi) of rank `rank` out of `world` (balanced to +-1)."""
     if world <= 0 or not (0 <= rank < world):

@@ -377,3 +377,29 @@ def test_abi_argument_errors():
         m.rfr_forward(DS, s, DA, grid, sig, ws[:64])
     with pytest.raises(m.RfrError):
         m.rfr_forward(DS, s, DA, grid, sig.cpu(), ws)     # no CPU fallback
+
+
+def test_comm_path_one_rank_is_identity():
+    """librfr's NCCL communicator (rfr_comm_*) on one rank: rfr_backward / rfr_filter with the comm
+    issue the all-reduce and return bitwise the same results as without it."""
+    m = rfr()
+    p = problem("c1")
+    b = p.bundles[0]
+    DS, DA = m.DeviceSamples.from_host(b.samples, dev()), m.DeviceAntennas.from_host(b.antennas, dev())
+    n = b.samples.n
+    ws = m.workspace(n, b.antennas.n, p.grid.n_freq, n, dev())
+    G = f32c(p.random_grad())
+    comm = m.Comm.create()
+    try:
+        o1, o2 = m.Grads.empty(n, dev()), m.Grads.empty(n, dev())
+        m.rfr_backward(G, DS, p.sharpness, DA, p.grid, o1, ws)
+        m.rfr_backward(G, DS, p.sharpness, DA, p.grid, o2, ws, comm=comm)
+        P1, P2 = torch.empty(n, device=dev()), torch.empty(n, device=dev())
+        m.rfr_filter(G, DA, p.grid, DS.x, DS.y, DS.z, P1, ws)
+        m.rfr_filter(G, DA, p.grid, DS.x, DS.y, DS.z, P2, ws, comm=comm)
+        torch.cuda.synchronize()
+        for k in m.Grads.NAMES:
+            assert torch.equal(getattr(o1, k), getattr(o2, k)), k
+        assert torch.equal(P1, P2)
+    finally:
+        comm.close()
