@@ -64,7 +64,7 @@ bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
   const int64_t n_tiles = (n_a > 0 ? cdiv(n_a, (int64_t)kFwdWarps * p.taw) : 1) * p.chunks;
   // split-K over the summed points (samples for K2, queries for K5)
   auto fwd = [&](int64_t n_pts, int &sp, int64_t &sps) {
-    const int64_t target = (int64_t)p.n_sm * 2 * 32;       // ~32 waves at 2 CTAs / SM
+    const int64_t target = (int64_t)p.n_sm * kFwdMinBlocks * 32;   // ~32 waves
     int64_t splits = cdiv(target, n_tiles);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, cdiv(n_pts, kFwdTJ * 16)));
     const size_t per_split = (size_t)std::max<int64_t>(n_a, 1) * nf * 8;

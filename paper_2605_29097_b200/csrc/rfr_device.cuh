@@ -19,6 +19,12 @@ __device__ __forceinline__ f2x pk(float x, float y) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
   return r;
 }
+// same, but opaque to the optimiser (a loop-invariant pair stays one register pair)
+__device__ __forceinline__ f2x pkv(float x, float y) {
+  f2x r;
+  asm volatile("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
 __device__ __forceinline__ float2 upk(f2x r) {
   float2 v;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
@@ -112,14 +118,28 @@ struct PairBwd {
   bool ok;            // false: closer than u_min (contributes 0)
 };
 
+// Distance in fp64 from its square: r0 = rsqrt in fp32 (MUFU, rel. error ~1e-7), then one Newton
+// step in fp64, y + (d2 - y^2) r0 / 2 with y = d2 r0, which leaves a relative error ~1e-14 (enough
+// for the phase: 1e-10 of a 0.5 m path is 5e-11 m) without the IEEE fp64 sqrt sequence and its slow
+// path.  *inv = r0 ~ 1/d in fp32 for the directions and the path loss.
+__device__ __forceinline__ double dist_from_sq(double d2, float *inv) {
+  d2 = fmax(d2, 1e-24);            // coincident points stay finite (and fail the u_min guard)
+  const float r0 = rsqrtf((float)d2);
+  const double y = d2 * (double)r0;
+  const double e = fma(-y, y, d2);
+  *inv = r0;
+  return fma(e, (double)(0.5f * r0), y);
+}
+
 // Path length d_t + d_r in fp64 only (matched-filter adjoint: no amplitude factors, Eq. 3)
 template <bool MONO>
 __device__ __forceinline__ double pair_length(const Rec &r, const AntD &a) {
   double dx = r.x - a.x, dy = r.y - a.y, dz = r.z - a.z;
-  double dt = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+  float it;
+  double dt = dist_from_sq(fma(dx, dx, fma(dy, dy, dz * dz)), &it);
   if (MONO) return 2.0 * dt;
   double ex = a.rx - r.x, ey = a.ry - r.y, ez = a.rz - r.z;
-  return dt + sqrt(fma(ex, ex, fma(ey, ey, ez * ez)));
+  return dt + dist_from_sq(fma(ex, ex, fma(ey, ey, ez * ez)), &it);
 }
 
 // Shared geometry: distances in fp64 (phase precision), directions / gain / decay in fp32.
@@ -127,16 +147,15 @@ template <bool MONO, bool CORR>
 __device__ __forceinline__ void pair_geometry(const Rec &r, const AntD &a, bool no_gain,
                                               PairBwd &o) {
   double dx = r.x - a.x, dy = r.y - a.y, dz = r.z - a.z;
-  double dt = sqrt(fma(dx, dx, fma(dy, dy, dz * dz)));
+  float it;
+  double dt = dist_from_sq(fma(dx, dx, fma(dy, dy, dz * dz)), &it);
   double dr = dt;
   float wix, wiy, wiz, wrx, wry, wrz;
-  float ft = (float)dt, it = 1.f / ft;
   wix = (float)dx * it; wiy = (float)dy * it; wiz = (float)dz * it;
-  float fr = ft, ir = it;
+  float ir = it;
   if (!MONO) {
     double ex = a.rx - r.x, ey = a.ry - r.y, ez = a.rz - r.z;
-    dr = sqrt(fma(ex, ex, fma(ey, ey, ez * ez)));
-    fr = (float)dr; ir = 1.f / fr;
+    dr = dist_from_sq(fma(ex, ex, fma(ey, ey, ez * ez)), &ir);
     wrx = (float)ex * ir; wry = (float)ey * ir; wrz = (float)ez * ir;
   } else {
     wrx = -wix; wry = -wiy; wrz = -wiz;

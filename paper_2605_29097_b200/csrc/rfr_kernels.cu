@@ -81,13 +81,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int B, bool MONO, bool CORR, int KIND>
-__global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbc = a.nb, taw = a.taw;
   unsigned char *wb = smem_raw + (size_t)warp * a.warp_smem;
-  float4 *anc = reinterpret_cast<float4 *>(wb);                          // [TJ][nbc][taw]
-  float *kv = reinterpret_cast<float *>(wb + kFwdTJ * 32 * 16);          // [TJ][taw]
+  // fixed strides (32 slots per sample) so that phase-2 addresses are compile-time offsets
+  float4 *anc = reinterpret_cast<float4 *>(wb);                          // [TJ][32]: slot b*taw+aa
+  float *kv = reinterpret_cast<float *>(wb + kFwdTJ * 32 * 16);          // [TJ][32]: slot aa
   AntD *ant = reinterpret_cast<AntD *>(wb + kFwdTJ * 32 * 20);           // [taw]
   Rec *rbuf = reinterpret_cast<Rec *>(wb + kFwdTJ * 32 * 20 + 32 * sizeof(AntD));  // [2][TJ]
   const int64_t a0 = ((int64_t)blockIdx.x * kFwdWarps + warp) * taw;
@@ -119,10 +120,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
   for (int m = 0; m < B; ++m) acc[m] = 0ull;
   bool domain = false;
 
-  // records of one tile: TJ x 48 B = 24 chunks of 16 B, one per lane (lanes 24..31 idle)
+  // records of one tile: TJ x 48 B = 3 TJ chunks of 16 B spread over the lanes
   auto prefetch = [&](int64_t jt, int buf) {
-    if (lane < kFwdTJ * 3) {
-      const int jj = lane / 3, part = lane % 3;
+    for (int c = lane; c < kFwdTJ * 3; c += 32) {
+      const int jj = c / 3, part = c % 3;
       const int64_t j = jt + jj;
       if (j < j_hi)
         cp_async16(reinterpret_cast<float4 *>(rbuf + buf * kFwdTJ + jj) + part,
@@ -140,10 +141,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
     for (int pr = lane; pr < taw * kFwdTJ; pr += 32) {
       const int aa = pr % taw, jj = pr / taw;
       const int64_t j = jt + jj;
-      float4 *dst = anc + (size_t)jj * nbc * taw + aa;
+      float4 *dst = anc + jj * 32 + aa;
       if (j >= j_hi || a0 + aa >= a.n_a) {
-        for (int b = 0; b < nb_here; ++b) dst[(size_t)b * taw] = make_float4(0.f, 0.f, 0.f, 0.f);
-        kv[jj * taw + aa] = 2.f;
+        for (int b = 0; b < nb_here; ++b) dst[b * taw] = make_float4(0.f, 0.f, 0.f, 0.f);
+        kv[jj * 32 + aa] = 2.f;
         continue;
       }
       const Rec rec = rbuf[buf * kFwdTJ + jj];
@@ -175,18 +176,20 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
       const f2x zz = pk(zc, -zs), ww = pk(wc, -ws);
       for (int b = 0; b < nb_here; ++b) {
         const float2 y0 = upk(c), y1 = upk(cmul2(c, zz));
-        dst[(size_t)b * taw] = make_float4(y0.x, y0.y, y1.x, y1.y);
+        dst[b * taw] = make_float4(y0.x, y0.y, y1.x, y1.y);
         c = cmul2(c, ww);
       }
-      kv[jj * taw + aa] = 2.f * zc;
+      kv[jj * 32 + aa] = 2.f * zc;
     }
     __syncwarp();
     // ---------------- phase 2: bin recurrences
     if (active) {
-#pragma unroll 2
+      const float4 *ap = anc + my_b * taw + my_a;
+      const float *kp_ = kv + my_a;
+#pragma unroll 1
       for (int jj = 0; jj < kFwdTJ; ++jj) {
-        const float4 Y = anc[((size_t)jj * nbc + my_b) * taw + my_a];
-        const float k = kv[jj * taw + my_a];
+        const float4 Y = ap[jj * 32];
+        const float k = kp_[jj * 32];
         const f2x kp = pk(k, k), kn = pk(-k, -k);
         f2x q0 = pk(Y.x, Y.y), q1 = pk(Y.z, Y.w);
         acc[0] = fadd2(acc[0], q0);
@@ -225,13 +228,13 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_trace_fwd(FwdArgs a) {
 // bins with X(i, .) broadcast from shared memory (2 FFMA2 per complex step).
 //   MODE_BWD: R = Re(E h) -> per-sample sums S1, S2, S3 (Eq. 5 chain), written as partials.
 //   MODE_FLT: M += E h (complex) -> partial matched-filter output.
-template <int MODE, int SPT, bool MONO, bool CORR>
+template <int MODE, int SPT, bool MONO, bool CORR, int NF>
 __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
   AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
   const int tid = threadIdx.x;
-  const int nf = a.n_f;
+  const int nf = NF > 0 ? NF : a.n_f;
   const int64_t base = (int64_t)blockIdx.x * (kAdjThreads * SPT);
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
@@ -293,21 +296,37 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
         __sincosf(kTwoPi * fr0, &es, &ec);
         sincospif(2.f * frd, &zs, &zc);
         Er[s] = ec; Ei[s] = es;                    // E = e^{+j theta0}
-        w1[s] = pk(zc, zs);                        // w = e^{+j theta_d}
-        w2[s] = pk(-zs, zc);
+        w1[s] = pkv(zc, zs);                       // w = e^{+j theta_d}
+        w2[s] = pkv(-zs, zc);                      // (opaque: keeps ptxas from re-deriving it in the loop)
         h[s] = 0ull;
       }
       const float2 *Xa = X + aa * nf;
-      // Horner from the top bin down: h = h w + X_m  (2 FFMA2 per complex step)
-#pragma unroll 8
-      for (int m = nf - 1; m >= 0; --m) {
-        const float2 xv = Xa[m];
-        const f2x xm = pk(xv.x, xv.y);
+      // Horner from the top bin down: h = h w + X_m  (2 FFMA2 per complex step).  With NF > 0
+      // the bin loop is straight-line code (no loop-carried register renames: in a rolled loop
+      // ptxas spent ~25% extra FMA-pipe slots on IMAD.MOV / re-derived w2 at every back edge).
+      if (NF > 0) {
 #pragma unroll
-        for (int s = 0; s < SPT; ++s) {
-          const float2 hv = upk(h[s]);
-          const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
-          h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
+        for (int m = NF - 1; m >= 0; --m) {
+          const float2 xv = Xa[m];
+          const f2x xm = pk(xv.x, xv.y);
+#pragma unroll
+          for (int s = 0; s < SPT; ++s) {
+            const float2 hv = upk(h[s]);
+            const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
+            h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
+          }
+        }
+      } else {
+#pragma unroll 8
+        for (int m = nf - 1; m >= 0; --m) {
+          const float2 xv = Xa[m];
+          const f2x xm = pk(xv.x, xv.y);
+#pragma unroll
+          for (int s = 0; s < SPT; ++s) {
+            const float2 hv = upk(h[s]);
+            const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
+            h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
+          }
         }
       }
 #pragma unroll
@@ -603,7 +622,12 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
 
 template <int MODE, bool MONO, bool CORR>
 static cudaError_t adj_t(const AdjArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
-  auto k = k_adjoint<MODE, kAdjSPT, MONO, CORR>;
+  // bin counts with a straight-line Horner specialisation (the configs' 64 / 128 / 256 / 512)
+  auto k = a.n_f == 256 ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 256>
+         : a.n_f == 512 ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 512>
+         : a.n_f == 128 ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 128>
+         : a.n_f == 64  ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 64>
+                        : k_adjoint<MODE, kAdjSPT, MONO, CORR, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, kAdjThreads, smem, st>>>(a);

@@ -8,9 +8,10 @@ namespace rfr {
 
 struct Rec;
 
-constexpr int kFwdThreads = 256;   // K2 CTA size
+constexpr int kFwdThreads = 128;   // K2 CTA size (4 warps)
+constexpr int kFwdMinBlocks = 3;   // K2 CTAs per SM (register budget ~170)
 constexpr int kFwdWarps = kFwdThreads / 32;
-constexpr int kFwdTJ = 8;          // samples per K2 shared-memory tile
+constexpr int kFwdTJ = 16;         // samples per K2 warp tile
 constexpr int kAdjThreads = 128;   // K3/K4 CTA size
 constexpr int kAdjSPT = 2;         // samples (queries) per K3/K4 thread
 constexpr int kAdjGA = 8;          // antennas per K3/K4 shared-memory stage
