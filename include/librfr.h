@@ -13,7 +13,7 @@
  * Conventions (all calls):
  *  - Every array pointer is a DEVICE pointer owned by the caller.  The library never allocates,
  *    frees or retains caller memory and never allocates on the hot path; its scratch space is the
- *    caller-provided workspace `ws` (size from rfr_workspace_size, alignment >= 256 bytes).
+ *    caller-provided rfr_workspace `ws` (size from rfr_workspace_size, alignment >= 256 bytes).
  *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream), returns
  *    an rfr_status, and never throws across the ABI.  Argument errors are reported before any
  *    launch; RFR_E_CUDA reports a launch failure (cudaGetLastError).
@@ -104,8 +104,23 @@ typedef struct {
   uint32_t flags; /* RFR_NO_GAIN | RFR_CHECK_FINITE | RFR_REUSE_BLEND */
 } rfr_opts;
 
-/* Workspace bytes needed for calls on sample sets of n_samples, n_ant antennas, n_freq bins and
- * n_query filter queries, on the current device (split counts depend on its SM count).
+/* Caller-owned scratch memory of the library.  `ptr` is DEVICE memory of `bytes` >=
+ * rfr_workspace_size(n_samples, n_ant, n_freq, n_query), 256-byte aligned.  The four planning
+ * dimensions are upper bounds for every call that uses the workspace (a call with more samples or
+ * queries than planned returns RFR_E_SHAPE); the internal layout is a function of them only, so
+ * the K1 records cached by rfr_forward (RFR_REUSE_BLEND) survive any filter / loss / adjoint call
+ * on the same workspace.  One workspace must not be used by two calls running concurrently. */
+typedef struct {
+  void *ptr;
+  size_t bytes;
+  int64_t n_samples;
+  int64_t n_ant;
+  int32_t n_freq;
+  int64_t n_query;
+} rfr_workspace;
+
+/* Workspace bytes needed for calls on sample sets of up to n_samples, n_ant antennas, n_freq bins
+ * and n_query filter queries, on the current device (split counts depend on its SM count).
  * Pass 0 for a size that will not be used.  Host-only; no device work. */
 rfr_status rfr_workspace_size(int64_t n_samples, int64_t n_ant, int32_t n_freq, int64_t n_query,
                               size_t *bytes);
@@ -115,12 +130,12 @@ rfr_status rfr_workspace_size(int64_t n_samples, int64_t n_ant, int32_t n_freq, 
  * tau_ij = (d_t + d_r)/c.  Runs K1 (unless RFR_REUSE_BLEND), then K2 and its split reduction. */
 rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_antennas *ants,
                        const rfr_freq_grid *grid, const rfr_opts *opts, float *signal,
-                       void *ws, size_t ws_bytes, rfr_stream_t stream);
+                       const rfr_workspace *ws, rfr_stream_t stream);
 
 /* Signal-domain L2 loss (K6): grad_signal = signal - target, *loss = 1/2 sum |signal - target|^2
  * (device float).  n_complex = n_ant * n_freq.  grad_signal may alias signal. */
 rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex, float *grad_signal,
-                    float *loss, void *ws, size_t ws_bytes, rfr_stream_t stream);
+                    float *loss, const rfr_workspace *ws, rfr_stream_t stream);
 
 /* Eq. 3 matched filter at n_query points: M_q = sum_i sum_m s(i,m) exp(+j 2 pi f_m tau_iq),
  * power[q] = |M_q| (float32), mf (optional, complex64 [n_query]) = M_q.  Sign as printed (Q2).
@@ -128,13 +143,13 @@ rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex,
  * ranks (ncclAllReduce on `stream`) before |M|, so every rank returns the full P and M. */
 rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_freq_grid *grid,
                       const float *qx, const float *qy, const float *qz, int64_t n_query,
-                      float *power, float *mf, const rfr_comm *comm, void *ws, size_t ws_bytes,
+                      float *power, float *mf, const rfr_comm *comm, const rfr_workspace *ws,
                       rfr_stream_t stream);
 /* Antenna-shard partial of the filter: mf (required) = this shard's complex M_q. */
 rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
                               const rfr_freq_grid *grid, const float *qx, const float *qy,
-                              const float *qz, int64_t n_query, float *mf, void *ws,
-                              size_t ws_bytes, rfr_stream_t stream);
+                              const float *qz, int64_t n_query, float *mf,
+                              const rfr_workspace *ws, rfr_stream_t stream);
 /* power[q] = |mf[q]| after the caller's all-reduce of mf. */
 rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_stream_t stream);
 
@@ -150,7 +165,7 @@ rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_
 rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const float *power,
                                float eps, const rfr_antennas *ants, const rfr_freq_grid *grid,
                                const float *qx, const float *qy, const float *qz, int64_t n_query,
-                               float *grad_signal, void *ws, size_t ws_bytes, rfr_stream_t stream);
+                               float *grad_signal, const rfr_workspace *ws, rfr_stream_t stream);
 
 /* K7, heatmap-domain L2 with dynamic loss masking (masking P:L392-402, SPEC
  * S:L425-430).  keep_q = !(history[cell[q]] > thr_hi && power[q] < ratio * history[cell[q]])
@@ -161,8 +176,8 @@ rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const f
  * each query into the caller's history grid, float [n_cells] >= 0). */
 rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n_query,
                             const int32_t *cell, float *history, float thr_hi, float ratio,
-                            float *grad_power, uint8_t *mask, float *loss, void *ws,
-                            size_t ws_bytes, rfr_stream_t stream);
+                            float *grad_power, uint8_t *mask, float *loss,
+                            const rfr_workspace *ws, rfr_stream_t stream);
 
 /* Backward: grad_signal = G = dL/dRe s + j dL/dIm s, complex64 [n_ant][n_freq] (Q14).
  * Writes dL/d{sdf, refl, n, power} per sample and dL/dsharpness.  = partial + finish.
@@ -171,8 +186,8 @@ rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n
  * full gradients. */
 rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,
                         const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_opts *opts,
-                        const rfr_sample_grads *out, const rfr_comm *comm, void *ws,
-                        size_t ws_bytes, rfr_stream_t stream);
+                        const rfr_sample_grads *out, const rfr_comm *comm,
+                        const rfr_workspace *ws, rfr_stream_t stream);
 /* K3: per-sample antenna sums of this antenna shard, partials float32 SoA [5][n_samples]:
  *   row 0  S1 = sum_i R_ij g gamma T_t T_r                 (= dL/dw_j, w = p a alpha)
  *   row 1  S2 = sum_i R_ij g gamma (T_r chi_t + T_t chi_r)  (dL/dT_j = w_j S2)
@@ -181,11 +196,11 @@ rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, fl
 rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *samples,
                                 float sharpness, const rfr_antennas *ants,
                                 const rfr_freq_grid *grid, const rfr_opts *opts, float *partials,
-                                void *ws, size_t ws_bytes, rfr_stream_t stream);
+                                const rfr_workspace *ws, rfr_stream_t stream);
 /* K1': chain the (all-reduced) partials through Eq. 5 and the blend of every ray. */
 rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
-                               const rfr_opts *opts, const rfr_sample_grads *out, void *ws,
-                               size_t ws_bytes, rfr_stream_t stream);
+                               const rfr_opts *opts, const rfr_sample_grads *out,
+                               const rfr_workspace *ws, rfr_stream_t stream);
 
 /* Multi-GPU communicator.  Rank 0 calls rfr_comm_unique_id (128 opaque bytes) and the caller
  * distributes the bytes to every rank; each rank then calls rfr_comm_init on its own device (it
@@ -196,7 +211,7 @@ rfr_status rfr_comm_init(const void *id, int nranks, int rank, rfr_comm **out);
 rfr_status rfr_comm_destroy(rfr_comm *comm);
 
 /* Synchronously read (and clear) the device flags RFR_FLAG_DOMAIN / RFR_FLAG_NUMERIC. */
-rfr_status rfr_poll_flags(void *ws, uint32_t *flags);
+rfr_status rfr_poll_flags(const rfr_workspace *ws, uint32_t *flags);
 const char *rfr_status_string(rfr_status s);
 int rfr_abi_version(void);
 /* Diagnostic: number of kernels this library has launched in the process so far. */

@@ -1,9 +1,11 @@
-// librfr.cu -- C ABI (include/librfr.h): argument validation, workspace planning, kernel launches.
+// librfr.cu -- C ABI (include/librfr.h): argument validation, workspace planning, kernel launches,
+// and the library-owned NCCL communicator of the multi-GPU path.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <nccl.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <new>
 
@@ -16,9 +18,9 @@ using namespace rfr;
 namespace {
 
 constexpr double kC = 299792458.0;
-constexpr size_t kHdr = 256;                 // workspace header: flags word at offset 0
-constexpr int kTmpN = 512;                   // reduction scratch (floats)
-constexpr size_t kSplitCap = size_t(2) << 30;  // cap on split-partial buffers (bytes)
+constexpr size_t kHdr = 256;                   // workspace header: flags word at offset 0
+constexpr int kTmpN = 512;                     // reduction scratch (floats)
+constexpr size_t kSplitCap = size_t(2) << 30;  // cap on each split-partial region (bytes)
 
 int device_sms() {
   static std::mutex mu;
@@ -37,78 +39,112 @@ int device_sms() {
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-struct Plan {
-  int n_sm = 148;
-  // forward (K2)
-  int B = 32, nb = 1, nb_total = 1, taw = 32, chunks = 1, fwd_splits = 1, mfa_splits = 1;
-  int64_t fwd_sps = 0, mfa_sps = 0;
-  // adjoint (K3) and filter (K4)
-  int bwd_splits = 1, flt_splits = 1;
-  int64_t bwd_aps = 0, flt_aps = 0;
-  // workspace layout
-  size_t off_rec = 0, off_fwdp = 0, off_bwdp = 0, off_bwds = 0, off_fltp = 0, off_fltm = 0,
-         off_ds = 0, off_tmp = 0, off_qrec = 0, total = 0;
+// ---------------------------------------------------------------------------- K2 / K5 tiling
+// B bins per lane, nb blocks per warp (one bin chunk), taw = 32 / nb antennas per warp.
+struct FwdGeom {
+  int B = 32, nb = 1, nb_total = 1, taw = 32, chunks = 1;
+};
+bool fwd_geom(int32_t n_f, FwdGeom &g) {
+  const int nf = n_f > 0 ? n_f : 1;
+  g.B = nf >= 32 ? 32 : (nf >= 16 ? 16 : 8);
+  g.nb_total = (int)cdiv(nf, g.B);
+  if (g.nb_total > 256) return false;                      // n_freq > 8192: unsupported
+  g.nb = std::min(g.nb_total, 32);
+  g.chunks = (int)cdiv(g.nb_total, g.nb);
+  g.taw = 32 / g.nb;
+  return true;
+}
+
+struct Split {
+  int splits = 1;
+  int64_t per_split = 0;   // points (K2/K5) or antennas (K3/K4) per split
 };
 
-bool make_plan(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Plan &p) {
+// split-K over the summed points of K2 / K5: ~32 waves of kFwdMinBlocks CTAs per SM, bounded by
+// the points and by the partial-buffer capacity `cap` (bytes); splits == 1 writes the output
+// directly (no partial buffer).
+Split fwd_split(int64_t n_pts, int64_t n_a, int32_t n_f, const FwdGeom &g, size_t cap) {
+  const int64_t n_tiles =
+      (n_a > 0 ? cdiv(n_a, (int64_t)kFwdWarps * g.taw) : 1) * g.chunks;
+  int64_t s = cdiv((int64_t)device_sms() * kFwdMinBlocks * 32, n_tiles);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_pts, kFwdTJ * 16)));
+  const size_t per = (size_t)std::max<int64_t>(n_a, 1) * std::max(n_f, 1) * 8;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t)(std::min(cap, kSplitCap) / per)));
+  s = std::max<int64_t>(s, 1);
+  Split r;
+  r.per_split = cdiv(cdiv(std::max<int64_t>(n_pts, 1), s), kFwdTJ) * kFwdTJ;
+  r.splits = (int)std::max<int64_t>(1, cdiv(n_pts, r.per_split));
+  if (r.splits == 1) r.per_split = std::max<int64_t>(n_pts, 1);
+  return r;
+}
+
+// split over antennas of K3 / K4 (one thread per point): ~16 waves of 4 CTAs per SM
+Split adj_split(int64_t n_pts, int64_t n_a, int floats_per_pt, size_t cap) {
+  const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
+  const int64_t tiles = std::max<int64_t>(1, cdiv(n_pts, per_cta));
+  int64_t s = cdiv((int64_t)device_sms() * 4 * 16, tiles);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, kAdjGA)));
+  const size_t per = (size_t)std::max<int64_t>(n_pts, 1) * floats_per_pt * 4;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t)(std::min(cap, kSplitCap) / per)));
+  s = std::max<int64_t>(s, 1);
+  Split r;
+  r.per_split = cdiv(cdiv(std::max<int64_t>(n_a, 1), s), kAdjGA) * kAdjGA;
+  r.splits = (int)std::max<int64_t>(1, cdiv(n_a, r.per_split));
+  return r;
+}
+
+// ---------------------------------------------------------------------------- workspace layout
+// The layout depends ONLY on the workspace's planning dimensions, so every call that shares a
+// workspace sees the same regions: K1's records (the RFR_REUSE_BLEND cache) are never touched by
+// the filter, K5 or the loss.
+//   header | records [n_s] 48 B | ray ds [n_s] | tmp | backward sums [5][n_s] | filter M [n_q] |
+//   K5 query records [n_q] 48 B | K2/K5 split partials | K3 split partials | K4 split partials
+struct Layout {
+  size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
+         off_fwdp = 0, off_bwdp = 0, off_fltp = 0, total = 0;
+  size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
+};
+
+bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) {
   if (n_s < 0 || n_a < 0 || n_q < 0 || n_f < 0) return false;
-  p.n_sm = device_sms();
-  const int nf = n_f > 0 ? n_f : 1;
-  // ---- K2: B bins per thread, nb blocks per antenna, ta antennas per CTA
-  p.B = nf >= 32 ? 32 : (nf >= 16 ? 16 : 8);
-  p.nb_total = (int)cdiv(nf, p.B);
-  if (p.nb_total > 256) return false;                      // n_freq > 8192
-  p.nb = std::min(p.nb_total, 32);                         // bin blocks per warp (one chunk)
-  p.chunks = (int)cdiv(p.nb_total, p.nb);
-  p.taw = 32 / p.nb;                                       // antennas per warp
-  const int64_t n_tiles = (n_a > 0 ? cdiv(n_a, (int64_t)kFwdWarps * p.taw) : 1) * p.chunks;
-  // split-K over the summed points (samples for K2, queries for K5)
-  auto fwd = [&](int64_t n_pts, int &sp, int64_t &sps) {
-    const int64_t target = (int64_t)p.n_sm * kFwdMinBlocks * 32;   // ~32 waves
-    int64_t splits = cdiv(target, n_tiles);
-    splits = std::min<int64_t>(splits, std::max<int64_t>(1, cdiv(n_pts, kFwdTJ * 16)));
-    const size_t per_split = (size_t)std::max<int64_t>(n_a, 1) * nf * 8;
-    splits = std::min<int64_t>(splits, std::max<int64_t>(1, (int64_t)(kSplitCap / per_split)));
-    splits = std::max<int64_t>(splits, 1);
-    sps = cdiv(cdiv(std::max<int64_t>(n_pts, 1), splits), kFwdTJ) * kFwdTJ;
-    sp = (int)std::max<int64_t>(1, cdiv(n_pts, sps));
-  };
-  fwd(n_s, p.fwd_splits, p.fwd_sps);
-  fwd(n_q, p.mfa_splits, p.mfa_sps);
-  // ---- K3 / K4: splits over antennas
-  auto adj = [&](int64_t n_pts, int floats_per_pt, int &sp, int64_t &aps) {
-    const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
-    const int64_t tiles = std::max<int64_t>(1, cdiv(n_pts, per_cta));
-    int64_t s = cdiv((int64_t)p.n_sm * 4 * 16, tiles);
-    s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, kAdjGA)));
-    const size_t per = (size_t)std::max<int64_t>(n_pts, 1) * floats_per_pt * 4;
-    s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t)(kSplitCap / per)));
-    s = std::max<int64_t>(s, 1);
-    aps = cdiv(cdiv(std::max<int64_t>(n_a, 1), s), kAdjGA) * kAdjGA;
-    sp = (int)std::max<int64_t>(1, cdiv(n_a, aps));
-  };
-  adj(n_s, 5, p.bwd_splits, p.bwd_aps);
-  adj(n_q, 2, p.flt_splits, p.flt_aps);
-  // ---- layout
+  FwdGeom g;
+  if (!fwd_geom(n_f, g)) return false;
+  const int32_t nf = std::max(n_f, 1);
+  const Split f2 = fwd_split(n_s, n_a, nf, g, kSplitCap);
+  const Split f5 = fwd_split(n_q, n_a, nf, g, kSplitCap);
+  const Split b3 = adj_split(n_s, n_a, 5, kSplitCap);
+  const Split b4 = adj_split(n_q, n_a, 2, kSplitCap);
+  const int fsp = std::max(f2.splits, f5.splits);
+  L.cap_fwdp = fsp > 1 ? (size_t)fsp * n_a * nf * 8 : 0;
+  L.cap_bwdp = b3.splits > 1 ? (size_t)b3.splits * 5 * n_s * 4 : 0;
+  L.cap_fltp = b4.splits > 1 ? (size_t)b4.splits * n_q * 8 : 0;
   size_t o = kHdr;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
-  // prefix that depends on n_s only (rfr_backward_finish relies on it), then the split buffers
-  p.off_rec = take((size_t)n_s * sizeof(Rec));
-  p.off_ds = take((size_t)n_s * 4);
-  p.off_tmp = take((size_t)kTmpN * 4);
-  p.off_bwds = take((size_t)5 * n_s * 4);
-  p.off_fltm = take((size_t)n_q * 8);
-  p.off_qrec = take((size_t)n_q * sizeof(Rec));
-  const int fsp = std::max(p.fwd_splits, p.mfa_splits);
-  p.off_fwdp = take(fsp > 1 ? (size_t)fsp * n_a * n_f * 8 : 0);
-  p.off_bwdp = take(p.bwd_splits > 1 ? (size_t)p.bwd_splits * 5 * n_s * 4 : 0);
-  p.off_fltp = take(p.flt_splits > 1 ? (size_t)p.flt_splits * n_q * 8 : 0);
-  p.total = o;
+  L.off_rec = take((size_t)n_s * sizeof(Rec));
+  L.off_ds = take((size_t)n_s * 4);
+  L.off_tmp = take((size_t)kTmpN * 4);
+  L.off_bwds = take((size_t)5 * n_s * 4);
+  L.off_fltm = take((size_t)n_q * 8);
+  L.off_qrec = take((size_t)n_q * sizeof(Rec));
+  L.off_fwdp = take(L.cap_fwdp);
+  L.off_bwdp = take(L.cap_bwdp);
+  L.off_fltp = take(L.cap_fltp);
+  L.total = o;
   return true;
 }
 
 template <typename T>
-T *at(void *ws, size_t off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
+T *at(const rfr_workspace *ws, size_t off) {
+  return reinterpret_cast<T *>(static_cast<char *>(ws->ptr) + off);
+}
+
+// A call's workspace: planned for at least n_s samples and n_q queries.
+rfr_status check_ws(const rfr_workspace *ws, int64_t n_s, int64_t n_q, Layout &L) {
+  if (!ws || !ws->ptr) return RFR_E_ARG;
+  if (!make_layout(ws->n_samples, ws->n_ant, ws->n_freq, ws->n_query, L)) return RFR_E_SHAPE;
+  if (ws->bytes < L.total || n_s > ws->n_samples || n_q > ws->n_query) return RFR_E_SHAPE;
+  return RFR_OK;
+}
 
 rfr_status check_samples(const rfr_samples *s) {
   if (!s || s->n_rays < 0) return RFR_E_ARG;
@@ -132,6 +168,7 @@ rfr_status check_grid(const rfr_freq_grid *g) {
   if (!g || g->n_freq <= 0 || !(g->df_hz > 0.0) || !(g->f0_hz >= 0.0) || !isfinite(g->f0_hz) ||
       !isfinite(g->df_hz))
     return RFR_E_ARG;
+  if (g->n_freq > 8192) return RFR_E_SHAPE;
   return RFR_OK;
 }
 
@@ -140,14 +177,14 @@ rfr_status cuda_status(cudaError_t e) { return e == cudaSuccess ? RFR_OK : RFR_E
 #define RFR_TRY(x) do { rfr_status _s = (x); if (_s != RFR_OK) return _s; } while (0)
 #define RFR_CU(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return RFR_E_CUDA; } while (0)
 
-rfr_status run_blend(const rfr_samples *s, float sharpness, uint32_t flags, void *ws,
-                     const Plan &p, cudaStream_t st) {
+rfr_status run_blend(const rfr_samples *s, float sharpness, uint32_t flags,
+                     const rfr_workspace *ws, const Layout &L, cudaStream_t st) {
   if (flags & RFR_REUSE_BLEND) return RFR_OK;
   BlendArgs b;
   b.x = s->x; b.y = s->y; b.z = s->z; b.sdf = s->sdf; b.refl = s->refl;
   b.nx = s->nx; b.ny = s->ny; b.nz = s->nz; b.power = s->power; b.phi_origin = s->phi_origin;
   b.n_rays = s->n_rays; b.n_per_ray = s->n_per_ray; b.s = sharpness;
-  b.rec = at<Rec>(ws, p.off_rec);
+  b.rec = at<Rec>(ws, L.off_rec);
   b.flags = at<unsigned>(ws, 0);
   b.check_finite = (flags & RFR_CHECK_FINITE) != 0;
   return cuda_status(launch_blend(b, st));
@@ -155,6 +192,39 @@ rfr_status run_blend(const rfr_samples *s, float sharpness, uint32_t flags, void
 
 bool has_corr(const rfr_samples *s, const rfr_antennas *a) {
   return s->phi_origin || a->phi_tx || a->phi_rx;
+}
+
+// K2 (trace) or K5 (matched-filter adjoint) over `rec` [n_pts] into out [n_a][n_f] (+ split sum)
+rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
+                   const rfr_freq_grid *grid, bool no_gain, bool corr, int kind, float *out,
+                   const rfr_workspace *ws, const Layout &L, cudaStream_t st) {
+  FwdGeom g;
+  if (!fwd_geom(grid->n_freq, g)) return RFR_E_SHAPE;
+  const Split sp = fwd_split(n_pts, ants->n_ant, grid->n_freq, g, L.cap_fwdp);
+  FwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rec = rec;
+  a.n_s = n_pts;
+  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
+  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
+  a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
+  a.n_a = ants->n_ant;
+  a.n_f = grid->n_freq; a.nb = g.nb; a.nb_total = g.nb_total; a.taw = g.taw;
+  a.warp_smem = fwd_warp_smem();
+  a.k0 = grid->f0_hz / kC;
+  a.kd = grid->df_hz / kC;
+  a.kw = grid->df_hz * g.B / kC;
+  a.kchunk = grid->df_hz * g.B * g.nb / kC;
+  a.samples_per_split = sp.per_split;
+  a.out = sp.splits > 1 ? at<float2>(ws, L.off_fwdp) : reinterpret_cast<float2 *>(out);
+  a.flags = at<unsigned>(ws, 0);
+  a.no_gain = no_gain;
+  const bool mono = ants->rx_x == nullptr;
+  RFR_CU(launch_trace_fwd(a, g.B, mono, corr, kind, sp.splits, st));
+  if (sp.splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, L.off_fwdp), sp.splits,
+                             ants->n_ant * (int64_t)grid->n_freq * 2, out, device_sms(), st));
+  return RFR_OK;
 }
 
 }  // namespace
@@ -210,7 +280,6 @@ rfr_status rfr_comm_destroy(rfr_comm *c) {
   return r == ncclSuccess ? RFR_OK : RFR_E_NCCL;
 }
 
-
 int rfr_abi_version(void) { return RFR_ABI_VERSION; }
 
 uint64_t rfr_launch_count(void) { return (uint64_t)launch_count(); }
@@ -232,60 +301,37 @@ const char *rfr_status_string(rfr_status s) {
 rfr_status rfr_workspace_size(int64_t n_samples, int64_t n_ant, int32_t n_freq, int64_t n_query,
                               size_t *bytes) {
   if (!bytes) return RFR_E_ARG;
-  Plan p;
-  if (!make_plan(n_samples, n_ant, n_freq, n_query, p)) return RFR_E_SHAPE;
-  *bytes = p.total;
+  Layout L;
+  if (!make_layout(n_samples, n_ant, n_freq, n_query, L)) return RFR_E_SHAPE;
+  *bytes = L.total;
   return RFR_OK;
 }
 
 rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_antennas *ants,
-                       const rfr_freq_grid *grid, const rfr_opts *opts, float *signal, void *ws,
-                       size_t ws_bytes, rfr_stream_t stream) {
+                       const rfr_freq_grid *grid, const rfr_opts *opts, float *signal,
+                       const rfr_workspace *ws, rfr_stream_t stream) {
   RFR_TRY(check_samples(samples));
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
-  if (!(sharpness > 0.f) || !ws || (!signal && ants->n_ant > 0)) return RFR_E_ARG;
+  if (!(sharpness > 0.f) || (!signal && ants->n_ant > 0)) return RFR_E_ARG;
   const uint32_t flags = opts ? opts->flags : 0u;
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
-  Plan p;
-  if (!make_plan(n_s, ants->n_ant, grid->n_freq, 0, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, n_s, 0, L));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (ants->n_ant == 0) return RFR_OK;
-  RFR_TRY(run_blend(samples, sharpness, flags, ws, p, st));
-  FwdArgs a;
-  a.rec = at<Rec>(ws, p.off_rec);
-  a.n_s = n_s;
-  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
-  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
-  a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
-  a.n_a = ants->n_ant;
-  a.n_f = grid->n_freq; a.nb = p.nb; a.nb_total = p.nb_total; a.taw = p.taw;
-  a.warp_smem = fwd_warp_smem();
-  a.k0 = grid->f0_hz / kC;
-  a.kd = grid->df_hz / kC;
-  a.kw = grid->df_hz * p.B / kC;
-  a.kchunk = grid->df_hz * p.B * p.nb / kC;
-  a.samples_per_split = p.fwd_sps;
-  a.out = p.fwd_splits > 1 ? at<float2>(ws, p.off_fwdp) : reinterpret_cast<float2 *>(signal);
-  a.flags = at<unsigned>(ws, 0);
-  a.no_gain = (flags & RFR_NO_GAIN) != 0;
-  const bool mono = ants->rx_x == nullptr;
-  RFR_CU(launch_trace_fwd(a, p.B, mono, has_corr(samples, ants), kFwdTrace, p.fwd_splits, st));
-  if (p.fwd_splits > 1)
-    RFR_CU(launch_sum_splits(at<float>(ws, p.off_fwdp), p.fwd_splits,
-                             ants->n_ant * (int64_t)grid->n_freq * 2, signal, p.n_sm, st));
-  return RFR_OK;
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
+  return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, (flags & RFR_NO_GAIN) != 0,
+                 has_corr(samples, ants), kFwdTrace, signal, ws, L, st);
 }
 
 rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex, float *grad_signal,
-                    float *loss, void *ws, size_t ws_bytes, rfr_stream_t stream) {
-  if (!signal || !target || !grad_signal || !loss || !ws || n_complex < 0) return RFR_E_ARG;
-  Plan p;
-  if (!make_plan(0, 0, 1, 0, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
+                    float *loss, const rfr_workspace *ws, rfr_stream_t stream) {
+  if (!signal || !target || !grad_signal || !loss || n_complex < 0) return RFR_E_ARG;
+  Layout L;
+  RFR_TRY(check_ws(ws, 0, 0, L));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  RFR_CU(launch_loss(signal, target, n_complex, grad_signal, at<float>(ws, p.off_tmp), kTmpN, loss,
+  RFR_CU(launch_loss(signal, target, n_complex, grad_signal, at<float>(ws, L.off_tmp), kTmpN, loss,
                      st));
   return RFR_OK;
 }
@@ -293,17 +339,16 @@ rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex,
 static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
                               const rfr_freq_grid *grid, const float *qx, const float *qy,
                               const float *qz, int64_t n_query, float *power, float *mf,
-                              const rfr_comm *comm, void *ws, size_t ws_bytes, cudaStream_t st) {
+                              const rfr_comm *comm, const rfr_workspace *ws, cudaStream_t st) {
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
-  if (n_query < 0 || !ws || (n_query > 0 && (!qx || !qy || !qz)) ||
-      (ants->n_ant > 0 && !signal))
+  if (n_query < 0 || (n_query > 0 && (!qx || !qy || !qz)) || (ants->n_ant > 0 && !signal))
     return RFR_E_ARG;
-  Plan p;
-  if (!make_plan(0, ants->n_ant, grid->n_freq, n_query, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, 0, n_query, L));
   if (n_query == 0) return RFR_OK;
-  float *M = mf ? mf : at<float>(ws, p.off_fltm);
+  float *M = mf ? mf : at<float>(ws, L.off_fltm);
+  const Split sp = adj_split(n_query, ants->n_ant, 2, L.cap_fltp);
   AdjArgs a;
   memset(&a, 0, sizeof(a));
   a.qx = qx; a.qy = qy; a.qz = qz;
@@ -315,35 +360,36 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.X = reinterpret_cast<const float2 *>(signal);
-  a.ants_per_split = p.flt_aps;
-  a.out = p.flt_splits > 1 ? at<float>(ws, p.off_fltp) : M;
+  a.ants_per_split = sp.per_split;
+  a.out = sp.splits > 1 ? at<float>(ws, L.off_fltp) : M;
   a.smem_ant_off = adj_smem_ant_off(grid->n_freq);
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = false;
   const bool mono = ants->rx_x == nullptr;
-  RFR_CU(launch_adjoint(a, kModeFlt, mono, false, p.flt_splits, st));
-  if (p.flt_splits > 1)
-    RFR_CU(launch_sum_splits(at<float>(ws, p.off_fltp), p.flt_splits, n_query * 2, M, p.n_sm, st));
+  RFR_CU(launch_adjoint(a, kModeFlt, mono, false, sp.splits, st));
+  if (sp.splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, n_query * 2, M, device_sms(),
+                             st));
   RFR_TRY(allreduce_sum(comm, M, 2 * n_query, st));     // antenna shards -> full M (a4)
-  if (power) RFR_CU(launch_abs(M, n_query, power, p.n_sm, st));
+  if (power) RFR_CU(launch_abs(M, n_query, power, device_sms(), st));
   return RFR_OK;
 }
 
 rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_freq_grid *grid,
                       const float *qx, const float *qy, const float *qz, int64_t n_query,
-                      float *power, float *mf, const rfr_comm *comm, void *ws, size_t ws_bytes,
+                      float *power, float *mf, const rfr_comm *comm, const rfr_workspace *ws,
                       rfr_stream_t stream) {
   if (!power && n_query > 0) return RFR_E_ARG;
-  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, comm, ws, ws_bytes,
+  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, comm, ws,
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
 rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
                               const rfr_freq_grid *grid, const float *qx, const float *qy,
-                              const float *qz, int64_t n_query, float *mf, void *ws,
-                              size_t ws_bytes, rfr_stream_t stream) {
+                              const float *qz, int64_t n_query, float *mf,
+                              const rfr_workspace *ws, rfr_stream_t stream) {
   if (!mf && n_query > 0) return RFR_E_ARG;
-  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, nullptr, mf, nullptr, ws, ws_bytes,
+  return filter_impl(signal, ants, grid, qx, qy, qz, n_query, nullptr, mf, nullptr, ws,
                      reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -357,23 +403,22 @@ rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_
 rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *samples,
                                 float sharpness, const rfr_antennas *ants,
                                 const rfr_freq_grid *grid, const rfr_opts *opts, float *partials,
-                                void *ws, size_t ws_bytes, rfr_stream_t stream) {
+                                const rfr_workspace *ws, rfr_stream_t stream) {
   RFR_TRY(check_samples(samples));
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
-  if (!(sharpness > 0.f) || !ws || !partials || (ants->n_ant > 0 && !grad_signal))
-    return RFR_E_ARG;
+  if (!(sharpness > 0.f) || !partials || (ants->n_ant > 0 && !grad_signal)) return RFR_E_ARG;
   const uint32_t flags = opts ? opts->flags : 0u;
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
-  Plan p;
-  if (!make_plan(n_s, ants->n_ant, grid->n_freq, 0, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, n_s, 0, L));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (n_s == 0) return RFR_OK;
-  RFR_TRY(run_blend(samples, sharpness, flags, ws, p, st));
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
+  const Split sp = adj_split(n_s, ants->n_ant, 5, L.cap_bwdp);
   AdjArgs a;
   memset(&a, 0, sizeof(a));
-  a.rec = at<Rec>(ws, p.off_rec);
+  a.rec = at<Rec>(ws, L.off_rec);
   a.n_s = n_s;
   a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
   a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
@@ -383,134 +428,108 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.X = reinterpret_cast<const float2 *>(grad_signal);
-  a.ants_per_split = p.bwd_aps;
-  a.out = p.bwd_splits > 1 ? at<float>(ws, p.off_bwdp) : partials;
+  a.ants_per_split = sp.per_split;
+  a.out = sp.splits > 1 ? at<float>(ws, L.off_bwdp) : partials;
   a.smem_ant_off = adj_smem_ant_off(grid->n_freq);
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;
-  RFR_CU(launch_adjoint(a, kModeBwd, mono, has_corr(samples, ants), p.bwd_splits, st));
-  if (p.bwd_splits > 1)
-    RFR_CU(launch_sum_splits(at<float>(ws, p.off_bwdp), p.bwd_splits, 5 * n_s, partials, p.n_sm,
-                             st));
+  RFR_CU(launch_adjoint(a, kModeBwd, mono, has_corr(samples, ants), sp.splits, st));
+  if (sp.splits > 1)
+    RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
+                             device_sms(), st));
   return RFR_OK;
 }
 
 rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
-                               const rfr_opts *opts, const rfr_sample_grads *out, void *ws,
-                               size_t ws_bytes, rfr_stream_t stream) {
+                               const rfr_opts *opts, const rfr_sample_grads *out,
+                               const rfr_workspace *ws, rfr_stream_t stream) {
   RFR_TRY(check_samples(samples));
-  if (!(sharpness > 0.f) || !ws || !partials || !out || !out->sdf || !out->refl || !out->nx ||
+  if (!(sharpness > 0.f) || !partials || !out || !out->sdf || !out->refl || !out->nx ||
       !out->ny || !out->nz || !out->power || !out->sharpness)
     return RFR_E_ARG;
   const uint32_t flags = opts ? opts->flags : 0u;
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
-  Plan p;
-  if (!make_plan(n_s, 0, 1, 0, p)) return RFR_E_SHAPE;
-  // the caller's workspace may be planned for more antennas / bins: only the prefix layout matters
-  if (ws_bytes < p.off_bwds) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, n_s, 0, L));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  RFR_TRY(run_blend(samples, sharpness, flags, ws, p, st));
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
   BlendBwdArgs b;
   b.sdf = samples->sdf; b.refl = samples->refl; b.power = samples->power;
-  b.rec = at<Rec>(ws, p.off_rec);
+  b.rec = at<Rec>(ws, L.off_rec);
   b.partials = partials;
   b.n_rays = samples->n_rays; b.n_s = n_s; b.n_per_ray = samples->n_per_ray;
   b.s = sharpness;
   b.g_sdf = out->sdf; b.g_refl = out->refl; b.g_nx = out->nx; b.g_ny = out->ny; b.g_nz = out->nz;
   b.g_power = out->power;
-  b.ds_part = at<float>(ws, p.off_ds);
+  b.ds_part = at<float>(ws, L.off_ds);
   RFR_CU(launch_blend_bwd(b, st));
-  RFR_CU(launch_reduce_sum(b.ds_part, samples->n_rays, at<float>(ws, p.off_tmp), kTmpN,
+  RFR_CU(launch_reduce_sum(b.ds_part, samples->n_rays, at<float>(ws, L.off_tmp), kTmpN,
                            out->sharpness, st));
   return RFR_OK;
 }
 
 rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, float sharpness,
                         const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_opts *opts,
-                        const rfr_sample_grads *out, const rfr_comm *comm, void *ws,
-                        size_t ws_bytes, rfr_stream_t stream) {
+                        const rfr_sample_grads *out, const rfr_comm *comm,
+                        const rfr_workspace *ws, rfr_stream_t stream) {
   RFR_TRY(check_samples(samples));
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
-  Plan p;
-  if (!make_plan(n_s, ants->n_ant, grid->n_freq, 0, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
-  float *part = at<float>(ws, p.off_bwds);
+  Layout L;
+  RFR_TRY(check_ws(ws, n_s, 0, L));
+  float *part = at<float>(ws, L.off_bwds);
   RFR_TRY(rfr_backward_partial(grad_signal, samples, sharpness, ants, grid, opts, part, ws,
-                               ws_bytes, stream));
+                               stream));
   // a7: sum the per-sample partials over the antenna shards
   RFR_TRY(allreduce_sum(comm, part, 5 * n_s, reinterpret_cast<cudaStream_t>(stream)));
   rfr_opts o2;
   o2.flags = (opts ? opts->flags : 0u) | RFR_REUSE_BLEND;   // K1 ran in the partial call
-  return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, ws_bytes, stream);
+  return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, stream);
 }
 
 rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const float *power,
                                float eps, const rfr_antennas *ants, const rfr_freq_grid *grid,
                                const float *qx, const float *qy, const float *qz, int64_t n_query,
-                               float *grad_signal, void *ws, size_t ws_bytes,
+                               float *grad_signal, const rfr_workspace *ws,
                                rfr_stream_t stream) {
   RFR_TRY(check_ants(ants));
   RFR_TRY(check_grid(grid));
-  if (n_query < 0 || !ws || !(eps >= 0.f) || (ants->n_ant > 0 && !grad_signal) ||
+  if (n_query < 0 || !(eps >= 0.f) || (ants->n_ant > 0 && !grad_signal) ||
       (n_query > 0 && (!grad_power || !mf || !qx || !qy || !qz)))
     return RFR_E_ARG;
   if (ants->phi_tx || ants->phi_rx) return RFR_E_ARG;      // the filter has no transmittance
-  Plan p;
-  if (!make_plan(0, ants->n_ant, grid->n_freq, n_query, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, 0, n_query, L));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (ants->n_ant == 0) return RFR_OK;
-  Rec *qrec = at<Rec>(ws, p.off_qrec);
-  RFR_CU(launch_mf_adj_pack(grad_power, mf, power, eps, qx, qy, qz, n_query, qrec, p.n_sm, st));
-  FwdArgs a;
-  memset(&a, 0, sizeof(a));
-  a.rec = qrec;
-  a.n_s = n_query;
-  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
-  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
-  a.n_a = ants->n_ant;
-  a.n_f = grid->n_freq; a.nb = p.nb; a.nb_total = p.nb_total; a.taw = p.taw;
-  a.warp_smem = fwd_warp_smem();
-  a.k0 = grid->f0_hz / kC;
-  a.kd = grid->df_hz / kC;
-  a.kw = grid->df_hz * p.B / kC;
-  a.kchunk = grid->df_hz * p.B * p.nb / kC;
-  a.samples_per_split = p.mfa_sps;
-  a.out = p.mfa_splits > 1 ? at<float2>(ws, p.off_fwdp) : reinterpret_cast<float2 *>(grad_signal);
-  a.flags = at<unsigned>(ws, 0);
-  a.no_gain = false;
-  const bool mono = ants->rx_x == nullptr;
-  RFR_CU(launch_trace_fwd(a, p.B, mono, false, kFwdMFAdj, p.mfa_splits, st));
-  if (p.mfa_splits > 1)
-    RFR_CU(launch_sum_splits(at<float>(ws, p.off_fwdp), p.mfa_splits,
-                             ants->n_ant * (int64_t)grid->n_freq * 2, grad_signal, p.n_sm, st));
-  return RFR_OK;
+  Rec *qrec = at<Rec>(ws, L.off_qrec);
+  RFR_CU(launch_mf_adj_pack(grad_power, mf, power, eps, qx, qy, qz, n_query, qrec, device_sms(),
+                            st));
+  return run_fwd(qrec, n_query, ants, grid, false, false, kFwdMFAdj, grad_signal, ws, L, st);
 }
 
 rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n_query,
                             const int32_t *cell, float *history, float thr_hi, float ratio,
-                            float *grad_power, uint8_t *mask, float *loss, void *ws,
-                            size_t ws_bytes, rfr_stream_t stream) {
-  if (n_query < 0 || !ws || !loss || (n_query > 0 && (!power || !power_gt || !grad_power)) ||
+                            float *grad_power, uint8_t *mask, float *loss,
+                            const rfr_workspace *ws, rfr_stream_t stream) {
+  if (n_query < 0 || !loss || (n_query > 0 && (!power || !power_gt || !grad_power)) ||
       ((history == nullptr) != (cell == nullptr)))
     return RFR_E_ARG;
-  Plan p;
-  if (!make_plan(0, 0, 1, 0, p)) return RFR_E_SHAPE;
-  if (ws_bytes < p.total) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, 0, 0, L));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   RFR_CU(launch_heat_loss(power, power_gt, n_query, cell, history, thr_hi, ratio, grad_power, mask,
-                          at<float>(ws, p.off_tmp), kTmpN, loss, st));
+                          at<float>(ws, L.off_tmp), kTmpN, loss, st));
   return RFR_OK;
 }
 
-rfr_status rfr_poll_flags(void *ws, uint32_t *flags) {
-  if (!ws || !flags) return RFR_E_ARG;
+rfr_status rfr_poll_flags(const rfr_workspace *ws, uint32_t *flags) {
+  if (!ws || !ws->ptr || !flags) return RFR_E_ARG;
   uint32_t v = 0;
-  if (cudaMemcpy(&v, ws, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return RFR_E_CUDA;
-  if (cudaMemset(ws, 0, 4) != cudaSuccess) return RFR_E_CUDA;
+  if (cudaMemcpy(&v, ws->ptr, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return RFR_E_CUDA;
+  if (cudaMemset(ws->ptr, 0, 4) != cudaSuccess) return RFR_E_CUDA;
   *flags = v;
   return RFR_OK;
 }

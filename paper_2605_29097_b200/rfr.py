@@ -51,6 +51,11 @@ class rfr_opts(C.Structure):
     _fields_ = [("flags", C.c_uint32)]
 
 
+class rfr_workspace(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("bytes", C.c_size_t), ("n_samples", C.c_int64),
+                ("n_ant", C.c_int64), ("n_freq", C.c_int32), ("n_query", C.c_int64)]
+
+
 STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too small",
           3: "domain", 4: "numeric", 5: "CUDA launch failure", 6: "unsupported", 7: "NCCL failure"}
 
@@ -79,19 +84,20 @@ def load(path: str = LIB_PATH):
     vp, i64, i32, u32, f = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32, C.c_float
     S, A, G, O, R = (C.POINTER(rfr_samples), C.POINTER(rfr_antennas), C.POINTER(rfr_freq_grid),
                      C.POINTER(rfr_opts), C.POINTER(rfr_sample_grads))
+    W = C.POINTER(rfr_workspace)
     sig = {
         "rfr_workspace_size": [i64, i64, i32, i64, C.POINTER(C.c_size_t)],
-        "rfr_forward": [S, f, A, G, O, vp, vp, C.c_size_t, vp],
-        "rfr_loss": [vp, vp, i64, vp, vp, vp, C.c_size_t, vp],
-        "rfr_filter": [vp, A, G, vp, vp, vp, i64, vp, vp, vp, vp, C.c_size_t, vp],
-        "rfr_filter_partial": [vp, A, G, vp, vp, vp, i64, vp, vp, C.c_size_t, vp],
+        "rfr_forward": [S, f, A, G, O, vp, W, vp],
+        "rfr_loss": [vp, vp, i64, vp, vp, W, vp],
+        "rfr_filter": [vp, A, G, vp, vp, vp, i64, vp, vp, vp, W, vp],
+        "rfr_filter_partial": [vp, A, G, vp, vp, vp, i64, vp, W, vp],
         "rfr_filter_power": [vp, i64, vp, vp],
-        "rfr_backward": [vp, S, f, A, G, O, R, vp, vp, C.c_size_t, vp],
-        "rfr_backward_partial": [vp, S, f, A, G, O, vp, vp, C.c_size_t, vp],
-        "rfr_backward_finish": [vp, S, f, O, R, vp, C.c_size_t, vp],
-        "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, vp, C.c_size_t, vp],
-        "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, vp, C.c_size_t, vp],
-        "rfr_poll_flags": [vp, C.POINTER(u32)],
+        "rfr_backward": [vp, S, f, A, G, O, R, vp, W, vp],
+        "rfr_backward_partial": [vp, S, f, A, G, O, vp, W, vp],
+        "rfr_backward_finish": [vp, S, f, O, R, W, vp],
+        "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, W, vp],
+        "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, W, vp],
+        "rfr_poll_flags": [W, C.POINTER(u32)],
         "rfr_comm_unique_id": [vp],
         "rfr_comm_init": [vp, C.c_int, C.c_int, C.POINTER(vp)],
         "rfr_comm_destroy": [vp],
@@ -204,25 +210,53 @@ def rfr_workspace_size(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0
     return out.value
 
 
-def workspace(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0, device="cuda"):
-    nb = rfr_workspace_size(n_samples, n_ant, n_freq, n_query)
-    ws = torch.zeros(max(nb, 256), dtype=torch.uint8, device=device)
-    return ws
+class Workspace:
+    """Device scratch of librfr (rfr_workspace): a uint8 tensor plus its planning dimensions, the
+    upper bounds of every call that uses it (include/librfr.h)."""
+
+    def __init__(self, n_samples: int, n_ant: int, n_freq: int, n_query: int = 0, device="cuda",
+                 nbytes: Optional[int] = None):
+        self.dims = (int(n_samples), int(n_ant), int(n_freq), int(n_query))
+        need = rfr_workspace_size(*self.dims)
+        self.tensor = torch.zeros(max(need if nbytes is None else nbytes, 256), dtype=torch.uint8,
+                                  device=device)
+
+    def numel(self) -> int:
+        return self.tensor.numel()
+
+    def struct(self) -> rfr_workspace:
+        return rfr_workspace(_ptr(self.tensor), self.tensor.numel(), *self.dims)
+
+    def truncated(self, nbytes: int) -> "Workspace":
+        """A view of the first nbytes with the same planning dims (for argument-error tests)."""
+        w = Workspace.__new__(Workspace)
+        w.dims, w.tensor = self.dims, self.tensor[:nbytes]
+        return w
+
+
+def workspace(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0, device="cuda") -> Workspace:
+    return Workspace(n_samples, n_ant, n_freq, n_query, device)
+
+
+def _ws(ws: Workspace):
+    if not isinstance(ws, Workspace):
+        raise RfrError("expected an rfr.Workspace")
+    return C.byref(ws.struct())
 
 
 def rfr_forward(samples: DeviceSamples, sharpness: float, ants: DeviceAntennas, grid,
                 signal: torch.Tensor, ws: torch.Tensor, flags: int = 0, stream=None):
     s, a, g, o = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags)
     _check(load().rfr_forward(C.byref(s), float(sharpness), C.byref(a), C.byref(g), C.byref(o),
-                              _ptr(signal), _ptr(ws), ws.numel(), _stream(stream)), "rfr_forward")
+                              _ptr(signal), _ws(ws), _stream(stream)), "rfr_forward")
     return signal
 
 
 def rfr_loss(signal: torch.Tensor, target: torch.Tensor, grad: torch.Tensor, loss: torch.Tensor,
              ws: torch.Tensor, stream=None):
     n = signal.numel() // 2
-    _check(load().rfr_loss(_ptr(signal), _ptr(target), n, _ptr(grad), _ptr(loss), _ptr(ws),
-                           ws.numel(), _stream(stream)), "rfr_loss")
+    _check(load().rfr_loss(_ptr(signal), _ptr(target), n, _ptr(grad), _ptr(loss), _ws(ws),
+                           _stream(stream)), "rfr_loss")
     return loss, grad
 
 
@@ -231,8 +265,8 @@ def rfr_filter(signal: torch.Tensor, ants: DeviceAntennas, grid, qx, qy, qz, pow
                stream=None):
     a, g = ants.struct(), grid_struct(grid)
     _check(load().rfr_filter(_ptr(signal), C.byref(a), C.byref(g), _ptr(qx), _ptr(qy), _ptr(qz),
-                             int(qx.numel()), _ptr(power), _ptr(mf), _comm(comm), _ptr(ws),
-                             ws.numel(), _stream(stream)), "rfr_filter")
+                             int(qx.numel()), _ptr(power), _ptr(mf), _comm(comm), _ws(ws),
+                             _stream(stream)), "rfr_filter")
     return power
 
 
@@ -240,7 +274,7 @@ def rfr_filter_partial(signal, ants: DeviceAntennas, grid, qx, qy, qz, mf: torch
                        ws: torch.Tensor, stream=None):
     a, g = ants.struct(), grid_struct(grid)
     _check(load().rfr_filter_partial(_ptr(signal), C.byref(a), C.byref(g), _ptr(qx), _ptr(qy),
-                                     _ptr(qz), int(qx.numel()), _ptr(mf), _ptr(ws), ws.numel(),
+                                     _ptr(qz), int(qx.numel()), _ptr(mf), _ws(ws),
                                      _stream(stream)), "rfr_filter_partial")
     return mf
 
@@ -258,7 +292,7 @@ def rfr_filter_backward(grad_power: torch.Tensor, mf: torch.Tensor, ants: Device
     a, g = ants.struct(), grid_struct(grid)
     _check(load().rfr_filter_backward(_ptr(grad_power), _ptr(mf), _ptr(power), float(eps),
                                       C.byref(a), C.byref(g), _ptr(qx), _ptr(qy), _ptr(qz),
-                                      int(qx.numel()), _ptr(grad_signal), _ptr(ws), ws.numel(),
+                                      int(qx.numel()), _ptr(grad_signal), _ws(ws),
                                       _stream(stream)), "rfr_filter_backward")
     return grad_signal
 
@@ -274,7 +308,7 @@ def rfr_heatmap_loss(power: torch.Tensor, power_gt: torch.Tensor, grad_power: to
         raise RfrError("mask must be uint8")
     _check(load().rfr_heatmap_loss(_ptr(power), _ptr(power_gt), int(power.numel()), _ptr(cell),
                                    _ptr(history), float(thr_hi), float(ratio), _ptr(grad_power),
-                                   _ptr(mask), _ptr(loss), _ptr(ws), ws.numel(), _stream(stream)),
+                                   _ptr(mask), _ptr(loss), _ws(ws), _stream(stream)),
            "rfr_heatmap_loss")
     return loss, grad_power
 
@@ -305,8 +339,8 @@ def rfr_backward(grad_signal: torch.Tensor, samples: DeviceSamples, sharpness: f
                  comm: "Comm" = None, stream=None):
     s, a, g, o, r = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags), out.struct()
     _check(load().rfr_backward(_ptr(grad_signal), C.byref(s), float(sharpness), C.byref(a),
-                               C.byref(g), C.byref(o), C.byref(r), _comm(comm), _ptr(ws),
-                               ws.numel(), _stream(stream)), "rfr_backward")
+                               C.byref(g), C.byref(o), C.byref(r), _comm(comm), _ws(ws),
+                               _stream(stream)), "rfr_backward")
     return out
 
 
@@ -315,8 +349,8 @@ def rfr_backward_partial(grad_signal, samples: DeviceSamples, sharpness: float,
                          flags: int = 0, stream=None):
     s, a, g, o = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags)
     _check(load().rfr_backward_partial(_ptr(grad_signal), C.byref(s), float(sharpness), C.byref(a),
-                                       C.byref(g), C.byref(o), _ptr(partials), _ptr(ws),
-                                       ws.numel(), _stream(stream)), "rfr_backward_partial")
+                                       C.byref(g), C.byref(o), _ptr(partials), _ws(ws),
+                                       _stream(stream)), "rfr_backward_partial")
     return partials
 
 
@@ -324,7 +358,7 @@ def rfr_backward_finish(partials: torch.Tensor, samples: DeviceSamples, sharpnes
                         out: Grads, ws: torch.Tensor, flags: int = 0, stream=None):
     s, o, r = samples.struct(), rfr_opts(flags), out.struct()
     _check(load().rfr_backward_finish(_ptr(partials), C.byref(s), float(sharpness), C.byref(o),
-                                      C.byref(r), _ptr(ws), ws.numel(), _stream(stream)),
+                                      C.byref(r), _ws(ws), _stream(stream)),
            "rfr_backward_finish")
     return out
 
@@ -335,7 +369,7 @@ def rfr_launch_count() -> int:
 
 def rfr_poll_flags(ws: torch.Tensor) -> int:
     v = C.c_uint32()
-    _check(load().rfr_poll_flags(_ptr(ws), C.byref(v)), "rfr_poll_flags")
+    _check(load().rfr_poll_flags(_ws(ws), C.byref(v)), "rfr_poll_flags")
     return v.value
 
 

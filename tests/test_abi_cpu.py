@@ -56,11 +56,13 @@ def test_argument_errors_before_any_launch():
     rfr, lib = _lib()
     g = rfr.rfr_freq_grid(77e9, 1e6, 8)
     # null sample struct / null workspace -> RFR_E_ARG without touching a device
-    assert lib.rfr_forward(None, 1.0, None, C.byref(g), None, None, None, 0, None) == 1
+    assert lib.rfr_forward(None, 1.0, None, C.byref(g), None, None, None, None) == 1
     s = rfr.rfr_samples()
     s.n_rays, s.n_per_ray = 1, 1
     a = rfr.rfr_antennas()
-    assert lib.rfr_forward(C.byref(s), 1.0, C.byref(a), C.byref(g), None, None, None, 0, None) == 1
+    assert lib.rfr_forward(C.byref(s), 1.0, C.byref(a), C.byref(g), None, None, None, None) == 1
+    w = rfr.rfr_workspace(None, 0, 1, 1, 8, 0)
+    assert lib.rfr_loss(None, None, 0, None, None, C.byref(w), None) == 1
     assert lib.rfr_filter_power(None, 4, None, None) == 1
     assert lib.rfr_filter_power(None, 0, None, None) == 0
 

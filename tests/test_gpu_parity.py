@@ -374,9 +374,39 @@ def test_abi_argument_errors():
     with pytest.raises(m.RfrError, match="invalid argument"):
         m.rfr_forward(DS, s, DA, FreqGrid(77e9, 0.0, grid.n_freq), sig, ws)
     with pytest.raises(m.RfrError, match="workspace too small"):
-        m.rfr_forward(DS, s, DA, grid, sig, ws[:64])
+        m.rfr_forward(DS, s, DA, grid, sig, ws.truncated(64))
     with pytest.raises(m.RfrError):
         m.rfr_forward(DS, s, DA, grid, sig.cpu(), ws)     # no CPU fallback
+    # more samples than the workspace was planned for
+    small = m.workspace(S.n - 1, A.n, grid.n_freq, 0, dev())
+    with pytest.raises(m.RfrError, match="workspace too small"):
+        m.rfr_forward(DS, s, DA, grid, sig, small)
+
+
+def test_workspace_regions_are_stable_across_call_types():
+    """K1 records cached by rfr_forward survive a filter, a filter adjoint and a loss call on the
+    same workspace (the layout depends only on the planning dims), so RFR_REUSE_BLEND afterwards
+    gives bitwise the gradients of a fresh K1."""
+    m = rfr()
+    p = problem("c1")
+    b = p.bundles[0]
+    DS, DA = m.DeviceSamples.from_host(b.samples, dev()), m.DeviceAntennas.from_host(b.antennas, dev())
+    n, na, nf = b.samples.n, b.antennas.n, p.grid.n_freq
+    ws = m.workspace(n, na, nf, n, dev())
+    sig = torch.empty(na, nf, 2, device=dev())
+    m.rfr_forward(DS, p.sharpness, DA, p.grid, sig, ws)
+    P, M = torch.empty(n, device=dev()), torch.empty(n, 2, device=dev())
+    m.rfr_filter(sig, DA, p.grid, DS.x, DS.y, DS.z, P, ws, mf=M)
+    G = torch.empty_like(sig)
+    m.rfr_filter_backward(P, M, DA, p.grid, DS.x, DS.y, DS.z, G, ws, power=P, eps=1e-30)
+    L = torch.empty(1, device=dev())
+    m.rfr_loss(sig, sig, torch.empty_like(sig), L, ws)
+    o1, o2 = m.Grads.empty(n, dev()), m.Grads.empty(n, dev())
+    m.rfr_backward(G, DS, p.sharpness, DA, p.grid, o1, ws, flags=m.RFR_REUSE_BLEND)
+    m.rfr_backward(G, DS, p.sharpness, DA, p.grid, o2, ws)
+    torch.cuda.synchronize()
+    for k in m.Grads.NAMES:
+        assert torch.equal(getattr(o1, k), getattr(o2, k)), k
 
 
 def test_comm_path_one_rank_is_identity():
