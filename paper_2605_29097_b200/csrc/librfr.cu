@@ -80,7 +80,7 @@ Split fwd_split(int64_t n_pts, int64_t n_a, int32_t n_f, const FwdGeom &g, size_
 
 // split over antennas of K3 / K4 (one thread per point): ~16 waves of 4 CTAs per SM
 Split adj_split(int64_t n_pts, int64_t n_a, int floats_per_pt, size_t cap) {
-  const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
+  const int64_t per_cta = (int64_t)kAdjThreads;
   const int64_t tiles = std::max<int64_t>(1, cdiv(n_pts, per_cta));
   int64_t s = cdiv((int64_t)device_sms() * 4 * 16, tiles);
   s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, kAdjGA)));

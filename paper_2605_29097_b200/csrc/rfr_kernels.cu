@@ -223,43 +223,43 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
 }
 
 // ================================================================================== K3 / K4
-// One thread owns SPT samples (or queries) and loops over the antennas of its split.  Per pair:
+// One thread owns one sample (or query) and loops over the antennas of its split.  Per pair:
 // fp64 path length, E = e^{+j2pi f0 tau}, w = e^{+j2pi df tau}; Horner h = sum_m X(i,m) w^m over the
 // bins with X(i, .) broadcast from shared memory (2 FFMA2 per complex step).
 //   MODE_BWD: R = Re(E h) -> per-sample sums S1, S2, S3 (Eq. 5 chain), written as partials.
 //   MODE_FLT: M += E h (complex) -> partial matched-filter output.
-template <int MODE, int SPT, bool MONO, bool CORR, int NF>
+// NF > 0 (the configs' bin counts): straight-line code over two independent Horner chains that
+// share w -- bins [NF/2, NF) and [0, NF/2), merged as h = h_lo + w^{NF/2} h_hi.  Both FFMA2 of a
+// step read w from the same register (ptxas folds the (-Im, Re) swizzle into the operand), so w
+// stays in the operand reuse cache across the chains and each FFMA2 reads at most two registers
+// per bank: the issue interval drops from 3 to 2 cycles (tools/sass_banks.py).  X is staged
+// interleaved, X'[m] = (X[m], X[m + NF/2]), one LDS.128 per step.  NF == 0: rolled single chain.
+template <int MODE, bool MONO, bool CORR, int NF>
 __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
   AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
   const int tid = threadIdx.x;
   const int nf = NF > 0 ? NF : a.n_f;
-  const int64_t base = (int64_t)blockIdx.x * (kAdjThreads * SPT);
+  constexpr int H = NF / 2;
+  const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
   const bool no_gain = a.no_gain;
+  const bool valid = j < a.n_s;
 
-  Rec rec[SPT];
-  bool valid[SPT];
-  float S1[SPT], S2[SPT], S3x[SPT], S3y[SPT], S3z[SPT];
-#pragma unroll
-  for (int s = 0; s < SPT; ++s) {
-    const int64_t j = base + s * kAdjThreads + tid;
-    valid[s] = j < a.n_s;
-    if (MODE == kModeBwd) {
-      if (valid[s]) rec[s] = a.rec[j];
-      else { rec[s].x = rec[s].y = 0.0; rec[s].z = 1.0; rec[s].w = 0.f; rec[s].T = 0.f;
-             rec[s].nx = rec[s].ny = 0.f; rec[s].nz = 1.f; rec[s].papr = 1.f; }
-    } else {
-      rec[s].x = valid[s] ? (double)a.qx[j] : 0.0;
-      rec[s].y = valid[s] ? (double)a.qy[j] : 0.0;
-      rec[s].z = valid[s] ? (double)a.qz[j] : 1.0;
-      rec[s].w = 0.f; rec[s].T = 1.f; rec[s].nx = rec[s].ny = 0.f; rec[s].nz = 1.f;
-      rec[s].papr = 1.f;
-    }
-    S1[s] = S2[s] = S3x[s] = S3y[s] = S3z[s] = 0.f;
+  Rec rec;
+  if (MODE == kModeBwd) {
+    if (valid) rec = a.rec[j];
+    else { rec.x = rec.y = 0.0; rec.z = 1.0; rec.w = 0.f; rec.T = 0.f;
+           rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f; }
+  } else {
+    rec.x = valid ? (double)a.qx[j] : 0.0;
+    rec.y = valid ? (double)a.qy[j] : 0.0;
+    rec.z = valid ? (double)a.qz[j] : 1.0;
+    rec.w = 0.f; rec.T = 1.f; rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f;
   }
+  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
   bool domain = false;
 
   for (int64_t ic = i_lo; ic < i_hi; ic += kAdjGA) {
@@ -268,7 +268,15 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
     {   // stage X rows [ga][nf] (contiguous in global memory) and the antennas
       const float2 *src = a.X + ic * nf;
       const int n2 = ga * nf;
-      for (int t = tid; t < n2; t += kAdjThreads) X[t] = src[t];
+      if (NF > 0) {      // interleave the two chains' bins: X'[row][2m + c] = X[row][m + c H]
+        for (int t = tid; t < n2; t += kAdjThreads) {
+          const int row = t / NF, col = t % NF;
+          const int c = col >= H, m = col - c * H;
+          X[row * NF + 2 * m + c] = src[t];
+        }
+      } else {
+        for (int t = tid; t < n2; t += kAdjThreads) X[t] = src[t];
+      }
       for (int aa = tid; aa < ga; aa += kAdjThreads) {
         const int64_t ia = ic + aa;
         AntD d;
@@ -283,89 +291,78 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
     __syncthreads();
     for (int aa = 0; aa < ga; ++aa) {
       const AntD an = ant[aa];
-      PairBwd g[SPT];
-      f2x w1[SPT], w2[SPT], h[SPT];
-      float Er[SPT], Ei[SPT];
-#pragma unroll
-      for (int s = 0; s < SPT; ++s) {
-        pair_geometry<MONO, CORR>(rec[s], an, no_gain, g[s]);
-        domain |= (MODE == kModeBwd) && valid[s] && !g[s].ok;
-        const float fr0 = frac_cycles(g[s].L * a.k0);
-        const float frd = frac_cycles(g[s].L * a.kd);
-        float es, ec, zs, zc;
-        __sincosf(kTwoPi * fr0, &es, &ec);
-        sincospif(2.f * frd, &zs, &zc);
-        Er[s] = ec; Ei[s] = es;                    // E = e^{+j theta0}
-        w1[s] = pkv(zc, zs);                       // w = e^{+j theta_d}
-        w2[s] = pkv(-zs, zc);                      // (opaque: keeps ptxas from re-deriving it in the loop)
-        h[s] = 0ull;
-      }
-      const float2 *Xa = X + aa * nf;
-      // Horner from the top bin down: h = h w + X_m  (2 FFMA2 per complex step).  With NF > 0
-      // the bin loop is straight-line code (no loop-carried register renames: in a rolled loop
-      // ptxas spent ~25% extra FMA-pipe slots on IMAD.MOV / re-derived w2 at every back edge).
+      PairBwd g;
+      pair_geometry<MONO, CORR>(rec, an, no_gain, g);
+      domain |= (MODE == kModeBwd) && valid && !g.ok;
+      const float fr0 = frac_cycles(g.L * a.k0);
+      const float frd = frac_cycles(g.L * a.kd);
+      float es, ec, zs, zc;
+      __sincosf(kTwoPi * fr0, &es, &ec);
+      sincospif(2.f * frd, &zs, &zc);
+      const f2x w = pk(zc, zs);                     // w = e^{+j theta_d}
+      float hr, hi;
       if (NF > 0) {
+        const float4 *X4 = reinterpret_cast<const float4 *>(X + aa * NF);
+        f2x ha = 0ull, hb = 0ull;                   // chains over bins [H, NF) and [0, H)
 #pragma unroll
-        for (int m = NF - 1; m >= 0; --m) {
-          const float2 xv = Xa[m];
-          const f2x xm = pk(xv.x, xv.y);
-#pragma unroll
-          for (int s = 0; s < SPT; ++s) {
-            const float2 hv = upk(h[s]);
-            const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
-            h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
-          }
+        for (int m = H - 1; m >= 0; --m) {
+          const float4 xv = X4[m];                  // (X[m], X[m + H])
+          const float2 va = upk(ha), vb = upk(hb);
+          const f2x ta = ffma2(w, pk(va.x, va.x), pk(xv.z, xv.w));
+          const f2x tb = ffma2(w, pk(vb.x, vb.x), pk(xv.x, xv.y));
+          const f2x w2 = pk(-zs, zc);
+          ha = ffma2(w2, pk(va.y, va.y), ta);
+          hb = ffma2(w2, pk(vb.y, vb.y), tb);
         }
+        // h = h_lo + w^H h_hi, w^H from the fp64 cycle count (accurate, not by powering)
+        float us, uc;
+        sincospif(2.f * frac_cycles(g.L * a.kd * (double)H), &us, &uc);
+        const float2 va = upk(ha), vb = upk(hb);
+        hr = vb.x + (uc * va.x - us * va.y);
+        hi = vb.y + (uc * va.y + us * va.x);
       } else {
-#pragma unroll 8
+        const float2 *Xa = X + aa * nf;
+        f2x h = 0ull;
+        const f2x w2 = pkv(-zs, zc);
+#pragma unroll 4
         for (int m = nf - 1; m >= 0; --m) {
           const float2 xv = Xa[m];
-          const f2x xm = pk(xv.x, xv.y);
-#pragma unroll
-          for (int s = 0; s < SPT; ++s) {
-            const float2 hv = upk(h[s]);
-            const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
-            h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
-          }
+          const float2 hv = upk(h);
+          const f2x t = ffma2(w, pk(hv.x, hv.x), pk(xv.x, xv.y));
+          h = ffma2(w2, pk(hv.y, hv.y), t);
         }
+        const float2 hv = upk(h);
+        hr = hv.x;
+        hi = hv.y;
       }
-#pragma unroll
-      for (int s = 0; s < SPT; ++s) {
-        const float2 hv = upk(h[s]);
-        if (MODE == kModeBwd) {
-          const float R = Er[s] * hv.x - Ei[s] * hv.y;      // Re(E h)
-          const float TT = g[s].Tt * g[s].Tr;
-          const float Rg = R * g[s].gg;
-          S1[s] = fmaf(Rg, TT, S1[s]);
-          S2[s] = fmaf(Rg, g[s].Tr * g[s].chit + g[s].Tt * g[s].chir, S2[s]);
-          const float Rc = R * g[s].gamma * TT;
-          S3x[s] = fmaf(Rc, g[s].dgx, S3x[s]);
-          S3y[s] = fmaf(Rc, g[s].dgy, S3y[s]);
-          S3z[s] = fmaf(Rc, g[s].dgz, S3z[s]);
-        } else {
-          // M += E h
-          S1[s] = fmaf(Er[s], hv.x, fmaf(-Ei[s], hv.y, S1[s]));
-          S2[s] = fmaf(Er[s], hv.y, fmaf(Ei[s], hv.x, S2[s]));
-        }
+      if (MODE == kModeBwd) {
+        const float R = ec * hr - es * hi;          // Re(E h), E = e^{+j theta0}
+        const float TT = g.Tt * g.Tr;
+        const float Rg = R * g.gg;
+        S1 = fmaf(Rg, TT, S1);
+        S2 = fmaf(Rg, g.Tr * g.chit + g.Tt * g.chir, S2);
+        const float Rc = R * g.gamma * TT;
+        S3x = fmaf(Rc, g.dgx, S3x);
+        S3y = fmaf(Rc, g.dgy, S3y);
+        S3z = fmaf(Rc, g.dgz, S3z);
+      } else {                                      // M += E h
+        S1 = fmaf(ec, hr, fmaf(-es, hi, S1));
+        S2 = fmaf(ec, hi, fmaf(es, hr, S2));
       }
     }
   }
   if (domain) atomicOr(a.flags, 1u);
-#pragma unroll
-  for (int s = 0; s < SPT; ++s) {
-    const int64_t j = base + s * kAdjThreads + tid;
-    if (!valid[s]) continue;
-    if (MODE == kModeBwd) {
-      float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
-      P[j] = S1[s];
-      P[a.n_s + j] = S2[s];
-      P[2 * a.n_s + j] = S3x[s];
-      P[3 * a.n_s + j] = S3y[s];
-      P[4 * a.n_s + j] = S3z[s];
-    } else {
-      float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
-      M[j] = make_float2(S1[s], S2[s]);
-    }
+  if (!valid) return;
+  if (MODE == kModeBwd) {
+    float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
+    P[j] = S1;
+    P[a.n_s + j] = S2;
+    P[2 * a.n_s + j] = S3x;
+    P[3 * a.n_s + j] = S3y;
+    P[4 * a.n_s + j] = S3z;
+  } else {
+    float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
+    M[j] = make_float2(S1, S2);
   }
 }
 
@@ -623,11 +620,11 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
 template <int MODE, bool MONO, bool CORR>
 static cudaError_t adj_t(const AdjArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
   // bin counts with a straight-line Horner specialisation (the configs' 64 / 128 / 256 / 512)
-  auto k = a.n_f == 256 ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 256>
-         : a.n_f == 512 ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 512>
-         : a.n_f == 128 ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 128>
-         : a.n_f == 64  ? k_adjoint<MODE, kAdjSPT, MONO, CORR, 64>
-                        : k_adjoint<MODE, kAdjSPT, MONO, CORR, 0>;
+  auto k = a.n_f == 256 ? k_adjoint<MODE, MONO, CORR, 256>
+         : a.n_f == 512 ? k_adjoint<MODE, MONO, CORR, 512>
+         : a.n_f == 128 ? k_adjoint<MODE, MONO, CORR, 128>
+         : a.n_f == 64  ? k_adjoint<MODE, MONO, CORR, 64>
+                        : k_adjoint<MODE, MONO, CORR, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, kAdjThreads, smem, st>>>(a);
@@ -636,7 +633,7 @@ static cudaError_t adj_t(const AdjArgs &a, dim3 grid, size_t smem, cudaStream_t 
 
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st) {
-  const int64_t per_cta = (int64_t)kAdjThreads * kAdjSPT;
+  const int64_t per_cta = (int64_t)kAdjThreads;
   dim3 grid((unsigned)((a.n_s + per_cta - 1) / per_cta), (unsigned)n_splits);
   const size_t smem = adj_smem_bytes(a.n_f);
   if (mode == kModeBwd) {

@@ -13,7 +13,6 @@ constexpr int kFwdMinBlocks = 3;   // K2 CTAs per SM (register budget ~170)
 constexpr int kFwdWarps = kFwdThreads / 32;
 constexpr int kFwdTJ = 16;         // samples per K2 warp tile
 constexpr int kAdjThreads = 128;   // K3/K4 CTA size
-constexpr int kAdjSPT = 2;         // samples (queries) per K3/K4 thread
 constexpr int kAdjGA = 8;          // antennas per K3/K4 shared-memory stage
 constexpr int kModeBwd = 0, kModeFlt = 1;
 constexpr int kFwdTrace = 0, kFwdMFAdj = 1;  // K2 signal tracing / K5 matched-filter adjoint
