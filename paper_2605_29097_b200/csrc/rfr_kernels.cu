@@ -270,9 +270,10 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
       const int n2 = ga * nf;
       if (NF > 0) {      // interleave the two chains' bins: X'[row][2m + c] = X[row][m + c H]
         for (int t = tid; t < n2; t += kAdjThreads) {
-          const int row = t / NF, col = t % NF;
+          constexpr int NFd = NF > 0 ? NF : 1;       // (NF == 0 never takes this branch)
+          const int row = t / NFd, col = t % NFd;
           const int c = col >= H, m = col - c * H;
-          X[row * NF + 2 * m + c] = src[t];
+          X[row * NFd + 2 * m + c] = src[t];
         }
       } else {
         for (int t = tid; t < n2; t += kAdjThreads) X[t] = src[t];
