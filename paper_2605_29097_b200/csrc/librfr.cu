@@ -362,7 +362,6 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   a.X = reinterpret_cast<const float2 *>(signal);
   a.ants_per_split = sp.per_split;
   a.out = sp.splits > 1 ? at<float>(ws, L.off_fltp) : M;
-  a.smem_ant_off = adj_smem_ant_off(grid->n_freq);
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = false;
   const bool mono = ants->rx_x == nullptr;
@@ -430,7 +429,6 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   a.X = reinterpret_cast<const float2 *>(grad_signal);
   a.ants_per_split = sp.per_split;
   a.out = sp.splits > 1 ? at<float>(ws, L.off_bwdp) : partials;
-  a.smem_ant_off = adj_smem_ant_off(grid->n_freq);
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;

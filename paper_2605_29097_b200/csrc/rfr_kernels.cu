@@ -186,10 +186,17 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
     if (active) {
       const float4 *ap = anc + my_b * taw + my_a;
       const float *kp_ = kv + my_a;
+      // software pipeline: the next sample's anchors are loaded before this sample's chain runs
+      float4 Yn = ap[0];
+      float knx = kp_[0];
 #pragma unroll 1
       for (int jj = 0; jj < kFwdTJ; ++jj) {
-        const float4 Y = ap[jj * 32];
-        const float k = kp_[jj * 32];
+        const float4 Y = Yn;
+        const float k = knx;
+        if (jj + 1 < kFwdTJ) {
+          Yn = ap[(jj + 1) * 32];
+          knx = kp_[(jj + 1) * 32];
+        }
         const f2x kp = pk(k, k), kn = pk(-k, -k);
         f2x q0 = pk(Y.x, Y.y), q1 = pk(Y.z, Y.w);
         acc[0] = fadd2(acc[0], q0);
@@ -237,11 +244,15 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
 template <int MODE, bool MONO, bool CORR, int NF>
 __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
-  AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
+  // NF > 0: double-buffered stages of GA antennas, X rows copied with cp.async while the previous
+  // stage computes (one barrier per stage, load latency hidden).  NF == 0: one buffer, kAdjGA.
+  constexpr int GA = NF > 0 ? adj_stage_ants(NF) : kAdjGA;
+  constexpr int NB = NF > 0 ? 2 : 1;
   const int tid = threadIdx.x;
   const int nf = NF > 0 ? NF : a.n_f;
   constexpr int H = NF / 2;
+  float2 *Xb = reinterpret_cast<float2 *>(smem_raw);                     // [NB][GA][nf]
+  AntD *antb = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);      // [NB][GA]
   const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
@@ -262,34 +273,49 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
   float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
   bool domain = false;
 
-  for (int64_t ic = i_lo; ic < i_hi; ic += kAdjGA) {
-    const int ga = (int)min((int64_t)kAdjGA, i_hi - ic);
-    __syncthreads();
-    {   // stage X rows [ga][nf] (contiguous in global memory) and the antennas
+  // stage the X rows [ga][nf] (contiguous in global memory) and the antennas of [ic, ic + ga)
+  auto stage = [&](int64_t ic, int buf) {
+    const int ga = (int)min((int64_t)GA, i_hi - ic);
+    float2 *X = Xb + (size_t)buf * GA * nf;
+    AntD *ant = antb + buf * GA;
+    if (NF > 0) {
+      const float4 *src = reinterpret_cast<const float4 *>(a.X + ic * NF);
+      for (int c = tid; c < ga * NF / 2; c += kAdjThreads)
+        cp_async16(reinterpret_cast<float4 *>(X) + c, src + c);
+      cp_async_commit();
+    } else {
       const float2 *src = a.X + ic * nf;
-      const int n2 = ga * nf;
-      if (NF > 0) {      // interleave the two chains' bins: X'[row][2m + c] = X[row][m + c H]
-        for (int t = tid; t < n2; t += kAdjThreads) {
-          constexpr int NFd = NF > 0 ? NF : 1;       // (NF == 0 never takes this branch)
-          const int row = t / NFd, col = t % NFd;
-          const int c = col >= H, m = col - c * H;
-          X[row * NFd + 2 * m + c] = src[t];
-        }
-      } else {
-        for (int t = tid; t < n2; t += kAdjThreads) X[t] = src[t];
-      }
-      for (int aa = tid; aa < ga; aa += kAdjThreads) {
-        const int64_t ia = ic + aa;
-        AntD d;
-        d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
-        if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
-        else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
-        d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
-        d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
-        ant[aa] = d;
-      }
+      for (int t = tid; t < ga * nf; t += kAdjThreads) X[t] = src[t];
     }
-    __syncthreads();
+    for (int aa = tid; aa < ga; aa += kAdjThreads) {
+      const int64_t ia = ic + aa;
+      AntD d;
+      d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+      if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+      else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+      d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+      d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+      ant[aa] = d;
+    }
+  };
+
+  const int n_stages = (int)((max(i_hi - i_lo, (int64_t)0) + GA - 1) / GA);
+  if (NF > 0 && n_stages > 0) stage(i_lo, 0);
+  for (int st = 0; st < n_stages; ++st) {
+    const int64_t ic = i_lo + (int64_t)st * GA;
+    const int ga = (int)min((int64_t)GA, i_hi - ic);
+    const int buf = NB == 2 ? (st & 1) : 0;
+    if (NF > 0) {
+      cp_async_wait_all();
+      __syncthreads();                    // stage st visible; every warp is done with stage st-1
+      if (st + 1 < n_stages) stage(ic + GA, buf ^ 1);
+    } else {
+      __syncthreads();
+      stage(ic, 0);
+      __syncthreads();
+    }
+    const float2 *X = Xb + (size_t)buf * GA * nf;
+    const AntD *ant = antb + buf * GA;
     for (int aa = 0; aa < ga; ++aa) {
       const AntD an = ant[aa];
       PairBwd g;
@@ -303,24 +329,27 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
       const f2x w = pk(zc, zs);                     // w = e^{+j theta_d}
       float hr, hi;
       if (NF > 0) {
+        // two chains sharing the step v = w^2: even bins and odd bins, h = h_e + w h_o.  One
+        // LDS.128 = (X[2k], X[2k+1]) feeds both chains; both FFMA2 of a step read v from the
+        // same register (reuse cache), so each reads at most two registers per bank.
+        float vs_, vc_;
+        sincospif(4.f * frd, &vs_, &vc_);             // v = e^{+j 2 theta_d}, accurate
+        const f2x v = pk(vc_, vs_);
         const float4 *X4 = reinterpret_cast<const float4 *>(X + aa * NF);
-        f2x ha = 0ull, hb = 0ull;                   // chains over bins [H, NF) and [0, H)
+        f2x he = 0ull, ho = 0ull;
 #pragma unroll
-        for (int m = H - 1; m >= 0; --m) {
-          const float4 xv = X4[m];                  // (X[m], X[m + H])
-          const float2 va = upk(ha), vb = upk(hb);
-          const f2x ta = ffma2(w, pk(va.x, va.x), pk(xv.z, xv.w));
-          const f2x tb = ffma2(w, pk(vb.x, vb.x), pk(xv.x, xv.y));
-          const f2x w2 = pk(-zs, zc);
-          ha = ffma2(w2, pk(va.y, va.y), ta);
-          hb = ffma2(w2, pk(vb.y, vb.y), tb);
+        for (int k = H - 1; k >= 0; --k) {
+          const float4 xv = X4[k];                    // (X[2k], X[2k+1])
+          const float2 ve = upk(he), vo = upk(ho);
+          const f2x te = ffma2(v, pk(ve.x, ve.x), pk(xv.x, xv.y));
+          const f2x to = ffma2(v, pk(vo.x, vo.x), pk(xv.z, xv.w));
+          const f2x v2 = pk(-vs_, vc_);
+          he = ffma2(v2, pk(ve.y, ve.y), te);
+          ho = ffma2(v2, pk(vo.y, vo.y), to);
         }
-        // h = h_lo + w^H h_hi, w^H from the fp64 cycle count (accurate, not by powering)
-        float us, uc;
-        sincospif(2.f * frac_cycles(g.L * a.kd * (double)H), &us, &uc);
-        const float2 va = upk(ha), vb = upk(hb);
-        hr = vb.x + (uc * va.x - us * va.y);
-        hi = vb.y + (uc * va.y + us * va.x);
+        const float2 ve = upk(he), vo = upk(ho);
+        hr = ve.x + (zc * vo.x - zs * vo.y);
+        hi = ve.y + (zc * vo.y + zs * vo.x);
       } else {
         const float2 *Xa = X + aa * nf;
         f2x h = 0ull;
@@ -619,16 +648,23 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
 }
 
 template <int MODE, bool MONO, bool CORR>
-static cudaError_t adj_t(const AdjArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
-  // bin counts with a straight-line Horner specialisation (the configs' 64 / 128 / 256 / 512)
-  auto k = a.n_f == 256 ? k_adjoint<MODE, MONO, CORR, 256>
-         : a.n_f == 512 ? k_adjoint<MODE, MONO, CORR, 512>
-         : a.n_f == 128 ? k_adjoint<MODE, MONO, CORR, 128>
-         : a.n_f == 64  ? k_adjoint<MODE, MONO, CORR, 64>
-                        : k_adjoint<MODE, MONO, CORR, 0>;
+static cudaError_t adj_t(const AdjArgs &a, dim3 grid, cudaStream_t st) {
+  // bin counts with a straight-line Horner specialisation (the configs' 64 / 128 / 256 / 512);
+  // the cp.async staging needs 16-byte aligned rows
+  const bool al = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  const int nf = al ? a.n_f : 0;
+  auto k = nf == 256 ? k_adjoint<MODE, MONO, CORR, 256>
+         : nf == 512 ? k_adjoint<MODE, MONO, CORR, 512>
+         : nf == 128 ? k_adjoint<MODE, MONO, CORR, 128>
+         : nf == 64  ? k_adjoint<MODE, MONO, CORR, 64>
+                     : k_adjoint<MODE, MONO, CORR, 0>;
+  const int spec = (nf == 256 || nf == 512 || nf == 128 || nf == 64) ? nf : 0;
+  AdjArgs b = a;
+  b.smem_ant_off = adj_smem_ant_off(a.n_f, spec);
+  const size_t smem = adj_smem_bytes(a.n_f, spec);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, kAdjThreads, smem, st>>>(a);
+  k<<<grid, kAdjThreads, smem, st>>>(b);
   return counted(cudaGetLastError());
 }
 
@@ -636,15 +672,14 @@ cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int
                            cudaStream_t st) {
   const int64_t per_cta = (int64_t)kAdjThreads;
   dim3 grid((unsigned)((a.n_s + per_cta - 1) / per_cta), (unsigned)n_splits);
-  const size_t smem = adj_smem_bytes(a.n_f);
   if (mode == kModeBwd) {
-    if (mono) return corr ? adj_t<kModeBwd, true, true>(a, grid, smem, st)
-                          : adj_t<kModeBwd, true, false>(a, grid, smem, st);
-    return corr ? adj_t<kModeBwd, false, true>(a, grid, smem, st)
-                : adj_t<kModeBwd, false, false>(a, grid, smem, st);
+    if (mono) return corr ? adj_t<kModeBwd, true, true>(a, grid, st)
+                          : adj_t<kModeBwd, true, false>(a, grid, st);
+    return corr ? adj_t<kModeBwd, false, true>(a, grid, st)
+                : adj_t<kModeBwd, false, false>(a, grid, st);
   }
-  return mono ? adj_t<kModeFlt, true, false>(a, grid, smem, st)
-              : adj_t<kModeFlt, false, false>(a, grid, smem, st);
+  return mono ? adj_t<kModeFlt, true, false>(a, grid, st)
+              : adj_t<kModeFlt, false, false>(a, grid, st);
 }
 
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st) {
