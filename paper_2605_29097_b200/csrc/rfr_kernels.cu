@@ -241,24 +241,48 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
 // stays in the operand reuse cache across the chains and each FFMA2 reads at most two registers
 // per bank: the issue interval drops from 3 to 2 cycles (tools/sass_banks.py).  X is staged
 // interleaved, X'[m] = (X[m], X[m + NF/2]), one LDS.128 per step.  NF == 0: rolled single chain.
-template <int MODE, bool MONO, bool CORR, int NF>
-__global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // NF > 0: double-buffered stages of GA antennas, X rows copied with cp.async while the previous
-  // stage computes (one barrier per stage, load latency hidden).  NF == 0: one buffer, kAdjGA.
-  constexpr int GA = NF > 0 ? adj_stage_ants(NF) : kAdjGA;
-  constexpr int NB = NF > 0 ? 2 : 1;
-  const int tid = threadIdx.x;
-  const int nf = NF > 0 ? NF : a.n_f;
-  constexpr int H = NF / 2;
-  float2 *Xb = reinterpret_cast<float2 *>(smem_raw);                     // [NB][GA][nf]
-  AntD *antb = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);      // [NB][GA]
-  const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
-  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
-  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
-  const bool no_gain = a.no_gain;
-  const bool valid = j < a.n_s;
+// ---- mbarrier / bulk-copy (TMA engine) helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  } while (!ok);
+}
+// contiguous global -> shared copy by the bulk-copy (TMA) engine, completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 
+template <bool MONO>
+__device__ __forceinline__ AntD load_ant(const AdjArgs &a, int64_t ia) {
+  AntD d;
+  d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+  if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+  else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+  d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+  d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+  return d;
+}
+
+template <int MODE>
+__device__ __forceinline__ Rec load_point(const AdjArgs &a, int64_t j, bool valid) {
   Rec rec;
   if (MODE == kModeBwd) {
     if (valid) rec = a.rec[j];
@@ -270,119 +294,33 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
     rec.z = valid ? (double)a.qz[j] : 1.0;
     rec.w = 0.f; rec.T = 1.f; rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f;
   }
-  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
-  bool domain = false;
+  return rec;
+}
 
-  // stage the X rows [ga][nf] (contiguous in global memory) and the antennas of [ic, ic + ga)
-  auto stage = [&](int64_t ic, int buf) {
-    const int ga = (int)min((int64_t)GA, i_hi - ic);
-    float2 *X = Xb + (size_t)buf * GA * nf;
-    AntD *ant = antb + buf * GA;
-    if (NF > 0) {
-      const float4 *src = reinterpret_cast<const float4 *>(a.X + ic * NF);
-      for (int c = tid; c < ga * NF / 2; c += kAdjThreads)
-        cp_async16(reinterpret_cast<float4 *>(X) + c, src + c);
-      cp_async_commit();
-    } else {
-      const float2 *src = a.X + ic * nf;
-      for (int t = tid; t < ga * nf; t += kAdjThreads) X[t] = src[t];
-    }
-    for (int aa = tid; aa < ga; aa += kAdjThreads) {
-      const int64_t ia = ic + aa;
-      AntD d;
-      d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
-      if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
-      else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
-      d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
-      d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
-      ant[aa] = d;
-    }
-  };
-
-  const int n_stages = (int)((max(i_hi - i_lo, (int64_t)0) + GA - 1) / GA);
-  if (NF > 0 && n_stages > 0) stage(i_lo, 0);
-  for (int st = 0; st < n_stages; ++st) {
-    const int64_t ic = i_lo + (int64_t)st * GA;
-    const int ga = (int)min((int64_t)GA, i_hi - ic);
-    const int buf = NB == 2 ? (st & 1) : 0;
-    if (NF > 0) {
-      cp_async_wait_all();
-      __syncthreads();                    // stage st visible; every warp is done with stage st-1
-      if (st + 1 < n_stages) stage(ic + GA, buf ^ 1);
-    } else {
-      __syncthreads();
-      stage(ic, 0);
-      __syncthreads();
-    }
-    const float2 *X = Xb + (size_t)buf * GA * nf;
-    const AntD *ant = antb + buf * GA;
-    for (int aa = 0; aa < ga; ++aa) {
-      const AntD an = ant[aa];
-      PairBwd g;
-      pair_geometry<MONO, CORR>(rec, an, no_gain, g);
-      domain |= (MODE == kModeBwd) && valid && !g.ok;
-      const float fr0 = frac_cycles(g.L * a.k0);
-      const float frd = frac_cycles(g.L * a.kd);
-      float es, ec, zs, zc;
-      __sincosf(kTwoPi * fr0, &es, &ec);
-      sincospif(2.f * frd, &zs, &zc);
-      const f2x w = pk(zc, zs);                     // w = e^{+j theta_d}
-      float hr, hi;
-      if (NF > 0) {
-        // two chains sharing the step v = w^2: even bins and odd bins, h = h_e + w h_o.  One
-        // LDS.128 = (X[2k], X[2k+1]) feeds both chains; both FFMA2 of a step read v from the
-        // same register (reuse cache), so each reads at most two registers per bank.
-        float vs_, vc_;
-        sincospif(4.f * frd, &vs_, &vc_);             // v = e^{+j 2 theta_d}, accurate
-        const f2x v = pk(vc_, vs_);
-        const float4 *X4 = reinterpret_cast<const float4 *>(X + aa * NF);
-        f2x he = 0ull, ho = 0ull;
-#pragma unroll
-        for (int k = H - 1; k >= 0; --k) {
-          const float4 xv = X4[k];                    // (X[2k], X[2k+1])
-          const float2 ve = upk(he), vo = upk(ho);
-          const f2x te = ffma2(v, pk(ve.x, ve.x), pk(xv.x, xv.y));
-          const f2x to = ffma2(v, pk(vo.x, vo.x), pk(xv.z, xv.w));
-          const f2x v2 = pk(-vs_, vc_);
-          he = ffma2(v2, pk(ve.y, ve.y), te);
-          ho = ffma2(v2, pk(vo.y, vo.y), to);
-        }
-        const float2 ve = upk(he), vo = upk(ho);
-        hr = ve.x + (zc * vo.x - zs * vo.y);
-        hi = ve.y + (zc * vo.y + zs * vo.x);
-      } else {
-        const float2 *Xa = X + aa * nf;
-        f2x h = 0ull;
-        const f2x w2 = pkv(-zs, zc);
-#pragma unroll 4
-        for (int m = nf - 1; m >= 0; --m) {
-          const float2 xv = Xa[m];
-          const float2 hv = upk(h);
-          const f2x t = ffma2(w, pk(hv.x, hv.x), pk(xv.x, xv.y));
-          h = ffma2(w2, pk(hv.y, hv.y), t);
-        }
-        const float2 hv = upk(h);
-        hr = hv.x;
-        hi = hv.y;
-      }
-      if (MODE == kModeBwd) {
-        const float R = ec * hr - es * hi;          // Re(E h), E = e^{+j theta0}
-        const float TT = g.Tt * g.Tr;
-        const float Rg = R * g.gg;
-        S1 = fmaf(Rg, TT, S1);
-        S2 = fmaf(Rg, g.Tr * g.chit + g.Tt * g.chir, S2);
-        const float Rc = R * g.gamma * TT;
-        S3x = fmaf(Rc, g.dgx, S3x);
-        S3y = fmaf(Rc, g.dgy, S3y);
-        S3z = fmaf(Rc, g.dgz, S3z);
-      } else {                                      // M += E h
-        S1 = fmaf(ec, hr, fmaf(-es, hi, S1));
-        S2 = fmaf(ec, hi, fmaf(es, hr, S2));
-      }
-    }
+// Per-pair epilogue shared by both K3/K4 kernels: R = Re(E h) into the Eq. 5 sums, or M += E h.
+template <int MODE>
+__device__ __forceinline__ void adj_accumulate(const PairBwd &g, float ec, float es, float hr,
+                                               float hi, float &S1, float &S2, float &S3x,
+                                               float &S3y, float &S3z) {
+  if (MODE == kModeBwd) {
+    const float R = ec * hr - es * hi;            // Re(E h), E = e^{+j theta0}
+    const float TT = g.Tt * g.Tr;
+    const float Rg = R * g.gg;
+    S1 = fmaf(Rg, TT, S1);
+    S2 = fmaf(Rg, g.Tr * g.chit + g.Tt * g.chir, S2);
+    const float Rc = R * g.gamma * TT;
+    S3x = fmaf(Rc, g.dgx, S3x);
+    S3y = fmaf(Rc, g.dgy, S3y);
+    S3z = fmaf(Rc, g.dgz, S3z);
+  } else {                                        // M += E h
+    S1 = fmaf(ec, hr, fmaf(-es, hi, S1));
+    S2 = fmaf(ec, hi, fmaf(es, hr, S2));
   }
-  if (domain) atomicOr(a.flags, 1u);
-  if (!valid) return;
+}
+
+template <int MODE>
+__device__ __forceinline__ void adj_store(const AdjArgs &a, int64_t j, float S1, float S2,
+                                          float S3x, float S3y, float S3z) {
   if (MODE == kModeBwd) {
     float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
     P[j] = S1;
@@ -394,6 +332,156 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
     float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
     M[j] = make_float2(S1, S2);
   }
+}
+
+// Specialised bin count NF (64/128/256/512).  Warps 0..3 are consumers (one sample or query per
+// thread); warp 4 is the producer: its lane 0 streams the X rows of the split, kAdjRowsStage
+// antennas per stage, through a kAdjStages-deep shared-memory ring with the bulk-copy (TMA)
+// engine, signalled by "full" mbarriers (transaction bytes) and released by "empty" mbarriers
+// (one arrive per consumer warp).  No CTA-wide barrier on the hot path: a consumer warp waits
+// only for the bytes it needs, so warps that drift apart are absorbed by the ring.
+// Horner: two chains per sample stepping by v = w^2 over the even and odd bins, h = h_e + w h_o;
+// one LDS.128 = (X[2k], X[2k+1]) feeds both, and both FFMA2 of a step read v from one register
+// (operand reuse cache), so each FFMA2 reads at most two registers per bank.
+template <int MODE, bool MONO, bool CORR, int NF>
+__global__ void __launch_bounds__(kAdjThreads + 32, 5) k_adjoint_tma(AdjArgs a) {
+  constexpr int GA = adj_stage_ants(NF);
+  constexpr int NS = kAdjStages;
+  constexpr int H = NF / 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2 *Xs = reinterpret_cast<float2 *>(smem_raw);                          // [NS][GA][NF]
+  unsigned long long *full = reinterpret_cast<unsigned long long *>(
+      smem_raw + (size_t)NS * GA * NF * sizeof(float2));
+  unsigned long long *empty = full + NS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  const int n_stages = (int)((max(i_hi - i_lo, (int64_t)0) + GA - 1) / GA);
+  if (tid == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kAdjThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kAdjThreads / 32) {                 // ------------------------------ producer
+    if (lane == 0) {
+      for (int st = 0; st < n_stages; ++st) {
+        const int b = st % NS;
+        if (st >= NS) mbar_wait(&empty[b], ((st / NS) - 1) & 1);
+        const int64_t ic = i_lo + (int64_t)st * GA;
+        const int ga = (int)min((int64_t)GA, i_hi - ic);
+        const unsigned bytes = (unsigned)(ga * NF * sizeof(float2));
+        mbar_arrive_expect_tx(&full[b], bytes);
+        bulk_g2s(Xs + (size_t)b * GA * NF, a.X + ic * NF, bytes, &full[b]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------------------ consumers
+  const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
+  const bool valid = j < a.n_s;
+  const Rec rec = load_point<MODE>(a, j, valid);
+  const bool no_gain = a.no_gain;
+  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
+  bool domain = false;
+  AntD an_next = n_stages > 0 ? load_ant<MONO>(a, i_lo) : AntD();
+  for (int st = 0; st < n_stages; ++st) {
+    const int b = st % NS;
+    const int64_t ic = i_lo + (int64_t)st * GA;
+    const int ga = (int)min((int64_t)GA, i_hi - ic);
+    mbar_wait(&full[b], (st / NS) & 1);
+    const float2 *X = Xs + (size_t)b * GA * NF;
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = an_next;
+      if (ic + aa + 1 < i_hi) an_next = load_ant<MONO>(a, ic + aa + 1);   // prefetch
+      PairBwd g;
+      pair_geometry<MONO, CORR>(rec, an, no_gain, g);
+      domain |= (MODE == kModeBwd) && valid && !g.ok;
+      const float fr0 = frac_cycles(g.L * a.k0);
+      const float frd = frac_cycles(g.L * a.kd);
+      float es, ec, zs, zc, vs_, vc_;
+      __sincosf(kTwoPi * fr0, &es, &ec);
+      sincospif(2.f * frd, &zs, &zc);             // w = e^{+j theta_d}
+      sincospif(4.f * frd, &vs_, &vc_);           // v = w^2, accurate
+      const f2x v = pk(vc_, vs_);
+      const float4 *X4 = reinterpret_cast<const float4 *>(X + aa * NF);
+      f2x he = 0ull, ho = 0ull;
+#pragma unroll
+      for (int k = H - 1; k >= 0; --k) {
+        const float4 xv = X4[k];                  // (X[2k], X[2k+1])
+        const float2 ve = upk(he), vo = upk(ho);
+        const f2x te = ffma2(v, pk(ve.x, ve.x), pk(xv.x, xv.y));
+        const f2x to = ffma2(v, pk(vo.x, vo.x), pk(xv.z, xv.w));
+        const f2x v2 = pk(-vs_, vc_);
+        he = ffma2(v2, pk(ve.y, ve.y), te);
+        ho = ffma2(v2, pk(vo.y, vo.y), to);
+      }
+      const float2 ve = upk(he), vo = upk(ho);
+      const float hr = ve.x + (zc * vo.x - zs * vo.y);
+      const float hi = ve.y + (zc * vo.y + zs * vo.x);
+      adj_accumulate<MODE>(g, ec, es, hr, hi, S1, S2, S3x, S3y, S3z);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);       // this warp is done with buffer b
+  }
+  if (domain) atomicOr(a.flags, 1u);
+  if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
+}
+
+// Generic bin count (or unaligned rows): one buffer of kAdjGA antennas, CTA barriers, rolled Horner.
+template <int MODE, bool MONO, bool CORR>
+__global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
+  AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
+  const int tid = threadIdx.x;
+  const int nf = a.n_f;
+  const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  const bool no_gain = a.no_gain;
+  const bool valid = j < a.n_s;
+  const Rec rec = load_point<MODE>(a, j, valid);
+  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
+  bool domain = false;
+  for (int64_t ic = i_lo; ic < i_hi; ic += kAdjGA) {
+    const int ga = (int)min((int64_t)kAdjGA, i_hi - ic);
+    __syncthreads();
+    const float2 *src = a.X + ic * nf;
+    for (int t = tid; t < ga * nf; t += kAdjThreads) X[t] = src[t];
+    for (int aa = tid; aa < ga; aa += kAdjThreads) ant[aa] = load_ant<MONO>(a, ic + aa);
+    __syncthreads();
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = ant[aa];
+      PairBwd g;
+      pair_geometry<MONO, CORR>(rec, an, no_gain, g);
+      domain |= (MODE == kModeBwd) && valid && !g.ok;
+      const float fr0 = frac_cycles(g.L * a.k0);
+      const float frd = frac_cycles(g.L * a.kd);
+      float es, ec, zs, zc;
+      __sincosf(kTwoPi * fr0, &es, &ec);
+      sincospif(2.f * frd, &zs, &zc);
+      const f2x w = pk(zc, zs);                   // w = e^{+j theta_d}
+      const f2x w2 = pkv(-zs, zc);
+      const float2 *Xa = X + aa * nf;
+      f2x h = 0ull;
+#pragma unroll 4
+      for (int m = nf - 1; m >= 0; --m) {
+        const float2 xv = Xa[m];
+        const float2 hv = upk(h);
+        const f2x t = ffma2(w, pk(hv.x, hv.x), pk(xv.x, xv.y));
+        h = ffma2(w2, pk(hv.y, hv.y), t);
+      }
+      const float2 hv = upk(h);
+      adj_accumulate<MODE>(g, ec, es, hv.x, hv.y, S1, S2, S3x, S3y, S3z);
+    }
+  }
+  if (domain) atomicOr(a.flags, 1u);
+  if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
 }
 
 // ================================================================================== K1' backward
@@ -649,19 +737,25 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
 
 template <int MODE, bool MONO, bool CORR>
 static cudaError_t adj_t(const AdjArgs &a, dim3 grid, cudaStream_t st) {
-  // bin counts with a straight-line Horner specialisation (the configs' 64 / 128 / 256 / 512);
-  // the cp.async staging needs 16-byte aligned rows
+  // bin counts with the TMA-ring / straight-line Horner specialisation (the configs' 64 / 128 /
+  // 256 / 512); the bulk copies need 16-byte aligned rows
   const bool al = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
   const int nf = al ? a.n_f : 0;
-  auto k = nf == 256 ? k_adjoint<MODE, MONO, CORR, 256>
-         : nf == 512 ? k_adjoint<MODE, MONO, CORR, 512>
-         : nf == 128 ? k_adjoint<MODE, MONO, CORR, 128>
-         : nf == 64  ? k_adjoint<MODE, MONO, CORR, 64>
-                     : k_adjoint<MODE, MONO, CORR, 0>;
-  const int spec = (nf == 256 || nf == 512 || nf == 128 || nf == 64) ? nf : 0;
+  if (nf == 256 || nf == 512 || nf == 128 || nf == 64) {
+    auto k = nf == 256 ? k_adjoint_tma<MODE, MONO, CORR, 256>
+           : nf == 512 ? k_adjoint_tma<MODE, MONO, CORR, 512>
+           : nf == 128 ? k_adjoint_tma<MODE, MONO, CORR, 128>
+                       : k_adjoint_tma<MODE, MONO, CORR, 64>;
+    const size_t smem = adj_tma_smem_bytes(nf);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kAdjThreads + 32, smem, st>>>(a);
+    return counted(cudaGetLastError());
+  }
+  auto k = k_adjoint<MODE, MONO, CORR>;
   AdjArgs b = a;
-  b.smem_ant_off = adj_smem_ant_off(a.n_f, spec);
-  const size_t smem = adj_smem_bytes(a.n_f, spec);
+  b.smem_ant_off = adj_smem_ant_off(a.n_f);
+  const size_t smem = adj_smem_bytes(a.n_f);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, kAdjThreads, smem, st>>>(b);

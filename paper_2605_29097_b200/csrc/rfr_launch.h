@@ -78,19 +78,18 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline size_t fwd_warp_smem() {
   return align_up((size_t)kFwdTJ * 32 * 20 + 32 * 56 + 2 * kFwdTJ * 48, 128);
 }
-// K3/K4 staging: specialised bin counts (spec > 0) use two buffers of adj_stage_ants(spec)
-// antennas (16 KB of X rows each); the generic kernel (spec == 0) one buffer of kAdjGA.
+// K3/K4 staging.  TMA-ring kernel (specialised bin counts): kAdjStages buffers of
+// adj_stage_ants(nf) antennas (8 KB of X rows each) + 2 mbarriers per stage.  Generic kernel:
+// one buffer of kAdjGA antennas + their AntD records.
+constexpr int kAdjStages = 4;
 __host__ __device__ constexpr int adj_stage_ants(int nf) {
-  return nf > 0 ? (16384 / (nf * 8) > 0 ? 16384 / (nf * 8) : 1) : kAdjGA;
+  return 8192 / (nf * 8) > 0 ? 8192 / (nf * 8) : 1;
 }
-inline size_t adj_smem_ant_off(int n_f, int spec) {
-  const int ga = adj_stage_ants(spec), nb = spec > 0 ? 2 : 1;
-  return align_up((size_t)nb * ga * n_f * 8, 16);
+inline size_t adj_tma_smem_bytes(int nf) {
+  return (size_t)kAdjStages * adj_stage_ants(nf) * nf * 8 + 2 * kAdjStages * 8;
 }
-inline size_t adj_smem_bytes(int n_f, int spec) {
-  const int ga = adj_stage_ants(spec), nb = spec > 0 ? 2 : 1;
-  return adj_smem_ant_off(n_f, spec) + (size_t)nb * ga * 56;
-}
+inline size_t adj_smem_ant_off(int n_f) { return align_up((size_t)kAdjGA * n_f * 8, 16); }
+inline size_t adj_smem_bytes(int n_f) { return adj_smem_ant_off(n_f) + (size_t)kAdjGA * 56; }
 
 unsigned long long launch_count();
 cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st);
