@@ -255,12 +255,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit instead of
+// spinning on issue slots (the producer waits most of the time once the ring is full)
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
   const unsigned a = smem_u32(bar);
   unsigned ok = 0;
   do {
-    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
   } while (!ok);
 }
 // contiguous global -> shared copy by the bulk-copy (TMA) engine, completing on `bar`
@@ -344,11 +346,11 @@ __device__ __forceinline__ void adj_store(const AdjArgs &a, int64_t j, float S1,
 // one LDS.128 = (X[2k], X[2k+1]) feeds both, and both FFMA2 of a step read v from one register
 // (operand reuse cache), so each FFMA2 reads at most two registers per bank.
 template <int MODE, bool MONO, bool CORR, int NF>
-__global__ void __launch_bounds__(kAdjThreads + 32, 5) k_adjoint_tma(AdjArgs a) {
+__global__ void __launch_bounds__(kAdjThreads + 32, 4) k_adjoint_tma(AdjArgs a) {
   constexpr int GA = adj_stage_ants(NF);
   constexpr int NS = kAdjStages;
   constexpr int H = NF / 2;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   float2 *Xs = reinterpret_cast<float2 *>(smem_raw);                          // [NS][GA][NF]
   unsigned long long *full = reinterpret_cast<unsigned long long *>(
       smem_raw + (size_t)NS * GA * NF * sizeof(float2));
@@ -388,7 +390,9 @@ __global__ void __launch_bounds__(kAdjThreads + 32, 5) k_adjoint_tma(AdjArgs a) 
   const bool no_gain = a.no_gain;
   float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
   bool domain = false;
-  AntD an_next = n_stages > 0 ? load_ant<MONO>(a, i_lo) : AntD();
+  // antenna coordinates prefetched one pair ahead (floats; widened to fp64 at use)
+  float nx_ = 0.f, ny_ = 0.f, nz_ = 0.f;
+  if (n_stages > 0) { nx_ = a.tx_x[i_lo]; ny_ = a.tx_y[i_lo]; nz_ = a.tx_z[i_lo]; }
   for (int st = 0; st < n_stages; ++st) {
     const int b = st % NS;
     const int64_t ic = i_lo + (int64_t)st * GA;
@@ -396,8 +400,17 @@ __global__ void __launch_bounds__(kAdjThreads + 32, 5) k_adjoint_tma(AdjArgs a) 
     mbar_wait(&full[b], (st / NS) & 1);
     const float2 *X = Xs + (size_t)b * GA * NF;
     for (int aa = 0; aa < ga; ++aa) {
-      const AntD an = an_next;
-      if (ic + aa + 1 < i_hi) an_next = load_ant<MONO>(a, ic + aa + 1);   // prefetch
+      AntD an;
+      if (MONO && !a.phi_tx) {
+        an.x = nx_; an.y = ny_; an.z = nz_;
+        an.rx = an.x; an.ry = an.y; an.rz = an.z;
+        an.ptx = an.prx = 1.f;
+      } else {
+        an = load_ant<MONO>(a, ic + aa);
+      }
+      if (ic + aa + 1 < i_hi) {                   // prefetch the next antenna
+        nx_ = a.tx_x[ic + aa + 1]; ny_ = a.tx_y[ic + aa + 1]; nz_ = a.tx_z[ic + aa + 1];
+      }
       PairBwd g;
       pair_geometry<MONO, CORR>(rec, an, no_gain, g);
       domain |= (MODE == kModeBwd) && valid && !g.ok;
