@@ -445,6 +445,141 @@ __global__ void __launch_bounds__(kAdjThreads + 32, 4) k_adjoint_tma(AdjArgs a) 
   if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
 }
 
+// Backward (K3) at specialised bin counts: two samples per thread share every X load (LDS.64
+// broadcast, half the shared-memory wavefronts of the one-sample kernels), single Horner chain per
+// sample in straight-line code, one CTA barrier per stage of kAdjGA antennas.  Measured faster
+// than the TMA-ring kernel for the backward, whose heavier per-pair epilogue (Eq. 5 gradient
+// sums) favours sharing the stage across two samples.
+template <int MODE, bool MONO, bool CORR, int NF>
+__global__ void __launch_bounds__(kAdjThreads) k_adjoint_s2(AdjArgs a) {
+  constexpr int SPT = 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
+  AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
+  const int tid = threadIdx.x;
+  constexpr int nf = NF;
+  const int64_t base = (int64_t)blockIdx.x * (kAdjThreads * SPT);
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  const bool no_gain = a.no_gain;
+
+  Rec rec[SPT];
+  bool valid[SPT];
+  float S1[SPT], S2[SPT], S3x[SPT], S3y[SPT], S3z[SPT];
+#pragma unroll
+  for (int s = 0; s < SPT; ++s) {
+    const int64_t j = base + s * kAdjThreads + tid;
+    valid[s] = j < a.n_s;
+    if (MODE == kModeBwd) {
+      if (valid[s]) rec[s] = a.rec[j];
+      else { rec[s].x = rec[s].y = 0.0; rec[s].z = 1.0; rec[s].w = 0.f; rec[s].T = 0.f;
+             rec[s].nx = rec[s].ny = 0.f; rec[s].nz = 1.f; rec[s].papr = 1.f; }
+    } else {
+      rec[s].x = valid[s] ? (double)a.qx[j] : 0.0;
+      rec[s].y = valid[s] ? (double)a.qy[j] : 0.0;
+      rec[s].z = valid[s] ? (double)a.qz[j] : 1.0;
+      rec[s].w = 0.f; rec[s].T = 1.f; rec[s].nx = rec[s].ny = 0.f; rec[s].nz = 1.f;
+      rec[s].papr = 1.f;
+    }
+    S1[s] = S2[s] = S3x[s] = S3y[s] = S3z[s] = 0.f;
+  }
+  bool domain = false;
+
+  for (int64_t ic = i_lo; ic < i_hi; ic += kAdjGA) {
+    const int ga = (int)min((int64_t)kAdjGA, i_hi - ic);
+    __syncthreads();
+    {   // stage X rows [ga][nf] (contiguous in global memory) and the antennas
+      const float2 *src = a.X + ic * nf;
+      const int n2 = ga * nf;
+      for (int t = tid; t < n2; t += kAdjThreads) X[t] = src[t];
+      for (int aa = tid; aa < ga; aa += kAdjThreads) {
+        const int64_t ia = ic + aa;
+        AntD d;
+        d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+        if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+        else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+        d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+        d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+        ant[aa] = d;
+      }
+    }
+    __syncthreads();
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = ant[aa];   // (staged per stage, broadcast)
+      PairBwd g[SPT];
+      f2x w1[SPT], w2[SPT], h[SPT];
+      float Er[SPT], Ei[SPT];
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        pair_geometry<MONO, CORR>(rec[s], an, no_gain, g[s]);
+        domain |= (MODE == kModeBwd) && valid[s] && !g[s].ok;
+        const float fr0 = frac_cycles(g[s].L * a.k0);
+        const float frd = frac_cycles(g[s].L * a.kd);
+        float es, ec, zs, zc;
+        __sincosf(kTwoPi * fr0, &es, &ec);
+        sincospif(2.f * frd, &zs, &zc);
+        Er[s] = ec; Ei[s] = es;                    // E = e^{+j theta0}
+        w1[s] = pkv(zc, zs);                       // w = e^{+j theta_d}
+        w2[s] = pkv(-zs, zc);                      // (opaque: keeps ptxas from re-deriving it in the loop)
+        h[s] = 0ull;
+      }
+      const float2 *Xa = X + aa * nf;
+      // Horner from the top bin down: h = h w + X_m  (2 FFMA2 per complex step).  With NF > 0
+      // the bin loop is straight-line code (no loop-carried register renames: in a rolled loop
+      // ptxas spent ~25% extra FMA-pipe slots on IMAD.MOV / re-derived w2 at every back edge).
+      {
+#pragma unroll
+        for (int m = NF - 1; m >= 0; --m) {
+          const float2 xv = Xa[m];
+          const f2x xm = pk(xv.x, xv.y);
+#pragma unroll
+          for (int s = 0; s < SPT; ++s) {
+            const float2 hv = upk(h[s]);
+            const f2x t = ffma2(pk(hv.x, hv.x), w1[s], xm);
+            h[s] = ffma2(pk(hv.y, hv.y), w2[s], t);
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < SPT; ++s) {
+        const float2 hv = upk(h[s]);
+        if (MODE == kModeBwd) {
+          const float R = Er[s] * hv.x - Ei[s] * hv.y;      // Re(E h)
+          const float TT = g[s].Tt * g[s].Tr;
+          const float Rg = R * g[s].gg;
+          S1[s] = fmaf(Rg, TT, S1[s]);
+          S2[s] = fmaf(Rg, g[s].Tr * g[s].chit + g[s].Tt * g[s].chir, S2[s]);
+          const float Rc = R * g[s].gamma * TT;
+          S3x[s] = fmaf(Rc, g[s].dgx, S3x[s]);
+          S3y[s] = fmaf(Rc, g[s].dgy, S3y[s]);
+          S3z[s] = fmaf(Rc, g[s].dgz, S3z[s]);
+        } else {
+          // M += E h
+          S1[s] = fmaf(Er[s], hv.x, fmaf(-Ei[s], hv.y, S1[s]));
+          S2[s] = fmaf(Er[s], hv.y, fmaf(Ei[s], hv.x, S2[s]));
+        }
+      }
+    }
+  }
+  if (domain) atomicOr(a.flags, 1u);
+#pragma unroll
+  for (int s = 0; s < SPT; ++s) {
+    const int64_t j = base + s * kAdjThreads + tid;
+    if (!valid[s]) continue;
+    if (MODE == kModeBwd) {
+      float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
+      P[j] = S1[s];
+      P[a.n_s + j] = S2[s];
+      P[2 * a.n_s + j] = S3x[s];
+      P[3 * a.n_s + j] = S3y[s];
+      P[4 * a.n_s + j] = S3z[s];
+    } else {
+      float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
+      M[j] = make_float2(S1[s], S2[s]);
+    }
+  }
+}
+
 // Generic bin count (or unaligned rows): one buffer of kAdjGA antennas, CTA barriers, rolled Horner.
 template <int MODE, bool MONO, bool CORR>
 __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
@@ -754,6 +889,21 @@ static cudaError_t adj_t(const AdjArgs &a, dim3 grid, cudaStream_t st) {
   // 256 / 512); the bulk copies need 16-byte aligned rows
   const bool al = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
   const int nf = al ? a.n_f : 0;
+  const bool spec = a.n_f == 256 || a.n_f == 512 || a.n_f == 128 || a.n_f == 64;
+  if (MODE == kModeBwd && spec) {
+    auto k = a.n_f == 256 ? k_adjoint_s2<MODE, MONO, CORR, 256>
+           : a.n_f == 512 ? k_adjoint_s2<MODE, MONO, CORR, 512>
+           : a.n_f == 128 ? k_adjoint_s2<MODE, MONO, CORR, 128>
+                          : k_adjoint_s2<MODE, MONO, CORR, 64>;
+    AdjArgs b = a;
+    b.smem_ant_off = adj_smem_ant_off(a.n_f);
+    const size_t smem = adj_smem_bytes(a.n_f);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 g2((unsigned)((a.n_s + 2 * kAdjThreads - 1) / (2 * kAdjThreads)), grid.y);
+    k<<<g2, kAdjThreads, smem, st>>>(b);
+    return counted(cudaGetLastError());
+  }
   if (nf == 256 || nf == 512 || nf == 128 || nf == 64) {
     auto k = nf == 256 ? k_adjoint_tma<MODE, MONO, CORR, 256>
            : nf == 512 ? k_adjoint_tma<MODE, MONO, CORR, 512>
