@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "rfr_launch.h"
+
 namespace rfr {
 
 // ------------------------------------------------------------------------------ packed f32x2
@@ -191,6 +193,112 @@ __device__ __forceinline__ void pair_geometry(const Rec &r, const AntD &a, bool 
     o.chit = o.chir = chi;
   }
   if (!o.ok) { o.gg = 0.f; o.gamma = 0.f; }
+}
+
+// ------------------------------------------------------------------------------ async copies
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+
+// ---- mbarrier / bulk-copy (TMA engine) helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit instead of
+// spinning on issue slots (the producer waits most of the time once the ring is full)
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
+  } while (!ok);
+}
+// contiguous global -> shared copy by the bulk-copy (TMA) engine, completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+
+// ------------------------------------------------------------------------------ K3/K4 shared pieces
+template <bool MONO>
+__device__ __forceinline__ AntD load_ant(const AdjArgs &a, int64_t ia) {
+  AntD d;
+  d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+  if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+  else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+  d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+  d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+  return d;
+}
+
+template <int MODE>
+__device__ __forceinline__ Rec load_point(const AdjArgs &a, int64_t j, bool valid) {
+  Rec rec;
+  if (MODE == kModeBwd) {
+    if (valid) rec = a.rec[j];
+    else { rec.x = rec.y = 0.0; rec.z = 1.0; rec.w = 0.f; rec.T = 0.f;
+           rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f; }
+  } else {
+    rec.x = valid ? (double)a.qx[j] : 0.0;
+    rec.y = valid ? (double)a.qy[j] : 0.0;
+    rec.z = valid ? (double)a.qz[j] : 1.0;
+    rec.w = 0.f; rec.T = 1.f; rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f;
+  }
+  return rec;
+}
+
+// Per-pair epilogue shared by both K3/K4 kernels: R = Re(E h) into the Eq. 5 sums, or M += E h.
+template <int MODE>
+__device__ __forceinline__ void adj_accumulate(const PairBwd &g, float ec, float es, float hr,
+                                               float hi, float &S1, float &S2, float &S3x,
+                                               float &S3y, float &S3z) {
+  if (MODE == kModeBwd) {
+    const float R = ec * hr - es * hi;            // Re(E h), E = e^{+j theta0}
+    const float TT = g.Tt * g.Tr;
+    const float Rg = R * g.gg;
+    S1 = fmaf(Rg, TT, S1);
+    S2 = fmaf(Rg, g.Tr * g.chit + g.Tt * g.chir, S2);
+    const float Rc = R * g.gamma * TT;
+    S3x = fmaf(Rc, g.dgx, S3x);
+    S3y = fmaf(Rc, g.dgy, S3y);
+    S3z = fmaf(Rc, g.dgz, S3z);
+  } else {                                        // M += E h
+    S1 = fmaf(ec, hr, fmaf(-es, hi, S1));
+    S2 = fmaf(ec, hi, fmaf(es, hr, S2));
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void adj_store(const AdjArgs &a, int64_t j, float S1, float S2,
+                                          float S3x, float S3y, float S3z) {
+  if (MODE == kModeBwd) {
+    float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
+    P[j] = S1;
+    P[a.n_s + j] = S2;
+    P[2 * a.n_s + j] = S3x;
+    P[3 * a.n_s + j] = S3y;
+    P[4 * a.n_s + j] = S3z;
+  } else {
+    float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
+    M[j] = make_float2(S1, S2);
+  }
 }
 
 }  // namespace rfr

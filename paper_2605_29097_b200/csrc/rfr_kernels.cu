@@ -14,6 +14,8 @@
 #include "rfr_launch.h"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace rfr {
 
@@ -73,13 +75,6 @@ __global__ void k_blend(BlendArgs a) {
 // k_mf_adj_pack as {x, y, z, w = Re c_q, T = Im c_q} with c_q = (dL/dP_q) M_q / max(P_q, eps); the
 // per-pair amplitude is the complex c_q itself (no gain, decay or transmittance), so the kernel
 // computes dL/ds(i,m) = sum_q c_q e^{-j 2 pi f_m tau_iq} with the same anchors and recurrence.
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 template <int B, bool MONO, bool CORR, int KIND>
 __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -241,101 +236,6 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
 // stays in the operand reuse cache across the chains and each FFMA2 reads at most two registers
 // per bank: the issue interval drops from 3 to 2 cycles (tools/sass_banks.py).  X is staged
 // interleaved, X'[m] = (X[m], X[m + NF/2]), one LDS.128 per step.  NF == 0: rolled single chain.
-// ---- mbarrier / bulk-copy (TMA engine) helpers
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes) : "memory");
-}
-// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit instead of
-// spinning on issue slots (the producer waits most of the time once the ring is full)
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-  const unsigned a = smem_u32(bar);
-  unsigned ok = 0;
-  do {
-    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
-  } while (!ok);
-}
-// contiguous global -> shared copy by the bulk-copy (TMA) engine, completing on `bar`
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
-                                         unsigned long long *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
-template <bool MONO>
-__device__ __forceinline__ AntD load_ant(const AdjArgs &a, int64_t ia) {
-  AntD d;
-  d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
-  if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
-  else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
-  d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
-  d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
-  return d;
-}
-
-template <int MODE>
-__device__ __forceinline__ Rec load_point(const AdjArgs &a, int64_t j, bool valid) {
-  Rec rec;
-  if (MODE == kModeBwd) {
-    if (valid) rec = a.rec[j];
-    else { rec.x = rec.y = 0.0; rec.z = 1.0; rec.w = 0.f; rec.T = 0.f;
-           rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f; }
-  } else {
-    rec.x = valid ? (double)a.qx[j] : 0.0;
-    rec.y = valid ? (double)a.qy[j] : 0.0;
-    rec.z = valid ? (double)a.qz[j] : 1.0;
-    rec.w = 0.f; rec.T = 1.f; rec.nx = rec.ny = 0.f; rec.nz = 1.f; rec.papr = 1.f;
-  }
-  return rec;
-}
-
-// Per-pair epilogue shared by both K3/K4 kernels: R = Re(E h) into the Eq. 5 sums, or M += E h.
-template <int MODE>
-__device__ __forceinline__ void adj_accumulate(const PairBwd &g, float ec, float es, float hr,
-                                               float hi, float &S1, float &S2, float &S3x,
-                                               float &S3y, float &S3z) {
-  if (MODE == kModeBwd) {
-    const float R = ec * hr - es * hi;            // Re(E h), E = e^{+j theta0}
-    const float TT = g.Tt * g.Tr;
-    const float Rg = R * g.gg;
-    S1 = fmaf(Rg, TT, S1);
-    S2 = fmaf(Rg, g.Tr * g.chit + g.Tt * g.chir, S2);
-    const float Rc = R * g.gamma * TT;
-    S3x = fmaf(Rc, g.dgx, S3x);
-    S3y = fmaf(Rc, g.dgy, S3y);
-    S3z = fmaf(Rc, g.dgz, S3z);
-  } else {                                        // M += E h
-    S1 = fmaf(ec, hr, fmaf(-es, hi, S1));
-    S2 = fmaf(ec, hi, fmaf(es, hr, S2));
-  }
-}
-
-template <int MODE>
-__device__ __forceinline__ void adj_store(const AdjArgs &a, int64_t j, float S1, float S2,
-                                          float S3x, float S3y, float S3z) {
-  if (MODE == kModeBwd) {
-    float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
-    P[j] = S1;
-    P[a.n_s + j] = S2;
-    P[2 * a.n_s + j] = S3x;
-    P[3 * a.n_s + j] = S3y;
-    P[4 * a.n_s + j] = S3z;
-  } else {
-    float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
-    M[j] = make_float2(S1, S2);
-  }
-}
-
 // Specialised bin count NF (64/128/256/512).  Warps 0..3 are consumers (one sample or query per
 // thread); warp 4 is the producer: its lane 0 streams the X rows of the split, kAdjRowsStage
 // antennas per stage, through a kAdjStages-deep shared-memory ring with the bulk-copy (TMA)
@@ -925,8 +825,22 @@ static cudaError_t adj_t(const AdjArgs &a, dim3 grid, cudaStream_t st) {
   return counted(cudaGetLastError());
 }
 
+// K3/K4 implementation: tensor-core factorisation (rfr_tc.cu) where the bin count allows, else
+// SIMT.  RFR_ADJOINT=simt forces the SIMT kernels (A/B measurements).
+static bool use_tensor_cores() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RFR_ADJOINT");
+    v = (e && strcmp(e, "simt") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st) {
+  if (use_tensor_cores() && adjoint_tc_supported(a.n_f) &&
+      (reinterpret_cast<uintptr_t>(a.X) & 7) == 0)
+    return counted(launch_adjoint_tc(a, mode, mono, corr, n_splits, st));
   const int64_t per_cta = (int64_t)kAdjThreads;
   dim3 grid((unsigned)((a.n_s + per_cta - 1) / per_cta), (unsigned)n_splits);
   if (mode == kModeBwd) {

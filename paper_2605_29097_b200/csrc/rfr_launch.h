@@ -103,6 +103,9 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
                              int tmp_n, float *loss, cudaStream_t st);
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st);
+bool adjoint_tc_supported(int n_f);
+cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
+                              cudaStream_t st);
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st);
 cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, int n_sm,
                               cudaStream_t st);

@@ -1,0 +1,299 @@
+// rfr_tc.cu -- tensor-core (tcgen05 / TMEM) form of the adjoint sums K3 (backward) and K4 (filter).
+//
+// Both compute, per (sample or query j, antenna i), the bin sum
+//     h_ij = sum_{m < NF} X_i[m] w_ij^m,   w_ij = e^{+j 2 pi df tau_ij}
+// (X = G for K3, X = s for K4; App. A.5, Eq. 3).  With m = 16 m1 + m0 it
+// factorises EXACTLY (no approximation) into a dense complex contraction over m0 followed by a
+// short Horner sum over m1:
+//     U_ij[m1] = sum_{m0 < 16} X_i[16 m1 + m0] w_ij^{m0},      h_ij = sum_{m1} (w_ij^16)^{m1} U_ij[m1].
+// For a fixed antenna i the first step is a real GEMM D = A B^T over a tile of 128 samples:
+//     A[j][k]   : k < 16 -> Re w^k,  16 <= k < 32 -> Im w^(k-16)                   (M = 128, K = 32)
+//     B^T[n][k] : n < P -> (Re X, -Im X) of bins 16 n + k,  P <= n < 2P -> (Im X, Re X)   (N = 2P)
+//     D[j][n]   : n < P -> Re U[n],  n >= P -> Im U[n - P]                           (P = NF / 16)
+// run on the 5th-generation tensor cores as tcgen05.mma.kind::tf32 with A in tensor memory (each
+// thread writes its own row with tcgen05.st), B in shared memory (K-major, no swizzle) and D in
+// tensor memory.  fp32 accuracy comes from the 3xTF32 split (A_hi B_hi + A_hi B_lo + A_lo B_hi,
+// hi = round-to-tf32, lo = x - hi): measured 7e-7 relative against fp64 on random operands
+// (tools/microbench/umma_tf32_probe.cu).  The per-pair SIMT work (fp64 geometry, the 16 powers of w,
+// the Horner over m1, the Eq. 5 epilogue) overlaps the MMAs of the previous antenna: A is single-
+// buffered (the MMA of antenna a-1 is awaited after the SIMT part of antenna a), D is double-
+// buffered in tensor memory.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rfr_device.cuh"
+#include "rfr_launch.h"
+
+namespace rfr {
+
+namespace {
+
+// shared-memory matrix descriptor: K-major, SWIZZLE_NONE canonical layout, Blackwell version 1
+__device__ __forceinline__ uint64_t umma_sdesc(unsigned saddr, unsigned lbo, unsigned sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// byte offset of element (row n, column k) of a K-major interleaved operand with 32 columns:
+// 16-byte chunks of 4 columns; 8 rows x 16 B core matrices; chunk stride 128 B, row-group 1024 B
+__device__ __forceinline__ unsigned bT_off(int n, int k) {
+  return (unsigned)((k >> 2) * 128 + (n >> 3) * 1024 + (n & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void tmem_st32(unsigned addr, const unsigned (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(unsigned addr, unsigned (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]^T, one K step of 8 tf32 columns
+__device__ __forceinline__ void umma_tf32_ts(unsigned d_tmem, unsigned a_tmem, uint64_t b_desc,
+                                             unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred pa;\n setp.ne.b32 pa, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, pa;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// per-pair state carried from the SIMT part of antenna a to its epilogue
+struct PairTC {
+  PairBwd g;
+  float ec, es;     // E = e^{+j 2 pi f0 tau}
+  float Wc, Ws;     // W = w^16
+};
+
+}  // namespace
+
+template <int NF>
+struct TCShape {
+  static constexpr int P = NF / 16;                  // m1 values
+  static constexpr int N = 2 * P;                    // D columns
+  static constexpr int COLS = 64 + 2 * N;            // A_hi, A_lo (32 each) + 2 D buffers
+  static constexpr int ALLOC = COLS <= 128 ? 128 : 256;
+  static constexpr int MINB = ALLOC == 128 ? 4 : 2;  // CTAs per SM (512 TMEM columns)
+};
+
+template <int MODE, bool MONO, bool CORR, int NF>
+__global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(AdjArgs a) {
+  using S = TCShape<NF>;
+  constexpr int P = S::P, N = S::N;
+  static_assert(kAdjThreads == 128, "one TMEM lane per thread");
+  __shared__ __align__(128) unsigned char bsm[2 * N * 128];          // B_hi, B_lo [N][32] fp32
+  __shared__ __align__(8) unsigned long long mma_bar;
+  __shared__ unsigned tmem_base_sh;
+  unsigned char *Bhi = bsm, *Blo = bsm + N * 128;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  const int na = (int)max(i_hi - i_lo, (int64_t)0);
+  const bool valid = j < a.n_s;
+  const bool no_gain = a.no_gain;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&tmem_base_sh)), "n"(S::ALLOC));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mma_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = tmem_base_sh;
+  const unsigned lane_off = (unsigned)(warp * 32) << 16;
+  const unsigned a_hi = tmem, a_lo = tmem + 32, d0 = tmem + 64;
+  // kind::tf32, fp32 accumulate, both operands K-major, M = 128, N
+  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(N >> 3) << 17) |
+                         ((unsigned)(128 >> 4) << 24);
+
+  const Rec rec = load_point<MODE>(a, j, valid);
+  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
+  bool domain = false;
+  PairTC prev;
+  const double kd16 = a.kd * 16.0;
+
+  for (int ai = 0; ai <= na; ++ai) {
+    PairTC cur;
+    if (ai < na) {
+      // ---------------- SIMT: pair data and the powers of w for antenna ai (overlaps MMA ai-1)
+      const int64_t ia = i_lo + ai;
+      const AntD an = load_ant<MONO>(a, ia);
+      double L;
+      if (MODE == kModeBwd) {
+        pair_geometry<MONO, CORR>(rec, an, no_gain, cur.g);
+        domain |= valid && !cur.g.ok;
+        L = cur.g.L;
+      } else {
+        L = pair_length<MONO>(rec, an);
+      }
+      const float fr0 = frac_cycles(L * a.k0);
+      const float frd = frac_cycles(L * a.kd);
+      const float f16 = frac_cycles(L * kd16);
+      __sincosf(kTwoPi * fr0, &cur.es, &cur.ec);
+      float zs, zc;
+      sincospif(2.f * frd, &zs, &zc);            // w (accurate)
+      sincospif(2.f * f16, &cur.Ws, &cur.Wc);    // W = w^16 from the fp64 cycle count
+      unsigned hv[32], lv[32];
+      float pr = 1.f, pi = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float hr = tf32_rna(pr), hi_ = tf32_rna(pi);
+        hv[k] = __float_as_uint(hr);
+        lv[k] = __float_as_uint(pr - hr);
+        hv[16 + k] = __float_as_uint(hi_);
+        lv[16 + k] = __float_as_uint(pi - hi_);
+        const float nr = fmaf(pr, zc, -pi * zs), ni = fmaf(pr, zs, pi * zc);
+        pr = nr;
+        pi = ni;
+      }
+      // ---------------- MMA ai-1 must be done before A / B are overwritten
+      if (ai > 0) mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
+      tc_fence_after();
+      tmem_st32(a_hi + lane_off, hv);
+      tmem_st32(a_lo + lane_off, lv);
+      // B^T rows of antenna ai from its X row (bins 16 m1 + m0), hi / lo
+      const float2 *Xr = a.X + ia * NF;
+#pragma unroll
+      for (int m = tid; m < NF; m += kAdjThreads) {
+        const float2 x = Xr[m];
+        const int m1 = m >> 4, m0 = m & 15;
+        const float v4[4] = {x.x, -x.y, x.y, x.x};
+        const int n4[4] = {m1, m1, P + m1, P + m1};
+        const int k4[4] = {m0, 16 + m0, m0, 16 + m0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float h = tf32_rna(v4[q]);
+          const unsigned off = bT_off(n4[q], k4[q]);
+          *reinterpret_cast<float *>(Bhi + off) = h;
+          *reinterpret_cast<float *>(Blo + off) = v4[q] - h;
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      if (tid == 0) {
+        const unsigned d = d0 + (unsigned)((ai & 1) * N);
+        const unsigned acol[3] = {a_hi, a_hi, a_lo};
+        const unsigned char *bs[3] = {Bhi, Blo, Bhi};
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            umma_tf32_ts(d, acol[p] + 8 * ks,
+                         umma_sdesc(smem_u32(bs[p]) + ks * 256, 128, 1024), idesc,
+                         (p | ks) ? 1u : 0u);
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];"
+                     ::"l"((uint64_t)smem_u32(&mma_bar)) : "memory");
+      }
+    }
+    if (ai > 0) {
+      // ---------------- epilogue of antenna ai-1: U from TMEM, Horner over m1, Eq. 5 / M sums
+      if (ai == na) {
+        mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
+        tc_fence_after();
+      }
+      const unsigned d = d0 + (unsigned)(((ai - 1) & 1) * N) + lane_off;
+      float Ur[P], Ui[P];
+#pragma unroll
+      for (int c = 0; c < N; c += 16) {
+        unsigned v[16];
+        tmem_ld16(d + c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int n = c + q;
+          if (n < P) Ur[n] = __uint_as_float(v[q]);
+          else Ui[n - P] = __uint_as_float(v[q]);
+        }
+      }
+      const f2x W = pk(prev.Wc, prev.Ws), W2 = pk(-prev.Ws, prev.Wc);
+      f2x h = pk(Ur[P - 1], Ui[P - 1]);
+#pragma unroll
+      for (int m1 = P - 2; m1 >= 0; --m1) {
+        const float2 hv = upk(h);
+        const f2x t = ffma2(W, pk(hv.x, hv.x), pk(Ur[m1], Ui[m1]));
+        h = ffma2(W2, pk(hv.y, hv.y), t);
+      }
+      const float2 hh = upk(h);
+      adj_accumulate<MODE>(prev.g, prev.ec, prev.es, hh.x, hh.y, S1, S2, S3x, S3y, S3z);
+    }
+    prev = cur;
+  }
+  if (domain) atomicOr(a.flags, 1u);
+  if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(S::ALLOC));
+}
+
+template <int MODE, bool MONO, bool CORR, int NF>
+static cudaError_t tc_launch(const AdjArgs &a, dim3 grid, cudaStream_t st) {
+  k_adjoint_tc<MODE, MONO, CORR, NF><<<grid, kAdjThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE, bool MONO, bool CORR>
+static cudaError_t tc_nf(const AdjArgs &a, dim3 grid, cudaStream_t st) {
+  switch (a.n_f) {
+    case 128: return tc_launch<MODE, MONO, CORR, 128>(a, grid, st);
+    case 256: return tc_launch<MODE, MONO, CORR, 256>(a, grid, st);
+    case 512: return tc_launch<MODE, MONO, CORR, 512>(a, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+bool adjoint_tc_supported(int n_f) { return n_f == 128 || n_f == 256 || n_f == 512; }
+
+cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
+                              cudaStream_t st) {
+  dim3 grid((unsigned)((a.n_s + kAdjThreads - 1) / kAdjThreads), (unsigned)n_splits);
+  if (mode == kModeBwd) {
+    if (mono) return corr ? tc_nf<kModeBwd, true, true>(a, grid, st)
+                          : tc_nf<kModeBwd, true, false>(a, grid, st);
+    return corr ? tc_nf<kModeBwd, false, true>(a, grid, st)
+                : tc_nf<kModeBwd, false, false>(a, grid, st);
+  }
+  return mono ? tc_nf<kModeFlt, true, false>(a, grid, st)
+              : tc_nf<kModeFlt, false, false>(a, grid, st);
+}
+
+}  // namespace rfr
