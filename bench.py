@@ -37,6 +37,8 @@ FP32_LANES_PER_SM = 128
 #   backward : 2 FFMA2           = 4 lane-ops (complex Horner step)
 #   filter   : 2 FFMA2           = 4 lane-ops
 OPS_PER_CONTRIB = 4
+# K3/K4 on tensor cores: D = A.B^T per 16-bin block, 4 real MACs per contribution, 3 tf32 products
+TC_FLOP_PER_CONTRIB = 24
 
 
 def peaks():
@@ -294,29 +296,48 @@ def run_gpu(args):
     pk = peaks()
     clocks = clk.summary()
     peak_ops = N_SM * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6
+    # tf32 tensor peak: the measured bf16 burst peak x the nominal tf32/bf16 ratio (1.1 / 2.25)
+    bf16 = pk.get("bf16_tflops", 1590.0)
+    peak_tf32 = bf16 * 1e12 * (1.1 / 2.25)
+    tc = os.environ.get("RFR_ADJOINT", "tc") != "simt" and grid.n_freq in (128, 256, 512)
     per_step = lambda ms: ms / args.steps
-    # dominant kernels: K2 (forward call, K1+split sum included) and K3 (backward partial call)
+    clk_ratio = (clocks["sm_mhz"] / pk.get("sm_max_mhz", 1965.0)) if clocks.get("sm_mhz") else None
     roofs = []
-    for name, ms in (("k_trace_fwd (K2, rfr_forward)", f_ms),
-                     ("k_adjoint<bwd> (K3+K1', rfr_backward)", b_ms),
-                     ("k_adjoint<flt> (K4, rfr_filter)", q_ms)):
-        ach = OPS_PER_CONTRIB * (Nc / world) / (per_step(ms) * 1e-3)
-        roofs.append({"kernel": name, "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
-                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                      "frac_at_measured_clock": (ach / (peak_ops * clocks["sm_mhz"] /
-                                                        pk.get("sm_max_mhz", 1965.0))
-                                                 if clocks.get("sm_mhz") else None),
-                      "ms_per_step": per_step(ms)})
+    # K2 forward: FP32-pipe bound, 4 lane-ops per contribution (1 FFMA2 + 1 FADD2)
+    ach = OPS_PER_CONTRIB * (Nc / world) / (per_step(f_ms) * 1e-3)
+    roofs.append({"kernel": "k_trace_fwd (K2, rfr_forward)", "bound": "alu",
+                  "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
+                  "frac": ach / peak_ops,
+                  "frac_at_measured_clock": ach / (peak_ops * clk_ratio) if clk_ratio else None,
+                  "ms_per_step": per_step(f_ms)})
+    for name, ms in (("k_adjoint_tc<bwd> (K3+K1', rfr_backward)", b_ms),
+                     ("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms)):
+        rate = (Nc / world) / (per_step(ms) * 1e-3)
+        if tc:
+            # exact 16-bin block factorisation on tcgen05 kind::tf32, 3xTF32: per contribution
+            # 4 real MACs x 3 products = 24 tensor FLOP
+            ach = TC_FLOP_PER_CONTRIB * rate
+            roofs.append({"kernel": name, "bound": "tensor", "achieved": ach / 1e12,
+                          "peak": peak_tf32 / 1e12, "unit": "T tf32 FLOP/s", "frac": ach / peak_tf32,
+                          "alu_equivalent_frac": OPS_PER_CONTRIB * rate / peak_ops,
+                          "ms_per_step": per_step(ms)})
+        else:
+            ach = OPS_PER_CONTRIB * rate
+            roofs.append({"kernel": name.replace("_tc", ""), "bound": "alu", "achieved": ach / 1e12,
+                          "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
+                          "frac": ach / peak_ops, "ms_per_step": per_step(ms)})
     dom = max(roofs, key=lambda r: r["ms_per_step"])
     traffic = None
     try:
         traffic = json.load(open(TRAFFIC_PATH)).get(args.config, {}).get(dom["kernel"].split()[0])
     except Exception:
         pass
-    roof = {"bound": "alu", "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-            "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
-            "peak_note": "148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); "
-                         "4 lane-ops per contribution"}
+    roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
+            "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
+            "peak_note": ("148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); 4 lane-ops "
+                          "per contribution" if dom["bound"] == "alu" else
+                          "measured bf16 burst peak x 1.1/2.25 (tf32/bf16 nominal); 24 tensor "
+                          "FLOP per contribution")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         r = oracle_sample_rates(prob, budget_s=args.ref_budget)

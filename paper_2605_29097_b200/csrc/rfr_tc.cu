@@ -13,7 +13,7 @@
 // run on the 5th-generation tensor cores as tcgen05.mma.kind::tf32 with A in tensor memory (each
 // thread writes its own row with tcgen05.st), B in shared memory (K-major, no swizzle) and D in
 // tensor memory.  fp32 accuracy comes from the 3xTF32 split (A_hi B_hi + A_hi B_lo + A_lo B_hi,
-// hi = round-to-tf32, lo = x - hi): measured 7e-7 relative against fp64 on random operands
+// hi = x truncated to tf32, lo = x - hi): 3xTF32 measured 7e-7 relative against fp64 on random operands
 // (tools/microbench/umma_tf32_probe.cu).  The per-pair SIMT work (fp64 geometry, the 16 powers of w,
 // the Horner over m1, the Eq. 5 epilogue) overlaps the MMAs of the previous antenna: A is single-
 // buffered (the MMA of antenna a-1 is awaited after the SIMT part of antenna a), D is double-
@@ -44,10 +44,11 @@ __device__ __forceinline__ unsigned bT_off(int n, int k) {
   return (unsigned)((k >> 2) * 128 + (n >> 3) * 1024 + (n & 7) * 16 + (k & 3) * 4);
 }
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  unsigned r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// 3xTF32 split by truncation: hi = x with the 13 low mantissa bits cleared (exactly a tf32
+// value, one LOP3), lo = x - hi (exact in fp32; the tensor core truncates it to tf32, leaving a
+// relative error <= 2^-21 of x).  cvt.rna.tf32 compiles to 4 SASS instructions on sm_100a.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void tmem_st32(unsigned addr, const unsigned (&v)[32]) {
@@ -169,17 +170,21 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
       sincospif(2.f * frd, &zs, &zc);            // w (accurate)
       sincospif(2.f * f16, &cur.Ws, &cur.Wc);    // W = w^16 from the fp64 cycle count
       unsigned hv[32], lv[32];
-      float pr = 1.f, pi = 0.f;
+      {
+        // powers p_k = w^k (packed complex, one FMUL2 + one FFMA2 each) and their hi / lo split
+        const f2x wz = pk(zc, zs);
+        f2x p = pk(1.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float hr = tf32_rna(pr), hi_ = tf32_rna(pi);
-        hv[k] = __float_as_uint(hr);
-        lv[k] = __float_as_uint(pr - hr);
-        hv[16 + k] = __float_as_uint(hi_);
-        lv[16 + k] = __float_as_uint(pi - hi_);
-        const float nr = fmaf(pr, zc, -pi * zs), ni = fmaf(pr, zs, pi * zc);
-        pr = nr;
-        pi = ni;
+        for (int k = 0; k < 16; ++k) {
+          const float2 pv = upk(p);
+          const float hr = tf32_hi(pv.x), hi_ = tf32_hi(pv.y);
+          const float2 lo = upk(fadd2(p, pk(-hr, -hi_)));
+          hv[k] = __float_as_uint(hr);
+          hv[16 + k] = __float_as_uint(hi_);
+          lv[k] = __float_as_uint(lo.x);
+          lv[16 + k] = __float_as_uint(lo.y);
+          if (k < 15) p = cmul2(p, wz);
+        }
       }
       // ---------------- MMA ai-1 must be done before A / B are overwritten
       if (ai > 0) mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
         const int k4[4] = {m0, 16 + m0, m0, 16 + m0};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float h = tf32_rna(v4[q]);
+          const float h = tf32_hi(v4[q]);
           const unsigned off = bT_off(n4[q], k4[q]);
           *reinterpret_cast<float *>(Bhi + off) = h;
           *reinterpret_cast<float *>(Blo + off) = v4[q] - h;
