@@ -6,10 +6,13 @@
 // factorises EXACTLY (no approximation) into a dense complex contraction over m0 followed by a
 // short Horner sum over m1:
 //     U_ij[m1] = sum_{m0 < 16} X_i[16 m1 + m0] w_ij^{m0},      h_ij = sum_{m1} (w_ij^16)^{m1} U_ij[m1].
-// For a fixed antenna i the first step is a real GEMM D = A B^T over a tile of 128 samples:
-//     A[j][k]   : k < 16 -> Re w^k,  16 <= k < 32 -> Im w^(k-16)                   (M = 128, K = 32)
-//     B^T[n][k] : n < P -> (Re X, -Im X) of bins 16 n + k,  P <= n < 2P -> (Im X, Re X)   (N = 2P)
-//     D[j][n]   : n < P -> Re U[n],  n >= P -> Im U[n - P]                           (P = NF / 16)
+// For a fixed antenna i the first step is a real GEMM D = A B^T over a tile of 128 samples, with
+// complex values interleaved (re, im) along both K and N so that packed f32x2 registers map 1:1
+// onto tensor-memory columns:
+//     A[j][2 m0 + c]        : c = 0 -> Re w^m0, c = 1 -> Im w^m0                    (M = 128, K = 32)
+//     B^T[2 m1][2 m0 + c]   : (Re X, -Im X)[c] of bin 16 m1 + m0   -> D[j][2 m1]     = Re U[m1]
+//     B^T[2 m1 + 1][2m0 + c]: (Im X,  Re X)[c]                     -> D[j][2 m1 + 1] = Im U[m1]
+//                                                                   (N = 2P, P = NF / 16)
 // run on the 5th-generation tensor cores as tcgen05.mma.kind::tf32 with A in tensor memory (each
 // thread writes its own row with tcgen05.st), B in shared memory (K-major, no swizzle) and D in
 // tensor memory.  fp32 accuracy comes from the 3xTF32 split (A_hi B_hi + A_hi B_lo + A_lo B_hi,
@@ -179,10 +182,10 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
           const float2 pv = upk(p);
           const float hr = tf32_hi(pv.x), hi_ = tf32_hi(pv.y);
           const float2 lo = upk(fadd2(p, pk(-hr, -hi_)));
-          hv[k] = __float_as_uint(hr);
-          hv[16 + k] = __float_as_uint(hi_);
-          lv[k] = __float_as_uint(lo.x);
-          lv[16 + k] = __float_as_uint(lo.y);
+          hv[2 * k] = __float_as_uint(hr);
+          hv[2 * k + 1] = __float_as_uint(hi_);
+          lv[2 * k] = __float_as_uint(lo.x);
+          lv[2 * k + 1] = __float_as_uint(lo.y);
           if (k < 15) p = cmul2(p, wz);
         }
       }
@@ -198,8 +201,8 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
         const float2 x = Xr[m];
         const int m1 = m >> 4, m0 = m & 15;
         const float v4[4] = {x.x, -x.y, x.y, x.x};
-        const int n4[4] = {m1, m1, P + m1, P + m1};
-        const int k4[4] = {m0, 16 + m0, m0, 16 + m0};
+        const int n4[4] = {2 * m1, 2 * m1, 2 * m1 + 1, 2 * m1 + 1};
+        const int k4[4] = {2 * m0, 2 * m0 + 1, 2 * m0, 2 * m0 + 1};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float h = tf32_hi(v4[q]);
@@ -242,10 +245,9 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
         tmem_ld16(d + c, v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int n = c + q;
-          if (n < P) Ur[n] = __uint_as_float(v[q]);
-          else Ui[n - P] = __uint_as_float(v[q]);
+        for (int q = 0; q < 16; q += 2) {
+          Ur[(c + q) / 2] = __uint_as_float(v[q]);
+          Ui[(c + q) / 2] = __uint_as_float(v[q + 1]);
         }
       }
       const f2x W = pk(prev.Wc, prev.Ws), W2 = pk(-prev.Ws, prev.Wc);
