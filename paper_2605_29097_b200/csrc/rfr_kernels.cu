@@ -839,7 +839,7 @@ static bool use_tensor_cores() {
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st) {
   if (use_tensor_cores() && adjoint_tc_supported(a.n_f) &&
-      (reinterpret_cast<uintptr_t>(a.X) & 7) == 0)
+      (reinterpret_cast<uintptr_t>(a.X) & 15) == 0)
     return counted(launch_adjoint_tc(a, mode, mono, corr, n_splits, st));
   const int64_t per_cta = (int64_t)kAdjThreads;
   dim3 grid((unsigned)((a.n_s + per_cta - 1) / per_cta), (unsigned)n_splits);

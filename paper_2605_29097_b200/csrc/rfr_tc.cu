@@ -113,6 +113,7 @@ template <int MODE, bool MONO, bool CORR, int NF>
 __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(AdjArgs a) {
   using S = TCShape<NF>;
   constexpr int P = S::P, N = S::N;
+  constexpr int CH = (N * 8 + kAdjThreads - 1) / kAdjThreads;     // B chunks per thread
   static_assert(kAdjThreads == 128, "one TMEM lane per thread");
   __shared__ __align__(128) unsigned char bsm[2 * N * 128];          // B_hi, B_lo [N][32] fp32
   __shared__ __align__(8) unsigned long long mma_bar;
@@ -156,6 +157,18 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
     if (ai < na) {
       // ---------------- SIMT: pair data and the powers of w for antenna ai (overlaps MMA ai-1)
       const int64_t ia = i_lo + ai;
+      // this antenna's B chunks come from 16-byte pieces of its X row: load them first so the
+      // global latency overlaps the geometry below
+      float4 xq[CH];
+      {
+        const float4 *X4 = reinterpret_cast<const float4 *>(a.X + ia * NF);
+#pragma unroll
+        for (int r = 0; r < CH; ++r) {
+          const int q = tid + r * kAdjThreads;
+          const int n = q % N, c = q / N;
+          xq[r] = q < N * 8 ? X4[(16 * (n >> 1) + 2 * c) >> 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
       const AntD an = load_ant<MONO>(a, ia);
       double L;
       if (MODE == kModeBwd) {
@@ -194,21 +207,23 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
       tc_fence_after();
       tmem_st32(a_hi + lane_off, hv);
       tmem_st32(a_lo + lane_off, lv);
-      // B^T rows of antenna ai from its X row (bins 16 m1 + m0), hi / lo
-      const float2 *Xr = a.X + ia * NF;
+      // B^T of antenna ai, one 16-byte chunk (row n, columns 4c..4c+3) per thread and pass: the
+      // chunk holds bins b, b+1 (b = 16 (n / 2) + 2c) as (Re, -Im) (n even) or (Im, Re) (n odd).
+      // Thread -> (n = q % N, c = q / N) makes a warp's 32 stores cover the 8 rows of a core
+      // matrix 4 times: conflict-free 128-bit shared stores.
 #pragma unroll
-      for (int m = tid; m < NF; m += kAdjThreads) {
-        const float2 x = Xr[m];
-        const int m1 = m >> 4, m0 = m & 15;
-        const float v4[4] = {x.x, -x.y, x.y, x.x};
-        const int n4[4] = {2 * m1, 2 * m1, 2 * m1 + 1, 2 * m1 + 1};
-        const int k4[4] = {2 * m0, 2 * m0 + 1, 2 * m0, 2 * m0 + 1};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float h = tf32_hi(v4[q]);
-          const unsigned off = bT_off(n4[q], k4[q]);
-          *reinterpret_cast<float *>(Bhi + off) = h;
-          *reinterpret_cast<float *>(Blo + off) = v4[q] - h;
+      for (int r = 0; r < CH; ++r) {
+        const int q = tid + r * kAdjThreads;
+        if (q < N * 8) {
+          const int n = q % N, c = q / N;
+          const float4 x = xq[r];
+          const float4 v = (n & 1) ? make_float4(x.y, x.x, x.w, x.z)
+                                   : make_float4(x.x, -x.y, x.z, -x.w);
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+          const unsigned off = bT_off(n, 4 * c);
+          *reinterpret_cast<float4 *>(Bhi + off) = h;
+          *reinterpret_cast<float4 *>(Blo + off) = l;
         }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
