@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <new>
 
@@ -44,9 +45,18 @@ int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct FwdGeom {
   int B = 32, nb = 1, nb_total = 1, taw = 32, chunks = 1;
 };
+// bins per lane: 32 (3 CTAs / SM) or, with RFR_FWD_B=16, 16 (5 CTAs / SM, twice the anchors)
+int fwd_b_pref() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RFR_FWD_B");
+    v = (e && atoi(e) == 16) ? 16 : 32;
+  }
+  return v;
+}
 bool fwd_geom(int32_t n_f, FwdGeom &g) {
   const int nf = n_f > 0 ? n_f : 1;
-  g.B = nf >= 32 ? 32 : (nf >= 16 ? 16 : 8);
+  g.B = nf >= 32 ? fwd_b_pref() : (nf >= 16 ? 16 : 8);
   g.nb_total = (int)cdiv(nf, g.B);
   if (g.nb_total > 256) return false;                      // n_freq > 8192: unsupported
   g.nb = std::min(g.nb_total, 32);
@@ -66,13 +76,14 @@ struct Split {
 Split fwd_split(int64_t n_pts, int64_t n_a, int32_t n_f, const FwdGeom &g, size_t cap) {
   const int64_t n_tiles =
       (n_a > 0 ? cdiv(n_a, (int64_t)kFwdWarps * g.taw) : 1) * g.chunks;
-  int64_t s = cdiv((int64_t)device_sms() * kFwdMinBlocks * 32, n_tiles);
-  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_pts, kFwdTJ * 16)));
+  const int tj = fwd_tj(g.B);
+  int64_t s = cdiv((int64_t)device_sms() * fwd_min_blocks(g.B) * 32, n_tiles);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_pts, tj * 16)));
   const size_t per = (size_t)std::max<int64_t>(n_a, 1) * std::max(n_f, 1) * 8;
   s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t)(std::min(cap, kSplitCap) / per)));
   s = std::max<int64_t>(s, 1);
   Split r;
-  r.per_split = cdiv(cdiv(std::max<int64_t>(n_pts, 1), s), kFwdTJ) * kFwdTJ;
+  r.per_split = cdiv(cdiv(std::max<int64_t>(n_pts, 1), s), tj) * tj;
   r.splits = (int)std::max<int64_t>(1, cdiv(n_pts, r.per_split));
   if (r.splits == 1) r.per_split = std::max<int64_t>(n_pts, 1);
   return r;
@@ -210,7 +221,7 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
   a.n_a = ants->n_ant;
   a.n_f = grid->n_freq; a.nb = g.nb; a.nb_total = g.nb_total; a.taw = g.taw;
-  a.warp_smem = fwd_warp_smem();
+  a.warp_smem = fwd_warp_smem(g.B);
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.kw = grid->df_hz * g.B / kC;

@@ -76,16 +76,17 @@ __global__ void k_blend(BlendArgs a) {
 // per-pair amplitude is the complex c_q itself (no gain, decay or transmittance), so the kernel
 // computes dL/ds(i,m) = sum_q c_q e^{-j 2 pi f_m tau_iq} with the same anchors and recurrence.
 template <int B, bool MONO, bool CORR, int KIND>
-__global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(FwdArgs a) {
+  constexpr int TJ = fwd_tj(B);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbc = a.nb, taw = a.taw;
   unsigned char *wb = smem_raw + (size_t)warp * a.warp_smem;
   // fixed strides (32 slots per sample) so that phase-2 addresses are compile-time offsets
   float4 *anc = reinterpret_cast<float4 *>(wb);                          // [TJ][32]: slot b*taw+aa
-  float *kv = reinterpret_cast<float *>(wb + kFwdTJ * 32 * 16);          // [TJ][32]: slot aa
-  AntD *ant = reinterpret_cast<AntD *>(wb + kFwdTJ * 32 * 20);           // [taw]
-  Rec *rbuf = reinterpret_cast<Rec *>(wb + kFwdTJ * 32 * 20 + 32 * sizeof(AntD));  // [2][TJ]
+  float *kv = reinterpret_cast<float *>(wb + TJ * 32 * 16);          // [TJ][32]: slot aa
+  AntD *ant = reinterpret_cast<AntD *>(wb + TJ * 32 * 20);           // [taw]
+  Rec *rbuf = reinterpret_cast<Rec *>(wb + TJ * 32 * 20 + 32 * sizeof(AntD));  // [2][TJ]
   const int64_t a0 = ((int64_t)blockIdx.x * kFwdWarps + warp) * taw;
   const int64_t j_lo = (int64_t)blockIdx.y * a.samples_per_split;
   const int64_t j_hi = min(a.n_s, j_lo + a.samples_per_split);
@@ -117,23 +118,23 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
 
   // records of one tile: TJ x 48 B = 3 TJ chunks of 16 B spread over the lanes
   auto prefetch = [&](int64_t jt, int buf) {
-    for (int c = lane; c < kFwdTJ * 3; c += 32) {
+    for (int c = lane; c < TJ * 3; c += 32) {
       const int jj = c / 3, part = c % 3;
       const int64_t j = jt + jj;
       if (j < j_hi)
-        cp_async16(reinterpret_cast<float4 *>(rbuf + buf * kFwdTJ + jj) + part,
+        cp_async16(reinterpret_cast<float4 *>(rbuf + buf * TJ + jj) + part,
                    reinterpret_cast<const float4 *>(a.rec + j) + part);
     }
     cp_async_commit();
   };
   if (j_lo < j_hi) prefetch(j_lo, 0);
   int buf = 0;
-  for (int64_t jt = j_lo; jt < j_hi; jt += kFwdTJ, buf ^= 1) {
+  for (int64_t jt = j_lo; jt < j_hi; jt += TJ, buf ^= 1) {
     cp_async_wait_all();
     __syncwarp();
-    if (jt + kFwdTJ < j_hi) prefetch(jt + kFwdTJ, buf ^ 1);
+    if (jt + TJ < j_hi) prefetch(jt + TJ, buf ^ 1);
     // ---------------- phase 1: per-pair geometry and anchors (one pair per lane)
-    for (int pr = lane; pr < taw * kFwdTJ; pr += 32) {
+    for (int pr = lane; pr < taw * TJ; pr += 32) {
       const int aa = pr % taw, jj = pr / taw;
       const int64_t j = jt + jj;
       float4 *dst = anc + jj * 32 + aa;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
         kv[jj * 32 + aa] = 2.f;
         continue;
       }
-      const Rec rec = rbuf[buf * kFwdTJ + jj];
+      const Rec rec = rbuf[buf * TJ + jj];
       double L;
       float Ar, Ai;
       if (KIND == kFwdTrace) {
@@ -185,10 +186,10 @@ __global__ void __launch_bounds__(kFwdThreads, kFwdMinBlocks) k_trace_fwd(FwdArg
       float4 Yn = ap[0];
       float knx = kp_[0];
 #pragma unroll 1
-      for (int jj = 0; jj < kFwdTJ; ++jj) {
+      for (int jj = 0; jj < TJ; ++jj) {
         const float4 Y = Yn;
         const float k = knx;
-        if (jj + 1 < kFwdTJ) {
+        if (jj + 1 < TJ) {
           Yn = ap[(jj + 1) * 32];
           knx = kp_[(jj + 1) * 32];
         }

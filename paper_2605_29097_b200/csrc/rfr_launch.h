@@ -11,7 +11,10 @@ struct Rec;
 constexpr int kFwdThreads = 128;   // K2 CTA size (4 warps)
 constexpr int kFwdMinBlocks = 3;   // K2 CTAs per SM (register budget ~170)
 constexpr int kFwdWarps = kFwdThreads / 32;
-constexpr int kFwdTJ = 16;         // samples per K2 warp tile
+constexpr int kFwdTJ = 16;         // samples per K2 warp tile (B = 32)
+// K2 tile shape per bins-per-lane B: samples per warp tile and CTAs per SM (register budget)
+__host__ __device__ constexpr int fwd_tj(int B) { return B == 32 ? 16 : 8; }
+__host__ __device__ constexpr int fwd_min_blocks(int B) { return B == 32 ? 3 : 5; }
 constexpr int kAdjThreads = 128;   // K3/K4 CTA size
 constexpr int kAdjGA = 8;          // antennas per K3/K4 shared-memory stage
 constexpr int kModeBwd = 0, kModeFlt = 1;
@@ -75,8 +78,9 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // K2 per-warp shared memory: anchors [TJ][32] float4, 2cos(theta) [TJ][32] float, antennas [32]
 // (56 B each), double-buffered records [2][TJ] (48 B each)
-inline size_t fwd_warp_smem() {
-  return align_up((size_t)kFwdTJ * 32 * 20 + 32 * 56 + 2 * kFwdTJ * 48, 128);
+inline size_t fwd_warp_smem(int B) {
+  const int tj = fwd_tj(B);
+  return align_up((size_t)tj * 32 * 20 + 32 * 56 + 2 * tj * 48, 128);
 }
 // K3/K4 staging.  TMA-ring kernel (specialised bin counts): kAdjStages buffers of
 // adj_stage_ants(nf) antennas (8 KB of X rows each) + 2 mbarriers per stage.  Generic kernel:
