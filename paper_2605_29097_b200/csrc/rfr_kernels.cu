@@ -178,31 +178,26 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
       kv[jj * 32 + aa] = 2.f * zc;
     }
     __syncwarp();
-    // ---------------- phase 2: bin recurrences
+    // ---------------- phase 2: bin recurrences, two samples interleaved (independent chains)
     if (active) {
       const float4 *ap = anc + my_b * taw + my_a;
       const float *kp_ = kv + my_a;
-      // software pipeline: the next sample's anchors are loaded before this sample's chain runs
-      float4 Yn = ap[0];
-      float knx = kp_[0];
 #pragma unroll 1
-      for (int jj = 0; jj < TJ; ++jj) {
-        const float4 Y = Yn;
-        const float k = knx;
-        if (jj + 1 < TJ) {
-          Yn = ap[(jj + 1) * 32];
-          knx = kp_[(jj + 1) * 32];
-        }
-        const f2x kp = pk(k, k), kn = pk(-k, -k);
-        f2x q0 = pk(Y.x, Y.y), q1 = pk(Y.z, Y.w);
-        acc[0] = fadd2(acc[0], q0);
-        acc[1] = fadd2(acc[1], q1);
+      for (int jj = 0; jj < TJ; jj += 2) {
+        const float4 Ya = ap[jj * 32], Yb = ap[(jj + 1) * 32];
+        const float ka = kp_[jj * 32], kb = kp_[(jj + 1) * 32];
+        const f2x kpa = pk(ka, ka), kna = pk(-ka, -ka), kpb = pk(kb, kb), knb = pk(-kb, -kb);
+        f2x a0 = pk(Ya.x, Ya.y), a1 = pk(Ya.z, Ya.w);
+        f2x b0 = pk(Yb.x, Yb.y), b1 = pk(Yb.z, Yb.w);
+        acc[0] = fadd2(fadd2(acc[0], a0), b0);
+        acc[1] = fadd2(fadd2(acc[1], a1), b1);
 #pragma unroll
         for (int m = 1; m < B - 1; ++m) {
-          const f2x q2 = ffma2((m & 1) ? kn : kp, q1, q0);
-          acc[m + 1] = fadd2(acc[m + 1], q2);
-          q0 = q1;
-          q1 = q2;
+          const f2x a2 = ffma2((m & 1) ? kna : kpa, a1, a0);
+          const f2x b2 = ffma2((m & 1) ? knb : kpb, b1, b0);
+          acc[m + 1] = fadd2(fadd2(acc[m + 1], a2), b2);
+          a0 = a1; a1 = a2;
+          b0 = b1; b1 = b2;
         }
       }
     }
