@@ -328,8 +328,9 @@ def run_gpu(args):
                           "frac": ach / peak_ops, "ms_per_step": per_step(ms)})
     dom = max(roofs, key=lambda r: r["ms_per_step"])
     traffic = None
-    try:
-        traffic = json.load(open(TRAFFIC_PATH)).get(args.config, {}).get(dom["kernel"].split()[0])
+    try:   # bytes per launch from the committed full-size ncu capture (profiles/traffic.json)
+        key = dom["kernel"].split()[0]
+        traffic = json.load(open(TRAFFIC_PATH)).get(args.config, {}).get(key)
     except Exception:
         pass
     roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],

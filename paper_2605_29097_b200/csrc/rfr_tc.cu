@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
   static_assert(kAdjThreads == 128, "one TMEM lane per thread");
   __shared__ __align__(128) unsigned char bsm[2 * N * 128];          // B_hi, B_lo [N][32] fp32
   __shared__ __align__(8) unsigned long long mma_bar;
+  __shared__ __align__(8) unsigned long long a_full;    // one arrive per warp per antenna
   __shared__ unsigned tmem_base_sh;
   unsigned char *Bhi = bsm, *Blo = bsm + N * 128;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
   }
   if (tid == 0) {
     mbar_init(&mma_bar, 1);
+    mbar_init(&a_full, kAdjThreads / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -187,19 +189,29 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
       sincospif(2.f * f16, &cur.Ws, &cur.Wc);    // W = w^16 from the fp64 cycle count
       unsigned hv[32], lv[32];
       {
-        // powers p_k = w^k (packed complex, one FMUL2 + one FFMA2 each) and their hi / lo split
-        const f2x wz = pk(zc, zs);
-        f2x p = pk(1.f, 0.f);
+        // powers p_k = w^k (packed complex mults) by binary expansion -- dependency depth 4
+        // instead of a 15-long chain -- and their hi / lo split
+        f2x pw[16];
+        pw[0] = pk(1.f, 0.f);
+        pw[1] = pk(zc, zs);
+        pw[2] = cmul2(pw[1], pw[1]);
+        pw[4] = cmul2(pw[2], pw[2]);
+        pw[8] = cmul2(pw[4], pw[4]);
+        pw[3] = cmul2(pw[2], pw[1]);
+        pw[5] = cmul2(pw[4], pw[1]);
+        pw[6] = cmul2(pw[4], pw[2]);
+        pw[7] = cmul2(pw[4], pw[3]);
+#pragma unroll
+        for (int k = 9; k < 16; ++k) pw[k] = cmul2(pw[8], pw[k - 8]);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float2 pv = upk(p);
+          const float2 pv = upk(pw[k]);
           const float hr = tf32_hi(pv.x), hi_ = tf32_hi(pv.y);
-          const float2 lo = upk(fadd2(p, pk(-hr, -hi_)));
+          const float2 lo = upk(fadd2(pw[k], pk(-hr, -hi_)));
           hv[2 * k] = __float_as_uint(hr);
           hv[2 * k + 1] = __float_as_uint(hi_);
           lv[2 * k] = __float_as_uint(lo.x);
           lv[2 * k + 1] = __float_as_uint(lo.y);
-          if (k < 15) p = cmul2(p, wz);
         }
       }
       // ---------------- MMA ai-1 must be done before A / B are overwritten
@@ -229,9 +241,13 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
+      // every warp signals "my A rows and B chunks are written"; only the issuing thread waits,
+      // so the other warps go straight on to the previous antenna's epilogue
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&a_full);
       if (tid == 0) {
+        mbar_wait(&a_full, (unsigned)(ai & 1));
+        tc_fence_after();
         const unsigned d = d0 + (unsigned)((ai & 1) * N);
         const unsigned acol[3] = {a_hi, a_hi, a_lo};
         const unsigned char *bs[3] = {Bhi, Blo, Bhi};
