@@ -218,14 +218,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, u
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes) : "memory");
 }
-// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit instead of
-// spinning on issue slots (the producer waits most of the time once the ring is full)
+// Wait for the phase with the given parity to complete.  Plain try_wait (the hardware may
+// suspend the thread for a short, system-defined time per probe).  A suspend-time hint was tried
+// and made things worse: ptxas turns it into NANOSLEEP up to the hint after a failed probe.
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
   const unsigned a = smem_u32(bar);
   unsigned ok = 0;
   do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  } while (!ok);
+}
+// Same with a suspend-time hint (ns): for a producer that is expected to wait long (TMA ring).
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long *bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  unsigned ok = 0;
+  do {
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity), "r"(20000u) : "memory");
   } while (!ok);
 }
 // contiguous global -> shared copy by the bulk-copy (TMA) engine, completing on `bar`

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kAdjThreads + 32, 4) k_adjoint_tma(AdjArgs a) 
     if (lane == 0) {
       for (int st = 0; st < n_stages; ++st) {
         const int b = st % NS;
-        if (st >= NS) mbar_wait(&empty[b], ((st / NS) - 1) & 1);
+        if (st >= NS) mbar_wait_sleep(&empty[b], ((st / NS) - 1) & 1);
         const int64_t ic = i_lo + (int64_t)st * GA;
         const int ga = (int)min((int64_t)GA, i_hi - ic);
         const unsigned bytes = (unsigned)(ga * NF * sizeof(float2));
