@@ -117,7 +117,6 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
   static_assert(kAdjThreads == 128, "one TMEM lane per thread");
   __shared__ __align__(128) unsigned char bsm[2 * N * 128];          // B_hi, B_lo [N][32] fp32
   __shared__ __align__(8) unsigned long long mma_bar;
-  __shared__ __align__(8) unsigned long long a_full;    // one arrive per warp per antenna
   __shared__ unsigned tmem_base_sh;
   unsigned char *Bhi = bsm, *Blo = bsm + N * 128;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -135,7 +134,6 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
   }
   if (tid == 0) {
     mbar_init(&mma_bar, 1);
-    mbar_init(&a_full, kAdjThreads / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -241,13 +239,12 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
-      // every warp signals "my A rows and B chunks are written"; only the issuing thread waits,
-      // so the other warps go straight on to the previous antenna's epilogue
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(&a_full);
+      // all A rows and B chunks written before the MMA is issued.  (An mbarrier that only the
+      // issuing thread waits on measured slower: the other warps then reach the single-buffered A
+      // of the next antenna before the late-issued MMA has finished with it.)
+      __syncthreads();
+      tc_fence_after();
       if (tid == 0) {
-        mbar_wait(&a_full, (unsigned)(ai & 1));
-        tc_fence_after();
         const unsigned d = d0 + (unsigned)((ai & 1) * N);
         const unsigned acol[3] = {a_hi, a_hi, a_lo};
         const unsigned char *bs[3] = {Bhi, Blo, Bhi};
