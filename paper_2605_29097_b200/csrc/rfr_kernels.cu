@@ -75,12 +75,14 @@ __global__ void k_blend(BlendArgs a) {
 // k_mf_adj_pack as {x, y, z, w = Re c_q, T = Im c_q} with c_q = (dL/dP_q) M_q / max(P_q, eps); the
 // per-pair amplitude is the complex c_q itself (no gain, decay or transmittance), so the kernel
 // computes dL/ds(i,m) = sum_q c_q e^{-j 2 pi f_m tau_iq} with the same anchors and recurrence.
-template <int B, bool MONO, bool CORR, int KIND>
+// NB > 0: compile-time bin blocks per warp (n_f = 32 NB x chunks, no partial chunk), so the
+// per-pair loops and the slot arithmetic of phase 1 fold to constants; NB == 0: runtime.
+template <int B, bool MONO, bool CORR, int KIND, int NB>
 __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(FwdArgs a) {
   constexpr int TJ = fwd_tj(B);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nbc = a.nb, taw = a.taw;
+  const int nbc = NB > 0 ? NB : a.nb, taw = NB > 0 ? 32 / NB : a.taw;
   unsigned char *wb = smem_raw + (size_t)warp * a.warp_smem;
   // fixed strides (32 slots per sample) so that phase-2 addresses are compile-time offsets
   float4 *anc = reinterpret_cast<float4 *>(wb);                          // [TJ][32]: slot b*taw+aa
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
   const int64_t j_hi = min(a.n_s, j_lo + a.samples_per_split);
   const int chunk = blockIdx.z;
   const double k0 = a.k0 + (double)chunk * a.kchunk;                    // f0 of this bin chunk / c
-  const int nb_here = min(nbc, a.nb_total - chunk * nbc);               // blocks in this chunk
+  const int nb_here = NB > 0 ? NB : min(nbc, a.nb_total - chunk * nbc);   // blocks in this chunk
   const bool no_gain = a.no_gain;
 
   for (int aa = lane; aa < taw; aa += 32) {
@@ -666,7 +668,12 @@ cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st) {
 
 template <int B, bool MONO, bool CORR, int KIND>
 static cudaError_t fwd_t(const FwdArgs &a, dim3 grid, size_t smem, cudaStream_t st) {
-  auto k = k_trace_fwd<B, MONO, CORR, KIND>;
+  const bool full = a.nb_total % a.nb == 0;
+  auto k = (B == 32 && full && a.nb == 8) ? k_trace_fwd<B, MONO, CORR, KIND, 8>
+         : (B == 32 && full && a.nb == 16) ? k_trace_fwd<B, MONO, CORR, KIND, 16>
+         : (B == 32 && full && a.nb == 4) ? k_trace_fwd<B, MONO, CORR, KIND, 4>
+         : (B == 32 && full && a.nb == 2) ? k_trace_fwd<B, MONO, CORR, KIND, 2>
+                                          : k_trace_fwd<B, MONO, CORR, KIND, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<grid, kFwdThreads, smem, st>>>(a);
