@@ -223,19 +223,30 @@ def run_gpu(args):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
+    fused = not args.separate
+
     def step(rec=None):
+        # fused (default): K2 forward, K6 loss, then K3 + K4 in one tensor-core sweep
+        # (rfr_backward_filter: filter queries = the samples).  --separate: rfr_filter before the
+        # loss and rfr_backward after it, as two sweeps.
         for s in B:
             e = [ev() for _ in range(5)] if rec is not None else None
             if e: e[0].record(st)
             rfr.rfr_forward(s["S"], prob.sharpness, s["A"], grid, s["sig"], s["ws"])
             if e: e[1].record(st)
-            rfr.rfr_filter(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P"], s["ws"],
-                           mf=s["M"], comm=comm)
+            if not fused:
+                rfr.rfr_filter(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P"],
+                               s["ws"], mf=s["M"], comm=comm)
             if e: e[2].record(st)
             rfr.rfr_loss(s["sig"], s["y"], s["G"], s["loss"], s["ws"])
             if e: e[3].record(st)
-            rfr.rfr_backward(s["G"], s["S"], prob.sharpness, s["A"], grid, s["out"], s["ws"],
-                             flags=rfr.RFR_REUSE_BLEND, comm=comm)
+            if fused:
+                rfr.rfr_backward_filter(s["G"], s["sig"], s["S"], prob.sharpness, s["A"], grid,
+                                        s["out"], s["P"], s["ws"], mf=s["M"],
+                                        flags=rfr.RFR_REUSE_BLEND, comm=comm)
+            else:
+                rfr.rfr_backward(s["G"], s["S"], prob.sharpness, s["A"], grid, s["out"], s["ws"],
+                                 flags=rfr.RFR_REUSE_BLEND, comm=comm)
             if e:
                 e[4].record(st)
                 rec.append(e)
@@ -310,9 +321,13 @@ def run_gpu(args):
                   "frac": ach / peak_ops,
                   "frac_at_measured_clock": ach / (peak_ops * clk_ratio) if clk_ratio else None,
                   "ms_per_step": per_step(f_ms)})
-    for name, ms in (("k_adjoint_tc<bwd> (K3+K1', rfr_backward)", b_ms),
-                     ("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms)):
-        rate = (Nc / world) / (per_step(ms) * 1e-3)
+    if fused:
+        adj = [("k_adjoint_tc<both> (K3+K4 fused +K1', rfr_backward_filter)", b_ms, 2)]
+    else:
+        adj = [("k_adjoint_tc<bwd> (K3+K1', rfr_backward)", b_ms, 1),
+               ("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms, 1)]
+    for name, ms, npass in adj:
+        rate = npass * (Nc / world) / (per_step(ms) * 1e-3)     # contributions of all its passes
         if tc:
             # exact 16-bin block factorisation on tcgen05 kind::tf32, 3xTF32: per contribution
             # 4 real MACs x 3 products = 24 tensor FLOP
@@ -355,13 +370,20 @@ def run_gpu(args):
                        "n_antennas": [b.antennas.n for b in prob.bundles][0],
                        "n_freq": grid.n_freq, "parallelism": f"antenna-shard x{world}",
                        "l2": "flushed between steps (512 MiB memset, outside the step events)",
-                       "step": "K1 blend + K2 forward + K4 filter (+NCCL all-reduce of M) + K6 "
-                               "loss + K3 backward (+NCCL all-reduce of partials) + K1' finish"},
-            "passes": {"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
-                       "filter_G_per_s": Nc / (per_step(q_ms) * 1e-3) / 1e9,
-                       "bwd_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
-                       "fwd_plus_bwd_G_per_s": Nc / (per_step(f_ms + b_ms) * 1e-3) / 1e9,
-                       "loss_ms": per_step(l_ms)},
+                       "step": ("K1 blend + K2 forward + K6 loss + K3/K4 fused backward + "
+                                "matched filter at the samples (+NCCL all-reduce of partials and "
+                                "M) + K1' finish" if fused else
+                                "K1 blend + K2 forward + K4 filter (+NCCL all-reduce of M) + K6 "
+                                "loss + K3 backward (+NCCL all-reduce of partials) + K1' finish")},
+            "passes": ({"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
+                        "filter_plus_bwd_fused_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
+                        "loss_ms": per_step(l_ms), "fwd_ms": per_step(f_ms),
+                        "filter_plus_bwd_ms": per_step(b_ms)} if fused else
+                       {"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
+                        "filter_G_per_s": Nc / (per_step(q_ms) * 1e-3) / 1e9,
+                        "bwd_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
+                        "fwd_plus_bwd_G_per_s": Nc / (per_step(f_ms + b_ms) * 1e-3) / 1e9,
+                        "loss_ms": per_step(l_ms)}),
             "roofline": roof, "rooflines": roofs, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed": t_wall}
     print(json.dumps(line), flush=True)
@@ -426,6 +448,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=20.0,
                     help="seconds of oracle work per reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--separate", action="store_true",
+                    help="filter and backward as two sweeps (rfr_filter + rfr_backward)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

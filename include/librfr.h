@@ -197,6 +197,21 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
                                 float sharpness, const rfr_antennas *ants,
                                 const rfr_freq_grid *grid, const rfr_opts *opts, float *partials,
                                 const rfr_workspace *ws, rfr_stream_t stream);
+/* K3 + K4 in ONE sweep over the (sample, antenna) pairs: the backward of rfr_backward (from
+ * grad_signal) and the matched filter of rfr_filter (from signal) evaluated at the sample points
+ * themselves (queries = samples).  Both are adjoint bin sums over the same pairs
+ * (App. A.5 P:L725-728 and Eq. 3), so the fp64 pair geometry, the phasors and the
+ * tensor-core A operand are computed once; results equal rfr_backward + rfr_filter(q = samples)
+ * to rounding.  signal / grad_signal: [n_ant][n_freq] complex64 (this rank's rows); power:
+ * [n_samples] |M| (required); mf: optional complex M [n_samples] (NULL = workspace scratch).  The
+ * workspace must be planned with n_query >= n_samples.  comm: the partial M and the partial sums
+ * are all-reduced before |M| and K1' (NULL = one GPU).  Errors as rfr_backward / rfr_filter. */
+rfr_status rfr_backward_filter(const float *grad_signal, const float *signal,
+                               const rfr_samples *samples, float sharpness,
+                               const rfr_antennas *ants, const rfr_freq_grid *grid,
+                               const rfr_opts *opts, const rfr_sample_grads *out, float *power,
+                               float *mf, const rfr_comm *comm, const rfr_workspace *ws,
+                               rfr_stream_t stream);
 /* K1': chain the (all-reduced) partials through Eq. 5 and the blend of every ray. */
 rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
                                const rfr_opts *opts, const rfr_sample_grads *out,

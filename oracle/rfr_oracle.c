@@ -124,8 +124,10 @@ static void pair_eval(const orc_samples *S, int64_t j, double w_j, double T_j,
   double ptx = Ant->phi_tx ? Ant->phi_tx[i] : 1.0;
   double prx = Ant->phi_rx ? Ant->phi_rx[i] : (Ant->phi_tx && !bistatic ? ptx : 1.0);
   double tt = T_j + (ptx - papr), tr = T_j + (prx - papr);   /* = T - Phi_apr + Phi_ant */
-  o->chi_t = (tt > 0.0 && tt < 1.0);
-  o->chi_r = (tr > 0.0 && tr < 1.0);
+  /* clamp derivative (Q25b): the upper clamp can only act when the correction is positive; with
+     Phi_ant - Phi_apr <= 0, T_raw <= T_j <= 1 and the clamp is the identity on the feasible side */
+  o->chi_t = (tt > 0.0 && (tt < 1.0 || ptx - papr <= 0.0));
+  o->chi_r = (tr > 0.0 && (tr < 1.0 || prx - papr <= 0.0));
   o->Tt = tt < 0.0 ? 0.0 : (tt > 1.0 ? 1.0 : tt);
   o->Tr = tr < 0.0 ? 0.0 : (tr > 1.0 ? 1.0 : tr);
   /* Eq. 5 discretised: A = a * (w_o.w_r) * gamma * T^2 * alpha * A'_tx  (T^2 alpha, Q10) */

@@ -42,6 +42,10 @@ __device__ __forceinline__ f2x fadd2(f2x a, f2x b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// acc += x in place (register-stable accumulators: no MOV rotation at the loop end)
+__device__ __forceinline__ void acc2(f2x &acc, f2x x) {
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(x));
+}
 __device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
   f2x d;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -126,7 +130,8 @@ struct PairBwd {
 // path.  *inv = r0 ~ 1/d in fp32 for the directions and the path loss.
 __device__ __forceinline__ double dist_from_sq(double d2, float *inv) {
   d2 = fmax(d2, 1e-24);            // coincident points stay finite (and fail the u_min guard)
-  const float r0 = rsqrtf((float)d2);
+  float r0;                        // MUFU.RSQ without the denormal rescaling (d2 >= 1e-24)
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"((float)d2));
   const double y = d2 * (double)r0;
   const double e = fma(-y, y, d2);
   *inv = r0;
@@ -183,13 +188,16 @@ __device__ __forceinline__ void pair_geometry(const Rec &r, const AntD &a, bool 
   o.gg = g * o.gamma;
   if (CORR) {                                        // Eq. 7 as printed, clamped (Q11, Q12)
     float tt = r.T + (a.ptx - r.papr), tr = r.T + (a.prx - r.papr);   // T - Phi_apr + Phi_ant
-    o.chit = (tt > 0.f && tt < 1.f) ? 1.f : 0.f;
-    o.chir = (tr > 0.f && tr < 1.f) ? 1.f : 0.f;
+    // clamp derivative (Q25b): the upper clamp acts only for a positive correction
+    o.chit = (tt > 0.f && (tt < 1.f || a.ptx - r.papr <= 0.f)) ? 1.f : 0.f;
+    o.chir = (tr > 0.f && (tr < 1.f || a.prx - r.papr <= 0.f)) ? 1.f : 0.f;
     o.Tt = fminf(fmaxf(tt, 0.f), 1.f);
     o.Tr = fminf(fmaxf(tr, 0.f), 1.f);
   } else {
     o.Tt = o.Tr = r.T;
-    float chi = (r.T > 0.f && r.T < 1.f) ? 1.f : 0.f;
+    // no correction: T_ij = T_j <= 1 and the clamp is the identity on [0, 1] (Q25b); T_j rounds
+    // to 1 in fp32 behind faint (alpha ~ 1e-14) intervals, so T < 1 must not gate the derivative
+    float chi = r.T > 0.f ? 1.f : 0.f;
     o.chit = o.chir = chi;
   }
   if (!o.ok) { o.gg = 0.f; o.gamma = 0.f; }

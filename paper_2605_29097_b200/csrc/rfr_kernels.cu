@@ -119,13 +119,15 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
   bool domain = false;
 
   // records of one tile: TJ x 48 B = 3 TJ chunks of 16 B spread over the lanes
+  // the tile's records are one contiguous run of TJ x 48 B: copy it as 16-byte chunks
   auto prefetch = [&](int64_t jt, int buf) {
-    for (int c = lane; c < TJ * 3; c += 32) {
-      const int jj = c / 3, part = c % 3;
-      const int64_t j = jt + jj;
-      if (j < j_hi)
-        cp_async16(reinterpret_cast<float4 *>(rbuf + buf * TJ + jj) + part,
-                   reinterpret_cast<const float4 *>(a.rec + j) + part);
+    const int n_chunks = 3 * (int)min((int64_t)TJ, j_hi - jt);
+    const float4 *src = reinterpret_cast<const float4 *>(a.rec + jt);
+    float4 *dst = reinterpret_cast<float4 *>(rbuf + buf * TJ);
+#pragma unroll
+    for (int c0 = 0; c0 < TJ * 3; c0 += 32) {
+      const int c = c0 + lane;
+      if (c < n_chunks) cp_async16(dst + c, src + c);
     }
     cp_async_commit();
   };
@@ -191,13 +193,13 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
         const f2x kpa = pk(ka, ka), kna = pk(-ka, -ka), kpb = pk(kb, kb), knb = pk(-kb, -kb);
         f2x a0 = pk(Ya.x, Ya.y), a1 = pk(Ya.z, Ya.w);
         f2x b0 = pk(Yb.x, Yb.y), b1 = pk(Yb.z, Yb.w);
-        acc[0] = fadd2(fadd2(acc[0], a0), b0);
-        acc[1] = fadd2(fadd2(acc[1], a1), b1);
+        acc2(acc[0], a0); acc2(acc[0], b0);
+        acc2(acc[1], a1); acc2(acc[1], b1);
 #pragma unroll
         for (int m = 1; m < B - 1; ++m) {
           const f2x a2 = ffma2((m & 1) ? kna : kpa, a1, a0);
           const f2x b2 = ffma2((m & 1) ? knb : kpb, b1, b0);
-          acc[m + 1] = fadd2(fadd2(acc[m + 1], a2), b2);
+          acc2(acc[m + 1], a2); acc2(acc[m + 1], b2);
           a0 = a1; a1 = a2;
           b0 = b1; b1 = b2;
         }
@@ -842,8 +844,17 @@ static bool use_tensor_cores() {
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st) {
   if (use_tensor_cores() && adjoint_tc_supported(a.n_f) &&
-      (reinterpret_cast<uintptr_t>(a.X) & 15) == 0)
+      (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
+      (mode != kModeBoth || (reinterpret_cast<uintptr_t>(a.X2) & 15) == 0))
     return counted(launch_adjoint_tc(a, mode, mono, corr, n_splits, st));
+  if (mode == kModeBoth) {          // SIMT: the two sweeps one after the other
+    cudaError_t e = launch_adjoint(a, kModeBwd, mono, corr, n_splits, st);
+    if (e != cudaSuccess) return e;
+    AdjArgs f = a;
+    f.X = a.X2;
+    f.out = a.out2;
+    return launch_adjoint(f, kModeFlt, mono, false, n_splits, st);
+  }
   const int64_t per_cta = (int64_t)kAdjThreads;
   dim3 grid((unsigned)((a.n_s + per_cta - 1) / per_cta), (unsigned)n_splits);
   if (mode == kModeBwd) {

@@ -14,10 +14,11 @@ constexpr int kFwdWarps = kFwdThreads / 32;
 constexpr int kFwdTJ = 16;         // samples per K2 warp tile (B = 32)
 // K2 tile shape per bins-per-lane B: samples per warp tile and CTAs per SM (register budget)
 __host__ __device__ constexpr int fwd_tj(int B) { return B == 32 ? 16 : 8; }
-__host__ __device__ constexpr int fwd_min_blocks(int B) { return B == 32 ? 3 : 5; }
+__host__ __device__ constexpr int fwd_min_blocks(int B) { return B == 32 ? 4 : 5; }
 constexpr int kAdjThreads = 128;   // K3/K4 CTA size
 constexpr int kAdjGA = 8;          // antennas per K3/K4 shared-memory stage
 constexpr int kModeBwd = 0, kModeFlt = 1;
+constexpr int kModeBoth = 2;       // K3 + K4 fused (tensor-core kernel only): X = G, X2 = signal
 constexpr int kFwdTrace = 0, kFwdMFAdj = 1;  // K2 signal tracing / K5 matched-filter adjoint
 
 struct BlendArgs {
@@ -58,6 +59,8 @@ struct AdjArgs {
   const float2 *X;                 // G (K3) or signal (K4), [n_a][n_f]
   int64_t ants_per_split;
   float *out;                      // K3: [split][5][n_s]; K4: [split][n_s] complex
+  const float2 *X2;                // kModeBoth: the signal s, [n_a][n_f] (filter at the samples)
+  float *out2;                     // kModeBoth: [split][n_s] complex partial M
   size_t smem_ant_off;
   unsigned int *flags;
   bool no_gain;

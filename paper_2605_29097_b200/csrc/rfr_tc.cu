@@ -100,20 +100,30 @@ struct PairTC {
 
 }  // namespace
 
-template <int NF>
+template <int NF, int NX>
 struct TCShape {
   static constexpr int P = NF / 16;                  // m1 values
-  static constexpr int N = 2 * P;                    // D columns
-  static constexpr int COLS = 64 + 2 * N;            // A_hi, A_lo (32 each) + 2 D buffers
-  static constexpr int ALLOC = COLS <= 128 ? 128 : 256;
-  static constexpr int MINB = ALLOC == 128 ? 4 : 2;  // CTAs per SM (512 TMEM columns)
+  static constexpr int N1 = 2 * P;                   // D columns per X row
+  static constexpr int N = NX * N1;                  // D columns (NX = 2: [G | s] side by side)
+  // D double-buffered (epilogue of antenna a-1 overlaps the MMA of antenna a) unless that would
+  // halve the CTAs per SM; single-buffered D reads antenna a-1 before the MMA of a is issued.
+  static constexpr int DBUF = (NX == 1 || 64 + 2 * N <= 128) ? 2 : 1;
+  static constexpr int COLS = 64 + DBUF * N;         // A_hi, A_lo (32 each) + D buffers
+  static constexpr int ALLOC = COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512);
+  static constexpr int MINB = 512 / ALLOC;           // CTAs per SM (512 TMEM columns)
 };
 
+// MODE == kModeBoth: K3 and K4 in one sweep (the filter's queries are the samples): the pair
+// geometry, the powers of w and the A operand are shared; B^T stacks the G rows over the signal
+// rows, so one MMA with N = 2 N1 yields both U_G and U_s.
 template <int MODE, bool MONO, bool CORR, int NF>
-__global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(AdjArgs a) {
-  using S = TCShape<NF>;
-  constexpr int P = S::P, N = S::N;
+__global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2 : 1>::MINB)
+    k_adjoint_tc(AdjArgs a) {
+  constexpr int NX = MODE == kModeBoth ? 2 : 1;
+  using S = TCShape<NF, NX>;
+  constexpr int P = S::P, N1 = S::N1, N = S::N, DBUF = S::DBUF;
   constexpr int CH = (N * 8 + kAdjThreads - 1) / kAdjThreads;     // B chunks per thread
+  constexpr int GEO = MODE == kModeFlt ? kModeFlt : kModeBwd;     // geometry / record kind
   static_assert(kAdjThreads == 128, "one TMEM lane per thread");
   __shared__ __align__(128) unsigned char bsm[2 * N * 128];          // B_hi, B_lo [N][32] fp32
   __shared__ __align__(8) unsigned long long mma_bar;
@@ -146,32 +156,67 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
   const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(N >> 3) << 17) |
                          ((unsigned)(128 >> 4) << 24);
 
-  const Rec rec = load_point<MODE>(a, j, valid);
+  const Rec rec = load_point<GEO>(a, j, valid);
   float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
+  float M1 = 0.f, M2 = 0.f;                       // kModeBoth: the filter's complex M
   bool domain = false;
   PairTC prev;
   const double kd16 = a.kd * 16.0;
+
+  // epilogue of antenna ai-1: U from TMEM, Horner over m1, Eq. 5 / M sums
+  auto epilogue = [&](int ai) {
+    const unsigned d = d0 + (unsigned)((DBUF == 2 ? ((ai - 1) & 1) : 0) * N) + lane_off;
+#pragma unroll
+    for (int x = 0; x < NX; ++x) {
+      float Ur[P], Ui[P];
+#pragma unroll
+      for (int c = 0; c < N1; c += 16) {
+        unsigned v[16];
+        tmem_ld16(d + x * N1 + c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+          Ur[(c + q) / 2] = __uint_as_float(v[q]);
+          Ui[(c + q) / 2] = __uint_as_float(v[q + 1]);
+        }
+      }
+      const f2x W = pk(prev.Wc, prev.Ws), W2 = pk(-prev.Ws, prev.Wc);
+      f2x h = pk(Ur[P - 1], Ui[P - 1]);
+#pragma unroll
+      for (int m1 = P - 2; m1 >= 0; --m1) {
+        const float2 hv = upk(h);
+        const f2x t = ffma2(W, pk(hv.x, hv.x), pk(Ur[m1], Ui[m1]));
+        h = ffma2(W2, pk(hv.y, hv.y), t);
+      }
+      const float2 hh = upk(h);
+      if (MODE != kModeBoth)
+        adj_accumulate<MODE>(prev.g, prev.ec, prev.es, hh.x, hh.y, S1, S2, S3x, S3y, S3z);
+      else if (x == 0)
+        adj_accumulate<kModeBwd>(prev.g, prev.ec, prev.es, hh.x, hh.y, S1, S2, S3x, S3y, S3z);
+      else
+        adj_accumulate<kModeFlt>(prev.g, prev.ec, prev.es, hh.x, hh.y, M1, M2, S3x, S3y, S3z);
+    }
+  };
 
   for (int ai = 0; ai <= na; ++ai) {
     PairTC cur;
     if (ai < na) {
       // ---------------- SIMT: pair data and the powers of w for antenna ai (overlaps MMA ai-1)
       const int64_t ia = i_lo + ai;
-      // this antenna's B chunks come from 16-byte pieces of its X row: load them first so the
+      // this antenna's B chunks come from 16-byte pieces of its X row(s): load them first so the
       // global latency overlaps the geometry below
       float4 xq[CH];
-      {
-        const float4 *X4 = reinterpret_cast<const float4 *>(a.X + ia * NF);
 #pragma unroll
-        for (int r = 0; r < CH; ++r) {
-          const int q = tid + r * kAdjThreads;
-          const int n = q % N, c = q / N;
-          xq[r] = q < N * 8 ? X4[(16 * (n >> 1) + 2 * c) >> 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+      for (int r = 0; r < CH; ++r) {
+        const int q = tid + r * kAdjThreads;
+        const int n = q % N, c = q / N;
+        const int x = n / N1, nn = n % N1;
+        const float4 *X4 = reinterpret_cast<const float4 *>((x == 0 ? a.X : a.X2) + ia * NF);
+        xq[r] = q < N * 8 ? X4[(16 * (nn >> 1) + 2 * c) >> 1] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       const AntD an = load_ant<MONO>(a, ia);
       double L;
-      if (MODE == kModeBwd) {
+      if (GEO == kModeBwd) {
         pair_geometry<MONO, CORR>(rec, an, no_gain, cur.g);
         domain |= valid && !cur.g.ok;
         L = cur.g.L;
@@ -212,11 +257,12 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
           lv[2 * k + 1] = __float_as_uint(lo.y);
         }
       }
-      // ---------------- MMA ai-1 must be done before A / B are overwritten
+      // ---------------- MMA ai-1 must be done before A / B (and a single D) are reused
       if (ai > 0) mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
       tc_fence_after();
       tmem_st32(a_hi + lane_off, hv);
       tmem_st32(a_lo + lane_off, lv);
+      if (DBUF == 1 && ai > 0) epilogue(ai);      // read D of ai-1 before the MMA of ai
       // B^T of antenna ai, one 16-byte chunk (row n, columns 4c..4c+3) per thread and pass: the
       // chunk holds bins b, b+1 (b = 16 (n / 2) + 2c) as (Re, -Im) (n even) or (Im, Re) (n odd).
       // Thread -> (n = q % N, c = q / N) makes a warp's 32 stores cover the 8 rows of a core
@@ -245,7 +291,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
       __syncthreads();
       tc_fence_after();
       if (tid == 0) {
-        const unsigned d = d0 + (unsigned)((ai & 1) * N);
+        const unsigned d = d0 + (unsigned)((DBUF == 2 ? (ai & 1) : 0) * N);
         const unsigned acol[3] = {a_hi, a_hi, a_lo};
         const unsigned char *bs[3] = {Bhi, Blo, Bhi};
 #pragma unroll
@@ -258,41 +304,23 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF>::MINB) k_adjoint_tc(A
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];"
                      ::"l"((uint64_t)smem_u32(&mma_bar)) : "memory");
       }
-    }
-    if (ai > 0) {
-      // ---------------- epilogue of antenna ai-1: U from TMEM, Horner over m1, Eq. 5 / M sums
-      if (ai == na) {
-        mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
-        tc_fence_after();
-      }
-      const unsigned d = d0 + (unsigned)(((ai - 1) & 1) * N) + lane_off;
-      float Ur[P], Ui[P];
-#pragma unroll
-      for (int c = 0; c < N; c += 16) {
-        unsigned v[16];
-        tmem_ld16(d + c, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int q = 0; q < 16; q += 2) {
-          Ur[(c + q) / 2] = __uint_as_float(v[q]);
-          Ui[(c + q) / 2] = __uint_as_float(v[q + 1]);
-        }
-      }
-      const f2x W = pk(prev.Wc, prev.Ws), W2 = pk(-prev.Ws, prev.Wc);
-      f2x h = pk(Ur[P - 1], Ui[P - 1]);
-#pragma unroll
-      for (int m1 = P - 2; m1 >= 0; --m1) {
-        const float2 hv = upk(h);
-        const f2x t = ffma2(W, pk(hv.x, hv.x), pk(Ur[m1], Ui[m1]));
-        h = ffma2(W2, pk(hv.y, hv.y), t);
-      }
-      const float2 hh = upk(h);
-      adj_accumulate<MODE>(prev.g, prev.ec, prev.es, hh.x, hh.y, S1, S2, S3x, S3y, S3z);
+      if (DBUF == 2 && ai > 0) epilogue(ai);
+    } else if (ai > 0) {
+      mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
+      tc_fence_after();
+      epilogue(ai);
     }
     prev = cur;
   }
   if (domain) atomicOr(a.flags, 1u);
-  if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
+  if (valid) {
+    if (MODE != kModeBoth) {
+      adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
+    } else {
+      adj_store<kModeBwd>(a, j, S1, S2, S3x, S3y, S3z);
+      reinterpret_cast<float2 *>(a.out2)[(int64_t)blockIdx.y * a.n_s + j] = make_float2(M1, M2);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
@@ -326,6 +354,12 @@ cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, 
                           : tc_nf<kModeBwd, true, false>(a, grid, st);
     return corr ? tc_nf<kModeBwd, false, true>(a, grid, st)
                 : tc_nf<kModeBwd, false, false>(a, grid, st);
+  }
+  if (mode == kModeBoth) {
+    if (mono) return corr ? tc_nf<kModeBoth, true, true>(a, grid, st)
+                          : tc_nf<kModeBoth, true, false>(a, grid, st);
+    return corr ? tc_nf<kModeBoth, false, true>(a, grid, st)
+                : tc_nf<kModeBoth, false, false>(a, grid, st);
   }
   return mono ? tc_nf<kModeFlt, true, false>(a, grid, st)
               : tc_nf<kModeFlt, false, false>(a, grid, st);

@@ -61,7 +61,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too sm
 
 EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_filter_partial",
            "rfr_filter_power", "rfr_backward", "rfr_backward_partial", "rfr_backward_finish",
-           "rfr_filter_backward", "rfr_heatmap_loss",
+           "rfr_backward_filter", "rfr_filter_backward", "rfr_heatmap_loss",
            "rfr_comm_unique_id", "rfr_comm_init", "rfr_comm_destroy",
            "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count")
 
@@ -95,6 +95,7 @@ def load(path: str = LIB_PATH):
         "rfr_backward": [vp, S, f, A, G, O, R, vp, W, vp],
         "rfr_backward_partial": [vp, S, f, A, G, O, vp, W, vp],
         "rfr_backward_finish": [vp, S, f, O, R, W, vp],
+        "rfr_backward_filter": [vp, vp, S, f, A, G, O, R, vp, vp, vp, W, vp],
         "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, W, vp],
         "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, W, vp],
         "rfr_poll_flags": [W, C.POINTER(u32)],
@@ -342,6 +343,20 @@ def rfr_backward(grad_signal: torch.Tensor, samples: DeviceSamples, sharpness: f
                                C.byref(g), C.byref(o), C.byref(r), _comm(comm), _ws(ws),
                                _stream(stream)), "rfr_backward")
     return out
+
+
+def rfr_backward_filter(grad_signal: torch.Tensor, signal: torch.Tensor, samples: DeviceSamples,
+                        sharpness: float, ants: DeviceAntennas, grid, out: Grads,
+                        power: torch.Tensor, ws: torch.Tensor, mf: Optional[torch.Tensor] = None,
+                        flags: int = 0, comm: "Comm" = None, stream=None):
+    """K3 + K4 in one sweep: rfr_backward from grad_signal and rfr_filter of signal at the sample
+    points (see include/librfr.h)."""
+    s, a, g, o, r = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags), out.struct()
+    _check(load().rfr_backward_filter(_ptr(grad_signal), _ptr(signal), C.byref(s), float(sharpness),
+                                      C.byref(a), C.byref(g), C.byref(o), C.byref(r), _ptr(power),
+                                      _ptr(mf), _comm(comm), _ws(ws), _stream(stream)),
+           "rfr_backward_filter")
+    return out, power
 
 
 def rfr_backward_partial(grad_signal, samples: DeviceSamples, sharpness: float,

@@ -382,6 +382,26 @@ def test_backward_partials_sum_over_antenna_shards():
     assert np.linalg.norm(full - parts) <= 1e-12 * np.linalg.norm(full)
 
 
+def test_q25b_uncorrected_clamp_is_identity_including_t_equal_one():
+    """Without the Eq. 7 correction A_ij = w g gamma T_j^2, so dA/dT_j = 2 w g gamma T_j: the
+    partials obey S2_j T_j = 2 S1_j for every T_j > 0 -- including the samples where T_j = 1
+    exactly (first samples, and samples behind intervals whose alpha rounds away), where the
+    [0, 1] clamp is the identity on the feasible side (reading Q25b)."""
+    p = synth.make("c1")
+    b = p.bundles[0]
+    S = b.samples.subset_rays(np.arange(0, 256, 5))
+    rng = np.random.default_rng(21)
+    G = rng.standard_normal((64, 64)) + 1j * rng.standard_normal((64, 64))
+    part = oracle.backward_partials(G, S, p.sharpness, b.antennas, p.grid)
+    _, _, T = oracle.blend(S.sdf, S.n_rays, S.n_per_ray, p.sharpness)
+    on = T > 0
+    assert np.any(T == 1.0) and np.any((T > 0) & (T < 1))
+    lhs, rhs = part[on, 1] * T[on], 2.0 * part[on, 0]
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(rhs)
+    one = T == 1.0
+    assert np.allclose(part[one, 1], 2.0 * part[one, 0], rtol=1e-12, atol=0)
+
+
 # ------------------------------------------------------------------------------------------ P9
 def test_p9_filter_autocorrelation_is_n_freq():
     grid = FreqGrid(77e9, 62.5e6, 64)

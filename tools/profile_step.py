@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--ants", type=int, default=0, help="profile on the first N antennas only")
+    ap.add_argument("--separate", action="store_true", help="filter and backward as two sweeps")
     a = ap.parse_args()
     p = synth.make(a.config)
     b = p.bundles[0]
@@ -39,9 +40,14 @@ def main():
     out = rfr.Grads.empty(n, dev)
     for _ in range(a.steps):
         rfr.rfr_forward(S, p.sharpness, A, p.grid, sig, ws)
-        rfr.rfr_filter(sig, A, p.grid, S.x, S.y, S.z, P, ws, mf=M)
-        rfr.rfr_backward_partial(G, S, p.sharpness, A, p.grid, part, ws, flags=rfr.RFR_REUSE_BLEND)
-        rfr.rfr_backward_finish(part, S, p.sharpness, out, ws, flags=rfr.RFR_REUSE_BLEND)
+        if a.separate:
+            rfr.rfr_filter(sig, A, p.grid, S.x, S.y, S.z, P, ws, mf=M)
+            rfr.rfr_backward_partial(G, S, p.sharpness, A, p.grid, part, ws,
+                                     flags=rfr.RFR_REUSE_BLEND)
+            rfr.rfr_backward_finish(part, S, p.sharpness, out, ws, flags=rfr.RFR_REUSE_BLEND)
+        else:
+            rfr.rfr_backward_filter(G, sig, S, p.sharpness, A, p.grid, out, P, ws, mf=M,
+                                    flags=rfr.RFR_REUSE_BLEND)
         rfr.rfr_filter_backward(P, M, A, p.grid, S.x, S.y, S.z, G, ws, power=P, eps=1e-20)
     torch.cuda.synchronize()
     print("profile_step ok", a.config, rfr.rfr_launch_count())
