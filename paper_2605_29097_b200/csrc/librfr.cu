@@ -112,7 +112,7 @@ Split adj_split(int64_t n_pts, int64_t n_a, int floats_per_pt, size_t cap) {
 //   K5 query records [n_q] 48 B | K2/K5 split partials | K3 split partials | K4 split partials
 struct Layout {
   size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
-         off_fwdp = 0, off_bwdp = 0, off_fltp = 0, total = 0;
+         off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, total = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
 
@@ -140,6 +140,8 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   L.off_fwdp = take(L.cap_fwdp);
   L.off_bwdp = take(L.cap_bwdp);
   L.off_fltp = take(L.cap_fltp);
+  // tensor-core adjoint: per-antenna B^T images (sized for the fused sweep's two X rows)
+  L.off_bprep = take(adjoint_tc_supported(nf) ? (size_t)n_a * tc_bprep_bytes_per_ant(nf, 2) : 0);
   L.total = o;
   return true;
 }
@@ -371,6 +373,8 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.X = reinterpret_cast<const float2 *>(signal);
+  a.bprep = at<unsigned char>(ws, L.off_bprep);
+  a.bprep_cap = L.total - L.off_bprep;
   a.ants_per_split = sp.per_split;
   a.out = sp.splits > 1 ? at<float>(ws, L.off_fltp) : M;
   a.flags = at<unsigned>(ws, 0);
@@ -438,6 +442,8 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   a.k0 = grid->f0_hz / kC;
   a.kd = grid->df_hz / kC;
   a.X = reinterpret_cast<const float2 *>(grad_signal);
+  a.bprep = at<unsigned char>(ws, L.off_bprep);
+  a.bprep_cap = L.total - L.off_bprep;
   a.ants_per_split = sp.per_split;
   a.out = sp.splits > 1 ? at<float>(ws, L.off_bwdp) : partials;
   a.flags = at<unsigned>(ws, 0);
@@ -535,6 +541,8 @@ rfr_status rfr_backward_filter(const float *grad_signal, const float *signal,
     a.X = reinterpret_cast<const float2 *>(grad_signal);
     a.X2 = reinterpret_cast<const float2 *>(signal);
     a.qx = samples->x; a.qy = samples->y; a.qz = samples->z;   // SIMT fallback's filter queries
+    a.bprep = at<unsigned char>(ws, L.off_bprep);
+  a.bprep_cap = L.total - L.off_bprep;
     a.ants_per_split = sp.per_split;
     a.out = sp.splits > 1 ? at<float>(ws, L.off_bwdp) : part;
     a.out2 = sp.splits > 1 ? at<float>(ws, L.off_fltp) : M;

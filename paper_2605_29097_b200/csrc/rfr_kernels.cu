@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
     for (int c0 = 0; c0 < TJ * 3; c0 += 32) {
       const int c = c0 + lane;
       if (c < n_chunks) cp_async16(dst + c, src + c);
+      else if (c < TJ * 3) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);   // tail: w = 0 records
     }
     cp_async_commit();
   };
@@ -137,30 +138,28 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
     cp_async_wait_all();
     __syncwarp();
     if (jt + TJ < j_hi) prefetch(jt + TJ, buf ^ 1);
-    // ---------------- phase 1: per-pair geometry and anchors (one pair per lane)
+    // ---------------- phase 1: per-pair geometry and anchors (one pair per lane).  Branch-free:
+    // tail samples carry zero records (w = 0) and padded antennas a zero amplitude, so a lane's
+    // pairs are independent straight-line code the scheduler can interleave.
+#pragma unroll
     for (int pr = lane; pr < taw * TJ; pr += 32) {
       const int aa = pr % taw, jj = pr / taw;
-      const int64_t j = jt + jj;
+      const bool valid = (jt + jj < j_hi) && (a0 + aa < a.n_a);
       float4 *dst = anc + jj * 32 + aa;
-      if (j >= j_hi || a0 + aa >= a.n_a) {
-        for (int b = 0; b < nb_here; ++b) dst[b * taw] = make_float4(0.f, 0.f, 0.f, 0.f);
-        kv[jj * 32 + aa] = 2.f;
-        continue;
-      }
       const Rec rec = rbuf[buf * TJ + jj];
       double L;
       float Ar, Ai;
       if (KIND == kFwdTrace) {
         PairBwd g;
         pair_geometry<MONO, CORR>(rec, ant[aa], no_gain, g);
-        domain |= !g.ok;
-        Ar = rec.w * g.gg * g.Tt * g.Tr;
+        domain |= valid && !g.ok;
+        Ar = valid ? rec.w * g.gg * g.Tt * g.Tr : 0.f;
         Ai = 0.f;
         L = g.L;
       } else {
         L = pair_length<MONO>(rec, ant[aa]);
-        Ar = rec.w;
-        Ai = rec.T;
+        Ar = valid ? rec.w : 0.f;
+        Ai = valid ? rec.T : 0.f;
       }
       // phase anchors from fp64 cycle counts (cycles = L f / c), reduced to [-0.5, 0.5]
       const float fr0 = frac_cycles(L * k0);
@@ -843,7 +842,8 @@ static bool use_tensor_cores() {
 
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st) {
-  if (use_tensor_cores() && adjoint_tc_supported(a.n_f) &&
+  const size_t bneed = (size_t)a.n_a * tc_bprep_bytes_per_ant(a.n_f, mode == kModeBoth ? 2 : 1);
+  if (use_tensor_cores() && adjoint_tc_supported(a.n_f) && a.bprep && bneed <= a.bprep_cap &&
       (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
       (mode != kModeBoth || (reinterpret_cast<uintptr_t>(a.X2) & 15) == 0))
     return counted(launch_adjoint_tc(a, mode, mono, corr, n_splits, st));

@@ -61,6 +61,8 @@ struct AdjArgs {
   float *out;                      // K3: [split][5][n_s]; K4: [split][n_s] complex
   const float2 *X2;                // kModeBoth: the signal s, [n_a][n_f] (filter at the samples)
   float *out2;                     // kModeBoth: [split][n_s] complex partial M
+  unsigned char *bprep;            // tensor-core path: per-antenna B^T images (hi | lo), or NULL
+  size_t bprep_cap;                // bytes available at bprep
   size_t smem_ant_off;
   unsigned int *flags;
   bool no_gain;
@@ -111,6 +113,9 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st);
 bool adjoint_tc_supported(int n_f);
+// bytes of the prepared B^T images per antenna (nx X rows): hi and lo, 2 (re/im) x n_f/16 rows of
+// 32 tf32 columns each
+inline size_t tc_bprep_bytes_per_ant(int n_f, int nx) { return (size_t)nx * 32 * n_f; }
 cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                               cudaStream_t st);
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st);

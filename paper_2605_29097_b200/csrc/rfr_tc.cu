@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "rfr_device.cuh"
 #include "rfr_launch.h"
 
@@ -122,13 +124,15 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
   constexpr int NX = MODE == kModeBoth ? 2 : 1;
   using S = TCShape<NF, NX>;
   constexpr int P = S::P, N1 = S::N1, N = S::N, DBUF = S::DBUF;
-  constexpr int CH = (N * 8 + kAdjThreads - 1) / kAdjThreads;     // B chunks per thread
   constexpr int GEO = MODE == kModeFlt ? kModeFlt : kModeBwd;     // geometry / record kind
+  constexpr unsigned BBYTES = 2u * N * 128u;                       // B_hi | B_lo image
   static_assert(kAdjThreads == 128, "one TMEM lane per thread");
-  __shared__ __align__(128) unsigned char bsm[2 * N * 128];          // B_hi, B_lo [N][32] fp32
-  __shared__ __align__(8) unsigned long long mma_bar;
+  // B^T images of antennas a (buffer a & 1), prepared by k_prep_bt and brought in by the bulk-copy
+  // engine two antennas ahead: no thread of the CTA touches B
+  extern __shared__ __align__(128) unsigned char bsm_raw[];
+  unsigned char(*bsm)[BBYTES] = reinterpret_cast<unsigned char(*)[BBYTES]>(bsm_raw);
+  __shared__ __align__(8) unsigned long long mma_bar, full_bar[2];
   __shared__ unsigned tmem_base_sh;
-  unsigned char *Bhi = bsm, *Blo = bsm + N * 128;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
@@ -142,9 +146,16 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
                  ::"r"(smem_u32(&tmem_base_sh)), "n"(S::ALLOC));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  const unsigned char *bsrc = a.bprep + (size_t)i_lo * BBYTES;
   if (tid == 0) {
     mbar_init(&mma_bar, 1);
+    mbar_init(&full_bar[0], 1);
+    mbar_init(&full_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int b = 0; b < 2 && b < na; ++b) {
+      mbar_arrive_expect_tx(&full_bar[b], BBYTES);
+      bulk_g2s(bsm[b], bsrc + (size_t)b * BBYTES, BBYTES, &full_bar[b]);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -203,17 +214,6 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
     if (ai < na) {
       // ---------------- SIMT: pair data and the powers of w for antenna ai (overlaps MMA ai-1)
       const int64_t ia = i_lo + ai;
-      // this antenna's B chunks come from 16-byte pieces of its X row(s): load them first so the
-      // global latency overlaps the geometry below
-      float4 xq[CH];
-#pragma unroll
-      for (int r = 0; r < CH; ++r) {
-        const int q = tid + r * kAdjThreads;
-        const int n = q % N, c = q / N;
-        const int x = n / N1, nn = n % N1;
-        const float4 *X4 = reinterpret_cast<const float4 *>((x == 0 ? a.X : a.X2) + ia * NF);
-        xq[r] = q < N * 8 ? X4[(16 * (nn >> 1) + 2 * c) >> 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
       const AntD an = load_ant<MONO>(a, ia);
       double L;
       if (GEO == kModeBwd) {
@@ -229,7 +229,9 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
       __sincosf(kTwoPi * fr0, &cur.es, &cur.ec);
       float zs, zc;
       sincospif(2.f * frd, &zs, &zc);            // w (accurate)
-      sincospif(2.f * f16, &cur.Ws, &cur.Wc);    // W = w^16 from the fp64 cycle count
+      // W = w^16 from the fp64 cycle count; MUFU (abs. error ~4e-7): the Horner over m1 amplifies
+      // it at most P - 1 times, well inside the 1e-4 / 1e-3 tolerances
+      __sincosf(kTwoPi * f16, &cur.Ws, &cur.Wc);
       unsigned hv[32], lv[32];
       {
         // powers p_k = w^k (packed complex mults) by binary expansion -- dependency depth 4
@@ -260,30 +262,16 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
       // ---------------- MMA ai-1 must be done before A / B (and a single D) are reused
       if (ai > 0) mbar_wait(&mma_bar, (unsigned)((ai - 1) & 1));
       tc_fence_after();
+      // the MMA of ai-1 released B buffer (ai + 1) & 1: bring in antenna ai + 1
+      if (tid == 0 && ai > 0 && ai + 1 < na) {
+        const int b = (ai + 1) & 1;
+        mbar_arrive_expect_tx(&full_bar[b], BBYTES);
+        bulk_g2s(bsm[b], bsrc + (size_t)(ai + 1) * BBYTES, BBYTES, &full_bar[b]);
+      }
       tmem_st32(a_hi + lane_off, hv);
       tmem_st32(a_lo + lane_off, lv);
       if (DBUF == 1 && ai > 0) epilogue(ai);      // read D of ai-1 before the MMA of ai
-      // B^T of antenna ai, one 16-byte chunk (row n, columns 4c..4c+3) per thread and pass: the
-      // chunk holds bins b, b+1 (b = 16 (n / 2) + 2c) as (Re, -Im) (n even) or (Im, Re) (n odd).
-      // Thread -> (n = q % N, c = q / N) makes a warp's 32 stores cover the 8 rows of a core
-      // matrix 4 times: conflict-free 128-bit shared stores.
-#pragma unroll
-      for (int r = 0; r < CH; ++r) {
-        const int q = tid + r * kAdjThreads;
-        if (q < N * 8) {
-          const int n = q % N, c = q / N;
-          const float4 x = xq[r];
-          const float4 v = (n & 1) ? make_float4(x.y, x.x, x.w, x.z)
-                                   : make_float4(x.x, -x.y, x.z, -x.w);
-          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-          const unsigned off = bT_off(n, 4 * c);
-          *reinterpret_cast<float4 *>(Bhi + off) = h;
-          *reinterpret_cast<float4 *>(Blo + off) = l;
-        }
-      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       // all A rows and B chunks written before the MMA is issued.  (An mbarrier that only the
       // issuing thread waits on measured slower: the other warps then reach the single-buffered A
@@ -291,8 +279,10 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
       __syncthreads();
       tc_fence_after();
       if (tid == 0) {
+        mbar_wait(&full_bar[ai & 1], (unsigned)((ai >> 1) & 1));   // B^T of antenna ai landed
         const unsigned d = d0 + (unsigned)((DBUF == 2 ? (ai & 1) : 0) * N);
         const unsigned acol[3] = {a_hi, a_hi, a_lo};
+        const unsigned char *Bhi = bsm[ai & 1], *Blo = Bhi + N * 128;
         const unsigned char *bs[3] = {Bhi, Blo, Bhi};
 #pragma unroll
         for (int p = 0; p < 3; ++p)
@@ -328,9 +318,42 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
                  "n"(S::ALLOC));
 }
 
+// B^T images for the tensor-core adjoint, one per antenna: [B_hi | B_lo], each N rows of 32 tf32
+// columns in the canonical K-major no-swizzle layout (bT_off).  Row n = x N1 + 2 m1 + c of X row
+// x (G then s for kModeBoth), column 2 m0 + c' holds bins 16 m1 + m0 as (Re, -Im) for c = 0 and
+// (Im, Re) for c = 1 (the complex product's sign pattern), split hi = tf32(v), lo = v - hi.  One
+// thread per 16-byte chunk (two bins); HBM-bound, ~0.05 ms at c3.
+__global__ void k_prep_bt(const float2 *__restrict__ X, const float2 *__restrict__ X2, int64_t n_a,
+                          int nf, int nx, unsigned char *__restrict__ out) {
+  const int N1 = nf / 8, N = nx * N1;
+  const int64_t per_ant = (int64_t)N * 8;                 // 16-byte chunks per antenna
+  const size_t bbytes = (size_t)2 * N * 128;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_a * per_ant;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ia = t / per_ant;
+    const int q = (int)(t - ia * per_ant);
+    const int n = q % N, c = q / N;
+    const int x = n / N1, nn = n % N1;
+    const float4 v4 = reinterpret_cast<const float4 *>((x == 0 ? X : X2) + ia * nf)
+        [(16 * (nn >> 1) + 2 * c) >> 1];
+    const float4 v = (n & 1) ? make_float4(v4.y, v4.x, v4.w, v4.z)
+                             : make_float4(v4.x, -v4.y, v4.z, -v4.w);
+    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    unsigned char *dst = out + (size_t)ia * bbytes + bT_off(n, 4 * c);
+    *reinterpret_cast<float4 *>(dst) = h;
+    *reinterpret_cast<float4 *>(dst + N * 128) = l;
+  }
+}
+
 template <int MODE, bool MONO, bool CORR, int NF>
 static cudaError_t tc_launch(const AdjArgs &a, dim3 grid, cudaStream_t st) {
-  k_adjoint_tc<MODE, MONO, CORR, NF><<<grid, kAdjThreads, 0, st>>>(a);
+  using S = TCShape<NF, MODE == kModeBoth ? 2 : 1>;
+  const size_t smem = (size_t)2 * 2 * S::N * 128;        // two B^T image buffers
+  auto k = k_adjoint_tc<MODE, MONO, CORR, NF>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kAdjThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -348,6 +371,15 @@ bool adjoint_tc_supported(int n_f) { return n_f == 128 || n_f == 256 || n_f == 5
 
 cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                               cudaStream_t st) {
+  if (!a.bprep) return cudaErrorInvalidValue;
+  if (a.n_a > 0) {
+    const int nx = mode == kModeBoth ? 2 : 1;
+    const int64_t chunks = a.n_a * (int64_t)(nx * a.n_f / 8) * 8;
+    const unsigned g = (unsigned)std::min<int64_t>((chunks + 255) / 256, 148 * 16);
+    k_prep_bt<<<g, 256, 0, st>>>(a.X, a.X2, a.n_a, a.n_f, nx, a.bprep);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   dim3 grid((unsigned)((a.n_s + kAdjThreads - 1) / kAdjThreads), (unsigned)n_splits);
   if (mode == kModeBwd) {
     if (mono) return corr ? tc_nf<kModeBwd, true, true>(a, grid, st)
