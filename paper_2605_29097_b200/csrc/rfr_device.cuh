@@ -266,6 +266,30 @@ __device__ __forceinline__ AntD load_ant(const AdjArgs &a, int64_t ia) {
   return d;
 }
 
+// fp32 antenna record as stored (prefetched in registers), widened to AntD at use
+struct AntF {
+  float x, y, z, rx, ry, rz, ptx, prx;
+};
+template <bool MONO>
+__device__ __forceinline__ AntF load_antf(const AdjArgs &a, int64_t ia) {
+  AntF d;
+  d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
+  if (MONO) { d.rx = d.ry = d.rz = 0.f; }
+  else { d.rx = a.rx_x[ia]; d.ry = a.rx_y[ia]; d.rz = a.rx_z[ia]; }
+  d.ptx = a.phi_tx ? a.phi_tx[ia] : 1.f;
+  d.prx = a.phi_rx ? a.phi_rx[ia] : (MONO ? d.ptx : 1.f);
+  return d;
+}
+template <bool MONO>
+__device__ __forceinline__ AntD widen_ant(const AntF &f) {
+  AntD d;
+  d.x = f.x; d.y = f.y; d.z = f.z;
+  if (MONO) { d.rx = d.x; d.ry = d.y; d.rz = d.z; }
+  else { d.rx = f.rx; d.ry = f.ry; d.rz = f.rz; }
+  d.ptx = f.ptx; d.prx = f.prx;
+  return d;
+}
+
 template <int MODE>
 __device__ __forceinline__ Rec load_point(const AdjArgs &a, int64_t j, bool valid) {
   Rec rec;

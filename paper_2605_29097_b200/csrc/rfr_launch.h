@@ -113,9 +113,9 @@ cudaError_t launch_heat_loss(const float *P, const float *Pgt, int64_t n, const 
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st);
 bool adjoint_tc_supported(int n_f);
-// bytes of the prepared B^T images per antenna (nx X rows): hi and lo, 2 (re/im) x n_f/16 rows of
-// 32 tf32 columns each
-inline size_t tc_bprep_bytes_per_ant(int n_f, int nx) { return (size_t)nx * 32 * n_f; }
+// bytes of the prepared B^T data per antenna (nx X rows): fp16 hi and lo images, nx x n_f / 8
+// rows of 32 fp16 columns each, plus the float2 of inverse row scales
+inline size_t tc_bprep_bytes_per_ant(int n_f, int nx) { return (size_t)nx * 16 * n_f + 8; }
 cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                               cudaStream_t st);
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st);

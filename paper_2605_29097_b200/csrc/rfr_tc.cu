@@ -13,14 +13,17 @@
 //     B^T[2 m1][2 m0 + c]   : (Re X, -Im X)[c] of bin 16 m1 + m0   -> D[j][2 m1]     = Re U[m1]
 //     B^T[2 m1 + 1][2m0 + c]: (Im X,  Re X)[c]                     -> D[j][2 m1 + 1] = Im U[m1]
 //                                                                   (N = 2P, P = NF / 16)
-// run on the 5th-generation tensor cores as tcgen05.mma.kind::tf32 with A in tensor memory (each
-// thread writes its own row with tcgen05.st), B in shared memory (K-major, no swizzle) and D in
-// tensor memory.  fp32 accuracy comes from the 3xTF32 split (A_hi B_hi + A_hi B_lo + A_lo B_hi,
-// hi = x truncated to tf32, lo = x - hi): 3xTF32 measured 7e-7 relative against fp64 on random operands
-// (tools/microbench/umma_tf32_probe.cu).  The per-pair SIMT work (fp64 geometry, the 16 powers of w,
-// the Horner over m1, the Eq. 5 epilogue) overlaps the MMAs of the previous antenna: A is single-
-// buffered (the MMA of antenna a-1 is awaited after the SIMT part of antenna a), D is double-
-// buffered in tensor memory.
+// run on the 5th-generation tensor cores as tcgen05.mma.kind::f16 (fp16 operands, fp32
+// accumulation) with A in tensor memory (each thread writes its own row with tcgen05.st, two fp16
+// per 32-bit column, even K element in the low half), B in shared memory (K-major, no swizzle) and
+// D in tensor memory.  fp32 accuracy comes from the "3xFP16" split (A_hi B_hi + A_hi B_lo +
+// A_lo B_hi, hi = x with the 13 low mantissa bits cleared, exact in fp16, lo = x - hi): 22
+// significant bits, like 3xTF32 (fp16 and tf32 share the 10-bit mantissa), at twice the tf32 MMA
+// rate (tools/microbench/umma_f16_probe.cu: rel-L2 4.7e-7; 232 vs 432 tensor cycles per 128 x 64
+// x 32 x 3 round).  fp16's range is handled by scaling every B row (antenna, X) by a power of two
+// to max |component| in [0.5, 1) in k_prep_bt; the epilogue undoes it.  The per-pair SIMT work
+// (fp64 geometry, the 16 powers of w, the Horner over m1, the Eq. 5 epilogue) overlaps the MMAs
+// of the previous antenna.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,27 +46,31 @@ __device__ __forceinline__ uint64_t umma_sdesc(unsigned saddr, unsigned lbo, uns
   return d;
 }
 
-// byte offset of element (row n, column k) of a K-major interleaved operand with 32 columns:
-// 16-byte chunks of 4 columns; 8 rows x 16 B core matrices; chunk stride 128 B, row-group 1024 B
+// byte offset of element (row n, column k) of a K-major 16-bit operand with 32 columns: 16-byte
+// chunks of 8 columns; 8 rows x 16 B core matrices; chunk stride 128 B, row-group stride 512 B
 __device__ __forceinline__ unsigned bT_off(int n, int k) {
-  return (unsigned)((k >> 2) * 128 + (n >> 3) * 1024 + (n & 7) * 16 + (k & 3) * 4);
+  return (unsigned)((k >> 3) * 128 + (n >> 3) * 512 + (n & 7) * 16 + (k & 7) * 2);
+}
+// two floats -> f16x2, `lo_elem` in bits 0..15 (the even K element of an A column)
+__device__ __forceinline__ unsigned pack_h2(float lo_elem, float hi_elem) {
+  unsigned r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
 }
 
-// 3xTF32 split by truncation: hi = x with the 13 low mantissa bits cleared (exactly a tf32
-// value, one LOP3), lo = x - hi (exact in fp32; the tensor core truncates it to tf32, leaving a
-// relative error <= 2^-21 of x).  cvt.rna.tf32 compiles to 4 SASS instructions on sm_100a.
+// hi part of the 3-term split: x with the 13 low mantissa bits cleared (one LOP3).  It has 11
+// significant bits, so it is exact in fp16 for |x| >= 2^-14 (below that the fp16 conversion
+// leaves an absolute error < 2^-25 of the row scale); lo = x - hi is exact in fp32.
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-__device__ __forceinline__ void tmem_st32(unsigned addr, const unsigned (&v)[32]) {
+__device__ __forceinline__ void tmem_st16(unsigned addr, const unsigned (&v)[16]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(addr),
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
-      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
-      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 
@@ -84,12 +91,12 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// D[tmem] (+)= A[tmem] . B[smem]^T, one K step of 8 tf32 columns
-__device__ __forceinline__ void umma_tf32_ts(unsigned d_tmem, unsigned a_tmem, uint64_t b_desc,
-                                             unsigned idesc, unsigned accumulate) {
+// D[tmem] (+)= A[tmem] . B[smem]^T, one K step of 16 fp16 columns (8 TMEM columns of A)
+__device__ __forceinline__ void umma_f16_ts(unsigned d_tmem, unsigned a_tmem, uint64_t b_desc,
+                                            unsigned idesc, unsigned accumulate) {
   asm volatile(
       "{\n .reg .pred pa;\n setp.ne.b32 pa, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, pa;\n}" ::"r"(d_tmem),
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, pa;\n}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
@@ -98,6 +105,7 @@ struct PairTC {
   PairBwd g;
   float ec, es;     // E = e^{+j 2 pi f0 tau}
   float Wc, Ws;     // W = w^16
+  float inv[2];     // 1 / (B row scale) of the antenna's X rows
 };
 
 }  // namespace
@@ -109,8 +117,8 @@ struct TCShape {
   static constexpr int N = NX * N1;                  // D columns (NX = 2: [G | s] side by side)
   // D double-buffered (epilogue of antenna a-1 overlaps the MMA of antenna a) unless that would
   // halve the CTAs per SM; single-buffered D reads antenna a-1 before the MMA of a is issued.
-  static constexpr int DBUF = (NX == 1 || 64 + 2 * N <= 128) ? 2 : 1;
-  static constexpr int COLS = 64 + DBUF * N;         // A_hi, A_lo (32 each) + D buffers
+  static constexpr int DBUF = (32 + 2 * N <= 128) ? 2 : 1;
+  static constexpr int COLS = 32 + DBUF * N;         // A_hi, A_lo (16 f16x2 each) + D buffers
   static constexpr int ALLOC = COLS <= 128 ? 128 : (COLS <= 256 ? 256 : 512);
   static constexpr int MINB = 512 / ALLOC;           // CTAs per SM (512 TMEM columns)
 };
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
   using S = TCShape<NF, NX>;
   constexpr int P = S::P, N1 = S::N1, N = S::N, DBUF = S::DBUF;
   constexpr int GEO = MODE == kModeFlt ? kModeFlt : kModeBwd;     // geometry / record kind
-  constexpr unsigned BBYTES = 2u * N * 128u;                       // B_hi | B_lo image
+  constexpr unsigned BBYTES = 2u * N * 64u;                        // B_hi | B_lo fp16 image
   static_assert(kAdjThreads == 128, "one TMEM lane per thread");
   // B^T images of antennas a (buffer a & 1), prepared by k_prep_bt and brought in by the bulk-copy
   // engine two antennas ahead: no thread of the CTA touches B
@@ -147,6 +155,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   const unsigned char *bsrc = a.bprep + (size_t)i_lo * BBYTES;
+  const float2 *bscale = reinterpret_cast<const float2 *>(a.bprep + (size_t)a.n_a * BBYTES);
   if (tid == 0) {
     mbar_init(&mma_bar, 1);
     mbar_init(&full_bar[0], 1);
@@ -162,10 +171,9 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
   tc_fence_after();
   const unsigned tmem = tmem_base_sh;
   const unsigned lane_off = (unsigned)(warp * 32) << 16;
-  const unsigned a_hi = tmem, a_lo = tmem + 32, d0 = tmem + 64;
-  // kind::tf32, fp32 accumulate, both operands K-major, M = 128, N
-  const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(N >> 3) << 17) |
-                         ((unsigned)(128 >> 4) << 24);
+  const unsigned a_hi = tmem, a_lo = tmem + 16, d0 = tmem + 32;
+  // kind::f16: fp16 A and B, fp32 accumulate, both operands K-major, M = 128, N
+  const unsigned idesc = (1u << 4) | ((unsigned)(N >> 3) << 17) | ((unsigned)(128 >> 4) << 24);
 
   const Rec rec = load_point<GEO>(a, j, valid);
   float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
@@ -173,6 +181,11 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
   bool domain = false;
   PairTC prev;
   const double kd16 = a.kd * 16.0;
+  // antenna records prefetched one antenna ahead (the global-load latency was exposed at the
+  // first fp64 difference of the pair geometry)
+  AntF nxt;
+  float2 nxt_inv = make_float2(1.f, 1.f);
+  if (na > 0) { nxt = load_antf<MONO>(a, i_lo); nxt_inv = bscale[i_lo]; }
 
   // epilogue of antenna ai-1: U from TMEM, Horner over m1, Eq. 5 / M sums
   auto epilogue = [&](int ai) {
@@ -199,7 +212,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
         const f2x t = ffma2(W, pk(hv.x, hv.x), pk(Ur[m1], Ui[m1]));
         h = ffma2(W2, pk(hv.y, hv.y), t);
       }
-      const float2 hh = upk(h);
+      const float2 hh = upk(fmul2(h, pk(prev.inv[x], prev.inv[x])));
       if (MODE != kModeBoth)
         adj_accumulate<MODE>(prev.g, prev.ec, prev.es, hh.x, hh.y, S1, S2, S3x, S3y, S3z);
       else if (x == 0)
@@ -214,7 +227,10 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
     if (ai < na) {
       // ---------------- SIMT: pair data and the powers of w for antenna ai (overlaps MMA ai-1)
       const int64_t ia = i_lo + ai;
-      const AntD an = load_ant<MONO>(a, ia);
+      const AntD an = widen_ant<MONO>(nxt);
+      cur.inv[0] = nxt_inv.x;
+      cur.inv[1] = nxt_inv.y;
+      if (ai + 1 < na) { nxt = load_antf<MONO>(a, ia + 1); nxt_inv = bscale[ia + 1]; }
       double L;
       if (GEO == kModeBwd) {
         pair_geometry<MONO, CORR>(rec, an, no_gain, cur.g);
@@ -232,7 +248,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
       // W = w^16 from the fp64 cycle count; MUFU (abs. error ~4e-7): the Horner over m1 amplifies
       // it at most P - 1 times, well inside the 1e-4 / 1e-3 tolerances
       __sincosf(kTwoPi * f16, &cur.Ws, &cur.Wc);
-      unsigned hv[32], lv[32];
+      unsigned hv[16], lv[16];
       {
         // powers p_k = w^k (packed complex mults) by binary expansion -- dependency depth 4
         // instead of a 15-long chain -- and their hi / lo split
@@ -249,14 +265,12 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
 #pragma unroll
         for (int k = 9; k < 16; ++k) pw[k] = cmul2(pw[8], pw[k - 8]);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 16; ++k) {          // column k = (Re, Im) of w^k: K elements 2k, 2k+1
           const float2 pv = upk(pw[k]);
           const float hr = tf32_hi(pv.x), hi_ = tf32_hi(pv.y);
           const float2 lo = upk(fadd2(pw[k], pk(-hr, -hi_)));
-          hv[2 * k] = __float_as_uint(hr);
-          hv[2 * k + 1] = __float_as_uint(hi_);
-          lv[2 * k] = __float_as_uint(lo.x);
-          lv[2 * k + 1] = __float_as_uint(lo.y);
+          hv[k] = pack_h2(hr, hi_);
+          lv[k] = pack_h2(lo.x, lo.y);
         }
       }
       // ---------------- MMA ai-1 must be done before A / B (and a single D) are reused
@@ -268,8 +282,8 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
         mbar_arrive_expect_tx(&full_bar[b], BBYTES);
         bulk_g2s(bsm[b], bsrc + (size_t)(ai + 1) * BBYTES, BBYTES, &full_bar[b]);
       }
-      tmem_st32(a_hi + lane_off, hv);
-      tmem_st32(a_lo + lane_off, lv);
+      tmem_st16(a_hi + lane_off, hv);
+      tmem_st16(a_lo + lane_off, lv);
       if (DBUF == 1 && ai > 0) epilogue(ai);      // read D of ai-1 before the MMA of ai
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
@@ -282,15 +296,15 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
         mbar_wait(&full_bar[ai & 1], (unsigned)((ai >> 1) & 1));   // B^T of antenna ai landed
         const unsigned d = d0 + (unsigned)((DBUF == 2 ? (ai & 1) : 0) * N);
         const unsigned acol[3] = {a_hi, a_hi, a_lo};
-        const unsigned char *Bhi = bsm[ai & 1], *Blo = Bhi + N * 128;
+        const unsigned char *Bhi = bsm[ai & 1], *Blo = Bhi + N * 64;
         const unsigned char *bs[3] = {Bhi, Blo, Bhi};
 #pragma unroll
         for (int p = 0; p < 3; ++p)
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            umma_tf32_ts(d, acol[p] + 8 * ks,
-                         umma_sdesc(smem_u32(bs[p]) + ks * 256, 128, 1024), idesc,
-                         (p | ks) ? 1u : 0u);
+          for (int ks = 0; ks < 2; ++ks)
+            umma_f16_ts(d, acol[p] + 8 * ks,
+                        umma_sdesc(smem_u32(bs[p]) + ks * 256, 128, 512), idesc,
+                        (p | ks) ? 1u : 0u);
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];"
                      ::"l"((uint64_t)smem_u32(&mma_bar)) : "memory");
       }
@@ -318,38 +332,68 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
                  "n"(S::ALLOC));
 }
 
-// B^T images for the tensor-core adjoint, one per antenna: [B_hi | B_lo], each N rows of 32 tf32
+// B^T images for the tensor-core adjoint, one per antenna: [B_hi | B_lo], each N rows of 32 fp16
 // columns in the canonical K-major no-swizzle layout (bT_off).  Row n = x N1 + 2 m1 + c of X row
-// x (G then s for kModeBoth), column 2 m0 + c' holds bins 16 m1 + m0 as (Re, -Im) for c = 0 and
-// (Im, Re) for c = 1 (the complex product's sign pattern), split hi = tf32(v), lo = v - hi.  One
-// thread per 16-byte chunk (two bins); HBM-bound, ~0.05 ms at c3.
+// x (G then s for kModeBoth), column 2 m0 + c' holds bin 16 m1 + m0 as (Re, -Im) for c = 0 and
+// (Im, Re) for c = 1 (the complex product's sign pattern), scaled by 2^-e so that the row's max
+// |component| lies in [0.5, 1) (fp16 range), split hi = x with 13 low mantissa bits cleared,
+// lo = x - hi.  The inverse scales 2^e go to a float2 per antenna after the images.  One warp
+// per antenna; HBM-bound, ~0.05 ms at c3.
 __global__ void k_prep_bt(const float2 *__restrict__ X, const float2 *__restrict__ X2, int64_t n_a,
                           int nf, int nx, unsigned char *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
   const int N1 = nf / 8, N = nx * N1;
-  const int64_t per_ant = (int64_t)N * 8;                 // 16-byte chunks per antenna
-  const size_t bbytes = (size_t)2 * N * 128;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_a * per_ant;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ia = t / per_ant;
-    const int q = (int)(t - ia * per_ant);
-    const int n = q % N, c = q / N;
-    const int x = n / N1, nn = n % N1;
-    const float4 v4 = reinterpret_cast<const float4 *>((x == 0 ? X : X2) + ia * nf)
-        [(16 * (nn >> 1) + 2 * c) >> 1];
-    const float4 v = (n & 1) ? make_float4(v4.y, v4.x, v4.w, v4.z)
-                             : make_float4(v4.x, -v4.y, v4.z, -v4.w);
-    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-    const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-    unsigned char *dst = out + (size_t)ia * bbytes + bT_off(n, 4 * c);
-    *reinterpret_cast<float4 *>(dst) = h;
-    *reinterpret_cast<float4 *>(dst + N * 128) = l;
+  const size_t bbytes = (size_t)N * 128;                 // hi + lo, N rows x 64 B each
+  float2 *scales = reinterpret_cast<float2 *>(out + (size_t)n_a * bbytes);
+  for (int64_t ia = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; ia < n_a;
+       ia += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float sc[2] = {1.f, 1.f}, inv[2] = {1.f, 1.f};
+    for (int x = 0; x < nx; ++x) {
+      const float4 *row = reinterpret_cast<const float4 *>((x == 0 ? X : X2) + ia * nf);
+      float m = 0.f;
+      for (int q = lane; q < nf / 2; q += 32) {
+        const float4 v = row[q];
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (m > 0.f && isfinite(m)) {
+        int e;
+        frexpf(m, &e);                                   // m = f 2^e, f in [0.5, 1)
+        sc[x] = ldexpf(1.f, -e);
+        inv[x] = ldexpf(1.f, e);
+      }
+    }
+    if (lane == 0) scales[ia] = make_float2(inv[0], inv[1]);
+    unsigned char *img = out + (size_t)ia * bbytes;
+    // 16-byte chunk (row n, columns 8c .. 8c+7) = bins 16 (n' / 2) + 4c .. +3 of row x
+    for (int q = lane; q < N * 4; q += 32) {
+      const int n = q % N, c = q / N;
+      const int x = n / N1, nn = n % N1;
+      const float4 *row = reinterpret_cast<const float4 *>((x == 0 ? X : X2) + ia * nf);
+      const int b = 16 * (nn >> 1) + 4 * c;
+      const float4 u = row[b >> 1], w = row[(b >> 1) + 1];
+      float v[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
+      unsigned hv[4], lv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float re = v[2 * t] * sc[x], im = v[2 * t + 1] * sc[x];
+        const float e0 = (n & 1) ? im : re, e1 = (n & 1) ? re : -im;
+        const float h0 = tf32_hi(e0), h1 = tf32_hi(e1);
+        hv[t] = pack_h2(h0, h1);
+        lv[t] = pack_h2(e0 - h0, e1 - h1);
+      }
+      *reinterpret_cast<uint4 *>(img + bT_off(n, 8 * c)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+      *reinterpret_cast<uint4 *>(img + N * 64 + bT_off(n, 8 * c)) =
+          make_uint4(lv[0], lv[1], lv[2], lv[3]);
+    }
   }
 }
 
 template <int MODE, bool MONO, bool CORR, int NF>
 static cudaError_t tc_launch(const AdjArgs &a, dim3 grid, cudaStream_t st) {
   using S = TCShape<NF, MODE == kModeBoth ? 2 : 1>;
-  const size_t smem = (size_t)2 * 2 * S::N * 128;        // two B^T image buffers
+  const size_t smem = (size_t)2 * 2 * S::N * 64;         // two B^T image buffers (fp16 hi | lo)
   auto k = k_adjoint_tc<MODE, MONO, CORR, NF>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -374,8 +418,7 @@ cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, 
   if (!a.bprep) return cudaErrorInvalidValue;
   if (a.n_a > 0) {
     const int nx = mode == kModeBoth ? 2 : 1;
-    const int64_t chunks = a.n_a * (int64_t)(nx * a.n_f / 8) * 8;
-    const unsigned g = (unsigned)std::min<int64_t>((chunks + 255) / 256, 148 * 16);
+    const unsigned g = (unsigned)std::min<int64_t>((a.n_a + 7) / 8, 148 * 32);   // 8 warps / CTA
     k_prep_bt<<<g, 256, 0, st>>>(a.X, a.X2, a.n_a, a.n_f, nx, a.bprep);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
