@@ -37,7 +37,8 @@ FP32_LANES_PER_SM = 128
 #   backward : 2 FFMA2           = 4 lane-ops (complex Horner step)
 #   filter   : 2 FFMA2           = 4 lane-ops
 OPS_PER_CONTRIB = 4
-# K3/K4 on tensor cores: D = A.B^T per 16-bin block, 4 real MACs per contribution, 3 tf32 products
+# K3/K4 on tensor cores: D = A.B^T per 16-bin block, 4 real MACs per contribution, 3 fp16 products
+# (3xFP16 split, tcgen05.mma kind::f16 with fp32 accumulation)
 TC_FLOP_PER_CONTRIB = 24
 
 
@@ -307,9 +308,9 @@ def run_gpu(args):
     pk = peaks()
     clocks = clk.summary()
     peak_ops = N_SM * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6
-    # tf32 tensor peak: the measured bf16 burst peak x the nominal tf32/bf16 ratio (1.1 / 2.25)
+    # fp16 tensor peak (kind::f16 runs at the bf16 rate): the measured bf16 burst peak
     bf16 = pk.get("bf16_tflops", 1590.0)
-    peak_tf32 = bf16 * 1e12 * (1.1 / 2.25)
+    peak_f16 = bf16 * 1e12
     tc = os.environ.get("RFR_ADJOINT", "tc") != "simt" and grid.n_freq in (128, 256, 512)
     per_step = lambda ms: ms / args.steps
     clk_ratio = (clocks["sm_mhz"] / pk.get("sm_max_mhz", 1965.0)) if clocks.get("sm_mhz") else None
@@ -329,11 +330,11 @@ def run_gpu(args):
     for name, ms, npass in adj:
         rate = npass * (Nc / world) / (per_step(ms) * 1e-3)     # contributions of all its passes
         if tc:
-            # exact 16-bin block factorisation on tcgen05 kind::tf32, 3xTF32: per contribution
+            # exact 16-bin block factorisation on tcgen05 kind::f16, 3xFP16: per contribution
             # 4 real MACs x 3 products = 24 tensor FLOP
             ach = TC_FLOP_PER_CONTRIB * rate
             roofs.append({"kernel": name, "bound": "tensor", "achieved": ach / 1e12,
-                          "peak": peak_tf32 / 1e12, "unit": "T tf32 FLOP/s", "frac": ach / peak_tf32,
+                          "peak": peak_f16 / 1e12, "unit": "T f16 FLOP/s", "frac": ach / peak_f16,
                           "alu_equivalent_frac": OPS_PER_CONTRIB * rate / peak_ops,
                           "ms_per_step": per_step(ms)})
         else:
@@ -352,8 +353,8 @@ def run_gpu(args):
             "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
             "peak_note": ("148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); 4 lane-ops "
                           "per contribution" if dom["bound"] == "alu" else
-                          "measured bf16 burst peak x 1.1/2.25 (tf32/bf16 nominal); 24 tensor "
-                          "FLOP per contribution")}
+                          "measured bf16 burst peak (kind::f16 runs at the bf16 rate); 24 tensor "
+                          "FLOP per contribution (3xFP16)")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         r = oracle_sample_rates(prob, budget_s=args.ref_budget)

@@ -212,6 +212,15 @@ rfr_status rfr_backward_filter(const float *grad_signal, const float *signal,
                                const rfr_opts *opts, const rfr_sample_grads *out, float *power,
                                float *mf, const rfr_comm *comm, const rfr_workspace *ws,
                                rfr_stream_t stream);
+/* The sweep of rfr_backward_filter for one antenna shard, without communication or finish:
+ * partials [5][n_samples] as rfr_backward_partial and mf [n_samples] complex64 the partial
+ * matched filter M at the samples; both are additive over antenna shards.  The caller sums them
+ * over shards and calls rfr_backward_finish / rfr_filter_power. */
+rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *signal,
+                                       const rfr_samples *samples, float sharpness,
+                                       const rfr_antennas *ants, const rfr_freq_grid *grid,
+                                       const rfr_opts *opts, float *partials, float *mf,
+                                       const rfr_workspace *ws, rfr_stream_t stream);
 /* K1': chain the (all-reduced) partials through Eq. 5 and the blend of every ray. */
 rfr_status rfr_backward_finish(const float *partials, const rfr_samples *samples, float sharpness,
                                const rfr_opts *opts, const rfr_sample_grads *out,

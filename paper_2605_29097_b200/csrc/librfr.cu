@@ -504,6 +504,57 @@ rfr_status rfr_backward(const float *grad_signal, const rfr_samples *samples, fl
   return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, stream);
 }
 
+rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *signal,
+                                       const rfr_samples *samples, float sharpness,
+                                       const rfr_antennas *ants, const rfr_freq_grid *grid,
+                                       const rfr_opts *opts, float *partials, float *mf,
+                                       const rfr_workspace *ws, rfr_stream_t stream) {
+  RFR_TRY(check_samples(samples));
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  if (!(sharpness > 0.f) || (ants->n_ant > 0 && (!grad_signal || !signal))) return RFR_E_ARG;
+  const uint32_t flags = opts ? opts->flags : 0u;
+  const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
+  if (n_s > 0 && (!partials || !mf)) return RFR_E_ARG;
+  Layout L;
+  RFR_TRY(check_ws(ws, n_s, n_s, L));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (n_s == 0) return RFR_OK;
+  RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
+  // one split count for both partial sets: the backward's (5 floats per sample) is the tighter
+  const Split sp = adj_split(n_s, ants->n_ant, 5, std::min(L.cap_bwdp, L.cap_fltp * 5 / 2));
+  AdjArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rec = at<Rec>(ws, L.off_rec);
+  a.n_s = n_s;
+  a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
+  a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
+  a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
+  a.n_a = ants->n_ant;
+  a.n_f = grid->n_freq;
+  a.k0 = grid->f0_hz / kC;
+  a.kd = grid->df_hz / kC;
+  a.X = reinterpret_cast<const float2 *>(grad_signal);
+  a.X2 = reinterpret_cast<const float2 *>(signal);
+  a.qx = samples->x; a.qy = samples->y; a.qz = samples->z;   // SIMT fallback's filter queries
+  a.bprep = at<unsigned char>(ws, L.off_bprep);
+  a.bprep_cap = L.total - L.off_bprep;
+  a.ants_per_split = sp.per_split;
+  a.out = sp.splits > 1 ? at<float>(ws, L.off_bwdp) : partials;
+  a.out2 = sp.splits > 1 ? at<float>(ws, L.off_fltp) : mf;
+  a.flags = at<unsigned>(ws, 0);
+  a.no_gain = (flags & RFR_NO_GAIN) != 0;
+  const bool mono = ants->rx_x == nullptr;
+  RFR_CU(launch_adjoint(a, kModeBoth, mono, has_corr(samples, ants), sp.splits, st));
+  if (sp.splits > 1) {
+    RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
+                             device_sms(), st));
+    RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, 2 * n_s, mf, device_sms(),
+                             st));
+  }
+  return RFR_OK;
+}
+
 rfr_status rfr_backward_filter(const float *grad_signal, const float *signal,
                                const rfr_samples *samples, float sharpness,
                                const rfr_antennas *ants, const rfr_freq_grid *grid,
@@ -511,10 +562,7 @@ rfr_status rfr_backward_filter(const float *grad_signal, const float *signal,
                                float *mf, const rfr_comm *comm, const rfr_workspace *ws,
                                rfr_stream_t stream) {
   RFR_TRY(check_samples(samples));
-  RFR_TRY(check_ants(ants));
-  RFR_TRY(check_grid(grid));
-  if (!(sharpness > 0.f) || !out || (ants->n_ant > 0 && (!grad_signal || !signal)))
-    return RFR_E_ARG;
+  if (!out) return RFR_E_ARG;
   const uint32_t flags = opts ? opts->flags : 0u;
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
   if (n_s > 0 && !power) return RFR_E_ARG;
@@ -523,46 +571,14 @@ rfr_status rfr_backward_filter(const float *grad_signal, const float *signal,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   float *part = at<float>(ws, L.off_bwds);
   float *M = mf ? mf : at<float>(ws, L.off_fltm);
-  if (n_s > 0) {
-    RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
-    // one split count for both partial sets: the backward's (5 floats per sample) is the tighter
-    const Split sp = adj_split(n_s, ants->n_ant, 5, std::min(L.cap_bwdp, L.cap_fltp * 5 / 2));
-    AdjArgs a;
-    memset(&a, 0, sizeof(a));
-    a.rec = at<Rec>(ws, L.off_rec);
-    a.n_s = n_s;
-    a.tx_x = ants->tx_x; a.tx_y = ants->tx_y; a.tx_z = ants->tx_z;
-    a.rx_x = ants->rx_x; a.rx_y = ants->rx_y; a.rx_z = ants->rx_z;
-    a.phi_tx = ants->phi_tx; a.phi_rx = ants->phi_rx;
-    a.n_a = ants->n_ant;
-    a.n_f = grid->n_freq;
-    a.k0 = grid->f0_hz / kC;
-    a.kd = grid->df_hz / kC;
-    a.X = reinterpret_cast<const float2 *>(grad_signal);
-    a.X2 = reinterpret_cast<const float2 *>(signal);
-    a.qx = samples->x; a.qy = samples->y; a.qz = samples->z;   // SIMT fallback's filter queries
-    a.bprep = at<unsigned char>(ws, L.off_bprep);
-  a.bprep_cap = L.total - L.off_bprep;
-    a.ants_per_split = sp.per_split;
-    a.out = sp.splits > 1 ? at<float>(ws, L.off_bwdp) : part;
-    a.out2 = sp.splits > 1 ? at<float>(ws, L.off_fltp) : M;
-    a.flags = at<unsigned>(ws, 0);
-    a.no_gain = (flags & RFR_NO_GAIN) != 0;
-    const bool mono = ants->rx_x == nullptr;
-    RFR_CU(launch_adjoint(a, kModeBoth, mono, has_corr(samples, ants), sp.splits, st));
-    if (sp.splits > 1) {
-      RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, part,
-                               device_sms(), st));
-      RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, 2 * n_s, M, device_sms(),
-                               st));
-    }
-  }
+  RFR_TRY(rfr_backward_filter_partial(grad_signal, signal, samples, sharpness, ants, grid, opts,
+                                      part, M, ws, stream));
   // a7 and the filter's shard sum
   RFR_TRY(allreduce_sum(comm, part, 5 * n_s, st));
   RFR_TRY(allreduce_sum(comm, M, 2 * n_s, st));
   if (n_s > 0) RFR_CU(launch_abs(M, n_s, power, device_sms(), st));
   rfr_opts o2;
-  o2.flags = flags | RFR_REUSE_BLEND;                 // K1 ran above
+  o2.flags = flags | RFR_REUSE_BLEND;                 // K1 ran in the partial call
   return rfr_backward_finish(part, samples, sharpness, &o2, out, ws, stream);
 }
 

@@ -61,7 +61,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too sm
 
 EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_filter_partial",
            "rfr_filter_power", "rfr_backward", "rfr_backward_partial", "rfr_backward_finish",
-           "rfr_backward_filter", "rfr_filter_backward", "rfr_heatmap_loss",
+           "rfr_backward_filter", "rfr_backward_filter_partial", "rfr_filter_backward", "rfr_heatmap_loss",
            "rfr_comm_unique_id", "rfr_comm_init", "rfr_comm_destroy",
            "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count")
 
@@ -96,6 +96,7 @@ def load(path: str = LIB_PATH):
         "rfr_backward_partial": [vp, S, f, A, G, O, vp, W, vp],
         "rfr_backward_finish": [vp, S, f, O, R, W, vp],
         "rfr_backward_filter": [vp, vp, S, f, A, G, O, R, vp, vp, vp, W, vp],
+        "rfr_backward_filter_partial": [vp, vp, S, f, A, G, O, vp, vp, W, vp],
         "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, W, vp],
         "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, W, vp],
         "rfr_poll_flags": [W, C.POINTER(u32)],
@@ -357,6 +358,18 @@ def rfr_backward_filter(grad_signal: torch.Tensor, signal: torch.Tensor, samples
                                       _ptr(mf), _comm(comm), _ws(ws), _stream(stream)),
            "rfr_backward_filter")
     return out, power
+
+
+def rfr_backward_filter_partial(grad_signal, signal, samples: DeviceSamples, sharpness: float,
+                                ants: DeviceAntennas, grid, partials: torch.Tensor,
+                                mf: torch.Tensor, ws: torch.Tensor, flags: int = 0, stream=None):
+    """The fused sweep for one antenna shard: partials [5][n_s] and partial complex M [n_s]."""
+    s, a, g, o = samples.struct(), ants.struct(), grid_struct(grid), rfr_opts(flags)
+    _check(load().rfr_backward_filter_partial(_ptr(grad_signal), _ptr(signal), C.byref(s),
+                                              float(sharpness), C.byref(a), C.byref(g), C.byref(o),
+                                              _ptr(partials), _ptr(mf), _ws(ws), _stream(stream)),
+           "rfr_backward_filter_partial")
+    return partials, mf
 
 
 def rfr_backward_partial(grad_signal, samples: DeviceSamples, sharpness: float,

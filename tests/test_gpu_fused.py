@@ -137,3 +137,48 @@ def test_fused_empty_and_errors():
     assert torch.all(P == 0)
     for k in FIELDS:
         assert torch.all(getattr(out, k) == 0), k
+
+
+def test_fused_sharded_equals_oracle_and_comm_identity():
+    """Multi-GPU algorithm on one GPU: per-shard fused partials (antenna slices = pointer offsets)
+    summed in rank order as the all-reduce would, then K1' and |M|; and the NCCL path of
+    rfr_backward_filter on one rank is bitwise the same as without it."""
+    m = rfr()
+    p = problem("c1")
+    b = p.bundles[0]
+    G = p.random_grad()
+    sig = (0.5 * p.random_grad()[::-1]).astype(np.complex64)
+    DS, DA = m.DeviceSamples.from_host(b.samples, dev()), m.DeviceAntennas.from_host(b.antennas, dev())
+    Gt, St = f32c(G), f32c(sig)
+    n, na = b.samples.n, b.antennas.n
+    ws = m.workspace(n, na, p.grid.n_freq, n, dev())
+    world = 4
+    part_tot = torch.zeros(5, n, device=dev())
+    m_tot = torch.zeros(n, 2, device=dev())
+    for r in range(world):
+        lo, hi = m.shard_range(na, r, world)
+        pr, mr = torch.empty(5, n, device=dev()), torch.empty(n, 2, device=dev())
+        m.rfr_backward_filter_partial(Gt[lo:hi], St[lo:hi], DS, p.sharpness, DA.slice(lo, hi),
+                                      p.grid, pr, mr, ws)
+        part_tot += pr
+        m_tot += mr
+    out = m.Grads.empty(n, dev())
+    m.rfr_backward_finish(part_tot, DS, p.sharpness, out, ws)
+    P = torch.empty(n, device=dev())
+    m.rfr_filter_power(m_tot, P)
+    torch.cuda.synchronize()
+    g = {k: getattr(out, k).cpu().numpy().astype(np.float64) for k in m.Grads.NAMES}
+    _check_all(g, P.cpu().numpy().astype(np.float64), c64(m_tot), G, sig, b.samples, b.antennas,
+               p.grid, p.sharpness, what="sharded")
+    comm = m.Comm.create()
+    try:
+        o1, o2 = m.Grads.empty(n, dev()), m.Grads.empty(n, dev())
+        P1, P2 = torch.empty(n, device=dev()), torch.empty(n, device=dev())
+        m.rfr_backward_filter(Gt, St, DS, p.sharpness, DA, p.grid, o1, P1, ws)
+        m.rfr_backward_filter(Gt, St, DS, p.sharpness, DA, p.grid, o2, P2, ws, comm=comm)
+        torch.cuda.synchronize()
+        for k in m.Grads.NAMES:
+            assert torch.equal(getattr(o1, k), getattr(o2, k)), k
+        assert torch.equal(P1, P2)
+    finally:
+        comm.close()
