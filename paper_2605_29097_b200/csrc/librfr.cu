@@ -20,6 +20,7 @@ namespace {
 
 constexpr double kC = 299792458.0;
 constexpr size_t kHdr = 256;                   // workspace header: flags word at offset 0
+constexpr size_t kChebHdrOff = 64;             // ChebHdr of the Chebyshev-moment forward
 constexpr int kTmpN = 512;                     // reduction scratch (floats)
 constexpr size_t kSplitCap = size_t(2) << 30;  // cap on each split-partial region (bytes)
 
@@ -104,6 +105,28 @@ Split adj_split(int64_t n_pts, int64_t n_a, int floats_per_pt, size_t cap) {
   return r;
 }
 
+// split-K over the points of the Chebyshev-moment forward: ~8 waves of 4 CTAs of 128 antennas per
+// SM, at least 512 points per split
+Split cheb_split(int64_t n_pts, int64_t n_a) {
+  const int64_t tiles = std::max<int64_t>(1, cdiv(n_a, cheb_threads()));
+  int64_t s = cdiv((int64_t)device_sms() * 4 * 8, tiles);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_pts, 512)));
+  s = std::max<int64_t>(s, 1);
+  Split r;
+  r.per_split = cdiv(std::max<int64_t>(n_pts, 1), s);
+  r.splits = (int)std::max<int64_t>(1, cdiv(n_pts, r.per_split));
+  return r;
+}
+// the Chebyshev path is on unless RFR_FWD=direct (A/B measurements)
+bool cheb_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RFR_FWD");
+    v = (e && strcmp(e, "direct") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // ---------------------------------------------------------------------------- workspace layout
 // The layout depends ONLY on the workspace's planning dimensions, so every call that shares a
 // workspace sees the same regions: K1's records (the RFR_REUSE_BLEND cache) are never touched by
@@ -112,7 +135,9 @@ Split adj_split(int64_t n_pts, int64_t n_a, int floats_per_pt, size_t cap) {
 //   K5 query records [n_q] 48 B | K2/K5 split partials | K3 split partials | K4 split partials
 struct Layout {
   size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
-         off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, total = 0;
+         off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, off_cbox = 0, off_clc = 0,
+         off_ccoef = 0, off_cpart = 0, total = 0;
+  size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
 
@@ -142,6 +167,13 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   L.off_fltp = take(L.cap_fltp);
   // tensor-core adjoint: per-antenna B^T images (sized for the fused sweep's two X rows)
   L.off_bprep = take(adjoint_tc_supported(nf) ? (size_t)n_a * tc_bprep_bytes_per_ant(nf, 2) : 0);
+  // Chebyshev-moment forward: box partials, per-antenna centres, coefficients, partial moments
+  const Split cs = cheb_split(std::max(n_s, n_q), n_a);
+  L.cap_cpart = (size_t)cs.splits * std::max<int64_t>(n_a, 1) * kChebPMax * 8;
+  L.off_cbox = take((size_t)cheb_box_blocks() * 6 * 8);
+  L.off_clc = take((size_t)std::max<int64_t>(n_a, 1) * 8);
+  L.off_ccoef = take((size_t)nf * kChebPMax * 8);
+  L.off_cpart = take(L.cap_cpart);
   L.total = o;
   return true;
 }
@@ -233,10 +265,43 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = no_gain;
   const bool mono = ants->rx_x == nullptr;
+  // Chebyshev-moment path (rfr_cheb.cu): chosen on the device from the delay spread; the direct
+  // kernel and its split sum return at once when it runs, and vice versa
+  ChebHdr *hdr = at<ChebHdr>(ws, kChebHdrOff);
+  const Split cs = cheb_split(n_pts, ants->n_ant);
+  const bool cheb = ants->n_ant > 0 && n_pts > 0 &&
+                    (size_t)cs.splits * ants->n_ant * kChebPMax * 8 <= L.cap_cpart;
+  ChebArgs c;
+  memset(&c, 0, sizeof(c));
+  if (cheb) {
+    c.rec = rec;
+    c.n_s = n_pts;
+    c.tx_x = ants->tx_x; c.tx_y = ants->tx_y; c.tx_z = ants->tx_z;
+    c.rx_x = ants->rx_x; c.rx_y = ants->rx_y; c.rx_z = ants->rx_z;
+    c.phi_tx = ants->phi_tx; c.phi_rx = ants->phi_rx;
+    c.n_a = ants->n_ant;
+    c.n_f = grid->n_freq;
+    c.kd = grid->df_hz / kC;
+    c.kc = (grid->f0_hz + (double)(grid->n_freq / 2) * grid->df_hz) / kC;
+    c.samples_per_split = cs.per_split;
+    c.lc = at<double>(ws, L.off_clc);
+    c.hdr = hdr;
+    c.coef = at<float2>(ws, L.off_ccoef);
+    c.pmax = kChebPMax;
+    c.part = at<float2>(ws, L.off_cpart);
+    c.flags = at<unsigned>(ws, 0);
+    c.no_gain = no_gain;
+    c.enable = cheb_enabled();
+    RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
+    a.skip = hdr;
+  }
   RFR_CU(launch_trace_fwd(a, g.B, mono, corr, kind, sp.splits, st));
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_fwdp), sp.splits,
-                             ants->n_ant * (int64_t)grid->n_freq * 2, out, device_sms(), st));
+                             ants->n_ant * (int64_t)grid->n_freq * 2, out, device_sms(), st,
+                             cheb ? hdr : nullptr));
+  if (cheb)
+    RFR_CU(launch_cheb_fwd(c, mono, corr, kind, cs.splits, reinterpret_cast<float2 *>(out), st));
   return RFR_OK;
 }
 

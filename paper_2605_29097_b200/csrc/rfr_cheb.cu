@@ -1,0 +1,343 @@
+// rfr_cheb.cu -- forward signal tracing (Eq. 4) by a Jacobi-Anger / Chebyshev
+// factorisation of the bin dependence ("range-profile factorisation").
+//
+// For antenna i write the per-pair delay in cycles per bin step as u_ij = L_ij df / c and centre it
+// on the antenna: u_ij = u_c,i + delta x_ij with |x_ij| <= 1, where [u_c,i -+ delta_i] bounds the
+// delays of every sample of the call (from the samples' bounding box) and delta = max_i delta_i.
+// With centred bins m' = m - N/2 and c_ij = A_ij exp(-j 2 pi f_c tau_ij), f_c = f0 + (N/2) df:
+//     s_i[m] = exp(-j 2 pi m' u_c,i) sum_j c_ij exp(-j z_m' x_ij),      z_m' = 2 pi m' delta,
+//     exp(-j z x) = sum_p eps_p (-j)^p J_p(z) T_p(x)                     (Jacobi-Anger)
+// so the N_f-bin sum of every pair collapses to P Chebyshev moments M_i[p] = sum_j c_ij T_p(x_ij),
+// and the bins come from one small dense complex product per antenna,
+//     s_i[m] = exp(-j 2 pi m' u_c,i) sum_p a[m][p] M_i[p],    a[m][p] = eps_p (-j)^p J_p(z_m').
+// The truncation after P terms is below 1e-9 of sum |c| for |z| <= z_P (P = 16 / 32 / 48 for
+// z <= 3.4 / 13.3 / 25.3); wider delay spreads fall back to the direct recurrence kernel (K2).
+// Per pair: the fp64 geometry, one MUFU sincos and P steps of Reinsch's stabilised Chebyshev
+// recurrence (d_{p+1} = 2 (x - 1) T_p + d_p, T_{p+1} = T_p + d_{p+1}: absolute error O(p u) up to
+// |x| = 1, where the plain three-term recurrence grows like p^2 u) with one complex-real FFMA2 each:
+// ~4 FP32 lane-ops per moment instead of 4 per bin.  No atomics: split-K partial moments summed in
+// fixed order, results bitwise reproducible.
+//
+// The choice between this path and K2 is taken on the device (the delay spread is only known
+// there): k_cheb_setup writes the selected P (0 = direct) into the workspace header, and the kernels
+// of the path not taken return at once.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "rfr_device.cuh"
+#include "rfr_launch.h"
+
+namespace rfr {
+
+namespace {
+constexpr int kBoxBlocks = 256;
+constexpr int kChebThreads = 128;
+constexpr int kChebTJ = 32;                       // records per shared-memory tile
+}  // namespace
+
+// ------------------------------------------------------------------ bounding box of the samples
+__global__ void k_cheb_box(const Rec *__restrict__ rec, int64_t n, double *__restrict__ part) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const Rec r = rec[j];
+    lo[0] = fmin(lo[0], r.x); hi[0] = fmax(hi[0], r.x);
+    lo[1] = fmin(lo[1], r.y); hi[1] = fmax(hi[1], r.y);
+    lo[2] = fmin(lo[2], r.z); hi[2] = fmax(hi[2], r.z);
+  }
+  __shared__ double sh[6][256];
+  for (int c = 0; c < 3; ++c) { sh[c][threadIdx.x] = lo[c]; sh[3 + c][threadIdx.x] = hi[c]; }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int c = 0; c < 3; ++c) {
+        sh[c][threadIdx.x] = fmin(sh[c][threadIdx.x], sh[c][threadIdx.x + s]);
+        sh[3 + c][threadIdx.x] = fmax(sh[3 + c][threadIdx.x], sh[3 + c][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// distance range [dmin, dmax] from a point to an axis-aligned box
+__device__ __forceinline__ void box_dist(const double *b, double px, double py, double pz,
+                                         double &dmin, double &dmax) {
+  const double p[3] = {px, py, pz};
+  double s0 = 0.0, s1 = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double l = b[c], h = b[3 + c];
+    const double out = fmax(fmax(l - p[c], p[c] - h), 0.0);
+    s0 += out * out;
+    const double far = fmax(fabs(p[c] - l), fabs(p[c] - h));
+    s1 += far * far;
+  }
+  dmin = sqrt(s0);
+  dmax = sqrt(s1);
+}
+
+// ----------------------------------------------- per-antenna delay centre, global spread, P choice
+// One CTA of 1024 threads.  lc[i] = centre path length (m) of antenna i; hdr gets the selected P
+// (0: delay spread too wide -> direct kernel), delta and kd / delta.
+__global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ part, int nblk,
+                                                     ChebArgs a, double *__restrict__ lc,
+                                                     ChebHdr *__restrict__ hdr) {
+  __shared__ double box[6];
+  __shared__ double red[1024];
+  if (threadIdx.x < 6) {
+    double v = threadIdx.x < 3 ? 1e300 : -1e300;
+    for (int b = 0; b < nblk; ++b) {
+      const double u = part[b * 6 + threadIdx.x];
+      v = threadIdx.x < 3 ? fmin(v, u) : fmax(v, u);
+    }
+    box[threadIdx.x] = v;
+  }
+  __syncthreads();
+  double dmax_half = 0.0;
+  for (int64_t i = threadIdx.x; i < a.n_a; i += blockDim.x) {
+    double tmin, tmax, rmin, rmax;
+    box_dist(box, a.tx_x[i], a.tx_y[i], a.tx_z[i], tmin, tmax);
+    if (a.rx_x) box_dist(box, a.rx_x[i], a.rx_y[i], a.rx_z[i], rmin, rmax);
+    else { rmin = tmin; rmax = tmax; }
+    const double Lmin = tmin + rmin, Lmax = tmax + rmax;
+    lc[i] = 0.5 * (Lmin + Lmax);
+    dmax_half = fmax(dmax_half, 0.5 * (Lmax - Lmin));
+  }
+  red[threadIdx.x] = dmax_half;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // spread in cycles per bin, with a small margin for the fp32 rounding of the positions
+    const double delta = fmax(red[0] * a.kd * (1.0 + 1e-6), 1e-30);
+    const double zmax = 2.0 * 3.14159265358979323846 * (double)(a.n_f / 2 + 1) * delta;
+    int P = 0;
+    if (a.enable) {
+      if (zmax <= 3.4) P = 16;
+      else if (zmax <= 13.3) P = 32;
+      else if (zmax <= 25.3) P = 48;
+    }
+    hdr->sel = P > 0 ? 1u : 0u;
+    hdr->P = P;
+    hdr->delta = delta;
+    hdr->inv = a.kd / delta;
+  }
+}
+
+// ------------------------------------------------ a[m][p] = eps_p (-j)^p J_p(2 pi (m - N/2) delta)
+// One thread per bin: Bessel J_0..J_{P-1} by Miller's backward recurrence in fp64 (rescaled
+// against overflow), normalised by J_0 + 2 sum_k J_2k = 1.
+__global__ void k_cheb_coef(const ChebHdr *__restrict__ hdr, int n_f, int pmax,
+                            float2 *__restrict__ coef) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n_f || hdr->sel == 0) return;
+  const int P = hdr->P;
+  const double z0 = 2.0 * 3.14159265358979323846 * (double)(m - n_f / 2) * hdr->delta;
+  const double z = fabs(z0);
+  double J[128];
+  if (z < 1e-12) {
+    for (int p = 0; p < P; ++p) J[p] = p == 0 ? 1.0 : 0.0;
+  } else {
+    const int top = min(127, P + 24 + (int)z);
+    double jp1 = 0.0, jp = 1e-30, norm = 0.0;   // jp = J_k, jp1 = J_{k+1} (common scale)
+    for (int k = top; k >= 1; --k) {
+      if (k < P) J[k] = jp;
+      if ((k & 1) == 0) norm += 2.0 * jp;
+      const double jm1 = (2.0 * k / z) * jp - jp1;
+      jp1 = jp;
+      jp = jm1;
+      if (fabs(jp) > 1e200) {                    // rescale everything accumulated so far
+        jp *= 1e-200; jp1 *= 1e-200; norm *= 1e-200;
+        for (int q = k; q < P; ++q) J[q] *= 1e-200;
+      }
+    }
+    J[0] = jp;
+    norm += jp;
+    for (int p = 0; p < P; ++p) J[p] /= norm;
+  }
+  for (int p = 0; p < P; ++p) {
+    double v = (p == 0 ? 1.0 : 2.0) * J[p];
+    if (z0 < 0.0 && (p & 1)) v = -v;             // J_p(-z) = (-1)^p J_p(z)
+    // (-j)^p = 1, -j, -1, j
+    const int q = p & 3;
+    const float2 c = q == 0 ? make_float2((float)v, 0.f)
+                   : q == 1 ? make_float2(0.f, (float)-v)
+                   : q == 2 ? make_float2((float)-v, 0.f)
+                            : make_float2(0.f, (float)v);
+    coef[(int64_t)m * pmax + p] = c;
+  }
+}
+
+// ------------------------------------------------------------------------- moments M_i[p]
+// Thread = antenna; the CTA walks its split's samples in tiles of kChebTJ records staged in shared
+// memory (every thread reads the same record: broadcast).  KIND == kFwdMFAdj: the records are the
+// K5 query records {x, y, z, w = Re c_q, T = Im c_q} and the pair amplitude is c_q.
+template <int P, bool MONO, bool CORR, int KIND>
+__global__ void __launch_bounds__(kChebThreads, P <= 32 ? 4 : 3) k_cheb_fwd(ChebArgs a) {
+  if (a.hdr->P != P) return;                     // another P (or the direct kernel) was chosen
+  __shared__ __align__(16) Rec rb[2][kChebTJ];
+  const int tid = threadIdx.x;
+  const int64_t ia = (int64_t)blockIdx.x * kChebThreads + tid;
+  const bool ant_ok = ia < a.n_a;
+  const int64_t j_lo = (int64_t)blockIdx.y * a.samples_per_split;
+  const int64_t j_hi = min(a.n_s, j_lo + a.samples_per_split);
+  AntF af;
+  if (ant_ok) af = load_antf<MONO>(a, ia);
+  else { af.x = af.y = 0.f; af.z = 1.f; af.rx = af.ry = 0.f; af.rz = 1.f; af.ptx = af.prx = 1.f; }
+  const AntD an = widen_ant<MONO>(af);
+  const double Lc = ant_ok ? a.lc[ia] : 0.0;
+  const double inv = a.hdr->inv;
+  const bool no_gain = a.no_gain;
+  f2x M[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) M[p] = 0ull;
+  bool domain = false;
+
+  auto prefetch = [&](int64_t jt, int b) {
+    const int nv = (int)min((int64_t)kChebTJ, j_hi - jt);
+    const float4 *src = reinterpret_cast<const float4 *>(a.rec + jt);
+    float4 *dst = reinterpret_cast<float4 *>(rb[b]);
+    if (tid < kChebTJ * 3) {
+      if (tid < 3 * nv) cp_async16(dst + tid, src + tid);
+      else dst[tid] = make_float4(0.f, 0.f, 0.f, 0.f);      // tail: w = 0 records
+    }
+    cp_async_commit();
+  };
+  if (j_lo < j_hi) prefetch(j_lo, 0);
+  int b = 0;
+  for (int64_t jt = j_lo; jt < j_hi; jt += kChebTJ, b ^= 1) {
+    cp_async_wait_all();
+    __syncthreads();
+    if (jt + kChebTJ < j_hi) prefetch(jt + kChebTJ, b ^ 1);
+    const int nv = (int)min((int64_t)kChebTJ, j_hi - jt);
+#pragma unroll 1
+    for (int jj = 0; jj < nv; ++jj) {
+      const Rec rec = rb[b][jj];
+      double L;
+      float Ar, Ai;
+      if (KIND == kFwdTrace) {
+        PairBwd g;
+        pair_geometry<MONO, CORR>(rec, an, no_gain, g);
+        domain |= ant_ok && !g.ok;
+        Ar = rec.w * g.gg * g.Tt * g.Tr;
+        Ai = 0.f;
+        L = g.L;
+      } else {
+        L = pair_length<MONO>(rec, an);
+        Ar = rec.w;
+        Ai = rec.T;
+      }
+      // c = A exp(-j 2 pi f_c tau) from the fp64 cycle count at the centre frequency
+      float es, ec;
+      __sincosf(kTwoPi * frac_cycles(L * a.kc), &es, &ec);
+      const f2x c = (KIND == kFwdTrace) ? pk(Ar * ec, -Ar * es)
+                                        : pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
+      float x = (float)((L - Lc) * inv);
+      x = fminf(fmaxf(x, -1.f), 1.f);
+      // T_p(x) = (-1)^p T_p(|x|): odd moments take -c for x < 0
+      const f2x co = x < 0.f ? pk(-upk(c).x, -upk(c).y) : c;
+      const float xm1 = fabsf(x) - 1.f, twoxm1 = 2.f * xm1;
+      float t = 1.f, d = xm1;                      // T_0, d_1 = T_1 - T_0
+      acc2(M[0], c);
+      t += d;                                      // T_1
+      M[1] = ffma2(pk(t, t), co, M[1]);
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d = fmaf(twoxm1, t, d);
+        t += d;
+        M[p] = ffma2(pk(t, t), (p & 1) ? co : c, M[p]);
+      }
+    }
+  }
+  cp_async_wait_all();
+  if (domain) atomicOr(a.flags, 1u);
+  if (ant_ok) {
+    float2 *dst = a.part + ((int64_t)blockIdx.y * a.n_a + ia) * a.pmax;
+#pragma unroll
+    for (int p = 0; p < P; ++p) dst[p] = upk(M[p]);
+  }
+}
+
+// ------------------------------------------------ bins: s_i[m] = e^{-j 2pi m' u_c} sum_p a M_i[p]
+__global__ void k_cheb_out(ChebArgs a, int splits, float2 *__restrict__ out) {
+  if (a.hdr->sel == 0) return;
+  const int P = a.hdr->P;
+  __shared__ float2 Ms[64];
+  const int64_t i = blockIdx.x;
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    float2 v = make_float2(0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {          // fixed order over the splits
+      const float2 u = a.part[((int64_t)s * a.n_a + i) * a.pmax + p];
+      v.x += u.x;
+      v.y += u.y;
+    }
+    Ms[p] = v;
+  }
+  __syncthreads();
+  const double uc = a.lc[i] * a.kd;
+  for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
+    const float2 *cf = a.coef + (int64_t)m * a.pmax;
+    float re = 0.f, im = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float2 c = cf[p], v = Ms[p];
+      re = fmaf(c.x, v.x, fmaf(-c.y, v.y, re));
+      im = fmaf(c.x, v.y, fmaf(c.y, v.x, im));
+    }
+    float ps, pc;
+    sincospif(2.f * frac_cycles((double)(m - a.n_f / 2) * uc), &ps, &pc);   // e^{-j 2 pi m' u_c}
+    out[i * a.n_f + m] = make_float2(fmaf(pc, re, ps * im), fmaf(pc, im, -ps * re));
+  }
+}
+
+// ------------------------------------------------------------------------------- launchers
+template <int P, bool MONO, bool CORR, int KIND>
+static cudaError_t cheb_fwd_t(const ChebArgs &a, dim3 g, cudaStream_t st) {
+  k_cheb_fwd<P, MONO, CORR, KIND><<<g, kChebThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+template <bool MONO, bool CORR, int KIND>
+static cudaError_t cheb_fwd_all(const ChebArgs &a, dim3 g, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cheb_fwd_t<16, MONO, CORR, KIND>(a, g, st)) != cudaSuccess) return e;
+  if ((e = cheb_fwd_t<32, MONO, CORR, KIND>(a, g, st)) != cudaSuccess) return e;
+  return cheb_fwd_t<48, MONO, CORR, KIND>(a, g, st);
+}
+
+int cheb_box_blocks() { return kBoxBlocks; }
+int cheb_threads() { return kChebThreads; }
+
+cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_t st) {
+  k_cheb_box<<<kBoxBlocks, 256, 0, st>>>(a.rec, a.n_s, box_part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_cheb_setup<<<1, 1024, 0, st>>>(box_part, kBoxBlocks, a, a.lc, a.hdr);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_cheb_coef<<<(a.n_f + 127) / 128, 128, 0, st>>>(a.hdr, a.n_f, a.pmax, a.coef);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(3);
+  return e;
+}
+
+cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,
+                            float2 *out, cudaStream_t st) {
+  if (a.n_a <= 0) return cudaSuccess;
+  dim3 g((unsigned)((a.n_a + kChebThreads - 1) / kChebThreads), (unsigned)splits);
+  cudaError_t e;
+  if (kind == kFwdMFAdj)
+    e = mono ? cheb_fwd_all<true, false, kFwdMFAdj>(a, g, st)
+             : cheb_fwd_all<false, false, kFwdMFAdj>(a, g, st);
+  else if (mono)
+    e = corr ? cheb_fwd_all<true, true, kFwdTrace>(a, g, st)
+             : cheb_fwd_all<true, false, kFwdTrace>(a, g, st);
+  else
+    e = corr ? cheb_fwd_all<false, true, kFwdTrace>(a, g, st)
+             : cheb_fwd_all<false, false, kFwdTrace>(a, g, st);
+  if (e != cudaSuccess) return e;
+  k_cheb_out<<<(unsigned)a.n_a, 256, 0, st>>>(a, splits, out);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(4);
+  return e;
+}
+
+}  // namespace rfr

@@ -270,8 +270,8 @@ __device__ __forceinline__ AntD load_ant(const AdjArgs &a, int64_t ia) {
 struct AntF {
   float x, y, z, rx, ry, rz, ptx, prx;
 };
-template <bool MONO>
-__device__ __forceinline__ AntF load_antf(const AdjArgs &a, int64_t ia) {
+template <bool MONO, typename Args>
+__device__ __forceinline__ AntF load_antf(const Args &a, int64_t ia) {
   AntF d;
   d.x = a.tx_x[ia]; d.y = a.tx_y[ia]; d.z = a.tx_z[ia];
   if (MONO) { d.rx = d.ry = d.rz = 0.f; }

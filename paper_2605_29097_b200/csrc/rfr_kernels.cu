@@ -80,6 +80,7 @@ __global__ void k_blend(BlendArgs a) {
 template <int B, bool MONO, bool CORR, int KIND, int NB>
 __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(FwdArgs a) {
   constexpr int TJ = fwd_tj(B);
+  if (a.skip && a.skip->sel) return;              // the Chebyshev-moment path was chosen
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbc = NB > 0 ? NB : a.nb, taw = NB > 0 ? 32 / NB : a.taw;
@@ -583,7 +584,8 @@ __global__ void k_blend_bwd(BlendBwdArgs a) {
 // ================================================================================== reductions
 // out[k] = sum_{s < S} part[s * n + k], fixed order (float2 / float granularity via float4 loads)
 __global__ void k_sum_splits(const float4 *__restrict__ part, int S, int64_t n4,
-                             float4 *__restrict__ out) {
+                             float4 *__restrict__ out, const ChebHdr *skip) {
+  if (skip && skip->sel) return;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4;
        k += (int64_t)gridDim.x * blockDim.x) {
     float4 v = part[k];
@@ -595,7 +597,8 @@ __global__ void k_sum_splits(const float4 *__restrict__ part, int S, int64_t n4,
   }
 }
 __global__ void k_sum_splits_tail(const float *__restrict__ part, int S, int64_t n, int64_t lo,
-                                  float *__restrict__ out) {
+                                  float *__restrict__ out, const ChebHdr *skip) {
+  if (skip && skip->sel) return;
   const int64_t k = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   float v = part[k];
@@ -660,6 +663,7 @@ static inline cudaError_t counted(cudaError_t e, int n = 1) {
   return e;
 }
 unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+void add_launches(int n) { __atomic_add_fetch(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
 cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st) {
   if (a.n_rays <= 0) return cudaSuccess;
@@ -874,7 +878,7 @@ cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, int n_sm,
-                              cudaStream_t st) {
+                              cudaStream_t st, const ChebHdr *skip) {
   if (n <= 0) return cudaSuccess;
   const int64_t n4 = n / 4;
   if (n4 > 0) {
@@ -882,11 +886,11 @@ cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, i
     // the float4 view of split s starts at s * n floats: needs n % 4 == 0 for alignment
     if (n % 4 == 0) {
       k_sum_splits<<<g, 256, 0, st>>>(reinterpret_cast<const float4 *>(part), S, n4,
-                                      reinterpret_cast<float4 *>(out));
+                                      reinterpret_cast<float4 *>(out), skip);
       return counted(cudaGetLastError());
     }
   }
-  k_sum_splits_tail<<<grid1(n, 256), 256, 0, st>>>(part, S, n, 0, out);
+  k_sum_splits_tail<<<grid1(n, 256), 256, 0, st>>>(part, S, n, 0, out, skip);
   return counted(cudaGetLastError());
 }
 

@@ -31,7 +31,34 @@ struct BlendArgs {
   bool check_finite;
 };
 
+// Chebyshev-moment forward (rfr_cheb.cu): device-side choice written by k_cheb_setup
+struct ChebHdr {
+  unsigned sel;                    // 1: the Chebyshev path runs, 0: the direct kernel K2 runs
+  int P;                           // moments (16 / 32 / 48), 0 if not selected
+  double delta;                    // half spread of the delays, cycles per bin step
+  double inv;                      // (df / c) / delta: metres of path -> x in [-1, 1]
+};
+
+struct ChebArgs {
+  const Rec *rec;
+  int64_t n_s;
+  const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
+  int64_t n_a;
+  int n_f;
+  double kd, kc;                   // df / c and the centre frequency f0 + (n_f / 2) df over c
+  int64_t samples_per_split;
+  double *lc;                      // [n_a] centre path length (m)
+  ChebHdr *hdr;
+  float2 *coef;                    // [n_f][pmax]
+  int pmax;
+  float2 *part;                    // [split][n_a][pmax] partial moments
+  unsigned int *flags;
+  bool no_gain;
+  bool enable;                     // false: always the direct kernel
+};
+
 struct FwdArgs {
+  const ChebHdr *skip;             // non-NULL: return at once when the Chebyshev path was chosen
   const Rec *rec;
   int64_t n_s;
   const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
@@ -101,6 +128,7 @@ inline size_t adj_smem_ant_off(int n_f) { return align_up((size_t)kAdjGA * n_f *
 inline size_t adj_smem_bytes(int n_f) { return adj_smem_ant_off(n_f) + (size_t)kAdjGA * 56; }
 
 unsigned long long launch_count();
+void add_launches(int n);
 cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st);
 cudaError_t launch_trace_fwd(const FwdArgs &a, int B, bool mono, bool corr, int kind, int n_splits,
                              cudaStream_t st);
@@ -120,7 +148,13 @@ cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, 
                               cudaStream_t st);
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st);
 cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, int n_sm,
-                              cudaStream_t st);
+                              cudaStream_t st, const ChebHdr *skip = nullptr);
+constexpr int kChebPMax = 48;
+int cheb_box_blocks();
+int cheb_threads();
+cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_t st);
+cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,
+                            float2 *out, cudaStream_t st);
 cudaError_t launch_abs(const float *m, int64_t n, float *p, int n_sm, cudaStream_t st);
 cudaError_t launch_reduce_sum(const float *x, int64_t n, float *tmp, int tmp_n, float *out,
                               cudaStream_t st);
