@@ -136,7 +136,7 @@ bool cheb_enabled() {
 struct Layout {
   size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
          off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, off_cbox = 0, off_clc = 0,
-         off_ccoef = 0, off_cpart = 0, total = 0;
+         off_ccoef = 0, off_cpart = 0, off_cbadj = 0, total = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
@@ -174,6 +174,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   L.off_clc = take((size_t)std::max<int64_t>(n_a, 1) * 8);
   L.off_ccoef = take((size_t)nf * kChebPMax * 8);
   L.off_cpart = take(L.cap_cpart);
+  L.off_cbadj = take((size_t)std::max<int64_t>(n_a, 1) * kChebPMax * 2 * 8);
   L.total = o;
   return true;
 }
@@ -240,6 +241,33 @@ bool has_corr(const rfr_samples *s, const rfr_antennas *a) {
 }
 
 // K2 (trace) or K5 (matched-filter adjoint) over `rec` [n_pts] into out [n_a][n_f] (+ split sum)
+// Chebyshev-moment arguments for a call over `rec` (n_pts points) and this antenna set
+ChebArgs make_cheb(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
+                   const rfr_freq_grid *grid, bool no_gain, const rfr_workspace *ws,
+                   const Layout &L, int64_t per_split) {
+  ChebArgs c;
+  memset(&c, 0, sizeof(c));
+  c.rec = rec;
+  c.n_s = n_pts;
+  c.tx_x = ants->tx_x; c.tx_y = ants->tx_y; c.tx_z = ants->tx_z;
+  c.rx_x = ants->rx_x; c.rx_y = ants->rx_y; c.rx_z = ants->rx_z;
+  c.phi_tx = ants->phi_tx; c.phi_rx = ants->phi_rx;
+  c.n_a = ants->n_ant;
+  c.n_f = grid->n_freq;
+  c.kd = grid->df_hz / kC;
+  c.kc = (grid->f0_hz + (double)(grid->n_freq / 2) * grid->df_hz) / kC;
+  c.samples_per_split = per_split;
+  c.lc = at<double>(ws, L.off_clc);
+  c.hdr = at<ChebHdr>(ws, kChebHdrOff);
+  c.coef = at<float2>(ws, L.off_ccoef);
+  c.pmax = kChebPMax;
+  c.part = at<float2>(ws, L.off_cpart);
+  c.flags = at<unsigned>(ws, 0);
+  c.no_gain = no_gain;
+  c.enable = cheb_enabled();
+  return c;
+}
+
 rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
                    const rfr_freq_grid *grid, bool no_gain, bool corr, int kind, float *out,
                    const rfr_workspace *ws, const Layout &L, cudaStream_t st) {
@@ -271,27 +299,8 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   const Split cs = cheb_split(n_pts, ants->n_ant);
   const bool cheb = ants->n_ant > 0 && n_pts > 0 &&
                     (size_t)cs.splits * ants->n_ant * kChebPMax * 8 <= L.cap_cpart;
-  ChebArgs c;
-  memset(&c, 0, sizeof(c));
+  const ChebArgs c = make_cheb(rec, n_pts, ants, grid, no_gain, ws, L, cs.per_split);
   if (cheb) {
-    c.rec = rec;
-    c.n_s = n_pts;
-    c.tx_x = ants->tx_x; c.tx_y = ants->tx_y; c.tx_z = ants->tx_z;
-    c.rx_x = ants->rx_x; c.rx_y = ants->rx_y; c.rx_z = ants->rx_z;
-    c.phi_tx = ants->phi_tx; c.phi_rx = ants->phi_rx;
-    c.n_a = ants->n_ant;
-    c.n_f = grid->n_freq;
-    c.kd = grid->df_hz / kC;
-    c.kc = (grid->f0_hz + (double)(grid->n_freq / 2) * grid->df_hz) / kC;
-    c.samples_per_split = cs.per_split;
-    c.lc = at<double>(ws, L.off_clc);
-    c.hdr = hdr;
-    c.coef = at<float2>(ws, L.off_ccoef);
-    c.pmax = kChebPMax;
-    c.part = at<float2>(ws, L.off_cpart);
-    c.flags = at<unsigned>(ws, 0);
-    c.no_gain = no_gain;
-    c.enable = cheb_enabled();
     RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
     a.skip = hdr;
   }
@@ -514,7 +523,18 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;
+  // Chebyshev-moment adjoint (rfr_cheb.cu), chosen on the device; the direct kernels return at
+  // once when it runs
+  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0);
+  const bool cheb = ants->n_ant > 0;
+  if (cheb) {
+    RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
+    a.skip = c.hdr;
+  }
   RFR_CU(launch_adjoint(a, kModeBwd, mono, has_corr(samples, ants), sp.splits, st));
+  if (cheb)
+    RFR_CU(launch_cheb_adj(c, a, at<float2>(ws, L.off_cbadj), kModeBwd, mono,
+                           has_corr(samples, ants), sp.splits, st));
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
                              device_sms(), st));
@@ -610,7 +630,16 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;
+  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0);
+  const bool cheb = ants->n_ant > 0;
+  if (cheb) {
+    RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
+    a.skip = c.hdr;
+  }
   RFR_CU(launch_adjoint(a, kModeBoth, mono, has_corr(samples, ants), sp.splits, st));
+  if (cheb)
+    RFR_CU(launch_cheb_adj(c, a, at<float2>(ws, L.off_cbadj), kModeBoth, mono,
+                           has_corr(samples, ants), sp.splits, st));
   if (sp.splits > 1) {
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
                              device_sms(), st));

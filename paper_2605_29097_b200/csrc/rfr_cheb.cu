@@ -292,6 +292,198 @@ __global__ void k_cheb_out(ChebArgs a, int splits, float2 *__restrict__ out) {
   }
 }
 
+// =============================================================================== adjoint
+// E_ij h_ij = sum_m X_i[m] e^{+j 2 pi f_m tau_ij} = e^{+j 2 pi f_c tau_ij} sum_p T_p(x_ij) B_i[p],
+//     B_i[p] = sum_m X_i[m] e^{+j 2 pi m' u_c,i} conj(a[m][p])
+// (the conjugate expansion e^{+j z x} = sum_p eps_p j^p J_p(z) T_p(x)).  k_cheb_adj_prep forms the
+// antenna moments B (fixed-order sums), k_cheb_adj runs one thread per sample over the antennas of
+// its split with the Reinsch recurrence and the Eq. 5 / matched-filter epilogue of the direct
+// kernels.  bmom layout: [n_a][kChebPMax][2] float2 (X row 0 = G or the signal, row 1 = the signal
+// in the fused sweep), so one 16-byte load feeds both MACs of a moment.
+constexpr int kAdjPrepThreads = 256;
+
+__global__ void __launch_bounds__(kAdjPrepThreads) k_cheb_adj_prep(ChebArgs c, const float2 *X0,
+                                                                   const float2 *X1, int nx,
+                                                                   float2 *__restrict__ bmom) {
+  if (c.hdr->sel == 0) return;
+  extern __shared__ float2 ysh[];                 // [n_f] rotated row, then [8][64] partials
+  const int P = c.hdr->P;
+  const int64_t i = blockIdx.x;
+  const double uc = c.lc[i] * c.kd;
+  const int N = c.n_f;
+  float2 *part = ysh + N;
+  for (int x = 0; x < nx; ++x) {
+    const float2 *row = (x == 0 ? X0 : X1) + i * N;
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+      float ps, pc;                                // e^{+j 2 pi m' u_c}
+      sincospif(2.f * frac_cycles((double)(m - N / 2) * uc), &ps, &pc);
+      const float2 v = row[m];
+      ysh[m] = make_float2(fmaf(pc, v.x, -ps * v.y), fmaf(pc, v.y, ps * v.x));
+    }
+    __syncthreads();
+    // thread (p, q): partial over bins m = q, q + 8, ... ; then a fixed-order sum over q
+    const int p = threadIdx.x & 63, q = threadIdx.x >> 6;     // 64 x 4
+    float re = 0.f, im = 0.f;
+    if (p < P)
+      for (int m = q; m < N; m += 4) {
+        const float2 a = c.coef[(int64_t)m * c.pmax + p], y = ysh[m];   // y conj(a)
+        re = fmaf(y.x, a.x, fmaf(y.y, a.y, re));
+        im = fmaf(y.y, a.x, fmaf(-y.x, a.y, im));
+      }
+    part[q * 64 + p] = make_float2(re, im);
+    __syncthreads();
+    if (threadIdx.x < P) {
+      float2 v = part[threadIdx.x];
+      for (int qq = 1; qq < 4; ++qq) {
+        v.x += part[qq * 64 + threadIdx.x].x;
+        v.y += part[qq * 64 + threadIdx.x].y;
+      }
+      bmom[(i * kChebPMax + threadIdx.x) * 2 + x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kChebGA = 16;                        // antennas per shared-memory stage
+
+template <int P, int MODE, bool MONO, bool CORR>
+__global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArgs a,
+                                                              const float2 *__restrict__ bmom) {
+  if (c.hdr->P != P) return;
+  constexpr int NX = MODE == kModeBoth ? 2 : 1;
+  constexpr int GEO = MODE == kModeFlt ? kModeFlt : kModeBwd;
+  __shared__ __align__(16) float4 bs[kChebGA][P];   // (B_0[p], B_1[p]) per antenna of the stage
+  __shared__ AntF as[kChebGA];
+  __shared__ double ls[kChebGA];
+  const int tid = threadIdx.x;
+  const int64_t j = (int64_t)blockIdx.x * kChebThreads + tid;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  const bool valid = j < a.n_s;
+  const Rec rec = load_point<GEO>(a, j, valid);
+  const bool no_gain = a.no_gain;
+  const double inv = c.hdr->inv;
+  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f, M1 = 0.f, M2 = 0.f;
+  bool domain = false;
+  for (int64_t i0 = i_lo; i0 < i_hi; i0 += kChebGA) {
+    const int ga = (int)min((int64_t)kChebGA, i_hi - i0);
+    __syncthreads();
+    for (int t = tid; t < ga * P; t += kChebThreads) {
+      const int aa = t / P, p = t % P;
+      bs[aa][p] = reinterpret_cast<const float4 *>(bmom)[(i0 + aa) * kChebPMax + p];
+    }
+    if (tid < ga) {
+      as[tid] = load_antf<MONO>(a, i0 + tid);
+      ls[tid] = c.lc[i0 + tid];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = widen_ant<MONO>(as[aa]);
+      PairBwd g;
+      double L;
+      if (GEO == kModeBwd) {
+        pair_geometry<MONO, CORR>(rec, an, no_gain, g);
+        domain |= valid && !g.ok;
+        L = g.L;
+      } else {
+        L = pair_length<MONO>(rec, an);
+      }
+      float es, ec;                                 // E_c = e^{+j 2 pi f_c tau}
+      __sincosf(kTwoPi * frac_cycles(L * c.kc), &es, &ec);
+      float x = (float)((L - ls[aa]) * inv);
+      x = fminf(fmaxf(x, -1.f), 1.f);
+      const float xm1 = fabsf(x) - 1.f, twoxm1 = 2.f * xm1;
+      const float4 *B = bs[aa];
+      // even / odd partial sums in T_p(|x|); T_p(x) = (-1)^p T_p(|x|)
+      float4 b = B[0];
+      f2x he0 = pk(b.x, b.y), he1 = pk(b.z, b.w), ho0 = 0ull, ho1 = 0ull;
+      float t = 1.f, d = xm1;
+      t += d;                                       // T_1
+      b = B[1];
+      ho0 = ffma2(pk(t, t), pk(b.x, b.y), ho0);
+      if (NX == 2) ho1 = ffma2(pk(t, t), pk(b.z, b.w), ho1);
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d = fmaf(twoxm1, t, d);
+        t += d;
+        b = B[p];
+        if (p & 1) {
+          ho0 = ffma2(pk(t, t), pk(b.x, b.y), ho0);
+          if (NX == 2) ho1 = ffma2(pk(t, t), pk(b.z, b.w), ho1);
+        } else {
+          he0 = ffma2(pk(t, t), pk(b.x, b.y), he0);
+          if (NX == 2) he1 = ffma2(pk(t, t), pk(b.z, b.w), he1);
+        }
+      }
+      const float sg = x < 0.f ? -1.f : 1.f;
+      const float2 h0 = upk(ffma2(pk(sg, sg), ho0, he0));
+      if (MODE == kModeBwd) {
+        adj_accumulate<kModeBwd>(g, ec, es, h0.x, h0.y, S1, S2, S3x, S3y, S3z);
+      } else if (MODE == kModeFlt) {
+        adj_accumulate<kModeFlt>(g, ec, es, h0.x, h0.y, M1, M2, S3x, S3y, S3z);
+      } else {
+        const float2 h1 = upk(ffma2(pk(sg, sg), ho1, he1));
+        adj_accumulate<kModeBwd>(g, ec, es, h0.x, h0.y, S1, S2, S3x, S3y, S3z);
+        adj_accumulate<kModeFlt>(g, ec, es, h1.x, h1.y, M1, M2, S3x, S3y, S3z);
+      }
+    }
+  }
+  if (domain) atomicOr(a.flags, 1u);
+  if (valid) {
+    if (MODE == kModeBwd) {
+      adj_store<kModeBwd>(a, j, S1, S2, S3x, S3y, S3z);
+    } else if (MODE == kModeFlt) {
+      adj_store<kModeFlt>(a, j, M1, M2, 0.f, 0.f, 0.f);
+    } else {
+      adj_store<kModeBwd>(a, j, S1, S2, S3x, S3y, S3z);
+      reinterpret_cast<float2 *>(a.out2)[(int64_t)blockIdx.y * a.n_s + j] = make_float2(M1, M2);
+    }
+  }
+}
+
+template <int MODE, bool MONO, bool CORR>
+static cudaError_t cheb_adj_all(const ChebArgs &c, const AdjArgs &a, const float2 *bmom, dim3 g,
+                                cudaStream_t st) {
+  k_cheb_adj<16, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  k_cheb_adj<32, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  k_cheb_adj<48, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, int mode,
+                            bool mono, bool corr, int n_splits, cudaStream_t st) {
+  if (a.n_a <= 0 || a.n_s <= 0) return cudaSuccess;
+  const int nx = mode == kModeBoth ? 2 : 1;
+  const size_t sm = ((size_t)c.n_f + 4 * 64) * sizeof(float2);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_cheb_adj_prep,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  k_cheb_adj_prep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(c, a.X, mode == kModeBoth ? a.X2
+                                                                                         : a.X,
+                                                                nx, bmom);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g((unsigned)((a.n_s + kChebThreads - 1) / kChebThreads), (unsigned)n_splits);
+  if (mode == kModeBwd)
+    e = mono ? (corr ? cheb_adj_all<kModeBwd, true, true>(c, a, bmom, g, st)
+                     : cheb_adj_all<kModeBwd, true, false>(c, a, bmom, g, st))
+             : (corr ? cheb_adj_all<kModeBwd, false, true>(c, a, bmom, g, st)
+                     : cheb_adj_all<kModeBwd, false, false>(c, a, bmom, g, st));
+  else if (mode == kModeBoth)
+    e = mono ? (corr ? cheb_adj_all<kModeBoth, true, true>(c, a, bmom, g, st)
+                     : cheb_adj_all<kModeBoth, true, false>(c, a, bmom, g, st))
+             : (corr ? cheb_adj_all<kModeBoth, false, true>(c, a, bmom, g, st)
+                     : cheb_adj_all<kModeBoth, false, false>(c, a, bmom, g, st));
+  else
+    e = mono ? cheb_adj_all<kModeFlt, true, false>(c, a, bmom, g, st)
+             : cheb_adj_all<kModeFlt, false, false>(c, a, bmom, g, st);
+  if (e == cudaSuccess) add_launches(4);
+  return e;
+}
+
 // ------------------------------------------------------------------------------- launchers
 template <int P, bool MONO, bool CORR, int KIND>
 static cudaError_t cheb_fwd_t(const ChebArgs &a, dim3 g, cudaStream_t st) {

@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kFwdThreads, fwd_min_blocks(B)) k_trace_fwd(Fw
 // (operand reuse cache), so each FFMA2 reads at most two registers per bank.
 template <int MODE, bool MONO, bool CORR, int NF>
 __global__ void __launch_bounds__(kAdjThreads + 32, 4) k_adjoint_tma(AdjArgs a) {
+  if (a.skip && a.skip->sel) return;
   constexpr int GA = adj_stage_ants(NF);
   constexpr int NS = kAdjStages;
   constexpr int H = NF / 2;
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(kAdjThreads + 32, 4) k_adjoint_tma(AdjArgs a) 
 // sums) favours sharing the stage across two samples.
 template <int MODE, bool MONO, bool CORR, int NF>
 __global__ void __launch_bounds__(kAdjThreads) k_adjoint_s2(AdjArgs a) {
+  if (a.skip && a.skip->sel) return;
   constexpr int SPT = 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
@@ -483,6 +485,7 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint_s2(AdjArgs a) {
 // Generic bin count (or unaligned rows): one buffer of kAdjGA antennas, CTA barriers, rolled Horner.
 template <int MODE, bool MONO, bool CORR>
 __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
+  if (a.skip && a.skip->sel) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
   AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]

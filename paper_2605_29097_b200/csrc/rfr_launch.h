@@ -8,6 +8,15 @@ namespace rfr {
 
 struct Rec;
 
+// Chebyshev-moment forward (rfr_cheb.cu): device-side choice written by k_cheb_setup
+struct ChebHdr {
+  unsigned sel;                    // 1: the Chebyshev path runs, 0: the direct kernel K2 runs
+  int P;                           // moments (16 / 32 / 48), 0 if not selected
+  double delta;                    // half spread of the delays, cycles per bin step
+  double inv;                      // (df / c) / delta: metres of path -> x in [-1, 1]
+};
+
+
 constexpr int kFwdThreads = 128;   // K2 CTA size (4 warps)
 constexpr int kFwdMinBlocks = 3;   // K2 CTAs per SM (register budget ~170)
 constexpr int kFwdWarps = kFwdThreads / 32;
@@ -29,14 +38,6 @@ struct BlendArgs {
   Rec *rec;
   unsigned int *flags;
   bool check_finite;
-};
-
-// Chebyshev-moment forward (rfr_cheb.cu): device-side choice written by k_cheb_setup
-struct ChebHdr {
-  unsigned sel;                    // 1: the Chebyshev path runs, 0: the direct kernel K2 runs
-  int P;                           // moments (16 / 32 / 48), 0 if not selected
-  double delta;                    // half spread of the delays, cycles per bin step
-  double inv;                      // (df / c) / delta: metres of path -> x in [-1, 1]
 };
 
 struct ChebArgs {
@@ -88,6 +89,7 @@ struct AdjArgs {
   float *out;                      // K3: [split][5][n_s]; K4: [split][n_s] complex
   const float2 *X2;                // kModeBoth: the signal s, [n_a][n_f] (filter at the samples)
   float *out2;                     // kModeBoth: [split][n_s] complex partial M
+  const ChebHdr *skip;      // non-NULL: return at once when the Chebyshev adjoint was chosen
   unsigned char *bprep;            // tensor-core path: per-antenna B^T images (hi | lo), or NULL
   size_t bprep_cap;                // bytes available at bprep
   size_t smem_ant_off;
@@ -155,6 +157,9 @@ int cheb_threads();
 cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_t st);
 cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,
                             float2 *out, cudaStream_t st);
+// adjoint (K3 / fused K3+K4) by Chebyshev moments: B_i[p] per antenna, then per pair P steps
+cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, int mode,
+                            bool mono, bool corr, int n_splits, cudaStream_t st);
 cudaError_t launch_abs(const float *m, int64_t n, float *p, int n_sm, cudaStream_t st);
 cudaError_t launch_reduce_sum(const float *x, int64_t n, float *tmp, int tmp_n, float *out,
                               cudaStream_t st);

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
   __shared__ __align__(8) unsigned long long mma_bar, full_bar[2];
   __shared__ unsigned tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5;
+  if (a.skip && a.skip->sel) return;              // the Chebyshev adjoint was chosen
   const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(kAdjThreads, TCShape<NF, MODE == kModeBoth ? 2
 // lo = x - hi.  The inverse scales 2^e go to a float2 per antenna after the images.  One warp
 // per antenna; HBM-bound, ~0.05 ms at c3.
 __global__ void k_prep_bt(const float2 *__restrict__ X, const float2 *__restrict__ X2, int64_t n_a,
-                          int nf, int nx, unsigned char *__restrict__ out) {
+                          int nf, int nx, unsigned char *__restrict__ out, const ChebHdr *skip) {
+  if (skip && skip->sel) return;
   const int lane = threadIdx.x & 31;
   const int N1 = nf / 8, N = nx * N1;
   const size_t bbytes = (size_t)N * 128;                 // hi + lo, N rows x 64 B each
@@ -419,7 +421,7 @@ cudaError_t launch_adjoint_tc(const AdjArgs &a, int mode, bool mono, bool corr, 
   if (a.n_a > 0) {
     const int nx = mode == kModeBoth ? 2 : 1;
     const unsigned g = (unsigned)std::min<int64_t>((a.n_a + 7) / 8, 148 * 32);   // 8 warps / CTA
-    k_prep_bt<<<g, 256, 0, st>>>(a.X, a.X2, a.n_a, a.n_f, nx, a.bprep);
+    k_prep_bt<<<g, 256, 0, st>>>(a.X, a.X2, a.n_a, a.n_f, nx, a.bprep, a.skip);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

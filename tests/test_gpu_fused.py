@@ -95,7 +95,9 @@ def test_fused_tiny_variants(n_freq, variant):
 
 
 def test_fused_matches_separate_calls():
-    """Same outputs as rfr_backward + rfr_filter(queries = samples) on c2 (rounding-level)."""
+    """Same outputs as rfr_backward + rfr_filter(queries = samples) on c2: the gradients come from
+    the same kernel family (rounding-level); the standalone filter runs the tensor-core sweep while
+    the fused call takes the Chebyshev-moment path, so M / |M| agree to the parity tolerance."""
     m = rfr()
     p = problem("c2")
     b = p.bundles[0]
@@ -114,7 +116,7 @@ def test_fused_matches_separate_calls():
     for k in FIELDS:
         a = getattr(out, k).cpu().numpy().astype(np.float64)
         assert rel(g[k], a) <= 1e-5, k
-    assert rel(M, c64(M2)) <= 1e-6 and rel(P, P2.cpu().numpy()) <= 1e-6
+    assert rel(M, c64(M2)) <= TOL_SIG and rel(P, P2.cpu().numpy()) <= TOL_SIG
 
 
 def test_fused_empty_and_errors():
