@@ -262,6 +262,17 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step()
     barrier()
+    # which path the device chose (Chebyshev moments or direct kernels): one forward and one
+    # backward on bundle 0, read back from the workspace header (untimed diagnostic)
+    s0 = B[0]
+    rfr.rfr_forward(s0["S"], prob.sharpness, s0["A"], grid, s0["sig"], s0["ws"])
+    cf = rfr.cheb_state(s0["ws"])
+    rfr.rfr_backward_partial(s0["G"], s0["S"], prob.sharpness, s0["A"], grid, s0["part"], s0["ws"],
+                             flags=rfr.RFR_REUSE_BLEND)
+    ca = rfr.cheb_state(s0["ws"])
+    cheb_fwd_P = cf["P"] if cf["sel"] else 0
+    cheb_adj_P = ca["P"] if ca["sel"] else 0
+    barrier()
 
     # ---------------- timed region: K steps, per-step events, L2 flushed between steps
     n0 = rfr.rfr_launch_count()
@@ -315,18 +326,46 @@ def run_gpu(args):
     per_step = lambda ms: ms / args.steps
     clk_ratio = (clocks["sm_mhz"] / pk.get("sm_max_mhz", 1965.0)) if clocks.get("sm_mhz") else None
     roofs = []
-    # K2 forward: FP32-pipe bound, 4 lane-ops per contribution (1 FFMA2 + 1 FADD2)
-    ach = OPS_PER_CONTRIB * (Nc / world) / (per_step(f_ms) * 1e-3)
-    roofs.append({"kernel": "k_trace_fwd (K2, rfr_forward)", "bound": "alu",
-                  "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
-                  "frac": ach / peak_ops,
-                  "frac_at_measured_clock": ach / (peak_ops * clk_ratio) if clk_ratio else None,
-                  "ms_per_step": per_step(f_ms)})
-    if fused:
+    n_pairs = sum(b.samples.n * b.antennas.n for b in prob.bundles) / world
+    if cheb_fwd_P:
+        # Chebyshev-moment forward: per pair P steps of 1 FFMA + 1 FADD (Reinsch recurrence) +
+        # 1 FFMA2 (complex-real moment update) = 4 P FP32 lane-ops
+        ach = 4 * cheb_fwd_P * n_pairs / (per_step(f_ms) * 1e-3)
+        roofs.append({"kernel": f"k_cheb_fwd<P={cheb_fwd_P}> (rfr_forward)", "bound": "alu",
+                      "achieved": ach / 1e12, "peak": peak_ops / 1e12,
+                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
+                      "lane_ops_per_pair": 4 * cheb_fwd_P, "ms_per_step": per_step(f_ms)})
+    else:
+        # K2 forward: FP32-pipe bound, 4 lane-ops per contribution (1 FFMA2 + 1 FADD2)
+        ach = OPS_PER_CONTRIB * (Nc / world) / (per_step(f_ms) * 1e-3)
+        roofs.append({"kernel": "k_trace_fwd (K2, rfr_forward)", "bound": "alu",
+                      "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
+                      "frac": ach / peak_ops,
+                      "frac_at_measured_clock": ach / (peak_ops * clk_ratio) if clk_ratio else None,
+                      "ms_per_step": per_step(f_ms)})
+    if cheb_adj_P:
+        # Chebyshev-moment adjoint: per pair P steps of 1 FFMA + 1 FADD + one FFMA2 per X row
+        # (two in the fused sweep) = (2 + 2 nx) P FP32 lane-ops
+        nx = 2 if fused else 1
+        ops = (2 + 2 * nx) * cheb_adj_P
+        for name, ms in ([("k_cheb_adj<both> (K3+K4 fused + K1', rfr_backward_filter)", b_ms)]
+                         if fused else [("k_cheb_adj<bwd> (K3 + K1', rfr_backward)", b_ms)]):
+            ach = ops * n_pairs / (per_step(ms) * 1e-3)
+            roofs.append({"kernel": f"{name.split()[0]}<P={cheb_adj_P}> " + " ".join(name.split()[1:]),
+                          "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
+                          "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
+                          "lane_ops_per_pair": ops, "ms_per_step": per_step(ms)})
+    if cheb_adj_P and fused:
+        pass
+    elif fused:
         adj = [("k_adjoint_tc<both> (K3+K4 fused +K1', rfr_backward_filter)", b_ms, 2)]
+    elif cheb_adj_P:
+        adj = [("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms, 1)]
     else:
         adj = [("k_adjoint_tc<bwd> (K3+K1', rfr_backward)", b_ms, 1),
                ("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms, 1)]
+    if cheb_adj_P and fused:
+        adj = []
     for name, ms, npass in adj:
         rate = npass * (Nc / world) / (per_step(ms) * 1e-3)     # contributions of all its passes
         if tc:
@@ -345,14 +384,16 @@ def run_gpu(args):
     dom = max(roofs, key=lambda r: r["ms_per_step"])
     traffic = None
     try:   # bytes per launch from the committed full-size ncu capture (profiles/traffic.json)
-        key = dom["kernel"].split()[0]
+        key = dom["kernel"].split()[0].split("<P=")[0]
         traffic = json.load(open(TRAFFIC_PATH)).get(args.config, {}).get(key)
     except Exception:
         pass
     roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
             "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
-            "peak_note": ("148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); 4 lane-ops "
-                          "per contribution" if dom["bound"] == "alu" else
+            "peak_note": ("148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); "
+                          + (f"{dom['lane_ops_per_pair']} lane-ops per (sample, antenna) pair "
+                             "(Chebyshev moments)" if "lane_ops_per_pair" in dom else
+                             "4 lane-ops per contribution") if dom["bound"] == "alu" else
                           "measured bf16 burst peak (kind::f16 runs at the bf16 rate); 24 tensor "
                           "FLOP per contribution (3xFP16)")}
     cpu = None
@@ -371,10 +412,10 @@ def run_gpu(args):
                        "n_antennas": [b.antennas.n for b in prob.bundles][0],
                        "n_freq": grid.n_freq, "parallelism": f"antenna-shard x{world}",
                        "l2": "flushed between steps (512 MiB memset, outside the step events)",
-                       "step": ("K1 blend + K2 forward + K6 loss + K3/K4 fused backward + "
+                       "step": ("K1 blend + forward + K6 loss + K3/K4 fused backward + "
                                 "matched filter at the samples (+NCCL all-reduce of partials and "
                                 "M) + K1' finish" if fused else
-                                "K1 blend + K2 forward + K4 filter (+NCCL all-reduce of M) + K6 "
+                                "K1 blend + forward + K4 filter (+NCCL all-reduce of M) + K6 "
                                 "loss + K3 backward (+NCCL all-reduce of partials) + K1' finish")},
             "passes": ({"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
                         "filter_plus_bwd_fused_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
@@ -385,6 +426,10 @@ def run_gpu(args):
                         "bwd_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
                         "fwd_plus_bwd_G_per_s": Nc / (per_step(f_ms + b_ms) * 1e-3) / 1e9,
                         "loss_ms": per_step(l_ms)}),
+            "method": {"forward": f"chebyshev-moments P={cheb_fwd_P} (delta={cf['delta']:.4g} cycles)"
+                       if cheb_fwd_P else "direct recurrence (K2)",
+                       "adjoint": f"chebyshev-moments P={cheb_adj_P} (delta={ca['delta']:.4g} cycles)"
+                       if cheb_adj_P else "tensor-core 16-bin block GEMM"},
             "roofline": roof, "rooflines": roofs, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed": t_wall}
     print(json.dumps(line), flush=True)

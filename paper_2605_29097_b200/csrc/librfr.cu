@@ -454,7 +454,18 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = false;
   const bool mono = ants->rx_x == nullptr;
+  // Chebyshev-moment filter: the query points are packed as records (for their bounding box)
+  const bool cheb = ants->n_ant > 0;
+  const ChebArgs c = make_cheb(at<Rec>(ws, L.off_qrec), n_query, ants, grid, false, ws, L, 0);
+  if (cheb) {
+    RFR_CU(launch_pack_points(qx, qy, qz, n_query, at<Rec>(ws, L.off_qrec), device_sms(), st));
+    RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
+    a.skip = c.hdr;
+  }
   RFR_CU(launch_adjoint(a, kModeFlt, mono, false, sp.splits, st));
+  if (cheb)
+    RFR_CU(launch_cheb_adj(c, a, at<float2>(ws, L.off_cbadj), kModeFlt, mono, false, sp.splits,
+                           st));
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, n_query * 2, M, device_sms(),
                              st));

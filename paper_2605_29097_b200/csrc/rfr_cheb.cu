@@ -37,6 +37,28 @@ constexpr int kChebThreads = 128;
 constexpr int kChebTJ = 32;                       // records per shared-memory tile
 }  // namespace
 
+// query points as records (fp64 position; only the box kernel reads them)
+__global__ void k_pack_points(const float *__restrict__ x, const float *__restrict__ y,
+                              const float *__restrict__ z, int64_t n, Rec *__restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    Rec r;
+    r.x = x[q]; r.y = y[q]; r.z = z[q];
+    r.w = 0.f; r.T = 1.f; r.nx = r.ny = 0.f; r.nz = 1.f; r.papr = 1.f;
+    out[q] = r;
+  }
+}
+
+cudaError_t launch_pack_points(const float *x, const float *y, const float *z, int64_t n, Rec *out,
+                               int n_sm, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)n_sm * 8);
+  k_pack_points<<<g, 256, 0, st>>>(x, y, z, n, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(1);
+  return e;
+}
+
 // ------------------------------------------------------------------ bounding box of the samples
 __global__ void k_cheb_box(const Rec *__restrict__ rec, int64_t n, double *__restrict__ part) {
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};

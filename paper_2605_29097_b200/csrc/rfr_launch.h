@@ -153,6 +153,8 @@ cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, i
                               cudaStream_t st, const ChebHdr *skip = nullptr);
 constexpr int kChebPMax = 48;
 int cheb_box_blocks();
+cudaError_t launch_pack_points(const float *x, const float *y, const float *z, int64_t n, Rec *out,
+                               int n_sm, cudaStream_t st);
 int cheb_threads();
 cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_t st);
 cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,

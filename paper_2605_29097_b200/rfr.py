@@ -236,6 +236,15 @@ class Workspace:
         return w
 
 
+def cheb_state(ws: Workspace) -> dict:
+    """Diagnostic (synchronous): the Chebyshev-moment choice the LAST call on this workspace took,
+    read from the workspace header (librfr.cu kChebHdrOff): sel (0 = direct kernels), P, delta."""
+    import struct as _st
+    raw = bytes(ws.tensor[64:88].cpu().numpy().tobytes())
+    sel, P, delta, inv = _st.unpack("<Iidd", raw)
+    return {"sel": sel, "P": P, "delta": delta}
+
+
 def workspace(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0, device="cuda") -> Workspace:
     return Workspace(n_samples, n_ant, n_freq, n_query, device)
 
