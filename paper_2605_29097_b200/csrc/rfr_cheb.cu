@@ -235,42 +235,59 @@ __global__ void __launch_bounds__(kChebThreads, P <= 32 ? 4 : 3) k_cheb_fwd(Cheb
     __syncthreads();
     if (jt + kChebTJ < j_hi) prefetch(jt + kChebTJ, b ^ 1);
     const int nv = (int)min((int64_t)kChebTJ, j_hi - jt);
+    // two samples per step: their Reinsch recurrences run packed in one FFMA2 / FADD2 (lanes =
+    // samples), each moment update is one FFMA2 per sample.  An odd tail pairs the last record
+    // with a zero record of the tile (w = 0).
 #pragma unroll 1
-    for (int jj = 0; jj < nv; ++jj) {
-      const Rec rec = rb[b][jj];
-      double L;
-      float Ar, Ai;
-      if (KIND == kFwdTrace) {
-        PairBwd g;
-        pair_geometry<MONO, CORR>(rec, an, no_gain, g);
-        domain |= ant_ok && !g.ok;
-        Ar = rec.w * g.gg * g.Tt * g.Tr;
-        Ai = 0.f;
-        L = g.L;
-      } else {
-        L = pair_length<MONO>(rec, an);
-        Ar = rec.w;
-        Ai = rec.T;
+    for (int jj = 0; jj < nv; jj += 2) {
+      f2x cc0 = 0ull, co0 = 0ull, cc1 = 0ull, co1 = 0ull;
+      float xv0 = 0.f, xv1 = 0.f;
+#pragma unroll 1
+      for (int u = 0; u < 2; ++u) {
+        const Rec rec = rb[b][jj + u];
+        double L;
+        float Ar, Ai;
+        if (KIND == kFwdTrace) {
+          PairBwd g;
+          pair_geometry<MONO, CORR>(rec, an, no_gain, g);
+          domain |= ant_ok && (jj + u < nv) && !g.ok;
+          Ar = rec.w * g.gg * g.Tt * g.Tr;
+          Ai = 0.f;
+          L = g.L;
+        } else {
+          L = pair_length<MONO>(rec, an);
+          Ar = rec.w;
+          Ai = rec.T;
+        }
+        // c = A exp(-j 2 pi f_c tau) from the fp64 cycle count at the centre frequency
+        float es, ec;
+        __sincosf(kTwoPi * frac_cycles(L * a.kc), &es, &ec);
+        const f2x c = (KIND == kFwdTrace) ? pk(Ar * ec, -Ar * es)
+                                          : pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
+        float x = (float)((L - Lc) * inv);
+        x = fminf(fmaxf(x, -1.f), 1.f);
+        const f2x cneg = x < 0.f ? pk(-upk(c).x, -upk(c).y) : c;   // odd moments: T_p(x) = -T_p(|x|)
+        if (u == 0) { cc0 = c; co0 = cneg; xv0 = fabsf(x) - 1.f; }
+        else { cc1 = c; co1 = cneg; xv1 = fabsf(x) - 1.f; }
       }
-      // c = A exp(-j 2 pi f_c tau) from the fp64 cycle count at the centre frequency
-      float es, ec;
-      __sincosf(kTwoPi * frac_cycles(L * a.kc), &es, &ec);
-      const f2x c = (KIND == kFwdTrace) ? pk(Ar * ec, -Ar * es)
-                                        : pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
-      float x = (float)((L - Lc) * inv);
-      x = fminf(fmaxf(x, -1.f), 1.f);
-      // T_p(x) = (-1)^p T_p(|x|): odd moments take -c for x < 0
-      const f2x co = x < 0.f ? pk(-upk(c).x, -upk(c).y) : c;
-      const float xm1 = fabsf(x) - 1.f, twoxm1 = 2.f * xm1;
-      float t = 1.f, d = xm1;                      // T_0, d_1 = T_1 - T_0
-      acc2(M[0], c);
-      t += d;                                      // T_1
-      M[1] = ffma2(pk(t, t), co, M[1]);
+      const f2x cc[2] = {cc0, cc1}, co[2] = {co0, co1};
+      const f2x xm1 = pk(xv0, xv1), two_xm1 = pk(2.f * xv0, 2.f * xv1);
+      f2x d = xm1, t = pk(1.f, 1.f);
+      acc2(M[0], cc[0]);
+      acc2(M[0], cc[1]);
+      t = fadd2(t, d);                                     // (T_1, T_1')
+      {
+        const float2 tv = upk(t);
+        M[1] = ffma2(pk(tv.x, tv.x), co[0], M[1]);
+        M[1] = ffma2(pk(tv.y, tv.y), co[1], M[1]);
+      }
 #pragma unroll
       for (int p = 2; p < P; ++p) {
-        d = fmaf(twoxm1, t, d);
-        t += d;
-        M[p] = ffma2(pk(t, t), (p & 1) ? co : c, M[p]);
+        d = ffma2(two_xm1, t, d);
+        t = fadd2(t, d);
+        const float2 tv = upk(t);
+        M[p] = ffma2(pk(tv.x, tv.x), (p & 1) ? co[0] : cc[0], M[p]);
+        M[p] = ffma2(pk(tv.y, tv.y), (p & 1) ? co[1] : cc[1], M[p]);
       }
     }
   }
@@ -368,6 +385,9 @@ __global__ void __launch_bounds__(kAdjPrepThreads) k_cheb_adj_prep(ChebArgs c, c
 
 constexpr int kChebGA = 16;                        // antennas per shared-memory stage
 
+// Two samples per thread (j and j + 128 of a 256-sample CTA tile): their Reinsch recurrences run
+// packed (one FFMA2 + one FADD2 per moment for both) and every B[p] load from shared memory feeds
+// the moment updates of both samples.
 template <int P, int MODE, bool MONO, bool CORR>
 __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArgs a,
                                                               const float2 *__restrict__ bmom) {
@@ -378,14 +398,20 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
   __shared__ AntF as[kChebGA];
   __shared__ double ls[kChebGA];
   const int tid = threadIdx.x;
-  const int64_t j = (int64_t)blockIdx.x * kChebThreads + tid;
+  const int64_t jb = (int64_t)blockIdx.x * (2 * kChebThreads) + tid;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
-  const bool valid = j < a.n_s;
-  const Rec rec = load_point<GEO>(a, j, valid);
+  bool valid[2];
+  Rec rec[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    valid[u] = jb + u * kChebThreads < a.n_s;
+    rec[u] = load_point<GEO>(a, jb + u * kChebThreads, valid[u]);
+  }
   const bool no_gain = a.no_gain;
   const double inv = c.hdr->inv;
-  float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f, M1 = 0.f, M2 = 0.f;
+  float S1[2] = {0.f, 0.f}, S2[2] = {0.f, 0.f}, S3x[2] = {0.f, 0.f}, S3y[2] = {0.f, 0.f},
+        S3z[2] = {0.f, 0.f}, M1[2] = {0.f, 0.f}, M2[2] = {0.f, 0.f};
   bool domain = false;
   for (int64_t i0 = i_lo; i0 < i_hi; i0 += kChebGA) {
     const int ga = (int)min((int64_t)kChebGA, i_hi - i0);
@@ -402,64 +428,92 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
 #pragma unroll 1
     for (int aa = 0; aa < ga; ++aa) {
       const AntD an = widen_ant<MONO>(as[aa]);
-      PairBwd g;
-      double L;
-      if (GEO == kModeBwd) {
-        pair_geometry<MONO, CORR>(rec, an, no_gain, g);
-        domain |= valid && !g.ok;
-        L = g.L;
-      } else {
-        L = pair_length<MONO>(rec, an);
-      }
-      float es, ec;                                 // E_c = e^{+j 2 pi f_c tau}
-      __sincosf(kTwoPi * frac_cycles(L * c.kc), &es, &ec);
-      float x = (float)((L - ls[aa]) * inv);
-      x = fminf(fmaxf(x, -1.f), 1.f);
-      const float xm1 = fabsf(x) - 1.f, twoxm1 = 2.f * xm1;
-      const float4 *B = bs[aa];
-      // even / odd partial sums in T_p(|x|); T_p(x) = (-1)^p T_p(|x|)
-      float4 b = B[0];
-      f2x he0 = pk(b.x, b.y), he1 = pk(b.z, b.w), ho0 = 0ull, ho1 = 0ull;
-      float t = 1.f, d = xm1;
-      t += d;                                       // T_1
-      b = B[1];
-      ho0 = ffma2(pk(t, t), pk(b.x, b.y), ho0);
-      if (NX == 2) ho1 = ffma2(pk(t, t), pk(b.z, b.w), ho1);
+      PairBwd g[2];
+      float ec[2], es[2], xv[2], sg[2];
 #pragma unroll
-      for (int p = 2; p < P; ++p) {
-        d = fmaf(twoxm1, t, d);
-        t += d;
-        b = B[p];
-        if (p & 1) {
-          ho0 = ffma2(pk(t, t), pk(b.x, b.y), ho0);
-          if (NX == 2) ho1 = ffma2(pk(t, t), pk(b.z, b.w), ho1);
+      for (int u = 0; u < 2; ++u) {
+        double L;
+        if (GEO == kModeBwd) {
+          pair_geometry<MONO, CORR>(rec[u], an, no_gain, g[u]);
+          domain |= valid[u] && !g[u].ok;
+          L = g[u].L;
         } else {
-          he0 = ffma2(pk(t, t), pk(b.x, b.y), he0);
-          if (NX == 2) he1 = ffma2(pk(t, t), pk(b.z, b.w), he1);
+          L = pair_length<MONO>(rec[u], an);
+        }
+        __sincosf(kTwoPi * frac_cycles(L * c.kc), &es[u], &ec[u]);   // E_c = e^{+j 2 pi f_c tau}
+        float x = (float)((L - ls[aa]) * inv);
+        x = fminf(fmaxf(x, -1.f), 1.f);
+        xv[u] = fabsf(x) - 1.f;
+        sg[u] = x < 0.f ? -1.f : 1.f;
+      }
+      const float4 *B = bs[aa];
+      // even / odd partial sums in T_p(|x|) per sample and X row; T_p(x) = (-1)^p T_p(|x|)
+      f2x he[2][2], ho[2][2];
+      float4 b = B[0];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        he[u][0] = pk(b.x, b.y); he[u][1] = pk(b.z, b.w);
+        ho[u][0] = 0ull; ho[u][1] = 0ull;
+      }
+      const f2x two_xm1 = pk(2.f * xv[0], 2.f * xv[1]);
+      f2x d = pk(xv[0], xv[1]);
+      f2x t = fadd2(pk(1.f, 1.f), d);                // (T_1, T_1')
+      b = B[1];
+      {
+        const float2 tv = upk(t);
+        ho[0][0] = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), ho[0][0]);
+        ho[1][0] = ffma2(pk(tv.y, tv.y), pk(b.x, b.y), ho[1][0]);
+        if (NX == 2) {
+          ho[0][1] = ffma2(pk(tv.x, tv.x), pk(b.z, b.w), ho[0][1]);
+          ho[1][1] = ffma2(pk(tv.y, tv.y), pk(b.z, b.w), ho[1][1]);
         }
       }
-      const float sg = x < 0.f ? -1.f : 1.f;
-      const float2 h0 = upk(ffma2(pk(sg, sg), ho0, he0));
-      if (MODE == kModeBwd) {
-        adj_accumulate<kModeBwd>(g, ec, es, h0.x, h0.y, S1, S2, S3x, S3y, S3z);
-      } else if (MODE == kModeFlt) {
-        adj_accumulate<kModeFlt>(g, ec, es, h0.x, h0.y, M1, M2, S3x, S3y, S3z);
-      } else {
-        const float2 h1 = upk(ffma2(pk(sg, sg), ho1, he1));
-        adj_accumulate<kModeBwd>(g, ec, es, h0.x, h0.y, S1, S2, S3x, S3y, S3z);
-        adj_accumulate<kModeFlt>(g, ec, es, h1.x, h1.y, M1, M2, S3x, S3y, S3z);
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d = ffma2(two_xm1, t, d);
+        t = fadd2(t, d);
+        b = B[p];
+        const float2 tv = upk(t);
+        f2x(&h)[2][2] = (p & 1) ? ho : he;
+        h[0][0] = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), h[0][0]);
+        h[1][0] = ffma2(pk(tv.y, tv.y), pk(b.x, b.y), h[1][0]);
+        if (NX == 2) {
+          h[0][1] = ffma2(pk(tv.x, tv.x), pk(b.z, b.w), h[0][1]);
+          h[1][1] = ffma2(pk(tv.y, tv.y), pk(b.z, b.w), h[1][1]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float2 h0 = upk(ffma2(pk(sg[u], sg[u]), ho[u][0], he[u][0]));
+        if (MODE == kModeBwd) {
+          adj_accumulate<kModeBwd>(g[u], ec[u], es[u], h0.x, h0.y, S1[u], S2[u], S3x[u], S3y[u],
+                                   S3z[u]);
+        } else if (MODE == kModeFlt) {
+          adj_accumulate<kModeFlt>(g[u], ec[u], es[u], h0.x, h0.y, M1[u], M2[u], S3x[u], S3y[u],
+                                   S3z[u]);
+        } else {
+          const float2 h1 = upk(ffma2(pk(sg[u], sg[u]), ho[u][1], he[u][1]));
+          adj_accumulate<kModeBwd>(g[u], ec[u], es[u], h0.x, h0.y, S1[u], S2[u], S3x[u], S3y[u],
+                                   S3z[u]);
+          adj_accumulate<kModeFlt>(g[u], ec[u], es[u], h1.x, h1.y, M1[u], M2[u], S3x[u], S3y[u],
+                                   S3z[u]);
+        }
       }
     }
   }
   if (domain) atomicOr(a.flags, 1u);
-  if (valid) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int64_t j = jb + u * kChebThreads;
+    if (!valid[u]) continue;
     if (MODE == kModeBwd) {
-      adj_store<kModeBwd>(a, j, S1, S2, S3x, S3y, S3z);
+      adj_store<kModeBwd>(a, j, S1[u], S2[u], S3x[u], S3y[u], S3z[u]);
     } else if (MODE == kModeFlt) {
-      adj_store<kModeFlt>(a, j, M1, M2, 0.f, 0.f, 0.f);
+      adj_store<kModeFlt>(a, j, M1[u], M2[u], 0.f, 0.f, 0.f);
     } else {
-      adj_store<kModeBwd>(a, j, S1, S2, S3x, S3y, S3z);
-      reinterpret_cast<float2 *>(a.out2)[(int64_t)blockIdx.y * a.n_s + j] = make_float2(M1, M2);
+      adj_store<kModeBwd>(a, j, S1[u], S2[u], S3x[u], S3y[u], S3z[u]);
+      reinterpret_cast<float2 *>(a.out2)[(int64_t)blockIdx.y * a.n_s + j] =
+          make_float2(M1[u], M2[u]);
     }
   }
 }
@@ -488,7 +542,7 @@ cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, i
                                                                 nx, bmom);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 g((unsigned)((a.n_s + kChebThreads - 1) / kChebThreads), (unsigned)n_splits);
+  dim3 g((unsigned)((a.n_s + 2 * kChebThreads - 1) / (2 * kChebThreads)), (unsigned)n_splits);
   if (mode == kModeBwd)
     e = mono ? (corr ? cheb_adj_all<kModeBwd, true, true>(c, a, bmom, g, st)
                      : cheb_adj_all<kModeBwd, true, false>(c, a, bmom, g, st))

@@ -14,14 +14,14 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 FULL="python tools/profile_step.py --config c3 --steps 1"
 timeout 600 $FULL > $OUT/full_plain.log 2>&1 && \
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-  -k regex:"k_trace_fwd|k_adjoint|k_blend" --csv --log-file $OUT/traffic.csv $FULL > $OUT/ncu_traffic.log 2>&1
+  -k regex:"${TRAFFIC_RX:-k_trace_fwd|k_adjoint|k_blend}" --csv --log-file $OUT/traffic.csv $FULL > $OUT/ncu_traffic.log 2>&1
 echo "traffic rc=$?" >> $OUT/ncu_traffic.log
 CMD="python tools/profile_step.py --config c3 --steps 2 --ants 2048"
 timeout 600 $CMD > $OUT/profile_plain.log 2>&1 || { echo "plain run failed" >> $OUT/profile_plain.log; exit 0; }
 i=0
-for e in k_trace_fwd:0 k_adjoint_tc:1; do
+for e in ${NCU_KERNELS:-k_trace_fwd:0 k_adjoint_tc:1}; do
   rx=${e%%:*}; sk=${e##*:}
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $sk -c 1 -o $OUT/prof$i $CMD > $OUT/ncu_full$i.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$rx" -s $sk -c 1 -o $OUT/prof$i $CMD > $OUT/ncu_full$i.log 2>&1
   echo "ncu $rx rc=$?" >> $OUT/ncu_full$i.log
   i=$((i+1))
 done
