@@ -21,6 +21,7 @@ namespace {
 constexpr double kC = 299792458.0;
 constexpr size_t kHdr = 256;                   // workspace header: flags word at offset 0
 constexpr size_t kChebHdrOff = 64;             // ChebHdr of the Chebyshev-moment forward
+constexpr size_t kActiveOff = 128;             // int64 count of the compacted active records
 constexpr int kTmpN = 512;                     // reduction scratch (floats)
 constexpr size_t kSplitCap = size_t(2) << 30;  // cap on each split-partial region (bytes)
 
@@ -136,7 +137,7 @@ bool cheb_enabled() {
 struct Layout {
   size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
          off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, off_cbox = 0, off_clc = 0,
-         off_ccoef = 0, off_cpart = 0, off_cbadj = 0, total = 0;
+         off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, total = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
@@ -175,6 +176,8 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   L.off_ccoef = take((size_t)nf * kChebPMax * 8);
   L.off_cpart = take(L.cap_cpart);
   L.off_cbadj = take((size_t)std::max<int64_t>(n_a, 1) * kChebPMax * 2 * 8);
+  L.off_recc = take((size_t)n_s * sizeof(Rec));             // compacted active records
+  L.off_ccnt = take((size_t)(compact_blocks(n_s) + 1) * 4);
   L.total = o;
   return true;
 }
@@ -270,7 +273,8 @@ ChebArgs make_cheb(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
 
 rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
                    const rfr_freq_grid *grid, bool no_gain, bool corr, int kind, float *out,
-                   const rfr_workspace *ws, const Layout &L, cudaStream_t st) {
+                   const rfr_workspace *ws, const Layout &L, cudaStream_t st,
+                   const Rec *rec_c = nullptr, const int64_t *n_dev = nullptr) {
   FwdGeom g;
   if (!fwd_geom(grid->n_freq, g)) return RFR_E_SHAPE;
   const Split sp = fwd_split(n_pts, ants->n_ant, grid->n_freq, g, L.cap_fwdp);
@@ -299,7 +303,8 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   const Split cs = cheb_split(n_pts, ants->n_ant);
   const bool cheb = ants->n_ant > 0 && n_pts > 0 &&
                     (size_t)cs.splits * ants->n_ant * kChebPMax * 8 <= L.cap_cpart;
-  const ChebArgs c = make_cheb(rec, n_pts, ants, grid, no_gain, ws, L, cs.per_split);
+  ChebArgs c = make_cheb(rec_c ? rec_c : rec, n_pts, ants, grid, no_gain, ws, L, cs.per_split);
+  c.n_dev = rec_c ? n_dev : nullptr;
   if (cheb) {
     RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
     a.skip = hdr;
@@ -408,8 +413,14 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (ants->n_ant == 0) return RFR_OK;
   RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
-  return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, (flags & RFR_NO_GAIN) != 0,
-                 has_corr(samples, ants), kFwdTrace, signal, ws, L, st);
+  // empty-space skipping for the Chebyshev path: the records with a non-zero amplitude, compacted
+  const bool corr = has_corr(samples, ants);
+  Rec *rec_c = at<Rec>(ws, L.off_recc);
+  int64_t *n_act = at<int64_t>(ws, kActiveOff);
+  RFR_CU(launch_compact(at<Rec>(ws, L.off_rec), n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c,
+                        st));
+  return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, (flags & RFR_NO_GAIN) != 0, corr,
+                 kFwdTrace, signal, ws, L, st, rec_c, n_act);
 }
 
 rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex, float *grad_signal,

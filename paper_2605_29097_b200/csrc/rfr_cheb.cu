@@ -37,6 +37,84 @@ constexpr int kChebThreads = 128;
 constexpr int kChebTJ = 32;                       // records per shared-memory tile
 }  // namespace
 
+// ---------------------------------------------------------- empty-space skipping (forward)
+// A sample contributes A_ij = w_j g gamma T_t T_r to the forward: nothing when w_j = p a alpha is
+// exactly 0 (alpha underflows to 0 in fp32 a few millimetres from any surface at s = 2e4 / m) or,
+// without the Eq. 7 correction, when T_j is exactly 0 (behind a surface).  The forward's Chebyshev
+// path runs over the compacted list of the other records (order preserved: an ordered stream
+// compaction, deterministic); the count stays on the device.
+constexpr int kCompactBlock = 1024;
+
+__device__ __forceinline__ bool rec_active(const Rec &r, bool corr) {
+  return r.w != 0.f && (corr || r.T != 0.f);
+}
+
+__global__ void __launch_bounds__(kCompactBlock) k_compact_count(const Rec *__restrict__ rec,
+                                                                 int64_t n, bool corr,
+                                                                 int *__restrict__ cnt) {
+  const int64_t j = (int64_t)blockIdx.x * kCompactBlock + threadIdx.x;
+  const bool act = j < n && rec_active(rec[j], corr);
+  const int c = __syncthreads_count(act);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = c;
+}
+
+// exclusive scan of the block counts (one CTA, sequential over chunks of 1024) and the total
+__global__ void __launch_bounds__(1024) k_compact_scan(int *__restrict__ cnt, int nb,
+                                                       int64_t *__restrict__ total) {
+  __shared__ int sh[1024];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nb; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    const int v = b < nb ? cnt[b] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {            // Hillis-Steele inclusive scan
+      const int u = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += u;
+      __syncthreads();
+    }
+    if (b < nb) cnt[b] = (int)(carry + sh[threadIdx.x] - v);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += sh[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(kCompactBlock) k_compact_write(const Rec *__restrict__ rec,
+                                                                 int64_t n, bool corr,
+                                                                 const int *__restrict__ off,
+                                                                 Rec *__restrict__ out) {
+  __shared__ int wsum[kCompactBlock / 32];
+  const int64_t j = (int64_t)blockIdx.x * kCompactBlock + threadIdx.x;
+  Rec r;
+  bool act = false;
+  if (j < n) { r = rec[j]; act = rec_active(r, corr); }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, act);
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  int base = off[blockIdx.x];
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  if (act) out[base + __popc(bal & ((1u << lane) - 1u))] = r;
+}
+
+cudaError_t launch_compact(const Rec *rec, int64_t n, bool corr, int *cnt, int64_t *total, Rec *out,
+                           cudaStream_t st) {
+  const int nb = (int)((n + kCompactBlock - 1) / kCompactBlock);
+  if (nb == 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), st);
+  k_compact_count<<<nb, kCompactBlock, 0, st>>>(rec, n, corr, cnt);
+  k_compact_scan<<<1, 1024, 0, st>>>(cnt, nb, total);
+  k_compact_write<<<nb, kCompactBlock, 0, st>>>(rec, n, corr, cnt, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(3);
+  return e;
+}
+int compact_blocks(int64_t n) { return (int)((n + kCompactBlock - 1) / kCompactBlock); }
+
 // query points as records (fp64 position; only the box kernel reads them)
 __global__ void k_pack_points(const float *__restrict__ x, const float *__restrict__ y,
                               const float *__restrict__ z, int64_t n, Rec *__restrict__ out) {
@@ -60,7 +138,9 @@ cudaError_t launch_pack_points(const float *x, const float *y, const float *z, i
 }
 
 // ------------------------------------------------------------------ bounding box of the samples
-__global__ void k_cheb_box(const Rec *__restrict__ rec, int64_t n, double *__restrict__ part) {
+__global__ void k_cheb_box(const Rec *__restrict__ rec, int64_t n, const int64_t *n_dev,
+                           double *__restrict__ part) {
+  if (n_dev) n = *n_dev;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -114,6 +194,10 @@ __global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ 
       v = threadIdx.x < 3 ? fmin(v, u) : fmax(v, u);
     }
     box[threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && !(box[0] <= box[3])) {   // no points (empty compacted list): any box
+    for (int c = 0; c < 6; ++c) box[c] = 0.0;       // gives zero moments; keep the centres finite
   }
   __syncthreads();
   double dmax_half = 0.0;
@@ -204,8 +288,11 @@ __global__ void __launch_bounds__(kChebThreads, P <= 32 ? 4 : 3) k_cheb_fwd(Cheb
   const int tid = threadIdx.x;
   const int64_t ia = (int64_t)blockIdx.x * kChebThreads + tid;
   const bool ant_ok = ia < a.n_a;
-  const int64_t j_lo = (int64_t)blockIdx.y * a.samples_per_split;
-  const int64_t j_hi = min(a.n_s, j_lo + a.samples_per_split);
+  // point range of this split: from the device count when the records are a compacted list
+  const int64_t n_pts = a.n_dev ? *a.n_dev : a.n_s;
+  const int64_t per = a.n_dev ? (n_pts + gridDim.y - 1) / gridDim.y : a.samples_per_split;
+  const int64_t j_lo = (int64_t)blockIdx.y * per;
+  const int64_t j_hi = min(n_pts, j_lo + per);
   AntF af;
   if (ant_ok) af = load_antf<MONO>(a, ia);
   else { af.x = af.y = 0.f; af.z = 1.f; af.rx = af.ry = 0.f; af.rz = 1.f; af.ptx = af.prx = 1.f; }
@@ -578,7 +665,7 @@ int cheb_box_blocks() { return kBoxBlocks; }
 int cheb_threads() { return kChebThreads; }
 
 cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_t st) {
-  k_cheb_box<<<kBoxBlocks, 256, 0, st>>>(a.rec, a.n_s, box_part);
+  k_cheb_box<<<kBoxBlocks, 256, 0, st>>>(a.rec, a.n_s, a.n_dev, box_part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_cheb_setup<<<1, 1024, 0, st>>>(box_part, kBoxBlocks, a, a.lc, a.hdr);

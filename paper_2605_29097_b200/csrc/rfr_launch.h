@@ -42,7 +42,8 @@ struct BlendArgs {
 
 struct ChebArgs {
   const Rec *rec;
-  int64_t n_s;
+  int64_t n_s;                     // points at rec (upper bound when n_dev is set)
+  const int64_t *n_dev;            // device count of a compacted list, or NULL
   const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
   int64_t n_a;
   int n_f;
@@ -153,6 +154,9 @@ cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, i
                               cudaStream_t st, const ChebHdr *skip = nullptr);
 constexpr int kChebPMax = 48;
 int cheb_box_blocks();
+cudaError_t launch_compact(const Rec *rec, int64_t n, bool corr, int *cnt, int64_t *total, Rec *out,
+                           cudaStream_t st);
+int compact_blocks(int64_t n);
 cudaError_t launch_pack_points(const float *x, const float *y, const float *z, int64_t n, Rec *out,
                                int n_sm, cudaStream_t st);
 int cheb_threads();
