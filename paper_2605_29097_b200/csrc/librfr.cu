@@ -22,6 +22,7 @@ constexpr double kC = 299792458.0;
 constexpr size_t kHdr = 256;                   // workspace header: flags word at offset 0
 constexpr size_t kChebHdrOff = 64;             // ChebHdr of the Chebyshev-moment forward
 constexpr size_t kActiveOff = 128;             // int64 count of the compacted active records
+constexpr size_t kActiveBwdOff = 136;          // int64 count of the backward's active samples
 constexpr int kTmpN = 512;                     // reduction scratch (floats)
 constexpr size_t kSplitCap = size_t(2) << 30;  // cap on each split-partial region (bytes)
 
@@ -137,7 +138,8 @@ bool cheb_enabled() {
 struct Layout {
   size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
          off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, off_cbox = 0, off_clc = 0,
-         off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, total = 0;
+         off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, off_aflag = 0,
+         off_idxc = 0, total = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
@@ -178,6 +180,8 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   L.off_cbadj = take((size_t)std::max<int64_t>(n_a, 1) * kChebPMax * 2 * 8);
   L.off_recc = take((size_t)n_s * sizeof(Rec));             // compacted active records
   L.off_ccnt = take((size_t)(compact_blocks(n_s) + 1) * 4);
+  L.off_aflag = take((size_t)n_s);                           // K1: alpha != 0 per sample
+  L.off_idxc = take((size_t)n_s * 4);                        // compacted list: original index
   L.total = o;
   return true;
 }
@@ -234,6 +238,7 @@ rfr_status run_blend(const rfr_samples *s, float sharpness, uint32_t flags,
   b.nx = s->nx; b.ny = s->ny; b.nz = s->nz; b.power = s->power; b.phi_origin = s->phi_origin;
   b.n_rays = s->n_rays; b.n_per_ray = s->n_per_ray; b.s = sharpness;
   b.rec = at<Rec>(ws, L.off_rec);
+  b.aflag = at<unsigned char>(ws, L.off_aflag);
   b.flags = at<unsigned>(ws, 0);
   b.check_finite = (flags & RFR_CHECK_FINITE) != 0;
   return cuda_status(launch_blend(b, st));
@@ -547,16 +552,30 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   const bool mono = ants->rx_x == nullptr;
   // Chebyshev-moment adjoint (rfr_cheb.cu), chosen on the device; the direct kernels return at
   // once when it runs
-  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0);
+  // Chebyshev adjoint over the samples with alpha != 0 only (DESIGN 5c): the others' partials are
+  // zero (their gradients vanish or carry sigma(-s f) factors below the fp32 range)
+  const bool corr = has_corr(samples, ants);
   const bool cheb = ants->n_ant > 0;
+  Rec *rec_c = at<Rec>(ws, L.off_recc);
+  int *idx_c = at<int>(ws, L.off_idxc);
+  int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
+  ChebArgs c = make_cheb(rec_c, n_s, ants, grid, a.no_gain, ws, L, 0);
+  c.n_dev = n_act;
+  c.idx = idx_c;
   if (cheb) {
+    RFR_CU(launch_compact(a.rec, n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c, st,
+                          at<unsigned char>(ws, L.off_aflag), idx_c));
     RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
     a.skip = c.hdr;
+    RFR_CU(cudaMemsetAsync(a.out, 0, (size_t)sp.splits * 5 * n_s * 4, st));
   }
-  RFR_CU(launch_adjoint(a, kModeBwd, mono, has_corr(samples, ants), sp.splits, st));
-  if (cheb)
-    RFR_CU(launch_cheb_adj(c, a, at<float2>(ws, L.off_cbadj), kModeBwd, mono,
-                           has_corr(samples, ants), sp.splits, st));
+  RFR_CU(launch_adjoint(a, kModeBwd, mono, corr, sp.splits, st));
+  if (cheb) {
+    AdjArgs ab = a;
+    ab.rec = rec_c;
+    RFR_CU(launch_cheb_adj(c, ab, at<float2>(ws, L.off_cbadj), kModeBwd, mono, corr, sp.splits,
+                           st));
+  }
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
                              device_sms(), st));
@@ -652,16 +671,40 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = (flags & RFR_NO_GAIN) != 0;
   const bool mono = ants->rx_x == nullptr;
-  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0);
+  // Chebyshev path: the filter over every sample (row 1 of B = the signal), the backward over the
+  // samples with alpha != 0 only (row 0 = G, compacted list, DESIGN 5c)
+  const bool corr = has_corr(samples, ants);
   const bool cheb = ants->n_ant > 0;
+  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0);
   if (cheb) {
     RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
     a.skip = c.hdr;
+    // the compacted backward leaves the inactive samples' partials at zero (the direct sweep, if
+    // the device chooses it, overwrites every entry)
+    RFR_CU(cudaMemsetAsync(a.out, 0, (size_t)sp.splits * 5 * n_s * 4, st));
   }
-  RFR_CU(launch_adjoint(a, kModeBoth, mono, has_corr(samples, ants), sp.splits, st));
-  if (cheb)
-    RFR_CU(launch_cheb_adj(c, a, at<float2>(ws, L.off_cbadj), kModeBoth, mono,
-                           has_corr(samples, ants), sp.splits, st));
+  RFR_CU(launch_adjoint(a, kModeBoth, mono, corr, sp.splits, st));
+  if (cheb) {
+    float2 *bmom = at<float2>(ws, L.off_cbadj);
+    ChebArgs cf = c;
+    cf.row = 1;
+    AdjArgs af = a;
+    af.out = a.out2;
+    RFR_CU(launch_cheb_adj(cf, af, bmom, kModeFlt, mono, false, sp.splits, st, 2));
+    Rec *rec_c = at<Rec>(ws, L.off_recc);
+    int *idx_c = at<int>(ws, L.off_idxc);
+    int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
+    RFR_CU(launch_compact(a.rec, n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c, st,
+                          at<unsigned char>(ws, L.off_aflag), idx_c));
+    ChebArgs cb = c;
+    cb.rec = rec_c;
+    cb.n_dev = n_act;
+    cb.idx = idx_c;
+    cb.row = 0;
+    AdjArgs ab = a;
+    ab.rec = rec_c;
+    RFR_CU(launch_cheb_adj(cb, ab, bmom, kModeBwd, mono, corr, sp.splits, st, -1));
+  }
   if (sp.splits > 1) {
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
                              device_sms(), st));

@@ -45,15 +45,19 @@ constexpr int kChebTJ = 32;                       // records per shared-memory t
 // compaction, deterministic); the count stays on the device.
 constexpr int kCompactBlock = 1024;
 
-__device__ __forceinline__ bool rec_active(const Rec &r, bool corr) {
-  return r.w != 0.f && (corr || r.T != 0.f);
+// forward: w = p a alpha != 0; backward (aflag given): alpha != 0 -- every gradient of a sample
+// with alpha = 0 in fp32 is 0 or carries a factor sigma(-s f) below the fp32 range (DESIGN 5c)
+__device__ __forceinline__ bool rec_active(const Rec &r, bool corr, const unsigned char *aflag,
+                                           int64_t j) {
+  return (aflag ? aflag[j] != 0 : r.w != 0.f) && (corr || r.T != 0.f);
 }
 
 __global__ void __launch_bounds__(kCompactBlock) k_compact_count(const Rec *__restrict__ rec,
                                                                  int64_t n, bool corr,
+                                                                 const unsigned char *aflag,
                                                                  int *__restrict__ cnt) {
   const int64_t j = (int64_t)blockIdx.x * kCompactBlock + threadIdx.x;
-  const bool act = j < n && rec_active(rec[j], corr);
+  const bool act = j < n && rec_active(rec[j], corr, aflag, j);
   const int c = __syncthreads_count(act);
   if (threadIdx.x == 0) cnt[blockIdx.x] = c;
 }
@@ -86,29 +90,35 @@ __global__ void __launch_bounds__(1024) k_compact_scan(int *__restrict__ cnt, in
 
 __global__ void __launch_bounds__(kCompactBlock) k_compact_write(const Rec *__restrict__ rec,
                                                                  int64_t n, bool corr,
+                                                                 const unsigned char *aflag,
                                                                  const int *__restrict__ off,
-                                                                 Rec *__restrict__ out) {
+                                                                 Rec *__restrict__ out,
+                                                                 int *__restrict__ idx) {
   __shared__ int wsum[kCompactBlock / 32];
   const int64_t j = (int64_t)blockIdx.x * kCompactBlock + threadIdx.x;
   Rec r;
   bool act = false;
-  if (j < n) { r = rec[j]; act = rec_active(r, corr); }
+  if (j < n) { r = rec[j]; act = rec_active(r, corr, aflag, j); }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned bal = __ballot_sync(0xffffffffu, act);
   if (lane == 0) wsum[warp] = __popc(bal);
   __syncthreads();
   int base = off[blockIdx.x];
   for (int w = 0; w < warp; ++w) base += wsum[w];
-  if (act) out[base + __popc(bal & ((1u << lane) - 1u))] = r;
+  if (act) {
+    const int pos = base + __popc(bal & ((1u << lane) - 1u));
+    out[pos] = r;
+    if (idx) idx[pos] = (int)j;
+  }
 }
 
 cudaError_t launch_compact(const Rec *rec, int64_t n, bool corr, int *cnt, int64_t *total, Rec *out,
-                           cudaStream_t st) {
+                           cudaStream_t st, const unsigned char *aflag, int *idx) {
   const int nb = (int)((n + kCompactBlock - 1) / kCompactBlock);
   if (nb == 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), st);
-  k_compact_count<<<nb, kCompactBlock, 0, st>>>(rec, n, corr, cnt);
+  k_compact_count<<<nb, kCompactBlock, 0, st>>>(rec, n, corr, aflag, cnt);
   k_compact_scan<<<1, 1024, 0, st>>>(cnt, nb, total);
-  k_compact_write<<<nb, kCompactBlock, 0, st>>>(rec, n, corr, cnt, out);
+  k_compact_write<<<nb, kCompactBlock, 0, st>>>(rec, n, corr, aflag, cnt, out, idx);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(3);
   return e;
@@ -485,16 +495,21 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
   __shared__ AntF as[kChebGA];
   __shared__ double ls[kChebGA];
   const int tid = threadIdx.x;
+  // points: all n_s, or the compacted list of c.n_dev points (records at a.rec, original index
+  // c.idx[j] for the outputs)
+  const int64_t n_pts = c.n_dev ? *c.n_dev : a.n_s;
   const int64_t jb = (int64_t)blockIdx.x * (2 * kChebThreads) + tid;
+  if ((int64_t)blockIdx.x * (2 * kChebThreads) >= n_pts) return;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
   bool valid[2];
   Rec rec[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    valid[u] = jb + u * kChebThreads < a.n_s;
+    valid[u] = jb + u * kChebThreads < n_pts;
     rec[u] = load_point<GEO>(a, jb + u * kChebThreads, valid[u]);
   }
+  const bool row1 = NX == 1 && c.row == 1;
   const bool no_gain = a.no_gain;
   const double inv = c.hdr->inv;
   float S1[2] = {0.f, 0.f}, S2[2] = {0.f, 0.f}, S3x[2] = {0.f, 0.f}, S3y[2] = {0.f, 0.f},
@@ -537,6 +552,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
       // even / odd partial sums in T_p(|x|) per sample and X row; T_p(x) = (-1)^p T_p(|x|)
       f2x he[2][2], ho[2][2];
       float4 b = B[0];
+      if (row1) b = make_float4(b.z, b.w, b.x, b.y);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         he[u][0] = pk(b.x, b.y); he[u][1] = pk(b.z, b.w);
@@ -546,6 +562,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
       f2x d = pk(xv[0], xv[1]);
       f2x t = fadd2(pk(1.f, 1.f), d);                // (T_1, T_1')
       b = B[1];
+      if (row1) b = make_float4(b.z, b.w, b.x, b.y);
       {
         const float2 tv = upk(t);
         ho[0][0] = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), ho[0][0]);
@@ -560,6 +577,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
         d = ffma2(two_xm1, t, d);
         t = fadd2(t, d);
         b = B[p];
+        if (row1) b = make_float4(b.z, b.w, b.x, b.y);
         const float2 tv = upk(t);
         f2x(&h)[2][2] = (p & 1) ? ho : he;
         h[0][0] = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), h[0][0]);
@@ -591,8 +609,8 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
   if (domain) atomicOr(a.flags, 1u);
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const int64_t j = jb + u * kChebThreads;
     if (!valid[u]) continue;
+    const int64_t j = c.idx ? (int64_t)c.idx[jb + u * kChebThreads] : jb + u * kChebThreads;
     if (MODE == kModeBwd) {
       adj_store<kModeBwd>(a, j, S1[u], S2[u], S3x[u], S3y[u], S3z[u]);
     } else if (MODE == kModeFlt) {
@@ -615,20 +633,21 @@ static cudaError_t cheb_adj_all(const ChebArgs &c, const AdjArgs &a, const float
 }
 
 cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, int mode,
-                            bool mono, bool corr, int n_splits, cudaStream_t st) {
+                            bool mono, bool corr, int n_splits, cudaStream_t st, int prep_nx) {
   if (a.n_a <= 0 || a.n_s <= 0) return cudaSuccess;
-  const int nx = mode == kModeBoth ? 2 : 1;
+  const int nx = prep_nx > 0 ? prep_nx : (mode == kModeBoth ? 2 : 1);
   const size_t sm = ((size_t)c.n_f + 4 * 64) * sizeof(float2);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_cheb_adj_prep,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k_cheb_adj_prep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(c, a.X, mode == kModeBoth ? a.X2
-                                                                                         : a.X,
-                                                                nx, bmom);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (prep_nx >= 0) {                              // prep_nx < 0: B already prepared
+    k_cheb_adj_prep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(
+        c, a.X, (mode == kModeBoth || nx == 2) ? a.X2 : a.X, nx, bmom);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   dim3 g((unsigned)((a.n_s + 2 * kChebThreads - 1) / (2 * kChebThreads)), (unsigned)n_splits);
   if (mode == kModeBwd)
     e = mono ? (corr ? cheb_adj_all<kModeBwd, true, true>(c, a, bmom, g, st)

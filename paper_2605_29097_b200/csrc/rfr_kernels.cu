@@ -45,6 +45,7 @@ __global__ void k_blend(BlendArgs a) {
     Rec rec;
     rec.x = (double)x; rec.y = (double)y; rec.z = (double)z;
     rec.w = p * refl * alpha;
+    if (a.aflag) a.aflag[j] = alpha != 0.f ? 1 : 0;
     rec.T = T;
     rec.nx = nx; rec.ny = ny; rec.nz = nz_;
     rec.papr = papr;

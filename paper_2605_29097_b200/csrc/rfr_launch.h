@@ -36,6 +36,7 @@ struct BlendArgs {
   int n_per_ray;
   float s;
   Rec *rec;
+  unsigned char *aflag;            // [n_s] 1 where alpha != 0 (the backward's active samples), or NULL
   unsigned int *flags;
   bool check_finite;
 };
@@ -44,6 +45,8 @@ struct ChebArgs {
   const Rec *rec;
   int64_t n_s;                     // points at rec (upper bound when n_dev is set)
   const int64_t *n_dev;            // device count of a compacted list, or NULL
+  const int *idx;                  // adjoint over a compacted list: original index of each point
+  int row;                         // single-row adjoint: which B row (0 = G / signal, 1 = signal)
   const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z, *phi_tx, *phi_rx;
   int64_t n_a;
   int n_f;
@@ -155,7 +158,8 @@ cudaError_t launch_sum_splits(const float *part, int S, int64_t n, float *out, i
 constexpr int kChebPMax = 48;
 int cheb_box_blocks();
 cudaError_t launch_compact(const Rec *rec, int64_t n, bool corr, int *cnt, int64_t *total, Rec *out,
-                           cudaStream_t st);
+                           cudaStream_t st, const unsigned char *aflag = nullptr,
+                           int *idx = nullptr);
 int compact_blocks(int64_t n);
 cudaError_t launch_pack_points(const float *x, const float *y, const float *z, int64_t n, Rec *out,
                                int n_sm, cudaStream_t st);
@@ -164,8 +168,9 @@ cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_
 cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,
                             float2 *out, cudaStream_t st);
 // adjoint (K3 / fused K3+K4) by Chebyshev moments: B_i[p] per antenna, then per pair P steps
+// prep_nx: 0 = prepare B for the mode's rows, 2 = prepare both rows (X, X2), -1 = B is ready
 cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, int mode,
-                            bool mono, bool corr, int n_splits, cudaStream_t st);
+                            bool mono, bool corr, int n_splits, cudaStream_t st, int prep_nx = 0);
 cudaError_t launch_abs(const float *m, int64_t n, float *p, int n_sm, cudaStream_t st);
 cudaError_t launch_reduce_sum(const float *x, int64_t n, float *tmp, int tmp_n, float *out,
                               cudaStream_t st);
