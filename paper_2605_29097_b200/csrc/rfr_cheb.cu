@@ -10,8 +10,8 @@
 // so the N_f-bin sum of every pair collapses to P Chebyshev moments M_i[p] = sum_j c_ij T_p(x_ij),
 // and the bins come from one small dense complex product per antenna,
 //     s_i[m] = exp(-j 2 pi m' u_c,i) sum_p a[m][p] M_i[p],    a[m][p] = eps_p (-j)^p J_p(z_m').
-// The truncation after P terms is below 1e-9 of sum |c| for |z| <= z_P (P = 16 / 32 / 48 for
-// z <= 3.4 / 13.3 / 25.3); wider delay spreads fall back to the direct recurrence kernel (K2).
+// The truncation after P terms is below 1e-8 of sum |c| for |z| <= z_P (P = 16 / 24 / 28 / 32 / 48
+// for z <= 4.0 / 8.9 / 11.7 / 14.6 / 27.0); wider delay spreads fall back to the direct kernels.
 // Per pair: the fp64 geometry, one MUFU sincos and P steps of Reinsch's stabilised Chebyshev
 // recurrence (d_{p+1} = 2 (x - 1) T_p + d_p, T_{p+1} = T_p + d_{p+1}: absolute error O(p u) up to
 // |x| = 1, where the plain three-term recurrence grows like p^2 u) with one complex-real FFMA2 each:
@@ -230,11 +230,14 @@ __global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ 
     // spread in cycles per bin, with a small margin for the fp32 rounding of the positions
     const double delta = fmax(red[0] * a.kd * (1.0 + 1e-6), 1e-30);
     const double zmax = 2.0 * 3.14159265358979323846 * (double)(a.n_f / 2 + 1) * delta;
+    // truncation tail sum_{p>=P} eps_p |J_p(z)| < 1e-8 of sum |c| (tests/test_cheb_math.py)
     int P = 0;
     if (a.enable) {
-      if (zmax <= 3.4) P = 16;
-      else if (zmax <= 13.3) P = 32;
-      else if (zmax <= 25.3) P = 48;
+      if (zmax <= 4.0) P = 16;
+      else if (zmax <= 8.9) P = 24;
+      else if (zmax <= 11.7) P = 28;
+      else if (zmax <= 14.6) P = 32;
+      else if (zmax <= 27.0) P = 48;
     }
     hdr->sel = P > 0 ? 1u : 0u;
     hdr->P = P;
@@ -549,10 +552,16 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
         sg[u] = x < 0.f ? -1.f : 1.f;
       }
       const float4 *B = bs[aa];
+      // single-row modes read only their row of (B_0[p], B_1[p]): one 8-byte load per moment
+      const float2 *B1 = reinterpret_cast<const float2 *>(B) + (row1 ? 1 : 0);
+      auto ldb = [&](int p) -> float4 {
+        if (NX == 2) return B[p];
+        const float2 v = B1[2 * p];
+        return make_float4(v.x, v.y, 0.f, 0.f);
+      };
       // even / odd partial sums in T_p(|x|) per sample and X row; T_p(x) = (-1)^p T_p(|x|)
       f2x he[2][2], ho[2][2];
-      float4 b = B[0];
-      if (row1) b = make_float4(b.z, b.w, b.x, b.y);
+      float4 b = ldb(0);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         he[u][0] = pk(b.x, b.y); he[u][1] = pk(b.z, b.w);
@@ -561,8 +570,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
       const f2x two_xm1 = pk(2.f * xv[0], 2.f * xv[1]);
       f2x d = pk(xv[0], xv[1]);
       f2x t = fadd2(pk(1.f, 1.f), d);                // (T_1, T_1')
-      b = B[1];
-      if (row1) b = make_float4(b.z, b.w, b.x, b.y);
+      b = ldb(1);
       {
         const float2 tv = upk(t);
         ho[0][0] = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), ho[0][0]);
@@ -576,8 +584,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
       for (int p = 2; p < P; ++p) {
         d = ffma2(two_xm1, t, d);
         t = fadd2(t, d);
-        b = B[p];
-        if (row1) b = make_float4(b.z, b.w, b.x, b.y);
+        b = ldb(p);
         const float2 tv = upk(t);
         f2x(&h)[2][2] = (p & 1) ? ho : he;
         h[0][0] = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), h[0][0]);
@@ -627,6 +634,8 @@ template <int MODE, bool MONO, bool CORR>
 static cudaError_t cheb_adj_all(const ChebArgs &c, const AdjArgs &a, const float2 *bmom, dim3 g,
                                 cudaStream_t st) {
   k_cheb_adj<16, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  k_cheb_adj<24, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  k_cheb_adj<28, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
   k_cheb_adj<32, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
   k_cheb_adj<48, MODE, MONO, CORR><<<g, kChebThreads, 0, st>>>(c, a, bmom);
   return cudaGetLastError();
@@ -662,7 +671,7 @@ cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, i
   else
     e = mono ? cheb_adj_all<kModeFlt, true, false>(c, a, bmom, g, st)
              : cheb_adj_all<kModeFlt, false, false>(c, a, bmom, g, st);
-  if (e == cudaSuccess) add_launches(4);
+  if (e == cudaSuccess) add_launches(prep_nx >= 0 ? 6 : 5);
   return e;
 }
 
@@ -676,6 +685,8 @@ template <bool MONO, bool CORR, int KIND>
 static cudaError_t cheb_fwd_all(const ChebArgs &a, dim3 g, cudaStream_t st) {
   cudaError_t e;
   if ((e = cheb_fwd_t<16, MONO, CORR, KIND>(a, g, st)) != cudaSuccess) return e;
+  if ((e = cheb_fwd_t<24, MONO, CORR, KIND>(a, g, st)) != cudaSuccess) return e;
+  if ((e = cheb_fwd_t<28, MONO, CORR, KIND>(a, g, st)) != cudaSuccess) return e;
   if ((e = cheb_fwd_t<32, MONO, CORR, KIND>(a, g, st)) != cudaSuccess) return e;
   return cheb_fwd_t<48, MONO, CORR, KIND>(a, g, st);
 }
@@ -710,7 +721,7 @@ cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, i
              : cheb_fwd_all<false, false, kFwdTrace>(a, g, st);
   if (e != cudaSuccess) return e;
   k_cheb_out<<<(unsigned)a.n_a, 256, 0, st>>>(a, splits, out);
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(4);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(6);
   return e;
 }
 
