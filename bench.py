@@ -267,8 +267,12 @@ def run_gpu(args):
     s0 = B[0]
     rfr.rfr_forward(s0["S"], prob.sharpness, s0["A"], grid, s0["sig"], s0["ws"])
     cf = rfr.cheb_state(s0["ws"])
-    rfr.rfr_backward_partial(s0["G"], s0["S"], prob.sharpness, s0["A"], grid, s0["part"], s0["ws"],
-                             flags=rfr.RFR_REUSE_BLEND)
+    if fused:
+        rfr.rfr_backward_filter(s0["G"], s0["sig"], s0["S"], prob.sharpness, s0["A"], grid,
+                                s0["out"], s0["P"], s0["ws"], mf=s0["M"], flags=rfr.RFR_REUSE_BLEND)
+    else:
+        rfr.rfr_backward_partial(s0["G"], s0["S"], prob.sharpness, s0["A"], grid, s0["part"],
+                                 s0["ws"], flags=rfr.RFR_REUSE_BLEND)
     ca = rfr.cheb_state(s0["ws"])
     cheb_fwd_P = cf["P"] if cf["sel"] else 0
     cheb_adj_P = ca["P"] if ca["sel"] else 0
