@@ -10,8 +10,8 @@
 // so the N_f-bin sum of every pair collapses to P Chebyshev moments M_i[p] = sum_j c_ij T_p(x_ij),
 // and the bins come from one small dense complex product per antenna,
 //     s_i[m] = exp(-j 2 pi m' u_c,i) sum_p a[m][p] M_i[p],    a[m][p] = eps_p (-j)^p J_p(z_m').
-// The truncation after P terms is below 1e-8 of sum |c| for |z| <= z_P (P = 16 / 24 / 28 / 32 / 48
-// for z <= 4.0 / 8.9 / 11.7 / 14.6 / 27.0); wider delay spreads fall back to the direct kernels.
+// The truncation after P terms is below 1e-7 of sum |c| for |z| <= z_P (P = 16 / 24 / 28 / 32 / 48
+// for z <= 4.7 / 9.9 / 12.9 / 15.8 / 28.6); wider delay spreads fall back to the direct kernels.
 // Per pair: the fp64 geometry, one MUFU sincos and P steps of Reinsch's stabilised Chebyshev
 // recurrence (d_{p+1} = 2 (x - 1) T_p + d_p, T_{p+1} = T_p + d_{p+1}: absolute error O(p u) up to
 // |x| = 1, where the plain three-term recurrence grows like p^2 u) with one complex-real FFMA2 each:
@@ -230,14 +230,15 @@ __global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ 
     // spread in cycles per bin, with a small margin for the fp32 rounding of the positions
     const double delta = fmax(red[0] * a.kd * (1.0 + 1e-6), 1e-30);
     const double zmax = 2.0 * 3.14159265358979323846 * (double)(a.n_f / 2 + 1) * delta;
-    // truncation tail sum_{p>=P} eps_p |J_p(z)| < 1e-8 of sum |c| (tests/test_cheb_math.py)
+    // truncation tail sum_{p>=P} eps_p |J_p(z)| < 1e-7 of sum |c|, 10^3 below the 1e-4 signal
+    // tolerance (tests/test_cheb_math.py)
     int P = 0;
     if (a.enable) {
-      if (zmax <= 4.0) P = 16;
-      else if (zmax <= 8.9) P = 24;
-      else if (zmax <= 11.7) P = 28;
-      else if (zmax <= 14.6) P = 32;
-      else if (zmax <= 27.0) P = 48;
+      if (zmax <= 4.7) P = 16;
+      else if (zmax <= 9.9) P = 24;
+      else if (zmax <= 12.9) P = 28;
+      else if (zmax <= 15.8) P = 32;
+      else if (zmax <= 28.6) P = 48;
     }
     hdr->sel = P > 0 ? 1u : 0u;
     hdr->P = P;

@@ -6,7 +6,7 @@ import pytest
 from scipy.special import jv
 
 # device rule (k_cheb_setup): P moments for |z| <= Z_MAX[P]
-Z_MAX = {16: 4.0, 24: 8.9, 28: 11.7, 32: 14.6, 48: 27.0}
+Z_MAX = {16: 4.7, 24: 9.9, 28: 12.9, 32: 15.8, 48: 28.6}
 
 
 def tail(P, z):
@@ -15,10 +15,10 @@ def tail(P, z):
 
 @pytest.mark.parametrize("P", sorted(Z_MAX))
 def test_truncation_rule_bounds_the_tail(P):
-    """sum_{p>=P} eps_p |J_p(z)| < 1e-8 for every |z| up to the threshold: the error of the
-    truncated expansion relative to sum_j |c_j| (|T_p| <= 1), 10^4 below the 1e-4 tolerance."""
+    """sum_{p>=P} eps_p |J_p(z)| < 1e-7 for every |z| up to the threshold: the error of the
+    truncated expansion relative to sum_j |c_j| (|T_p| <= 1), 10^3 below the 1e-4 tolerance."""
     for z in np.linspace(0.0, Z_MAX[P], 60):
-        assert tail(P, z) < 1e-8, (P, z)
+        assert tail(P, z) < 1e-7, (P, z)
 
 
 @pytest.mark.parametrize("sign", [-1, 1])
@@ -33,7 +33,7 @@ def test_jacobi_anger_expansion_matches_exponential(sign):
         coef = np.array([(1 if p == 0 else 2) * (sign * 1j) ** p * jv(p, z) for p in range(P)])
         approx = coef @ T
         exact = np.exp(sign * 1j * z * x)
-        assert np.max(np.abs(approx - exact)) < 1e-9
+        assert np.max(np.abs(approx - exact)) < 1e-7
 
 
 def test_reinsch_recurrence_fp32_error_is_uniform_up_to_the_ends():
