@@ -480,8 +480,7 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   }
   RFR_CU(launch_adjoint(a, kModeFlt, mono, false, sp.splits, st));
   if (cheb)
-    RFR_CU(launch_cheb_adj(c, a, at<float2>(ws, L.off_cbadj), kModeFlt, mono, false, sp.splits,
-                           st));
+    RFR_CU(launch_cheb_flt(c, a, at<float2>(ws, L.off_cbadj), mono, sp.splits, st));
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, n_query * 2, M, device_sms(),
                              st));
@@ -690,7 +689,7 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     cf.row = 1;
     AdjArgs af = a;
     af.out = a.out2;
-    RFR_CU(launch_cheb_adj(cf, af, bmom, kModeFlt, mono, false, sp.splits, st, 2));
+    RFR_CU(launch_cheb_flt(cf, af, bmom, mono, sp.splits, st, 2));
     Rec *rec_c = at<Rec>(ws, L.off_recc);
     int *idx_c = at<int>(ws, L.off_idxc);
     int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);

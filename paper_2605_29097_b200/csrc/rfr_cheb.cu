@@ -631,6 +631,141 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
   }
 }
 
+// Matched filter only (the fused sweep's pass over every sample, and rfr_filter): four query
+// points per thread -- two packed recurrence chains, and every B[p] load (8 bytes, this row
+// only) feeds four moment updates.  No amplitude factors (Eq. 3): the pair needs only its path
+// length.  Output: M partials [split][n_s] complex at a.out.
+template <int P, bool MONO>
+__global__ void __launch_bounds__(kChebThreads, 4) k_cheb_flt4(ChebArgs c, AdjArgs a,
+                                                               const float2 *__restrict__ bmom) {
+  if (c.hdr->P != P) return;
+  constexpr int SPT = 4;
+  __shared__ __align__(16) float2 bs[kChebGA][P];
+  __shared__ AntF as[kChebGA];
+  __shared__ double ls[kChebGA];
+  const int tid = threadIdx.x;
+  const int64_t jb = (int64_t)blockIdx.x * (SPT * kChebThreads) + tid;
+  if ((int64_t)blockIdx.x * (SPT * kChebThreads) >= a.n_s) return;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  Rec q[SPT];
+  bool valid[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    valid[u] = jb + u * kChebThreads < a.n_s;
+    q[u] = load_point<kModeFlt>(a, jb + u * kChebThreads, valid[u]);
+  }
+  const double inv = c.hdr->inv;
+  const int row = c.row;
+  float M1[SPT], M2[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) { M1[u] = 0.f; M2[u] = 0.f; }
+  float d0 = 0.f, d1 = 0.f, d2 = 0.f;               // unused S3 slots of adj_accumulate
+  for (int64_t i0 = i_lo; i0 < i_hi; i0 += kChebGA) {
+    const int ga = (int)min((int64_t)kChebGA, i_hi - i0);
+    __syncthreads();
+    for (int t = tid; t < ga * P; t += kChebThreads) {
+      const int aa = t / P, p = t % P;
+      bs[aa][p] = bmom[((i0 + aa) * kChebPMax + p) * 2 + row];
+    }
+    if (tid < ga) {
+      as[tid] = load_antf<MONO>(a, i0 + tid);
+      ls[tid] = c.lc[i0 + tid];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = widen_ant<MONO>(as[aa]);
+      float ec[SPT], es[SPT], xv[SPT], sg[SPT];
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        const double L = pair_length<MONO>(q[u], an);
+        __sincosf(kTwoPi * frac_cycles(L * c.kc), &es[u], &ec[u]);   // E_c = e^{+j 2 pi f_c tau}
+        float x = (float)((L - ls[aa]) * inv);
+        x = fminf(fmaxf(x, -1.f), 1.f);
+        xv[u] = fabsf(x) - 1.f;
+        sg[u] = x < 0.f ? -1.f : 1.f;
+      }
+      const float2 *B = bs[aa];
+      f2x he[SPT], ho[SPT];
+      const float2 b0 = B[0];
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) { he[u] = pk(b0.x, b0.y); ho[u] = 0ull; }
+      const f2x two01 = pk(2.f * xv[0], 2.f * xv[1]), two23 = pk(2.f * xv[2], 2.f * xv[3]);
+      f2x d01 = pk(xv[0], xv[1]), d23 = pk(xv[2], xv[3]);
+      f2x t01 = fadd2(pk(1.f, 1.f), d01), t23 = fadd2(pk(1.f, 1.f), d23);   // T_1
+      {
+        const float2 b = B[1];
+        const f2x pb = pk(b.x, b.y);
+        const float2 v01 = upk(t01), v23 = upk(t23);
+        ho[0] = ffma2(pk(v01.x, v01.x), pb, ho[0]);
+        ho[1] = ffma2(pk(v01.y, v01.y), pb, ho[1]);
+        ho[2] = ffma2(pk(v23.x, v23.x), pb, ho[2]);
+        ho[3] = ffma2(pk(v23.y, v23.y), pb, ho[3]);
+      }
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d01 = ffma2(two01, t01, d01);
+        d23 = ffma2(two23, t23, d23);
+        t01 = fadd2(t01, d01);
+        t23 = fadd2(t23, d23);
+        const float2 b = B[p];
+        const f2x pb = pk(b.x, b.y);
+        const float2 v01 = upk(t01), v23 = upk(t23);
+        f2x *h = (p & 1) ? ho : he;
+        h[0] = ffma2(pk(v01.x, v01.x), pb, h[0]);
+        h[1] = ffma2(pk(v01.y, v01.y), pb, h[1]);
+        h[2] = ffma2(pk(v23.x, v23.x), pb, h[2]);
+        h[3] = ffma2(pk(v23.y, v23.y), pb, h[3]);
+      }
+      PairBwd g;                                      // unused by the filter epilogue
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        const float2 hh = upk(ffma2(pk(sg[u], sg[u]), ho[u], he[u]));
+        adj_accumulate<kModeFlt>(g, ec[u], es[u], hh.x, hh.y, M1[u], M2[u], d0, d1, d2);
+      }
+    }
+  }
+  float2 *out = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
+#pragma unroll
+  for (int u = 0; u < SPT; ++u)
+    if (valid[u]) out[jb + u * kChebThreads] = make_float2(M1[u], M2[u]);
+}
+
+cudaError_t launch_cheb_flt(const ChebArgs &c, const AdjArgs &a, float2 *bmom, bool mono,
+                            int n_splits, cudaStream_t st, int prep_nx) {
+  if (a.n_a <= 0 || a.n_s <= 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (prep_nx >= 0) {
+    const int nx = prep_nx > 0 ? prep_nx : 1;
+    const size_t sm = ((size_t)c.n_f + 4 * 64) * sizeof(float2);
+    if (sm > 48 * 1024) {
+      e = cudaFuncSetAttribute(k_cheb_adj_prep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm);
+      if (e != cudaSuccess) return e;
+    }
+    k_cheb_adj_prep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(c, a.X, nx == 2 ? a.X2 : a.X,
+                                                                  nx, bmom);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  dim3 g((unsigned)((a.n_s + 4 * kChebThreads - 1) / (4 * kChebThreads)), (unsigned)n_splits);
+  if (mono) {
+    k_cheb_flt4<16, true><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<24, true><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<28, true><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<32, true><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<48, true><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  } else {
+    k_cheb_flt4<16, false><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<24, false><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<28, false><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<32, false><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+    k_cheb_flt4<48, false><<<g, kChebThreads, 0, st>>>(c, a, bmom);
+  }
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(prep_nx >= 0 ? 6 : 5);
+  return e;
+}
+
 template <int MODE, bool MONO, bool CORR>
 static cudaError_t cheb_adj_all(const ChebArgs &c, const AdjArgs &a, const float2 *bmom, dim3 g,
                                 cudaStream_t st) {

@@ -168,6 +168,9 @@ cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_
 cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,
                             float2 *out, cudaStream_t st);
 // adjoint (K3 / fused K3+K4) by Chebyshev moments: B_i[p] per antenna, then per pair P steps
+// matched filter only, four points per thread (row c.row of B); prep_nx as launch_cheb_adj
+cudaError_t launch_cheb_flt(const ChebArgs &c, const AdjArgs &a, float2 *bmom, bool mono,
+                            int n_splits, cudaStream_t st, int prep_nx = 0);
 // prep_nx: 0 = prepare B for the mode's rows, 2 = prepare both rows (X, X2), -1 = B is ready
 cudaError_t launch_cheb_adj(const ChebArgs &c, const AdjArgs &a, float2 *bmom, int mode,
                             bool mono, bool corr, int n_splits, cudaStream_t st, int prep_nx = 0);
