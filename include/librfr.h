@@ -58,6 +58,8 @@ typedef struct rfr_comm rfr_comm;
 /* option flags (rfr_opts.flags) */
 #define RFR_NO_GAIN 1u       /* drop the directive gain (w_o . w_r): the E11 ablation   */
 #define RFR_CHECK_FINITE 2u  /* K1 checks every sample field for NaN/Inf and raises RFR_FLAG_NUMERIC */
+#define RFR_DIRECT 8u        /* run the direct kernels (K2 recurrence / tensor-core adjoint) instead
+                                of the Chebyshev-moment path (DESIGN 5b); for A/B comparisons      */
 #define RFR_REUSE_BLEND 4u   /* workspace already holds K1's records for THIS sample set and s
                                 (set by the caller after rfr_forward on the same inputs); skips K1 */
 
@@ -101,7 +103,7 @@ typedef struct {
 } rfr_sample_grads;
 
 typedef struct {
-  uint32_t flags; /* RFR_NO_GAIN | RFR_CHECK_FINITE | RFR_REUSE_BLEND */
+  uint32_t flags; /* RFR_NO_GAIN | RFR_CHECK_FINITE | RFR_REUSE_BLEND | RFR_DIRECT */
 } rfr_opts;
 
 /* Caller-owned scratch memory of the library.  `ptr` is DEVICE memory of `bytes` >=

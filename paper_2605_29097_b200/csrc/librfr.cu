@@ -252,7 +252,7 @@ bool has_corr(const rfr_samples *s, const rfr_antennas *a) {
 // Chebyshev-moment arguments for a call over `rec` (n_pts points) and this antenna set
 ChebArgs make_cheb(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
                    const rfr_freq_grid *grid, bool no_gain, const rfr_workspace *ws,
-                   const Layout &L, int64_t per_split) {
+                   const Layout &L, int64_t per_split, bool direct = false) {
   ChebArgs c;
   memset(&c, 0, sizeof(c));
   c.rec = rec;
@@ -272,14 +272,15 @@ ChebArgs make_cheb(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   c.part = at<float2>(ws, L.off_cpart);
   c.flags = at<unsigned>(ws, 0);
   c.no_gain = no_gain;
-  c.enable = cheb_enabled();
+  c.enable = cheb_enabled() && !direct;
   return c;
 }
 
 rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
                    const rfr_freq_grid *grid, bool no_gain, bool corr, int kind, float *out,
                    const rfr_workspace *ws, const Layout &L, cudaStream_t st,
-                   const Rec *rec_c = nullptr, const int64_t *n_dev = nullptr) {
+                   const Rec *rec_c = nullptr, const int64_t *n_dev = nullptr,
+                   bool direct = false) {
   FwdGeom g;
   if (!fwd_geom(grid->n_freq, g)) return RFR_E_SHAPE;
   const Split sp = fwd_split(n_pts, ants->n_ant, grid->n_freq, g, L.cap_fwdp);
@@ -308,7 +309,8 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   const Split cs = cheb_split(n_pts, ants->n_ant);
   const bool cheb = ants->n_ant > 0 && n_pts > 0 &&
                     (size_t)cs.splits * ants->n_ant * kChebPMax * 8 <= L.cap_cpart;
-  ChebArgs c = make_cheb(rec_c ? rec_c : rec, n_pts, ants, grid, no_gain, ws, L, cs.per_split);
+  ChebArgs c = make_cheb(rec_c ? rec_c : rec, n_pts, ants, grid, no_gain, ws, L, cs.per_split,
+                         direct);
   c.n_dev = rec_c ? n_dev : nullptr;
   if (cheb) {
     RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
@@ -425,7 +427,7 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
   RFR_CU(launch_compact(at<Rec>(ws, L.off_rec), n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c,
                         st));
   return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, (flags & RFR_NO_GAIN) != 0, corr,
-                 kFwdTrace, signal, ws, L, st, rec_c, n_act);
+                 kFwdTrace, signal, ws, L, st, rec_c, n_act, (flags & RFR_DIRECT) != 0);
 }
 
 rfr_status rfr_loss(const float *signal, const float *target, int64_t n_complex, float *grad_signal,
@@ -558,7 +560,7 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   Rec *rec_c = at<Rec>(ws, L.off_recc);
   int *idx_c = at<int>(ws, L.off_idxc);
   int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
-  ChebArgs c = make_cheb(rec_c, n_s, ants, grid, a.no_gain, ws, L, 0);
+  ChebArgs c = make_cheb(rec_c, n_s, ants, grid, a.no_gain, ws, L, 0, (flags & RFR_DIRECT) != 0);
   c.n_dev = n_act;
   c.idx = idx_c;
   if (cheb) {
@@ -674,7 +676,8 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
   // samples with alpha != 0 only (row 0 = G, compacted list, DESIGN 5c)
   const bool corr = has_corr(samples, ants);
   const bool cheb = ants->n_ant > 0;
-  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0);
+  const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0,
+                               (flags & RFR_DIRECT) != 0);
   if (cheb) {
     RFR_CU(launch_cheb_prepare(c, at<double>(ws, L.off_cbox), st));
     a.skip = c.hdr;

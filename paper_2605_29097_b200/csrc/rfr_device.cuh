@@ -138,15 +138,26 @@ __device__ __forceinline__ double dist_from_sq(double d2, float *inv) {
   return fma(e, (double)(0.5f * r0), y);
 }
 
+// Same without the fp32 inverse: one fp32->fp64 conversion (the 1/2 r0 of the Newton step is an
+// fp64 multiply instead of a second conversion)
+__device__ __forceinline__ double dist_only(double d2) {
+  d2 = fmax(d2, 1e-24);
+  float r0;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"((float)d2));
+  const double h = (double)r0;
+  const double y = d2 * h;
+  const double e = fma(-y, y, d2);
+  return fma(e, 0.5 * h, y);
+}
+
 // Path length d_t + d_r in fp64 only (matched-filter adjoint: no amplitude factors, Eq. 3)
 template <bool MONO>
 __device__ __forceinline__ double pair_length(const Rec &r, const AntD &a) {
   double dx = r.x - a.x, dy = r.y - a.y, dz = r.z - a.z;
-  float it;
-  double dt = dist_from_sq(fma(dx, dx, fma(dy, dy, dz * dz)), &it);
+  double dt = dist_only(fma(dx, dx, fma(dy, dy, dz * dz)));
   if (MONO) return 2.0 * dt;
   double ex = a.rx - r.x, ey = a.ry - r.y, ez = a.rz - r.z;
-  return dt + dist_from_sq(fma(ex, ex, fma(ey, ey, ez * ez)), &it);
+  return dt + dist_only(fma(ex, ex, fma(ey, ey, ez * ez)));
 }
 
 // Shared geometry: distances in fp64 (phase precision), directions / gain / decay in fp32.

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "librfr.so")
 RFR_NO_GAIN = 1
 RFR_CHECK_FINITE = 2
 RFR_REUSE_BLEND = 4
+RFR_DIRECT = 8          # direct kernels instead of the Chebyshev-moment path (A/B)
 RFR_FLAG_DOMAIN = 1
 RFR_FLAG_NUMERIC = 2
 
