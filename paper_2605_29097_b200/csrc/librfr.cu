@@ -139,7 +139,8 @@ struct Layout {
   size_t off_rec = 0, off_ds = 0, off_tmp = 0, off_bwds = 0, off_fltm = 0, off_qrec = 0,
          off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, off_cbox = 0, off_clc = 0,
          off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, off_aflag = 0,
-         off_idxc = 0, total = 0;
+         off_idxc = 0, off_ttile = 0, off_tbcnt = 0, off_tstart = 0, off_tperm = 0, off_tqs = 0,
+         off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, total = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
@@ -173,7 +174,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   // Chebyshev-moment forward: box partials, per-antenna centres, coefficients, partial moments
   const Split cs = cheb_split(std::max(n_s, n_q), n_a);
   L.cap_cpart = (size_t)cs.splits * std::max<int64_t>(n_a, 1) * kChebPMax * 8;
-  L.off_cbox = take((size_t)cheb_box_blocks() * 6 * 8);
+  L.off_cbox = take((size_t)(cheb_box_blocks() + 1) * 6 * 8);   // block partials + the box
   L.off_clc = take((size_t)std::max<int64_t>(n_a, 1) * 8);
   L.off_ccoef = take((size_t)nf * kChebPMax * 8);
   L.off_cpart = take(L.cap_cpart);
@@ -182,6 +183,22 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
   L.off_ccnt = take((size_t)(compact_blocks(n_s) + 1) * 4);
   L.off_aflag = take((size_t)n_s);                           // K1: alpha != 0 per sample
   L.off_idxc = take((size_t)n_s * 4);                        // compacted list: original index
+  // tiled matched filter (DESIGN 5d): tile of each point, counts, starts, sorted points, tiles'
+  // boxes and per-(antenna, tile) centres, its own choice header, coefficients and moments
+  {
+    const int64_t np = std::max(n_s, n_q);
+    const int64_t na1 = std::max<int64_t>(n_a, 1);
+    L.off_ttile = take((size_t)np);
+    L.off_tbcnt = take((size_t)(tile_count_blocks(np) + 1) * kTiles * 4);
+    L.off_tstart = take((size_t)2 * (kTiles + 1) * 4);
+    L.off_tperm = take((size_t)np * 4);
+    L.off_tqs = take((size_t)np * 16);
+    L.off_tbox = take((size_t)kTiles * 6 * 8);
+    L.off_tlc = take((size_t)kTiles * na1 * 8);
+    L.off_thdr = take(64);
+    L.off_tcoef = take((size_t)nf * kChebPMax * 8);
+    L.off_tbmom = take((size_t)na1 * kTiles * kChebPMax * 8);
+  }
   L.total = o;
   return true;
 }
@@ -274,6 +291,50 @@ ChebArgs make_cheb(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   c.no_gain = no_gain;
   c.enable = cheb_enabled() && !direct;
   return c;
+}
+
+// tiled matched filter over n points at (qx, qy, qz) of the signal rows X into M partials `out`
+TileArgs make_tile(const float *qx, const float *qy, const float *qz, int64_t n,
+                   const rfr_antennas *ants, const rfr_freq_grid *grid, const ChebArgs &c,
+                   const float2 *X, float2 *out, int64_t ants_per_split, const rfr_workspace *ws,
+                   const Layout &L) {
+  TileArgs t;
+  memset(&t, 0, sizeof(t));
+  t.qx = qx; t.qy = qy; t.qz = qz;
+  t.n = n;
+  t.tx_x = ants->tx_x; t.tx_y = ants->tx_y; t.tx_z = ants->tx_z;
+  t.rx_x = ants->rx_x; t.rx_y = ants->rx_y; t.rx_z = ants->rx_z;
+  t.n_a = ants->n_ant;
+  t.n_f = grid->n_freq;
+  t.kd = c.kd;
+  t.kc = c.kc;
+  t.ghdr = c.hdr;
+  t.gbox = at<double>(ws, L.off_cbox) + (size_t)cheb_box_blocks() * 6;
+  t.tile = at<unsigned char>(ws, L.off_ttile);
+  t.bcnt = at<int>(ws, L.off_tbcnt);
+  t.tstart = at<int>(ws, L.off_tstart);
+  t.cstart = t.tstart + kTiles + 1;
+  t.perm = at<int>(ws, L.off_tperm);
+  t.qs = at<float4>(ws, L.off_tqs);
+  t.tbox = at<double>(ws, L.off_tbox);
+  t.lc = at<double>(ws, L.off_tlc);
+  t.hdr = at<ChebHdr>(ws, L.off_thdr);
+  t.dmax = reinterpret_cast<unsigned long long *>(at<char>(ws, L.off_thdr) + 32);
+  t.coef = at<float2>(ws, L.off_tcoef);
+  t.bmom = at<float2>(ws, L.off_tbmom);
+  t.X = X;
+  t.out = out;
+  t.ants_per_split = ants_per_split;
+  return t;
+}
+// the tiled filter is on unless RFR_TILE=0 (A/B)
+bool tile_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RFR_TILE");
+    v = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
 }
 
 rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
@@ -482,7 +543,14 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   }
   RFR_CU(launch_adjoint(a, kModeFlt, mono, false, sp.splits, st));
   if (cheb)
-    RFR_CU(launch_cheb_flt(c, a, at<float2>(ws, L.off_cbadj), mono, sp.splits, st));
+    if (tile_enabled()) {
+      const TileArgs ta = make_tile(qx, qy, qz, n_query, ants, grid, c,
+                                    reinterpret_cast<const float2 *>(signal),
+                                    reinterpret_cast<float2 *>(a.out), sp.per_split, ws, L);
+      RFR_CU(launch_tiled_filter(ta, mono, sp.splits, st));
+    } else {
+      RFR_CU(launch_cheb_flt(c, a, at<float2>(ws, L.off_cbadj), mono, sp.splits, st));
+    }
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, n_query * 2, M, device_sms(),
                              st));
@@ -692,7 +760,15 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     cf.row = 1;
     AdjArgs af = a;
     af.out = a.out2;
-    RFR_CU(launch_cheb_flt(cf, af, bmom, mono, sp.splits, st, 2));
+    if (tile_enabled()) {
+      // B of the backward rows (G) only; the filter prepares its own per-tile moments
+      RFR_CU(launch_cheb_adj_prep_only(c, a, bmom, st));
+      const TileArgs ta = make_tile(samples->x, samples->y, samples->z, n_s, ants, grid, c, a.X2,
+                                    reinterpret_cast<float2 *>(a.out2), sp.per_split, ws, L);
+      RFR_CU(launch_tiled_filter(ta, mono, sp.splits, st));
+    } else {
+      RFR_CU(launch_cheb_flt(cf, af, bmom, mono, sp.splits, st, 2));
+    }
     Rec *rec_c = at<Rec>(ws, L.off_recc);
     int *idx_c = at<int>(ws, L.off_idxc);
     int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);

@@ -189,10 +189,21 @@ __device__ __forceinline__ void box_dist(const double *b, double px, double py, 
   dmax = sqrt(s1);
 }
 
+// truncation tail sum_{p>=P} eps_p |J_p(z)| < 1e-7 of sum |c|, 10^3 below the 1e-4 signal
+// tolerance (tests/test_cheb_math.py); 0: spread too wide for the moment path
+__device__ __forceinline__ int cheb_select_P(double zmax) {
+  if (zmax <= 4.7) return 16;
+  if (zmax <= 9.9) return 24;
+  if (zmax <= 12.9) return 28;
+  if (zmax <= 15.8) return 32;
+  if (zmax <= 28.6) return 48;
+  return 0;
+}
+
 // ----------------------------------------------- per-antenna delay centre, global spread, P choice
 // One CTA of 1024 threads.  lc[i] = centre path length (m) of antenna i; hdr gets the selected P
 // (0: delay spread too wide -> direct kernel), delta and kd / delta.
-__global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ part, int nblk,
+__global__ void __launch_bounds__(1024) k_cheb_setup(double *__restrict__ part, int nblk,
                                                      ChebArgs a, double *__restrict__ lc,
                                                      ChebHdr *__restrict__ hdr) {
   __shared__ double box[6];
@@ -210,6 +221,7 @@ __global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ 
     for (int c = 0; c < 6; ++c) box[c] = 0.0;       // gives zero moments; keep the centres finite
   }
   __syncthreads();
+  if (threadIdx.x < 6) part[nblk * 6 + threadIdx.x] = box[threadIdx.x];   // the box, for later kernels
   double dmax_half = 0.0;
   for (int64_t i = threadIdx.x; i < a.n_a; i += blockDim.x) {
     double tmin, tmax, rmin, rmax;
@@ -230,16 +242,7 @@ __global__ void __launch_bounds__(1024) k_cheb_setup(const double *__restrict__ 
     // spread in cycles per bin, with a small margin for the fp32 rounding of the positions
     const double delta = fmax(red[0] * a.kd * (1.0 + 1e-6), 1e-30);
     const double zmax = 2.0 * 3.14159265358979323846 * (double)(a.n_f / 2 + 1) * delta;
-    // truncation tail sum_{p>=P} eps_p |J_p(z)| < 1e-7 of sum |c|, 10^3 below the 1e-4 signal
-    // tolerance (tests/test_cheb_math.py)
-    int P = 0;
-    if (a.enable) {
-      if (zmax <= 4.7) P = 16;
-      else if (zmax <= 9.9) P = 24;
-      else if (zmax <= 12.9) P = 28;
-      else if (zmax <= 15.8) P = 32;
-      else if (zmax <= 28.6) P = 48;
-    }
+    const int P = a.enable ? cheb_select_P(zmax) : 0;
     hdr->sel = P > 0 ? 1u : 0u;
     hdr->P = P;
     hdr->delta = delta;
@@ -730,6 +733,358 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_flt4(ChebArgs c, AdjAr
 #pragma unroll
   for (int u = 0; u < SPT; ++u)
     if (valid[u]) out[jb + u * kChebThreads] = make_float2(M1[u], M2[u]);
+}
+
+// =============================================================== tiled matched filter (5d)
+constexpr int kTileBlock = 1024;
+constexpr int kTileChunk = 4 * kChebThreads;       // points per filter CTA
+
+int tile_count_blocks(int64_t n) { return (int)((n + kTileBlock - 1) / kTileBlock); }
+
+__device__ __forceinline__ int tile_of(const double *b, float x, float y, float z) {
+  const float p[3] = {x, y, z};
+  int id = 0;
+  for (int c = 2; c >= 0; --c) {
+    const double w = b[3 + c] - b[c];
+    int k = w > 0.0 ? (int)((p[c] - b[c]) / w * kTileDim) : 0;
+    k = min(max(k, 0), kTileDim - 1);
+    id = id * kTileDim + k;
+  }
+  return id;
+}
+
+// per-warp counts of each tile by ballots -> smem [warps][kTiles]
+__device__ __forceinline__ void warp_tile_counts(int t, bool ok, int (*wc)[kTiles]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = 0; q < kTiles; ++q) {
+    const unsigned b = __ballot_sync(0xffffffffu, ok && t == q);
+    if (lane == 0) wc[warp][q] = __popc(b);
+  }
+}
+
+__global__ void __launch_bounds__(kTileBlock) k_tile_count(TileArgs a) {
+  if (a.ghdr->sel == 0) return;
+  __shared__ int wc[kTileBlock / 32][kTiles];
+  const int64_t j = (int64_t)blockIdx.x * kTileBlock + threadIdx.x;
+  const bool ok = j < a.n;
+  const int t = ok ? tile_of(a.gbox, a.qx[j], a.qy[j], a.qz[j]) : 0;
+  if (ok) a.tile[j] = (unsigned char)t;
+  warp_tile_counts(t, ok, wc);
+  __syncthreads();
+  if (threadIdx.x < kTiles) {
+    int c = 0;
+    for (int w = 0; w < kTileBlock / 32; ++w) c += wc[w][threadIdx.x];
+    a.bcnt[(int64_t)blockIdx.x * kTiles + threadIdx.x] = c;
+  }
+}
+
+// thread q: exclusive offsets of tile q over the blocks; then the tile and CTA starts
+__global__ void k_tile_scan(TileArgs a, int nb) {
+  if (a.ghdr->sel == 0) return;
+  __shared__ int tot[kTiles];
+  const int q = threadIdx.x;
+  int run = 0;
+  for (int b = 0; b < nb; ++b) {
+    const int c = a.bcnt[(int64_t)b * kTiles + q];
+    a.bcnt[(int64_t)b * kTiles + q] = run;
+    run += c;
+  }
+  tot[q] = run;
+  __syncthreads();
+  if (q == 0) {
+    int s = 0, cs = 0;
+    for (int k = 0; k < kTiles; ++k) {
+      a.tstart[k] = s;
+      a.cstart[k] = cs;
+      s += tot[k];
+      cs += (tot[k] + kTileChunk - 1) / kTileChunk;
+    }
+    a.tstart[kTiles] = s;
+    a.cstart[kTiles] = cs;
+  }
+}
+
+__global__ void __launch_bounds__(kTileBlock) k_tile_write(TileArgs a) {
+  if (a.ghdr->sel == 0) return;
+  __shared__ int wc[kTileBlock / 32][kTiles];
+  const int64_t j = (int64_t)blockIdx.x * kTileBlock + threadIdx.x;
+  const bool ok = j < a.n;
+  const int t = ok ? (int)a.tile[j] : 0;
+  warp_tile_counts(t, ok, wc);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned m = __match_any_sync(0xffffffffu, ok ? t : -1);
+  if (ok) {
+    int pos = a.tstart[t] + a.bcnt[(int64_t)blockIdx.x * kTiles + t];
+    for (int w = 0; w < warp; ++w) pos += wc[w][t];
+    pos += __popc(m & ((1u << lane) - 1u));
+    a.perm[pos] = (int)j;
+    a.qs[pos] = make_float4(a.qx[j], a.qy[j], a.qz[j], 0.f);
+  }
+}
+
+__global__ void k_tile_box(TileArgs a) {
+  if (a.ghdr->sel == 0) return;
+  const int t = blockIdx.x;
+  const int lo = a.tstart[t], hi = a.tstart[t + 1];
+  double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+  for (int k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    const float4 v = a.qs[k];
+    mn[0] = fmin(mn[0], (double)v.x); mx[0] = fmax(mx[0], (double)v.x);
+    mn[1] = fmin(mn[1], (double)v.y); mx[1] = fmax(mx[1], (double)v.y);
+    mn[2] = fmin(mn[2], (double)v.z); mx[2] = fmax(mx[2], (double)v.z);
+  }
+  __shared__ double sh[6][256];
+  for (int c = 0; c < 3; ++c) { sh[c][threadIdx.x] = mn[c]; sh[3 + c][threadIdx.x] = mx[c]; }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int c = 0; c < 3; ++c) {
+        sh[c][threadIdx.x] = fmin(sh[c][threadIdx.x], sh[c][threadIdx.x + s]);
+        sh[3 + c][threadIdx.x] = fmax(sh[3 + c][threadIdx.x], sh[3 + c][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) a.tbox[t * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// per (antenna, tile): centre path length; max half-spread over everything (fp64 bits, atomicMax:
+// order-independent)
+__global__ void k_tile_setup(TileArgs a) {
+  if (a.ghdr->sel == 0) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double dm = 0.0;
+  if (i < a.n_a) {
+    for (int t = 0; t < kTiles; ++t) {
+      const double *b = a.tbox + t * 6;
+      if (!(b[0] <= b[3])) { a.lc[(int64_t)t * a.n_a + i] = 0.0; continue; }   // empty tile
+      double tmin, tmax, rmin, rmax;
+      box_dist(b, a.tx_x[i], a.tx_y[i], a.tx_z[i], tmin, tmax);
+      if (a.rx_x) box_dist(b, a.rx_x[i], a.rx_y[i], a.rx_z[i], rmin, rmax);
+      else { rmin = tmin; rmax = tmax; }
+      a.lc[(int64_t)t * a.n_a + i] = 0.5 * (tmin + rmin + tmax + rmax);
+      dm = fmax(dm, 0.5 * (tmax + rmax - tmin - rmin));
+    }
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = dm;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(a.dmax, (unsigned long long)__double_as_longlong(red[0]));
+}
+
+__global__ void k_tile_select(TileArgs a) {
+  const double delta = fmax(__longlong_as_double((long long)*a.dmax) * a.kd * (1.0 + 1e-6), 1e-30);
+  const double zmax = 2.0 * 3.14159265358979323846 * (double)(a.n_f / 2 + 1) * delta;
+  const int P = a.ghdr->sel ? cheb_select_P(zmax) : 0;
+  a.hdr->sel = P > 0 ? 1u : 0u;
+  a.hdr->P = P;
+  a.hdr->delta = delta;
+  a.hdr->inv = a.kd / delta;
+}
+
+// B[i][t][p] = sum_m X_i[m] e^{+j 2 pi m' u_c,i,t} conj(a[m][p]); one CTA per antenna: per tile
+// the rotated row (one sincospi per bin) into shared memory, then fixed-order partial sums
+__global__ void __launch_bounds__(kAdjPrepThreads) k_tile_bprep(TileArgs a) {
+  if (a.hdr->sel == 0) return;
+  extern __shared__ float2 xs[];                    // [n_f] row, [n_f] rotated row, [4][64]
+  const int P = a.hdr->P;
+  const int64_t i = blockIdx.x;
+  const int N = a.n_f;
+  float2 *ys = xs + N, *part = xs + 2 * N;
+  for (int m = threadIdx.x; m < N; m += blockDim.x) xs[m] = a.X[i * N + m];
+  const int p = threadIdx.x & 63, q = threadIdx.x >> 6;
+  for (int t = 0; t < kTiles; ++t) {
+    if (a.tstart[t + 1] == a.tstart[t]) continue;   // empty tile: never read
+    const double uc = a.lc[(int64_t)t * a.n_a + i] * a.kd;
+    __syncthreads();
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+      float ps, pc;                                 // e^{+j 2 pi m' u_c}
+      sincospif(2.f * frac_cycles((double)(m - N / 2) * uc), &ps, &pc);
+      const float2 v = xs[m];
+      ys[m] = make_float2(fmaf(pc, v.x, -ps * v.y), fmaf(pc, v.y, ps * v.x));
+    }
+    __syncthreads();
+    float re = 0.f, im = 0.f;
+    if (p < P)
+      for (int m = q; m < N; m += 4) {
+        const float2 y = ys[m], c = a.coef[(int64_t)m * kChebPMax + p];   // y conj(c)
+        re = fmaf(y.x, c.x, fmaf(y.y, c.y, re));
+        im = fmaf(y.y, c.x, fmaf(-y.x, c.y, im));
+      }
+    part[q * 64 + p] = make_float2(re, im);
+    __syncthreads();
+    if (threadIdx.x < P) {
+      float2 v = part[threadIdx.x];
+      for (int qq = 1; qq < 4; ++qq) {
+        v.x += part[qq * 64 + threadIdx.x].x;
+        v.y += part[qq * 64 + threadIdx.x].y;
+      }
+      a.bmom[(i * kTiles + t) * kChebPMax + threadIdx.x] = v;
+    }
+  }
+}
+
+// the filter over the sorted points: CTA -> (tile, chunk of kTileChunk points), 4 per thread
+template <int P, bool MONO>
+__global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
+  if (a.hdr->P != P) return;
+  constexpr int SPT = 4;
+  const int blk = blockIdx.x;
+  if (blk >= a.cstart[kTiles]) return;
+  int t = 0;
+  while (a.cstart[t + 1] <= blk) ++t;               // the tile of this CTA (kTiles entries)
+  const int64_t base = a.tstart[t] + (int64_t)(blk - a.cstart[t]) * kTileChunk;
+  const int64_t end = a.tstart[t + 1];
+  __shared__ __align__(16) float2 bs[kChebGA][P];
+  __shared__ AntF as[kChebGA];
+  __shared__ double ls[kChebGA];
+  const int tid = threadIdx.x;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  Rec q[SPT];
+  bool valid[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    const int64_t k = base + tid + u * kChebThreads;
+    valid[u] = k < end;
+    const float4 v = valid[u] ? a.qs[k] : make_float4(0.f, 0.f, 1.f, 0.f);
+    q[u].x = v.x; q[u].y = v.y; q[u].z = v.z;
+    q[u].w = 0.f; q[u].T = 1.f; q[u].nx = q[u].ny = 0.f; q[u].nz = 1.f; q[u].papr = 1.f;
+  }
+  const double inv = a.hdr->inv;
+  float M1[SPT], M2[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) { M1[u] = 0.f; M2[u] = 0.f; }
+  float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+  for (int64_t i0 = i_lo; i0 < i_hi; i0 += kChebGA) {
+    const int ga = (int)min((int64_t)kChebGA, i_hi - i0);
+    __syncthreads();
+    for (int w = tid; w < ga * P; w += kChebThreads) {
+      const int aa = w / P, p = w % P;
+      bs[aa][p] = a.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+    }
+    if (tid < ga) {
+      AntF f;
+      const int64_t ia = i0 + tid;
+      f.x = a.tx_x[ia]; f.y = a.tx_y[ia]; f.z = a.tx_z[ia];
+      if (MONO) { f.rx = f.ry = f.rz = 0.f; }
+      else { f.rx = a.rx_x[ia]; f.ry = a.rx_y[ia]; f.rz = a.rx_z[ia]; }
+      f.ptx = f.prx = 1.f;
+      as[tid] = f;
+      ls[tid] = a.lc[(int64_t)t * a.n_a + ia];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = widen_ant<MONO>(as[aa]);
+      float ec[SPT], es[SPT], xv[SPT], sg[SPT];
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        const double L = pair_length<MONO>(q[u], an);
+        __sincosf(kTwoPi * frac_cycles(L * a.kc), &es[u], &ec[u]);
+        float x = (float)((L - ls[aa]) * inv);
+        x = fminf(fmaxf(x, -1.f), 1.f);
+        xv[u] = fabsf(x) - 1.f;
+        sg[u] = x < 0.f ? -1.f : 1.f;
+      }
+      const float2 *B = bs[aa];
+      f2x he[SPT], ho[SPT];
+      const float2 b0 = B[0];
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) { he[u] = pk(b0.x, b0.y); ho[u] = 0ull; }
+      const f2x two01 = pk(2.f * xv[0], 2.f * xv[1]), two23 = pk(2.f * xv[2], 2.f * xv[3]);
+      f2x d01 = pk(xv[0], xv[1]), d23 = pk(xv[2], xv[3]);
+      f2x t01 = fadd2(pk(1.f, 1.f), d01), t23 = fadd2(pk(1.f, 1.f), d23);
+      {
+        const float2 b = B[1];
+        const f2x pb = pk(b.x, b.y);
+        const float2 v01 = upk(t01), v23 = upk(t23);
+        ho[0] = ffma2(pk(v01.x, v01.x), pb, ho[0]);
+        ho[1] = ffma2(pk(v01.y, v01.y), pb, ho[1]);
+        ho[2] = ffma2(pk(v23.x, v23.x), pb, ho[2]);
+        ho[3] = ffma2(pk(v23.y, v23.y), pb, ho[3]);
+      }
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d01 = ffma2(two01, t01, d01);
+        d23 = ffma2(two23, t23, d23);
+        t01 = fadd2(t01, d01);
+        t23 = fadd2(t23, d23);
+        const float2 b = B[p];
+        const f2x pb = pk(b.x, b.y);
+        const float2 v01 = upk(t01), v23 = upk(t23);
+        f2x *h = (p & 1) ? ho : he;
+        h[0] = ffma2(pk(v01.x, v01.x), pb, h[0]);
+        h[1] = ffma2(pk(v01.y, v01.y), pb, h[1]);
+        h[2] = ffma2(pk(v23.x, v23.x), pb, h[2]);
+        h[3] = ffma2(pk(v23.y, v23.y), pb, h[3]);
+      }
+      PairBwd g;
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        const float2 hh = upk(ffma2(pk(sg[u], sg[u]), ho[u], he[u]));
+        adj_accumulate<kModeFlt>(g, ec[u], es[u], hh.x, hh.y, M1[u], M2[u], d0, d1, d2);
+      }
+    }
+  }
+  float2 *out = a.out + (int64_t)blockIdx.y * a.n;
+#pragma unroll
+  for (int u = 0; u < SPT; ++u)
+    if (valid[u]) out[a.perm[base + tid + u * kChebThreads]] = make_float2(M1[u], M2[u]);
+}
+
+template <bool MONO>
+static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
+  k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_flt4<24, MONO><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_flt4<28, MONO><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_flt4<32, MONO><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_flt4<48, MONO><<<g, kChebThreads, 0, st>>>(a);
+}
+
+cudaError_t launch_tiled_filter(const TileArgs &a, bool mono, int n_splits, cudaStream_t st) {
+  if (a.n_a <= 0 || a.n <= 0) return cudaSuccess;
+  const int nb = tile_count_blocks(a.n);
+  k_tile_count<<<nb, kTileBlock, 0, st>>>(a);
+  k_tile_scan<<<1, kTiles, 0, st>>>(a, nb);
+  k_tile_write<<<nb, kTileBlock, 0, st>>>(a);
+  k_tile_box<<<kTiles, 256, 0, st>>>(a);
+  cudaError_t e = cudaMemsetAsync(a.dmax, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  k_tile_setup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
+  k_tile_select<<<1, 1, 0, st>>>(a);
+  k_cheb_coef<<<(a.n_f + 127) / 128, 128, 0, st>>>(a.hdr, a.n_f, kChebPMax, a.coef);
+  const size_t sm = (2 * (size_t)a.n_f + 4 * 64) * sizeof(float2);
+  if (sm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_tile_bprep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  k_tile_bprep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(a);
+  dim3 g((unsigned)((a.n + kTileChunk - 1) / kTileChunk + kTiles), (unsigned)n_splits);
+  if (mono) tile_flt_all<true>(a, g, st);
+  else tile_flt_all<false>(a, g, st);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(14);
+  return e;
+}
+
+// B moments of row a.X only (row 0), for a later launch_cheb_adj(..., prep_nx = -1)
+cudaError_t launch_cheb_adj_prep_only(const ChebArgs &c, const AdjArgs &a, float2 *bmom,
+                                      cudaStream_t st) {
+  if (a.n_a <= 0) return cudaSuccess;
+  const size_t sm = ((size_t)c.n_f + 4 * 64) * sizeof(float2);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_cheb_adj_prep,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  k_cheb_adj_prep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(c, a.X, a.X, 1, bmom);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(1);
+  return e;
 }
 
 cudaError_t launch_cheb_flt(const ChebArgs &c, const AdjArgs &a, float2 *bmom, bool mono,

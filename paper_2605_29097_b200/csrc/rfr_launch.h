@@ -168,6 +168,40 @@ cudaError_t launch_cheb_prepare(const ChebArgs &a, double *box_part, cudaStream_
 cudaError_t launch_cheb_fwd(const ChebArgs &a, bool mono, bool corr, int kind, int splits,
                             float2 *out, cudaStream_t st);
 // adjoint (K3 / fused K3+K4) by Chebyshev moments: B_i[p] per antenna, then per pair P steps
+// Tiled matched filter (rfr_cheb.cu, DESIGN 5d): the query points are sorted into kTiles spatial
+// tiles of the points' bounding box; each (antenna, tile) gets its own delay centre, so the spread
+// -- and the number of Chebyshev moments -- shrinks with the tile.
+constexpr int kTileDim = 4;
+constexpr int kTiles = kTileDim * kTileDim * kTileDim;
+struct TileArgs {
+  const float *qx, *qy, *qz;
+  int64_t n;
+  const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z;
+  int64_t n_a;
+  int n_f;
+  double kd, kc;
+  const ChebHdr *ghdr;             // the call's global choice: sel == 0 -> the direct kernels run
+  const double *gbox;              // the points' bounding box [6] (k_cheb_setup)
+  unsigned char *tile;             // [n] tile of each point
+  int *bcnt;                       // [blocks][kTiles] counts -> block offsets
+  int *tstart;                     // [kTiles + 1] first sorted position of each tile
+  int *cstart;                     // [kTiles + 1] first CTA of each tile
+  int *perm;                       // [n] sorted position -> original index
+  float4 *qs;                      // [n] sorted positions
+  double *tbox;                    // [kTiles][6]
+  double *lc;                      // [kTiles][n_a] centre path lengths
+  ChebHdr *hdr;                    // the tiled choice (P, delta)
+  unsigned long long *dmax;        // max half-spread (fp64 bits)
+  float2 *coef;                    // [n_f][kChebPMax]
+  float2 *bmom;                    // [n_a][kTiles][kChebPMax]
+  const float2 *X;                 // the signal rows [n_a][n_f]
+  float2 *out;                     // M partials [split][n]
+  int64_t ants_per_split;
+};
+cudaError_t launch_tiled_filter(const TileArgs &t, bool mono, int n_splits, cudaStream_t st);
+cudaError_t launch_cheb_adj_prep_only(const ChebArgs &c, const AdjArgs &a, float2 *bmom,
+                                      cudaStream_t st);
+int tile_count_blocks(int64_t n);
 // matched filter only, four points per thread (row c.row of B); prep_nx as launch_cheb_adj
 cudaError_t launch_cheb_flt(const ChebArgs &c, const AdjArgs &a, float2 *bmom, bool mono,
                             int n_splits, cudaStream_t st, int prep_nx = 0);
