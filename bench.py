@@ -355,10 +355,11 @@ def run_gpu(args):
     if cheb_adj_P:
         # Chebyshev-moment adjoint: per pair P steps of 1 FFMA + 1 FADD + one FFMA2 per X row
         # (two in the fused sweep) = (2 + 2 nx) P FP32 lane-ops
-        # per pair 4 P lane-ops for the filter (every sample) and 4 P for the backward (the
-        # samples with alpha != 0, section 5c)
+        # per pair 4 P lane-ops: the filter over every sample (with the tiled filter's own P,
+        # section 5d) and the backward over the samples with alpha != 0 (section 5c)
+        p_flt = ca.get("P_tiled_filter") or cheb_adj_P
         ops = 4 * cheb_adj_P
-        work = n_pairs * ((1.0 + act_bwd) if fused else act_bwd)
+        work = n_pairs * ((p_flt / cheb_adj_P + act_bwd) if fused else act_bwd)
         for name, ms in ([("k_cheb_adj (filter + backward, rfr_backward_filter)", b_ms)]
                          if fused else [("k_cheb_adj (backward, rfr_backward)", b_ms)]):
             ach = ops * work / (per_step(ms) * 1e-3)
@@ -440,7 +441,8 @@ def run_gpu(args):
                         "loss_ms": per_step(l_ms)}),
             "method": {"forward": f"chebyshev-moments P={cheb_fwd_P} (delta={cf['delta']:.4g} cycles)"
                        if cheb_fwd_P else "direct recurrence (K2)",
-                       "adjoint": f"chebyshev-moments P={cheb_adj_P} (delta={ca['delta']:.4g} cycles)"
+                       "adjoint": (f"chebyshev-moments P={cheb_adj_P} (delta={ca['delta']:.4g} "
+                                   f"cycles); tiled filter P={ca.get('P_tiled_filter')}")
                        if cheb_adj_P else "tensor-core 16-bin block GEMM",
                        "empty_space_skipping": {
                            "forward_active_samples": act_fwd, "backward_active_samples": act_bwd,

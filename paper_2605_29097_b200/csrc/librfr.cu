@@ -23,6 +23,7 @@ constexpr size_t kHdr = 256;                   // workspace header: flags word a
 constexpr size_t kChebHdrOff = 64;             // ChebHdr of the Chebyshev-moment forward
 constexpr size_t kActiveOff = 128;             // int64 count of the compacted active records
 constexpr size_t kActiveBwdOff = 136;          // int64 count of the backward's active samples
+constexpr size_t kTilePOff = 144;              // int: moments of the last tiled filter
 constexpr int kTmpN = 512;                     // reduction scratch (floats)
 constexpr size_t kSplitCap = size_t(2) << 30;  // cap on each split-partial region (bytes)
 
@@ -325,6 +326,7 @@ TileArgs make_tile(const float *qx, const float *qy, const float *qz, int64_t n,
   t.X = X;
   t.out = out;
   t.ants_per_split = ants_per_split;
+  t.pub = at<int>(ws, kTilePOff);
   return t;
 }
 // the tiled filter is on unless RFR_TILE=0 (A/B)

@@ -884,6 +884,7 @@ __global__ void k_tile_select(TileArgs a) {
   a.hdr->P = P;
   a.hdr->delta = delta;
   a.hdr->inv = a.kd / delta;
+  if (a.pub) *a.pub = P;
 }
 
 // B[i][t][p] = sum_m X_i[m] e^{+j 2 pi m' u_c,i,t} conj(a[m][p]); one CTA per antenna: per tile

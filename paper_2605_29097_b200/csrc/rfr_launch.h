@@ -191,6 +191,7 @@ struct TileArgs {
   double *tbox;                    // [kTiles][6]
   double *lc;                      // [kTiles][n_a] centre path lengths
   ChebHdr *hdr;                    // the tiled choice (P, delta)
+  int *pub;                        // workspace header slot: the tiled P (diagnostics)
   unsigned long long *dmax;        // max half-spread (fp64 bits)
   float2 *coef;                    // [n_f][kChebPMax]
   float2 *bmom;                    // [n_a][kTiles][kChebPMax]

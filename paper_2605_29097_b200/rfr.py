@@ -242,10 +242,12 @@ def cheb_state(ws: Workspace) -> dict:
     read from the workspace header (librfr.cu kChebHdrOff): sel (0 = direct kernels), P, delta, and
     the empty-space-skipping counts of the last forward / backward (samples that carry work)."""
     import struct as _st
-    raw = bytes(ws.tensor[64:144].cpu().numpy().tobytes())
+    raw = bytes(ws.tensor[64:148].cpu().numpy().tobytes())
     sel, P, delta, inv = _st.unpack("<Iidd", raw[:24])
     n_fwd, n_bwd = _st.unpack("<qq", raw[64:80])      # compacted active counts (offsets 128, 136)
-    return {"sel": sel, "P": P, "delta": delta, "n_active_fwd": n_fwd, "n_active_bwd": n_bwd}
+    (p_tile,) = _st.unpack("<i", raw[80:84])           # moments of the last tiled filter (144)
+    return {"sel": sel, "P": P, "delta": delta, "n_active_fwd": n_fwd, "n_active_bwd": n_bwd,
+            "P_tiled_filter": p_tile}
 
 
 def workspace(n_samples: int, n_ant: int, n_freq: int, n_query: int = 0, device="cuda") -> Workspace:
