@@ -897,7 +897,9 @@ __global__ void __launch_bounds__(kAdjPrepThreads) k_tile_bprep(TileArgs a) {
   const int N = a.n_f;
   float2 *ys = xs + N, *part = xs + 2 * N;
   for (int m = threadIdx.x; m < N; m += blockDim.x) xs[m] = a.X[i * N + m];
-  const int p = threadIdx.x & 63, q = threadIdx.x >> 6;
+  // thread (p, q): moment p over the bins m = q, q + Q, ...; PP = P rounded up to a power of two
+  const int PP = P <= 16 ? 16 : (P <= 32 ? 32 : 64), Q = kAdjPrepThreads / PP;
+  const int p = threadIdx.x % PP, q = threadIdx.x / PP;
   for (int t = 0; t < kTiles; ++t) {
     if (a.tstart[t + 1] == a.tstart[t]) continue;   // empty tile: never read
     const double uc = a.lc[(int64_t)t * a.n_a + i] * a.kd;
@@ -911,18 +913,18 @@ __global__ void __launch_bounds__(kAdjPrepThreads) k_tile_bprep(TileArgs a) {
     __syncthreads();
     float re = 0.f, im = 0.f;
     if (p < P)
-      for (int m = q; m < N; m += 4) {
+      for (int m = q; m < N; m += Q) {
         const float2 y = ys[m], c = a.coef[(int64_t)m * kChebPMax + p];   // y conj(c)
         re = fmaf(y.x, c.x, fmaf(y.y, c.y, re));
         im = fmaf(y.y, c.x, fmaf(-y.x, c.y, im));
       }
-    part[q * 64 + p] = make_float2(re, im);
+    part[q * PP + p] = make_float2(re, im);
     __syncthreads();
-    if (threadIdx.x < P) {
+    if (threadIdx.x < P) {                          // fixed-order sum over the Q partials
       float2 v = part[threadIdx.x];
-      for (int qq = 1; qq < 4; ++qq) {
-        v.x += part[qq * 64 + threadIdx.x].x;
-        v.y += part[qq * 64 + threadIdx.x].y;
+      for (int qq = 1; qq < Q; ++qq) {
+        v.x += part[qq * PP + threadIdx.x].x;
+        v.y += part[qq * PP + threadIdx.x].y;
       }
       a.bmom[(i * kTiles + t) * kChebPMax + threadIdx.x] = v;
     }
@@ -941,7 +943,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
   const int64_t base = a.tstart[t] + (int64_t)(blk - a.cstart[t]) * kTileChunk;
   const int64_t end = a.tstart[t + 1];
   __shared__ __align__(16) float2 bs[kChebGA][P];
-  __shared__ AntF as[kChebGA];
+  __shared__ AntD as[kChebGA];                      // widened once per stage
   __shared__ double ls[kChebGA];
   const int tid = threadIdx.x;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
@@ -975,17 +977,17 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
       if (MONO) { f.rx = f.ry = f.rz = 0.f; }
       else { f.rx = a.rx_x[ia]; f.ry = a.rx_y[ia]; f.rz = a.rx_z[ia]; }
       f.ptx = f.prx = 1.f;
-      as[tid] = f;
+      as[tid] = widen_ant<MONO>(f);
       ls[tid] = a.lc[(int64_t)t * a.n_a + ia];
     }
     __syncthreads();
 #pragma unroll 1
     for (int aa = 0; aa < ga; ++aa) {
-      const AntD an = widen_ant<MONO>(as[aa]);
+      const AntD an = as[aa];
       float ec[SPT], es[SPT], xv[SPT], sg[SPT];
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
-        const double L = pair_length<MONO>(q[u], an);
+        const double L = pair_length64<MONO>(q[u], an);
         __sincosf(kTwoPi * frac_cycles(L * a.kc), &es[u], &ec[u]);
         float x = (float)((L - ls[aa]) * inv);
         x = fminf(fmaxf(x, -1.f), 1.f);
