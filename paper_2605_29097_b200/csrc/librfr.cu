@@ -141,7 +141,8 @@ struct Layout {
          off_fwdp = 0, off_bwdp = 0, off_fltp = 0, off_bprep = 0, off_cbox = 0, off_clc = 0,
          off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, off_aflag = 0,
          off_idxc = 0, off_ttile = 0, off_tbcnt = 0, off_tstart = 0, off_tperm = 0, off_tqs = 0,
-         off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, total = 0;
+         off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, off_trs = 0,
+         total = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
@@ -199,6 +200,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_thdr = take(64);
     L.off_tcoef = take((size_t)nf * kChebPMax * 8);
     L.off_tbmom = take((size_t)na1 * kTiles * kChebPMax * 8);
+    L.off_trs = take((size_t)n_s * sizeof(Rec));            // tiled backward: sorted records
   }
   L.total = o;
   return true;
@@ -305,6 +307,7 @@ TileArgs make_tile(const float *qx, const float *qy, const float *qz, int64_t n,
   t.n = n;
   t.tx_x = ants->tx_x; t.tx_y = ants->tx_y; t.tx_z = ants->tx_z;
   t.rx_x = ants->rx_x; t.rx_y = ants->rx_y; t.rx_z = ants->rx_z;
+  t.phi_tx = ants->phi_tx; t.phi_rx = ants->phi_rx;
   t.n_a = ants->n_ant;
   t.n_f = grid->n_freq;
   t.kd = c.kd;
@@ -642,10 +645,20 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   }
   RFR_CU(launch_adjoint(a, kModeBwd, mono, corr, sp.splits, st));
   if (cheb) {
-    AdjArgs ab = a;
-    ab.rec = rec_c;
-    RFR_CU(launch_cheb_adj(c, ab, at<float2>(ws, L.off_cbadj), kModeBwd, mono, corr, sp.splits,
-                           st));
+    if (tile_enabled()) {
+      TileArgs tb = make_tile(nullptr, nullptr, nullptr, n_s, ants, grid, c, a.X, nullptr,
+                              sp.per_split, ws, L);
+      tb.rec = rec_c;
+      tb.n_dev = n_act;
+      tb.idx = idx_c;
+      tb.rs = at<Rec>(ws, L.off_trs);
+      RFR_CU(launch_tiled_backward(tb, a, mono, corr, sp.splits, st));
+    } else {
+      AdjArgs ab = a;
+      ab.rec = rec_c;
+      RFR_CU(launch_cheb_adj(c, ab, at<float2>(ws, L.off_cbadj), kModeBwd, mono, corr,
+                             sp.splits, st));
+    }
   }
   if (sp.splits > 1)
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
@@ -762,9 +775,8 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     cf.row = 1;
     AdjArgs af = a;
     af.out = a.out2;
-    if (tile_enabled()) {
-      // B of the backward rows (G) only; the filter prepares its own per-tile moments
-      RFR_CU(launch_cheb_adj_prep_only(c, a, bmom, st));
+    const bool tiled = tile_enabled();
+    if (tiled) {
       const TileArgs ta = make_tile(samples->x, samples->y, samples->z, n_s, ants, grid, c, a.X2,
                                     reinterpret_cast<float2 *>(a.out2), sp.per_split, ws, L);
       RFR_CU(launch_tiled_filter(ta, mono, sp.splits, st));
@@ -776,14 +788,24 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
     RFR_CU(launch_compact(a.rec, n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c, st,
                           at<unsigned char>(ws, L.off_aflag), idx_c));
-    ChebArgs cb = c;
-    cb.rec = rec_c;
-    cb.n_dev = n_act;
-    cb.idx = idx_c;
-    cb.row = 0;
-    AdjArgs ab = a;
-    ab.rec = rec_c;
-    RFR_CU(launch_cheb_adj(cb, ab, bmom, kModeBwd, mono, corr, sp.splits, st, -1));
+    if (tiled) {
+      TileArgs tb = make_tile(nullptr, nullptr, nullptr, n_s, ants, grid, c, a.X, nullptr,
+                              sp.per_split, ws, L);
+      tb.rec = rec_c;
+      tb.n_dev = n_act;
+      tb.idx = idx_c;
+      tb.rs = at<Rec>(ws, L.off_trs);
+      RFR_CU(launch_tiled_backward(tb, a, mono, corr, sp.splits, st));
+    } else {
+      ChebArgs cb = c;
+      cb.rec = rec_c;
+      cb.n_dev = n_act;
+      cb.idx = idx_c;
+      cb.row = 0;
+      AdjArgs ab = a;
+      ab.rec = rec_c;
+      RFR_CU(launch_cheb_adj(cb, ab, bmom, kModeBwd, mono, corr, sp.splits, st, -1));
+    }
   }
   if (sp.splits > 1) {
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,

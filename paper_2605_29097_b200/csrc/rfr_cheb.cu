@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_flt4(ChebArgs c, AdjAr
 
 // =============================================================== tiled matched filter (5d)
 constexpr int kTileBlock = 1024;
-constexpr int kTileChunk = 4 * kChebThreads;       // points per filter CTA
+constexpr int kTileChunk = 4 * kChebThreads;       // points per filter CTA (TileArgs.chunk)
 
 int tile_count_blocks(int64_t n) { return (int)((n + kTileBlock - 1) / kTileBlock); }
 
@@ -765,10 +765,15 @@ __device__ __forceinline__ void warp_tile_counts(int t, bool ok, int (*wc)[kTile
 __global__ void __launch_bounds__(kTileBlock) k_tile_count(TileArgs a) {
   if (a.ghdr->sel == 0) return;
   __shared__ int wc[kTileBlock / 32][kTiles];
+  const int64_t n = a.n_dev ? *a.n_dev : a.n;
   const int64_t j = (int64_t)blockIdx.x * kTileBlock + threadIdx.x;
-  const bool ok = j < a.n;
-  const int t = ok ? tile_of(a.gbox, a.qx[j], a.qy[j], a.qz[j]) : 0;
-  if (ok) a.tile[j] = (unsigned char)t;
+  const bool ok = j < n;
+  int t = 0;
+  if (ok) {
+    t = a.rec ? tile_of(a.gbox, (float)a.rec[j].x, (float)a.rec[j].y, (float)a.rec[j].z)
+              : tile_of(a.gbox, a.qx[j], a.qy[j], a.qz[j]);
+    a.tile[j] = (unsigned char)t;
+  }
   warp_tile_counts(t, ok, wc);
   __syncthreads();
   if (threadIdx.x < kTiles) {
@@ -797,7 +802,7 @@ __global__ void k_tile_scan(TileArgs a, int nb) {
       a.tstart[k] = s;
       a.cstart[k] = cs;
       s += tot[k];
-      cs += (tot[k] + kTileChunk - 1) / kTileChunk;
+      cs += (tot[k] + a.chunk - 1) / a.chunk;
     }
     a.tstart[kTiles] = s;
     a.cstart[kTiles] = cs;
@@ -807,8 +812,9 @@ __global__ void k_tile_scan(TileArgs a, int nb) {
 __global__ void __launch_bounds__(kTileBlock) k_tile_write(TileArgs a) {
   if (a.ghdr->sel == 0) return;
   __shared__ int wc[kTileBlock / 32][kTiles];
+  const int64_t n = a.n_dev ? *a.n_dev : a.n;
   const int64_t j = (int64_t)blockIdx.x * kTileBlock + threadIdx.x;
-  const bool ok = j < a.n;
+  const bool ok = j < n;
   const int t = ok ? (int)a.tile[j] : 0;
   warp_tile_counts(t, ok, wc);
   __syncthreads();
@@ -819,7 +825,13 @@ __global__ void __launch_bounds__(kTileBlock) k_tile_write(TileArgs a) {
     for (int w = 0; w < warp; ++w) pos += wc[w][t];
     pos += __popc(m & ((1u << lane) - 1u));
     a.perm[pos] = (int)j;
-    a.qs[pos] = make_float4(a.qx[j], a.qy[j], a.qz[j], 0.f);
+    if (a.rec) {
+      const Rec r = a.rec[j];
+      a.rs[pos] = r;
+      a.qs[pos] = make_float4((float)r.x, (float)r.y, (float)r.z, 0.f);
+    } else {
+      a.qs[pos] = make_float4(a.qx[j], a.qy[j], a.qz[j], 0.f);
+    }
   }
 }
 
@@ -940,7 +952,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
   if (blk >= a.cstart[kTiles]) return;
   int t = 0;
   while (a.cstart[t + 1] <= blk) ++t;               // the tile of this CTA (kTiles entries)
-  const int64_t base = a.tstart[t] + (int64_t)(blk - a.cstart[t]) * kTileChunk;
+  const int64_t base = a.tstart[t] + (int64_t)(blk - a.cstart[t]) * a.chunk;
   const int64_t end = a.tstart[t + 1];
   __shared__ __align__(16) float2 bs[kChebGA][P];
   __shared__ AntD as[kChebGA];                      // widened once per stage
@@ -1049,8 +1061,7 @@ static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
   k_tile_flt4<48, MONO><<<g, kChebThreads, 0, st>>>(a);
 }
 
-cudaError_t launch_tiled_filter(const TileArgs &a, bool mono, int n_splits, cudaStream_t st) {
-  if (a.n_a <= 0 || a.n <= 0) return cudaSuccess;
+static cudaError_t tile_prepare(const TileArgs &a, cudaStream_t st) {
   const int nb = tile_count_blocks(a.n);
   k_tile_count<<<nb, kTileBlock, 0, st>>>(a);
   k_tile_scan<<<1, kTiles, 0, st>>>(a, nb);
@@ -1067,10 +1078,153 @@ cudaError_t launch_tiled_filter(const TileArgs &a, bool mono, int n_splits, cuda
     if (e != cudaSuccess) return e;
   }
   k_tile_bprep<<<(unsigned)a.n_a, kAdjPrepThreads, sm, st>>>(a);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(9);
+  return e;
+}
+
+cudaError_t launch_tiled_filter(const TileArgs &a0, bool mono, int n_splits, cudaStream_t st) {
+  if (a0.n_a <= 0 || a0.n <= 0) return cudaSuccess;
+  TileArgs a = a0;
+  a.chunk = kTileChunk;
+  cudaError_t e = tile_prepare(a, st);
+  if (e != cudaSuccess) return e;
   dim3 g((unsigned)((a.n + kTileChunk - 1) / kTileChunk + kTiles), (unsigned)n_splits);
   if (mono) tile_flt_all<true>(a, g, st);
   else tile_flt_all<false>(a, g, st);
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(14);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
+  return e;
+}
+
+// ------------------------------------------------- tiled backward (compacted active samples)
+// As k_cheb_adj (kModeBwd, two samples per thread) over the tile-sorted compacted records, with
+// the per-(antenna, tile) centres and moments of G; partials at the original sample index.
+template <int P, bool MONO, bool CORR>
+__global__ void __launch_bounds__(kChebThreads, 4) k_tile_bwd(TileArgs ta, AdjArgs a) {
+  if (ta.hdr->P != P) return;
+  const int blk = blockIdx.x;
+  if (blk >= ta.cstart[kTiles]) return;
+  int t = 0;
+  while (ta.cstart[t + 1] <= blk) ++t;
+  const int64_t base = ta.tstart[t] + (int64_t)(blk - ta.cstart[t]) * ta.chunk;
+  const int64_t end = ta.tstart[t + 1];
+  __shared__ __align__(16) float2 bs[kChebGA][P];
+  __shared__ AntF as[kChebGA];
+  __shared__ double ls[kChebGA];
+  const int tid = threadIdx.x;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  bool valid[2];
+  Rec rec[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int64_t k = base + tid + u * kChebThreads;
+    valid[u] = k < end;
+    if (valid[u]) rec[u] = ta.rs[k];
+    else { rec[u].x = rec[u].y = 0.0; rec[u].z = 1.0; rec[u].w = 0.f; rec[u].T = 0.f;
+           rec[u].nx = rec[u].ny = 0.f; rec[u].nz = 1.f; rec[u].papr = 1.f; }
+  }
+  const bool no_gain = a.no_gain;
+  const double inv = ta.hdr->inv;
+  float S1[2] = {0.f, 0.f}, S2[2] = {0.f, 0.f}, S3x[2] = {0.f, 0.f}, S3y[2] = {0.f, 0.f},
+        S3z[2] = {0.f, 0.f};
+  bool domain = false;
+  for (int64_t i0 = i_lo; i0 < i_hi; i0 += kChebGA) {
+    const int ga = (int)min((int64_t)kChebGA, i_hi - i0);
+    __syncthreads();
+    for (int w = tid; w < ga * P; w += kChebThreads) {
+      const int aa = w / P, p = w % P;
+      bs[aa][p] = ta.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+    }
+    if (tid < ga) {
+      as[tid] = load_antf<MONO>(a, i0 + tid);
+      ls[tid] = ta.lc[(int64_t)t * ta.n_a + i0 + tid];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int aa = 0; aa < ga; ++aa) {
+      const AntD an = widen_ant<MONO>(as[aa]);
+      PairBwd g[2];
+      float ec[2], es[2], xv[2], sg[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        pair_geometry<MONO, CORR>(rec[u], an, no_gain, g[u]);
+        domain |= valid[u] && !g[u].ok;
+        const double L = g[u].L;
+        __sincosf(kTwoPi * frac_cycles(L * ta.kc), &es[u], &ec[u]);
+        float x = (float)((L - ls[aa]) * inv);
+        x = fminf(fmaxf(x, -1.f), 1.f);
+        xv[u] = fabsf(x) - 1.f;
+        sg[u] = x < 0.f ? -1.f : 1.f;
+      }
+      const float2 *B = bs[aa];
+      const float2 b0 = B[0];
+      f2x he0 = pk(b0.x, b0.y), he1 = he0, ho0 = 0ull, ho1 = 0ull;
+      const f2x two_xm1 = pk(2.f * xv[0], 2.f * xv[1]);
+      f2x d = pk(xv[0], xv[1]);
+      f2x tt = fadd2(pk(1.f, 1.f), d);
+      {
+        const float2 b = B[1];
+        const float2 tv = upk(tt);
+        ho0 = ffma2(pk(tv.x, tv.x), pk(b.x, b.y), ho0);
+        ho1 = ffma2(pk(tv.y, tv.y), pk(b.x, b.y), ho1);
+      }
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d = ffma2(two_xm1, tt, d);
+        tt = fadd2(tt, d);
+        const float2 b = B[p];
+        const f2x pb = pk(b.x, b.y);
+        const float2 tv = upk(tt);
+        if (p & 1) {
+          ho0 = ffma2(pk(tv.x, tv.x), pb, ho0);
+          ho1 = ffma2(pk(tv.y, tv.y), pb, ho1);
+        } else {
+          he0 = ffma2(pk(tv.x, tv.x), pb, he0);
+          he1 = ffma2(pk(tv.y, tv.y), pb, he1);
+        }
+      }
+      const float2 h0 = upk(ffma2(pk(sg[0], sg[0]), ho0, he0));
+      const float2 h1 = upk(ffma2(pk(sg[1], sg[1]), ho1, he1));
+      adj_accumulate<kModeBwd>(g[0], ec[0], es[0], h0.x, h0.y, S1[0], S2[0], S3x[0], S3y[0],
+                               S3z[0]);
+      adj_accumulate<kModeBwd>(g[1], ec[1], es[1], h1.x, h1.y, S1[1], S2[1], S3x[1], S3y[1],
+                               S3z[1]);
+    }
+  }
+  if (domain) atomicOr(a.flags, 1u);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!valid[u]) continue;
+    const int64_t j = ta.idx[ta.perm[base + tid + u * kChebThreads]];
+    adj_store<kModeBwd>(a, j, S1[u], S2[u], S3x[u], S3y[u], S3z[u]);
+  }
+}
+
+template <bool MONO, bool CORR>
+static void tile_bwd_all(const TileArgs &ta, const AdjArgs &a, dim3 g, cudaStream_t st) {
+  k_tile_bwd<16, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
+  k_tile_bwd<24, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
+  k_tile_bwd<28, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
+  k_tile_bwd<32, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
+  k_tile_bwd<48, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
+}
+
+cudaError_t launch_tiled_backward(const TileArgs &t0, const AdjArgs &a, bool mono, bool corr,
+                                  int n_splits, cudaStream_t st) {
+  if (t0.n_a <= 0 || t0.n <= 0) return cudaSuccess;
+  TileArgs t = t0;
+  t.chunk = 2 * kChebThreads;
+  cudaError_t e = tile_prepare(t, st);
+  if (e != cudaSuccess) return e;
+  dim3 g((unsigned)((t.n + t.chunk - 1) / t.chunk + kTiles), (unsigned)n_splits);
+  if (mono) {
+    if (corr) tile_bwd_all<true, true>(t, a, g, st);
+    else tile_bwd_all<true, false>(t, a, g, st);
+  } else {
+    if (corr) tile_bwd_all<false, true>(t, a, g, st);
+    else tile_bwd_all<false, false>(t, a, g, st);
+  }
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
   return e;
 }
 

@@ -175,8 +175,14 @@ constexpr int kTileDim = 4;
 constexpr int kTiles = kTileDim * kTileDim * kTileDim;
 struct TileArgs {
   const float *qx, *qy, *qz;
-  int64_t n;
+  int64_t n;                       // points (upper bound when n_dev is set)
+  const Rec *rec;                  // backward: the compacted records instead of qx / qy / qz
+  const int64_t *n_dev;            // backward: device count of rec
+  Rec *rs;                         // backward: sorted records
+  const int *idx;                  // backward: original sample index of each compacted record
+  int chunk;                       // points per CTA of the sweep (filter 512, backward 256)
   const float *tx_x, *tx_y, *tx_z, *rx_x, *rx_y, *rx_z;
+  const float *phi_tx, *phi_rx;
   int64_t n_a;
   int n_f;
   double kd, kc;
@@ -200,6 +206,9 @@ struct TileArgs {
   int64_t ants_per_split;
 };
 cudaError_t launch_tiled_filter(const TileArgs &t, bool mono, int n_splits, cudaStream_t st);
+// tiled backward over the compacted active samples (t.rec, t.n_dev, t.idx): partials of a
+cudaError_t launch_tiled_backward(const TileArgs &t, const AdjArgs &a, bool mono, bool corr,
+                                  int n_splits, cudaStream_t st);
 cudaError_t launch_cheb_adj_prep_only(const ChebArgs &c, const AdjArgs &a, float2 *bmom,
                                       cudaStream_t st);
 int tile_count_blocks(int64_t n);
