@@ -971,6 +971,8 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
     q[u].w = 0.f; q[u].T = 1.f; q[u].nx = q[u].ny = 0.f; q[u].nz = 1.f; q[u].papr = 1.f;
   }
   const double inv = a.hdr->inv;
+  // monostatic: L = 2 d, so the cycle count is d (2 kc) and x = d (2 inv) - L_c inv (one DFMA)
+  const double kc2 = 2.0 * a.kc, inv2 = 2.0 * inv;
   float M1[SPT], M2[SPT];
 #pragma unroll
   for (int u = 0; u < SPT; ++u) { M1[u] = 0.f; M2[u] = 0.f; }
@@ -990,7 +992,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
       else { f.rx = a.rx_x[ia]; f.ry = a.rx_y[ia]; f.rz = a.rx_z[ia]; }
       f.ptx = f.prx = 1.f;
       as[tid] = widen_ant<MONO>(f);
-      ls[tid] = a.lc[(int64_t)t * a.n_a + ia];
+      ls[tid] = a.lc[(int64_t)t * a.n_a + ia] * (MONO ? inv : 1.0);   // L_c inv (mono) or L_c
     }
     __syncthreads();
 #pragma unroll 1
@@ -999,9 +1001,19 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
       float ec[SPT], es[SPT], xv[SPT], sg[SPT];
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
-        const double L = pair_length64<MONO>(q[u], an);
-        __sincosf(kTwoPi * frac_cycles(L * a.kc), &es[u], &ec[u]);
-        float x = (float)((L - ls[aa]) * inv);
+        double cyc, xd;
+        if (MONO) {
+          const double dx = q[u].x - an.x, dy = q[u].y - an.y, dz = q[u].z - an.z;
+          const double d = dist64(fma(dx, dx, fma(dy, dy, dz * dz)));
+          cyc = d * kc2;
+          xd = fma(d, inv2, -ls[aa]);
+        } else {
+          const double L = pair_length64<MONO>(q[u], an);
+          cyc = L * a.kc;
+          xd = (L - ls[aa]) * inv;
+        }
+        __sincosf(kTwoPi * frac_cycles(cyc), &es[u], &ec[u]);
+        float x = (float)xd;
         x = fminf(fmaxf(x, -1.f), 1.f);
         xv[u] = fabsf(x) - 1.f;
         sg[u] = x < 0.f ? -1.f : 1.f;
