@@ -738,6 +738,10 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_flt4(ChebArgs c, AdjAr
 // =============================================================== tiled matched filter (5d)
 constexpr int kTileBlock = 1024;
 constexpr int kTileChunk = 4 * kChebThreads;       // points per filter CTA (TileArgs.chunk)
+#ifndef RFR_TILE_FLT_MINB
+#define RFR_TILE_FLT_MINB 5
+#endif
+constexpr int kTileFltMinBlocks = RFR_TILE_FLT_MINB;  // CTAs per SM of the tiled filter
 
 int tile_count_blocks(int64_t n) { return (int)((n + kTileBlock - 1) / kTileBlock); }
 
@@ -945,7 +949,7 @@ __global__ void __launch_bounds__(kAdjPrepThreads) k_tile_bprep(TileArgs a) {
 
 // the filter over the sorted points: CTA -> (tile, chunk of kTileChunk points), 4 per thread
 template <int P, bool MONO>
-__global__ void __launch_bounds__(kChebThreads, 4) k_tile_flt4(TileArgs a) {
+__global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(TileArgs a) {
   if (a.hdr->P != P) return;
   constexpr int SPT = 4;
   const int blk = blockIdx.x;
