@@ -299,7 +299,7 @@ __global__ void k_cheb_coef(const ChebHdr *__restrict__ hdr, int n_f, int pmax,
 // memory (every thread reads the same record: broadcast).  KIND == kFwdMFAdj: the records are the
 // K5 query records {x, y, z, w = Re c_q, T = Im c_q} and the pair amplitude is c_q.
 template <int P, bool MONO, bool CORR, int KIND>
-__global__ void __launch_bounds__(kChebThreads, P <= 32 ? 4 : 3) k_cheb_fwd(ChebArgs a) {
+__global__ void __launch_bounds__(kChebThreads, (MONO && P <= 28) || P <= 16 ? 5 : (P <= 32 ? 4 : 3)) k_cheb_fwd(ChebArgs a) {
   if (a.hdr->P != P) return;                     // another P (or the direct kernel) was chosen
   __shared__ __align__(16) Rec rb[2][kChebTJ];
   const int tid = threadIdx.x;
