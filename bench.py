@@ -224,7 +224,17 @@ def run_gpu(args):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    fused = not args.separate
+    heat = args.step == "heatmap"
+    fused = not args.separate and not heat
+    if heat:
+        # NEXT-1: the paper's heatmap-domain L2.  Ground-truth heatmap = the filter of
+        # the noisy target y at the same queries (the samples), built untimed
+        for s in B:
+            s["P_gt"] = torch.empty(s["n"], device=dev)
+            s["gP"] = torch.empty(s["n"], device=dev)
+            rfr.rfr_filter(s["y"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P_gt"], s["ws"],
+                           comm=comm)
+        torch.cuda.synchronize()
 
     def step(rec=None):
         # fused (default): K2 forward, K6 loss, then K3 + K4 in one tensor-core sweep
@@ -239,7 +249,13 @@ def run_gpu(args):
                 rfr.rfr_filter(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P"],
                                s["ws"], mf=s["M"], comm=comm)
             if e: e[2].record(st)
-            rfr.rfr_loss(s["sig"], s["y"], s["G"], s["loss"], s["ws"])
+            if heat:
+                # K7 heatmap L2, then K5 (matched-filter adjoint) turns dL/dP into dL/ds
+                rfr.rfr_heatmap_loss(s["P"], s["P_gt"], s["gP"], s["loss"], s["ws"])
+                rfr.rfr_filter_backward(s["gP"], s["M"], s["A"], grid, s["S"].x, s["S"].y,
+                                        s["S"].z, s["G"], s["ws"], power=s["P"], eps=1e-20)
+            else:
+                rfr.rfr_loss(s["sig"], s["y"], s["G"], s["loss"], s["ws"])
             if e: e[3].record(st)
             if fused:
                 rfr.rfr_backward_filter(s["G"], s["sig"], s["S"], prob.sharpness, s["A"], grid,
@@ -267,6 +283,20 @@ def run_gpu(args):
     s0 = B[0]
     rfr.rfr_forward(s0["S"], prob.sharpness, s0["A"], grid, s0["sig"], s0["ws"])
     cf = rfr.cheb_state(s0["ws"])
+    p_flt_sep = p_k5 = 0
+    if not fused:
+        rfr.rfr_filter(s0["sig"], s0["A"], grid, s0["S"].x, s0["S"].y, s0["S"].z, s0["P"],
+                       s0["ws"], mf=s0["M"])
+        cq = rfr.cheb_state(s0["ws"])
+        p_flt_sep = cq["P_tiled_filter"] if cq["sel"] else 0
+    if heat:
+        rfr.rfr_heatmap_loss(s0["P"], s0["P_gt"], s0["gP"], s0["loss"], s0["ws"])
+        rfr.rfr_filter_backward(s0["gP"], s0["M"], s0["A"], grid, s0["S"].x, s0["S"].y, s0["S"].z,
+                                s0["G"], s0["ws"], power=s0["P"], eps=1e-20)
+        ck = rfr.cheb_state(s0["ws"])
+        # tiled K5 (DESIGN 6b) publishes its own P like the tiled filter; RFR_TILE=0: untiled
+        p_k5 = ((ck["P_tiled_filter"] if os.environ.get("RFR_TILE") != "0" else ck["P"])
+                if ck["sel"] else 0)
     if fused:
         rfr.rfr_backward_filter(s0["G"], s0["sig"], s0["S"], prob.sharpness, s0["A"], grid,
                                 s0["out"], s0["P"], s0["ws"], mf=s0["M"], flags=rfr.RFR_REUSE_BLEND)
@@ -368,16 +398,30 @@ def run_gpu(args):
                           "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
                           "lane_ops_per_pair": ops, "active_sample_fraction": act_bwd,
                           "ms_per_step": per_step(ms)})
-    if cheb_adj_P and fused:
+    if p_flt_sep:
+        # tiled Chebyshev filter (section 5d) over every (sample, antenna) pair: 4 P lane-ops
+        ach = 4 * p_flt_sep * n_pairs / (per_step(q_ms) * 1e-3)
+        roofs.append({"kernel": f"k_tile_flt4<P={p_flt_sep}> (K4, rfr_filter)", "bound": "alu",
+                      "achieved": ach / 1e12, "peak": peak_ops / 1e12,
+                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
+                      "lane_ops_per_pair": 4 * p_flt_sep, "ms_per_step": per_step(q_ms)})
+    if p_k5:
+        # K5 = a forward-shaped Chebyshev sweep over the queries: 4 P lane-ops
+        # per (query, antenna) pair; its segment also holds the (negligible) K7 heatmap loss
+        ach = 4 * p_k5 * n_pairs / (per_step(l_ms) * 1e-3)
+        k5 = "k_tile_fwd" if os.environ.get("RFR_TILE") != "0" else "k_cheb_fwd"
+        roofs.append({"kernel": f"{k5}<P={p_k5},MFAdj> (K5+K7, rfr_filter_backward)",
+                      "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
+                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
+                      "lane_ops_per_pair": 4 * p_k5, "ms_per_step": per_step(l_ms)})
+    if cheb_adj_P:
         pass
     elif fused:
         adj = [("k_adjoint_tc<both> (K3+K4 fused +K1', rfr_backward_filter)", b_ms, 2)]
-    elif cheb_adj_P:
-        adj = [("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms, 1)]
     else:
         adj = [("k_adjoint_tc<bwd> (K3+K1', rfr_backward)", b_ms, 1),
                ("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms, 1)]
-    if cheb_adj_P and fused:
+    if cheb_adj_P:
         adj = []
     for name, ms, npass in adj:
         rate = npass * (Nc / world) / (per_step(ms) * 1e-3)     # contributions of all its passes
@@ -425,7 +469,11 @@ def run_gpu(args):
                        "n_antennas": [b.antennas.n for b in prob.bundles][0],
                        "n_freq": grid.n_freq, "parallelism": f"antenna-shard x{world}",
                        "l2": "flushed between steps (512 MiB memset, outside the step events)",
-                       "step": ("K1 blend + forward + K6 loss + K3/K4 fused backward + "
+                       "loss": "heatmap L2 (NEXT-1)" if heat else "signal-domain complex residual",
+                       "step": ("K1 blend + forward + K4 filter (+NCCL all-reduce of M) + K7 "
+                                "heatmap loss + K5 matched-filter adjoint + K3 backward (+NCCL "
+                                "all-reduce of partials) + K1' finish" if heat else
+                                "K1 blend + forward + K6 loss + K3/K4 fused backward + "
                                 "matched filter at the samples (+NCCL all-reduce of partials and "
                                 "M) + K1' finish" if fused else
                                 "K1 blend + forward + K4 filter (+NCCL all-reduce of M) + K6 "
@@ -434,6 +482,9 @@ def run_gpu(args):
                         "filter_plus_bwd_fused_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
                         "loss_ms": per_step(l_ms), "fwd_ms": per_step(f_ms),
                         "filter_plus_bwd_ms": per_step(b_ms)} if fused else
+                       {"fwd_ms": per_step(f_ms), "filter_ms": per_step(q_ms),
+                        "heat_loss_plus_k5_ms": per_step(l_ms), "bwd_ms": per_step(b_ms),
+                        "k5_G_per_s": Nc / (per_step(l_ms) * 1e-3) / 1e9} if heat else
                        {"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
                         "filter_G_per_s": Nc / (per_step(q_ms) * 1e-3) / 1e9,
                         "bwd_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
@@ -471,7 +522,8 @@ def run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step):
         for f in ("tx_x", "tx_y", "tx_z"):
             d = getattr(s["A"], f)
             host_in.append(d.cpu().pin_memory()); dev_in.append(d)
-        host_in.append(s["y"].cpu().pin_memory()); dev_in.append(s["y"])
+        tgt = s["P_gt"] if "P_gt" in s else s["y"]      # heatmap step: the target heatmap
+        host_in.append(tgt.cpu().pin_memory()); dev_in.append(tgt)
         for f in ("sdf", "refl", "nx", "ny", "nz", "power", "sharpness"):
             d = getattr(s["out"], f)
             host_out.append(torch.empty(d.shape, dtype=d.dtype).pin_memory()); dev_out.append(d)
@@ -513,6 +565,10 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=20.0,
                     help="seconds of oracle work per reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--step", default="signal", choices=["signal", "heatmap"],
+                    help="signal: the north_star step (signal-domain residual, default); heatmap: "
+                         "the paper's heatmap-domain L2 through the matched-filter adjoint K5 "
+                         "(SURVEY 8f NEXT-1)")
     ap.add_argument("--separate", action="store_true",
                     help="filter and backward as two sweeps (rfr_filter + rfr_backward)")
     args = ap.parse_args()

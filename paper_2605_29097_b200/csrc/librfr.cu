@@ -142,7 +142,8 @@ struct Layout {
          off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, off_aflag = 0,
          off_idxc = 0, off_ttile = 0, off_tbcnt = 0, off_tstart = 0, off_tperm = 0, off_tqs = 0,
          off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, off_trs = 0,
-         total = 0;
+         off_tfp = 0, total = 0;
+  size_t cap_trs = 0, cap_tfp = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
@@ -200,7 +201,11 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_thdr = take(64);
     L.off_tcoef = take((size_t)nf * kChebPMax * 8);
     L.off_tbmom = take((size_t)na1 * kTiles * kChebPMax * 8);
-    L.off_trs = take((size_t)n_s * sizeof(Rec));            // tiled backward: sorted records
+    // tiled backward / K5: sorted records; tiled K5: moments per (chunk CTA, antenna)
+    L.cap_trs = (size_t)np * sizeof(Rec);
+    L.off_trs = take(L.cap_trs);
+    L.cap_tfp = (size_t)tile_fwd_blocks(n_q) * na1 * kChebPMax * 8;
+    L.off_tfp = take(L.cap_tfp);
   }
   L.total = o;
   return true;
@@ -387,8 +392,20 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
     RFR_CU(launch_sum_splits(at<float>(ws, L.off_fwdp), sp.splits,
                              ants->n_ant * (int64_t)grid->n_freq * 2, out, device_sms(), st,
                              cheb ? hdr : nullptr));
-  if (cheb)
-    RFR_CU(launch_cheb_fwd(c, mono, corr, kind, cs.splits, reinterpret_cast<float2 *>(out), st));
+  if (!cheb) return RFR_OK;
+  // K5 tiled (DESIGN 6b): per-(antenna, tile) centres cut P to the tiles' spread
+  if (kind == kFwdMFAdj && tile_enabled() && !rec_c && !direct &&
+      (size_t)n_pts * sizeof(Rec) <= L.cap_trs &&
+      (size_t)tile_fwd_blocks(n_pts) * ants->n_ant * kChebPMax * 8 <= L.cap_tfp) {
+    TileArgs ta = make_tile(nullptr, nullptr, nullptr, n_pts, ants, grid, c, nullptr, nullptr, 0,
+                            ws, L);
+    ta.rec = rec;
+    ta.rs = at<Rec>(ws, L.off_trs);
+    ta.fpart = at<float2>(ws, L.off_tfp);
+    RFR_CU(launch_tiled_mfadj(ta, mono, reinterpret_cast<float2 *>(out), st));
+    return RFR_OK;
+  }
+  RFR_CU(launch_cheb_fwd(c, mono, corr, kind, cs.splits, reinterpret_cast<float2 *>(out), st));
   return RFR_OK;
 }
 

@@ -1077,7 +1077,7 @@ static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
   k_tile_flt4<48, MONO><<<g, kChebThreads, 0, st>>>(a);
 }
 
-static cudaError_t tile_prepare(const TileArgs &a, cudaStream_t st) {
+static cudaError_t tile_prepare(const TileArgs &a, cudaStream_t st, bool bprep = true) {
   const int nb = tile_count_blocks(a.n);
   k_tile_count<<<nb, kTileBlock, 0, st>>>(a);
   k_tile_scan<<<1, kTiles, 0, st>>>(a, nb);
@@ -1088,6 +1088,10 @@ static cudaError_t tile_prepare(const TileArgs &a, cudaStream_t st) {
   k_tile_setup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
   k_tile_select<<<1, 1, 0, st>>>(a);
   k_cheb_coef<<<(a.n_f + 127) / 128, 128, 0, st>>>(a.hdr, a.n_f, kChebPMax, a.coef);
+  if (!bprep) {
+    if ((e = cudaGetLastError()) == cudaSuccess) add_launches(8);
+    return e;
+  }
   const size_t sm = (2 * (size_t)a.n_f + 4 * 64) * sizeof(float2);
   if (sm > 48 * 1024) {
     e = cudaFuncSetAttribute(k_tile_bprep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1108,6 +1112,243 @@ cudaError_t launch_tiled_filter(const TileArgs &a0, bool mono, int n_splits, cud
   if (mono) tile_flt_all<true>(a, g, st);
   else tile_flt_all<false>(a, g, st);
   if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
+  return e;
+}
+
+// --------------------------------------------------- tiled K5 (matched-filter adjoint, DESIGN 6b)
+// dL/ds_i[m] = sum_q c_q e^{-j 2 pi f_m tau_iq} is forward-shaped: per (antenna, tile) the moments
+// M_it[p] = sum_{q in t} c_q e^{-j 2 pi f_c tau_iq} T_p(x_iqt) around the tile's own centre
+// (x_iqt = (L_iq - L_c,it) inv), then s_i[m] = sum_t e^{-j 2 pi m' u_c,it} sum_p a[m][p] M_it[p].
+// CTA = (128 antennas, one chunk of one tile's sorted query records), as k_cheb_fwd.
+int64_t tile_fwd_chunk(int64_t n) { return std::max<int64_t>(256, (n + 63) / 64); }
+int64_t tile_fwd_blocks(int64_t n) {
+  return n > 0 ? (n + tile_fwd_chunk(n) - 1) / tile_fwd_chunk(n) + kTiles : 0;
+}
+
+template <int P, bool MONO, int MINB, bool QUAD = false>
+__global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
+  if (a.hdr->P != P) return;
+  const int blk = blockIdx.y;
+  if (blk >= a.cstart[kTiles]) return;
+  int t = 0;
+  while (a.cstart[t + 1] <= blk) ++t;               // the tile of this CTA (kTiles entries)
+  const int64_t j_lo = a.tstart[t] + (int64_t)(blk - a.cstart[t]) * a.chunk;
+  const int64_t j_hi = min((int64_t)a.tstart[t + 1], j_lo + a.chunk);
+  __shared__ __align__(16) Rec rb[2][kChebTJ];
+  const int tid = threadIdx.x;
+  const int64_t ia = (int64_t)blockIdx.x * kChebThreads + tid;
+  const bool ant_ok = ia < a.n_a;
+  AntF af;
+  if (ant_ok) af = load_antf<MONO>(a, ia);
+  else { af.x = af.y = 0.f; af.z = 1.f; af.rx = af.ry = 0.f; af.rz = 1.f; af.ptx = af.prx = 1.f; }
+  const AntD an = widen_ant<MONO>(af);
+  const double Lc = ant_ok ? a.lc[(int64_t)t * a.n_a + ia] : 0.0;
+  const double inv = a.hdr->inv;
+  const double kc2 = 2.0 * a.kc, inv2 = 2.0 * inv, lsi = Lc * inv;
+  f2x M[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) M[p] = 0ull;
+  auto prefetch = [&](int64_t jt, int b) {
+    const int nv = (int)min((int64_t)kChebTJ, j_hi - jt);
+    const float4 *src = reinterpret_cast<const float4 *>(a.rs + jt);
+    float4 *dst = reinterpret_cast<float4 *>(rb[b]);
+    if (tid < kChebTJ * 3) {
+      if (tid < 3 * nv) cp_async16(dst + tid, src + tid);
+      else dst[tid] = make_float4(0.f, 0.f, 0.f, 0.f);      // tail: c = 0 records
+    }
+    cp_async_commit();
+  };
+  if (j_lo < j_hi) prefetch(j_lo, 0);
+  int b = 0;
+  for (int64_t jt = j_lo; jt < j_hi; jt += kChebTJ, b ^= 1) {
+    cp_async_wait_all();
+    __syncthreads();
+    if (jt + kChebTJ < j_hi) prefetch(jt + kChebTJ, b ^ 1);
+    const int nv = (int)min((int64_t)kChebTJ, j_hi - jt);
+#pragma unroll 1
+    for (int jj = 0; jj < nv; jj += (MONO && P <= 16 && QUAD) ? 4 : 2) {
+      f2x cc0 = 0ull, co0 = 0ull, cc1 = 0ull, co1 = 0ull;
+      float xv0 = 0.f, xv1 = 0.f;
+      auto geom = [&](const Rec &rec, f2x &c, f2x &cn, float &xv) {
+        double cyc, xd;
+        if (MONO) {      // L = 2 d: cycles d (2 kc), x = d (2 inv) - L_c inv (as k_tile_flt4)
+          const double dx = rec.x - an.x, dy = rec.y - an.y, dz = rec.z - an.z;
+          const double dd = dist64(fma(dx, dx, fma(dy, dy, dz * dz)));
+          cyc = dd * kc2;
+          xd = fma(dd, inv2, -lsi);
+        } else {
+          const double L = pair_length64<MONO>(rec, an);
+          cyc = L * a.kc;
+          xd = (L - Lc) * inv;
+        }
+        const float Ar = rec.w, Ai = rec.T;               // c_q (k_mf_adj_pack)
+        float es, ec;
+        __sincosf(kTwoPi * frac_cycles(cyc), &es, &ec);
+        c = pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
+        float x = (float)xd;
+        x = fminf(fmaxf(x, -1.f), 1.f);
+        cn = x < 0.f ? pk(-upk(c).x, -upk(c).y) : c;     // odd moments: T_p(x) = -T_p(|x|)
+        xv = fabsf(x) - 1.f;
+      };
+      if (MONO && P <= 16 && QUAD) {   // four records per step: two packed recurrences
+        f2x cc2, co2, cc3, co3;
+        float xv2, xv3;
+        geom(rb[b][jj], cc0, co0, xv0);
+        geom(rb[b][jj + 1], cc1, co1, xv1);
+        geom(rb[b][jj + 2], cc2, co2, xv2);
+        geom(rb[b][jj + 3], cc3, co3, xv3);
+        const f2x two01 = pk(2.f * xv0, 2.f * xv1), two23 = pk(2.f * xv2, 2.f * xv3);
+        f2x d01 = pk(xv0, xv1), d23 = pk(xv2, xv3);
+        acc2(M[0], cc0);
+        acc2(M[0], cc1);
+        acc2(M[0], cc2);
+        acc2(M[0], cc3);
+        f2x t01 = fadd2(pk(1.f, 1.f), d01), t23 = fadd2(pk(1.f, 1.f), d23);
+        {
+          const float2 v01 = upk(t01), v23 = upk(t23);
+          M[1] = ffma2(pk(v01.x, v01.x), co0, M[1]);
+          M[1] = ffma2(pk(v01.y, v01.y), co1, M[1]);
+          M[1] = ffma2(pk(v23.x, v23.x), co2, M[1]);
+          M[1] = ffma2(pk(v23.y, v23.y), co3, M[1]);
+        }
+#pragma unroll
+        for (int p = 2; p < P; ++p) {
+          d01 = ffma2(two01, t01, d01);
+          d23 = ffma2(two23, t23, d23);
+          t01 = fadd2(t01, d01);
+          t23 = fadd2(t23, d23);
+          const float2 v01 = upk(t01), v23 = upk(t23);
+          M[p] = ffma2(pk(v01.x, v01.x), (p & 1) ? co0 : cc0, M[p]);
+          M[p] = ffma2(pk(v01.y, v01.y), (p & 1) ? co1 : cc1, M[p]);
+          M[p] = ffma2(pk(v23.x, v23.x), (p & 1) ? co2 : cc2, M[p]);
+          M[p] = ffma2(pk(v23.y, v23.y), (p & 1) ? co3 : cc3, M[p]);
+        }
+        continue;
+      }
+      if (MONO && P <= 16) {     // both geometries in flight (ILP; no spills at this size)
+        geom(rb[b][jj], cc0, co0, xv0);
+        geom(rb[b][jj + 1], cc1, co1, xv1);
+      } else {
+#pragma unroll 1
+        for (int u = 0; u < 2; ++u) {
+          f2x c, cn;
+          float xv;
+          geom(rb[b][jj + u], c, cn, xv);
+          if (u == 0) { cc0 = c; co0 = cn; xv0 = xv; }
+          else { cc1 = c; co1 = cn; xv1 = xv; }
+        }
+      }
+      const f2x cc[2] = {cc0, cc1}, co[2] = {co0, co1};
+      const f2x xm1 = pk(xv0, xv1), two_xm1 = pk(2.f * xv0, 2.f * xv1);
+      f2x d = xm1, tt = pk(1.f, 1.f);
+      acc2(M[0], cc[0]);
+      acc2(M[0], cc[1]);
+      tt = fadd2(tt, d);
+      {
+        const float2 tv = upk(tt);
+        M[1] = ffma2(pk(tv.x, tv.x), co[0], M[1]);
+        M[1] = ffma2(pk(tv.y, tv.y), co[1], M[1]);
+      }
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        d = ffma2(two_xm1, tt, d);
+        tt = fadd2(tt, d);
+        const float2 tv = upk(tt);
+        M[p] = ffma2(pk(tv.x, tv.x), (p & 1) ? co[0] : cc[0], M[p]);
+        M[p] = ffma2(pk(tv.y, tv.y), (p & 1) ? co[1] : cc[1], M[p]);
+      }
+    }
+  }
+  cp_async_wait_all();
+  if (ant_ok) {
+    float2 *dst = a.fpart + ((int64_t)blk * a.n_a + ia) * kChebPMax;
+#pragma unroll
+    for (int p = 0; p < P; ++p) dst[p] = upk(M[p]);
+  }
+}
+
+// bins: one CTA per antenna; the tiles' moments (fixed-order sums over their chunks) in shared
+// memory, one thread per bin with its coefficient row in registers, tiles in order
+template <int P>
+__global__ void __launch_bounds__(256) k_tile_out(TileArgs a, float2 *__restrict__ out) {
+  if (a.hdr->P != P) return;
+  __shared__ float2 Ms[kTiles][P];
+  __shared__ double uc[kTiles];
+  __shared__ int live[kTiles];
+  const int64_t i = blockIdx.x;
+  for (int w = threadIdx.x; w < kTiles * P; w += blockDim.x) {
+    const int t = w / P, p = w % P;
+    float2 v = make_float2(0.f, 0.f);
+    for (int c = a.cstart[t]; c < a.cstart[t + 1]; ++c) {
+      const float2 u = a.fpart[((int64_t)c * a.n_a + i) * kChebPMax + p];
+      v.x += u.x;
+      v.y += u.y;
+    }
+    Ms[t][p] = v;
+  }
+  if (threadIdx.x < kTiles) {
+    const int t = threadIdx.x;
+    live[t] = a.cstart[t + 1] > a.cstart[t];
+    uc[t] = a.lc[(int64_t)t * a.n_a + i] * a.kd;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
+    float2 cf[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) cf[p] = a.coef[(int64_t)m * kChebPMax + p];
+    const double mc = (double)(m - a.n_f / 2);
+    float re = 0.f, im = 0.f;
+#pragma unroll 1
+    for (int t = 0; t < kTiles; ++t) {
+      if (!live[t]) continue;
+      float vr = 0.f, vi = 0.f;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float2 c = cf[p], v = Ms[t][p];
+        vr = fmaf(c.x, v.x, fmaf(-c.y, v.y, vr));
+        vi = fmaf(c.x, v.y, fmaf(c.y, v.x, vi));
+      }
+      float ps, pc;                                   // e^{-j 2 pi m' u_c,it}
+      sincospif(2.f * frac_cycles(mc * uc[t]), &ps, &pc);
+      re += fmaf(pc, vr, ps * vi);
+      im += fmaf(pc, vi, -ps * vr);
+    }
+    out[i * a.n_f + m] = make_float2(re, im);
+  }
+}
+
+template <int P, bool MONO>
+constexpr int tile_fwd_minb() { return (MONO && P <= 28) || P <= 16 ? 5 : (P <= 32 ? 4 : 3); }
+template <bool MONO>
+static void tile_fwd_all(const TileArgs &a, dim3 g, cudaStream_t st) {
+  // P = 16: four records per step at 4 CTAs / SM (r02m: 64.7 ms at c3 against 68.3 ms for two
+  // records at 5 CTAs / SM); RFR_TFWD_MINB=5 selects the latter (A/B)
+  static int two = -1;
+  if (two < 0) { const char *e = getenv("RFR_TFWD_MINB"); two = (e && e[0] == '5') ? 1 : 0; }
+  if (two) k_tile_fwd<16, MONO, tile_fwd_minb<16, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+  else k_tile_fwd<16, MONO, 4, true><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_fwd<24, MONO, tile_fwd_minb<24, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_fwd<28, MONO, tile_fwd_minb<28, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_fwd<32, MONO, tile_fwd_minb<32, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+  k_tile_fwd<48, MONO, tile_fwd_minb<48, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+}
+
+cudaError_t launch_tiled_mfadj(const TileArgs &a0, bool mono, float2 *out, cudaStream_t st) {
+  if (a0.n_a <= 0 || a0.n <= 0) return cudaSuccess;
+  TileArgs a = a0;
+  a.chunk = (int)tile_fwd_chunk(a.n);
+  cudaError_t e = tile_prepare(a, st, false);
+  if (e != cudaSuccess) return e;
+  dim3 g((unsigned)((a.n_a + kChebThreads - 1) / kChebThreads), (unsigned)tile_fwd_blocks(a.n));
+  if (mono) tile_fwd_all<true>(a, g, st);
+  else tile_fwd_all<false>(a, g, st);
+  const unsigned na = (unsigned)a.n_a;
+  k_tile_out<16><<<na, 256, 0, st>>>(a, out);
+  k_tile_out<24><<<na, 256, 0, st>>>(a, out);
+  k_tile_out<28><<<na, 256, 0, st>>>(a, out);
+  k_tile_out<32><<<na, 256, 0, st>>>(a, out);
+  k_tile_out<48><<<na, 256, 0, st>>>(a, out);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(10);
   return e;
 }
 

@@ -204,6 +204,7 @@ struct TileArgs {
   const float2 *X;                 // the signal rows [n_a][n_f]
   float2 *out;                     // M partials [split][n]
   int64_t ants_per_split;
+  float2 *fpart;                   // tiled K5: moments per (chunk CTA, antenna) [blocks][n_a][kChebPMax]
 };
 cudaError_t launch_tiled_filter(const TileArgs &t, bool mono, int n_splits, cudaStream_t st);
 // tiled backward over the compacted active samples (t.rec, t.n_dev, t.idx): partials of a
@@ -212,6 +213,12 @@ cudaError_t launch_tiled_backward(const TileArgs &t, const AdjArgs &a, bool mono
 cudaError_t launch_cheb_adj_prep_only(const ChebArgs &c, const AdjArgs &a, float2 *bmom,
                                       cudaStream_t st);
 int tile_count_blocks(int64_t n);
+// tiled K5 (the matched-filter adjoint, a forward-shaped sweep; DESIGN 6b) over the query records
+// t.rec [t.n]: tile sort, per-(antenna, tile) centres and P, moments per (tile chunk, antenna) into
+// t.fpart, then the bins of every antenna into out [n_a][n_f] (fixed-order sums throughout)
+cudaError_t launch_tiled_mfadj(const TileArgs &t, bool mono, float2 *out, cudaStream_t st);
+int64_t tile_fwd_chunk(int64_t n);        // points per CTA of the tiled K5 sweep
+int64_t tile_fwd_blocks(int64_t n);       // upper bound of its chunk CTAs (fpart rows)
 // matched filter only, four points per thread (row c.row of B); prep_nx as launch_cheb_adj
 cudaError_t launch_cheb_flt(const ChebArgs &c, const AdjArgs &a, float2 *bmom, bool mono,
                             int n_splits, cudaStream_t st, int prep_nx = 0);
