@@ -142,7 +142,7 @@ struct Layout {
          off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, off_aflag = 0,
          off_idxc = 0, off_ttile = 0, off_tbcnt = 0, off_tstart = 0, off_tperm = 0, off_tqs = 0,
          off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, off_trs = 0,
-         off_tfp = 0, total = 0;
+         off_tfp = 0, off_tgeo = 0, total = 0;
   size_t cap_trs = 0, cap_tfp = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
@@ -206,6 +206,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_trs = take(L.cap_trs);
     L.cap_tfp = (size_t)tile_fwd_blocks(n_q) * na1 * kChebPMax * 8;
     L.off_tfp = take(L.cap_tfp);
+    L.off_tgeo = take((size_t)kTiles * na1 * 32);
   }
   L.total = o;
   return true;
@@ -335,6 +336,7 @@ TileArgs make_tile(const float *qx, const float *qy, const float *qz, int64_t n,
   t.out = out;
   t.ants_per_split = ants_per_split;
   t.pub = at<int>(ws, kTilePOff);
+  t.tgeo = at<float4>(ws, L.off_tgeo);
   return t;
 }
 // the tiled filter is on unless RFR_TILE=0 (A/B)

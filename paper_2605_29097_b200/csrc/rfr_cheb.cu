@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_adj(ChebArgs c, AdjArg
   __shared__ __align__(16) float4 bs[kChebGA][P];   // (B_0[p], B_1[p]) per antenna of the stage
   __shared__ AntF as[kChebGA];
   __shared__ double ls[kChebGA];
+  __shared__ float4 gs[kChebGA][2];                 // F32G: tile-relative antenna geometry
   const int tid = threadIdx.x;
   // points: all n_s, or the compacted list of c.n_dev points (records at a.rec, original index
   // c.idx[j] for the outputs)
@@ -646,6 +647,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_cheb_flt4(ChebArgs c, AdjAr
   __shared__ __align__(16) float2 bs[kChebGA][P];
   __shared__ AntF as[kChebGA];
   __shared__ double ls[kChebGA];
+  __shared__ float4 gs[kChebGA][2];                 // F32G: tile-relative antenna geometry
   const int tid = threadIdx.x;
   const int64_t jb = (int64_t)blockIdx.x * (SPT * kChebThreads) + tid;
   if ((int64_t)blockIdx.x * (SPT * kChebThreads) >= a.n_s) return;
@@ -864,6 +866,11 @@ __global__ void k_tile_box(TileArgs a) {
   if (threadIdx.x < 6) a.tbox[t * 6 + threadIdx.x] = sh[threadIdx.x][0];
 }
 
+// fp32 centre of a tile's box (the same rounding wherever it is evaluated)
+__device__ __forceinline__ float tile_centre(const double *b, int c) {
+  return (float)(0.5 * (b[c] + b[3 + c]));
+}
+
 // per (antenna, tile): centre path length; max half-spread over everything (fp64 bits, atomicMax:
 // order-independent)
 __global__ void k_tile_setup(TileArgs a) {
@@ -878,8 +885,23 @@ __global__ void k_tile_setup(TileArgs a) {
       box_dist(b, a.tx_x[i], a.tx_y[i], a.tx_z[i], tmin, tmax);
       if (a.rx_x) box_dist(b, a.rx_x[i], a.rx_y[i], a.rx_z[i], rmin, rmax);
       else { rmin = tmin; rmax = tmax; }
-      a.lc[(int64_t)t * a.n_a + i] = 0.5 * (tmin + rmin + tmax + rmax);
+      const double Lc = 0.5 * (tmin + rmin + tmax + rmax);
+      a.lc[(int64_t)t * a.n_a + i] = Lc;
       dm = fmax(dm, 0.5 * (tmax + rmax - tmin - rmin));
+      if (!a.rx_x) {
+        // monostatic tile-relative geometry around the fp32 tile centre c_t: a' = a - c_t,
+        // D = |a'|^2, d_a = sqrt(D); per pair d - d_a = delta / (d + d_a) with
+        // delta = |q'|^2 - 2 a'.q' in fp32 (k_tile_flt4 F32G)
+        double ap[3];
+        const double av[3] = {a.tx_x[i], a.tx_y[i], a.tx_z[i]};
+        for (int c = 0; c < 3; ++c) ap[c] = av[c] - (double)tile_centre(b, c);
+        const double D = ap[0] * ap[0] + ap[1] * ap[1] + ap[2] * ap[2];
+        const double da = sqrt(D);
+        float4 *g = a.tgeo + ((int64_t)t * a.n_a + i) * 2;
+        g[0] = make_float4((float)(-2.0 * ap[0]), (float)(-2.0 * ap[1]), (float)(-2.0 * ap[2]),
+                           (float)D);
+        g[1] = make_float4((float)da, frac_cycles(2.0 * da * a.kc), (float)(2.0 * da - Lc), 0.f);
+      }
     }
   }
   __shared__ double red[256];
@@ -948,7 +970,7 @@ __global__ void __launch_bounds__(kAdjPrepThreads) k_tile_bprep(TileArgs a) {
 }
 
 // the filter over the sorted points: CTA -> (tile, chunk of kTileChunk points), 4 per thread
-template <int P, bool MONO>
+template <int P, bool MONO, bool F32G = false>
 __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(TileArgs a) {
   if (a.hdr->P != P) return;
   constexpr int SPT = 4;
@@ -961,6 +983,7 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
   __shared__ __align__(16) float2 bs[kChebGA][P];
   __shared__ AntD as[kChebGA];                      // widened once per stage
   __shared__ double ls[kChebGA];
+  __shared__ float4 gs[kChebGA][2];                 // F32G: tile-relative antenna geometry
   const int tid = threadIdx.x;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
@@ -974,7 +997,21 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
     q[u].x = v.x; q[u].y = v.y; q[u].z = v.z;
     q[u].w = 0.f; q[u].T = 1.f; q[u].nx = q[u].ny = 0.f; q[u].nz = 1.f; q[u].papr = 1.f;
   }
+  // F32G: the points relative to the tile centre (fp32) and |q'|^2
+  float qp[SPT][4];
+  if (F32G) {
+    const double *tb = a.tbox + t * 6;
+    const float cx = tile_centre(tb, 0), cy = tile_centre(tb, 1), cz = tile_centre(tb, 2);
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      qp[u][0] = (float)(q[u].x - (double)cx);
+      qp[u][1] = (float)(q[u].y - (double)cy);
+      qp[u][2] = (float)(q[u].z - (double)cz);
+      qp[u][3] = fmaf(qp[u][0], qp[u][0], fmaf(qp[u][1], qp[u][1], qp[u][2] * qp[u][2]));
+    }
+  }
   const double inv = a.hdr->inv;
+  const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * inv);
   // monostatic: L = 2 d, so the cycle count is d (2 kc) and x = d (2 inv) - L_c inv (one DFMA)
   const double kc2 = 2.0 * a.kc, inv2 = 2.0 * inv;
   float M1[SPT], M2[SPT];
@@ -997,6 +1034,13 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
       f.ptx = f.prx = 1.f;
       as[tid] = widen_ant<MONO>(f);
       ls[tid] = a.lc[(int64_t)t * a.n_a + ia] * (MONO ? inv : 1.0);   // L_c inv (mono) or L_c
+      if (F32G) {
+        const float4 *g = a.tgeo + ((int64_t)t * a.n_a + ia) * 2;
+        float4 g1 = g[1];
+        g1.z = (float)((double)g1.z * inv);          // x at the antenna's tile distance d_a
+        gs[tid][0] = g[0];
+        gs[tid][1] = g1;
+      }
     }
     __syncthreads();
 #pragma unroll 1
@@ -1005,6 +1049,23 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
       float ec[SPT], es[SPT], xv[SPT], sg[SPT];
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
+        if (F32G) {
+          // d - d_a = delta / (d + d_a), delta = |q'|^2 - 2 a'.q' (fp32, all terms small);
+          // cycles = frac(2 d_a kc) + 2 kc (d - d_a), x = (2 d_a - L_c) inv + 2 inv (d - d_a)
+          const float4 g0 = gs[aa][0], g1 = gs[aa][1];
+          const float del = fmaf(g0.x, qp[u][0], fmaf(g0.y, qp[u][1], fmaf(g0.z, qp[u][2], qp[u][3])));
+          const float s2 = g0.w + del;
+          const float dd = s2 * rsqrtf(s2);
+          const float dl = __fdividef(del, dd + g1.x);
+          float cy = fmaf(dl, kc2f, g1.y);
+          cy -= rintf(cy);
+          __sincosf(kTwoPi * cy, &es[u], &ec[u]);
+          float x = fmaf(dl, inv2f, g1.z);
+          x = fminf(fmaxf(x, -1.f), 1.f);
+          xv[u] = fabsf(x) - 1.f;
+          sg[u] = x < 0.f ? -1.f : 1.f;
+          continue;
+        }
         double cyc, xd;
         if (MONO) {
           const double dx = q[u].x - an.x, dy = q[u].y - an.y, dz = q[u].z - an.z;
@@ -1068,9 +1129,15 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
     if (valid[u]) out[a.perm[base + tid + u * kChebThreads]] = make_float2(M1[u], M2[u]);
 }
 
+static bool tile_f32g() {           // RFR_F32G=0: the fp64 per-pair geometry (A/B)
+  static int v = -1;
+  if (v < 0) { const char *e = getenv("RFR_F32G"); v = (e && e[0] == '0') ? 0 : 1; }
+  return v == 1;
+}
 template <bool MONO>
 static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
-  k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
+  if (MONO && tile_f32g()) k_tile_flt4<16, MONO, true><<<g, kChebThreads, 0, st>>>(a);
+  else k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<24, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<28, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<32, MONO><<<g, kChebThreads, 0, st>>>(a);
@@ -1367,6 +1434,7 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_bwd(TileArgs ta, AdjAr
   __shared__ __align__(16) float2 bs[kChebGA][P];
   __shared__ AntF as[kChebGA];
   __shared__ double ls[kChebGA];
+  __shared__ float4 gs[kChebGA][2];                 // F32G: tile-relative antenna geometry
   const int tid = threadIdx.x;
   const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);

@@ -205,6 +205,7 @@ struct TileArgs {
   float2 *out;                     // M partials [split][n]
   int64_t ants_per_split;
   float2 *fpart;                   // tiled K5: moments per (chunk CTA, antenna) [blocks][n_a][kChebPMax]
+  float4 *tgeo;                    // monostatic tile-relative geometry [kTiles][n_a][2] (k_tile_setup)
 };
 cudaError_t launch_tiled_filter(const TileArgs &t, bool mono, int n_splits, cudaStream_t st);
 // tiled backward over the compacted active samples (t.rec, t.n_dev, t.idx): partials of a
