@@ -1192,7 +1192,7 @@ int64_t tile_fwd_blocks(int64_t n) {
   return n > 0 ? (n + tile_fwd_chunk(n) - 1) / tile_fwd_chunk(n) + kTiles : 0;
 }
 
-template <int P, bool MONO, int MINB, bool QUAD = false>
+template <int P, bool MONO, int MINB, bool QUAD = false, bool F32G = false>
 __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
   if (a.hdr->P != P) return;
   const int blk = blockIdx.y;
@@ -1212,6 +1212,22 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
   const double Lc = ant_ok ? a.lc[(int64_t)t * a.n_a + ia] : 0.0;
   const double inv = a.hdr->inv;
   const double kc2 = 2.0 * a.kc, inv2 = 2.0 * inv, lsi = Lc * inv;
+  // F32G (monostatic): tile-relative fp32 geometry as k_tile_flt4 (DESIGN 5d); the records'
+  // q' = q - c_t and |q'|^2 once per staged record
+  __shared__ float4 qf[kChebTJ];
+  float4 g0 = make_float4(0.f, 0.f, 0.f, 1.f), g1 = make_float4(1.f, 0.f, 0.f, 0.f);
+  float ctx = 0.f, cty = 0.f, ctz = 0.f;
+  const float kc2f = (float)kc2, inv2f = (float)inv2;
+  if (F32G) {
+    const double *tb = a.tbox + t * 6;
+    ctx = tile_centre(tb, 0); cty = tile_centre(tb, 1); ctz = tile_centre(tb, 2);
+    if (ant_ok) {
+      const float4 *g = a.tgeo + ((int64_t)t * a.n_a + ia) * 2;
+      g0 = g[0];
+      g1 = g[1];
+      g1.z = (float)((double)g1.z * inv);
+    }
+  }
   f2x M[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) M[p] = 0ull;
@@ -1230,13 +1246,39 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
   for (int64_t jt = j_lo; jt < j_hi; jt += kChebTJ, b ^= 1) {
     cp_async_wait_all();
     __syncthreads();
+    if (F32G) {
+      if (tid < kChebTJ) {
+        const Rec &r = rb[b][tid];
+        const float x = (float)r.x - ctx, y = (float)r.y - cty, z = (float)r.z - ctz;
+        qf[tid] = make_float4(x, y, z, fmaf(x, x, fmaf(y, y, z * z)));
+      }
+      __syncthreads();
+    }
     if (jt + kChebTJ < j_hi) prefetch(jt + kChebTJ, b ^ 1);
     const int nv = (int)min((int64_t)kChebTJ, j_hi - jt);
 #pragma unroll 1
     for (int jj = 0; jj < nv; jj += (MONO && P <= 16 && QUAD) ? 4 : 2) {
       f2x cc0 = 0ull, co0 = 0ull, cc1 = 0ull, co1 = 0ull;
       float xv0 = 0.f, xv1 = 0.f;
-      auto geom = [&](const Rec &rec, f2x &c, f2x &cn, float &xv) {
+      auto geom = [&](int k, f2x &c, f2x &cn, float &xv) {
+        const Rec &rec = rb[b][k];
+        if (F32G) {        // d - d_a = delta / (d + d_a), delta = |q'|^2 - 2 a'.q'
+          const float4 qv = qf[k];
+          const float del = fmaf(g0.x, qv.x, fmaf(g0.y, qv.y, fmaf(g0.z, qv.z, qv.w)));
+          const float s2 = g0.w + del;
+          const float dl = __fdividef(del, s2 * rsqrtf(s2) + g1.x);
+          float cy = fmaf(dl, kc2f, g1.y);
+          cy -= rintf(cy);
+          float es, ec;
+          __sincosf(kTwoPi * cy, &es, &ec);
+          const float Ar = rec.w, Ai = rec.T;
+          c = pk(fmaf(Ar, ec, Ai * es), fmaf(Ai, ec, -Ar * es));
+          float x = fmaf(dl, inv2f, g1.z);
+          x = fminf(fmaxf(x, -1.f), 1.f);
+          cn = x < 0.f ? pk(-upk(c).x, -upk(c).y) : c;
+          xv = fabsf(x) - 1.f;
+          return;
+        }
         double cyc, xd;
         if (MONO) {      // L = 2 d: cycles d (2 kc), x = d (2 inv) - L_c inv (as k_tile_flt4)
           const double dx = rec.x - an.x, dy = rec.y - an.y, dz = rec.z - an.z;
@@ -1260,10 +1302,10 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
       if (MONO && P <= 16 && QUAD) {   // four records per step: two packed recurrences
         f2x cc2, co2, cc3, co3;
         float xv2, xv3;
-        geom(rb[b][jj], cc0, co0, xv0);
-        geom(rb[b][jj + 1], cc1, co1, xv1);
-        geom(rb[b][jj + 2], cc2, co2, xv2);
-        geom(rb[b][jj + 3], cc3, co3, xv3);
+        geom(jj, cc0, co0, xv0);
+        geom(jj + 1, cc1, co1, xv1);
+        geom(jj + 2, cc2, co2, xv2);
+        geom(jj + 3, cc3, co3, xv3);
         const f2x two01 = pk(2.f * xv0, 2.f * xv1), two23 = pk(2.f * xv2, 2.f * xv3);
         f2x d01 = pk(xv0, xv1), d23 = pk(xv2, xv3);
         acc2(M[0], cc0);
@@ -1293,14 +1335,14 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
         continue;
       }
       if (MONO && P <= 16) {     // both geometries in flight (ILP; no spills at this size)
-        geom(rb[b][jj], cc0, co0, xv0);
-        geom(rb[b][jj + 1], cc1, co1, xv1);
+        geom(jj, cc0, co0, xv0);
+        geom(jj + 1, cc1, co1, xv1);
       } else {
 #pragma unroll 1
         for (int u = 0; u < 2; ++u) {
           f2x c, cn;
           float xv;
-          geom(rb[b][jj + u], c, cn, xv);
+          geom(jj + u, c, cn, xv);
           if (u == 0) { cc0 = c; co0 = cn; xv0 = xv; }
           else { cc1 = c; co1 = cn; xv1 = xv; }
         }
@@ -1393,6 +1435,7 @@ static void tile_fwd_all(const TileArgs &a, dim3 g, cudaStream_t st) {
   static int two = -1;
   if (two < 0) { const char *e = getenv("RFR_TFWD_MINB"); two = (e && e[0] == '5') ? 1 : 0; }
   if (two) k_tile_fwd<16, MONO, tile_fwd_minb<16, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+  else if (MONO && tile_f32g()) k_tile_fwd<16, MONO, 4, true, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_fwd<16, MONO, 4, true><<<g, kChebThreads, 0, st>>>(a);
   k_tile_fwd<24, MONO, tile_fwd_minb<24, MONO>()><<<g, kChebThreads, 0, st>>>(a);
   k_tile_fwd<28, MONO, tile_fwd_minb<28, MONO>()><<<g, kChebThreads, 0, st>>>(a);
