@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(kAdjPrepThreads) k_tile_bprep(TileArgs a) {
 }
 
 // the filter over the sorted points: CTA -> (tile, chunk of kTileChunk points), 4 per thread
-template <int P, bool MONO, bool F32G = false>
+template <int P, bool MONO, bool F32G = false, bool STD = false>
 __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(TileArgs a) {
   if (a.hdr->P != P) return;
   constexpr int SPT = 4;
@@ -1023,7 +1023,9 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
     __syncthreads();
     for (int w = tid; w < ga * P; w += kChebThreads) {
       const int aa = w / P, p = w % P;
-      bs[aa][p] = a.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+      float2 v = a.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+      if (STD && ((p >> 1) & 1)) { v.x = -v.x; v.y = -v.y; }   // B'_p = s_p B_p, s = (+ + - -)
+      bs[aa][p] = v;
     }
     if (tid < ga) {
       AntF f;
@@ -1062,7 +1064,7 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
           __sincosf(kTwoPi * cy, &es[u], &ec[u]);
           float x = fmaf(dl, inv2f, g1.z);
           x = fminf(fmaxf(x, -1.f), 1.f);
-          xv[u] = fabsf(x) - 1.f;
+          xv[u] = STD ? x : fabsf(x) - 1.f;
           sg[u] = x < 0.f ? -1.f : 1.f;
           continue;
         }
@@ -1084,6 +1086,43 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
         sg[u] = x < 0.f ? -1.f : 1.f;
       }
       const float2 *B = bs[aa];
+      if (STD) {
+        // plain three-term recurrence on v_p = s_p T_p(x), s = (+ + - -) repeating, so that
+        // v_p = (-1)^(p+1) 2x v_{p-1} + v_{p-2} is one FFMA2 per two points (P <= 16: the
+        // recurrence's ~p^2 u error stays < 2e-5); h = sum_p v_p B'_p, B'_p = s_p B_p
+        const f2x x01 = pk(xv[0], xv[1]), x23 = pk(xv[2], xv[3]);
+        const f2x tp01 = pk(2.f * xv[0], 2.f * xv[1]), tp23 = pk(2.f * xv[2], 2.f * xv[3]);
+        const f2x tn01 = pk(-2.f * xv[0], -2.f * xv[1]), tn23 = pk(-2.f * xv[2], -2.f * xv[3]);
+        f2x h[SPT];
+        const float2 b0 = B[0], b1 = B[1];
+        const f2x pb0 = pk(b0.x, b0.y), pb1 = pk(b1.x, b1.y);
+        h[0] = ffma2(pk(xv[0], xv[0]), pb1, pb0);
+        h[1] = ffma2(pk(xv[1], xv[1]), pb1, pb0);
+        h[2] = ffma2(pk(xv[2], xv[2]), pb1, pb0);
+        h[3] = ffma2(pk(xv[3], xv[3]), pb1, pb0);
+        f2x v2_01 = pk(1.f, 1.f), v2_23 = pk(1.f, 1.f), v1_01 = x01, v1_23 = x23;
+#pragma unroll
+        for (int p = 2; p < P; ++p) {
+          const f2x v01 = ffma2((p & 1) ? tp01 : tn01, v1_01, v2_01);
+          const f2x v23 = ffma2((p & 1) ? tp23 : tn23, v1_23, v2_23);
+          v2_01 = v1_01; v1_01 = v01;
+          v2_23 = v1_23; v1_23 = v23;
+          const float2 b = B[p];
+          const f2x pb = pk(b.x, b.y);
+          const float2 w01 = upk(v01), w23 = upk(v23);
+          h[0] = ffma2(pk(w01.x, w01.x), pb, h[0]);
+          h[1] = ffma2(pk(w01.y, w01.y), pb, h[1]);
+          h[2] = ffma2(pk(w23.x, w23.x), pb, h[2]);
+          h[3] = ffma2(pk(w23.y, w23.y), pb, h[3]);
+        }
+        PairBwd g;
+#pragma unroll
+        for (int u = 0; u < SPT; ++u) {
+          const float2 hh = upk(h[u]);
+          adj_accumulate<kModeFlt>(g, ec[u], es[u], hh.x, hh.y, M1[u], M2[u], d0, d1, d2);
+        }
+        continue;
+      }
       f2x he[SPT], ho[SPT];
       const float2 b0 = B[0];
 #pragma unroll
@@ -1136,7 +1175,10 @@ static bool tile_f32g() {           // RFR_F32G=0: the fp64 per-pair geometry (A
 }
 template <bool MONO>
 static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
-  if (MONO && tile_f32g()) k_tile_flt4<16, MONO, true><<<g, kChebThreads, 0, st>>>(a);
+  static int stdrec = -1;            // RFR_STDREC=0: Reinsch recurrence in the P = 16 filter (A/B)
+  if (stdrec < 0) { const char *e = getenv("RFR_STDREC"); stdrec = (e && e[0] == '0') ? 0 : 1; }
+  if (MONO && tile_f32g() && stdrec) k_tile_flt4<16, MONO, true, true><<<g, kChebThreads, 0, st>>>(a);
+  else if (MONO && tile_f32g()) k_tile_flt4<16, MONO, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<24, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<28, MONO><<<g, kChebThreads, 0, st>>>(a);
