@@ -1168,6 +1168,11 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
     if (valid[u]) out[a.perm[base + tid + u * kChebThreads]] = make_float2(M1[u], M2[u]);
 }
 
+static bool tile_stdrec() {         // RFR_STDREC=0: the Reinsch recurrence at P = 16 too (A/B)
+  static int v = -1;
+  if (v < 0) { const char *e = getenv("RFR_STDREC"); v = (e && e[0] == '0') ? 0 : 1; }
+  return v == 1;
+}
 static bool tile_f32g() {           // RFR_F32G=0: the fp64 per-pair geometry (A/B)
   static int v = -1;
   if (v < 0) { const char *e = getenv("RFR_F32G"); v = (e && e[0] == '0') ? 0 : 1; }
@@ -1175,9 +1180,7 @@ static bool tile_f32g() {           // RFR_F32G=0: the fp64 per-pair geometry (A
 }
 template <bool MONO>
 static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
-  static int stdrec = -1;            // RFR_STDREC=0: Reinsch recurrence in the P = 16 filter (A/B)
-  if (stdrec < 0) { const char *e = getenv("RFR_STDREC"); stdrec = (e && e[0] == '0') ? 0 : 1; }
-  if (MONO && tile_f32g() && stdrec) k_tile_flt4<16, MONO, true, true><<<g, kChebThreads, 0, st>>>(a);
+  if (MONO && tile_f32g() && tile_stdrec()) k_tile_flt4<16, MONO, true, true><<<g, kChebThreads, 0, st>>>(a);
   else if (MONO && tile_f32g()) k_tile_flt4<16, MONO, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<24, MONO><<<g, kChebThreads, 0, st>>>(a);
@@ -1507,7 +1510,7 @@ cudaError_t launch_tiled_mfadj(const TileArgs &a0, bool mono, float2 *out, cudaS
 // ------------------------------------------------- tiled backward (compacted active samples)
 // As k_cheb_adj (kModeBwd, two samples per thread) over the tile-sorted compacted records, with
 // the per-(antenna, tile) centres and moments of G; partials at the original sample index.
-template <int P, bool MONO, bool CORR>
+template <int P, bool MONO, bool CORR, bool STD = false>
 __global__ void __launch_bounds__(kChebThreads, 4) k_tile_bwd(TileArgs ta, AdjArgs a) {
   if (ta.hdr->P != P) return;
   const int blk = blockIdx.x;
@@ -1543,7 +1546,9 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_bwd(TileArgs ta, AdjAr
     __syncthreads();
     for (int w = tid; w < ga * P; w += kChebThreads) {
       const int aa = w / P, p = w % P;
-      bs[aa][p] = ta.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+      float2 v = ta.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+      if (STD && ((p >> 1) & 1)) { v.x = -v.x; v.y = -v.y; }   // B'_p = s_p B_p (k_tile_flt4)
+      bs[aa][p] = v;
     }
     if (tid < ga) {
       as[tid] = load_antf<MONO>(a, i0 + tid);
@@ -1563,10 +1568,34 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_bwd(TileArgs ta, AdjAr
         __sincosf(kTwoPi * frac_cycles(L * ta.kc), &es[u], &ec[u]);
         float x = (float)((L - ls[aa]) * inv);
         x = fminf(fmaxf(x, -1.f), 1.f);
-        xv[u] = fabsf(x) - 1.f;
+        xv[u] = STD ? x : fabsf(x) - 1.f;
         sg[u] = x < 0.f ? -1.f : 1.f;
       }
       const float2 *B = bs[aa];
+      if (STD) {           // plain three-term recurrence on v_p = s_p T_p(x), as k_tile_flt4
+        const f2x tp = pk(2.f * xv[0], 2.f * xv[1]), tn = pk(-2.f * xv[0], -2.f * xv[1]);
+        const float2 b0 = B[0], b1 = B[1];
+        const f2x pb0 = pk(b0.x, b0.y), pb1 = pk(b1.x, b1.y);
+        f2x h0v = ffma2(pk(xv[0], xv[0]), pb1, pb0), h1v = ffma2(pk(xv[1], xv[1]), pb1, pb0);
+        f2x v2 = pk(1.f, 1.f), v1 = pk(xv[0], xv[1]);
+#pragma unroll
+        for (int p = 2; p < P; ++p) {
+          const f2x v = ffma2((p & 1) ? tp : tn, v1, v2);
+          v2 = v1;
+          v1 = v;
+          const float2 b = B[p];
+          const f2x pb = pk(b.x, b.y);
+          const float2 w = upk(v);
+          h0v = ffma2(pk(w.x, w.x), pb, h0v);
+          h1v = ffma2(pk(w.y, w.y), pb, h1v);
+        }
+        const float2 h0 = upk(h0v), h1 = upk(h1v);
+        adj_accumulate<kModeBwd>(g[0], ec[0], es[0], h0.x, h0.y, S1[0], S2[0], S3x[0], S3y[0],
+                                 S3z[0]);
+        adj_accumulate<kModeBwd>(g[1], ec[1], es[1], h1.x, h1.y, S1[1], S2[1], S3x[1], S3y[1],
+                                 S3z[1]);
+        continue;
+      }
       const float2 b0 = B[0];
       f2x he0 = pk(b0.x, b0.y), he1 = he0, ho0 = 0ull, ho1 = 0ull;
       const f2x two_xm1 = pk(2.f * xv[0], 2.f * xv[1]);
@@ -1612,7 +1641,8 @@ __global__ void __launch_bounds__(kChebThreads, 4) k_tile_bwd(TileArgs ta, AdjAr
 
 template <bool MONO, bool CORR>
 static void tile_bwd_all(const TileArgs &ta, const AdjArgs &a, dim3 g, cudaStream_t st) {
-  k_tile_bwd<16, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
+  if (tile_stdrec()) k_tile_bwd<16, MONO, CORR, true><<<g, kChebThreads, 0, st>>>(ta, a);
+  else k_tile_bwd<16, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
   k_tile_bwd<24, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
   k_tile_bwd<28, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
   k_tile_bwd<32, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
