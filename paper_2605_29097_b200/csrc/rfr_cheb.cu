@@ -1237,7 +1237,7 @@ int64_t tile_fwd_blocks(int64_t n) {
   return n > 0 ? (n + tile_fwd_chunk(n) - 1) / tile_fwd_chunk(n) + kTiles : 0;
 }
 
-template <int P, bool MONO, int MINB, bool QUAD = false, bool F32G = false>
+template <int P, bool MONO, int MINB, bool QUAD = false, bool F32G = false, bool STD = false>
 __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
   if (a.hdr->P != P) return;
   const int blk = blockIdx.y;
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
           float x = fmaf(dl, inv2f, g1.z);
           x = fminf(fmaxf(x, -1.f), 1.f);
           cn = x < 0.f ? pk(-upk(c).x, -upk(c).y) : c;
-          xv = fabsf(x) - 1.f;
+          xv = STD ? x : fabsf(x) - 1.f;
           return;
         }
         double cyc, xd;
@@ -1351,6 +1351,32 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
         geom(jj + 1, cc1, co1, xv1);
         geom(jj + 2, cc2, co2, xv2);
         geom(jj + 3, cc3, co3, xv3);
+        if (STD) {       // plain recurrence on v_p = s_p T_p(x) (k_tile_flt4); M'[p] = s_p M[p]
+          const f2x tp01 = pk(2.f * xv0, 2.f * xv1), tp23 = pk(2.f * xv2, 2.f * xv3);
+          const f2x tn01 = pk(-2.f * xv0, -2.f * xv1), tn23 = pk(-2.f * xv2, -2.f * xv3);
+          acc2(M[0], cc0);
+          acc2(M[0], cc1);
+          acc2(M[0], cc2);
+          acc2(M[0], cc3);
+          M[1] = ffma2(pk(xv0, xv0), cc0, M[1]);
+          M[1] = ffma2(pk(xv1, xv1), cc1, M[1]);
+          M[1] = ffma2(pk(xv2, xv2), cc2, M[1]);
+          M[1] = ffma2(pk(xv3, xv3), cc3, M[1]);
+          f2x v2_01 = pk(1.f, 1.f), v2_23 = pk(1.f, 1.f), v1_01 = pk(xv0, xv1), v1_23 = pk(xv2, xv3);
+#pragma unroll
+          for (int p = 2; p < P; ++p) {
+            const f2x v01 = ffma2((p & 1) ? tp01 : tn01, v1_01, v2_01);
+            const f2x v23 = ffma2((p & 1) ? tp23 : tn23, v1_23, v2_23);
+            v2_01 = v1_01; v1_01 = v01;
+            v2_23 = v1_23; v1_23 = v23;
+            const float2 w01 = upk(v01), w23 = upk(v23);
+            M[p] = ffma2(pk(w01.x, w01.x), cc0, M[p]);
+            M[p] = ffma2(pk(w01.y, w01.y), cc1, M[p]);
+            M[p] = ffma2(pk(w23.x, w23.x), cc2, M[p]);
+            M[p] = ffma2(pk(w23.y, w23.y), cc3, M[p]);
+          }
+          continue;
+        }
         const f2x two01 = pk(2.f * xv0, 2.f * xv1), two23 = pk(2.f * xv2, 2.f * xv3);
         f2x d01 = pk(xv0, xv1), d23 = pk(xv2, xv3);
         acc2(M[0], cc0);
@@ -1417,7 +1443,11 @@ __global__ void __launch_bounds__(kChebThreads, MINB) k_tile_fwd(TileArgs a) {
   if (ant_ok) {
     float2 *dst = a.fpart + ((int64_t)blk * a.n_a + ia) * kChebPMax;
 #pragma unroll
-    for (int p = 0; p < P; ++p) dst[p] = upk(M[p]);
+    for (int p = 0; p < P; ++p) {
+      float2 v = upk(M[p]);
+      if (STD && ((p >> 1) & 1)) { v.x = -v.x; v.y = -v.y; }   // M[p] = s_p M'[p]
+      dst[p] = v;
+    }
   }
 }
 
@@ -1480,6 +1510,8 @@ static void tile_fwd_all(const TileArgs &a, dim3 g, cudaStream_t st) {
   static int two = -1;
   if (two < 0) { const char *e = getenv("RFR_TFWD_MINB"); two = (e && e[0] == '5') ? 1 : 0; }
   if (two) k_tile_fwd<16, MONO, tile_fwd_minb<16, MONO>()><<<g, kChebThreads, 0, st>>>(a);
+  else if (MONO && tile_f32g() && tile_stdrec())
+    k_tile_fwd<16, MONO, 4, true, true, true><<<g, kChebThreads, 0, st>>>(a);
   else if (MONO && tile_f32g()) k_tile_fwd<16, MONO, 4, true, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_fwd<16, MONO, 4, true><<<g, kChebThreads, 0, st>>>(a);
   k_tile_fwd<24, MONO, tile_fwd_minb<24, MONO>()><<<g, kChebThreads, 0, st>>>(a);
