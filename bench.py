@@ -382,38 +382,46 @@ def run_gpu(args):
                       "frac": ach / peak_ops,
                       "frac_at_measured_clock": ach / (peak_ops * clk_ratio) if clk_ratio else None,
                       "ms_per_step": per_step(f_ms)})
+    tiled = os.environ.get("RFR_TILE") != "0"
+
+    def lops(P):
+        # FP32 lane-ops per (point, antenna) pair of one tiled Chebyshev sweep: per moment one
+        # complex-real FFMA2 (2) + the recurrence: plain three-term at P <= 16 (1, DESIGN 5d),
+        # Reinsch otherwise (2)
+        return (3 if (P <= 16 and os.environ.get("RFR_STDREC") != "0") else 4) * P
+
     if cheb_adj_P:
-        # Chebyshev-moment adjoint: per pair P steps of 1 FFMA + 1 FADD + one FFMA2 per X row
-        # (two in the fused sweep) = (2 + 2 nx) P FP32 lane-ops
-        # per pair 4 P lane-ops: the filter over every sample (with the tiled filter's own P,
-        # section 5d) and the backward over the samples with alpha != 0 (section 5c)
-        p_flt = ca.get("P_tiled_filter") or cheb_adj_P
-        ops = 4 * cheb_adj_P
-        work = n_pairs * ((p_flt / cheb_adj_P + act_bwd) if fused else act_bwd)
-        for name, ms in ([("k_cheb_adj (filter + backward, rfr_backward_filter)", b_ms)]
-                         if fused else [("k_cheb_adj (backward, rfr_backward)", b_ms)]):
+        # fused call: the tiled filter over every pair + the tiled backward over the pairs of the
+        # samples with alpha != 0 (section 5c), both at the tiled P published by the call
+        p_t = (ca.get("P_tiled_filter") or cheb_adj_P) if tiled else cheb_adj_P
+        ops = lops(p_t) if tiled else 4 * cheb_adj_P
+        work = n_pairs * ((1.0 + act_bwd) if fused else act_bwd)
+        for name, ms in ([("k_tile_flt4+k_tile_bwd (filter + backward, rfr_backward_filter)", b_ms)]
+                         if fused else [("k_tile_bwd (backward, rfr_backward)", b_ms)]):
             ach = ops * work / (per_step(ms) * 1e-3)
-            roofs.append({"kernel": f"k_cheb_adj<P={cheb_adj_P}> " + " ".join(name.split()[1:]),
+            roofs.append({"kernel": (f"{name.split()[0]}<P={p_t}> " if tiled else
+                                     f"k_cheb_adj<P={cheb_adj_P}> ") + " ".join(name.split()[1:]),
                           "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
                           "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
                           "lane_ops_per_pair": ops, "active_sample_fraction": act_bwd,
                           "ms_per_step": per_step(ms)})
     if p_flt_sep:
-        # tiled Chebyshev filter (section 5d) over every (sample, antenna) pair: 4 P lane-ops
-        ach = 4 * p_flt_sep * n_pairs / (per_step(q_ms) * 1e-3)
+        # tiled Chebyshev filter (section 5d) over every (sample, antenna) pair
+        ach = lops(p_flt_sep) * n_pairs / (per_step(q_ms) * 1e-3)
         roofs.append({"kernel": f"k_tile_flt4<P={p_flt_sep}> (K4, rfr_filter)", "bound": "alu",
                       "achieved": ach / 1e12, "peak": peak_ops / 1e12,
                       "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                      "lane_ops_per_pair": 4 * p_flt_sep, "ms_per_step": per_step(q_ms)})
+                      "lane_ops_per_pair": lops(p_flt_sep), "ms_per_step": per_step(q_ms)})
     if p_k5:
-        # K5 = a forward-shaped Chebyshev sweep over the queries: 4 P lane-ops
-        # per (query, antenna) pair; its segment also holds the (negligible) K7 heatmap loss
-        ach = 4 * p_k5 * n_pairs / (per_step(l_ms) * 1e-3)
-        k5 = "k_tile_fwd" if os.environ.get("RFR_TILE") != "0" else "k_cheb_fwd"
+        # K5 = a forward-shaped Chebyshev sweep over the queries, per
+        # (query, antenna) pair; its segment also holds the (negligible) K7 heatmap loss
+        o5 = lops(p_k5) if tiled else 4 * p_k5
+        ach = o5 * n_pairs / (per_step(l_ms) * 1e-3)
+        k5 = "k_tile_fwd" if tiled else "k_cheb_fwd"
         roofs.append({"kernel": f"{k5}<P={p_k5},MFAdj> (K5+K7, rfr_filter_backward)",
                       "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
                       "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                      "lane_ops_per_pair": 4 * p_k5, "ms_per_step": per_step(l_ms)})
+                      "lane_ops_per_pair": o5, "ms_per_step": per_step(l_ms)})
     if cheb_adj_P:
         pass
     elif fused:
