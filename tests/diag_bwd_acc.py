@@ -1,6 +1,6 @@
 """Accuracy diagnostic of the backward on sampled rays of a config: per-field rel-L2 against the
 oracle for the separate backward, the fused backward+filter, for several ray draws.
-  python tools/diag_bwd_acc.py --config c4 --draws 4 --rays 2"""
+  python tests/diag_bwd_acc.py --config c4 --draws 4 --rays 2"""
 import argparse
 import os
 import sys

@@ -1,7 +1,7 @@
 """Accuracy margin of the matched filter at full size (the test_filter_sampled_queries_full_size
 setting, more queries): rel-L2 of M and P against the oracle on sampled queries.  The kernel variant
 comes from the environment (RFR_STDREC=0, RFR_F32G=0, RFR_TILE=0 for the A/B).
-  python tools/diag_flt_acc.py [config] [n_queries]"""
+  python tests/diag_flt_acc.py [config] [n_queries]"""
 import os
 import sys
 
