@@ -298,8 +298,10 @@ __global__ void k_cheb_coef(const ChebHdr *__restrict__ hdr, int n_f, int pmax,
 // Thread = antenna; the CTA walks its split's samples in tiles of kChebTJ records staged in shared
 // memory (every thread reads the same record: broadcast).  KIND == kFwdMFAdj: the records are the
 // K5 query records {x, y, z, w = Re c_q, T = Im c_q} and the pair amplitude is c_q.
+template <int P, bool MONO, int KIND>
+constexpr int kFwdUnroll = (MONO && P == 28 && KIND == kFwdTrace) ? 2 : 1;
 template <int P, bool MONO, bool CORR, int KIND>
-__global__ void __launch_bounds__(kChebThreads, (MONO && P <= 28) || P <= 16 ? 5 : (P <= 32 ? 4 : 3)) k_cheb_fwd(ChebArgs a) {
+__global__ void __launch_bounds__(kChebThreads, (MONO && P == 28 && KIND == kFwdTrace) ? 3 : ((MONO && P <= 28) || P <= 16 ? 5 : (P <= 32 ? 4 : 3))) k_cheb_fwd(ChebArgs a) {
   if (a.hdr->P != P) return;                     // another P (or the direct kernel) was chosen
   __shared__ __align__(16) Rec rb[2][kChebTJ];
   const int tid = threadIdx.x;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kChebThreads, (MONO && P <= 28) || P <= 16 ? 5
     for (int jj = 0; jj < nv; jj += 2) {
       f2x cc0 = 0ull, co0 = 0ull, cc1 = 0ull, co1 = 0ull;
       float xv0 = 0.f, xv1 = 0.f;
-#pragma unroll 1
+#pragma unroll (kFwdUnroll<P, MONO, KIND>)
       for (int u = 0; u < 2; ++u) {
         const Rec rec = rb[b][jj + u];
         double L;
