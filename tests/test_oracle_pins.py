@@ -353,6 +353,115 @@ def test_p7_backward_matches_central_finite_differences():
     assert abs(fd - g["sharpness"]) <= 1e-5 * max(abs(fd), 1e-12)
 
 
+def _bistatic_phi_fd_problem():
+    """c0b's samples seen by a BISTATIC 2x2 array (rx offset from tx in all three axes) with
+    distinct Eq. 7 origin terms Phi_apr (per sample), Phi_tx, Phi_rx (per antenna): the branch of
+    O6 the monostatic, Phi-free c0b never reaches -- the S2 cross terms T_r chi_t + T_t chi_r, the
+    chi gating at both clamps (reading Q25b) and the bistatic dg/dn (Eq. 7 P:L335-341,
+    origin terms detached P:L351-352)."""
+    p = synth.make("c0b")
+    b = p.bundles[0]
+    tx = b.antennas
+    rx = np.stack([tx.tx_x + 0.015, tx.tx_y - 0.007, tx.tx_z + 0.003], -1)
+    # Phi_apr: 0.70 at sample 1 lifts T_raw above 1 there (T_1 < 1 depends on the sdf); 0.995 at
+    # sample 6 (T_6 = 0.24) pushes T_raw below 0 for the antennas with Phi_ant < 0.75
+    phi_apr = f32([0.98, 0.70, 0.93, 0.60, 0.96, 0.72, 0.995, 0.62])
+    A = mk_ants(np.stack([tx.tx_x, tx.tx_y, tx.tx_z], -1), rx=rx,
+                phi_tx=[0.97, 0.81, 0.95, 0.66], phi_rx=[0.75, 0.99, 0.84, 0.91])
+    rng = np.random.default_rng(29)
+    # normals tilted 5-30 deg off the array axis (either sign): gains mostly > 0, so the bistatic
+    # dg/dn is exercised (c0b's isotropic normals clamp most gains to 0)
+    th, ph = np.radians(rng.uniform(5, 30, 8)), rng.uniform(0, 2 * np.pi, 8)
+    sgn = np.where(rng.random(8) < 0.5, -1.0, 1.0)
+    nrm = sgn[:, None] * np.stack([np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), -np.cos(th)], -1)
+    S = b.samples.replace(phi_origin=phi_apr, nx=f32(nrm[:, 0]), ny=f32(nrm[:, 1]), nz=f32(nrm[:, 2]))
+    y = (rng.standard_normal((4, 8)) + 1j * rng.standard_normal((4, 8))) * 1e-3
+    return p, S, A, y
+
+
+def test_p7_bistatic_phi_backward_matches_central_finite_differences():
+    """P7 on the bistatic / Eq. 7-corrected branch of O6.  The case is built so that every piece
+    of that branch is exercised away from its kinks (checked below before the FD comparison):
+    pairs with the upper T clamp active on a T_j < 1 that depends on the SDF, pairs with the
+    lower clamp active, pairs where exactly one of T_t, T_r is clamped (so a T_t <-> T_r swap of
+    the S2 cross terms changes the result), and positive and clamped gains."""
+    p, S, A, y = _bistatic_phi_fd_problem()
+    s = p.sharpness
+    _, _, T = oracle.blend(S.sdf, S.n_rays, S.n_per_ray, s)
+    papr = S.phi_origin.astype(np.float64)
+    Tt = T[:, None] + (A.phi_tx.astype(np.float64)[None, :] - papr[:, None])
+    Tr = T[:, None] + (A.phi_rx.astype(np.float64)[None, :] - papr[:, None])
+    first = (np.arange(S.n) % S.n_per_ray) == 0          # T_j = 1 there, independent of sdf
+    for raw in (Tt, Tr):                                  # away from both kinks
+        assert np.min(np.abs(raw)) > 1e-3 and np.min(np.abs(raw - 1.0)) > 1e-3
+    upper_dep = ((Tt > 1) | (Tr > 1)) & ~first[:, None]
+    assert np.any(upper_dep), "upper clamp must act on a T_j that depends on the sdf"
+    assert np.any((Tt < 0) | (Tr < 0)), "lower clamp must act somewhere"
+    one_clamped = ((Tt > 0) & (Tt < 1)) != ((Tr > 0) & (Tr < 1))
+    assert np.any(one_clamped & ~first[:, None] & (T[:, None] < 1))
+    base = {f: getattr(S, f).astype(np.float64) for f in S.FIELDS}
+    F = oracle.forward(S, s, A, p.grid)
+    _, G = oracle.loss(F, y)
+    g = oracle.backward(G, S, s, A, p.grid)
+    checked = 0
+    for field in ("sdf", "refl", "nx", "ny", "nz", "power"):
+        for j in range(S.n):
+            v = base[field][j]
+            h = 1e-6 * max(abs(v), 1e-3)
+            up = dict(base)
+            up[field] = base[field].copy()
+            up[field][j] = v + h
+            dn = dict(base)
+            dn[field] = base[field].copy()
+            dn[field][j] = v - h
+            fd = (_loss64(S, s, A, p.grid, y, up) - _loss64(S, s, A, p.grid, y, dn)) / (2 * h)
+            an = g[field][j]
+            scale = max(abs(fd), abs(an), 1e-12 * 1e3)
+            assert abs(fd - an) / scale < 1e-5, (field, j, fd, an)
+            checked += abs(an) > 1e-12
+    assert checked >= 30                                   # most probes carry a real gradient
+    h = 1e-6 * s
+    Lp = 0.5 * np.sum(np.abs(oracle.forward(S, s + h, A, p.grid) - y) ** 2)
+    Lm = 0.5 * np.sum(np.abs(oracle.forward(S, s - h, A, p.grid) - y) ** 2)
+    fd = (Lp - Lm) / (2 * h)
+    assert abs(fd - g["sharpness"]) <= 1e-5 * max(abs(fd), 1e-12)
+
+
+def test_p7_bistatic_phi_fd_detects_swapped_cross_terms():
+    """Sensitivity of the pin above: the sdf gradient built from S2 with T_t <-> T_r swapped in the
+    cross terms (T_t chi_t + T_r chi_r) differs from the oracle's by far more than the FD
+    tolerance on this case, so the FD test would catch that mistake."""
+    p, S, A, y = _bistatic_phi_fd_problem()
+    s = p.sharpness
+    F = oracle.forward(S, s, A, p.grid)
+    _, G = oracle.loss(F, y)
+    part = oracle.backward_partials(G, S, s, A, p.grid)
+    # rebuild S2 with the swapped pairing from per-antenna partials of single-antenna sets
+    _, _, T = oracle.blend(S.sdf, S.n_rays, S.n_per_ray, s)
+    papr = S.phi_origin.astype(np.float64)
+    S2_swapped = np.zeros(S.n)
+    for i in range(A.n):
+        Ai = A.take([i])
+        pi_ = oracle.backward_partials(G[i:i + 1], S, s, Ai, p.grid)
+        tt = T + (float(A.phi_tx[i]) - papr)
+        tr = T + (float(A.phi_rx[i]) - papr)
+        Tt, Tr = np.clip(tt, 0, 1), np.clip(tr, 0, 1)
+        ct = (tt > 0) & ((tt < 1) | (float(A.phi_tx[i]) - papr <= 0))
+        cr = (tr > 0) & ((tr < 1) | (float(A.phi_rx[i]) - papr <= 0))
+        # pi_[:,1] = R g gamma (Tr ct + Tt cr); R g gamma = pi_[:,0] / (Tt Tr) where Tt Tr > 0
+        ok = (Tt * Tr) > 0
+        rgg = np.where(ok, pi_[:, 0] / np.where(ok, Tt * Tr, 1.0), 0.0)
+        S2_swapped += rgg * (Tt * ct + Tr * cr)
+        assert np.allclose(np.where(ok, rgg * (Tr * ct + Tt * cr), pi_[:, 1]), pi_[:, 1],
+                           rtol=1e-9, atol=1e-30)
+    part_sw = part.copy()
+    part_sw[:, 1] = S2_swapped
+    g = oracle.backward_finish(part, S, s)
+    g_sw = oracle.backward_finish(part_sw, S, s)
+    rel = np.linalg.norm(g_sw["sdf"] - g["sdf"]) / np.linalg.norm(g["sdf"])
+    assert rel > 1e-3
+
+
 def test_p8_euler_identity_for_linear_loss():
     """F is homogeneous of degree 1 in power p and in reflectivity a, so for the linear loss
     L = Re<F, G> the backward must satisfy sum_j p_j dL/dp_j = L = sum_j a_j dL/da_j."""
