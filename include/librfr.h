@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define RFR_ABI_VERSION 1
+#define RFR_ABI_VERSION 2
 
 typedef struct CUstream_st *rfr_stream_t; /* == cudaStream_t */
 
@@ -236,8 +236,11 @@ rfr_status rfr_comm_unique_id(void *id /* 128 bytes, written */);
 rfr_status rfr_comm_init(const void *id, int nranks, int rank, rfr_comm **out);
 rfr_status rfr_comm_destroy(rfr_comm *comm);
 
-/* Synchronously read (and clear) the device flags RFR_FLAG_DOMAIN / RFR_FLAG_NUMERIC. */
-rfr_status rfr_poll_flags(const rfr_workspace *ws, uint32_t *flags);
+/* Read (and clear) the device flags RFR_FLAG_DOMAIN / RFR_FLAG_NUMERIC of the calls queued on
+ * `stream` before this one: the read and the clear are ordered on that stream, then the call waits
+ * for it (host-synchronous).  A flag raised by work on another stream is seen only if that work was
+ * ordered before this call (events).  RFR_E_CUDA on a copy failure.  (ABI 2: takes the stream.) */
+rfr_status rfr_poll_flags(const rfr_workspace *ws, uint32_t *flags, rfr_stream_t stream);
 const char *rfr_status_string(rfr_status s);
 int rfr_abi_version(void);
 /* Diagnostic: number of kernels this library has launched in the process so far. */

@@ -360,7 +360,10 @@ int orc_filter_backward(const double *grad_P, const double *M, const double *P, 
     ksum_t *acc = calloc((size_t)n_freq * 2, sizeof(ksum_t));
     for (int64_t q = 0; q < n_query; ++q) {
       double den = P[q] > eps ? P[q] : eps;
-      double cr = grad_P[q] * M[2 * q] / den, ci = grad_P[q] * M[2 * q + 1] / den;  /* G_M,q */
+      /* reading Q15b: at P_q = 0 the subgradient of |M| is taken as 0, so the query adds nothing
+         (also for eps = 0, where M / max(P, eps) would be 0 / 0) */
+      double sc = P[q] > 0.0 ? grad_P[q] / den : 0.0;
+      double cr = sc * M[2 * q], ci = sc * M[2 * q + 1];                            /* G_M,q */
       double dt[3] = {qx[q] - Ant->tx_x[i], qy[q] - Ant->tx_y[i], qz[q] - Ant->tx_z[i]};
       double d_t = sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]);
       double d_r = d_t;

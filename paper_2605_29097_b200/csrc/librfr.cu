@@ -217,11 +217,16 @@ T *at(const rfr_workspace *ws, size_t off) {
   return reinterpret_cast<T *>(static_cast<char *>(ws->ptr) + off);
 }
 
-// A call's workspace: planned for at least n_s samples and n_q queries.
-rfr_status check_ws(const rfr_workspace *ws, int64_t n_s, int64_t n_q, Layout &L) {
+// A call's workspace: planned for at least n_s samples, n_q queries, n_a antennas and n_f bins
+// (every region is sized from the planning dimensions, so a call beyond any of them would write
+// past its regions).  n_a = n_f = 0: the call touches no per-antenna / per-bin region.
+rfr_status check_ws(const rfr_workspace *ws, int64_t n_s, int64_t n_q, Layout &L, int64_t n_a = 0,
+                    int32_t n_f = 0) {
   if (!ws || !ws->ptr) return RFR_E_ARG;
   if (!make_layout(ws->n_samples, ws->n_ant, ws->n_freq, ws->n_query, L)) return RFR_E_SHAPE;
-  if (ws->bytes < L.total || n_s > ws->n_samples || n_q > ws->n_query) return RFR_E_SHAPE;
+  if (ws->bytes < L.total || n_s > ws->n_samples || n_q > ws->n_query || n_a > ws->n_ant ||
+      n_f > ws->n_freq)
+    return RFR_E_SHAPE;
   return RFR_OK;
 }
 
@@ -501,7 +506,7 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
   const uint32_t flags = opts ? opts->flags : 0u;
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
   Layout L;
-  RFR_TRY(check_ws(ws, n_s, 0, L));
+  RFR_TRY(check_ws(ws, n_s, 0, L, ants->n_ant, grid->n_freq));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (ants->n_ant == 0) return RFR_OK;
   RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
@@ -535,7 +540,7 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   if (n_query < 0 || (n_query > 0 && (!qx || !qy || !qz)) || (ants->n_ant > 0 && !signal))
     return RFR_E_ARG;
   Layout L;
-  RFR_TRY(check_ws(ws, 0, n_query, L));
+  RFR_TRY(check_ws(ws, 0, n_query, L, ants->n_ant, grid->n_freq));
   if (n_query == 0) return RFR_OK;
   float *M = mf ? mf : at<float>(ws, L.off_fltm);
   const Split sp = adj_split(n_query, ants->n_ant, 2, L.cap_fltp);
@@ -619,7 +624,7 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   const uint32_t flags = opts ? opts->flags : 0u;
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
   Layout L;
-  RFR_TRY(check_ws(ws, n_s, 0, L));
+  RFR_TRY(check_ws(ws, n_s, 0, L, ants->n_ant, grid->n_freq));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (n_s == 0) return RFR_OK;
   RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
@@ -746,7 +751,7 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
   const int64_t n_s = samples->n_rays * (int64_t)samples->n_per_ray;
   if (n_s > 0 && (!partials || !mf)) return RFR_E_ARG;
   Layout L;
-  RFR_TRY(check_ws(ws, n_s, n_s, L));
+  RFR_TRY(check_ws(ws, n_s, n_s, L, ants->n_ant, grid->n_freq));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (n_s == 0) return RFR_OK;
   RFR_TRY(run_blend(samples, sharpness, flags, ws, L, st));
@@ -874,7 +879,7 @@ rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const f
     return RFR_E_ARG;
   if (ants->phi_tx || ants->phi_rx) return RFR_E_ARG;      // the filter has no transmittance
   Layout L;
-  RFR_TRY(check_ws(ws, 0, n_query, L));
+  RFR_TRY(check_ws(ws, 0, n_query, L, ants->n_ant, grid->n_freq));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (ants->n_ant == 0) return RFR_OK;
   Rec *qrec = at<Rec>(ws, L.off_qrec);
@@ -898,11 +903,14 @@ rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n
   return RFR_OK;
 }
 
-rfr_status rfr_poll_flags(const rfr_workspace *ws, uint32_t *flags) {
+rfr_status rfr_poll_flags(const rfr_workspace *ws, uint32_t *flags, rfr_stream_t stream) {
   if (!ws || !ws->ptr || !flags) return RFR_E_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // read and clear on the caller's stream, after every kernel queued there before this call
   uint32_t v = 0;
-  if (cudaMemcpy(&v, ws->ptr, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return RFR_E_CUDA;
-  if (cudaMemset(ws->ptr, 0, 4) != cudaSuccess) return RFR_E_CUDA;
+  if (cudaMemcpyAsync(&v, ws->ptr, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) return RFR_E_CUDA;
+  if (cudaMemsetAsync(ws->ptr, 0, 4, st) != cudaSuccess) return RFR_E_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return RFR_E_CUDA;
   *flags = v;
   return RFR_OK;
 }

@@ -1170,6 +1170,194 @@ __global__ void __launch_bounds__(kChebThreads, kTileFltMinBlocks) k_tile_flt4(T
     if (valid[u]) out[a.perm[base + tid + u * kChebThreads]] = make_float2(M1[u], M2[u]);
 }
 
+// ------------------------------------------------ packed tiled filter (monostatic, fp32 geometry)
+// k_tile_flt4<P, mono, F32G, STD> with every per-pair step after the moment staging in f32x2
+// instructions over point pairs (0,1) and (2,3): on sm_100a a scalar 3-register FFMA / FMUL / FADD
+// occupies the FMA pipe as long as one FFMA2 does (B300_MICROARCH "rt_SMSP = 2"), so the scalar
+// geometry and epilogue were half of the kernel's FMA-pipe time (r02w SASS: 88 FFMA2 + 84 scalar
+// FP32 per antenna and 4 points).  MUFU operands use the .ftz forms (no denormal rescaling
+// sequences), and the epilogue keeps M = A1 + j A2 with A1 = sum ec h, A2 = sum es h (two FFMA2
+// per pair instead of four FFMA).  Same arithmetic as k_tile_flt4 otherwise (DESIGN 5d).
+__device__ __forceinline__ f2x bc(float v) { return pk(v, v); }
+__device__ __forceinline__ float rsqrt_ftz(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float rcp_ftz(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ void sincos_ftz(float v, float &s, float &c) {
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(v));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(v));
+}
+__device__ __forceinline__ float rint_f(float v) {
+  float r;
+  asm("cvt.rni.f32.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+// per point pair: the tile-relative geometry of k_tile_flt4 (F32G), returning E = (cos, sin) of
+// the centre phase per point and x per point, packed
+struct PairGeo2 {
+  f2x c, s, x;
+};
+__device__ __forceinline__ PairGeo2 tile_geo2(const float4 &g0, const float4 &g1, f2x qx, f2x qy,
+                                              f2x qz, f2x qw, float kc2f, float inv2f) {
+  // delta = |q'|^2 - 2 a'.q';  d - d_a = delta / (sqrt(D + delta) + d_a)
+  const f2x del = ffma2(bc(g0.x), qx, ffma2(bc(g0.y), qy, ffma2(bc(g0.z), qz, qw)));
+  const f2x s2 = fadd2(bc(g0.w), del);
+  const float2 s2v = upk(s2);
+  const f2x dd = fmul2(s2, pk(rsqrt_ftz(s2v.x), rsqrt_ftz(s2v.y)));
+  const float2 den = upk(fadd2(dd, bc(g1.x)));
+  const f2x dl = fmul2(del, pk(rcp_ftz(den.x), rcp_ftz(den.y)));
+  // cycles = frac(2 d_a kc) + 2 kc (d - d_a), reduced to [-1/2, 1/2] (exact subtraction)
+  const f2x cy = ffma2(dl, bc(kc2f), bc(g1.y));
+  const float2 cv = upk(cy);
+  const f2x ang = fmul2(fadd2(cy, pk(-rint_f(cv.x), -rint_f(cv.y))), bc(kTwoPi));
+  const float2 av = upk(ang);
+  PairGeo2 o;
+  float s0, c0, s1, c1;
+  sincos_ftz(av.x, s0, c0);
+  sincos_ftz(av.y, s1, c1);
+  o.c = pk(c0, c1);
+  o.s = pk(s0, s1);
+  const float2 xv = upk(ffma2(dl, bc(inv2f), bc(g1.z)));
+  o.x = pk(fminf(fmaxf(xv.x, -1.f), 1.f), fminf(fmaxf(xv.y, -1.f), 1.f));
+  return o;
+}
+
+// PIPE: the next antenna's geometry (MUFU chains) is issued ahead of the current antenna's moment
+// loop, so its latency hides under the FFMA2 stream of the same warp
+template <int P, bool PIPE, int MINB>
+__global__ void __launch_bounds__(kChebThreads, MINB) k_tile_flt_pk(TileArgs a) {
+  if (a.hdr->P != P) return;
+  constexpr int SPT = 4;
+  const int blk = blockIdx.x;
+  if (blk >= a.cstart[kTiles]) return;
+  int t = 0;
+  while (a.cstart[t + 1] <= blk) ++t;
+  const int64_t base = a.tstart[t] + (int64_t)(blk - a.cstart[t]) * a.chunk;
+  const int64_t end = a.tstart[t + 1];
+  __shared__ __align__(16) float2 bs[kChebGA][P];
+  __shared__ float4 gs[kChebGA][2];
+  const int tid = threadIdx.x;
+  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
+  bool valid[SPT];
+  float qp[SPT][4];
+  {
+    const double *tb = a.tbox + t * 6;
+    const float cx = tile_centre(tb, 0), cy = tile_centre(tb, 1), cz = tile_centre(tb, 2);
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const int64_t k = base + tid + u * kChebThreads;
+      valid[u] = k < end;
+      const float4 v = valid[u] ? a.qs[k] : make_float4(cx, cy, cz, 0.f);
+      qp[u][0] = (float)((double)v.x - (double)cx);
+      qp[u][1] = (float)((double)v.y - (double)cy);
+      qp[u][2] = (float)((double)v.z - (double)cz);
+      qp[u][3] = fmaf(qp[u][0], qp[u][0], fmaf(qp[u][1], qp[u][1], qp[u][2] * qp[u][2]));
+    }
+  }
+  const f2x qx01 = pk(qp[0][0], qp[1][0]), qy01 = pk(qp[0][1], qp[1][1]),
+            qz01 = pk(qp[0][2], qp[1][2]), qw01 = pk(qp[0][3], qp[1][3]);
+  const f2x qx23 = pk(qp[2][0], qp[3][0]), qy23 = pk(qp[2][1], qp[3][1]),
+            qz23 = pk(qp[2][2], qp[3][2]), qw23 = pk(qp[2][3], qp[3][3]);
+  const double inv = a.hdr->inv;
+  const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * inv);
+  f2x A1[SPT], A2[SPT];                             // sum ec h, sum es h (complex, packed)
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
+  for (int64_t i0 = i_lo; i0 < i_hi; i0 += kChebGA) {
+    const int ga = (int)min((int64_t)kChebGA, i_hi - i0);
+    __syncthreads();
+    for (int w = tid; w < ga * P; w += kChebThreads) {
+      const int aa = w / P, p = w % P;
+      float2 v = a.bmom[((i0 + aa) * kTiles + t) * kChebPMax + p];
+      if ((p >> 1) & 1) { v.x = -v.x; v.y = -v.y; }   // B'_p = s_p B_p, s = (+ + - -)
+      bs[aa][p] = v;
+    }
+    if (tid < ga) {
+      const int64_t ia = i0 + tid;
+      const float4 *g = a.tgeo + ((int64_t)t * a.n_a + ia) * 2;
+      float4 g1 = g[1];
+      g1.z = (float)((double)g1.z * inv);            // x at the antenna's tile distance d_a
+      gs[tid][0] = g[0];
+      gs[tid][1] = g1;
+    }
+    __syncthreads();
+    PairGeo2 n01, n23;
+    if (PIPE) {
+      const float4 g0 = gs[0][0], g1 = gs[0][1];
+      n01 = tile_geo2(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
+      n23 = tile_geo2(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
+    }
+#pragma unroll 1
+    for (int aa = 0; aa < ga; ++aa) {
+      PairGeo2 e01, e23;
+      if (PIPE) {
+        e01 = n01;
+        e23 = n23;
+        const int an = aa + 1 < ga ? aa + 1 : aa;       // (the last one recomputes: no branch)
+        const float4 g0 = gs[an][0], g1 = gs[an][1];
+        n01 = tile_geo2(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
+        n23 = tile_geo2(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
+      } else {
+        const float4 g0 = gs[aa][0], g1 = gs[aa][1];
+        e01 = tile_geo2(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
+        e23 = tile_geo2(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
+      }
+      const float2 *B = bs[aa];
+      // v_p = s_p T_p(x): v_p = (-1)^(p+1) 2x v_{p-1} + v_{p-2}; h = sum_p v_p B'_p
+      const f2x tp01 = fadd2(e01.x, e01.x), tp23 = fadd2(e23.x, e23.x);
+      const f2x tn01 = fmul2(e01.x, bc(-2.f)), tn23 = fmul2(e23.x, bc(-2.f));
+      const float2 x01 = upk(e01.x), x23 = upk(e23.x);
+      const float2 b0 = B[0], b1 = B[1];
+      const f2x pb0 = pk(b0.x, b0.y), pb1 = pk(b1.x, b1.y);
+      f2x h[SPT];
+      h[0] = ffma2(bc(x01.x), pb1, pb0);
+      h[1] = ffma2(bc(x01.y), pb1, pb0);
+      h[2] = ffma2(bc(x23.x), pb1, pb0);
+      h[3] = ffma2(bc(x23.y), pb1, pb0);
+      f2x v2_01 = bc(1.f), v2_23 = bc(1.f), v1_01 = e01.x, v1_23 = e23.x;
+#pragma unroll
+      for (int p = 2; p < P; ++p) {
+        const f2x v01 = ffma2((p & 1) ? tp01 : tn01, v1_01, v2_01);
+        const f2x v23 = ffma2((p & 1) ? tp23 : tn23, v1_23, v2_23);
+        v2_01 = v1_01; v1_01 = v01;
+        v2_23 = v1_23; v1_23 = v23;
+        const float2 b = B[p];
+        const f2x pb = pk(b.x, b.y);
+        const float2 w01 = upk(v01), w23 = upk(v23);
+        h[0] = ffma2(bc(w01.x), pb, h[0]);
+        h[1] = ffma2(bc(w01.y), pb, h[1]);
+        h[2] = ffma2(bc(w23.x), pb, h[2]);
+        h[3] = ffma2(bc(w23.y), pb, h[3]);
+      }
+      const float2 c01 = upk(e01.c), s01 = upk(e01.s), c23 = upk(e23.c), s23 = upk(e23.s);
+      A1[0] = ffma2(bc(c01.x), h[0], A1[0]); A2[0] = ffma2(bc(s01.x), h[0], A2[0]);
+      A1[1] = ffma2(bc(c01.y), h[1], A1[1]); A2[1] = ffma2(bc(s01.y), h[1], A2[1]);
+      A1[2] = ffma2(bc(c23.x), h[2], A1[2]); A2[2] = ffma2(bc(s23.x), h[2], A2[2]);
+      A1[3] = ffma2(bc(c23.y), h[3], A1[3]); A2[3] = ffma2(bc(s23.y), h[3], A2[3]);
+    }
+  }
+  float2 *out = a.out + (int64_t)blockIdx.y * a.n;
+#pragma unroll
+  for (int u = 0; u < SPT; ++u)
+    if (valid[u]) {
+      const float2 p1 = upk(A1[u]), p2 = upk(A2[u]);   // M = A1 + j A2
+      out[a.perm[base + tid + u * kChebThreads]] = make_float2(p1.x - p2.y, p1.y + p2.x);
+    }
+}
+
+static bool tile_fltpk() {          // RFR_FLTPK=0: the scalar-geometry k_tile_flt4 (A/B)
+  static int v = -1;
+  if (v < 0) { const char *e = getenv("RFR_FLTPK"); v = (e && e[0] == '0') ? 0 : 1; }
+  return v == 1;
+}
+
 static bool tile_stdrec() {         // RFR_STDREC=0: the Reinsch recurrence at P = 16 too (A/B)
   static int v = -1;
   if (v < 0) { const char *e = getenv("RFR_STDREC"); v = (e && e[0] == '0') ? 0 : 1; }
@@ -1182,7 +1370,15 @@ static bool tile_f32g() {           // RFR_F32G=0: the fp64 per-pair geometry (A
 }
 template <bool MONO>
 static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
-  if (MONO && tile_f32g() && tile_stdrec()) k_tile_flt4<16, MONO, true, true><<<g, kChebThreads, 0, st>>>(a);
+  if (MONO && tile_f32g() && tile_stdrec() && tile_fltpk()) {
+    static int pipe = -1;
+    if (pipe < 0) { const char *e = getenv("RFR_FLTPIPE"); pipe = e ? atoi(e) : 1; }
+    if (pipe == 1) k_tile_flt_pk<16, true, 4><<<g, kChebThreads, 0, st>>>(a);
+    else if (pipe == 2) k_tile_flt_pk<16, true, 5><<<g, kChebThreads, 0, st>>>(a);
+    else k_tile_flt_pk<16, false, kTileFltMinBlocks><<<g, kChebThreads, 0, st>>>(a);
+  }
+  else if (MONO && tile_f32g() && tile_stdrec())
+    k_tile_flt4<16, MONO, true, true><<<g, kChebThreads, 0, st>>>(a);
   else if (MONO && tile_f32g()) k_tile_flt4<16, MONO, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
   k_tile_flt4<24, MONO><<<g, kChebThreads, 0, st>>>(a);

@@ -726,7 +726,9 @@ __global__ void k_mf_adj_pack(const float *__restrict__ gP, const float2 *__rest
        q += (int64_t)gridDim.x * blockDim.x) {
     const float2 m = M[q];
     const float p = P ? P[q] : sqrtf(fmaf(m.x, m.x, m.y * m.y));
-    const float sc = gP[q] / fmaxf(p, eps);
+    // subgradient of |M| at M = 0 is 0: a query with P = 0 (zero signal) adds nothing, also for
+    // eps = 0 (a 0/0 here would make every antenna's dL/ds NaN through the sum over queries)
+    const float sc = p > 0.f ? gP[q] / fmaxf(p, eps) : 0.f;
     Rec r;
     r.x = (double)qx[q]; r.y = (double)qy[q]; r.z = (double)qz[q];
     r.w = sc * m.x;

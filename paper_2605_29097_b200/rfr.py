@@ -100,7 +100,7 @@ def load(path: str = LIB_PATH):
         "rfr_backward_filter_partial": [vp, vp, S, f, A, G, O, vp, vp, W, vp],
         "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, W, vp],
         "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, W, vp],
-        "rfr_poll_flags": [W, C.POINTER(u32)],
+        "rfr_poll_flags": [W, C.POINTER(u32), C.c_void_p],
         "rfr_comm_unique_id": [vp],
         "rfr_comm_init": [vp, C.c_int, C.c_int, C.POINTER(vp)],
         "rfr_comm_destroy": [vp],
@@ -409,9 +409,9 @@ def rfr_launch_count() -> int:
     return int(load().rfr_launch_count())
 
 
-def rfr_poll_flags(ws: torch.Tensor) -> int:
+def rfr_poll_flags(ws: torch.Tensor, stream=None) -> int:
     v = C.c_uint32()
-    _check(load().rfr_poll_flags(_ws(ws), C.byref(v)), "rfr_poll_flags")
+    _check(load().rfr_poll_flags(_ws(ws), C.byref(v), _stream(stream)), "rfr_poll_flags")
     return v.value
 
 

@@ -161,8 +161,9 @@ class RenderHeatmapLoss(torch.autograd.Function):
         rfr.rfr_filter_backward(gPs, M, A, bank.grid, st.x, st.y, st.z, G, st.ws, power=P,
                                 eps=st.eps)                                      # K5
         out = rfr.Grads.empty(S.n, gP.device)
-        rfr.rfr_backward(G, S, ctx.s_val, A, bank.grid, out, st.ws,
-                         flags=st.flags | rfr.RFR_REUSE_BLEND)                    # K3, K1'
+        # K1 re-runs here (no RFR_REUSE_BLEND): another call may have used st.ws between this
+        # Function's forward and backward (a second loss term, an eval render), and K1 is cheap
+        rfr.rfr_backward(G, S, ctx.s_val, A, bank.grid, out, st.ws, flags=st.flags)  # K1, K3, K1'
         return (out.sdf, out.refl, out.nx, out.ny, out.nz, out.power,
                 out.sharpness.reshape(ctx.s_shape), None)
 

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s), s
     assert set(declared_symbols()) == set(rfr.EXPORTS)
-    assert lib.rfr_abi_version() == 1
+    assert lib.rfr_abi_version() == 2
     assert lib.rfr_status_string(2) == b"shape mismatch or workspace too small"
 
 
@@ -83,3 +83,39 @@ def test_shard_range_partitions():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
             assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
+
+
+def test_workspace_planned_dims_bound_every_call():
+    """a call with more antennas or more bins than the workspace was planned for is a
+    shape error (RFR_E_SHAPE) before any launch -- the per-antenna and per-bin regions are sized
+    from the planning dimensions.  Host pointers stand in for device ones: nothing is launched."""
+    rfr, lib = _lib()
+    import numpy as np
+    na, nf, ns = 4, 8, 4
+    plan = dict(n_samples=ns, n_ant=na, n_freq=nf, n_query=ns)
+    nbytes = rfr.rfr_workspace_size(ns, na, nf, ns)
+    fake = C.c_void_p(0x1000)                           # never dereferenced on these paths
+    w = rfr.rfr_workspace(fake, nbytes, plan["n_samples"], plan["n_ant"], plan["n_freq"],
+                          plan["n_query"])
+    buf = np.zeros(64, np.float32)
+    p = C.c_void_p(buf.ctypes.data)
+    s = rfr.rfr_samples()
+    for f in ("x", "y", "z", "sdf", "refl", "nx", "ny", "nz", "power"):
+        setattr(s, f, p)
+    s.n_rays, s.n_per_ray = 1, ns
+
+    def ants(n):
+        a = rfr.rfr_antennas()
+        a.tx_x = a.tx_y = a.tx_z = p
+        a.n_ant = n
+        return a
+
+    sig = buf.ctypes.data_as(C.c_void_p)
+    for n_ant, n_freq in ((na + 1, nf), (na, nf + 1)):
+        a, g = ants(n_ant), rfr.rfr_freq_grid(77e9, 1e6, n_freq)
+        assert lib.rfr_forward(C.byref(s), 1.0, C.byref(a), C.byref(g), None, sig, C.byref(w),
+                               None) == 2
+        assert lib.rfr_filter(sig, C.byref(a), C.byref(g), p, p, p, ns, p, None, None, C.byref(w),
+                              None) == 2
+        assert lib.rfr_filter_backward(p, sig, p, C.c_float(0.0), C.byref(a), C.byref(g), p, p, p,
+                                       ns, sig, C.byref(w), None) == 2

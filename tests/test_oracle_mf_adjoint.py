@@ -85,6 +85,18 @@ def test_o7_zero_upstream_and_eps_guard():
     M0, P0 = oracle.filter(Z, A, grid, *q)
     g = oracle.filter_backward(np.ones_like(P0), M0, P0, A, grid, *q, eps=1e-30)
     assert np.all(np.isfinite(g)) and np.all(g == 0)
+    # reading Q15b: with eps = 0 a query at P = 0 takes the subgradient 0 of |M| at M = 0 (no 0/0),
+    # and the other queries are untouched (one zeroed query leaves the rest of the sum as is)
+    g0 = oracle.filter_backward(np.ones_like(P0), M0, P0, A, grid, *q, eps=0.0)
+    assert np.all(np.isfinite(g0)) and np.all(g0 == 0)
+    Mz, Pz = M.copy(), P.copy()
+    Mz[3], Pz[3] = 0.0, 0.0
+    keep = np.ones(P.shape[0], bool)
+    keep[3] = False
+    gz = oracle.filter_backward(np.ones_like(Pz), Mz, Pz, A, grid, *q, eps=0.0)
+    gk = oracle.filter_backward(np.ones_like(Pz[keep]), M[keep], P[keep], A, grid,
+                                *[c[keep] for c in q], eps=0.0)
+    assert np.all(np.isfinite(gz)) and np.allclose(gz, gk, rtol=1e-12, atol=0)
 
 
 def test_o7_row_subset_equals_full_rows():
