@@ -62,6 +62,8 @@ typedef struct rfr_comm rfr_comm;
                                 of the Chebyshev-moment path (DESIGN 5b); for A/B comparisons      */
 #define RFR_REUSE_BLEND 4u   /* workspace already holds K1's records for THIS sample set and s
                                 (set by the caller after rfr_forward on the same inputs); skips K1 */
+#define RFR_R1 16u           /* monostatic calls: the r1 kernels (rfr_cheb.cu) instead of the r2
+                                tiled engine (DESIGN 5e); for A/B comparisons                       */
 
 /* device-side flags read back by rfr_poll_flags */
 #define RFR_FLAG_DOMAIN 1u
@@ -245,6 +247,30 @@ const char *rfr_status_string(rfr_status s);
 int rfr_abi_version(void);
 /* Diagnostic: number of kernels this library has launched in the process so far. */
 uint64_t rfr_launch_count(void);
+
+/* Diagnostics of the r2 tiled engine.
+ * rfr_plan_state: the plan of the last engine call on `ws` (applied = 1: the engine ran; 0: the
+ * direct fallback kernels ran) -- tile grid, moments per tile P, moments of the global expansion
+ * Pg (0: direct node evaluation), points, and the tile / global delay half-spreads in cycles per
+ * bin.  Host-synchronous on `stream` (a 4-byte flag and the plan header are copied back).
+ * rfr_profile_enable(1) clears and starts per-sweep device timing: CUDA events are recorded on the
+ * launching stream around each sweep of the engine (ids below); rfr_profile_read returns the
+ * accumulated milliseconds and the number of timed launches of one sweep (it waits for the
+ * recorded events).  rfr_profile_enable(0) stops.  Both: RFR_E_ARG for an unknown id / NULL. */
+#define RFR_SWEEP_PLAN 0        /* box, grid choice, tile boxes, per-(tile, antenna) setup, tables */
+#define RFR_SWEEP_SORT 1        /* stable counting sort of a point set into the tiles           */
+#define RFR_SWEEP_PREP 2        /* global expansion + per-(tile, antenna) Horner coefficients     */
+#define RFR_SWEEP_FILTER 3      /* k2_filter (a4)                                               */
+#define RFR_SWEEP_BACKWARD 4    /* k2_bwd + split sum (a6)                                       */
+#define RFR_SWEEP_FORWARD 5     /* k2_fwd: per-(tile, antenna) moments (a3 / K5)                 */
+#define RFR_SWEEP_FORWARD_OUT 6 /* k2_fout: virtual sources -> global moments -> bins            */
+typedef struct {
+  int32_t applied, tiles, lx, ly, lz, P, Pg, n_points;
+  double delta_t, delta_g;
+} rfr_plan_info;
+rfr_status rfr_plan_state(const rfr_workspace *ws, rfr_plan_info *out, rfr_stream_t stream);
+rfr_status rfr_profile_enable(int on);
+rfr_status rfr_profile_read(int32_t sweep, double *ms, uint64_t *launches);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,7 @@
 #include "../../include/librfr.h"
 #include "rfr_device.cuh"
 #include "rfr_launch.h"
+#include "rfr_tiled.h"
 
 using namespace rfr;
 
@@ -24,6 +25,7 @@ constexpr size_t kChebHdrOff = 64;             // ChebHdr of the Chebyshev-momen
 constexpr size_t kActiveOff = 128;             // int64 count of the compacted active records
 constexpr size_t kActiveBwdOff = 136;          // int64 count of the backward's active samples
 constexpr size_t kTilePOff = 144;              // int: moments of the last tiled filter
+constexpr size_t kT2SkipOff = 192;             // ChebHdr: sel = 1 when the r2 engine's plan applies
 constexpr int kTmpN = 512;                     // reduction scratch (floats)
 constexpr size_t kSplitCap = size_t(2) << 30;  // cap on each split-partial region (bytes)
 
@@ -143,6 +145,12 @@ struct Layout {
          off_idxc = 0, off_ttile = 0, off_tbcnt = 0, off_tstart = 0, off_tperm = 0, off_tqs = 0,
          off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, off_trs = 0,
          off_tfp = 0, off_tgeo = 0, total = 0;
+  // r2 tiled engine (rfr_tiled.h): plan, tables, per-(tile, antenna) data, two sorted views
+  size_t off_t2plan = 0, off_t2boxp = 0, off_t2tabs = 0, off_t2tbox = 0, off_t2lc = 0,
+         off_t2geo = 0, off_t2lg = 0, off_t2acoef = 0, off_t2gexp = 0, off_t2coef = 0,
+         off_t2mom = 0, off_t2bwdp = 0;
+  size_t off_t2v[2][7] = {};        // per view: tstart+cstart+n_items, perm, pos, aux, bcnt
+  int t2_bwd_splits = 1;
   size_t cap_trs = 0, cap_tfp = 0;
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
@@ -207,6 +215,33 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.cap_tfp = (size_t)tile_fwd_blocks(n_q) * na1 * kChebPMax * 8;
     L.off_tfp = take(L.cap_tfp);
     L.off_tgeo = take((size_t)kTiles * na1 * 32);
+  }
+  {
+    const int64_t np = std::max<int64_t>(std::max(n_s, n_q), 1);
+    const int64_t na1 = std::max<int64_t>(n_a, 1);
+    L.off_t2plan = take(256);
+    L.off_t2boxp = take((size_t)kT2BoxBlocks * 6 * 4);
+    L.off_t2tabs = take((size_t)(3 * kT2PMax * kT2PMax + 128) * 8);
+    L.off_t2tbox = take((size_t)kT2Max * 6 * 4);
+    L.off_t2lc = take((size_t)kT2Max * na1 * 8);
+    L.off_t2geo = take((size_t)kT2Max * na1 * 32);
+    L.off_t2lg = take((size_t)na1 * 3 * 8);
+    L.off_t2acoef = take((size_t)nf * kT2PgMax * 8);
+    L.off_t2gexp = take((size_t)2 * na1 * kT2PgMax * 8);
+    L.off_t2coef = take((size_t)2 * kT2TP * na1 * 8);
+    L.off_t2mom = take((size_t)kT2TP * na1 * 8);
+    // backward split partials [S][5][n_s] (compacted index), S <= 16 within 1 GiB
+    const int64_t ns1 = std::max<int64_t>(n_s, 1);
+    L.t2_bwd_splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t(1) << 30) / (ns1 * 20)));
+    L.off_t2bwdp = take((size_t)L.t2_bwd_splits * 5 * ns1 * 4);
+    const int64_t nb = (np + kT2SortBlock - 1) / kT2SortBlock;
+    for (int v = 0; v < 2; ++v) {
+      L.off_t2v[v][0] = take((size_t)(2 * (kT2Max + 1) + 1) * 4);
+      L.off_t2v[v][1] = take((size_t)np * 4);
+      L.off_t2v[v][2] = take((size_t)np * 16);
+      L.off_t2v[v][3] = take((size_t)np * 16);
+      L.off_t2v[v][4] = take((size_t)nb * kT2Max * 4);
+    }
   }
   L.total = o;
   return true;
@@ -354,11 +389,71 @@ bool tile_enabled() {
   return v == 1;
 }
 
+// the r2 tiled engine (rfr_tiled.cu) serves monostatic calls without the Eq. 7 correction unless
+// RFR_V2=0 (A/B against the r1 kernels)
+bool v2_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("RFR_V2");
+    v = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+bool use_v2(const rfr_antennas *a, bool corr, uint32_t flags) {
+  return v2_enabled() && a->rx_x == nullptr && !corr && !(flags & (RFR_DIRECT | RFR_R1)) &&
+         cheb_enabled();
+}
+
+T2Args make_t2(const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_workspace *ws,
+               const Layout &L) {
+  T2Args t;
+  memset(&t, 0, sizeof(t));
+  t.plan = at<T2Plan>(ws, L.off_t2plan);
+  t.box_part = at<float>(ws, L.off_t2boxp);
+  t.tx_x = ants->tx_x; t.tx_y = ants->tx_y; t.tx_z = ants->tx_z;
+  t.n_a = ants->n_ant;
+  t.n_f = grid->n_freq;
+  t.kd = grid->df_hz / kC;
+  t.kc = (grid->f0_hz + (double)(grid->n_freq / 2) * grid->df_hz) / kC;
+  t.tbox = at<float>(ws, L.off_t2tbox);
+  t.lc = at<double>(ws, L.off_t2lc);
+  t.tgeo = at<float4>(ws, L.off_t2geo);
+  t.lg = at<double>(ws, L.off_t2lg);
+  t.acoef = at<float2>(ws, L.off_t2acoef);
+  t.tabs = at<double>(ws, L.off_t2tabs);
+  t.gexp = at<float2>(ws, L.off_t2gexp);
+  t.coef = at<float2>(ws, L.off_t2coef);
+  t.mom = at<float2>(ws, L.off_t2mom);
+  t.skip = at<ChebHdr>(ws, kT2SkipOff);
+  t.flags = at<unsigned>(ws, 0);
+  return t;
+}
+T2Sorted make_view(const rfr_workspace *ws, const Layout &L, int v, int chunk) {
+  T2Sorted s;
+  memset(&s, 0, sizeof(s));
+  s.tstart = at<int>(ws, L.off_t2v[v][0]);
+  s.cstart = s.tstart + kT2Max + 1;
+  s.n_items = s.cstart + kT2Max + 1;
+  s.chunk = chunk;
+  s.perm = at<int>(ws, L.off_t2v[v][1]);
+  s.pos = at<float4>(ws, L.off_t2v[v][2]);
+  s.aux = at<float4>(ws, L.off_t2v[v][3]);
+  s.bcnt = at<int>(ws, L.off_t2v[v][4]);
+  return s;
+}
+// antenna splits of a v2 adjoint sweep: enough work items for ~4 waves of the persistent grid
+int t2_splits(int64_t n_pts, int chunk, int64_t n_a, int cap) {
+  const int64_t items = std::max<int64_t>(1, cdiv(n_pts, chunk));
+  int64_t s = cdiv((int64_t)device_sms() * 5 * 4, items);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, 64)));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, cap));
+}
+
 rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
                    const rfr_freq_grid *grid, bool no_gain, bool corr, int kind, float *out,
                    const rfr_workspace *ws, const Layout &L, cudaStream_t st,
                    const Rec *rec_c = nullptr, const int64_t *n_dev = nullptr,
-                   bool direct = false) {
+                   bool direct = false, const ChebHdr *v2skip = nullptr) {
   FwdGeom g;
   if (!fwd_geom(grid->n_freq, g)) return RFR_E_SHAPE;
   const Split sp = fwd_split(n_pts, ants->n_ant, grid->n_freq, g, L.cap_fwdp);
@@ -381,6 +476,16 @@ rfr_status run_fwd(const Rec *rec, int64_t n_pts, const rfr_antennas *ants,
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = no_gain;
   const bool mono = ants->rx_x == nullptr;
+  if (v2skip) {
+    // the r2 engine ran first: this is its direct fallback, a no-op when the plan applied
+    a.skip = v2skip;
+    RFR_CU(launch_trace_fwd(a, g.B, mono, corr, kind, sp.splits, st));
+    if (sp.splits > 1)
+      RFR_CU(launch_sum_splits(at<float>(ws, L.off_fwdp), sp.splits,
+                               ants->n_ant * (int64_t)grid->n_freq * 2, out, device_sms(), st,
+                               v2skip));
+    return RFR_OK;
+  }
   // Chebyshev-moment path (rfr_cheb.cu): chosen on the device from the delay spread; the direct
   // kernel and its split sum return at once when it runs, and vice versa
   ChebHdr *hdr = at<ChebHdr>(ws, kChebHdrOff);
@@ -516,7 +621,21 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
   int64_t *n_act = at<int64_t>(ws, kActiveOff);
   RFR_CU(launch_compact(at<Rec>(ws, L.off_rec), n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c,
                         st));
-  return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, (flags & RFR_NO_GAIN) != 0, corr,
+  const bool no_gain = (flags & RFR_NO_GAIN) != 0;
+  if (use_v2(ants, corr, flags)) {
+    // r2 engine: plan over the active records, tiled moments, virtual sources -> bins
+    const T2Args t = make_t2(ants, grid, ws, L);
+    const T2Sorted v = make_view(ws, L, 0, kT2FltChunk);
+    T2Points pts;
+    memset(&pts, 0, sizeof(pts));
+    pts.rec = rec_c; pts.n_dev = n_act; pts.n = n_s;
+    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_forward(t, v, kFwdTrace, no_gain, reinterpret_cast<float2 *>(signal), device_sms(),
+                      st));
+    return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, no_gain, corr, kFwdTrace, signal, ws,
+                   L, st, nullptr, nullptr, false, t.skip);
+  }
+  return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, no_gain, corr,
                  kFwdTrace, signal, ws, L, st, rec_c, n_act, (flags & RFR_DIRECT) != 0);
 }
 
@@ -562,6 +681,29 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   a.flags = at<unsigned>(ws, 0);
   a.no_gain = false;
   const bool mono = ants->rx_x == nullptr;
+  if (ants->n_ant > 0 && use_v2(ants, false, 0)) {
+    // r2 engine: plan over the queries, Horner coefficients of the signal, filter sweep
+    const T2Args t = make_t2(ants, grid, ws, L);
+    const T2Sorted v = make_view(ws, L, 0, kT2FltChunk);
+    T2Points pts;
+    memset(&pts, 0, sizeof(pts));
+    pts.qx = qx; pts.qy = qy; pts.qz = qz; pts.n = n_query;
+    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_prep_adjoint(t, v.tstart, reinterpret_cast<const float2 *>(signal), nullptr, st));
+    const int S = t2_splits(n_query, kT2FltChunk, ants->n_ant, sp.splits);
+    const int64_t aps = cdiv(cdiv(ants->n_ant, S), 16) * 16;
+    float2 *o = reinterpret_cast<float2 *>(S > 1 ? at<float>(ws, L.off_fltp) : M);
+    RFR_CU(t2_filter(t, v, 0, o, n_query, S, aps, device_sms(), st));
+    if (S > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_fltp), S, n_query * 2, M, device_sms(), st));
+    a.skip = t.skip;                                   // direct fallback: no-op when planned
+    RFR_CU(launch_adjoint(a, kModeFlt, mono, false, sp.splits, st));
+    if (sp.splits > 1)
+      RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, n_query * 2, M,
+                               device_sms(), st, t.skip));
+    RFR_TRY(allreduce_sum(comm, M, 2 * n_query, st));
+    if (power) RFR_CU(launch_abs(M, n_query, power, device_sms(), st));
+    return RFR_OK;
+  }
   // Chebyshev-moment filter: the query points are packed as records (for their bounding box)
   const bool cheb = ants->n_ant > 0;
   const ChebArgs c = make_cheb(at<Rec>(ws, L.off_qrec), n_query, ants, grid, false, ws, L, 0);
@@ -657,6 +799,29 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
   Rec *rec_c = at<Rec>(ws, L.off_recc);
   int *idx_c = at<int>(ws, L.off_idxc);
   int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
+  if (cheb && use_v2(ants, corr, flags)) {
+    // r2 engine: plan over the alpha != 0 samples, Horner coefficients of G, backward sweep
+    RFR_CU(launch_compact(a.rec, n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c, st,
+                          at<unsigned char>(ws, L.off_aflag), idx_c));
+    const T2Args t = make_t2(ants, grid, ws, L);
+    const T2Sorted v = make_view(ws, L, 0, kT2BwdChunk);
+    T2Points pts;
+    memset(&pts, 0, sizeof(pts));
+    pts.rec = rec_c; pts.n_dev = n_act; pts.n = n_s;
+    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_prep_adjoint(t, v.tstart, a.X, nullptr, st));
+    RFR_CU(cudaMemsetAsync(partials, 0, (size_t)5 * n_s * 4, st));
+    const int S = std::max(1, std::min<int>(L.t2_bwd_splits, (int)cdiv(ants->n_ant, 1024)));
+    const int64_t aps = cdiv(cdiv(ants->n_ant, S), 16) * 16;
+    RFR_CU(t2_backward(t, v, 0, idx_c, n_act, n_s, at<float>(ws, L.off_t2bwdp), partials, n_s, S,
+                       aps, a.no_gain, device_sms(), st));
+    a.skip = t.skip;                                   // direct fallback: no-op when planned
+    RFR_CU(launch_adjoint(a, kModeBwd, mono, corr, sp.splits, st));
+    if (sp.splits > 1)
+      RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
+                               device_sms(), st, t.skip));
+    return RFR_OK;
+  }
   ChebArgs c = make_cheb(rec_c, n_s, ants, grid, a.no_gain, ws, L, 0, (flags & RFR_DIRECT) != 0);
   c.n_dev = n_act;
   c.idx = idx_c;
@@ -783,6 +948,46 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
   // samples with alpha != 0 only (row 0 = G, compacted list, DESIGN 5c)
   const bool corr = has_corr(samples, ants);
   const bool cheb = ants->n_ant > 0;
+  if (cheb && use_v2(ants, corr, flags)) {
+    // r2 engine: one plan over every sample (the filter's queries), Horner coefficients of both
+    // rows (G and s), the filter sweep over all samples and the backward sweep over the alpha != 0
+    // samples sorted into the same tiles
+    const T2Args t = make_t2(ants, grid, ws, L);
+    const T2Sorted v0 = make_view(ws, L, 0, kT2FltChunk), v1 = make_view(ws, L, 1, kT2BwdChunk);
+    T2Points all;
+    memset(&all, 0, sizeof(all));
+    all.qx = samples->x; all.qy = samples->y; all.qz = samples->z; all.n = n_s;
+    RFR_CU(t2_plan(t, all, v0, device_sms(), st));
+    RFR_CU(t2_prep_adjoint(t, v0.tstart, a.X, a.X2, st));
+    const int Sf = t2_splits(n_s, kT2FltChunk, ants->n_ant, sp.splits);
+    const int64_t apf = cdiv(cdiv(ants->n_ant, Sf), 16) * 16;
+    float2 *o = reinterpret_cast<float2 *>(Sf > 1 ? at<float>(ws, L.off_fltp) : mf);
+    RFR_CU(t2_filter(t, v0, 1, o, n_s, Sf, apf, device_sms(), st));
+    if (Sf > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_fltp), Sf, n_s * 2, mf, device_sms(), st));
+    Rec *rec_c = at<Rec>(ws, L.off_recc);
+    int *idx_c = at<int>(ws, L.off_idxc);
+    int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
+    RFR_CU(launch_compact(a.rec, n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c, st,
+                          at<unsigned char>(ws, L.off_aflag), idx_c));
+    T2Points act;
+    memset(&act, 0, sizeof(act));
+    act.rec = rec_c; act.n_dev = n_act; act.n = n_s;
+    RFR_CU(t2_sort(t, act, v1, st));
+    RFR_CU(cudaMemsetAsync(partials, 0, (size_t)5 * n_s * 4, st));
+    const int Sb = std::max(1, std::min<int>(L.t2_bwd_splits, (int)cdiv(ants->n_ant, 1024)));
+    const int64_t apb = cdiv(cdiv(ants->n_ant, Sb), 16) * 16;
+    RFR_CU(t2_backward(t, v1, 0, idx_c, n_act, n_s, at<float>(ws, L.off_t2bwdp), partials, n_s,
+                       Sb, apb, a.no_gain, device_sms(), st));
+    a.skip = t.skip;                                   // direct fallback: no-op when planned
+    RFR_CU(launch_adjoint(a, kModeBoth, mono, corr, sp.splits, st));
+    if (sp.splits > 1) {
+      RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
+                               device_sms(), st, t.skip));
+      RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, 2 * n_s, mf, device_sms(),
+                               st, t.skip));
+    }
+    return RFR_OK;
+  }
   const ChebArgs c = make_cheb(a.rec, n_s, ants, grid, a.no_gain, ws, L, 0,
                                (flags & RFR_DIRECT) != 0);
   if (cheb) {
@@ -885,6 +1090,19 @@ rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const f
   Rec *qrec = at<Rec>(ws, L.off_qrec);
   RFR_CU(launch_mf_adj_pack(grad_power, mf, power, eps, qx, qy, qz, n_query, qrec, device_sms(),
                             st));
+  if (use_v2(ants, false, 0)) {
+    // r2 engine: plan over the queries, tiled moments of the K5 weights c_q -> bins
+    const T2Args t = make_t2(ants, grid, ws, L);
+    const T2Sorted v = make_view(ws, L, 0, kT2FltChunk);
+    T2Points pts;
+    memset(&pts, 0, sizeof(pts));
+    pts.rec = qrec; pts.n = n_query;
+    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_forward(t, v, kFwdMFAdj, false, reinterpret_cast<float2 *>(grad_signal),
+                      device_sms(), st));
+    return run_fwd(qrec, n_query, ants, grid, false, false, kFwdMFAdj, grad_signal, ws, L, st,
+                   nullptr, nullptr, false, t.skip);
+  }
   return run_fwd(qrec, n_query, ants, grid, false, false, kFwdMFAdj, grad_signal, ws, L, st);
 }
 
@@ -900,6 +1118,43 @@ rfr_status rfr_heatmap_loss(const float *power, const float *power_gt, int64_t n
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   RFR_CU(launch_heat_loss(power, power_gt, n_query, cell, history, thr_hi, ratio, grad_power, mask,
                           at<float>(ws, L.off_tmp), kTmpN, loss, st));
+  return RFR_OK;
+}
+
+rfr_status rfr_plan_state(const rfr_workspace *ws, rfr_plan_info *out, rfr_stream_t stream) {
+  if (!ws || !ws->ptr || !out) return RFR_E_ARG;
+  Layout L;
+  RFR_TRY(check_ws(ws, 0, 0, L));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  T2Plan pl;
+  ChebHdr sk;
+  if (cudaMemcpyAsync(&pl, at<T2Plan>(ws, L.off_t2plan), sizeof(pl), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(&sk, at<ChebHdr>(ws, kT2SkipOff), sizeof(sk), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return RFR_E_CUDA;
+  out->applied = sk.sel ? 1 : 0;
+  out->tiles = pl.T;
+  out->lx = pl.L[0]; out->ly = pl.L[1]; out->lz = pl.L[2];
+  out->P = pl.P;
+  out->Pg = pl.Pg;
+  out->n_points = pl.n_pts;
+  out->delta_t = pl.delta_t;
+  out->delta_g = pl.delta_g;
+  return RFR_OK;
+}
+
+rfr_status rfr_profile_enable(int on) {
+  t2_profile_enable(on != 0);
+  return RFR_OK;
+}
+
+rfr_status rfr_profile_read(int32_t sweep, double *ms, uint64_t *launches) {
+  if (!ms || !launches || sweep < 0 || sweep >= kT2ProfSlots) return RFR_E_ARG;
+  unsigned long long n = 0;
+  t2_profile_read(sweep, ms, &n);
+  *launches = (uint64_t)n;
   return RFR_OK;
 }
 

@@ -1,0 +1,1464 @@
+// rfr_tiled.cu -- the r2 tiled engine (see rfr_tiled.h).
+//
+// Every sweep of the hot path sums, per (point q, antenna i), a phasor over the N_f uniform bins
+// (Eq. 3 P:L182-187 filter, Eq. 4 P:L231-234 forward, App. A.5 P:L725-728 adjoint).  With the delay
+// in cycles per bin u = L df / c (L = 2 d monostatic), the centred bins m' = m - N/2 and the centre
+// frequency f_c = f0 + (N/2) df, the adjoint bin sum is E * F_i(u) with E = e^{+j 2 pi f_c tau} and
+//     F_i(u) = sum_m X_i[m] e^{+j 2 pi m' u},
+// a band-limited function that varies by only a few cycles over the delays of one spatial tile.
+// On a tile t (delay interval u_c,it +- delta_t, x = (u - u_c,it) / delta_t in [-1, 1]) it is a
+// polynomial of degree P - 1 in x up to the Chebyshev interpolation error (<= 2 x the Jacobi-Anger
+// tail, < 2e-7 of sum |X| by the P rule).  The filter / backward sweeps evaluate that polynomial by
+// Horner from monomial coefficients (one FFMA2 per coefficient and point; the monomial form is
+// well conditioned here because sum_j |c_j| <= e^{z} sum |X| with z = 2 pi (N/2 + 1) delta_t <= 4.8).
+// The coefficients come from P values of F_i at the tile's Chebyshev nodes, evaluated through one
+// global expansion per antenna, F_i(u) = sum_q G_i[q] T_q((u - u_g,i) / delta_g) (Jacobi-Anger,
+// Pg <= 48 terms), so the per-(antenna, tile) preparation costs P * Pg instead of P * N_f.
+// The forward runs the transpose: per-(antenna, tile) Chebyshev moments of the tile's points, P
+// virtual sources per tile at the nodes (weights = Lagrange interpolation of the moments), their
+// global moments and the bins a[m][q] Mg[q].  All sums are fixed-order (no float atomics).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "rfr_device.cuh"
+#include "rfr_launch.h"
+#include "rfr_tiled.h"
+
+namespace rfr {
+
+// ------------------------------------------------------------ per-sweep device-time profiling
+// (rfr_profile_enable / rfr_profile_read): CUDA events recorded on the launching stream around
+// each sweep launch while enabled; read back (synchronising on the stop events) on request.
+namespace {
+struct ProfPending {
+  int id;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfPending> g_prof_pending;
+std::vector<cudaEvent_t> g_prof_pool;
+double g_prof_ms[kT2ProfSlots];
+unsigned long long g_prof_n[kT2ProfSlots];
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_drain() {                 // caller holds g_prof_mu
+  for (auto &p : g_prof_pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      g_prof_ms[p.id] += ms;
+      g_prof_n[p.id] += 1;
+    }
+    g_prof_pool.push_back(p.a);
+    g_prof_pool.push_back(p.b);
+  }
+  g_prof_pending.clear();
+}
+}  // namespace
+
+ProfScope::ProfScope(int id, cudaStream_t st) : st_(st), id_(-1), a_(nullptr) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  id_ = id;
+  a_ = prof_event();
+  cudaEventRecord(static_cast<cudaEvent_t>(a_), st_);
+}
+ProfScope::~ProfScope() {
+  if (id_ < 0) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEvent_t b = prof_event();
+  cudaEventRecord(b, st_);
+  g_prof_pending.push_back({id_, static_cast<cudaEvent_t>(a_), b});
+  if (g_prof_pending.size() > 4096) prof_drain();
+}
+void t2_profile_enable(bool on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  prof_drain();
+  if (on)
+    for (int k = 0; k < kT2ProfSlots; ++k) { g_prof_ms[k] = 0.0; g_prof_n[k] = 0; }
+  g_prof_on = on;
+}
+void t2_profile_read(int id, double *ms, unsigned long long *n) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  prof_drain();
+  *ms = (id >= 0 && id < kT2ProfSlots) ? g_prof_ms[id] : 0.0;
+  *n = (id >= 0 && id < kT2ProfSlots) ? g_prof_n[id] : 0ull;
+}
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr float kInv16Pi2f = 0.00633257759406206f;   // 1 / (4 pi)^2 (Q3)
+
+// ------------------------------------------------------------------ packed f32x2 helpers
+__device__ __forceinline__ f2x bcv(float v) { return pk(v, v); }
+__device__ __forceinline__ float rsq_ftz(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float rcp_ftz_(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ void sc_ftz(float v, float &s, float &c) {
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(v));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(v));
+}
+__device__ __forceinline__ float rni(float v) {
+  float r;
+  asm("cvt.rni.f32.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// truncation tail sum_{p >= P} eps_p |J_p(z)| < 1e-7 (tests/test_cheb_math.py pins the rule)
+__host__ __device__ inline int t2_select_P(double z) {
+  if (z <= 0.917) return 8;
+  if (z <= 1.683) return 10;
+  if (z <= 2.611) return 12;
+  if (z <= 3.663) return 14;
+  if (z <= 4.813) return 16;
+  return 0;
+}
+__device__ inline int t2_select_Pg(double z) {
+  if (z <= 4.813) return 16;
+  if (z <= 7.33) return 20;
+  if (z <= 10.061) return 24;
+  if (z <= 12.946) return 28;
+  if (z <= 15.948) return 32;
+  if (z <= 28.6) return 48;
+  return 0;
+}
+
+// distance range [dmin, dmax] from a point to an axis-aligned box (fp64)
+__device__ __forceinline__ void t2_box_dist(const float *b, double px, double py, double pz,
+                                            double &dmin, double &dmax) {
+  const double p[3] = {px, py, pz};
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double l = b[c], h = b[3 + c];
+    const double out = fmax(fmax(l - p[c], p[c] - h), 0.0);
+    s0 += out * out;
+    const double far = fmax(fabs(p[c] - l), fabs(p[c] - h));
+    s1 += far * far;
+  }
+  dmin = sqrt(s0);
+  dmax = sqrt(s1);
+}
+
+__device__ __forceinline__ int64_t t2_count(const T2Points &p) { return p.n_dev ? *p.n_dev : p.n; }
+__device__ __forceinline__ float3 t2_pos(const T2Points &p, int64_t j) {
+  if (p.rec) {
+    const Rec &r = p.rec[j];
+    return make_float3((float)r.x, (float)r.y, (float)r.z);
+  }
+  return make_float3(p.qx[j], p.qy[j], p.qz[j]);
+}
+
+// tile of a position in the plan's grid
+__device__ __forceinline__ int t2_tile_of(const T2Plan &pl, float3 q) {
+  const float v[3] = {q.x, q.y, q.z};
+  int id = 0;
+#pragma unroll
+  for (int c = 2; c >= 0; --c) {
+    const float lo = pl.gbox[c], w = pl.gbox[3 + c] - lo;
+    int k = w > 0.f ? (int)((v[c] - lo) / w * (float)pl.L[c]) : 0;
+    k = min(max(k, 0), pl.L[c] - 1);
+    id = id * pl.L[c] + k;
+  }
+  return id;
+}
+
+// fp32 centre of a tile's tight box (the same rounding wherever it is used)
+__device__ __forceinline__ float t2_centre(const float *tb, int c) { return 0.5f * (tb[c] + tb[3 + c]); }
+
+// ================================================================================= plan
+__global__ void __launch_bounds__(256) k2_box(T2Points p, float *part) {
+  const int64_t n = t2_count(p);
+  float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const float3 q = t2_pos(p, j);
+    lo[0] = fminf(lo[0], q.x); hi[0] = fmaxf(hi[0], q.x);
+    lo[1] = fminf(lo[1], q.y); hi[1] = fmaxf(hi[1], q.y);
+    lo[2] = fminf(lo[2], q.z); hi[2] = fmaxf(hi[2], q.z);
+  }
+  __shared__ float sh[6][256];
+  for (int c = 0; c < 3; ++c) { sh[c][threadIdx.x] = lo[c]; sh[3 + c][threadIdx.x] = hi[c]; }
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int c = 0; c < 3; ++c) {
+        sh[c][threadIdx.x] = fminf(sh[c][threadIdx.x], sh[c][threadIdx.x + s]);
+        sh[3 + c][threadIdx.x] = fmaxf(sh[3 + c][threadIdx.x], sh[3 + c][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// candidate grids: L_c in {1, 2, 4, 8, 16} per axis, T <= kT2Max
+constexpr int kT2Cand = 125;
+__device__ __forceinline__ void t2_cand(int c, int L[3]) {
+  L[0] = 1 << (c % 5);
+  L[1] = 1 << ((c / 5) % 5);
+  L[2] = 1 << (c / 25);
+}
+constexpr int kT2SubAnts = 32;
+
+// one CTA per candidate grid: max over its cells and a subsample of the antennas of the delay
+// half-spread (cell boxes bound the tight boxes from above), -> the candidate's P and cost
+__global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Args a,
+                                               int64_t n_pts_host, const int64_t *n_dev,
+                                               double *cost) {
+  __shared__ float box[6];
+  __shared__ double red[256];
+  if (threadIdx.x < 6) {
+    float v = threadIdx.x < 3 ? 3e38f : -3e38f;
+    for (int b = 0; b < nblk; ++b) {
+      const float u = part[b * 6 + threadIdx.x];
+      v = threadIdx.x < 3 ? fminf(v, u) : fmaxf(v, u);
+    }
+    box[threadIdx.x] = v;
+  }
+  __syncthreads();
+  int L[3];
+  t2_cand(blockIdx.x, L);
+  const int T = L[0] * L[1] * L[2];
+  const int64_t n = n_dev ? *n_dev : n_pts_host;
+  double hmax = 0.0;
+  if (T <= kT2Max && box[0] <= box[3]) {
+    const int ns = (int)(a.n_a < kT2SubAnts ? a.n_a : kT2SubAnts);
+    for (int w = threadIdx.x; w < T * ns; w += blockDim.x) {
+      const int t = w / ns, k = w % ns;
+      const int64_t i = ns > 1 ? (int64_t)k * (a.n_a - 1) / (ns - 1) : 0;
+      const int cx = t % L[0], cy = (t / L[0]) % L[1], cz = t / (L[0] * L[1]);
+      const int cc[3] = {cx, cy, cz};
+      float cb[6];
+      for (int c = 0; c < 3; ++c) {
+        const float lo = box[c], wd = (box[3 + c] - box[c]) / (float)L[c];
+        cb[c] = lo + wd * (float)cc[c];
+        cb[3 + c] = lo + wd * (float)(cc[c] + 1);
+      }
+      double dmin, dmax;
+      t2_box_dist(cb, a.tx_x[i], a.tx_y[i], a.tx_z[i], dmin, dmax);
+      hmax = fmax(hmax, dmax - dmin);            // half-spread of L = 2 d
+    }
+  }
+  red[threadIdx.x] = hmax;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double c = 1e300;
+    if (T <= kT2Max && box[0] <= box[3]) {
+      const double z = 2.0 * kPi * (double)(a.n_f / 2 + 1) * red[0] * a.kd * (1.0 + 1e-6);
+      const int P = t2_select_P(z);
+      // FMA-pipe cost per (point, antenna): P Horner steps + ~10 for the geometry; partially
+      // filled work items waste ~half a chunk per tile; T P <= kT2TP (coefficient storage)
+      if (P > 0 && T * P <= kT2TP)
+        c = (double)(P + 10) * ((double)n + (double)T * kT2FltChunk * 0.5) + (double)T * P * 64.0;
+    }
+    cost[blockIdx.x] = c;
+  }
+}
+
+// pick the cheapest candidate (ties: fewer tiles), write the box and the grid; reset scratch
+__global__ void __launch_bounds__(128) k2_pick(const float *part, int nblk, const double *cost,
+                                               T2Plan *pl, int64_t n_pts_host,
+                                               const int64_t *n_dev) {
+  __shared__ int best;
+  if (threadIdx.x == 0) {
+    int b = -1;
+    double bc = 1e300;
+    for (int c = 0; c < kT2Cand; ++c) {
+      int L[3];
+      t2_cand(c, L);
+      const double v = cost[c];
+      if (v < bc || (v == bc && b >= 0 && L[0] * L[1] * L[2] < pl->T)) { bc = v; b = c; pl->T = L[0] * L[1] * L[2]; }
+    }
+    best = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    float v = threadIdx.x < 3 ? 3e38f : -3e38f;
+    for (int b = 0; b < nblk; ++b) {
+      const float u = part[b * 6 + threadIdx.x];
+      v = threadIdx.x < 3 ? fminf(v, u) : fmaxf(v, u);
+    }
+    pl->gbox[threadIdx.x] = v;
+  }
+  const int64_t n = n_dev ? *n_dev : n_pts_host;
+  if (n == 0 && threadIdx.x < 6) pl->gbox[threadIdx.x] = 0.f;   // empty set: a trivial plan
+  if (threadIdx.x == 0) {
+    int L[3] = {1, 1, 1};
+    if (best >= 0) t2_cand(best, L);
+    if (n == 0) best = 0;
+    pl->L[0] = L[0]; pl->L[1] = L[1]; pl->L[2] = L[2];
+    pl->T = L[0] * L[1] * L[2];
+    pl->P = best >= 0 ? 1 : 0;              // provisional (k2_select decides)
+    pl->n_pts = (int)n;
+    pl->dmax_bits = 0ull;
+    pl->gmax_bits = 0ull;
+    pl->umin_bits = (unsigned long long)__double_as_longlong(1e300);
+  }
+}
+
+// ------------------------------------------------------------- stable counting sort by tile
+// per block of kT2SortBlock points: per-warp counts of each tile (match_any groups), so the order
+// inside a tile is the source order (deterministic)
+__device__ __forceinline__ void t2_block_counts(const T2Plan &pl, const T2Points &p, int64_t n,
+                                                int *wc /* [32][T] */, int T, int &t_out,
+                                                bool &ok_out, unsigned &peers_out) {
+  const int64_t j = (int64_t)blockIdx.x * kT2SortBlock + threadIdx.x;
+  const bool ok = j < n;
+  const int t = ok ? t2_tile_of(pl, t2_pos(p, j)) : -1;
+  for (int k = threadIdx.x; k < 32 * T; k += blockDim.x) wc[k] = 0;
+  __syncthreads();
+  const unsigned peers = __match_any_sync(0xffffffffu, t);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (ok && lane == __ffs(peers) - 1) wc[warp * T + t] = __popc(peers);
+  __syncthreads();
+  t_out = t;
+  ok_out = ok;
+  peers_out = peers;
+}
+
+__global__ void __launch_bounds__(kT2SortBlock) k2_count(const T2Plan *plp, T2Points p,
+                                                         T2Sorted s) {
+  extern __shared__ int wc[];
+  const T2Plan pl = *plp;
+  if (pl.P == 0) return;
+  const int T = pl.T;
+  const int64_t n = t2_count(p);
+  if ((int64_t)blockIdx.x * kT2SortBlock >= n) return;
+  int t;
+  bool ok;
+  unsigned peers;
+  t2_block_counts(pl, p, n, wc, T, t, ok, peers);
+  for (int q = threadIdx.x; q < T; q += blockDim.x) {
+    int c = 0;
+    for (int w = 0; w < kT2SortBlock / 32; ++w) c += wc[w * T + q];
+    s.bcnt[(int64_t)blockIdx.x * kT2Max + q] = c;
+  }
+}
+
+// thread per tile: exclusive offsets over the blocks, then tile starts and work-item starts
+__global__ void __launch_bounds__(kT2Max) k2_scan(const T2Plan *plp, const int64_t *n_dev,
+                                                  int64_t n_host, T2Sorted s) {
+  __shared__ int tot[kT2Max];
+  const T2Plan pl = *plp;
+  const int T = pl.P ? pl.T : 0;
+  const int64_t n = n_dev ? *n_dev : n_host;
+  const int nb = (int)((n + kT2SortBlock - 1) / kT2SortBlock);
+  const int q = threadIdx.x;
+  if (q < T) {
+    int run = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int c = s.bcnt[(int64_t)b * kT2Max + q];
+      s.bcnt[(int64_t)b * kT2Max + q] = run;
+      run += c;
+    }
+    tot[q] = run;
+  }
+  __syncthreads();
+  if (q == 0) {
+    int st = 0, cs = 0;
+    for (int k = 0; k < T; ++k) {
+      s.tstart[k] = st;
+      s.cstart[k] = cs;
+      st += tot[k];
+      cs += (tot[k] + s.chunk - 1) / s.chunk;
+    }
+    s.tstart[T] = st;
+    s.cstart[T] = cs;
+    *s.n_items = cs;
+  }
+}
+
+__global__ void __launch_bounds__(kT2SortBlock) k2_write(const T2Plan *plp, T2Points p,
+                                                         T2Sorted s) {
+  extern __shared__ int wc[];
+  const T2Plan pl = *plp;
+  if (pl.P == 0) return;
+  const int T = pl.T;
+  const int64_t n = t2_count(p);
+  if ((int64_t)blockIdx.x * kT2SortBlock >= n) return;
+  int t;
+  bool ok;
+  unsigned peers;
+  t2_block_counts(pl, p, n, wc, T, t, ok, peers);
+  // exclusive prefix over the warps, per tile
+  for (int q = threadIdx.x; q < T; q += blockDim.x) {
+    int run = 0;
+    for (int w = 0; w < kT2SortBlock / 32; ++w) {
+      const int c = wc[w * T + q];
+      wc[w * T + q] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (!ok) return;
+  const int64_t j = (int64_t)blockIdx.x * kT2SortBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pos = s.tstart[t] + s.bcnt[(int64_t)blockIdx.x * kT2Max + t] + wc[warp * T + t] +
+                  __popc(peers & ((1u << lane) - 1u));
+  s.perm[pos] = (int)j;
+  if (p.rec) {
+    const Rec r = p.rec[j];
+    s.pos[pos] = make_float4((float)r.x, (float)r.y, (float)r.z, r.w);
+    s.aux[pos] = make_float4(r.nx, r.ny, r.nz, r.T);
+  } else {
+    s.pos[pos] = make_float4(p.qx[j], p.qy[j], p.qz[j], 0.f);
+  }
+}
+
+// tight box per tile from the sorted positions
+__global__ void __launch_bounds__(256) k2_tbox(const T2Plan *plp, T2Sorted s, float *tbox) {
+  const int t = blockIdx.x;
+  if (plp->P == 0 || t >= plp->T) return;
+  const int lo = s.tstart[t], hi = s.tstart[t + 1];
+  float mn[3] = {3e38f, 3e38f, 3e38f}, mx[3] = {-3e38f, -3e38f, -3e38f};
+  for (int k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    const float4 v = s.pos[k];
+    mn[0] = fminf(mn[0], v.x); mx[0] = fmaxf(mx[0], v.x);
+    mn[1] = fminf(mn[1], v.y); mx[1] = fmaxf(mx[1], v.y);
+    mn[2] = fminf(mn[2], v.z); mx[2] = fmaxf(mx[2], v.z);
+  }
+  __shared__ float sh[6][256];
+  for (int c = 0; c < 3; ++c) { sh[c][threadIdx.x] = mn[c]; sh[3 + c][threadIdx.x] = mx[c]; }
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st)
+      for (int c = 0; c < 3; ++c) {
+        sh[c][threadIdx.x] = fminf(sh[c][threadIdx.x], sh[c][threadIdx.x + st]);
+        sh[3 + c][threadIdx.x] = fmaxf(sh[3 + c][threadIdx.x], sh[3 + c][threadIdx.x + st]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) tbox[t * 6 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+// per (tile, antenna): centre path length L_c = dmin + dmax, half-spread dmax - dmin, and the
+// tile-relative geometry around the fp32 tile centre c_t: g0 = (-2a', |a'|^2), g1 = (d_a,
+// frac(2 d_a kc), 2 d_a - L_c, 0) with a' = a - c_t, d_a = |a'| (fp64, rounded once)
+__global__ void __launch_bounds__(128) k2_tsetup(T2Args a, const int *tstart) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double hm = 0.0, lmin = 1e300, lmax = -1e300, umin = 1e300;
+  if (i < a.n_a) {
+    const double ax = a.tx_x[i], ay = a.tx_y[i], az = a.tx_z[i];
+    for (int t = 0; t < pl.T; ++t) {
+      if (tstart[t + 1] == tstart[t]) continue;      // empty tile: never read
+      const float *b = a.tbox + t * 6;
+      double dmin, dmax;
+      t2_box_dist(b, ax, ay, az, dmin, dmax);
+      umin = fmin(umin, dmin);
+      const double Lc = dmin + dmax;
+      a.lc[(int64_t)t * a.n_a + i] = Lc;
+      hm = fmax(hm, dmax - dmin);
+      lmin = fmin(lmin, Lc);
+      lmax = fmax(lmax, Lc);
+      const double px = ax - (double)t2_centre(b, 0), py = ay - (double)t2_centre(b, 1),
+                   pz = az - (double)t2_centre(b, 2);
+      const double D = px * px + py * py + pz * pz, da = sqrt(D);
+      const double cyc = 2.0 * da * a.kc;
+      float4 *g = a.tgeo + ((int64_t)t * a.n_a + i) * 2;
+      g[0] = make_float4((float)(-2.0 * px), (float)(-2.0 * py), (float)(-2.0 * pz), (float)D);
+      g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), 0.f);
+    }
+    a.lg[i * 3 + 1] = lmin;
+    a.lg[i * 3 + 2] = lmax;
+  }
+  __shared__ double red[128];
+  red[threadIdx.x] = hm;
+  __syncthreads();
+  for (int s = 64; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(&a.plan->dmax_bits, (unsigned long long)__double_as_longlong(red[0]));
+  __syncthreads();
+  red[threadIdx.x] = umin;
+  __syncthreads();
+  for (int s = 64; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMin(&a.plan->umin_bits, (unsigned long long)__double_as_longlong(red[0]));
+}
+
+// per antenna: the global interval covering every tile's [L_c -+ h_t]
+__global__ void __launch_bounds__(256) k2_gsetup(T2Args a) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0) return;
+  const double ht = __longlong_as_double((long long)pl.dmax_bits);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double hg = 0.0;
+  if (i < a.n_a) {
+    const double lmin = a.lg[i * 3 + 1], lmax = a.lg[i * 3 + 2];
+    a.lg[i * 3] = 0.5 * (lmin + lmax);
+    hg = 0.5 * (lmax - lmin) + ht;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = hg;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(&a.plan->gmax_bits, (unsigned long long)__double_as_longlong(red[0]));
+}
+
+__global__ void k2_select(T2Args a) {
+  T2Plan *pl = a.plan;
+  if (pl->P == 0) { a.skip->sel = 0u; return; }
+  const double ht = __longlong_as_double((long long)pl->dmax_bits);
+  const double hg = __longlong_as_double((long long)pl->gmax_bits);
+  // spreads in cycles per bin, with a margin for the fp32 rounding of the positions
+  const double dt = fmax(ht * a.kd * (1.0 + 1e-6), 1e-30);
+  const double dg = fmax(hg * a.kd * (1.0 + 1e-6), 1e-30);
+  const double zf = 2.0 * kPi * (double)(a.n_f / 2 + 1);
+  int P = t2_select_P(zf * dt);
+  if (pl->T * P > kT2TP) P = 0;
+  // u_min guard (Q24): a tile box closer than 1 mm to an antenna -> the direct kernels, which
+  // zero such pairs and raise RFR_FLAG_DOMAIN
+  if (__longlong_as_double((long long)pl->umin_bits) < kUmin) P = 0;
+  a.skip->sel = P ? 1u : 0u;
+  a.skip->P = 0;
+  pl->P = P;
+  pl->Pg = t2_select_Pg(zf * dg);
+  pl->delta_t = dt;
+  pl->inv_t = a.kd / dt;
+  pl->delta_g = dg;
+  pl->inv_g = a.kd / dg;
+}
+
+// ------------------------------------------------------------------ tables
+// a[m][q] = eps_q (-j)^q J_q(2 pi m' delta_g) (Miller's backward recurrence in fp64), q < Pg;
+// tabs[0][k] = node x_k = cos(pi (k + 1/2) / P); tabs[1][j][k] = W (node values -> monomial
+// coefficients of the interpolant); tabs[2][k][p] = lambda (moments -> node weights)
+__global__ void k2_tables(T2Args a) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0) return;
+  const int P = pl.P;
+  if (blockIdx.x == 0) {
+    __shared__ double tp[kT2PMax][kT2PMax];          // t_{p, j}: monomial coefficients of T_p
+    __shared__ double Tk[kT2PMax][kT2PMax];          // T_p(x_k)
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+      for (int p = 0; p < kT2PMax; ++p)
+        for (int j = 0; j < kT2PMax; ++j) tp[p][j] = 0.0;
+      tp[0][0] = 1.0;
+      tp[1][1] = 1.0;
+      for (int p = 1; p + 1 < kT2PMax; ++p)
+        for (int j = 0; j < kT2PMax; ++j)
+          tp[p + 1][j] = (j > 0 ? 2.0 * tp[p][j - 1] : 0.0) - tp[p - 1][j];
+    }
+    if (tid < P) {
+      const double x = cos(kPi * (tid + 0.5) / P);
+      a.tabs[tid] = x;
+      double t0 = 1.0, t1 = x;
+      Tk[0][tid] = 1.0;
+      if (P > 1) Tk[1][tid] = x;
+      for (int p = 2; p < P; ++p) {
+        const double t2 = 2.0 * x * t1 - t0;
+        Tk[p][tid] = t2;
+        t0 = t1;
+        t1 = t2;
+      }
+    }
+    __syncthreads();
+    for (int w = tid; w < P * P; w += blockDim.x) {
+      const int j = w / P, k = w % P;
+      double s = 0.0;
+      for (int p = 0; p < P; ++p) s += tp[p][j] * (p ? 2.0 : 1.0) / P * Tk[p][k];
+      a.tabs[kT2PMax * kT2PMax + j * kT2PMax + k] = s;                   // W[j][k]
+      a.tabs[2 * kT2PMax * kT2PMax + k * kT2PMax + j] = (j ? 2.0 : 1.0) / P * Tk[j][k];  // lambda[k][p=j]
+    }
+    return;
+  }
+  // Bessel table, one thread per bin
+  const int m = (blockIdx.x - 1) * blockDim.x + threadIdx.x;
+  const int Pg = pl.Pg;
+  if (m >= a.n_f || Pg == 0) return;
+  const double z0 = 2.0 * kPi * (double)(m - a.n_f / 2) * pl.delta_g;
+  const double z = fabs(z0);
+  double J[kT2PgMax];
+  if (z < 1e-12) {
+    for (int p = 0; p < Pg; ++p) J[p] = p == 0 ? 1.0 : 0.0;
+  } else {
+    const int top = min(200, Pg + 24 + (int)z);
+    double jp1 = 0.0, jp = 1e-30, norm = 0.0;
+    for (int k = top; k >= 1; --k) {
+      if (k < Pg) J[k] = jp;
+      if ((k & 1) == 0) norm += 2.0 * jp;
+      const double jm1 = (2.0 * k / z) * jp - jp1;
+      jp1 = jp;
+      jp = jm1;
+      if (fabs(jp) > 1e200) {
+        jp *= 1e-200; jp1 *= 1e-200; norm *= 1e-200;
+        for (int q = k; q < Pg; ++q) J[q] *= 1e-200;
+      }
+    }
+    J[0] = jp;
+    norm += jp;
+    for (int p = 0; p < Pg; ++p) J[p] /= norm;
+  }
+  for (int p = 0; p < Pg; ++p) {
+    double v = (p == 0 ? 1.0 : 2.0) * J[p];
+    if (z0 < 0.0 && (p & 1)) v = -v;
+    const int q = p & 3;                              // (-j)^p = 1, -j, -1, j
+    const float2 c = q == 0 ? make_float2((float)v, 0.f)
+                   : q == 1 ? make_float2(0.f, (float)-v)
+                   : q == 2 ? make_float2((float)-v, 0.f)
+                            : make_float2(0.f, (float)v);
+    a.acoef[(int64_t)m * kT2PgMax + p] = c;
+  }
+}
+
+}  // namespace
+
+cudaError_t t2_sort(const T2Args &a, const T2Points &pts, const T2Sorted &srt, cudaStream_t st) {
+  ProfScope prof(kProfSort, st);
+  const int nb = (int)std::max<int64_t>(1, (pts.n + kT2SortBlock - 1) / kT2SortBlock);
+  const size_t sm = (size_t)32 * kT2Max * sizeof(int);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k2_write, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k2_count<<<nb, kT2SortBlock, sm, st>>>(a.plan, pts, srt);
+  k2_scan<<<1, kT2Max, 0, st>>>(a.plan, pts.n_dev, pts.n, srt);
+  k2_write<<<nb, kT2SortBlock, sm, st>>>(a.plan, pts, srt);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(3);
+  return e;
+}
+
+cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, int n_sms,
+                    cudaStream_t st) {
+  (void)n_sms;
+  cudaError_t e;
+  {
+  ProfScope prof(kProfPlan, st);
+  k2_box<<<kT2BoxBlocks, 256, 0, st>>>(pts, a.box_part);
+  double *cost = reinterpret_cast<double *>(a.tabs + 3 * kT2PMax * kT2PMax);   // [kT2Cand]
+  k2_cand<<<kT2Cand, 256, 0, st>>>(a.box_part, kT2BoxBlocks, a, pts.n, pts.n_dev, cost);
+  k2_pick<<<1, 128, 0, st>>>(a.box_part, kT2BoxBlocks, cost, a.plan, pts.n, pts.n_dev);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  add_launches(3);
+  }
+  if ((e = t2_sort(a, pts, srt, st)) != cudaSuccess) return e;
+  ProfScope prof(kProfPlan, st);
+  k2_tbox<<<kT2Max, 256, 0, st>>>(a.plan, srt, a.tbox);
+  k2_tsetup<<<(unsigned)((a.n_a + 127) / 128), 128, 0, st>>>(a, srt.tstart);
+  k2_gsetup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
+  k2_select<<<1, 1, 0, st>>>(a);
+  k2_tables<<<1 + (a.n_f + 127) / 128, 128, 0, st>>>(a);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
+  return e;
+}
+
+// ============================================================================ adjoint prep
+namespace {
+
+constexpr int kGexpThreads = 256;
+
+// G[row][i][q] = sum_m X_row,i[m] e^{+j 2 pi m' u_g,i} conj(a[m][q]), q < Pg; one CTA per antenna
+__global__ void __launch_bounds__(kGexpThreads) k2_gexp(T2Args a, const float2 *X0,
+                                                        const float2 *X1) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0 || pl.Pg == 0) return;
+  extern __shared__ float2 ys[];                    // [n_f] rotated row, then [4][64] partials
+  const int Pg = pl.Pg;
+  const int64_t i = blockIdx.x;
+  const int N = a.n_f;
+  const double ug = a.lg[i * 3] * a.kd;
+  float2 *part = ys + N;
+  const int nrow = X1 ? 2 : 1;
+  for (int row = 0; row < nrow; ++row) {
+    const float2 *X = (row == 0 ? X0 : X1) + i * N;
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+      const double c = (double)(m - N / 2) * ug;
+      float ps, pc;                                  // e^{+j 2 pi m' u_g}
+      sincospif(2.f * (float)(c - rint(c)), &ps, &pc);
+      const float2 v = X[m];
+      ys[m] = make_float2(fmaf(pc, v.x, -ps * v.y), fmaf(pc, v.y, ps * v.x));
+    }
+    __syncthreads();
+    const int q = threadIdx.x & 63, r = threadIdx.x >> 6;    // 64 x 4
+    float re = 0.f, im = 0.f;
+    if (q < Pg)
+      for (int m = r; m < N; m += 4) {
+        const float2 c = a.acoef[(int64_t)m * kT2PgMax + q], y = ys[m];   // y conj(c)
+        re = fmaf(y.x, c.x, fmaf(y.y, c.y, re));
+        im = fmaf(y.y, c.x, fmaf(-y.x, c.y, im));
+      }
+    part[r * 64 + q] = make_float2(re, im);
+    __syncthreads();
+    if (threadIdx.x < Pg) {
+      float2 v = part[threadIdx.x];
+      for (int rr = 1; rr < 4; ++rr) {
+        v.x += part[rr * 64 + threadIdx.x].x;
+        v.y += part[rr * 64 + threadIdx.x].y;
+      }
+      a.gexp[((int64_t)row * a.n_a + i) * kT2PgMax + threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// per (antenna, tile): F at the tile's P Chebyshev nodes (global expansion, or the direct bin sum
+// when Pg == 0), then the monomial coefficients c_j = sum_k W[j][k] F_k in fp64.  CTA = one
+// antenna x 128 tiles (the antenna's expansion broadcast from shared memory).
+__global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, const float2 *X0,
+                                                const float2 *X1) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0) return;
+  const int P = pl.P, Pg = pl.Pg, T = pl.T;
+  const int64_t i = blockIdx.x;
+  const int t = blockIdx.y * blockDim.x + threadIdx.x;
+  const int nrow = X1 ? 2 : 1;
+  __shared__ float2 G[2][kT2PgMax];
+  __shared__ double W[kT2PMax][kT2PMax];
+  __shared__ double xk[kT2PMax];
+  for (int w = threadIdx.x; w < nrow * kT2PgMax; w += blockDim.x) {
+    const int row = w / kT2PgMax, q = w % kT2PgMax;
+    G[row][q] = Pg ? a.gexp[((int64_t)row * a.n_a + i) * kT2PgMax + q] : make_float2(0.f, 0.f);
+  }
+  for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
+    W[w / kT2PMax][w % kT2PMax] = a.tabs[kT2PMax * kT2PMax + w];
+  if (threadIdx.x < kT2PMax) xk[threadIdx.x] = a.tabs[threadIdx.x];
+  __syncthreads();
+  if (t >= T || tstart[t + 1] == tstart[t]) return;
+  const double uc = a.lc[(int64_t)t * a.n_a + i] * a.kd;
+  const double ug = a.lg[i * 3] * a.kd;
+  double Fr[2][kT2PMax], Fi[2][kT2PMax];
+  for (int k = 0; k < P; ++k) {
+    const double u = uc + pl.delta_t * xk[k];
+    if (Pg) {
+      // Clenshaw in fp32 on y = (u - u_g) / delta_g in [-1, 1]
+      const float y = (float)((u - ug) / pl.delta_g), y2 = 2.f * y;
+      for (int row = 0; row < nrow; ++row) {
+        float b1r = 0.f, b1i = 0.f, b2r = 0.f, b2i = 0.f;
+        for (int q = Pg - 1; q >= 1; --q) {
+          const float br = fmaf(y2, b1r, G[row][q].x - b2r), bi = fmaf(y2, b1i, G[row][q].y - b2i);
+          b2r = b1r; b2i = b1i;
+          b1r = br; b1i = bi;
+        }
+        Fr[row][k] = (double)fmaf(y, b1r, G[row][0].x - b2r);
+        Fi[row][k] = (double)fmaf(y, b1i, G[row][0].y - b2i);
+      }
+    } else {
+      // direct: F(u) = sum_m X[m] e^{+j 2 pi m' u} (wide global spread)
+      for (int row = 0; row < nrow; ++row) {
+        const float2 *X = (row == 0 ? X0 : X1) + i * a.n_f;
+        double sr = 0.0, si = 0.0;
+        for (int m = 0; m < a.n_f; ++m) {
+          const double c = (double)(m - a.n_f / 2) * u;
+          double ps, pc;
+          sincospi(2.0 * (c - rint(c)), &ps, &pc);
+          const float2 v = X[m];
+          sr += pc * v.x - ps * v.y;
+          si += pc * v.y + ps * v.x;
+        }
+        Fr[row][k] = sr;
+        Fi[row][k] = si;
+      }
+    }
+  }
+  for (int row = 0; row < nrow; ++row) {
+    float2 *dst = a.coef + (((int64_t)row * T + t) * a.n_a + i) * P;
+    for (int j = 0; j < P; ++j) {
+      double cr = 0.0, ci = 0.0;
+      for (int k = 0; k < P; ++k) {
+        cr = fma(W[j][k], Fr[row][k], cr);
+        ci = fma(W[j][k], Fi[row][k], ci);
+      }
+      dst[j] = make_float2((float)cr, (float)ci);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0, const float2 *X1,
+                            cudaStream_t st) {
+  if (a.n_a <= 0) return cudaSuccess;
+  ProfScope prof(kProfPrep, st);
+  const size_t sm = ((size_t)a.n_f + 4 * 64) * sizeof(float2);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k2_gexp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  k2_gexp<<<(unsigned)a.n_a, kGexpThreads, sm, st>>>(a, X0, X1);
+  dim3 g((unsigned)a.n_a, (unsigned)((kT2Max + 127) / 128));
+  k2_cprep<<<g, 128, 0, st>>>(a, tstart, X0, X1);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(2);
+  return e;
+}
+
+
+// ================================================================================= sweeps
+namespace {
+
+// work item -> tile (binary search over the work-item starts)
+__device__ __forceinline__ int t2_item_tile(const int *cstart, int T, int item) {
+  int lo = 0, hi = T;                             // cstart[lo] <= item < cstart[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (cstart[mid] <= item) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// per point pair: tile-relative geometry (DESIGN 5d): d - d_a = delta / (sqrt(D + delta) + d_a),
+// delta = |q'|^2 - 2 a'.q'; centre phase cycles = frac(2 d_a kc) + 2 kc (d - d_a) reduced to
+// [-1/2, 1/2]; x = (2 d_a - L_c) inv + 2 inv (d - d_a).  NEG: returns (cos, -sin).
+struct Geo2 {
+  f2x c, s, x, r;                                 // cos, sin of the centre phase, x, 1/d
+};
+template <bool NEG>
+__device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x qx, f2x qy, f2x qz,
+                                        f2x qw, float kc2f, float inv2f) {
+  const f2x del = ffma2(bcv(g0.x), qx, ffma2(bcv(g0.y), qy, ffma2(bcv(g0.z), qz, qw)));
+  const f2x s2 = fadd2(bcv(g0.w), del);
+  const float2 s2v = upk(s2);
+  const f2x r = pk(rsq_ftz(s2v.x), rsq_ftz(s2v.y));
+  const f2x dd = fmul2(s2, r);
+  const float2 den = upk(fadd2(dd, bcv(g1.x)));
+  const f2x dl = fmul2(del, pk(rcp_ftz_(den.x), rcp_ftz_(den.y)));
+  const f2x cy = ffma2(dl, bcv(kc2f), bcv(g1.y));
+  // reduce to [-1/2, 1/2] by round-to-nearest with the 1.5 * 2^23 magic constant on the FMA pipe
+  // (|cy| < 2^22; the XU pipe is the other bound of this loop: 4 MUFU per pair)
+  const f2x rn = fadd2(fadd2(cy, bcv(12582912.f)), bcv(-12582912.f));
+  const f2x ang = fmul2(ffma2(rn, bcv(-1.f), cy), bcv(NEG ? -kTwoPi : kTwoPi));
+  const float2 av = upk(ang);
+  Geo2 o;
+  float s0, c0, s1, c1;
+  sc_ftz(av.x, s0, c0);
+  sc_ftz(av.y, s1, c1);
+  o.c = pk(c0, c1);
+  o.s = pk(s0, s1);
+  o.x = ffma2(dl, bcv(inv2f), bcv(g1.z));
+  o.r = r;
+  return o;
+}
+
+constexpr int kT2GA = 16;                         // antennas per shared-memory stage
+
+// stage the coefficients (reversed: cs[aa][k] = c_{P-1-k}) and the geometry of antennas
+// [i0, i0 + ga) of tile t
+template <int P>
+__device__ __forceinline__ void t2_stage(const T2Args &a, const T2Plan &pl, int row, int t,
+                                         int64_t i0, int ga, float2 (*cs)[kT2PMax],
+                                         float4 (*gs)[2]) {
+  const float2 *src = a.coef + (((int64_t)row * pl.T + t) * a.n_a + i0) * P;
+  for (int w = threadIdx.x; w < ga * P; w += blockDim.x) {
+    const int aa = w / P, j = w % P;
+    cs[aa][P - 1 - j] = src[w];
+  }
+  if ((int)threadIdx.x < ga) {
+    const float4 *g = a.tgeo + ((int64_t)t * a.n_a + i0 + threadIdx.x) * 2;
+    float4 g1 = g[1];
+    g1.z = (float)((double)g1.z * pl.inv_t);       // x at the antenna's tile distance d_a
+    gs[threadIdx.x][0] = g[0];
+    gs[threadIdx.x][1] = g1;
+  }
+}
+
+// h = sum_j c_j x^j for two points (packed x), coefficients reversed in cs (P even, unrolled)
+template <int P>
+__device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x &h1) {
+  const float2 xv = upk(x);
+  const f2x x0 = bcv(xv.x), x1 = bcv(xv.y);
+  const float4 c01 = *reinterpret_cast<const float4 *>(cs);
+  const f2x p0 = pk(c01.x, c01.y), p1 = pk(c01.z, c01.w);
+  h0 = ffma2(x0, p0, p1);
+  h1 = ffma2(x1, p0, p1);
+#pragma unroll
+  for (int k = 2; k < P; k += 2) {
+    const float4 c = *reinterpret_cast<const float4 *>(cs + k);
+    const f2x pa = pk(c.x, c.y), pb = pk(c.z, c.w);
+    h0 = ffma2(x0, ffma2(x0, h0, pa), pb);
+    h1 = ffma2(x1, ffma2(x1, h1, pa), pb);
+  }
+}
+
+// ------------------------------------------------------------------------- filter sweep
+// work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
+template <int P>
+__device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
+                                               int row, float2 *__restrict__ out, int64_t n_out,
+                                               int n_splits, int64_t aps, float2 (*cs)[kT2PMax],
+                                               float4 (*gs)[2]) {
+  const int total = *s.n_items * n_splits;
+  const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int item = w / n_splits, split = w % n_splits;
+    const int t = t2_item_tile(s.cstart, pl.T, item);
+    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * kT2FltChunk;
+    const int64_t end = s.tstart[t + 1];
+    const float *tb = a.tbox + t * 6;
+    const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
+    float qp[4][4];
+    bool valid[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = base + threadIdx.x + u * 128;
+      valid[u] = k < end;
+      const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
+      qp[u][0] = v.x - cx; qp[u][1] = v.y - cy; qp[u][2] = v.z - cz;
+      qp[u][3] = fmaf(qp[u][0], qp[u][0], fmaf(qp[u][1], qp[u][1], qp[u][2] * qp[u][2]));
+    }
+    const f2x qx01 = pk(qp[0][0], qp[1][0]), qy01 = pk(qp[0][1], qp[1][1]),
+              qz01 = pk(qp[0][2], qp[1][2]), qw01 = pk(qp[0][3], qp[1][3]);
+    const f2x qx23 = pk(qp[2][0], qp[3][0]), qy23 = pk(qp[2][1], qp[3][1]),
+              qz23 = pk(qp[2][2], qp[3][2]), qw23 = pk(qp[2][3], qp[3][3]);
+    f2x A1[4], A2[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
+    const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA) {
+      const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
+      __syncthreads();
+      t2_stage<P>(a, pl, row, t, i0, ga, cs, gs);
+      __syncthreads();
+#pragma unroll 1
+      for (int aa = 0; aa < ga; ++aa) {
+        const float4 g0 = gs[aa][0], g1 = gs[aa][1];
+        const Geo2 e01 = t2_geo2<false>(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
+        const Geo2 e23 = t2_geo2<false>(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
+        f2x h[4];
+        t2_horner2<P>(cs[aa], e01.x, h[0], h[1]);
+        t2_horner2<P>(cs[aa], e23.x, h[2], h[3]);
+        const float2 c01 = upk(e01.c), s01 = upk(e01.s), c23 = upk(e23.c), s23 = upk(e23.s);
+        A1[0] = ffma2(bcv(c01.x), h[0], A1[0]); A2[0] = ffma2(bcv(s01.x), h[0], A2[0]);
+        A1[1] = ffma2(bcv(c01.y), h[1], A1[1]); A2[1] = ffma2(bcv(s01.y), h[1], A2[1]);
+        A1[2] = ffma2(bcv(c23.x), h[2], A1[2]); A2[2] = ffma2(bcv(s23.x), h[2], A2[2]);
+        A1[3] = ffma2(bcv(c23.y), h[3], A1[3]); A2[3] = ffma2(bcv(s23.y), h[3], A2[3]);
+      }
+    }
+    float2 *o = out + (int64_t)split * n_out;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (valid[u]) {
+        const float2 p1 = upk(A1[u]), p2 = upk(A2[u]);   // M = A1 + j A2
+        o[s.perm[base + threadIdx.x + u * 128]] = make_float2(p1.x - p2.y, p1.y + p2.x);
+      }
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
+                                                       float2 *__restrict__ out, int64_t n_out,
+                                                       int n_splits, int64_t aps) {
+  const T2Plan pl = *a.plan;
+  __shared__ __align__(16) float2 cs[kT2GA][kT2PMax];
+  __shared__ float4 gs[kT2GA][2];
+  switch (pl.P) {
+    case 8: k2_filter_body<8>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
+    case 10: k2_filter_body<10>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
+    case 12: k2_filter_body<12>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
+    case 14: k2_filter_body<14>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
+    case 16: k2_filter_body<16>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
+    default: break;
+  }
+}
+
+// ------------------------------------------------------------------------- backward sweep
+// Monostatic, no Eq. 7 correction: T_t = T_r = T_j, chi = [T_j > 0], g = max(2 (n.w)^2 - 1, 0),
+// dg/dn = 4 (n.w) w, gamma = 1 / (16 pi^2 d^2) (Eq. 5, gain P:L679-683), so per sample
+//   S1 = T^2 U,  S2 = 2 T chi U,  S3 = T^2 V,  U = sum_i R g gamma,  V = sum_i R gamma dg/dn
+// with R = Re(E h) (App. A.5).  Thread = 2 active samples (one packed pair).
+template <int P>
+__device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
+                                            int row, float *__restrict__ out, int64_t n_out,
+                                            int n_splits, int64_t aps, bool no_gain,
+                                            float2 (*cs)[kT2PMax], float4 (*gs)[2]) {
+  const int total = *s.n_items * n_splits;
+  const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int item = w / n_splits, split = w % n_splits;
+    const int t = t2_item_tile(s.cstart, pl.T, item);
+    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * kT2BwdChunk;
+    const int64_t end = s.tstart[t + 1];
+    const float *tb = a.tbox + t * 6;
+    const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
+    float qp[2][4], nv[2][3], Tj[2];
+    bool valid[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t k = base + threadIdx.x + u * 128;
+      valid[u] = k < end;
+      const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
+      const float4 n4 = valid[u] ? s.aux[k] : make_float4(0.f, 0.f, 1.f, 0.f);
+      qp[u][0] = v.x - cx; qp[u][1] = v.y - cy; qp[u][2] = v.z - cz;
+      qp[u][3] = fmaf(qp[u][0], qp[u][0], fmaf(qp[u][1], qp[u][1], qp[u][2] * qp[u][2]));
+      nv[u][0] = n4.x; nv[u][1] = n4.y; nv[u][2] = n4.z;
+      Tj[u] = n4.w;
+    }
+    const f2x qx = pk(qp[0][0], qp[1][0]), qy = pk(qp[0][1], qp[1][1]), qz = pk(qp[0][2], qp[1][2]),
+              qw = pk(qp[0][3], qp[1][3]);
+    const f2x nx = pk(nv[0][0], nv[1][0]), ny = pk(nv[0][1], nv[1][1]), nz = pk(nv[0][2], nv[1][2]);
+    // n . q' per sample
+    const f2x nq = ffma2(nx, qx, ffma2(ny, qy, fmul2(nz, qz)));
+    f2x U = 0ull, SF = 0ull, Wx = 0ull, Wy = 0ull, Wz = 0ull;
+    const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA) {
+      const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
+      __syncthreads();
+      t2_stage<P>(a, pl, row, t, i0, ga, cs, gs);
+      __syncthreads();
+#pragma unroll 1
+      for (int aa = 0; aa < ga; ++aa) {
+        const float4 g0 = gs[aa][0], g1 = gs[aa][1];
+        const Geo2 e = t2_geo2<true>(g0, g1, qx, qy, qz, qw, kc2f, inv2f);   // (cos, -sin)
+        f2x h0, h1;
+        t2_horner2<P>(cs[aa], e.x, h0, h1);
+        // R = Re(E h) = c hr - s hi
+        const float2 hv0 = upk(h0), hv1 = upk(h1);
+        const f2x R = ffma2(e.c, pk(hv0.x, hv1.x), fmul2(e.s, pk(hv0.y, hv1.y)));
+        const f2x r2 = fmul2(e.r, e.r);
+        // -a' = g0.xyz / 2:  n.(q' - a') = n.q' + n.(g0/2)
+        const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
+        const f2x nd = ffma2(nx, h0x, ffma2(ny, h0y, ffma2(nz, h0z, nq)));
+        const f2x Rr2 = fmul2(R, r2);
+        if (no_gain) {                               // E11 ablation: g = 1, dg/dn = 0
+          U = fadd2(U, Rr2);
+          continue;
+        }
+        const f2x ndr2 = fmul2(nd, r2);              // (n.w) / d
+        const f2x g = ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f));   // 2 (n.w)^2 - 1
+        const float2 gv = upk(g);
+        const f2x gpos = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
+        const f2x msk = pk(gv.x > 0.f ? 1.f : 0.f, gv.y > 0.f ? 1.f : 0.f);
+        U = ffma2(Rr2, gpos, U);
+        const f2x F = fmul2(fmul2(Rr2, ndr2), msk);  // R gamma 4 (n.w) / d without 4 / (4 pi)^2
+        SF = fadd2(SF, F);
+        Wx = ffma2(F, h0x, Wx);
+        Wy = ffma2(F, h0y, Wy);
+        Wz = ffma2(F, h0z, Wz);
+      }
+    }
+    float *o = out + (int64_t)split * 5 * n_out;
+    const float2 Uv = upk(U), SFv = upk(SF), Wxv = upk(Wx), Wyv = upk(Wy), Wzv = upk(Wz);
+    const float Us[2] = {Uv.x, Uv.y}, SFs[2] = {SFv.x, SFv.y}, Wxs[2] = {Wxv.x, Wxv.y},
+                Wys[2] = {Wyv.x, Wyv.y}, Wzs[2] = {Wzv.x, Wzv.y};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!valid[u]) continue;
+      const int k = (int)(base + threadIdx.x + u * 128);
+      const int64_t j = s.perm[k];                              // compacted index
+      const float T = Tj[u], TT = T * T;
+      const float u16 = Us[u] * kInv16Pi2f;
+      const float f4 = 4.f * kInv16Pi2f * TT;
+      o[j] = TT * u16;                                          // S1
+      o[n_out + j] = T > 0.f ? 2.f * T * u16 : 0.f;             // S2
+      o[2 * n_out + j] = f4 * fmaf(qp[u][0], SFs[u], Wxs[u]);   // S3 = T^2 sum F (q' - a')
+      o[3 * n_out + j] = f4 * fmaf(qp[u][1], SFs[u], Wys[u]);
+      o[4 * n_out + j] = f4 * fmaf(qp[u][2], SFs[u], Wzs[u]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, 4) k2_bwd(T2Args a, T2Sorted s, int row,
+                                                 float *__restrict__ out, int64_t n_out,
+                                                 int n_splits, int64_t aps, bool no_gain) {
+  const T2Plan pl = *a.plan;
+  __shared__ __align__(16) float2 cs[kT2GA][kT2PMax];
+  __shared__ float4 gs[kT2GA][2];
+  switch (pl.P) {
+    case 8: k2_bwd_body<8>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
+    case 10: k2_bwd_body<10>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
+    case 12: k2_bwd_body<12>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
+    case 14: k2_bwd_body<14>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
+    case 16: k2_bwd_body<16>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
+    default: break;
+  }
+}
+
+// fixed-order sum of the split partials [S][5][n_c] of the compacted list, scattered to the
+// sample index: out[r][idx[c]] (idx NULL: c itself)
+__global__ void k2_bsum(const T2Plan *plp, const float *__restrict__ part, int S, int64_t n_c,
+                        const int64_t *n_dev, const int *__restrict__ idx, float *__restrict__ out,
+                        int64_t n_s) {
+  if (plp->P == 0) return;
+  const int64_t n = n_dev ? *n_dev : n_c;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx ? (int64_t)idx[c] : c;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      float v = 0.f;
+      for (int sp = 0; sp < S; ++sp) v += part[((int64_t)sp * 5 + r) * n_c + c];
+      out[(int64_t)r * n_s + j] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------- forward sweep
+// work item = (tile, block of kT2FwdAnts antennas); thread = antenna, the tile's sorted records
+// staged through shared memory; Chebyshev moments M[t][i][p] = sum_j c_ij T_p(x_ij) with
+// c_ij = A_ij e^{-j 2 pi f_c tau_ij} (trace: A = w g gamma T^2, Eq. 5) or the K5 weight c_q.
+constexpr int kT2FwdTJ = kT2FwdAnts;             // records per shared-memory stage (one per thread)
+
+struct FwdStage {
+  float4 q[2][kT2FwdTJ];                          // q' = q - c_t, |q'|^2
+  float4 r[2][kT2FwdTJ];                          // trace: (w T^2, n.q', -, -); K5: (Re c, Im c)
+  float4 n[2][kT2FwdTJ];                          // trace: normal
+};
+
+template <int P, int KIND>
+__device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
+                                            bool no_gain, FwdStage &sm) {
+  const int nab = (int)((a.n_a + kT2FwdAnts - 1) / kT2FwdAnts);
+  const int total = pl.T * nab;
+  const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int t = w / nab, ab = w % nab;
+    const int64_t j_lo = s.tstart[t], j_hi = s.tstart[t + 1];
+    if (j_hi == j_lo) continue;
+    const int64_t i = (int64_t)ab * kT2FwdAnts + threadIdx.x;
+    const bool ok = i < a.n_a;
+    const float *tb = a.tbox + t * 6;
+    const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
+    float4 g0 = make_float4(0.f, 0.f, 0.f, 1.f), g1 = make_float4(1.f, 0.f, 0.f, 0.f);
+    if (ok) {
+      const float4 *g = a.tgeo + ((int64_t)t * a.n_a + i) * 2;
+      g0 = g[0];
+      g1 = g[1];
+      g1.z = (float)((double)g1.z * pl.inv_t);
+    }
+    const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
+    f2x M[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) M[p] = 0ull;
+    // this thread's record of the next stage, prefetched into registers
+    float4 pv = make_float4(cx, cy, cz, 0.f), pn = make_float4(0.f, 0.f, 1.f, 0.f);
+    if (j_lo + threadIdx.x < j_hi) { pv = s.pos[j_lo + threadIdx.x]; pn = s.aux[j_lo + threadIdx.x]; }
+    int b = 0;
+    for (int64_t jt = j_lo; jt < j_hi; jt += kT2FwdTJ, b ^= 1) {
+      {
+        const float x = pv.x - cx, y = pv.y - cy, z = pv.z - cz;
+        sm.q[b][threadIdx.x] = make_float4(x, y, z, fmaf(x, x, fmaf(y, y, z * z)));
+        if (KIND == kFwdTrace) {
+          sm.r[b][threadIdx.x] =
+              make_float4(pv.w * pn.w * pn.w, fmaf(pn.x, x, fmaf(pn.y, y, pn.z * z)), 0.f, 0.f);
+          sm.n[b][threadIdx.x] = make_float4(pn.x, pn.y, pn.z, 0.f);
+        } else {
+          sm.r[b][threadIdx.x] = make_float4(pv.w, pn.w, 0.f, 0.f);   // K5: w = Re c, T = Im c
+        }
+      }
+      __syncthreads();
+      const int64_t jn = jt + kT2FwdTJ + threadIdx.x;       // prefetch the next stage
+      pv = make_float4(cx, cy, cz, 0.f);
+      pn = make_float4(0.f, 0.f, 1.f, 0.f);
+      if (jn < j_hi) { pv = s.pos[jn]; pn = s.aux[jn]; }
+      const int nv = (int)min((int64_t)kT2FwdTJ, j_hi - jt);
+#pragma unroll 1
+      for (int jj = 0; jj < nv; jj += 2) {
+        const float4 qa = sm.q[b][jj], qb = sm.q[b][jj + 1];
+        const Geo2 e = t2_geo2<true>(g0, g1, pk(qa.x, qb.x), pk(qa.y, qb.y), pk(qa.z, qb.z),
+                                     pk(qa.w, qb.w), kc2f, inv2f);    // (cos, -sin)
+        const float4 ra = sm.r[b][jj], rb = sm.r[b][jj + 1];
+        f2x cre, cim;
+        if (KIND == kFwdTrace) {
+          const f2x r2 = fmul2(e.r, e.r);
+          f2x gg;
+          if (no_gain) {
+            gg = bcv(1.f);
+          } else {
+            const float4 na = sm.n[b][jj], nb = sm.n[b][jj + 1];
+            const f2x nd = ffma2(pk(na.x, nb.x), h0x,
+                                 ffma2(pk(na.y, nb.y), h0y, ffma2(pk(na.z, nb.z), h0z, pk(ra.y, rb.y))));
+            const f2x ndr2 = fmul2(nd, r2);
+            const float2 gv = upk(ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f)));
+            gg = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
+          }
+          // A = w T^2 g gamma; c = A e^{-j theta} = (A cos, A (-sin))
+          const f2x A = fmul2(fmul2(pk(ra.x, rb.x), gg), fmul2(r2, bcv(kInv16Pi2f)));
+          cre = fmul2(A, e.c);
+          cim = fmul2(A, e.s);
+        } else {
+          // c = (Ar + j Ai) e^{-j theta} = (Ar cos - Ai (-sin), Ai cos + Ar (-sin))
+          const f2x Ar = pk(ra.x, rb.x), Ai = pk(ra.y, rb.y);
+          cre = ffma2(Ar, e.c, fmul2(Ai, fmul2(e.s, bcv(-1.f))));
+          cim = ffma2(Ai, e.c, fmul2(Ar, e.s));
+        }
+        const float2 crv = upk(cre), civ = upk(cim);
+        const f2x c0 = pk(crv.x, civ.x), c1 = pk(crv.y, civ.y);
+        // plain recurrence on v_p = s_p T_p(x), s = (+ + - -); M'[p] = s_p M[p]
+        const f2x x = e.x, tp = fadd2(x, x), tn = fmul2(x, bcv(-2.f));
+        const float2 xv = upk(x);
+        M[0] = fadd2(M[0], fadd2(c0, c1));
+        M[1] = ffma2(bcv(xv.x), c0, ffma2(bcv(xv.y), c1, M[1]));
+        f2x v2 = bcv(1.f), v1 = x;
+#pragma unroll
+        for (int p = 2; p < P; ++p) {
+          const f2x v = ffma2((p & 1) ? tp : tn, v1, v2);
+          v2 = v1;
+          v1 = v;
+          const float2 wv = upk(v);
+          M[p] = ffma2(bcv(wv.x), c0, ffma2(bcv(wv.y), c1, M[p]));
+        }
+      }
+    }
+    __syncthreads();                                  // the stage buffers are reused by the next item
+    if (ok) {
+      float2 *dst = a.mom + ((int64_t)t * a.n_a + i) * P;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        float2 v = upk(M[p]);
+        if ((p >> 1) & 1) { v.x = -v.x; v.y = -v.y; }
+        dst[p] = v;
+      }
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kT2FwdAnts, 4) k2_fwd(T2Args a, T2Sorted s, bool no_gain) {
+  const T2Plan pl = *a.plan;
+  __shared__ FwdStage sm;
+  switch (pl.P) {
+    case 8: k2_fwd_body<8, KIND>(a, pl, s, no_gain, sm); break;
+    case 10: k2_fwd_body<10, KIND>(a, pl, s, no_gain, sm); break;
+    case 12: k2_fwd_body<12, KIND>(a, pl, s, no_gain, sm); break;
+    case 14: k2_fwd_body<14, KIND>(a, pl, s, no_gain, sm); break;
+    case 16: k2_fwd_body<16, KIND>(a, pl, s, no_gain, sm); break;
+    default: break;
+  }
+}
+
+// ------------------------------------------------------------------------- forward output
+// per antenna: tile t's moments -> P virtual sources at the nodes u_tk = u_c,it + delta_t x_k with
+// weights W_tk = sum_p lambda[k][p] M_t[p] (Chebyshev interpolation of e^{-j z x}); global moments
+// Mg[q] = sum_{t,k} W_tk T_q(y_tk), y = (u - u_g) / delta_g; bins
+// s[m] = e^{-j 2 pi m' u_g} sum_q a[m][q] Mg[q] (or, Pg == 0, the direct sum over the sources)
+constexpr int kT2OutThreads = 256;
+__global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *tstart,
+                                                         float2 *__restrict__ out) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0) return;
+  extern __shared__ unsigned char smraw[];
+  const int P = pl.P, T = pl.T, Pg = pl.Pg;
+  const int nv = T * P;
+  float *ys = reinterpret_cast<float *>(smraw);                        // [nv]
+  float2 *wsrc = reinterpret_cast<float2 *>(smraw + (size_t)nv * 4 + 8 * ((nv & 1) ? 1 : 0)); // [nv]
+  float2 *red = wsrc + nv;                                             // [256][16]
+  __shared__ double lam[kT2PMax][kT2PMax];
+  __shared__ double xk[kT2PMax];
+  __shared__ float2 Mg[kT2PgMax];
+  const int64_t i = blockIdx.x;
+  for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
+    lam[w / kT2PMax][w % kT2PMax] = a.tabs[2 * kT2PMax * kT2PMax + w];
+  if (threadIdx.x < kT2PMax) xk[threadIdx.x] = a.tabs[threadIdx.x];
+  __syncthreads();
+  const double ug = a.lg[i * 3] * a.kd;
+  // virtual sources (empty tiles: weight 0 at y = 0)
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const int t = v / P, k = v % P;
+    float2 wv = make_float2(0.f, 0.f);
+    float y = 0.f;
+    if (tstart[t + 1] > tstart[t]) {
+      const float2 *Mt = a.mom + ((int64_t)t * a.n_a + i) * P;
+      double wr = 0.0, wi = 0.0;
+      for (int p = 0; p < P; ++p) {
+        const float2 mv = Mt[p];
+        wr = fma(lam[k][p], (double)mv.x, wr);
+        wi = fma(lam[k][p], (double)mv.y, wi);
+      }
+      wv = make_float2((float)wr, (float)wi);
+      const double u = a.lc[(int64_t)t * a.n_a + i] * a.kd + pl.delta_t * xk[k];
+      y = Pg ? (float)((u - ug) / pl.delta_g) : (float)(u - ug);   // direct: offset in cycles/bin
+    }
+    ys[v] = y;
+    wsrc[v] = wv;
+  }
+  __syncthreads();
+  if (Pg) {
+    for (int q0 = 0; q0 < Pg; q0 += 16) {
+      f2x acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = 0ull;
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const float y = ys[v], y2 = 2.f * y;
+        const float2 wv = wsrc[v];
+        const f2x wp = pk(wv.x, wv.y);
+        float t0 = 1.f, t1 = y;
+        for (int q = 0; q < q0; ++q) {               // T_q up to q0 (recomputed per chunk)
+          const float t2 = fmaf(y2, t1, -t0);
+          t0 = t1;
+          t1 = t2;
+        }
+        // now t0 = T_q0, t1 = T_q0+1
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          acc[q] = ffma2(bcv(t0), wp, acc[q]);
+          const float t2 = fmaf(y2, t1, -t0);
+          t0 = t1;
+          t1 = t2;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) red[q * kT2OutThreads + threadIdx.x] = upk(acc[q]);
+      __syncthreads();
+      for (int st = kT2OutThreads / 2; st > 0; st >>= 1) {   // fixed-order tree
+        if ((int)threadIdx.x < st)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float2 &d = red[q * kT2OutThreads + threadIdx.x];
+            const float2 e = red[q * kT2OutThreads + threadIdx.x + st];
+            d.x += e.x;
+            d.y += e.y;
+          }
+        __syncthreads();
+      }
+      if ((int)threadIdx.x < 16 && q0 + (int)threadIdx.x < Pg)
+        Mg[q0 + threadIdx.x] = red[threadIdx.x * kT2OutThreads];
+      __syncthreads();
+    }
+    for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
+      const float2 *cf = a.acoef + (int64_t)m * kT2PgMax;
+      float re = 0.f, im = 0.f;
+      for (int q = 0; q < Pg; ++q) {
+        const float2 c = cf[q], v = Mg[q];
+        re = fmaf(c.x, v.x, fmaf(-c.y, v.y, re));
+        im = fmaf(c.x, v.y, fmaf(c.y, v.x, im));
+      }
+      const double c = (double)(m - a.n_f / 2) * ug;
+      float ps, pc;                                   // e^{-j 2 pi m' u_g}
+      sincospif(2.f * (float)(c - rint(c)), &ps, &pc);
+      out[i * a.n_f + m] = make_float2(fmaf(pc, re, ps * im), fmaf(pc, im, -ps * re));
+    }
+  } else {
+    // direct: s[m] = sum_v W_v e^{-j 2 pi m' u_v}, u_v = u_g + ys[v]
+    for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
+      const double mc = (double)(m - a.n_f / 2);
+      double re = 0.0, im = 0.0;
+      for (int v = 0; v < nv; ++v) {
+        const double c = mc * (ug + (double)ys[v]);
+        double ps, pc;
+        sincospi(2.0 * (c - rint(c)), &ps, &pc);
+        const float2 wv = wsrc[v];
+        re += pc * wv.x + ps * wv.y;
+        im += pc * wv.y - ps * wv.x;
+      }
+      out[i * a.n_f + m] = make_float2((float)re, (float)im);
+    }
+  }
+}
+
+// fixed-order sum of [S][n] split partials into out (only when the plan applies)
+__global__ void k2_ssum(const T2Plan *plp, const float *__restrict__ part, int S, int64_t n,
+                        float *__restrict__ out) {
+  if (plp->P == 0) return;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int sp = 0; sp < S; ++sp) v += part[(int64_t)sp * n + k];
+    out[k] = v;
+  }
+}
+
+int occ_blocks(const void *k, int threads) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, 0) != cudaSuccess || n < 1) n = 1;
+  return n;
+}
+
+}  // namespace
+
+cudaError_t t2_sum_splits(const T2Args &a, const float *part, int S, int64_t n, float *out,
+                          int n_sms, cudaStream_t st) {
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)n_sms * 8);
+  k2_ssum<<<g, 256, 0, st>>>(a.plan, part, S, n, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(1);
+  return e;
+}
+
+cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out, int64_t n_out,
+                      int n_splits, int64_t ants_per_split, int n_sms, cudaStream_t st) {
+  if (a.n_a <= 0 || n_out <= 0) return cudaSuccess;
+  ProfScope prof(kProfFilter, st);
+  static int occ = 0;
+  if (!occ) occ = occ_blocks((const void *)k2_filter<5>, 128);
+  k2_filter<5><<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, out, n_out, n_splits,
+                                                        ants_per_split);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(1);
+  return e;
+}
+
+cudaError_t t2_backward(const T2Args &a, const T2Sorted &srt, int row, const int *idx,
+                        const int64_t *n_dev, int64_t n_c, float *part, float *out, int64_t n_s,
+                        int n_splits, int64_t ants_per_split, bool no_gain, int n_sms,
+                        cudaStream_t st) {
+  if (a.n_a <= 0 || n_c <= 0) return cudaSuccess;
+  static int occ = 0;
+  if (!occ) occ = occ_blocks((const void *)k2_bwd, 128);
+  {
+    ProfScope prof(kProfBackward, st);
+    k2_bwd<<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
+                                                    ants_per_split, no_gain);
+  }
+  const unsigned g = (unsigned)std::min<int64_t>((n_c + 255) / 256, (int64_t)n_sms * 8);
+  k2_bsum<<<g, 256, 0, st>>>(a.plan, part, n_splits, n_c, n_dev, idx, out, n_s);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(2);
+  return e;
+}
+
+cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_gain, float2 *out,
+                       int n_sms, cudaStream_t st) {
+  if (a.n_a <= 0) return cudaSuccess;
+  {
+  ProfScope prof(kProfForward, st);
+  if (kind == kFwdTrace) {
+    static int occ = 0;
+    if (!occ) occ = occ_blocks((const void *)k2_fwd<kFwdTrace>, kT2FwdAnts);
+    k2_fwd<kFwdTrace><<<(unsigned)(n_sms * occ), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+  } else {
+    static int occ = 0;
+    if (!occ) occ = occ_blocks((const void *)k2_fwd<kFwdMFAdj>, kT2FwdAnts);
+    k2_fwd<kFwdMFAdj><<<(unsigned)(n_sms * occ), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+  }
+  }
+  ProfScope prof(kProfForwardOut, st);
+  const size_t sm = (size_t)kT2TP * 12 + 16 + (size_t)kT2OutThreads * 16 * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k2_fout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k2_fout<<<(unsigned)a.n_a, kT2OutThreads, sm, st>>>(a, srt.tstart, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) add_launches(2);
+  return e;
+}
+
+}  // namespace rfr

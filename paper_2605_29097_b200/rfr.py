@@ -22,6 +22,7 @@ RFR_NO_GAIN = 1
 RFR_CHECK_FINITE = 2
 RFR_REUSE_BLEND = 4
 RFR_DIRECT = 8          # direct kernels instead of the Chebyshev-moment path (A/B)
+RFR_R1 = 16             # the r1 kernels instead of the r2 tiled engine (A/B)
 RFR_FLAG_DOMAIN = 1
 RFR_FLAG_NUMERIC = 2
 
@@ -57,6 +58,15 @@ class rfr_workspace(C.Structure):
                 ("n_ant", C.c_int64), ("n_freq", C.c_int32), ("n_query", C.c_int64)]
 
 
+class rfr_plan_info(C.Structure):
+    _fields_ = [("applied", C.c_int32), ("tiles", C.c_int32), ("lx", C.c_int32), ("ly", C.c_int32),
+                ("lz", C.c_int32), ("P", C.c_int32), ("Pg", C.c_int32), ("n_points", C.c_int32),
+                ("delta_t", C.c_double), ("delta_g", C.c_double)]
+
+
+SWEEPS = {"plan": 0, "sort": 1, "prep": 2, "filter": 3, "backward": 4, "forward": 5,
+          "forward_out": 6}
+
 STATUS = {0: "ok", 1: "invalid argument", 2: "shape mismatch or workspace too small",
           3: "domain", 4: "numeric", 5: "CUDA launch failure", 6: "unsupported", 7: "NCCL failure"}
 
@@ -64,7 +74,8 @@ EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_f
            "rfr_filter_power", "rfr_backward", "rfr_backward_partial", "rfr_backward_finish",
            "rfr_backward_filter", "rfr_backward_filter_partial", "rfr_filter_backward", "rfr_heatmap_loss",
            "rfr_comm_unique_id", "rfr_comm_init", "rfr_comm_destroy",
-           "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count")
+           "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count",
+           "rfr_plan_state", "rfr_profile_enable", "rfr_profile_read")
 
 
 class RfrError(RuntimeError):
@@ -101,6 +112,9 @@ def load(path: str = LIB_PATH):
         "rfr_filter_backward": [vp, vp, vp, f, A, G, vp, vp, vp, i64, vp, W, vp],
         "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, W, vp],
         "rfr_poll_flags": [W, C.POINTER(u32), C.c_void_p],
+        "rfr_plan_state": [W, C.POINTER(rfr_plan_info), C.c_void_p],
+        "rfr_profile_enable": [C.c_int],
+        "rfr_profile_read": [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)],
         "rfr_comm_unique_id": [vp],
         "rfr_comm_init": [vp, C.c_int, C.c_int, C.POINTER(vp)],
         "rfr_comm_destroy": [vp],
@@ -407,6 +421,24 @@ def rfr_backward_finish(partials: torch.Tensor, samples: DeviceSamples, sharpnes
 
 def rfr_launch_count() -> int:
     return int(load().rfr_launch_count())
+
+
+def rfr_plan_state(ws: torch.Tensor, stream=None) -> dict:
+    """Plan of the last r2-engine call on ws (diagnostic, host-synchronous)."""
+    v = rfr_plan_info()
+    _check(load().rfr_plan_state(_ws(ws), C.byref(v), _stream(stream)), "rfr_plan_state")
+    return {f: getattr(v, f) for f, _ in rfr_plan_info._fields_}
+
+
+def rfr_profile_enable(on: bool = True):
+    _check(load().rfr_profile_enable(1 if on else 0), "rfr_profile_enable")
+
+
+def rfr_profile_read(sweep: str):
+    """(milliseconds, launches) accumulated for one sweep since rfr_profile_enable(True)."""
+    ms, n = C.c_double(), C.c_uint64()
+    _check(load().rfr_profile_read(SWEEPS[sweep], C.byref(ms), C.byref(n)), "rfr_profile_read")
+    return ms.value, n.value
 
 
 def rfr_poll_flags(ws: torch.Tensor, stream=None) -> int:

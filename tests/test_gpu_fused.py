@@ -188,9 +188,11 @@ def test_fused_sharded_equals_oracle_and_comm_identity():
 
 @pytest.mark.parametrize("name", ["c2", "c3"])
 def test_chebyshev_path_matches_direct_kernels(name):
-    """The default Chebyshev-moment path (with empty-space skipping) against the direct kernels
-    (RFR_DIRECT: K2 recurrence, tensor-core adjoint) on the same full-size inputs: forward signal,
-    fused matched filter and gradients agree far inside the parity tolerances."""
+    """The three implementations of the path on the same full-size inputs: the r2 tiled engine
+    (default: Horner sweeps over per-(antenna, tile) coefficients, DESIGN 5e), the r1 Chebyshev
+    kernels (RFR_R1) and the direct kernels (RFR_DIRECT: K2 recurrence, tensor-core adjoint).
+    Forward signal, fused matched filter and gradients agree far inside the parity tolerances, and
+    each call reports the path it took."""
     m = rfr()
     p = problem(name)
     b = p.bundles[0]
@@ -198,7 +200,7 @@ def test_chebyshev_path_matches_direct_kernels(name):
     DS, DA = m.DeviceSamples.from_host(S, dev()), m.DeviceAntennas.from_host(b.antennas, dev())
     ws = m.workspace(S.n, b.antennas.n, p.grid.n_freq, S.n, dev())
     res = {}
-    for key, fl in (("cheb", 0), ("direct", m.RFR_DIRECT)):
+    for key, fl in (("r2", 0), ("r1", m.RFR_R1), ("direct", m.RFR_DIRECT)):
         sig = torch.empty(b.antennas.n, p.grid.n_freq, 2, device=dev())
         m.rfr_forward(DS, p.sharpness, DA, p.grid, sig, ws, flags=fl)
         G = f32c(p.random_grad())
@@ -207,15 +209,17 @@ def test_chebyshev_path_matches_direct_kernels(name):
         M = torch.empty(S.n, 2, device=dev())
         m.rfr_backward_filter(G, sig, DS, p.sharpness, DA, p.grid, out, P, ws, mf=M,
                               flags=fl | m.RFR_REUSE_BLEND)
-        st = m.cheb_state(ws)
+        st = m.cheb_state(ws) if key != "r2" else m.rfr_plan_state(ws)
         torch.cuda.synchronize()
         res[key] = (c64(sig), c64(M), {k: getattr(out, k).cpu().numpy().astype(np.float64)
                                        for k in FIELDS}, st)
-    assert res["cheb"][3]["sel"] == 1 and res["direct"][3]["sel"] == 0
-    assert rel(res["cheb"][0], res["direct"][0]) <= 1e-5
-    assert rel(res["cheb"][1], res["direct"][1]) <= 1e-5
-    for k in FIELDS:
-        assert rel(res["cheb"][2][k], res["direct"][2][k]) <= 1e-4, k
+    assert res["r2"][3]["applied"] == 1 and 8 <= res["r2"][3]["P"] <= 16, res["r2"][3]
+    assert res["r1"][3]["sel"] == 1 and res["direct"][3]["sel"] == 0
+    for a_, b_ in (("r2", "direct"), ("r1", "direct"), ("r2", "r1")):
+        assert rel(res[a_][0], res[b_][0]) <= 1e-5, (a_, b_)
+        assert rel(res[a_][1], res[b_][1]) <= 1e-5, (a_, b_)
+        for k in FIELDS:
+            assert rel(res[a_][2][k], res[b_][2][k]) <= 1e-4, (a_, b_, k)
 
 
 def test_fused_and_filter_determinism_bitwise():

@@ -121,8 +121,9 @@ def test_filter_backward_ragged_and_bistatic(n_freq, bistatic):
 
 @pytest.mark.parametrize("bistatic", [False, True])
 def test_filter_backward_tiled_path(bistatic):
-    """Tiled K5 (DESIGN 6b): several chunks per tile (3001 queries, 256-point chunks), a ragged
-    antenna block (131 = 128 + 3); the call must have taken the tiled Chebyshev path."""
+    """Tiled K5: several chunks per tile (3001 queries), a ragged antenna block (131 = 128 + 3);
+    the call must have taken the tiled path -- the r2 engine (DESIGN 5e) when monostatic, the r1
+    tiled Chebyshev kernels (DESIGN 6b) when bistatic."""
     m = rfr()
     A, q, grid = _tiny(128, n_ant=131, n_q=3001, seed=5, bistatic=bistatic)
     M, P, gP = seeded_filter_state(len(q[0]), 21)
@@ -132,8 +133,12 @@ def test_filter_backward_tiled_path(bistatic):
     m.rfr_filter_backward(t32(gP), f32c(M), DA, grid, *[t32(v) for v in q], out, ws,
                           power=t32(P), eps=1e-20)
     torch.cuda.synchronize()
-    st = m.cheb_state(ws)
-    assert st["sel"] == 1 and st["P_tiled_filter"] > 0, st
+    if bistatic:
+        st = m.cheb_state(ws)
+        assert st["sel"] == 1 and st["P_tiled_filter"] > 0, st
+    else:
+        st = m.rfr_plan_state(ws)
+        assert st["applied"] == 1 and st["P"] > 0 and st["n_points"] == len(q[0]), st
     ref = oracle.filter_backward(gP, M, P, A, grid, *q, eps=1e-20)
     assert rel(c64(out), ref) <= TOL_SIG
 
