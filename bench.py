@@ -1,15 +1,22 @@
 #!/usr/bin/env python
-"""Benchmark of the renderer's hot path: one step = blend (K1) + forward (K2) + matched filter (K4)
-+ loss (K6) + backward (K3, K1') over one synthetic batch, on N GPUs of one node.
+"""Benchmark of the renderer's hot path on N GPUs of one node.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl librfr|reference]
   (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N)
 
+One step = the config's passes (BASELINE.json configs / synth Problem.passes) over one synthetic
+batch: K1 blend + forward (a1-a3), then
+  fwd + filter + bwd (c1, c3): loss (a5) + the fused filter at the samples and backward (a4, a6-a8);
+  fwd + bwd (c2, c4):          loss + backward;
+  fwd + filter (c5):           the matched filter at the samples.
 Metric (BASELINE.json): render fwd+bwd G contributions/s, one contribution = one (sample x antenna
-x frequency-bin) term.  value = N_c / t_step where N_c = sum over bundles of N_s * N_a * N_f and
-t_step is the device time of the whole step (filter and loss included, max over ranks).  Antennas
-are sharded across ranks (strong scaling); the backward partials and the filter's complex M are
-all-reduced with NCCL.  --impl reference times the fp64 CPU oracle on bounded samples.
+x frequency-bin) term.  value = N_c / t_step, N_c = sum over bundles of N_s * N_a * N_f, t_step the
+device time of the whole step (max over ranks).  Antennas are sharded across ranks; the backward
+partials and the filter's complex M are all-reduced with NCCL (or, --filter-collective gather, the
+signal rows are all-gathered and the queries sharded).  --impl reference times the fp64 CPU oracle
+on bounded samples.  --emulate-world N --emulate-rank r times rank r's whole share of an N-GPU run
+on one GPU (collectives excluded, reported as such).  --dense runs c3 with s = 200 / m, where no
+sample is skipped (every alpha is non-zero: the early-training regime).
 """
 from __future__ import annotations
 
@@ -29,17 +36,39 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
-METRIC = "render fwd+bwd G contributions/s (pts×antennas×freqs) at 1/2/4/8 B200"
+METRIC = "render fwd+bwd G contributions/s (pts\u00d7antennas\u00d7freqs) at 1/2/4/8 B200"
 N_SM = 148
 FP32_LANES_PER_SM = 128
-# FP32-pipe lane-operations per contribution:
-#   forward  : 1 FFMA2 + 1 FADD2 = 4 lane-ops (Chebyshev step + accumulate)
-#   backward : 2 FFMA2           = 4 lane-ops (complex Horner step)
-#   filter   : 2 FFMA2           = 4 lane-ops
-OPS_PER_CONTRIB = 4
-# K3/K4 on tensor cores: D = A.B^T per 16-bin block, 4 real MACs per contribution, 3 fp16 products
-# (3xFP16 split, tcgen05.mma kind::f16 with fp32 accumulation)
-TC_FLOP_PER_CONTRIB = 24
+XU_LANES_PER_SM = 16
+
+
+# Algorithmic work per (point, antenna) pair of the r2 engine's sweeps, in
+# FP32 lane-operations (one fp32 FMA / MUL / ADD on one lane) and XU operations (MUFU):
+#   pair geometry (all sweeps): delta = |q'|^2 - 2 a'.q' (3), s2 = D + delta (1), d = s2 rsqrt(s2)
+#     (1), d + d_a (1), d - d_a = delta / (d + d_a) (1), cycles (1), reduction to [-1/2, 1/2] (3),
+#     angle (1), x (1)                                             = 13 lane-ops, 4 XU (rsqrt, rcp,
+#                                                                    sin, cos)
+#   filter:   Horner over P monomial coefficients: (P - 1) complex x real FMAs = 2 (P - 1);
+#             carrier M += E h (complex MAC)                       = 4
+#   backward: Horner 2 (P - 1); R = Re(E h) (2); Eq. 5 sums U, V (gain 3, gamma 2, U 1, F 2,
+#             sum F 1, W 3)                                        = 14
+#   forward:  per moment one complex x real FMA (2) + the recurrence (1) = 3 P; amplitude
+#             (n.d 3, gain 3, gamma / A 3, c = A E 2)              = 11
+def lane_ops_per_pair(sweep: str, P: int) -> int:
+    geo = 13
+    if sweep == "filter":
+        return geo + 2 * (P - 1) + 4
+    if sweep == "backward":
+        return geo + 2 * (P - 1) + 2 + 14
+    return geo + 3 * P + 11
+
+
+def moment_ops_per_pair(sweep: str, P: int) -> int:
+    """The moment / polynomial part alone (the r1 accounting, for comparison)."""
+    return 2 * (P - 1) + (4 if sweep == "filter" else 2) if sweep != "forward" else 3 * P
+
+
+XU_PER_PAIR = 4
 
 
 def peaks():
@@ -142,12 +171,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import synth
-    prob = synth.make(args.config)
+    prob = make_problem(args)
     vals = []
     t0 = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        r = oracle_sample_rates(prob, budget_s=args.ref_budget)
+        r = oracle_sample_rates(prob, budget_s=args.ref_step_budget)
         if i >= args.warmup:
             vals.append(step_rate(r))
     wall = time.perf_counter() - t0
@@ -168,11 +196,21 @@ def run_reference(args):
 
 
 # ===================================================================================== GPU arm
+def make_problem(args):
+    import synth
+    prob = synth.make(args.config)
+    if args.dense:
+        # the early-training regime: a soft NeuS density (s = 200 / m), every alpha non-zero, so
+        # empty-space skipping removes nothing (DESIGN 5c)
+        prob.sharpness = 200.0
+        prob.name = prob.name + "-dense"
+    return prob
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    import synth
     from paper_2605_29097_b200 import rfr
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -185,23 +223,35 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     rfr.load()
-    # librfr's own NCCL communicator carries the data-path all-reduces (a4 M, a7 partials)
+    # librfr's own NCCL communicator carries the data-path collectives (a4 M, a7 partials)
     comm = rfr.Comm.create() if world > 1 else None
-    prob = synth.make(args.config)
+    # emulation of one rank of an N-GPU run on this GPU: rank r's antenna shard, no collective
+    ew, er = (args.emulate_world, args.emulate_rank) if args.emulate_world else (world, rank)
+    prob = make_problem(args)
     grid = prob.grid
     st = torch.cuda.current_stream()
+    passes = set(prob.passes) if not args.passes else set(args.passes.split(","))
+    has_flt, has_bwd = "filter" in passes, "bwd" in passes
+    heat = args.step == "heatmap"
+    if heat:
+        has_flt = has_bwd = True
+    fused = has_flt and has_bwd and not args.separate and not heat
+    gather = args.filter_collective == "gather" and has_flt and not has_bwd
 
     # ---------------- per-bundle device state
     B = []
     sum_F2 = torch.zeros(1, dtype=torch.float64, device=dev)
-    n_F = 0
     for k, b in enumerate(prob.bundles):
-        lo, hi = rfr.shard_range(b.antennas.n, rank, world)
+        lo, hi = rfr.shard_range(b.antennas.n, er, ew)
         DS = rfr.DeviceSamples.from_host(b.samples, dev)
-        DA = rfr.DeviceAntennas.from_host(b.antennas, dev).slice(lo, hi)
+        DA_full = rfr.DeviceAntennas.from_host(b.antennas, dev)
+        DA = DA_full.slice(lo, hi)
         n, na = b.samples.n, hi - lo
-        ws = rfr.workspace(n, na, grid.n_freq, n, dev)
-        st_k = dict(k=k, lo=lo, hi=hi, S=DS, A=DA, n=n, na=na, ws=ws,
+        qlo, qhi = rfr.shard_range(n, er, ew) if gather else (0, n)
+        ws = rfr.workspace(n, b.antennas.n if gather else na, grid.n_freq, n, dev)
+        st_k = dict(k=k, lo=lo, hi=hi, S=DS, A=DA, A_full=DA_full, n=n, na=na, ws=ws, qlo=qlo,
+                    qhi=qhi, sig_full=(torch.randn(b.antennas.n, grid.n_freq, 2, device=dev)
+                                       if gather and args.emulate_world else None),
                     sig=torch.empty(na, grid.n_freq, 2, device=dev),
                     G=torch.empty(na, grid.n_freq, 2, device=dev),
                     loss=torch.empty(1, device=dev),
@@ -210,22 +260,18 @@ def run_gpu(args):
         # target y = F(scene) + complex noise at the config's SNR (reading Q18), built untimed
         rfr.rfr_forward(DS, prob.sharpness, DA, grid, st_k["sig"], ws)
         sum_F2 += (st_k["sig"].double() ** 2).sum()
-        n_F += na * grid.n_freq
         B.append(st_k)
     if world > 1:
         dist.all_reduce(sum_F2)
     n_F_tot = sum(b.antennas.n for b in prob.bundles) * grid.n_freq
-    sigma = float(torch.sqrt(sum_F2 / n_F_tot / 10 ** (prob.snr_db / 10)).item())
+    # (emulation: the local rows stand for the full set in the noise level)
+    scale = 1.0 if (world > 1 or ew == 1) else float(ew)
+    sigma = float(torch.sqrt(sum_F2 * scale / n_F_tot / 10 ** (prob.snr_db / 10)).item())
     for st_k in B:
         nz = prob.noise_unit(st_k["k"])[st_k["lo"]:st_k["hi"]]
         noise = torch.as_tensor(np.stack([nz.real, nz.imag], -1).astype(np.float32)).to(dev)
         st_k["y"] = st_k["sig"] + sigma * noise
     torch.cuda.synchronize()
-
-    ev = lambda: torch.cuda.Event(enable_timing=True)
-
-    heat = args.step == "heatmap"
-    fused = not args.separate and not heat
     if heat:
         # NEXT-1: the paper's heatmap-domain L2.  Ground-truth heatmap = the filter of
         # the noisy target y at the same queries (the samples), built untimed
@@ -236,32 +282,46 @@ def run_gpu(args):
                            comm=comm)
         torch.cuda.synchronize()
 
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def filt(s):
+        if gather and args.emulate_world:
+            # the emulated rank's share of the query-sharded filter: every antenna (the gathered
+            # rows; their values do not change the work) x this rank's query slice
+            q = slice(s["qlo"], s["qhi"])
+            rfr.rfr_filter(s["sig_full"], s["A_full"], grid, s["S"].x[q], s["S"].y[q], s["S"].z[q],
+                           s["P"][q], s["ws"], mf=s["M"][q])
+        elif gather:
+            rfr.rfr_filter_gather(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z,
+                                  s["P"][s["qlo"]:s["qhi"]], s["ws"], comm=comm,
+                                  n_ant_total=prob.bundles[s["k"]].antennas.n,
+                                  mf=s["M"][s["qlo"]:s["qhi"]])
+        else:
+            rfr.rfr_filter(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P"],
+                           s["ws"], mf=s["M"], comm=comm)
+
     def step(rec=None):
-        # fused (default): K2 forward, K6 loss, then K3 + K4 in one tensor-core sweep
-        # (rfr_backward_filter: filter queries = the samples).  --separate: rfr_filter before the
-        # loss and rfr_backward after it, as two sweeps.
         for s in B:
             e = [ev() for _ in range(5)] if rec is not None else None
             if e: e[0].record(st)
             rfr.rfr_forward(s["S"], prob.sharpness, s["A"], grid, s["sig"], s["ws"])
             if e: e[1].record(st)
-            if not fused:
-                rfr.rfr_filter(s["sig"], s["A"], grid, s["S"].x, s["S"].y, s["S"].z, s["P"],
-                               s["ws"], mf=s["M"], comm=comm)
+            if has_flt and not fused:
+                filt(s)
             if e: e[2].record(st)
             if heat:
                 # K7 heatmap L2, then K5 (matched-filter adjoint) turns dL/dP into dL/ds
                 rfr.rfr_heatmap_loss(s["P"], s["P_gt"], s["gP"], s["loss"], s["ws"])
                 rfr.rfr_filter_backward(s["gP"], s["M"], s["A"], grid, s["S"].x, s["S"].y,
                                         s["S"].z, s["G"], s["ws"], power=s["P"], eps=1e-20)
-            else:
+            elif has_bwd:
                 rfr.rfr_loss(s["sig"], s["y"], s["G"], s["loss"], s["ws"])
             if e: e[3].record(st)
             if fused:
                 rfr.rfr_backward_filter(s["G"], s["sig"], s["S"], prob.sharpness, s["A"], grid,
                                         s["out"], s["P"], s["ws"], mf=s["M"],
                                         flags=rfr.RFR_REUSE_BLEND, comm=comm)
-            else:
+            elif has_bwd:
                 rfr.rfr_backward(s["G"], s["S"], prob.sharpness, s["A"], grid, s["out"], s["ws"],
                                  flags=rfr.RFR_REUSE_BLEND, comm=comm)
             if e:
@@ -278,54 +338,53 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step()
     barrier()
-    # which path the device chose (Chebyshev moments or direct kernels): one forward and one
-    # backward on bundle 0, read back from the workspace header (untimed diagnostic)
+    # untimed diagnostics (bundle 0): the r2 plan of each call type, active-sample counts
     s0 = B[0]
     rfr.rfr_forward(s0["S"], prob.sharpness, s0["A"], grid, s0["sig"], s0["ws"])
-    cf = rfr.cheb_state(s0["ws"])
-    p_flt_sep = p_k5 = 0
-    if not fused:
-        rfr.rfr_filter(s0["sig"], s0["A"], grid, s0["S"].x, s0["S"].y, s0["S"].z, s0["P"],
-                       s0["ws"], mf=s0["M"])
-        cq = rfr.cheb_state(s0["ws"])
-        p_flt_sep = cq["P_tiled_filter"] if cq["sel"] else 0
+    plan_fwd = rfr.rfr_plan_state(s0["ws"])
+    n_act_fwd = rfr.cheb_state(s0["ws"])["n_active_fwd"]
+    plan_flt = plan_bwd = plan_k5 = None
+    n_act_bwd = 0
+    if has_flt and not fused:
+        filt(s0)
+        plan_flt = rfr.rfr_plan_state(s0["ws"])
     if heat:
         rfr.rfr_heatmap_loss(s0["P"], s0["P_gt"], s0["gP"], s0["loss"], s0["ws"])
         rfr.rfr_filter_backward(s0["gP"], s0["M"], s0["A"], grid, s0["S"].x, s0["S"].y, s0["S"].z,
                                 s0["G"], s0["ws"], power=s0["P"], eps=1e-20)
-        ck = rfr.cheb_state(s0["ws"])
-        # tiled K5 (DESIGN 6b) publishes its own P like the tiled filter; RFR_TILE=0: untiled
-        p_k5 = ((ck["P_tiled_filter"] if os.environ.get("RFR_TILE") != "0" else ck["P"])
-                if ck["sel"] else 0)
-    if fused:
-        rfr.rfr_backward_filter(s0["G"], s0["sig"], s0["S"], prob.sharpness, s0["A"], grid,
-                                s0["out"], s0["P"], s0["ws"], mf=s0["M"], flags=rfr.RFR_REUSE_BLEND)
-    else:
-        rfr.rfr_backward_partial(s0["G"], s0["S"], prob.sharpness, s0["A"], grid, s0["part"],
-                                 s0["ws"], flags=rfr.RFR_REUSE_BLEND)
-    ca = rfr.cheb_state(s0["ws"])
-    cheb_fwd_P = cf["P"] if cf["sel"] else 0
-    cheb_adj_P = ca["P"] if ca["sel"] else 0
-    # empty-space skipping: samples that carry forward / backward work (bundle 0)
-    act_fwd = cf["n_active_fwd"] / s0["n"]
-    act_bwd = ca["n_active_bwd"] / s0["n"]
+        plan_k5 = rfr.rfr_plan_state(s0["ws"])
+    if has_bwd:
+        rfr.rfr_loss(s0["sig"], s0["y"], s0["G"], s0["loss"], s0["ws"])
+        if fused:
+            rfr.rfr_backward_filter(s0["G"], s0["sig"], s0["S"], prob.sharpness, s0["A"], grid,
+                                    s0["out"], s0["P"], s0["ws"], mf=s0["M"],
+                                    flags=rfr.RFR_REUSE_BLEND)
+            plan_flt = plan_bwd = rfr.rfr_plan_state(s0["ws"])
+        else:
+            rfr.rfr_backward_partial(s0["G"], s0["S"], prob.sharpness, s0["A"], grid, s0["part"],
+                                     s0["ws"], flags=rfr.RFR_REUSE_BLEND)
+            plan_bwd = rfr.rfr_plan_state(s0["ws"])
+        n_act_bwd = rfr.cheb_state(s0["ws"])["n_active_bwd"]
+    act_fwd = n_act_fwd / s0["n"]
+    act_bwd = n_act_bwd / s0["n"] if has_bwd else 0.0
     barrier()
 
     # ---------------- timed region: K steps, per-step events, L2 flushed between steps
     n0 = rfr.rfr_launch_count()
     step_ms, seg = [], {"fwd": 0.0, "filter": 0.0, "loss": 0.0, "bwd": 0.0}
+    rfr.rfr_profile_enable(True)
     with ClockSampler(local) as clk:
         barrier()
         t_wall = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()
-            s0, s1 = ev(), ev()
+            s0e, s1e = ev(), ev()
             recs = []
-            s0.record(st)
+            s0e.record(st)
             step(recs)
-            s1.record(st)
+            s1e.record(st)
             torch.cuda.synchronize()
-            step_ms.append(s0.elapsed_time(s1))
+            step_ms.append(s0e.elapsed_time(s1e))
             for e in recs:
                 seg["fwd"] += e[0].elapsed_time(e[1])
                 seg["filter"] += e[1].elapsed_time(e[2])
@@ -333,6 +392,8 @@ def run_gpu(args):
                 seg["bwd"] += e[3].elapsed_time(e[4])
         barrier()
         t_wall = time.perf_counter() - t_wall
+    sweeps = {k: rfr.rfr_profile_read(k) for k in rfr.SWEEPS}
+    rfr.rfr_profile_enable(False)
     launches = rfr.rfr_launch_count() - n0
     tot_ms = sum(step_ms)
     t = torch.tensor([tot_ms, seg["fwd"], seg["filter"], seg["loss"], seg["bwd"]], device=dev,
@@ -342,10 +403,12 @@ def run_gpu(args):
     tot_ms, f_ms, q_ms, l_ms, b_ms = (float(v) for v in t.tolist())
     ms_per_step = tot_ms / args.steps
     Nc = prob.n_contrib
-    value = Nc / (ms_per_step * 1e-3)
+    share = (1.0 / ew) if args.emulate_world else 1.0      # the emulated rank's share of N_c
+    value = Nc * share / (ms_per_step * 1e-3)
+    active_frac = {"fwd": act_fwd, "bwd": act_bwd}
 
     # ---------------- e2e: same step through the ABI with host buffers (pinned) every step
-    e2e = run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step)
+    e2e = run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step, share)
 
     if rank != 0:
         if comm is not None:
@@ -355,154 +418,99 @@ def run_gpu(args):
         return 0
     pk = peaks()
     clocks = clk.summary()
-    peak_ops = N_SM * FP32_LANES_PER_SM * pk.get("sm_max_mhz", 1965.0) * 1e6
-    # fp16 tensor peak (kind::f16 runs at the bf16 rate): the measured bf16 burst peak
-    bf16 = pk.get("bf16_tflops", 1590.0)
-    peak_f16 = bf16 * 1e12
-    tc = os.environ.get("RFR_ADJOINT", "tc") != "simt" and grid.n_freq in (128, 256, 512)
+    mhz = pk.get("sm_max_mhz", 1965.0)
+    peak_ops = N_SM * FP32_LANES_PER_SM * mhz * 1e6
+    peak_xu = N_SM * XU_LANES_PER_SM * mhz * 1e6
     per_step = lambda ms: ms / args.steps
-    clk_ratio = (clocks["sm_mhz"] / pk.get("sm_max_mhz", 1965.0)) if clocks.get("sm_mhz") else None
+    # pairs per step of each sweep on this rank (every bundle has the same shape)
+    na_loc = sum(s["na"] for s in B)
+    n_pts = B[0]["n"]
+    pairs = {"filter": sum(s["n"] * (s["hi"] - s["lo"]) for s in B) if has_flt else 0,
+             "backward": act_bwd * n_pts * na_loc if has_bwd else 0,
+             "forward": act_fwd * n_pts * na_loc}
+    if gather:
+        pairs["filter"] = sum((s["qhi"] - s["qlo"]) * prob.bundles[s["k"]].antennas.n for s in B)
+    plans = {"filter": plan_flt, "backward": plan_bwd, "forward": plan_fwd}
     roofs = []
-    n_pairs = sum(b.samples.n * b.antennas.n for b in prob.bundles) / world
-    if cheb_fwd_P:
-        # Chebyshev-moment forward: per pair P steps of 1 FFMA + 1 FADD (Reinsch recurrence) +
-        # 1 FFMA2 (complex-real moment update) = 4 P FP32 lane-ops, over
-        # the pairs of the samples that carry an amplitude (empty-space skipping, section 5c)
-        ach = 4 * cheb_fwd_P * n_pairs * act_fwd / (per_step(f_ms) * 1e-3)
-        roofs.append({"kernel": f"k_cheb_fwd<P={cheb_fwd_P}> (rfr_forward)", "bound": "alu",
-                      "achieved": ach / 1e12, "peak": peak_ops / 1e12,
-                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                      "lane_ops_per_pair": 4 * cheb_fwd_P, "active_sample_fraction": act_fwd,
-                      "ms_per_step": per_step(f_ms)})
-    else:
-        # K2 forward: FP32-pipe bound, 4 lane-ops per contribution (1 FFMA2 + 1 FADD2)
-        ach = OPS_PER_CONTRIB * (Nc / world) / (per_step(f_ms) * 1e-3)
-        roofs.append({"kernel": "k_trace_fwd (K2, rfr_forward)", "bound": "alu",
+    for sw in ("filter", "backward", "forward"):
+        ms_tot, nl = sweeps[sw]
+        pl = plans[sw]
+        if not nl or not pl or not pl["applied"] or not pairs[sw]:
+            continue
+        ms = ms_tot / args.steps
+        P = pl["P"]
+        ops = lane_ops_per_pair(sw, P)
+        ach = ops * pairs[sw] / (ms * 1e-3)
+        xu = XU_PER_PAIR * pairs[sw] / (ms * 1e-3)
+        kern = {"filter": "k2_filter", "backward": "k2_bwd", "forward": "k2_fwd"}[sw]
+        roofs.append({"kernel": f"{kern}<P={P}>", "sweep": sw, "bound": "alu",
                       "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
-                      "frac": ach / peak_ops,
-                      "frac_at_measured_clock": ach / (peak_ops * clk_ratio) if clk_ratio else None,
-                      "ms_per_step": per_step(f_ms)})
-    tiled = os.environ.get("RFR_TILE") != "0"
-
-    def lops(P):
-        # FP32 lane-ops per (point, antenna) pair of one tiled Chebyshev sweep: per moment one
-        # complex-real FFMA2 (2) + the recurrence: plain three-term at P <= 16 (1, DESIGN 5d),
-        # Reinsch otherwise (2)
-        return (3 if (P <= 16 and os.environ.get("RFR_STDREC") != "0") else 4) * P
-
-    if cheb_adj_P:
-        # fused call: the tiled filter over every pair + the tiled backward over the pairs of the
-        # samples with alpha != 0 (section 5c), both at the tiled P published by the call
-        p_t = (ca.get("P_tiled_filter") or cheb_adj_P) if tiled else cheb_adj_P
-        ops = lops(p_t) if tiled else 4 * cheb_adj_P
-        work = n_pairs * ((1.0 + act_bwd) if fused else act_bwd)
-        for name, ms in ([("k_tile_flt4+k_tile_bwd (filter + backward, rfr_backward_filter)", b_ms)]
-                         if fused else [("k_tile_bwd (backward, rfr_backward)", b_ms)]):
-            ach = ops * work / (per_step(ms) * 1e-3)
-            roofs.append({"kernel": (f"{name.split()[0]}<P={p_t}> " if tiled else
-                                     f"k_cheb_adj<P={cheb_adj_P}> ") + " ".join(name.split()[1:]),
-                          "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
-                          "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                          "lane_ops_per_pair": ops, "active_sample_fraction": act_bwd,
-                          "ms_per_step": per_step(ms)})
-    if p_flt_sep:
-        # tiled Chebyshev filter (section 5d) over every (sample, antenna) pair
-        ach = lops(p_flt_sep) * n_pairs / (per_step(q_ms) * 1e-3)
-        roofs.append({"kernel": f"k_tile_flt4<P={p_flt_sep}> (K4, rfr_filter)", "bound": "alu",
-                      "achieved": ach / 1e12, "peak": peak_ops / 1e12,
-                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                      "lane_ops_per_pair": lops(p_flt_sep), "ms_per_step": per_step(q_ms)})
-    if p_k5:
-        # K5 = a forward-shaped Chebyshev sweep over the queries, per
-        # (query, antenna) pair; its segment also holds the (negligible) K7 heatmap loss
-        o5 = lops(p_k5) if tiled else 4 * p_k5
-        ach = o5 * n_pairs / (per_step(l_ms) * 1e-3)
-        k5 = "k_tile_fwd" if tiled else "k_cheb_fwd"
-        roofs.append({"kernel": f"{k5}<P={p_k5},MFAdj> (K5+K7, rfr_filter_backward)",
-                      "bound": "alu", "achieved": ach / 1e12, "peak": peak_ops / 1e12,
-                      "unit": "T FP32 lane-ops/s", "frac": ach / peak_ops,
-                      "lane_ops_per_pair": o5, "ms_per_step": per_step(l_ms)})
-    if cheb_adj_P:
-        pass
-    elif fused:
-        adj = [("k_adjoint_tc<both> (K3+K4 fused +K1', rfr_backward_filter)", b_ms, 2)]
-    else:
-        adj = [("k_adjoint_tc<bwd> (K3+K1', rfr_backward)", b_ms, 1),
-               ("k_adjoint_tc<flt> (K4, rfr_filter)", q_ms, 1)]
-    if cheb_adj_P:
-        adj = []
-    for name, ms, npass in adj:
-        rate = npass * (Nc / world) / (per_step(ms) * 1e-3)     # contributions of all its passes
-        if tc:
-            # exact 16-bin block factorisation on tcgen05 kind::f16, 3xFP16: per contribution
-            # 4 real MACs x 3 products = 24 tensor FLOP
-            ach = TC_FLOP_PER_CONTRIB * rate
-            roofs.append({"kernel": name, "bound": "tensor", "achieved": ach / 1e12,
-                          "peak": peak_f16 / 1e12, "unit": "T f16 FLOP/s", "frac": ach / peak_f16,
-                          "alu_equivalent_frac": OPS_PER_CONTRIB * rate / peak_ops,
-                          "ms_per_step": per_step(ms)})
-        else:
-            ach = OPS_PER_CONTRIB * rate
-            roofs.append({"kernel": name.replace("_tc", ""), "bound": "alu", "achieved": ach / 1e12,
-                          "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
-                          "frac": ach / peak_ops, "ms_per_step": per_step(ms)})
-    dom = max(roofs, key=lambda r: r["ms_per_step"])
-    traffic = None
-    try:   # bytes per launch from the committed full-size ncu capture (profiles/traffic.json)
-        key = dom["kernel"].split()[0].split("<P=")[0]
-        traffic = json.load(open(TRAFFIC_PATH)).get(args.config, {}).get(key)
-    except Exception:
-        pass
-    roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
-            "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
-            "peak_note": ("148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); "
-                          + (f"{dom['lane_ops_per_pair']} lane-ops per (sample, antenna) pair "
-                             "(Chebyshev moments)" if "lane_ops_per_pair" in dom else
-                             "4 lane-ops per contribution") if dom["bound"] == "alu" else
-                          "measured bf16 burst peak (kind::f16 runs at the bf16 rate); 24 tensor "
-                          "FLOP per contribution (3xFP16)")}
+                      "frac": ach / peak_ops, "lane_ops_per_pair": ops,
+                      "frac_moments_only": moment_ops_per_pair(sw, P) * pairs[sw] / (ms * 1e-3) / peak_ops,
+                      "xu_frac": xu / peak_xu, "pairs_per_step": pairs[sw],
+                      "ms_per_step": ms, "launches_per_step": nl / args.steps,
+                      "tiles": [pl["lx"], pl["ly"], pl["lz"]], "Pg": pl["Pg"]})
+    dom = max(roofs, key=lambda r: r["ms_per_step"]) if roofs else None
+    roof = None
+    if dom:
+        traffic = None
+        try:   # DRAM bytes per launch from the committed full-size ncu capture
+            traffic = json.load(open(TRAFFIC_PATH)).get(args.config, {}).get(dom["kernel"].split("<")[0])
+        except Exception:
+            pass
+        roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
+                "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
+                "kernel": dom["kernel"], "xu_frac": dom["xu_frac"],
+                "frac_moments_only": dom["frac_moments_only"],
+                "peak_note": (f"148 SM x 128 FP32 lanes x sm_max_mhz (MEASURED_PEAKS.json); "
+                              f"{dom['lane_ops_per_pair']} lane-ops per (point, antenna) pair "
+                              "(DESIGN 5e work model: pair geometry + Horner / moments + epilogue), "
+                              "timed live per launch with CUDA events on the launching stream "
+                              "(rfr_profile); xu_frac: 4 MUFU per pair against 148 x 16 XU lanes")}
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not args.emulate_world:
         r = oracle_sample_rates(prob, budget_s=args.ref_budget)
         cpu = {"value": step_rate(r) / 1e9, "unit": "G contributions/s", "cores": r["cores"],
                "kind": "oracle", "sample": r["sample"],
                "per_pass_G_per_s": {k: r[k] / 1e9 for k in ("fwd", "filter", "bwd")}}
+    desc = ("K1 blend + forward + K4 filter (+NCCL all-reduce of M) + K7 heatmap loss + K5 "
+            "matched-filter adjoint + K3 backward (+NCCL all-reduce of partials) + K1' finish"
+            if heat else
+            "K1 blend + forward + K6 loss + fused backward + matched filter at the samples "
+            "(+NCCL all-reduce of partials and M) + K1' finish" if fused else
+            "K1 blend + forward + K4 filter + K6 loss + K3 backward + K1' finish"
+            if (has_flt and has_bwd) else
+            "K1 blend + forward + K6 loss + K3 backward (+NCCL all-reduce of partials) + K1' finish"
+            if has_bwd else
+            "K1 blend + forward + K4 matched filter at the samples (" +
+            ("all-gather of the signal rows, query-sharded" if gather else "+NCCL all-reduce of M")
+            + ")")
+    n_active_contrib = (pairs["forward"] + pairs["backward"] + pairs["filter"]) * grid.n_freq
     line = {"metric": METRIC, "value": value / 1e9, "unit": "G contributions/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "n_contrib_per_pass": Nc,
-                       "bundles": len(prob.bundles),
-                       "n_samples": [b.samples.n for b in prob.bundles][0],
-                       "n_antennas": [b.antennas.n for b in prob.bundles][0],
-                       "n_freq": grid.n_freq, "parallelism": f"antenna-shard x{world}",
+            "config": {"workload": prob.name, "n_contrib_per_pass": Nc,
+                       "passes": sorted(passes), "bundles": len(prob.bundles),
+                       "n_samples": n_pts, "n_antennas": prob.bundles[0].antennas.n,
+                       "n_freq": grid.n_freq, "sharpness_per_m": prob.sharpness,
+                       "parallelism": f"antenna-shard x{ew}" + (" (emulated rank "
+                                                                  f"{er} on one GPU)" if args.emulate_world else ""),
                        "l2": "flushed between steps (512 MiB memset, outside the step events)",
                        "loss": "heatmap L2 (NEXT-1)" if heat else "signal-domain complex residual",
-                       "step": ("K1 blend + forward + K4 filter (+NCCL all-reduce of M) + K7 "
-                                "heatmap loss + K5 matched-filter adjoint + K3 backward (+NCCL "
-                                "all-reduce of partials) + K1' finish" if heat else
-                                "K1 blend + forward + K6 loss + K3/K4 fused backward + "
-                                "matched filter at the samples (+NCCL all-reduce of partials and "
-                                "M) + K1' finish" if fused else
-                                "K1 blend + forward + K4 filter (+NCCL all-reduce of M) + K6 "
-                                "loss + K3 backward (+NCCL all-reduce of partials) + K1' finish")},
-            "passes": ({"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
-                        "filter_plus_bwd_fused_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
-                        "loss_ms": per_step(l_ms), "fwd_ms": per_step(f_ms),
-                        "filter_plus_bwd_ms": per_step(b_ms)} if fused else
-                       {"fwd_ms": per_step(f_ms), "filter_ms": per_step(q_ms),
-                        "heat_loss_plus_k5_ms": per_step(l_ms), "bwd_ms": per_step(b_ms),
-                        "k5_G_per_s": Nc / (per_step(l_ms) * 1e-3) / 1e9} if heat else
-                       {"fwd_G_per_s": Nc / (per_step(f_ms) * 1e-3) / 1e9,
-                        "filter_G_per_s": Nc / (per_step(q_ms) * 1e-3) / 1e9,
-                        "bwd_G_per_s": Nc / (per_step(b_ms) * 1e-3) / 1e9,
-                        "fwd_plus_bwd_G_per_s": Nc / (per_step(f_ms + b_ms) * 1e-3) / 1e9,
-                        "loss_ms": per_step(l_ms)}),
-            "method": {"forward": f"chebyshev-moments P={cheb_fwd_P} (delta={cf['delta']:.4g} cycles)"
-                       if cheb_fwd_P else "direct recurrence (K2)",
-                       "adjoint": (f"chebyshev-moments P={cheb_adj_P} (delta={ca['delta']:.4g} "
-                                   f"cycles); tiled filter P={ca.get('P_tiled_filter')}")
-                       if cheb_adj_P else "tensor-core 16-bin block GEMM",
+                       "step": desc},
+            "value_active": {"value": n_active_contrib / (ms_per_step * 1e-3) / 1e9,
+                             "unit": "G contributions/s",
+                             "note": "(point, antenna, bin) terms the kernels evaluate: every "
+                                     "sample for the filter, the alpha != 0 / amplitude != 0 samples "
+                                     "for the backward / forward (empty-space skipping, DESIGN 5c), "
+                                     "summed over the step's passes"},
+            "passes": {"fwd_ms": per_step(f_ms), "filter_ms": per_step(q_ms),
+                       "loss_ms": per_step(l_ms), "bwd_or_fused_ms": per_step(b_ms)},
+            "sweeps_ms_per_step": {k: v[0] / args.steps for k, v in sweeps.items()},
+            "method": {"engine": "r2 tiled (DESIGN 5e)",
+                       "plans": {k: v for k, v in (("forward", plan_fwd), ("filter", plan_flt),
+                                                   ("backward", plan_bwd), ("k5", plan_k5)) if v},
                        "empty_space_skipping": {
                            "forward_active_samples": act_fwd, "backward_active_samples": act_bwd,
                            "note": "samples whose amplitude (forward) or alpha (backward) is exactly "
@@ -510,6 +518,9 @@ def run_gpu(args):
                                    "antenna, bin) of the batch (the metric's definition)"}},
             "roofline": roof, "rooflines": roofs, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s_timed": t_wall}
+    if args.emulate_world:
+        line["emulated"] = {"world": ew, "rank": er, "note": "one rank's share on one GPU: "
+                            "value = that rank's contributions / its step time; collectives excluded"}
     print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
@@ -518,11 +529,12 @@ def run_gpu(args):
     return 0
 
 
-def run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step):
+def run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step, share):
     """Same step measured end to end through the public API: every step copies its inputs
     (samples, local antennas, local target rows) host->device from pinned buffers and reads the
-    result (loss + per-sample gradients) device->host."""
+    result (loss + per-sample gradients, or the heatmap) device->host."""
     host_in, dev_in, host_out, dev_out = [], [], [], []
+    has_bwd = "bwd" in prob.passes or args.step == "heatmap"
     for s in B:
         for f in rfr.DeviceSamples.FIELDS:
             d = getattr(s["S"], f)
@@ -530,12 +542,16 @@ def run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step):
         for f in ("tx_x", "tx_y", "tx_z"):
             d = getattr(s["A"], f)
             host_in.append(d.cpu().pin_memory()); dev_in.append(d)
-        tgt = s["P_gt"] if "P_gt" in s else s["y"]      # heatmap step: the target heatmap
-        host_in.append(tgt.cpu().pin_memory()); dev_in.append(tgt)
-        for f in ("sdf", "refl", "nx", "ny", "nz", "power", "sharpness"):
-            d = getattr(s["out"], f)
+        if has_bwd:
+            tgt = s["P_gt"] if "P_gt" in s else s["y"]      # heatmap step: the target heatmap
+            host_in.append(tgt.cpu().pin_memory()); dev_in.append(tgt)
+            for f in ("sdf", "refl", "nx", "ny", "nz", "power", "sharpness"):
+                d = getattr(s["out"], f)
+                host_out.append(torch.empty(d.shape, dtype=d.dtype).pin_memory()); dev_out.append(d)
+            host_out.append(torch.empty(1).pin_memory()); dev_out.append(s["loss"])
+        else:
+            d = s["P"][s["qlo"]:s["qhi"]]
             host_out.append(torch.empty(d.shape, dtype=d.dtype).pin_memory()); dev_out.append(d)
-        host_out.append(torch.empty(1).pin_memory()); dev_out.append(s["loss"])
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(t.numel() * t.element_size() for t in host_out)
     ev = lambda: torch.cuda.Event(enable_timing=True)
@@ -558,7 +574,7 @@ def run_e2e(args, prob, B, rfr, torch, dist, world, dev, st, step):
     t = torch.tensor([sum(ms) / steps], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    v = prob.n_contrib / (float(t.item()) * 1e-3)
+    v = prob.n_contrib * share / (float(t.item()) * 1e-3)
     return {"value": v / 1e9, "unit": "G contributions/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps}
 
@@ -571,7 +587,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="librfr", choices=["librfr", "reference"])
     ap.add_argument("--ref-budget", type=float, default=20.0,
-                    help="seconds of oracle work per reference sample")
+                    help="seconds of oracle work for the cpu_baseline sample")
+    ap.add_argument("--ref-step-budget", type=float, default=4.0,
+                    help="seconds of oracle work per step of --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--step", default="signal", choices=["signal", "heatmap"],
                     help="signal: the north_star step (signal-domain residual, default); heatmap: "
@@ -579,7 +597,23 @@ def main():
                          "(SURVEY 8f NEXT-1)")
     ap.add_argument("--separate", action="store_true",
                     help="filter and backward as two sweeps (rfr_filter + rfr_backward)")
+    ap.add_argument("--passes", default="", help="override the config's passes, e.g. fwd,filter")
+    ap.add_argument("--dense", action="store_true",
+                    help="s = 200 / m: no empty space to skip (early-training regime)")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="time one rank's share of an N-GPU run on this GPU")
+    ap.add_argument("--emulate-rank", type=int, default=0)
+    ap.add_argument("--filter-collective", default="auto", choices=["auto", "allreduce", "gather"],
+                    help="multi-GPU filter: all-reduce M, or all-gather the signal rows and shard "
+                         "the queries; auto = the smaller payload (SURVEY 8e)")
     args = ap.parse_args()
+    if args.filter_collective == "auto":
+        import synth
+        p = synth.make(args.config)
+        b = p.bundles[0]
+        # all-reduce of M: 8 B x N_q; all-gather of the signal rows: 8 B x N_a x N_f (+ positions)
+        args.filter_collective = ("gather" if 8 * b.antennas.n * p.grid.n_freq + 12 * b.antennas.n
+                                  < 8 * b.samples.n else "allreduce")
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

@@ -154,6 +154,18 @@ rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,
                               const rfr_freq_grid *grid, const float *qx, const float *qy,
                               const float *qz, int64_t n_query, float *mf,
                               const rfr_workspace *ws, rfr_stream_t stream);
+/* Query-sharded filter (the smaller collective when N_a N_f < N_q, e.g. c5): the ranks'
+ * antenna slices (contiguous, sizes from the rfr.shard_range convention over n_ant_total) and their
+ * signal rows are all-gathered into the workspace (one ncclBroadcast per rank in a group on
+ * `stream`, 8 B x n_freq + 12 B per antenna), then this rank filters its query slice
+ * [q_lo, q_hi) = shard_range(n_query, rank, nranks) over every antenna.  power / mf (optional) are
+ * [q_hi - q_lo]: the heatmap stays query-sharded (no collective on M).  comm == NULL: the plain
+ * filter over all n_query queries.  The workspace must be planned with n_ant >= n_ant_total.
+ * RFR_E_SHAPE if ants->n_ant differs from this rank's slice size. */
+rfr_status rfr_filter_gather(const float *signal, const rfr_antennas *ants, int64_t n_ant_total,
+                             const rfr_freq_grid *grid, const float *qx, const float *qy,
+                             const float *qz, int64_t n_query, float *power, float *mf,
+                             const rfr_comm *comm, const rfr_workspace *ws, rfr_stream_t stream);
 /* power[q] = |mf[q]| after the caller's all-reduce of mf. */
 rfr_status rfr_filter_power(const float *mf, int64_t n_query, float *power, rfr_stream_t stream);
 

@@ -150,6 +150,7 @@ struct Layout {
          off_t2geo = 0, off_t2lg = 0, off_t2acoef = 0, off_t2gexp = 0, off_t2coef = 0,
          off_t2mom = 0, off_t2bwdp = 0;
   size_t off_t2v[2][7] = {};        // per view: tstart+cstart+n_items, perm, pos, aux, bcnt
+  size_t off_gsig = 0, off_gant = 0; // rfr_filter_gather: gathered signal rows and positions
   int t2_bwd_splits = 1;
   size_t cap_trs = 0, cap_tfp = 0;
   size_t cap_cpart = 0;
@@ -234,6 +235,8 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     const int64_t ns1 = std::max<int64_t>(n_s, 1);
     L.t2_bwd_splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t(1) << 30) / (ns1 * 20)));
     L.off_t2bwdp = take((size_t)L.t2_bwd_splits * 5 * ns1 * 4);
+    L.off_gsig = take((size_t)na1 * nf * 8);
+    L.off_gant = take((size_t)3 * na1 * 4);
     const int64_t nb = (np + kT2SortBlock - 1) / kT2SortBlock;
     for (int v = 0; v < 2; ++v) {
       L.off_t2v[v][0] = take((size_t)(2 * (kT2Max + 1) + 1) * 4);
@@ -737,6 +740,59 @@ rfr_status rfr_filter(const float *signal, const rfr_antennas *ants, const rfr_f
   if (!power && n_query > 0) return RFR_E_ARG;
   return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, comm, ws,
                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+rfr_status rfr_filter_gather(const float *signal, const rfr_antennas *ants, int64_t n_ant_total,
+                             const rfr_freq_grid *grid, const float *qx, const float *qy,
+                             const float *qz, int64_t n_query, float *power, float *mf,
+                             const rfr_comm *comm, const rfr_workspace *ws, rfr_stream_t stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!comm) {
+    if (!power && n_query > 0) return RFR_E_ARG;
+    return filter_impl(signal, ants, grid, qx, qy, qz, n_query, power, mf, nullptr, ws, st);
+  }
+  RFR_TRY(check_ants(ants));
+  RFR_TRY(check_grid(grid));
+  if (ants->rx_x || ants->phi_tx || n_ant_total < 0 || n_query < 0) return RFR_E_ARG;
+  const int N = comm->nranks, r = comm->rank;
+  auto shard = [&](int64_t n, int k, int64_t &lo, int64_t &hi) {
+    const int64_t base = n / N, rem = n % N;
+    lo = k * base + std::min<int64_t>(k, rem);
+    hi = lo + base + (k < rem ? 1 : 0);
+  };
+  int64_t alo, ahi;
+  shard(n_ant_total, r, alo, ahi);
+  if (ants->n_ant != ahi - alo) return RFR_E_SHAPE;
+  Layout L;
+  RFR_TRY(check_ws(ws, 0, n_query, L, n_ant_total, grid->n_freq));
+  int64_t qlo, qhi;
+  shard(n_query, r, qlo, qhi);
+  if (qhi > qlo && !power) return RFR_E_ARG;
+  float2 *gsig = at<float2>(ws, L.off_gsig);
+  float *gant = at<float>(ws, L.off_gant);        // [3][n_ant_total]
+  // all-gather by one broadcast per rank (exact, contiguous slices; concurrent in the group)
+  if (ncclGroupStart() != ncclSuccess) return RFR_E_NCCL;
+  for (int k = 0; k < N; ++k) {
+    int64_t lo, hi;
+    shard(n_ant_total, k, lo, hi);
+    if (hi == lo) continue;
+    const size_t nrow = (size_t)(hi - lo);
+    const bool me = k == r;
+    ncclBroadcast(me ? (const void *)signal : nullptr, gsig + lo * grid->n_freq,
+                  nrow * grid->n_freq * 2, ncclFloat32, k, comm->nccl, st);
+    const float *src[3] = {ants->tx_x, ants->tx_y, ants->tx_z};
+    for (int c = 0; c < 3; ++c)
+      ncclBroadcast(me ? (const void *)src[c] : nullptr, gant + c * n_ant_total + lo, nrow,
+                    ncclFloat32, k, comm->nccl, st);
+  }
+  if (ncclGroupEnd() != ncclSuccess) return RFR_E_NCCL;
+  if (qhi == qlo) return RFR_OK;
+  rfr_antennas all;
+  memset(&all, 0, sizeof(all));
+  all.tx_x = gant; all.tx_y = gant + n_ant_total; all.tx_z = gant + 2 * n_ant_total;
+  all.n_ant = n_ant_total;
+  return filter_impl(reinterpret_cast<const float *>(gsig), &all, grid, qx + qlo, qy + qlo,
+                     qz + qlo, qhi - qlo, power, mf, nullptr, ws, st);
 }
 
 rfr_status rfr_filter_partial(const float *signal, const rfr_antennas *ants,

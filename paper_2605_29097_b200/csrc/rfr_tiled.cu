@@ -551,6 +551,21 @@ __global__ void k2_select(T2Args a) {
   pl->inv_g = a.kd / dg;
 }
 
+// g1.z = (2 d_a - L_c) -> (2 d_a - L_c) inv_t: x at the antenna's tile distance (the sweeps read
+// the geometry as stored)
+__global__ void k2_geofix(T2Args a, const int *tstart) {
+  const T2Plan pl = *a.plan;
+  if (pl.P == 0) return;
+  const int64_t n = (int64_t)pl.T * a.n_a;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(w / a.n_a);
+    if (tstart[t + 1] == tstart[t]) continue;
+    float4 *g = a.tgeo + w * 2 + 1;
+    g->z = (float)((double)g->z * pl.inv_t);
+  }
+}
+
 // ------------------------------------------------------------------ tables
 // a[m][q] = eps_q (-j)^q J_q(2 pi m' delta_g) (Miller's backward recurrence in fp64), q < Pg;
 // tabs[0][k] = node x_k = cos(pi (k + 1/2) / P); tabs[1][j][k] = W (node values -> monomial
@@ -674,8 +689,9 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
   k2_tsetup<<<(unsigned)((a.n_a + 127) / 128), 128, 0, st>>>(a, srt.tstart);
   k2_gsetup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
   k2_select<<<1, 1, 0, st>>>(a);
+  k2_geofix<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
   k2_tables<<<1 + (a.n_f + 127) / 128, 128, 0, st>>>(a);
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(6);
   return e;
 }
 
@@ -728,74 +744,103 @@ __global__ void __launch_bounds__(kGexpThreads) k2_gexp(T2Args a, const float2 *
   }
 }
 
-// per (antenna, tile): F at the tile's P Chebyshev nodes (global expansion, or the direct bin sum
-// when Pg == 0), then the monomial coefficients c_j = sum_k W[j][k] F_k in fp64.  CTA = one
-// antenna x 128 tiles (the antenna's expansion broadcast from shared memory).
+// per (tile, antenna): F at the tile's P Chebyshev nodes (global expansion; the direct bin sum when
+// Pg == 0), then the monomial coefficients c_j = sum_k W[j][k] F_k accumulated in fp64, stored
+// reversed (c_{P-1} first: the order the sweeps' Horner reads them).  Thread = (tile, antenna),
+// antennas fastest (coalesced centre reads and coefficient writes).
+// F(u) = sum_m X[m] e^{+j 2 pi m' u}, fp64 (the fallback when no global expansion applies)
+__device__ __noinline__ float2 t2_direct_F(const float2 *X, int n_f, double u) {
+  double sr = 0.0, si = 0.0;
+  for (int m = 0; m < n_f; ++m) {
+    const double c = (double)(m - n_f / 2) * u;
+    double ps, pc;
+    sincospi(2.0 * (c - rint(c)), &ps, &pc);
+    const float2 v = X[m];
+    sr += pc * v.x - ps * v.y;
+    si += pc * v.y + ps * v.x;
+  }
+  return make_float2((float)sr, (float)si);
+}
+
+template <int P>
+__device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, int t, int64_t i,
+                                             const float2 *X0, const float2 *X1,
+                                             const double (*W)[kT2PMax], const double *xk) {
+  const int Pg = pl.Pg, T = pl.T;
+  const int nrow = X1 ? 2 : 1;
+  const double uc = a.lc[(int64_t)t * a.n_a + i] * a.kd;
+  const double ug = a.lg[i * 3] * a.kd;
+  for (int row = 0; row < nrow; ++row) {
+    float Fr[P], Fi[P];
+    if (Pg) {
+      // Clenshaw over q for all nodes at once: b_q = G_q + 2 y b_{q+1} - b_{q+2}
+      float y[P], b1r[P], b1i[P], b2r[P], b2i[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        y[k] = (float)((uc + pl.delta_t * xk[k] - ug) / pl.delta_g);
+        b1r[k] = b1i[k] = b2r[k] = b2i[k] = 0.f;
+      }
+      const float2 *G = a.gexp + ((int64_t)row * a.n_a + i) * kT2PgMax;
+      for (int q = Pg - 1; q >= 1; --q) {
+        const float2 g = G[q];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const float br = fmaf(2.f * y[k], b1r[k], g.x - b2r[k]);
+          const float bi = fmaf(2.f * y[k], b1i[k], g.y - b2i[k]);
+          b2r[k] = b1r[k]; b2i[k] = b1i[k];
+          b1r[k] = br; b1i[k] = bi;
+        }
+      }
+      const float2 g0 = G[0];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        Fr[k] = fmaf(y[k], b1r[k], g0.x - b2r[k]);
+        Fi[k] = fmaf(y[k], b1i[k], g0.y - b2i[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < P; ++k) {          // direct bin sums (wide global spread, Pg == 0)
+        const float2 f = t2_direct_F((row == 0 ? X0 : X1) + i * a.n_f, a.n_f, uc + pl.delta_t * xk[k]);
+        Fr[k] = f.x;
+        Fi[k] = f.y;
+      }
+    }
+    float2 *dst = a.coef + (((int64_t)row * T + t) * a.n_a + i) * P;
+#pragma unroll 1
+    for (int j = 0; j < P; ++j) {
+      double cr = 0.0, ci = 0.0;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        cr = fma(W[j][k], (double)Fr[k], cr);
+        ci = fma(W[j][k], (double)Fi[k], ci);
+      }
+      dst[P - 1 - j] = make_float2((float)cr, (float)ci);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, const float2 *X0,
                                                 const float2 *X1) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
-  const int P = pl.P, Pg = pl.Pg, T = pl.T;
-  const int64_t i = blockIdx.x;
-  const int t = blockIdx.y * blockDim.x + threadIdx.x;
-  const int nrow = X1 ? 2 : 1;
-  __shared__ float2 G[2][kT2PgMax];
   __shared__ double W[kT2PMax][kT2PMax];
   __shared__ double xk[kT2PMax];
-  for (int w = threadIdx.x; w < nrow * kT2PgMax; w += blockDim.x) {
-    const int row = w / kT2PgMax, q = w % kT2PgMax;
-    G[row][q] = Pg ? a.gexp[((int64_t)row * a.n_a + i) * kT2PgMax + q] : make_float2(0.f, 0.f);
-  }
   for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
     W[w / kT2PMax][w % kT2PMax] = a.tabs[kT2PMax * kT2PMax + w];
   if (threadIdx.x < kT2PMax) xk[threadIdx.x] = a.tabs[threadIdx.x];
   __syncthreads();
-  if (t >= T || tstart[t + 1] == tstart[t]) return;
-  const double uc = a.lc[(int64_t)t * a.n_a + i] * a.kd;
-  const double ug = a.lg[i * 3] * a.kd;
-  double Fr[2][kT2PMax], Fi[2][kT2PMax];
-  for (int k = 0; k < P; ++k) {
-    const double u = uc + pl.delta_t * xk[k];
-    if (Pg) {
-      // Clenshaw in fp32 on y = (u - u_g) / delta_g in [-1, 1]
-      const float y = (float)((u - ug) / pl.delta_g), y2 = 2.f * y;
-      for (int row = 0; row < nrow; ++row) {
-        float b1r = 0.f, b1i = 0.f, b2r = 0.f, b2i = 0.f;
-        for (int q = Pg - 1; q >= 1; --q) {
-          const float br = fmaf(y2, b1r, G[row][q].x - b2r), bi = fmaf(y2, b1i, G[row][q].y - b2i);
-          b2r = b1r; b2i = b1i;
-          b1r = br; b1i = bi;
-        }
-        Fr[row][k] = (double)fmaf(y, b1r, G[row][0].x - b2r);
-        Fi[row][k] = (double)fmaf(y, b1i, G[row][0].y - b2i);
-      }
-    } else {
-      // direct: F(u) = sum_m X[m] e^{+j 2 pi m' u} (wide global spread)
-      for (int row = 0; row < nrow; ++row) {
-        const float2 *X = (row == 0 ? X0 : X1) + i * a.n_f;
-        double sr = 0.0, si = 0.0;
-        for (int m = 0; m < a.n_f; ++m) {
-          const double c = (double)(m - a.n_f / 2) * u;
-          double ps, pc;
-          sincospi(2.0 * (c - rint(c)), &ps, &pc);
-          const float2 v = X[m];
-          sr += pc * v.x - ps * v.y;
-          si += pc * v.y + ps * v.x;
-        }
-        Fr[row][k] = sr;
-        Fi[row][k] = si;
-      }
-    }
-  }
-  for (int row = 0; row < nrow; ++row) {
-    float2 *dst = a.coef + (((int64_t)row * T + t) * a.n_a + i) * P;
-    for (int j = 0; j < P; ++j) {
-      double cr = 0.0, ci = 0.0;
-      for (int k = 0; k < P; ++k) {
-        cr = fma(W[j][k], Fr[row][k], cr);
-        ci = fma(W[j][k], Fi[row][k], ci);
-      }
-      dst[j] = make_float2((float)cr, (float)ci);
+  const int64_t n = (int64_t)pl.T * a.n_a;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(w / a.n_a);
+    const int64_t i = w % a.n_a;
+    if (tstart[t + 1] == tstart[t]) continue;
+    switch (pl.P) {
+      case 8: k2_cprep_one<8>(a, pl, t, i, X0, X1, W, xk); break;
+      case 10: k2_cprep_one<10>(a, pl, t, i, X0, X1, W, xk); break;
+      case 12: k2_cprep_one<12>(a, pl, t, i, X0, X1, W, xk); break;
+      case 14: k2_cprep_one<14>(a, pl, t, i, X0, X1, W, xk); break;
+      default: k2_cprep_one<16>(a, pl, t, i, X0, X1, W, xk); break;
     }
   }
 }
@@ -812,7 +857,7 @@ cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0
     if (e != cudaSuccess) return e;
   }
   k2_gexp<<<(unsigned)a.n_a, kGexpThreads, sm, st>>>(a, X0, X1);
-  dim3 g((unsigned)a.n_a, (unsigned)((kT2Max + 127) / 128));
+  const unsigned g = (unsigned)std::min<int64_t>((kT2Max * a.n_a + 127) / 128, 148 * 64);
   k2_cprep<<<g, 128, 0, st>>>(a, tstart, X0, X1);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(2);
@@ -866,26 +911,30 @@ __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x 
   return o;
 }
 
-constexpr int kT2GA = 16;                         // antennas per shared-memory stage
+constexpr int kT2GA = 32;                         // antennas per shared-memory stage
 
-// stage the coefficients (reversed: cs[aa][k] = c_{P-1-k}) and the geometry of antennas
-// [i0, i0 + ga) of tile t
+// shared-memory stages of the adjoint sweeps, double-buffered: per antenna its P coefficients
+// (stored reversed by k2_cprep: cs[aa][k] = c_{P-1-k}) and its tile-relative geometry (g1.z already
+// scaled by inv_t), copied with cp.async while the previous stage is computed
+struct AdjStage {
+  float2 cs[2][kT2GA][kT2PMax];
+  float4 gs[2][kT2GA][2];
+};
 template <int P>
-__device__ __forceinline__ void t2_stage(const T2Args &a, const T2Plan &pl, int row, int t,
-                                         int64_t i0, int ga, float2 (*cs)[kT2PMax],
-                                         float4 (*gs)[2]) {
-  const float2 *src = a.coef + (((int64_t)row * pl.T + t) * a.n_a + i0) * P;
-  for (int w = threadIdx.x; w < ga * P; w += blockDim.x) {
-    const int aa = w / P, j = w % P;
-    cs[aa][P - 1 - j] = src[w];
+__device__ __forceinline__ void t2_stage_async(const T2Args &a, const T2Plan &pl, int row, int t,
+                                               int64_t i0, int ga, AdjStage &sm, int b) {
+  const float4 *src = reinterpret_cast<const float4 *>(
+      a.coef + (((int64_t)row * pl.T + t) * a.n_a + i0) * P);
+  float4 *dst = reinterpret_cast<float4 *>(&sm.cs[b][0][0]);
+  constexpr int kPerAnt = P / 2;                  // float4 chunks of one antenna's coefficients
+  for (int w = threadIdx.x; w < ga * kPerAnt; w += blockDim.x) {
+    const int aa = w / kPerAnt, c = w % kPerAnt;
+    cp_async16(dst + aa * (kT2PMax / 2) + c, src + w);
   }
-  if ((int)threadIdx.x < ga) {
-    const float4 *g = a.tgeo + ((int64_t)t * a.n_a + i0 + threadIdx.x) * 2;
-    float4 g1 = g[1];
-    g1.z = (float)((double)g1.z * pl.inv_t);       // x at the antenna's tile distance d_a
-    gs[threadIdx.x][0] = g[0];
-    gs[threadIdx.x][1] = g1;
-  }
+  const float4 *g = a.tgeo + ((int64_t)t * a.n_a + i0) * 2;
+  float4 *gd = &sm.gs[b][0][0];
+  for (int w = threadIdx.x; w < ga * 2; w += blockDim.x) cp_async16(gd + w, g + w);
+  cp_async_commit();
 }
 
 // h = sum_j c_j x^j for two points (packed x), coefficients reversed in cs (P even, unrolled)
@@ -911,8 +960,7 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 template <int P>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
-                                               int n_splits, int64_t aps, float2 (*cs)[kT2PMax],
-                                               float4 (*gs)[2]) {
+                                               int n_splits, int64_t aps, AdjStage &sm) {
   const int total = *s.n_items * n_splits;
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -940,19 +988,23 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
 #pragma unroll
     for (int u = 0; u < 4; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
-    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA) {
+    __syncthreads();                               // the previous item's stages are consumed
+    if (i_lo < i_hi) t2_stage_async<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    int b = 0;
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
+      cp_async_wait_all();
       __syncthreads();
-      t2_stage<P>(a, pl, row, t, i0, ga, cs, gs);
-      __syncthreads();
+      if (i0 + kT2GA < i_hi)
+        t2_stage_async<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
-        const float4 g0 = gs[aa][0], g1 = gs[aa][1];
+        const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
         const Geo2 e01 = t2_geo2<false>(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
         const Geo2 e23 = t2_geo2<false>(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
         f2x h[4];
-        t2_horner2<P>(cs[aa], e01.x, h[0], h[1]);
-        t2_horner2<P>(cs[aa], e23.x, h[2], h[3]);
+        t2_horner2<P>(sm.cs[b][aa], e01.x, h[0], h[1]);
+        t2_horner2<P>(sm.cs[b][aa], e23.x, h[2], h[3]);
         const float2 c01 = upk(e01.c), s01 = upk(e01.s), c23 = upk(e23.c), s23 = upk(e23.s);
         A1[0] = ffma2(bcv(c01.x), h[0], A1[0]); A2[0] = ffma2(bcv(s01.x), h[0], A2[0]);
         A1[1] = ffma2(bcv(c01.y), h[1], A1[1]); A2[1] = ffma2(bcv(s01.y), h[1], A2[1]);
@@ -975,14 +1027,13 @@ __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
   const T2Plan pl = *a.plan;
-  __shared__ __align__(16) float2 cs[kT2GA][kT2PMax];
-  __shared__ float4 gs[kT2GA][2];
+  __shared__ __align__(16) AdjStage sm;
   switch (pl.P) {
-    case 8: k2_filter_body<8>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
-    case 10: k2_filter_body<10>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
-    case 12: k2_filter_body<12>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
-    case 14: k2_filter_body<14>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
-    case 16: k2_filter_body<16>(a, pl, s, row, out, n_out, n_splits, aps, cs, gs); break;
+    case 8: k2_filter_body<8>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 16: k2_filter_body<16>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -996,7 +1047,7 @@ template <int P>
 __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                             int row, float *__restrict__ out, int64_t n_out,
                                             int n_splits, int64_t aps, bool no_gain,
-                                            float2 (*cs)[kT2PMax], float4 (*gs)[2]) {
+                                            AdjStage &sm) {
   const int total = *s.n_items * n_splits;
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -1026,17 +1077,21 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
     const f2x nq = ffma2(nx, qx, ffma2(ny, qy, fmul2(nz, qz)));
     f2x U = 0ull, SF = 0ull, Wx = 0ull, Wy = 0ull, Wz = 0ull;
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
-    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA) {
+    __syncthreads();                               // the previous item's stages are consumed
+    if (i_lo < i_hi) t2_stage_async<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    int b = 0;
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
+      cp_async_wait_all();
       __syncthreads();
-      t2_stage<P>(a, pl, row, t, i0, ga, cs, gs);
-      __syncthreads();
+      if (i0 + kT2GA < i_hi)
+        t2_stage_async<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
-        const float4 g0 = gs[aa][0], g1 = gs[aa][1];
+        const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
         const Geo2 e = t2_geo2<true>(g0, g1, qx, qy, qz, qw, kc2f, inv2f);   // (cos, -sin)
         f2x h0, h1;
-        t2_horner2<P>(cs[aa], e.x, h0, h1);
+        t2_horner2<P>(sm.cs[b][aa], e.x, h0, h1);
         // R = Re(E h) = c hr - s hi
         const float2 hv0 = upk(h0), hv1 = upk(h1);
         const f2x R = ffma2(e.c, pk(hv0.x, hv1.x), fmul2(e.s, pk(hv0.y, hv1.y)));
@@ -1087,14 +1142,13 @@ __global__ void __launch_bounds__(128, 4) k2_bwd(T2Args a, T2Sorted s, int row,
                                                  float *__restrict__ out, int64_t n_out,
                                                  int n_splits, int64_t aps, bool no_gain) {
   const T2Plan pl = *a.plan;
-  __shared__ __align__(16) float2 cs[kT2GA][kT2PMax];
-  __shared__ float4 gs[kT2GA][2];
+  __shared__ __align__(16) AdjStage sm;
   switch (pl.P) {
-    case 8: k2_bwd_body<8>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
-    case 10: k2_bwd_body<10>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
-    case 12: k2_bwd_body<12>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
-    case 14: k2_bwd_body<14>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
-    case 16: k2_bwd_body<16>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, cs, gs); break;
+    case 8: k2_bwd_body<8>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 10: k2_bwd_body<10>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 12: k2_bwd_body<12>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 14: k2_bwd_body<14>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 16: k2_bwd_body<16>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
     default: break;
   }
 }
@@ -1124,11 +1178,15 @@ __global__ void k2_bsum(const T2Plan *plp, const float *__restrict__ part, int S
 // c_ij = A_ij e^{-j 2 pi f_c tau_ij} (trace: A = w g gamma T^2, Eq. 5) or the K5 weight c_q.
 constexpr int kT2FwdTJ = kT2FwdAnts;             // records per shared-memory stage (one per thread)
 
+// staged records, one float per component (SoA) so that a float2 load yields a record pair:
+// 0-2 q' = q - c_t, 3 |q'|^2, 4 w T^2 (trace) / Re c (K5), 5 n.q' (trace) / Im c (K5), 6-8 n
 struct FwdStage {
-  float4 q[2][kT2FwdTJ];                          // q' = q - c_t, |q'|^2
-  float4 r[2][kT2FwdTJ];                          // trace: (w T^2, n.q', -, -); K5: (Re c, Im c)
-  float4 n[2][kT2FwdTJ];                          // trace: normal
+  float v[2][9][kT2FwdTJ];
 };
+__device__ __forceinline__ f2x ld2(const float *p) {
+  const float2 v = *reinterpret_cast<const float2 *>(p);
+  return pk(v.x, v.y);
+}
 
 template <int P, int KIND>
 __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
@@ -1149,12 +1207,11 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
       const float4 *g = a.tgeo + ((int64_t)t * a.n_a + i) * 2;
       g0 = g[0];
       g1 = g[1];
-      g1.z = (float)((double)g1.z * pl.inv_t);
     }
     const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
-    f2x M[P];
+    f2x Mre[P], Mim[P];
 #pragma unroll
-    for (int p = 0; p < P; ++p) M[p] = 0ull;
+    for (int p = 0; p < P; ++p) { Mre[p] = 0ull; Mim[p] = 0ull; }
     // this thread's record of the next stage, prefetched into registers
     float4 pv = make_float4(cx, cy, cz, 0.f), pn = make_float4(0.f, 0.f, 1.f, 0.f);
     if (j_lo + threadIdx.x < j_hi) { pv = s.pos[j_lo + threadIdx.x]; pn = s.aux[j_lo + threadIdx.x]; }
@@ -1162,13 +1219,16 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
     for (int64_t jt = j_lo; jt < j_hi; jt += kT2FwdTJ, b ^= 1) {
       {
         const float x = pv.x - cx, y = pv.y - cy, z = pv.z - cz;
-        sm.q[b][threadIdx.x] = make_float4(x, y, z, fmaf(x, x, fmaf(y, y, z * z)));
+        float(*v)[kT2FwdTJ] = sm.v[b];
+        const int k = threadIdx.x;
+        v[0][k] = x; v[1][k] = y; v[2][k] = z; v[3][k] = fmaf(x, x, fmaf(y, y, z * z));
         if (KIND == kFwdTrace) {
-          sm.r[b][threadIdx.x] =
-              make_float4(pv.w * pn.w * pn.w, fmaf(pn.x, x, fmaf(pn.y, y, pn.z * z)), 0.f, 0.f);
-          sm.n[b][threadIdx.x] = make_float4(pn.x, pn.y, pn.z, 0.f);
+          v[4][k] = pv.w * pn.w * pn.w;
+          v[5][k] = fmaf(pn.x, x, fmaf(pn.y, y, pn.z * z));
+          v[6][k] = pn.x; v[7][k] = pn.y; v[8][k] = pn.z;
         } else {
-          sm.r[b][threadIdx.x] = make_float4(pv.w, pn.w, 0.f, 0.f);   // K5: w = Re c, T = Im c
+          v[4][k] = pv.w;                                   // K5 records: w = Re c_q, T = Im c_q
+          v[5][k] = pn.w;
         }
       }
       __syncthreads();
@@ -1179,10 +1239,9 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
       const int nv = (int)min((int64_t)kT2FwdTJ, j_hi - jt);
 #pragma unroll 1
       for (int jj = 0; jj < nv; jj += 2) {
-        const float4 qa = sm.q[b][jj], qb = sm.q[b][jj + 1];
-        const Geo2 e = t2_geo2<true>(g0, g1, pk(qa.x, qb.x), pk(qa.y, qb.y), pk(qa.z, qb.z),
-                                     pk(qa.w, qb.w), kc2f, inv2f);    // (cos, -sin)
-        const float4 ra = sm.r[b][jj], rb = sm.r[b][jj + 1];
+        const float(*v)[kT2FwdTJ] = sm.v[b];
+        const Geo2 e = t2_geo2<true>(g0, g1, ld2(&v[0][jj]), ld2(&v[1][jj]), ld2(&v[2][jj]),
+                                     ld2(&v[3][jj]), kc2f, inv2f);    // (cos, -sin)
         f2x cre, cim;
         if (KIND == kFwdTrace) {
           const f2x r2 = fmul2(e.r, e.r);
@@ -1190,38 +1249,37 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
           if (no_gain) {
             gg = bcv(1.f);
           } else {
-            const float4 na = sm.n[b][jj], nb = sm.n[b][jj + 1];
-            const f2x nd = ffma2(pk(na.x, nb.x), h0x,
-                                 ffma2(pk(na.y, nb.y), h0y, ffma2(pk(na.z, nb.z), h0z, pk(ra.y, rb.y))));
+            const f2x nd = ffma2(ld2(&v[6][jj]), h0x,
+                                 ffma2(ld2(&v[7][jj]), h0y, ffma2(ld2(&v[8][jj]), h0z, ld2(&v[5][jj]))));
             const f2x ndr2 = fmul2(nd, r2);
             const float2 gv = upk(ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f)));
             gg = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
           }
           // A = w T^2 g gamma; c = A e^{-j theta} = (A cos, A (-sin))
-          const f2x A = fmul2(fmul2(pk(ra.x, rb.x), gg), fmul2(r2, bcv(kInv16Pi2f)));
+          const f2x A = fmul2(fmul2(ld2(&v[4][jj]), gg), fmul2(r2, bcv(kInv16Pi2f)));
           cre = fmul2(A, e.c);
           cim = fmul2(A, e.s);
         } else {
           // c = (Ar + j Ai) e^{-j theta} = (Ar cos - Ai (-sin), Ai cos + Ar (-sin))
-          const f2x Ar = pk(ra.x, rb.x), Ai = pk(ra.y, rb.y);
+          const f2x Ar = ld2(&v[4][jj]), Ai = ld2(&v[5][jj]);
           cre = ffma2(Ar, e.c, fmul2(Ai, fmul2(e.s, bcv(-1.f))));
           cim = ffma2(Ai, e.c, fmul2(Ar, e.s));
         }
-        const float2 crv = upk(cre), civ = upk(cim);
-        const f2x c0 = pk(crv.x, civ.x), c1 = pk(crv.y, civ.y);
-        // plain recurrence on v_p = s_p T_p(x), s = (+ + - -); M'[p] = s_p M[p]
+        // moments in record-packed pairs (lane = record): Mre[p] += v_p(x) cre, Mim[p] += v_p(x) cim,
+        // v_p = s_p T_p(x) by the plain recurrence, s = (+ + - -); no re-pairing of the records
         const f2x x = e.x, tp = fadd2(x, x), tn = fmul2(x, bcv(-2.f));
-        const float2 xv = upk(x);
-        M[0] = fadd2(M[0], fadd2(c0, c1));
-        M[1] = ffma2(bcv(xv.x), c0, ffma2(bcv(xv.y), c1, M[1]));
+        Mre[0] = fadd2(Mre[0], cre);
+        Mim[0] = fadd2(Mim[0], cim);
+        Mre[1] = ffma2(x, cre, Mre[1]);
+        Mim[1] = ffma2(x, cim, Mim[1]);
         f2x v2 = bcv(1.f), v1 = x;
 #pragma unroll
         for (int p = 2; p < P; ++p) {
           const f2x v = ffma2((p & 1) ? tp : tn, v1, v2);
           v2 = v1;
           v1 = v;
-          const float2 wv = upk(v);
-          M[p] = ffma2(bcv(wv.x), c0, ffma2(bcv(wv.y), c1, M[p]));
+          Mre[p] = ffma2(v, cre, Mre[p]);
+          Mim[p] = ffma2(v, cim, Mim[p]);
         }
       }
     }
@@ -1230,7 +1288,8 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
       float2 *dst = a.mom + ((int64_t)t * a.n_a + i) * P;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        float2 v = upk(M[p]);
+        const float2 r = upk(Mre[p]), i2 = upk(Mim[p]);
+        float2 v = make_float2(r.x + r.y, i2.x + i2.y);
         if ((p >> 1) & 1) { v.x = -v.x; v.y = -v.y; }
         dst[p] = v;
       }

@@ -75,7 +75,7 @@ EXPORTS = ("rfr_workspace_size", "rfr_forward", "rfr_loss", "rfr_filter", "rfr_f
            "rfr_backward_filter", "rfr_backward_filter_partial", "rfr_filter_backward", "rfr_heatmap_loss",
            "rfr_comm_unique_id", "rfr_comm_init", "rfr_comm_destroy",
            "rfr_poll_flags", "rfr_status_string", "rfr_abi_version", "rfr_launch_count",
-           "rfr_plan_state", "rfr_profile_enable", "rfr_profile_read")
+           "rfr_plan_state", "rfr_profile_enable", "rfr_profile_read", "rfr_filter_gather")
 
 
 class RfrError(RuntimeError):
@@ -113,6 +113,7 @@ def load(path: str = LIB_PATH):
         "rfr_heatmap_loss": [vp, vp, i64, vp, vp, f, f, vp, vp, vp, W, vp],
         "rfr_poll_flags": [W, C.POINTER(u32), C.c_void_p],
         "rfr_plan_state": [W, C.POINTER(rfr_plan_info), C.c_void_p],
+        "rfr_filter_gather": [vp, A, i64, G, vp, vp, vp, i64, vp, vp, vp, W, vp],
         "rfr_profile_enable": [C.c_int],
         "rfr_profile_read": [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)],
         "rfr_comm_unique_id": [vp],
@@ -309,6 +310,20 @@ def rfr_filter_partial(signal, ants: DeviceAntennas, grid, qx, qy, qz, mf: torch
     return mf
 
 
+def rfr_filter_gather(signal: torch.Tensor, ants: DeviceAntennas, grid, qx, qy, qz,
+                      power: torch.Tensor, ws: torch.Tensor, comm: Optional["Comm"] = None,
+                      n_ant_total: Optional[int] = None, mf: Optional[torch.Tensor] = None,
+                      stream=None):
+    """Query-sharded filter (see include/librfr.h): power / mf hold this rank's query slice
+    shard_range(len(qx), rank, world)."""
+    a, g = ants.struct(), grid_struct(grid)
+    n_tot = ants.n * (comm.nranks if comm else 1) if n_ant_total is None else n_ant_total
+    _check(load().rfr_filter_gather(_ptr(signal), C.byref(a), int(n_tot), C.byref(g), _ptr(qx),
+                                    _ptr(qy), _ptr(qz), int(qx.numel()), _ptr(power), _ptr(mf),
+                                    _comm(comm), _ws(ws), _stream(stream)), "rfr_filter_gather")
+    return power
+
+
 def rfr_filter_power(mf: torch.Tensor, power: torch.Tensor, stream=None):
     _check(load().rfr_filter_power(_ptr(mf), int(power.numel()), _ptr(power), _stream(stream)),
            "rfr_filter_power")
@@ -455,8 +470,10 @@ class Comm:
     def __init__(self, handle: int, nranks: int, rank: int):
         self.handle, self.nranks, self.rank = handle, nranks, rank
 
-    @classmethod
-    def create(cls, group=None) -> "Comm":
+    @staticmethod
+    def unique_id(group=None) -> bytes:
+        """Rank 0's NCCL unique id (rfr_comm_unique_id), broadcast to every rank of the group
+        (torch.distributed: plumbing only).  Host logic, no device needed."""
         import torch.distributed as dist
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -466,7 +483,16 @@ class Comm:
         if world > 1:
             obj = [bytes(uid)]
             dist.broadcast_object_list(obj, src=0, group=group)
-            C.memmove(uid, obj[0], 128)
+            return obj[0]
+        return bytes(uid)
+
+    @classmethod
+    def create(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_char * 128)()
+        C.memmove(uid, cls.unique_id(group), 128)
         h = C.c_void_p()
         _check(load().rfr_comm_init(uid, world, rank, C.byref(h)), "rfr_comm_init")
         return cls(h.value, world, rank)
