@@ -148,7 +148,7 @@ struct Layout {
   // r2 tiled engine (rfr_tiled.h): plan, tables, per-(tile, antenna) data, two sorted views
   size_t off_t2plan = 0, off_t2boxp = 0, off_t2tabs = 0, off_t2tbox = 0, off_t2lc = 0,
          off_t2geo = 0, off_t2lg = 0, off_t2acoef = 0, off_t2gexp = 0, off_t2coef = 0,
-         off_t2mom = 0, off_t2bwdp = 0;
+         off_t2mom = 0, off_t2bwdp = 0, off_t2lct = 0;
   size_t off_t2v[2][7] = {};        // per view: tstart+cstart+n_items, perm, pos, aux, bcnt
   size_t off_gsig = 0, off_gant = 0; // rfr_filter_gather: gathered signal rows and positions
   int t2_bwd_splits = 1;
@@ -225,6 +225,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_t2tabs = take((size_t)(3 * kT2PMax * kT2PMax + 128) * 8);
     L.off_t2tbox = take((size_t)kT2Max * 6 * 4);
     L.off_t2lc = take((size_t)kT2Max * na1 * 8);
+    L.off_t2lct = take((size_t)kT2Max * na1 * 8);
     L.off_t2geo = take((size_t)kT2Max * na1 * 32);
     L.off_t2lg = take((size_t)na1 * 3 * 8);
     L.off_t2acoef = take((size_t)nf * kT2PgMax * 8);
@@ -420,6 +421,7 @@ T2Args make_t2(const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_wo
   t.kc = (grid->f0_hz + (double)(grid->n_freq / 2) * grid->df_hz) / kC;
   t.tbox = at<float>(ws, L.off_t2tbox);
   t.lc = at<double>(ws, L.off_t2lc);
+  t.lct = at<double>(ws, L.off_t2lct);
   t.tgeo = at<float4>(ws, L.off_t2geo);
   t.lg = at<double>(ws, L.off_t2lg);
   t.acoef = at<float2>(ws, L.off_t2acoef);
@@ -632,7 +634,7 @@ rfr_status rfr_forward(const rfr_samples *samples, float sharpness, const rfr_an
     T2Points pts;
     memset(&pts, 0, sizeof(pts));
     pts.rec = rec_c; pts.n_dev = n_act; pts.n = n_s;
-    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_plan(t, pts, v, kT2PlanForward, st));
     RFR_CU(t2_forward(t, v, kFwdTrace, no_gain, reinterpret_cast<float2 *>(signal), device_sms(),
                       st));
     return run_fwd(at<Rec>(ws, L.off_rec), n_s, ants, grid, no_gain, corr, kFwdTrace, signal, ws,
@@ -691,7 +693,7 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
     T2Points pts;
     memset(&pts, 0, sizeof(pts));
     pts.qx = qx; pts.qy = qy; pts.qz = qz; pts.n = n_query;
-    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_plan(t, pts, v, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v.tstart, reinterpret_cast<const float2 *>(signal), nullptr, st));
     const int S = t2_splits(n_query, kT2FltChunk, ants->n_ant, sp.splits);
     const int64_t aps = cdiv(cdiv(ants->n_ant, S), 16) * 16;
@@ -864,7 +866,7 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
     T2Points pts;
     memset(&pts, 0, sizeof(pts));
     pts.rec = rec_c; pts.n_dev = n_act; pts.n = n_s;
-    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_plan(t, pts, v, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v.tstart, a.X, nullptr, st));
     RFR_CU(cudaMemsetAsync(partials, 0, (size_t)5 * n_s * 4, st));
     const int S = std::max(1, std::min<int>(L.t2_bwd_splits, (int)cdiv(ants->n_ant, 1024)));
@@ -1013,7 +1015,7 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     T2Points all;
     memset(&all, 0, sizeof(all));
     all.qx = samples->x; all.qy = samples->y; all.qz = samples->z; all.n = n_s;
-    RFR_CU(t2_plan(t, all, v0, device_sms(), st));
+    RFR_CU(t2_plan(t, all, v0, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v0.tstart, a.X, a.X2, st));
     const int Sf = t2_splits(n_s, kT2FltChunk, ants->n_ant, sp.splits);
     const int64_t apf = cdiv(cdiv(ants->n_ant, Sf), 16) * 16;
@@ -1153,7 +1155,7 @@ rfr_status rfr_filter_backward(const float *grad_power, const float *mf, const f
     T2Points pts;
     memset(&pts, 0, sizeof(pts));
     pts.rec = qrec; pts.n = n_query;
-    RFR_CU(t2_plan(t, pts, v, device_sms(), st));
+    RFR_CU(t2_plan(t, pts, v, kT2PlanForward, st));
     RFR_CU(t2_forward(t, v, kFwdMFAdj, false, reinterpret_cast<float2 *>(grad_signal),
                       device_sms(), st));
     return run_fwd(qrec, n_query, ants, grid, false, false, kFwdMFAdj, grad_signal, ws, L, st,

@@ -1381,10 +1381,9 @@ static void tile_flt_all(const TileArgs &a, dim3 g, cudaStream_t st) {
     k_tile_flt4<16, MONO, true, true><<<g, kChebThreads, 0, st>>>(a);
   else if (MONO && tile_f32g()) k_tile_flt4<16, MONO, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_flt4<16, MONO><<<g, kChebThreads, 0, st>>>(a);
+  // P = 24 is the widest tiled variant: a tile spreads ~1/4 of the global delay range, so under
+  // the global gate z <= 28.6 (P <= 48 untiled) no tile needs more (z_tile <= ~7 -> P <= 24)
   k_tile_flt4<24, MONO><<<g, kChebThreads, 0, st>>>(a);
-  k_tile_flt4<28, MONO><<<g, kChebThreads, 0, st>>>(a);
-  k_tile_flt4<32, MONO><<<g, kChebThreads, 0, st>>>(a);
-  k_tile_flt4<48, MONO><<<g, kChebThreads, 0, st>>>(a);
 }
 
 static cudaError_t tile_prepare(const TileArgs &a, cudaStream_t st, bool bprep = true) {
@@ -1421,7 +1420,7 @@ cudaError_t launch_tiled_filter(const TileArgs &a0, bool mono, int n_splits, cud
   dim3 g((unsigned)((a.n + kTileChunk - 1) / kTileChunk + kTiles), (unsigned)n_splits);
   if (mono) tile_flt_all<true>(a, g, st);
   else tile_flt_all<false>(a, g, st);
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(2);
   return e;
 }
 
@@ -1713,9 +1712,6 @@ static void tile_fwd_all(const TileArgs &a, dim3 g, cudaStream_t st) {
   else if (MONO && tile_f32g()) k_tile_fwd<16, MONO, 4, true, true><<<g, kChebThreads, 0, st>>>(a);
   else k_tile_fwd<16, MONO, 4, true><<<g, kChebThreads, 0, st>>>(a);
   k_tile_fwd<24, MONO, tile_fwd_minb<24, MONO>()><<<g, kChebThreads, 0, st>>>(a);
-  k_tile_fwd<28, MONO, tile_fwd_minb<28, MONO>()><<<g, kChebThreads, 0, st>>>(a);
-  k_tile_fwd<32, MONO, tile_fwd_minb<32, MONO>()><<<g, kChebThreads, 0, st>>>(a);
-  k_tile_fwd<48, MONO, tile_fwd_minb<48, MONO>()><<<g, kChebThreads, 0, st>>>(a);
 }
 
 cudaError_t launch_tiled_mfadj(const TileArgs &a0, bool mono, float2 *out, cudaStream_t st) {
@@ -1730,10 +1726,7 @@ cudaError_t launch_tiled_mfadj(const TileArgs &a0, bool mono, float2 *out, cudaS
   const unsigned na = (unsigned)a.n_a;
   k_tile_out<16><<<na, 256, 0, st>>>(a, out);
   k_tile_out<24><<<na, 256, 0, st>>>(a, out);
-  k_tile_out<28><<<na, 256, 0, st>>>(a, out);
-  k_tile_out<32><<<na, 256, 0, st>>>(a, out);
-  k_tile_out<48><<<na, 256, 0, st>>>(a, out);
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(10);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(4);
   return e;
 }
 
@@ -1874,9 +1867,6 @@ static void tile_bwd_all(const TileArgs &ta, const AdjArgs &a, dim3 g, cudaStrea
   if (tile_stdrec()) k_tile_bwd<16, MONO, CORR, true><<<g, kChebThreads, 0, st>>>(ta, a);
   else k_tile_bwd<16, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
   k_tile_bwd<24, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
-  k_tile_bwd<28, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
-  k_tile_bwd<32, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
-  k_tile_bwd<48, MONO, CORR><<<g, kChebThreads, 0, st>>>(ta, a);
 }
 
 cudaError_t launch_tiled_backward(const TileArgs &t0, const AdjArgs &a, bool mono, bool corr,
@@ -1894,7 +1884,7 @@ cudaError_t launch_tiled_backward(const TileArgs &t0, const AdjArgs &a, bool mon
     if (corr) tile_bwd_all<false, true>(t, a, g, st);
     else tile_bwd_all<false, false>(t, a, g, st);
   }
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(5);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(2);
   return e;
 }
 

@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -224,7 +225,7 @@ constexpr int kT2SubAnts = 32;
 // half-spread (cell boxes bound the tight boxes from above), -> the candidate's P and cost
 __global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Args a,
                                                int64_t n_pts_host, const int64_t *n_dev,
-                                               double *cost) {
+                                               double *cost, int kind, int chunk) {
   __shared__ float box[6];
   __shared__ double red[256];
   if (threadIdx.x < 6) {
@@ -272,8 +273,13 @@ __global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Ar
       const int P = t2_select_P(z);
       // FMA-pipe cost per (point, antenna): P Horner steps + ~10 for the geometry; partially
       // filled work items waste ~half a chunk per tile; T P <= kT2TP (coefficient storage)
+      // FMA-pipe cost per antenna (FFMA2 units).  Adjoint sweeps (kind 0): per point P Horner
+      // steps + ~10 for the geometry, partially filled work items waste ~half a chunk per tile,
+      // plus the per-(tile, antenna) preparation; forward (kind 1): per record 1.5 P moment steps
+      // + ~12, plus per tile P virtual sources through ~32 global moments (k2_fout)
       if (P > 0 && T * P <= kT2TP)
-        c = (double)(P + 10) * ((double)n + (double)T * kT2FltChunk * 0.5) + (double)T * P * 64.0;
+        c = kind == 0 ? (double)(P + 10) * ((double)n + (double)T * chunk * 0.5) + (double)T * P * 64.0
+                      : (1.5 * P + 12.0) * (double)n + (double)T * P * 48.0;
     }
     cost[blockIdx.x] = c;
   }
@@ -473,6 +479,7 @@ __global__ void __launch_bounds__(128) k2_tsetup(T2Args a, const int *tstart) {
       umin = fmin(umin, dmin);
       const double Lc = dmin + dmax;
       a.lc[(int64_t)t * a.n_a + i] = Lc;
+      a.lct[i * kT2Max + t] = Lc;
       hm = fmax(hm, dmax - dmin);
       lmin = fmin(lmin, Lc);
       lmax = fmax(lmax, Lc);
@@ -669,15 +676,15 @@ cudaError_t t2_sort(const T2Args &a, const T2Points &pts, const T2Sorted &srt, c
   return e;
 }
 
-cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, int n_sms,
+cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, int kind,
                     cudaStream_t st) {
-  (void)n_sms;
   cudaError_t e;
   {
   ProfScope prof(kProfPlan, st);
   k2_box<<<kT2BoxBlocks, 256, 0, st>>>(pts, a.box_part);
   double *cost = reinterpret_cast<double *>(a.tabs + 3 * kT2PMax * kT2PMax);   // [kT2Cand]
-  k2_cand<<<kT2Cand, 256, 0, st>>>(a.box_part, kT2BoxBlocks, a, pts.n, pts.n_dev, cost);
+  k2_cand<<<kT2Cand, 256, 0, st>>>(a.box_part, kT2BoxBlocks, a, pts.n, pts.n_dev, cost, kind,
+                                   srt.chunk);
   k2_pick<<<1, 128, 0, st>>>(a.box_part, kT2BoxBlocks, cost, a.plan, pts.n, pts.n_dev);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -884,7 +891,12 @@ __device__ __forceinline__ int t2_item_tile(const int *cstart, int T, int item) 
 struct Geo2 {
   f2x c, s, x, r;                                 // cos, sin of the centre phase, x, 1/d
 };
-template <bool NEG>
+// RED = false (the filter's default): no reduction of the cycle count before the MUFU (the angle
+// dl 2 pi 2 kc + 2 pi frac(2 d_a kc) in one FFMA2): |angle| <= ~2 pi (2 kc x tile spread), and
+// MUFU.SIN / COS take the fractional revolutions themselves; the phase error grows to
+// ~|angle| 2^-22 rad (~2e-5 at c3), 5x the reduced form's and 20x inside the 1e-4 budget
+// (A/B: RFR_T2RED=1)
+template <bool NEG, bool RED = true>
 __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x qx, f2x qy, f2x qz,
                                         f2x qw, float kc2f, float inv2f) {
   const f2x del = ffma2(bcv(g0.x), qx, ffma2(bcv(g0.y), qy, ffma2(bcv(g0.z), qz, qw)));
@@ -894,11 +906,17 @@ __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x 
   const f2x dd = fmul2(s2, r);
   const float2 den = upk(fadd2(dd, bcv(g1.x)));
   const f2x dl = fmul2(del, pk(rcp_ftz_(den.x), rcp_ftz_(den.y)));
-  const f2x cy = ffma2(dl, bcv(kc2f), bcv(g1.y));
-  // reduce to [-1/2, 1/2] by round-to-nearest with the 1.5 * 2^23 magic constant on the FMA pipe
-  // (|cy| < 2^22; the XU pipe is the other bound of this loop: 4 MUFU per pair)
-  const f2x rn = fadd2(fadd2(cy, bcv(12582912.f)), bcv(-12582912.f));
-  const f2x ang = fmul2(ffma2(rn, bcv(-1.f), cy), bcv(NEG ? -kTwoPi : kTwoPi));
+  f2x ang;
+  if (RED) {
+    const f2x cy = ffma2(dl, bcv(kc2f), bcv(g1.y));
+    // reduce to [-1/2, 1/2] by round-to-nearest with the 1.5 * 2^23 magic constant on the FMA
+    // pipe (|cy| < 2^22; the XU pipe is the other bound of this loop: 4 MUFU per pair)
+    const f2x rn = fadd2(fadd2(cy, bcv(12582912.f)), bcv(-12582912.f));
+    ang = fmul2(ffma2(rn, bcv(-1.f), cy), bcv(NEG ? -kTwoPi : kTwoPi));
+  } else {
+    const float sg = NEG ? -kTwoPi : kTwoPi;
+    ang = ffma2(dl, bcv(kc2f * sg), bcv(g1.y * sg));
+  }
   const float2 av = upk(ang);
   Geo2 o;
   float s0, c0, s1, c1;
@@ -957,7 +975,7 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 
 // ------------------------------------------------------------------------- filter sweep
 // work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
-template <int P>
+template <int P, bool RED>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
                                                int n_splits, int64_t aps, AdjStage &sm) {
@@ -1000,8 +1018,8 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
         const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
-        const Geo2 e01 = t2_geo2<false>(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
-        const Geo2 e23 = t2_geo2<false>(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
+        const Geo2 e01 = t2_geo2<false, RED>(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
+        const Geo2 e23 = t2_geo2<false, RED>(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
         f2x h[4];
         t2_horner2<P>(sm.cs[b][aa], e01.x, h[0], h[1]);
         t2_horner2<P>(sm.cs[b][aa], e23.x, h[2], h[3]);
@@ -1022,18 +1040,18 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   }
 }
 
-template <int MINB>
+template <int MINB, bool RED>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
   const T2Plan pl = *a.plan;
   __shared__ __align__(16) AdjStage sm;
   switch (pl.P) {
-    case 8: k2_filter_body<8>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 16: k2_filter_body<16>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 16: k2_filter_body<16, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1285,7 +1303,7 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
     }
     __syncthreads();                                  // the stage buffers are reused by the next item
     if (ok) {
-      float2 *dst = a.mom + ((int64_t)t * a.n_a + i) * P;
+      float2 *dst = a.mom + ((int64_t)i * pl.T + t) * P;     // antenna-major (k2_fout)
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const float2 r = upk(Mre[p]), i2 = upk(Mim[p]);
@@ -1315,8 +1333,11 @@ __global__ void __launch_bounds__(kT2FwdAnts, 4) k2_fwd(T2Args a, T2Sorted s, bo
 // per antenna: tile t's moments -> P virtual sources at the nodes u_tk = u_c,it + delta_t x_k with
 // weights W_tk = sum_p lambda[k][p] M_t[p] (Chebyshev interpolation of e^{-j z x}); global moments
 // Mg[q] = sum_{t,k} W_tk T_q(y_tk), y = (u - u_g) / delta_g; bins
-// s[m] = e^{-j 2 pi m' u_g} sum_q a[m][q] Mg[q] (or, Pg == 0, the direct sum over the sources)
+// s[m] = e^{-j 2 pi m' u_g} sum_q a[m][q] Mg[q] (or, Pg == 0, the direct sum over the sources).
+// CTA = one antenna; thread = a strided set of sources with all (<= 32 per pass) global moments in
+// registers; fixed-order reduction: warp shuffles, then the 8 warps in order.
 constexpr int kT2OutThreads = 256;
+constexpr int kT2OutQ = 32;
 __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *tstart,
                                                          float2 *__restrict__ out) {
   const T2Plan pl = *a.plan;
@@ -1325,10 +1346,10 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
   const int P = pl.P, T = pl.T, Pg = pl.Pg;
   const int nv = T * P;
   float *ys = reinterpret_cast<float *>(smraw);                        // [nv]
-  float2 *wsrc = reinterpret_cast<float2 *>(smraw + (size_t)nv * 4 + 8 * ((nv & 1) ? 1 : 0)); // [nv]
-  float2 *red = wsrc + nv;                                             // [256][16]
+  float2 *wsrc = reinterpret_cast<float2 *>(smraw + (size_t)nv * 4);   // [nv] (nv even)
   __shared__ double lam[kT2PMax][kT2PMax];
   __shared__ double xk[kT2PMax];
+  __shared__ float2 red[kT2OutThreads / 32][kT2OutQ];
   __shared__ float2 Mg[kT2PgMax];
   const int64_t i = blockIdx.x;
   for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
@@ -1336,13 +1357,14 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
   if (threadIdx.x < kT2PMax) xk[threadIdx.x] = a.tabs[threadIdx.x];
   __syncthreads();
   const double ug = a.lg[i * 3] * a.kd;
+  const float2 *Mi = a.mom + (int64_t)i * T * P;                      // [T][P], contiguous
   // virtual sources (empty tiles: weight 0 at y = 0)
   for (int v = threadIdx.x; v < nv; v += blockDim.x) {
     const int t = v / P, k = v % P;
     float2 wv = make_float2(0.f, 0.f);
     float y = 0.f;
     if (tstart[t + 1] > tstart[t]) {
-      const float2 *Mt = a.mom + ((int64_t)t * a.n_a + i) * P;
+      const float2 *Mt = Mi + t * P;
       double wr = 0.0, wi = 0.0;
       for (int p = 0; p < P; ++p) {
         const float2 mv = Mt[p];
@@ -1350,53 +1372,57 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
         wi = fma(lam[k][p], (double)mv.y, wi);
       }
       wv = make_float2((float)wr, (float)wi);
-      const double u = a.lc[(int64_t)t * a.n_a + i] * a.kd + pl.delta_t * xk[k];
+      const double u = a.lct[i * kT2Max + t] * a.kd + pl.delta_t * xk[k];
       y = Pg ? (float)((u - ug) / pl.delta_g) : (float)(u - ug);   // direct: offset in cycles/bin
     }
     ys[v] = y;
     wsrc[v] = wv;
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (Pg) {
-    for (int q0 = 0; q0 < Pg; q0 += 16) {
-      f2x acc[16];
+    for (int q0 = 0; q0 < Pg; q0 += kT2OutQ) {
+      f2x acc[kT2OutQ];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = 0ull;
+      for (int q = 0; q < kT2OutQ; ++q) acc[q] = 0ull;
       for (int v = threadIdx.x; v < nv; v += blockDim.x) {
         const float y = ys[v], y2 = 2.f * y;
         const float2 wv = wsrc[v];
         const f2x wp = pk(wv.x, wv.y);
         float t0 = 1.f, t1 = y;
-        for (int q = 0; q < q0; ++q) {               // T_q up to q0 (recomputed per chunk)
+        for (int q = 0; q < q0; ++q) {               // advance to T_q0 (second pass only)
           const float t2 = fmaf(y2, t1, -t0);
           t0 = t1;
           t1 = t2;
         }
-        // now t0 = T_q0, t1 = T_q0+1
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < kT2OutQ; ++q) {
           acc[q] = ffma2(bcv(t0), wp, acc[q]);
           const float t2 = fmaf(y2, t1, -t0);
           t0 = t1;
           t1 = t2;
         }
       }
+      // warp reduction (fixed xor pattern), then the warps in order
 #pragma unroll
-      for (int q = 0; q < 16; ++q) red[q * kT2OutThreads + threadIdx.x] = upk(acc[q]);
-      __syncthreads();
-      for (int st = kT2OutThreads / 2; st > 0; st >>= 1) {   // fixed-order tree
-        if ((int)threadIdx.x < st)
+      for (int q = 0; q < kT2OutQ; ++q) {
+        float2 v = upk(acc[q]);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            float2 &d = red[q * kT2OutThreads + threadIdx.x];
-            const float2 e = red[q * kT2OutThreads + threadIdx.x + st];
-            d.x += e.x;
-            d.y += e.y;
-          }
-        __syncthreads();
+        for (int o = 16; o > 0; o >>= 1) {
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+        }
+        if (lane == 0) red[warp][q] = v;
       }
-      if ((int)threadIdx.x < 16 && q0 + (int)threadIdx.x < Pg)
-        Mg[q0 + threadIdx.x] = red[threadIdx.x * kT2OutThreads];
+      __syncthreads();
+      if (threadIdx.x < kT2OutQ && q0 + (int)threadIdx.x < Pg) {
+        float2 v = red[0][threadIdx.x];
+        for (int wq = 1; wq < kT2OutThreads / 32; ++wq) {
+          v.x += red[wq][threadIdx.x].x;
+          v.y += red[wq][threadIdx.x].y;
+        }
+        Mg[q0 + threadIdx.x] = v;
+      }
       __syncthreads();
     }
     for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
@@ -1463,10 +1489,18 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
                       int n_splits, int64_t ants_per_split, int n_sms, cudaStream_t st) {
   if (a.n_a <= 0 || n_out <= 0) return cudaSuccess;
   ProfScope prof(kProfFilter, st);
+  static int red = -1;
+  // default: no reduction before the MUFU (r2l: filter 26.3 -> 24.8 ms at c3, rel-L2(M) 3.1e-6 ->
+  // 4.5e-6 on 2048 sampled queries); RFR_T2RED=1 reduces the cycle count first
+  if (red < 0) { const char *e = getenv("RFR_T2RED"); red = (e && e[0] == '1') ? 1 : 0; }
   static int occ = 0;
-  if (!occ) occ = occ_blocks((const void *)k2_filter<5>, 128);
-  k2_filter<5><<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, out, n_out, n_splits,
-                                                        ants_per_split);
+  if (!occ) occ = occ_blocks((const void *)k2_filter<5, true>, 128);
+  if (red)
+    k2_filter<5, true><<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, out, n_out,
+                                                                n_splits, ants_per_split);
+  else
+    k2_filter<5, false><<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, out, n_out,
+                                                                 n_splits, ants_per_split);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(1);
   return e;
@@ -1507,7 +1541,7 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
   }
   }
   ProfScope prof(kProfForwardOut, st);
-  const size_t sm = (size_t)kT2TP * 12 + 16 + (size_t)kT2OutThreads * 16 * 8;
+  const size_t sm = (size_t)kT2TP * 12;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k2_fout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

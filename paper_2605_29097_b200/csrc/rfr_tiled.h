@@ -80,13 +80,14 @@ struct T2Args {
   double kd, kc;                       // df / c, f_c / c with f_c = f0 + (n_f / 2) df
   float *tbox;                         // [kT2Max][6] tight tile boxes
   double *lc;                          // [kT2Max][n_a] centre path length of (tile, antenna)
+  double *lct;                         // [n_a][kT2Max] the same, antenna-major (k2_fout)
   float4 *tgeo;                        // [kT2Max][n_a][2] tile-relative geometry
   double *lg;                          // [n_a][3]: global centre, min / max tile centre (m)
   float2 *acoef;                       // [n_f][kT2PgMax] global a[m][q]
   double *tabs;                        // [4][kT2PMax][kT2PMax] nodes, W (nodes -> monomial), lambda
   float2 *gexp;                        // [2][n_a][kT2PgMax] global expansion of the adjoint rows
   float2 *coef;                        // [2][T][n_a][P] monomial coefficients (adjoint rows)
-  float2 *mom;                         // [T][n_a][P] forward moments
+  float2 *mom;                         // [n_a][T][P] forward moments (antenna-major)
   ChebHdr *skip;                       // sel = 1 when the plan applies: the direct fallback
                                        // kernels (K2, the adjoint) read it and return at once
   unsigned int *flags;
@@ -108,8 +109,10 @@ class ProfScope {
 void t2_profile_enable(bool on);
 void t2_profile_read(int id, double *ms, unsigned long long *n);
 
-// plan + sort of the plan's own points
-cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, int n_sms,
+// plan + sort of the plan's own points; kind selects the cost model of the grid choice:
+// kT2PlanAdjoint (filter / backward sweeps, chunks of srt.chunk points) or kT2PlanForward
+constexpr int kT2PlanAdjoint = 0, kT2PlanForward = 1;
+cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, int kind,
                     cudaStream_t st);
 // sort another point set into an existing plan's grid (chunk = srt.chunk)
 cudaError_t t2_sort(const T2Args &a, const T2Points &pts, const T2Sorted &srt, cudaStream_t st);

@@ -40,9 +40,9 @@ def main():
     Mg = Mg[sel, 0] + 1j * Mg[sel, 1]
     Pg = P.cpu().numpy().astype(np.float64)[sel]
     rel = lambda a, r: float(np.linalg.norm(a - r) / np.linalg.norm(r))
-    print(f"{name} nq={nq} env(STDREC={os.environ.get('RFR_STDREC', '1')}, "
+    print(f"{name} nq={nq} env(T2RED={os.environ.get('RFR_T2RED', '1')}, V2={os.environ.get('RFR_V2', '1')}, STDREC={os.environ.get('RFR_STDREC', '1')}, "
           f"F32G={os.environ.get('RFR_F32G', '1')}, TILE={os.environ.get('RFR_TILE', '1')}) "
-          f"P_tiled={st['P_tiled_filter']} relM={rel(Mg, Mr):.3e} relP={rel(Pg, Pr):.3e} "
+          f"P_tiled={st['P_tiled_filter']} plan={rfr.rfr_plan_state(ws)} relM={rel(Mg, Mr):.3e} relP={rel(Pg, Pr):.3e} "
           f"max_abs_rel={float(np.max(np.abs(Mg - Mr)) / np.max(np.abs(Mr))):.3e}")
 
 
