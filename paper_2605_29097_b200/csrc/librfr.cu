@@ -689,13 +689,13 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
   if (ants->n_ant > 0 && use_v2(ants, false, 0)) {
     // r2 engine: plan over the queries, Horner coefficients of the signal, filter sweep
     const T2Args t = make_t2(ants, grid, ws, L);
-    const T2Sorted v = make_view(ws, L, 0, kT2FltChunk);
+    const T2Sorted v = make_view(ws, L, 0, t2_filter_chunk());
     T2Points pts;
     memset(&pts, 0, sizeof(pts));
     pts.qx = qx; pts.qy = qy; pts.qz = qz; pts.n = n_query;
     RFR_CU(t2_plan(t, pts, v, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v.tstart, reinterpret_cast<const float2 *>(signal), nullptr, st));
-    const int S = t2_splits(n_query, kT2FltChunk, ants->n_ant, sp.splits);
+    const int S = t2_splits(n_query, t2_filter_chunk(), ants->n_ant, sp.splits);
     const int64_t aps = cdiv(cdiv(ants->n_ant, S), 16) * 16;
     float2 *o = reinterpret_cast<float2 *>(S > 1 ? at<float>(ws, L.off_fltp) : M);
     RFR_CU(t2_filter(t, v, 0, o, n_query, S, aps, device_sms(), st));
@@ -862,7 +862,7 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
     RFR_CU(launch_compact(a.rec, n_s, corr, at<int>(ws, L.off_ccnt), n_act, rec_c, st,
                           at<unsigned char>(ws, L.off_aflag), idx_c));
     const T2Args t = make_t2(ants, grid, ws, L);
-    const T2Sorted v = make_view(ws, L, 0, kT2BwdChunk);
+    const T2Sorted v = make_view(ws, L, 0, t2_backward_chunk());
     T2Points pts;
     memset(&pts, 0, sizeof(pts));
     pts.rec = rec_c; pts.n_dev = n_act; pts.n = n_s;
@@ -1011,13 +1011,13 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     // rows (G and s), the filter sweep over all samples and the backward sweep over the alpha != 0
     // samples sorted into the same tiles
     const T2Args t = make_t2(ants, grid, ws, L);
-    const T2Sorted v0 = make_view(ws, L, 0, kT2FltChunk), v1 = make_view(ws, L, 1, kT2BwdChunk);
+    const T2Sorted v0 = make_view(ws, L, 0, t2_filter_chunk()), v1 = make_view(ws, L, 1, t2_backward_chunk());
     T2Points all;
     memset(&all, 0, sizeof(all));
     all.qx = samples->x; all.qy = samples->y; all.qz = samples->z; all.n = n_s;
     RFR_CU(t2_plan(t, all, v0, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v0.tstart, a.X, a.X2, st));
-    const int Sf = t2_splits(n_s, kT2FltChunk, ants->n_ant, sp.splits);
+    const int Sf = t2_splits(n_s, t2_filter_chunk(), ants->n_ant, sp.splits);
     const int64_t apf = cdiv(cdiv(ants->n_ant, Sf), 16) * 16;
     float2 *o = reinterpret_cast<float2 *>(Sf > 1 ? at<float>(ws, L.off_fltp) : mf);
     RFR_CU(t2_filter(t, v0, 1, o, n_s, Sf, apf, device_sms(), st));

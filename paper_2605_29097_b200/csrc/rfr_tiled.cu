@@ -463,53 +463,65 @@ __global__ void __launch_bounds__(256) k2_tbox(const T2Plan *plp, T2Sorted s, fl
 
 // per (tile, antenna): centre path length L_c = dmin + dmax, half-spread dmax - dmin, and the
 // tile-relative geometry around the fp32 tile centre c_t: g0 = (-2a', |a'|^2), g1 = (d_a,
-// frac(2 d_a kc), 2 d_a - L_c, 0) with a' = a - c_t, d_a = |a'| (fp64, rounded once)
-__global__ void __launch_bounds__(128) k2_tsetup(T2Args a, const int *tstart) {
+// frac(2 d_a kc), 2 d_a - L_c, 0) with a' = a - c_t, d_a = |a'| (fp64, rounded once).  Thread =
+// (tile, antenna), antennas fastest; the per-antenna range of L_c and the global maxima by
+// order-independent atomics on the fp64 bits (positive values), so the results are deterministic.
+__global__ void __launch_bounds__(256) k2_tsetup(T2Args a, const int *tstart) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double hm = 0.0, lmin = 1e300, lmax = -1e300, umin = 1e300;
-  if (i < a.n_a) {
+  const int64_t n = (int64_t)pl.T * a.n_a;
+  double hm = 0.0, umin = 1e300;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(w / a.n_a);
+    const int64_t i = w % a.n_a;
+    if (tstart[t + 1] == tstart[t]) continue;        // empty tile: never read
     const double ax = a.tx_x[i], ay = a.tx_y[i], az = a.tx_z[i];
-    for (int t = 0; t < pl.T; ++t) {
-      if (tstart[t + 1] == tstart[t]) continue;      // empty tile: never read
-      const float *b = a.tbox + t * 6;
-      double dmin, dmax;
-      t2_box_dist(b, ax, ay, az, dmin, dmax);
-      umin = fmin(umin, dmin);
-      const double Lc = dmin + dmax;
-      a.lc[(int64_t)t * a.n_a + i] = Lc;
-      a.lct[i * kT2Max + t] = Lc;
-      hm = fmax(hm, dmax - dmin);
-      lmin = fmin(lmin, Lc);
-      lmax = fmax(lmax, Lc);
-      const double px = ax - (double)t2_centre(b, 0), py = ay - (double)t2_centre(b, 1),
-                   pz = az - (double)t2_centre(b, 2);
-      const double D = px * px + py * py + pz * pz, da = sqrt(D);
-      const double cyc = 2.0 * da * a.kc;
-      float4 *g = a.tgeo + ((int64_t)t * a.n_a + i) * 2;
-      g[0] = make_float4((float)(-2.0 * px), (float)(-2.0 * py), (float)(-2.0 * pz), (float)D);
-      g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), 0.f);
-    }
-    a.lg[i * 3 + 1] = lmin;
-    a.lg[i * 3 + 2] = lmax;
+    const float *b = a.tbox + t * 6;
+    double dmin, dmax;
+    t2_box_dist(b, ax, ay, az, dmin, dmax);
+    umin = fmin(umin, dmin);
+    const double Lc = dmin + dmax;
+    a.lc[w] = Lc;
+    a.lct[i * kT2Max + t] = Lc;
+    hm = fmax(hm, dmax - dmin);
+    unsigned long long *mm = reinterpret_cast<unsigned long long *>(a.lg + i * 3);
+    atomicMin(mm + 1, (unsigned long long)__double_as_longlong(Lc));
+    atomicMax(mm + 2, (unsigned long long)__double_as_longlong(Lc));
+    const double px = ax - (double)t2_centre(b, 0), py = ay - (double)t2_centre(b, 1),
+                 pz = az - (double)t2_centre(b, 2);
+    const double D = px * px + py * py + pz * pz, da = sqrt(D);
+    const double cyc = 2.0 * da * a.kc;
+    float4 *g = a.tgeo + w * 2;
+    g[0] = make_float4((float)(-2.0 * px), (float)(-2.0 * py), (float)(-2.0 * pz), (float)D);
+    g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), 0.f);
   }
-  __shared__ double red[128];
+  __shared__ double red[256];
   red[threadIdx.x] = hm;
   __syncthreads();
-  for (int s = 64; s > 0; s >>= 1) {
-    if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+  for (int st = 128; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + st]);
     __syncthreads();
   }
   if (threadIdx.x == 0) atomicMax(&a.plan->dmax_bits, (unsigned long long)__double_as_longlong(red[0]));
   __syncthreads();
   red[threadIdx.x] = umin;
   __syncthreads();
-  for (int s = 64; s > 0; s >>= 1) {
-    if ((int)threadIdx.x < s) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s]);
+  for (int st = 128; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + st]);
     __syncthreads();
   }
   if (threadIdx.x == 0) atomicMin(&a.plan->umin_bits, (unsigned long long)__double_as_longlong(red[0]));
+}
+
+// per antenna: reset the L_c range before k2_tsetup (min: +inf bits, max: 0)
+__global__ void k2_lg_reset(T2Args a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_a;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long *mm = reinterpret_cast<unsigned long long *>(a.lg + i * 3);
+    mm[1] = (unsigned long long)__double_as_longlong(1e300);
+    mm[2] = 0ull;
+  }
 }
 
 // per antenna: the global interval covering every tile's [L_c -+ h_t]
@@ -521,8 +533,9 @@ __global__ void __launch_bounds__(256) k2_gsetup(T2Args a) {
   double hg = 0.0;
   if (i < a.n_a) {
     const double lmin = a.lg[i * 3 + 1], lmax = a.lg[i * 3 + 2];
-    a.lg[i * 3] = 0.5 * (lmin + lmax);
-    hg = 0.5 * (lmax - lmin) + ht;
+    const bool any = lmin <= lmax;                   // the antenna sees at least one tile
+    a.lg[i * 3] = any ? 0.5 * (lmin + lmax) : 0.0;
+    hg = any ? 0.5 * (lmax - lmin) + ht : 0.0;
   }
   __shared__ double red[256];
   red[threadIdx.x] = hg;
@@ -693,12 +706,13 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
   if ((e = t2_sort(a, pts, srt, st)) != cudaSuccess) return e;
   ProfScope prof(kProfPlan, st);
   k2_tbox<<<kT2Max, 256, 0, st>>>(a.plan, srt, a.tbox);
-  k2_tsetup<<<(unsigned)((a.n_a + 127) / 128), 128, 0, st>>>(a, srt.tstart);
+  k2_lg_reset<<<(unsigned)std::min<int64_t>((a.n_a + 255) / 256, 1024), 256, 0, st>>>(a);
+  k2_tsetup<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
   k2_gsetup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
   k2_select<<<1, 1, 0, st>>>(a);
   k2_geofix<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
   k2_tables<<<1 + (a.n_f + 127) / 128, 128, 0, st>>>(a);
-  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(6);
+  if ((e = cudaGetLastError()) == cudaSuccess) add_launches(7);
   return e;
 }
 
@@ -772,37 +786,41 @@ __device__ __noinline__ float2 t2_direct_F(const float2 *X, int n_f, double u) {
 template <int P>
 __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, int t, int64_t i,
                                              const float2 *X0, const float2 *X1,
-                                             const double (*W)[kT2PMax], const double *xk) {
+                                             const double (*W)[kT2PMax], const double *xk,
+                                             const float2 (*Gs)[kT2PgMax]) {
   const int Pg = pl.Pg, T = pl.T;
   const int nrow = X1 ? 2 : 1;
-  const double uc = a.lc[(int64_t)t * a.n_a + i] * a.kd;
+  const double uc = a.lct[i * kT2Max + t] * a.kd;
   const double ug = a.lg[i * 3] * a.kd;
   for (int row = 0; row < nrow; ++row) {
     float Fr[P], Fi[P];
     if (Pg) {
-      // Clenshaw over q for all nodes at once: b_q = G_q + 2 y b_{q+1} - b_{q+2}
-      float y[P], b1r[P], b1i[P], b2r[P], b2i[P];
+      // Clenshaw over q for all nodes at once, complex b packed: b_q = G_q + 2 y b_{q+1} - b_{q+2}
+      float y[P];
+      f2x b1[P], b2[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         y[k] = (float)((uc + pl.delta_t * xk[k] - ug) / pl.delta_g);
-        b1r[k] = b1i[k] = b2r[k] = b2i[k] = 0.f;
+        b1[k] = 0ull;
+        b2[k] = 0ull;
       }
-      const float2 *G = a.gexp + ((int64_t)row * a.n_a + i) * kT2PgMax;
       for (int q = Pg - 1; q >= 1; --q) {
-        const float2 g = G[q];
+        const float2 gq = Gs[row][q];                // broadcast: one antenna per CTA
+        const f2x g = pk(gq.x, gq.y);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          const float br = fmaf(2.f * y[k], b1r[k], g.x - b2r[k]);
-          const float bi = fmaf(2.f * y[k], b1i[k], g.y - b2i[k]);
-          b2r[k] = b1r[k]; b2i[k] = b1i[k];
-          b1r[k] = br; b1i[k] = bi;
+          const f2x bn = ffma2(bcv(2.f * y[k]), b1[k], ffma2(b2[k], bcv(-1.f), g));
+          b2[k] = b1[k];
+          b1[k] = bn;
         }
       }
-      const float2 g0 = G[0];
+      const float2 gq0 = Gs[row][0];
+      const f2x g0 = pk(gq0.x, gq0.y);
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        Fr[k] = fmaf(y[k], b1r[k], g0.x - b2r[k]);
-        Fi[k] = fmaf(y[k], b1i[k], g0.y - b2i[k]);
+        const float2 f = upk(ffma2(bcv(y[k]), b1[k], ffma2(b2[k], bcv(-1.f), g0)));
+        Fr[k] = f.x;
+        Fi[k] = f.y;
       }
     } else {
 #pragma unroll
@@ -826,29 +844,34 @@ __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, 
   }
 }
 
+// CTA = (one antenna, 128 tiles): the antenna's global expansions staged in shared memory (every
+// thread reads the same coefficient: broadcast), antenna-major centres (coalesced)
 __global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, const float2 *X0,
                                                 const float2 *X1) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
   __shared__ double W[kT2PMax][kT2PMax];
   __shared__ double xk[kT2PMax];
+  __shared__ float2 Gs[2][kT2PgMax];
+  const int64_t i = blockIdx.x;
+  const int t = blockIdx.y * blockDim.x + threadIdx.x;
+  if (blockIdx.y * blockDim.x >= pl.T) return;
   for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
     W[w / kT2PMax][w % kT2PMax] = a.tabs[kT2PMax * kT2PMax + w];
   if (threadIdx.x < kT2PMax) xk[threadIdx.x] = a.tabs[threadIdx.x];
+  const int nrow = X1 ? 2 : 1;
+  for (int w = threadIdx.x; w < nrow * kT2PgMax; w += blockDim.x)
+    Gs[w / kT2PgMax][w % kT2PgMax] =
+        pl.Pg ? a.gexp[((int64_t)(w / kT2PgMax) * a.n_a + i) * kT2PgMax + w % kT2PgMax]
+              : make_float2(0.f, 0.f);
   __syncthreads();
-  const int64_t n = (int64_t)pl.T * a.n_a;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(w / a.n_a);
-    const int64_t i = w % a.n_a;
-    if (tstart[t + 1] == tstart[t]) continue;
-    switch (pl.P) {
-      case 8: k2_cprep_one<8>(a, pl, t, i, X0, X1, W, xk); break;
-      case 10: k2_cprep_one<10>(a, pl, t, i, X0, X1, W, xk); break;
-      case 12: k2_cprep_one<12>(a, pl, t, i, X0, X1, W, xk); break;
-      case 14: k2_cprep_one<14>(a, pl, t, i, X0, X1, W, xk); break;
-      default: k2_cprep_one<16>(a, pl, t, i, X0, X1, W, xk); break;
-    }
+  if (t >= pl.T || tstart[t + 1] == tstart[t]) return;
+  switch (pl.P) {
+    case 8: k2_cprep_one<8>(a, pl, t, i, X0, X1, W, xk, Gs); break;
+    case 10: k2_cprep_one<10>(a, pl, t, i, X0, X1, W, xk, Gs); break;
+    case 12: k2_cprep_one<12>(a, pl, t, i, X0, X1, W, xk, Gs); break;
+    case 14: k2_cprep_one<14>(a, pl, t, i, X0, X1, W, xk, Gs); break;
+    default: k2_cprep_one<16>(a, pl, t, i, X0, X1, W, xk, Gs); break;
   }
 }
 
@@ -864,8 +887,7 @@ cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0
     if (e != cudaSuccess) return e;
   }
   k2_gexp<<<(unsigned)a.n_a, kGexpThreads, sm, st>>>(a, X0, X1);
-  const unsigned g = (unsigned)std::min<int64_t>((kT2Max * a.n_a + 127) / 128, 148 * 64);
-  k2_cprep<<<g, 128, 0, st>>>(a, tstart, X0, X1);
+  k2_cprep<<<dim3((unsigned)a.n_a, (unsigned)(kT2Max / 128)), 128, 0, st>>>(a, tstart, X0, X1);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(2);
   return e;
@@ -956,6 +978,22 @@ __device__ __forceinline__ void t2_stage_async(const T2Args &a, const T2Plan &pl
 }
 
 // h = sum_j c_j x^j for two points (packed x), coefficients reversed in cs (P even, unrolled)
+// the same, point-packed: hre = (Re h(x0), Re h(x1)), him = (Im h(x0), Im h(x1)) -- two FFMA2
+// per coefficient and point pair with the coefficient's parts as broadcast operands; the results
+// stay in the point-packed layout of the geometry (no re-pairing in the epilogue)
+template <int P>
+__device__ __forceinline__ void t2_horner_pp(const float2 *cs, f2x x, f2x &hre, f2x &him) {
+  const float4 c01 = *reinterpret_cast<const float4 *>(cs);
+  hre = ffma2(x, bcv(c01.x), bcv(c01.z));
+  him = ffma2(x, bcv(c01.y), bcv(c01.w));
+#pragma unroll
+  for (int k = 2; k < P; k += 2) {
+    const float4 c = *reinterpret_cast<const float4 *>(cs + k);
+    hre = ffma2(x, ffma2(x, hre, bcv(c.x)), bcv(c.z));
+    him = ffma2(x, ffma2(x, him, bcv(c.y)), bcv(c.w));
+  }
+}
+
 template <int P>
 __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x &h1) {
   const float2 xv = upk(x);
@@ -975,36 +1013,41 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 
 // ------------------------------------------------------------------------- filter sweep
 // work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
-template <int P, bool RED>
+template <int P, bool RED, int NPAIR, bool PIPE>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
                                                int n_splits, int64_t aps, AdjStage &sm) {
+  constexpr int SPT = 2 * NPAIR;                   // points per thread (chunk = SPT * 128)
   const int total = *s.n_items * n_splits;
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
     const int t = t2_item_tile(s.cstart, pl.T, item);
-    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * kT2FltChunk;
+    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * (SPT * 128);
     const int64_t end = s.tstart[t + 1];
     const float *tb = a.tbox + t * 6;
     const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
-    float qp[4][4];
-    bool valid[4];
+    f2x qx[NPAIR], qy[NPAIR], qz[NPAIR], qw[NPAIR];
+    bool valid[SPT];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t k = base + threadIdx.x + u * 128;
-      valid[u] = k < end;
-      const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
-      qp[u][0] = v.x - cx; qp[u][1] = v.y - cy; qp[u][2] = v.z - cz;
-      qp[u][3] = fmaf(qp[u][0], qp[u][0], fmaf(qp[u][1], qp[u][1], qp[u][2] * qp[u][2]));
+    for (int pp = 0; pp < NPAIR; ++pp) {
+      float v4[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = 2 * pp + h;
+        const int64_t k = base + threadIdx.x + u * 128;
+        valid[u] = k < end;
+        const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
+        v4[h][0] = v.x - cx; v4[h][1] = v.y - cy; v4[h][2] = v.z - cz;
+        v4[h][3] = fmaf(v4[h][0], v4[h][0], fmaf(v4[h][1], v4[h][1], v4[h][2] * v4[h][2]));
+      }
+      qx[pp] = pk(v4[0][0], v4[1][0]); qy[pp] = pk(v4[0][1], v4[1][1]);
+      qz[pp] = pk(v4[0][2], v4[1][2]); qw[pp] = pk(v4[0][3], v4[1][3]);
     }
-    const f2x qx01 = pk(qp[0][0], qp[1][0]), qy01 = pk(qp[0][1], qp[1][1]),
-              qz01 = pk(qp[0][2], qp[1][2]), qw01 = pk(qp[0][3], qp[1][3]);
-    const f2x qx23 = pk(qp[2][0], qp[3][0]), qy23 = pk(qp[2][1], qp[3][1]),
-              qz23 = pk(qp[2][2], qp[3][2]), qw23 = pk(qp[2][3], qp[3][3]);
-    f2x A1[4], A2[4];
+    // per point M = A1 + j A2, A1 = sum cos h, A2 = sum sin h (complex h, one register pair)
+    f2x A1[SPT], A2[SPT];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
+    for (int u = 0; u < SPT; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
     if (i_lo < i_hi) t2_stage_async<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
@@ -1015,24 +1058,50 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
       __syncthreads();
       if (i0 + kT2GA < i_hi)
         t2_stage_async<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+      // PIPE: the next antenna's geometry (MUFU chains) is issued before this antenna's Horner
+      Geo2 nxt[NPAIR];
+      if (PIPE) {
+        const float4 g0 = sm.gs[b][0][0], g1 = sm.gs[b][0][1];
+#pragma unroll
+        for (int pp = 0; pp < NPAIR; ++pp)
+          nxt[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
+      }
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
-        const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
-        const Geo2 e01 = t2_geo2<false, RED>(g0, g1, qx01, qy01, qz01, qw01, kc2f, inv2f);
-        const Geo2 e23 = t2_geo2<false, RED>(g0, g1, qx23, qy23, qz23, qw23, kc2f, inv2f);
-        f2x h[4];
-        t2_horner2<P>(sm.cs[b][aa], e01.x, h[0], h[1]);
-        t2_horner2<P>(sm.cs[b][aa], e23.x, h[2], h[3]);
-        const float2 c01 = upk(e01.c), s01 = upk(e01.s), c23 = upk(e23.c), s23 = upk(e23.s);
-        A1[0] = ffma2(bcv(c01.x), h[0], A1[0]); A2[0] = ffma2(bcv(s01.x), h[0], A2[0]);
-        A1[1] = ffma2(bcv(c01.y), h[1], A1[1]); A2[1] = ffma2(bcv(s01.y), h[1], A2[1]);
-        A1[2] = ffma2(bcv(c23.x), h[2], A1[2]); A2[2] = ffma2(bcv(s23.x), h[2], A2[2]);
-        A1[3] = ffma2(bcv(c23.y), h[3], A1[3]); A2[3] = ffma2(bcv(s23.y), h[3], A2[3]);
+        Geo2 cur[NPAIR];
+        if (PIPE) {
+          const int an = aa + 1 < ga ? aa + 1 : aa;   // the last one recomputes (no branch)
+          const float4 g0 = sm.gs[b][an][0], g1 = sm.gs[b][an][1];
+#pragma unroll
+          for (int pp = 0; pp < NPAIR; ++pp) {
+            cur[pp] = nxt[pp];
+            nxt[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
+          }
+        } else {
+          const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
+#pragma unroll
+          for (int pp = 0; pp < NPAIR; ++pp)
+            cur[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
+        }
+#pragma unroll
+        for (int pp = 0; pp < NPAIR; ++pp) {
+          const Geo2 &e = cur[pp];
+          // complex h per point: the coefficients' (re, im) pair times the broadcast x -- the
+          // point-packed form (t2_horner_pp) needs the coefficient as a broadcast addend, which
+          // FFMA2 cannot take (MOVs: r2m, filter 24.8 -> 26.8 ms)
+          f2x h0, h1;
+          t2_horner2<P>(sm.cs[b][aa], e.x, h0, h1);
+          const float2 cv = upk(e.c), sv = upk(e.s);
+          A1[2 * pp] = ffma2(bcv(cv.x), h0, A1[2 * pp]);
+          A2[2 * pp] = ffma2(bcv(sv.x), h0, A2[2 * pp]);
+          A1[2 * pp + 1] = ffma2(bcv(cv.y), h1, A1[2 * pp + 1]);
+          A2[2 * pp + 1] = ffma2(bcv(sv.y), h1, A2[2 * pp + 1]);
+        }
       }
     }
     float2 *o = out + (int64_t)split * n_out;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < SPT; ++u)
       if (valid[u]) {
         const float2 p1 = upk(A1[u]), p2 = upk(A2[u]);   // M = A1 + j A2
         o[s.perm[base + threadIdx.x + u * 128]] = make_float2(p1.x - p2.y, p1.y + p2.x);
@@ -1040,18 +1109,18 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   }
 }
 
-template <int MINB, bool RED>
+template <int MINB, bool RED, int NPAIR, bool PIPE = false>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
   const T2Plan pl = *a.plan;
   __shared__ __align__(16) AdjStage sm;
   switch (pl.P) {
-    case 8: k2_filter_body<8, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 16: k2_filter_body<16, RED>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 16: k2_filter_body<16, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1061,39 +1130,45 @@ __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int
 // dg/dn = 4 (n.w) w, gamma = 1 / (16 pi^2 d^2) (Eq. 5, gain P:L679-683), so per sample
 //   S1 = T^2 U,  S2 = 2 T chi U,  S3 = T^2 V,  U = sum_i R g gamma,  V = sum_i R gamma dg/dn
 // with R = Re(E h) (App. A.5).  Thread = 2 active samples (one packed pair).
-template <int P>
+template <int P, int NPAIR>
 __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                             int row, float *__restrict__ out, int64_t n_out,
                                             int n_splits, int64_t aps, bool no_gain,
                                             AdjStage &sm) {
+  constexpr int SPT = 2 * NPAIR;
   const int total = *s.n_items * n_splits;
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
     const int t = t2_item_tile(s.cstart, pl.T, item);
-    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * kT2BwdChunk;
+    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * (SPT * 128);
     const int64_t end = s.tstart[t + 1];
     const float *tb = a.tbox + t * 6;
     const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
-    float qp[2][4], nv[2][3], Tj[2];
-    bool valid[2];
+    f2x qx[NPAIR], qy[NPAIR], qz[NPAIR], qw[NPAIR], nx[NPAIR], ny[NPAIR], nz[NPAIR], nq[NPAIR];
+    bool valid[SPT];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t k = base + threadIdx.x + u * 128;
-      valid[u] = k < end;
-      const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
-      const float4 n4 = valid[u] ? s.aux[k] : make_float4(0.f, 0.f, 1.f, 0.f);
-      qp[u][0] = v.x - cx; qp[u][1] = v.y - cy; qp[u][2] = v.z - cz;
-      qp[u][3] = fmaf(qp[u][0], qp[u][0], fmaf(qp[u][1], qp[u][1], qp[u][2] * qp[u][2]));
-      nv[u][0] = n4.x; nv[u][1] = n4.y; nv[u][2] = n4.z;
-      Tj[u] = n4.w;
+    for (int pp = 0; pp < NPAIR; ++pp) {
+      float v4[2][4], n3[2][3];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = 2 * pp + h;
+        const int64_t k = base + threadIdx.x + u * 128;
+        valid[u] = k < end;
+        const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
+        const float4 n4 = valid[u] ? s.aux[k] : make_float4(0.f, 0.f, 1.f, 0.f);
+        v4[h][0] = v.x - cx; v4[h][1] = v.y - cy; v4[h][2] = v.z - cz;
+        v4[h][3] = fmaf(v4[h][0], v4[h][0], fmaf(v4[h][1], v4[h][1], v4[h][2] * v4[h][2]));
+        n3[h][0] = n4.x; n3[h][1] = n4.y; n3[h][2] = n4.z;
+      }
+      qx[pp] = pk(v4[0][0], v4[1][0]); qy[pp] = pk(v4[0][1], v4[1][1]);
+      qz[pp] = pk(v4[0][2], v4[1][2]); qw[pp] = pk(v4[0][3], v4[1][3]);
+      nx[pp] = pk(n3[0][0], n3[1][0]); ny[pp] = pk(n3[0][1], n3[1][1]); nz[pp] = pk(n3[0][2], n3[1][2]);
+      nq[pp] = ffma2(nx[pp], qx[pp], ffma2(ny[pp], qy[pp], fmul2(nz[pp], qz[pp])));   // n . q'
     }
-    const f2x qx = pk(qp[0][0], qp[1][0]), qy = pk(qp[0][1], qp[1][1]), qz = pk(qp[0][2], qp[1][2]),
-              qw = pk(qp[0][3], qp[1][3]);
-    const f2x nx = pk(nv[0][0], nv[1][0]), ny = pk(nv[0][1], nv[1][1]), nz = pk(nv[0][2], nv[1][2]);
-    // n . q' per sample
-    const f2x nq = ffma2(nx, qx, ffma2(ny, qy, fmul2(nz, qz)));
-    f2x U = 0ull, SF = 0ull, Wx = 0ull, Wy = 0ull, Wz = 0ull;
+    f2x U[NPAIR], SF[NPAIR], Wx[NPAIR], Wy[NPAIR], Wz[NPAIR];
+#pragma unroll
+    for (int pp = 0; pp < NPAIR; ++pp) { U[pp] = SF[pp] = Wx[pp] = Wy[pp] = Wz[pp] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
     if (i_lo < i_hi) t2_stage_async<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
@@ -1107,66 +1182,73 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
         const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
-        const Geo2 e = t2_geo2<true>(g0, g1, qx, qy, qz, qw, kc2f, inv2f);   // (cos, -sin)
-        f2x h0, h1;
-        t2_horner2<P>(sm.cs[b][aa], e.x, h0, h1);
-        // R = Re(E h) = c hr - s hi
-        const float2 hv0 = upk(h0), hv1 = upk(h1);
-        const f2x R = ffma2(e.c, pk(hv0.x, hv1.x), fmul2(e.s, pk(hv0.y, hv1.y)));
-        const f2x r2 = fmul2(e.r, e.r);
         // -a' = g0.xyz / 2:  n.(q' - a') = n.q' + n.(g0/2)
         const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
-        const f2x nd = ffma2(nx, h0x, ffma2(ny, h0y, ffma2(nz, h0z, nq)));
-        const f2x Rr2 = fmul2(R, r2);
-        if (no_gain) {                               // E11 ablation: g = 1, dg/dn = 0
-          U = fadd2(U, Rr2);
-          continue;
+#pragma unroll
+        for (int pp = 0; pp < NPAIR; ++pp) {
+          const Geo2 e = t2_geo2<true>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);  // (cos, -sin)
+          f2x hre, him;
+          t2_horner_pp<P>(sm.cs[b][aa], e.x, hre, him);
+          const f2x R = ffma2(e.c, hre, fmul2(e.s, him));          // Re(E h) = c hr - s hi
+          const f2x r2 = fmul2(e.r, e.r);
+          const f2x Rr2 = fmul2(R, r2);
+          if (no_gain) {                               // E11 ablation: g = 1, dg/dn = 0
+            U[pp] = fadd2(U[pp], Rr2);
+            continue;
+          }
+          const f2x nd = ffma2(nx[pp], h0x, ffma2(ny[pp], h0y, ffma2(nz[pp], h0z, nq[pp])));
+          const f2x ndr2 = fmul2(nd, r2);              // (n.w) / d
+          const f2x g = ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f));   // 2 (n.w)^2 - 1
+          const float2 gv = upk(g);
+          const f2x gpos = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
+          const f2x msk = pk(gv.x > 0.f ? 1.f : 0.f, gv.y > 0.f ? 1.f : 0.f);
+          U[pp] = ffma2(Rr2, gpos, U[pp]);
+          const f2x F = fmul2(fmul2(Rr2, ndr2), msk);  // R gamma 4 (n.w) / d without 4 / (4 pi)^2
+          SF[pp] = fadd2(SF[pp], F);
+          Wx[pp] = ffma2(F, h0x, Wx[pp]);
+          Wy[pp] = ffma2(F, h0y, Wy[pp]);
+          Wz[pp] = ffma2(F, h0z, Wz[pp]);
         }
-        const f2x ndr2 = fmul2(nd, r2);              // (n.w) / d
-        const f2x g = ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f));   // 2 (n.w)^2 - 1
-        const float2 gv = upk(g);
-        const f2x gpos = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
-        const f2x msk = pk(gv.x > 0.f ? 1.f : 0.f, gv.y > 0.f ? 1.f : 0.f);
-        U = ffma2(Rr2, gpos, U);
-        const f2x F = fmul2(fmul2(Rr2, ndr2), msk);  // R gamma 4 (n.w) / d without 4 / (4 pi)^2
-        SF = fadd2(SF, F);
-        Wx = ffma2(F, h0x, Wx);
-        Wy = ffma2(F, h0y, Wy);
-        Wz = ffma2(F, h0z, Wz);
       }
     }
     float *o = out + (int64_t)split * 5 * n_out;
-    const float2 Uv = upk(U), SFv = upk(SF), Wxv = upk(Wx), Wyv = upk(Wy), Wzv = upk(Wz);
-    const float Us[2] = {Uv.x, Uv.y}, SFs[2] = {SFv.x, SFv.y}, Wxs[2] = {Wxv.x, Wxv.y},
-                Wys[2] = {Wyv.x, Wyv.y}, Wzs[2] = {Wzv.x, Wzv.y};
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      if (!valid[u]) continue;
-      const int k = (int)(base + threadIdx.x + u * 128);
-      const int64_t j = s.perm[k];                              // compacted index
-      const float T = Tj[u], TT = T * T;
-      const float u16 = Us[u] * kInv16Pi2f;
-      const float f4 = 4.f * kInv16Pi2f * TT;
-      o[j] = TT * u16;                                          // S1
-      o[n_out + j] = T > 0.f ? 2.f * T * u16 : 0.f;             // S2
-      o[2 * n_out + j] = f4 * fmaf(qp[u][0], SFs[u], Wxs[u]);   // S3 = T^2 sum F (q' - a')
-      o[3 * n_out + j] = f4 * fmaf(qp[u][1], SFs[u], Wys[u]);
-      o[4 * n_out + j] = f4 * fmaf(qp[u][2], SFs[u], Wzs[u]);
+    for (int pp = 0; pp < NPAIR; ++pp) {
+      const float2 Uv = upk(U[pp]), SFv = upk(SF[pp]), Wxv = upk(Wx[pp]), Wyv = upk(Wy[pp]),
+                   Wzv = upk(Wz[pp]), qxv = upk(qx[pp]), qyv = upk(qy[pp]), qzv = upk(qz[pp]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = 2 * pp + h;
+        if (!valid[u]) continue;
+        const int k = (int)(base + threadIdx.x + u * 128);
+        const int64_t j = s.perm[k];                            // compacted index
+        const float T = s.aux[k].w, TT = T * T;
+        const float Uu = h ? Uv.y : Uv.x, SFu = h ? SFv.y : SFv.x;
+        const float u16 = Uu * kInv16Pi2f;
+        const float f4 = 4.f * kInv16Pi2f * TT;
+        o[j] = TT * u16;                                        // S1
+        o[n_out + j] = T > 0.f ? 2.f * T * u16 : 0.f;           // S2
+        // S3 = T^2 sum F (q' - a')
+        o[2 * n_out + j] = f4 * fmaf(h ? qxv.y : qxv.x, SFu, h ? Wxv.y : Wxv.x);
+        o[3 * n_out + j] = f4 * fmaf(h ? qyv.y : qyv.x, SFu, h ? Wyv.y : Wyv.x);
+        o[4 * n_out + j] = f4 * fmaf(h ? qzv.y : qzv.x, SFu, h ? Wzv.y : Wzv.x);
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(128, 4) k2_bwd(T2Args a, T2Sorted s, int row,
-                                                 float *__restrict__ out, int64_t n_out,
-                                                 int n_splits, int64_t aps, bool no_gain) {
+template <int MINB, int NPAIR>
+__global__ void __launch_bounds__(128, MINB) k2_bwd(T2Args a, T2Sorted s, int row,
+                                                    float *__restrict__ out, int64_t n_out,
+                                                    int n_splits, int64_t aps, bool no_gain) {
   const T2Plan pl = *a.plan;
   __shared__ __align__(16) AdjStage sm;
   switch (pl.P) {
-    case 8: k2_bwd_body<8>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
-    case 10: k2_bwd_body<10>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
-    case 12: k2_bwd_body<12>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
-    case 14: k2_bwd_body<14>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
-    case 16: k2_bwd_body<16>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 8: k2_bwd_body<8, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 10: k2_bwd_body<10, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 12: k2_bwd_body<12, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 14: k2_bwd_body<14, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
+    case 16: k2_bwd_body<16, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
     default: break;
   }
 }
@@ -1345,40 +1427,41 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
   extern __shared__ unsigned char smraw[];
   const int P = pl.P, T = pl.T, Pg = pl.Pg;
   const int nv = T * P;
-  float *ys = reinterpret_cast<float *>(smraw);                        // [nv]
-  float2 *wsrc = reinterpret_cast<float2 *>(smraw + (size_t)nv * 4);   // [nv] (nv even)
-  __shared__ double lam[kT2PMax][kT2PMax];
-  __shared__ double xk[kT2PMax];
+  float2 *Ms = reinterpret_cast<float2 *>(smraw);                     // [T][P] this antenna's moments
+  double *Lt = reinterpret_cast<double *>(smraw + (size_t)nv * 8);     // [T] tile centres (m)
+  __shared__ float lam[kT2PMax][kT2PMax];
+  __shared__ float xk[kT2PMax];
   __shared__ float2 red[kT2OutThreads / 32][kT2OutQ];
   __shared__ float2 Mg[kT2PgMax];
   const int64_t i = blockIdx.x;
   for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
-    lam[w / kT2PMax][w % kT2PMax] = a.tabs[2 * kT2PMax * kT2PMax + w];
-  if (threadIdx.x < kT2PMax) xk[threadIdx.x] = a.tabs[threadIdx.x];
+    lam[w / kT2PMax][w % kT2PMax] = (float)a.tabs[2 * kT2PMax * kT2PMax + w];
+  if (threadIdx.x < kT2PMax) xk[threadIdx.x] = (float)a.tabs[threadIdx.x];
+  // coalesced staging of the antenna's moments and tile centres (empty tiles: zero moments)
+  const float2 *Mi = a.mom + (int64_t)i * nv;
+  for (int w = threadIdx.x; w < nv; w += blockDim.x) {
+    const int t = w / P;
+    Ms[w] = tstart[t + 1] > tstart[t] ? Mi[w] : make_float2(0.f, 0.f);
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x)
+    Lt[t] = tstart[t + 1] > tstart[t] ? a.lct[i * kT2Max + t] : a.lg[i * 3];
   __syncthreads();
   const double ug = a.lg[i * 3] * a.kd;
-  const float2 *Mi = a.mom + (int64_t)i * T * P;                      // [T][P], contiguous
-  // virtual sources (empty tiles: weight 0 at y = 0)
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+  const double dt = pl.delta_t;
+  // source v = (tile t, node k): u = u_c,it + delta_t x_k, weight W = sum_p lambda[k][p] M_t[p]
+  // (lambda is a well-conditioned interpolation transpose: |lambda| <= 2 / P, fp32)
+  auto source = [&](int v, float &y, float2 &wv) {
     const int t = v / P, k = v % P;
-    float2 wv = make_float2(0.f, 0.f);
-    float y = 0.f;
-    if (tstart[t + 1] > tstart[t]) {
-      const float2 *Mt = Mi + t * P;
-      double wr = 0.0, wi = 0.0;
-      for (int p = 0; p < P; ++p) {
-        const float2 mv = Mt[p];
-        wr = fma(lam[k][p], (double)mv.x, wr);
-        wi = fma(lam[k][p], (double)mv.y, wi);
-      }
-      wv = make_float2((float)wr, (float)wi);
-      const double u = a.lct[i * kT2Max + t] * a.kd + pl.delta_t * xk[k];
-      y = Pg ? (float)((u - ug) / pl.delta_g) : (float)(u - ug);   // direct: offset in cycles/bin
+    float wr = 0.f, wi = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float2 mv = Ms[t * P + p];
+      wr = fmaf(lam[k][p], mv.x, wr);
+      wi = fmaf(lam[k][p], mv.y, wi);
     }
-    ys[v] = y;
-    wsrc[v] = wv;
-  }
-  __syncthreads();
+    wv = make_float2(wr, wi);
+    const double u = Lt[t] * a.kd + dt * (double)xk[k];
+    y = Pg ? (float)((u - ug) / pl.delta_g) : (float)(u - ug);
+  };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (Pg) {
     for (int q0 = 0; q0 < Pg; q0 += kT2OutQ) {
@@ -1386,8 +1469,10 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
 #pragma unroll
       for (int q = 0; q < kT2OutQ; ++q) acc[q] = 0ull;
       for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        const float y = ys[v], y2 = 2.f * y;
-        const float2 wv = wsrc[v];
+        float y;
+        float2 wv;
+        source(v, y, wv);
+        const float y2 = 2.f * y;
         const f2x wp = pk(wv.x, wv.y);
         float t0 = 1.f, t1 = y;
         for (int q = 0; q < q0; ++q) {               // advance to T_q0 (second pass only)
@@ -1439,15 +1524,17 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
       out[i * a.n_f + m] = make_float2(fmaf(pc, re, ps * im), fmaf(pc, im, -ps * re));
     }
   } else {
-    // direct: s[m] = sum_v W_v e^{-j 2 pi m' u_v}, u_v = u_g + ys[v]
+    // direct (no global expansion applies): s[m] = sum_v W_v e^{-j 2 pi m' u_v}, u_v = u_g + y_v
     for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
       const double mc = (double)(m - a.n_f / 2);
       double re = 0.0, im = 0.0;
       for (int v = 0; v < nv; ++v) {
-        const double c = mc * (ug + (double)ys[v]);
+        float y;
+        float2 wv;
+        source(v, y, wv);
+        const double c = mc * (ug + (double)y);
         double ps, pc;
         sincospi(2.0 * (c - rint(c)), &ps, &pc);
-        const float2 wv = wsrc[v];
         re += pc * wv.x + ps * wv.y;
         im += pc * wv.y - ps * wv.x;
       }
@@ -1476,6 +1563,18 @@ int occ_blocks(const void *k, int threads) {
 
 }  // namespace
 
+int t2_backward_chunk() {
+  static int c = 0;
+  if (!c) { const char *e = getenv("RFR_T2BPT"); c = (e && atoi(e) == 4) ? 4 * 128 : kT2BwdChunk; }
+  return c;
+}
+
+int t2_filter_chunk() {
+  static int c = 0;
+  if (!c) { const char *e = getenv("RFR_T2SPT"); c = (e && atoi(e) == 8) ? 8 * 128 : kT2FltChunk; }
+  return c;
+}
+
 cudaError_t t2_sum_splits(const T2Args &a, const float *part, int S, int64_t n, float *out,
                           int n_sms, cudaStream_t st) {
   const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)n_sms * 8);
@@ -1489,18 +1588,22 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
                       int n_splits, int64_t ants_per_split, int n_sms, cudaStream_t st) {
   if (a.n_a <= 0 || n_out <= 0) return cudaSuccess;
   ProfScope prof(kProfFilter, st);
-  static int red = -1;
   // default: no reduction before the MUFU (r2l: filter 26.3 -> 24.8 ms at c3, rel-L2(M) 3.1e-6 ->
   // 4.5e-6 on 2048 sampled queries); RFR_T2RED=1 reduces the cycle count first
+  static int red = -1;
   if (red < 0) { const char *e = getenv("RFR_T2RED"); red = (e && e[0] == '1') ? 1 : 0; }
-  static int occ = 0;
-  if (!occ) occ = occ_blocks((const void *)k2_filter<5, true>, 128);
-  if (red)
-    k2_filter<5, true><<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, out, n_out,
-                                                                n_splits, ants_per_split);
-  else
-    k2_filter<5, false><<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, out, n_out,
-                                                                 n_splits, ants_per_split);
+  const unsigned g4 = (unsigned)(n_sms * 5), g8 = (unsigned)(n_sms * 3);
+  if (srt.chunk == 8 * 128) {
+    if (red) k2_filter<3, true, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else k2_filter<3, false, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else {
+    static int pipe = -1;
+    if (pipe < 0) { const char *e = getenv("RFR_T2PIPE"); pipe = e ? atoi(e) : 0; }
+    if (red) k2_filter<5, true, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else if (pipe == 1) k2_filter<5, false, 2, true><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else if (pipe == 2) k2_filter<4, false, 2, true><<<(unsigned)(n_sms * 4), 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else k2_filter<5, false, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(1);
   return e;
@@ -1511,12 +1614,14 @@ cudaError_t t2_backward(const T2Args &a, const T2Sorted &srt, int row, const int
                         int n_splits, int64_t ants_per_split, bool no_gain, int n_sms,
                         cudaStream_t st) {
   if (a.n_a <= 0 || n_c <= 0) return cudaSuccess;
-  static int occ = 0;
-  if (!occ) occ = occ_blocks((const void *)k2_bwd, 128);
   {
     ProfScope prof(kProfBackward, st);
-    k2_bwd<<<(unsigned)(n_sms * occ), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
-                                                    ants_per_split, no_gain);
+    if (srt.chunk == 4 * 128)
+      k2_bwd<3, 2><<<(unsigned)(n_sms * 3), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
+                                                          ants_per_split, no_gain);
+    else
+      k2_bwd<4, 1><<<(unsigned)(n_sms * 4), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
+                                                          ants_per_split, no_gain);
   }
   const unsigned g = (unsigned)std::min<int64_t>((n_c + 255) / 256, (int64_t)n_sms * 8);
   k2_bsum<<<g, 256, 0, st>>>(a.plan, part, n_splits, n_c, n_dev, idx, out, n_s);
@@ -1541,7 +1646,7 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
   }
   }
   ProfScope prof(kProfForwardOut, st);
-  const size_t sm = (size_t)kT2TP * 12;
+  const size_t sm = (size_t)kT2TP * 8 + (size_t)kT2Max * 8;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k2_fout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

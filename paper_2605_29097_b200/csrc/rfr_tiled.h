@@ -32,6 +32,8 @@ constexpr int kT2PgMax = 48;           // moments of the global expansion
 constexpr int kT2BoxBlocks = 128;
 constexpr int kT2SortBlock = 1024;     // points per counting-sort block
 constexpr int kT2FltChunk = 512;       // points per filter work item (4 per thread)
+int t2_filter_chunk();                 // 512, or 1024 (8 points per thread) with RFR_T2SPT=8
+int t2_backward_chunk();               // 256, or 512 (4 points per thread) with RFR_T2BPT=4
 constexpr int kT2BwdChunk = 256;       // points per backward work item (2 per thread)
 constexpr int kT2FwdAnts = 128;        // antennas per forward work item
 
