@@ -228,7 +228,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_t2lct = take((size_t)kT2Max * na1 * 8);
     L.off_t2geo = take((size_t)kT2Max * na1 * 32);
     L.off_t2lg = take((size_t)na1 * 3 * 8);
-    L.off_t2acoef = take((size_t)nf * kT2PgMax * 8);
+    L.off_t2acoef = take((size_t)2 * nf * kT2PgMax * 8);     // both layouts
     L.off_t2gexp = take((size_t)2 * na1 * kT2PgMax * 8);
     L.off_t2coef = take((size_t)2 * kT2TP * na1 * 8);
     L.off_t2mom = take((size_t)kT2TP * na1 * 8);

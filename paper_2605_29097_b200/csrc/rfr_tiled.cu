@@ -665,7 +665,8 @@ __global__ void k2_tables(T2Args a) {
                    : q == 1 ? make_float2(0.f, (float)-v)
                    : q == 2 ? make_float2((float)-v, 0.f)
                             : make_float2(0.f, (float)v);
-    a.acoef[(int64_t)m * kT2PgMax + p] = c;
+    a.acoef[(int64_t)p * a.n_f + m] = c;           // [q][m]: coalesced over bins (k2_fout)
+    a.acoef[(int64_t)kT2PgMax * a.n_f + (int64_t)m * kT2PgMax + p] = c;   // [m][q] (k2_gexp)
   }
 }
 
@@ -747,7 +748,7 @@ __global__ void __launch_bounds__(kGexpThreads) k2_gexp(T2Args a, const float2 *
     float re = 0.f, im = 0.f;
     if (q < Pg)
       for (int m = r; m < N; m += 4) {
-        const float2 c = a.acoef[(int64_t)m * kT2PgMax + q], y = ys[m];   // y conj(c)
+        const float2 c = a.acoef[(int64_t)kT2PgMax * N + (int64_t)m * kT2PgMax + q], y = ys[m];   // y conj(c)
         re = fmaf(y.x, c.x, fmaf(y.y, c.y, re));
         im = fmaf(y.y, c.x, fmaf(-y.x, c.y, im));
       }
@@ -954,30 +955,33 @@ __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x 
 constexpr int kT2GA = 32;                         // antennas per shared-memory stage
 
 // shared-memory stages of the adjoint sweeps, double-buffered: per antenna its P coefficients
-// (stored reversed by k2_cprep: cs[aa][k] = c_{P-1-k}) and its tile-relative geometry (g1.z already
-// scaled by inv_t), copied with cp.async while the previous stage is computed
+// (stored reversed by k2_cprep: c_{P-1} first) and its tile-relative geometry (g1.z already scaled
+// by inv_t).  Both blocks are contiguous in HBM for a run of antennas, so one thread moves a stage
+// with two bulk copies on the TMA engine (cp.async.bulk, completion on the buffer's mbarrier)
+// while the CTA computes the previous stage.
 struct AdjStage {
-  float2 cs[2][kT2GA][kT2PMax];
+  float2 cs[2][kT2GA * kT2PMax];                  // [buffer][antenna * P + k]
   float4 gs[2][kT2GA][2];
+  unsigned long long bar[2];
 };
-template <int P>
-__device__ __forceinline__ void t2_stage_async(const T2Args &a, const T2Plan &pl, int row, int t,
-                                               int64_t i0, int ga, AdjStage &sm, int b) {
-  const float4 *src = reinterpret_cast<const float4 *>(
-      a.coef + (((int64_t)row * pl.T + t) * a.n_a + i0) * P);
-  float4 *dst = reinterpret_cast<float4 *>(&sm.cs[b][0][0]);
-  constexpr int kPerAnt = P / 2;                  // float4 chunks of one antenna's coefficients
-  for (int w = threadIdx.x; w < ga * kPerAnt; w += blockDim.x) {
-    const int aa = w / kPerAnt, c = w % kPerAnt;
-    cp_async16(dst + aa * (kT2PMax / 2) + c, src + w);
+__device__ __forceinline__ void t2_stage_init(AdjStage &sm) {
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const float4 *g = a.tgeo + ((int64_t)t * a.n_a + i0) * 2;
-  float4 *gd = &sm.gs[b][0][0];
-  for (int w = threadIdx.x; w < ga * 2; w += blockDim.x) cp_async16(gd + w, g + w);
-  cp_async_commit();
+  __syncthreads();
+}
+template <int P>
+__device__ __forceinline__ void t2_stage_issue(const T2Args &a, const T2Plan &pl, int row, int t,
+                                               int64_t i0, int ga, AdjStage &sm, int b) {
+  if (threadIdx.x != 0) return;
+  const unsigned bc = (unsigned)(ga * P * 8), bg = (unsigned)(ga * 32);
+  mbar_arrive_expect_tx(&sm.bar[b], bc + bg);
+  bulk_g2s(&sm.cs[b][0], a.coef + (((int64_t)row * pl.T + t) * a.n_a + i0) * P, bc, &sm.bar[b]);
+  bulk_g2s(&sm.gs[b][0][0], a.tgeo + ((int64_t)t * a.n_a + i0) * 2, bg, &sm.bar[b]);
 }
 
-// h = sum_j c_j x^j for two points (packed x), coefficients reversed in cs (P even, unrolled)
 // the same, point-packed: hre = (Re h(x0), Re h(x1)), him = (Im h(x0), Im h(x1)) -- two FFMA2
 // per coefficient and point pair with the coefficient's parts as broadcast operands; the results
 // stay in the point-packed layout of the geometry (no re-pairing in the epilogue)
@@ -1013,12 +1017,13 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 
 // ------------------------------------------------------------------------- filter sweep
 // work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
-template <int P, bool RED, int NPAIR, bool PIPE>
+template <int P, bool RED, int NPAIR>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
                                                int n_splits, int64_t aps, AdjStage &sm) {
   constexpr int SPT = 2 * NPAIR;                   // points per thread (chunk = SPT * 128)
   const int total = *s.n_items * n_splits;
+  unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
@@ -1050,39 +1055,24 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
     for (int u = 0; u < SPT; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
-    if (i_lo < i_hi) t2_stage_async<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
-      cp_async_wait_all();
-      __syncthreads();
+      mbar_wait(&sm.bar[b], (ph >> b) & 1u);
+      ph ^= 1u << b;
+      __syncthreads();                             // every thread is done with buffer b ^ 1
       if (i0 + kT2GA < i_hi)
-        t2_stage_async<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
-      // PIPE: the next antenna's geometry (MUFU chains) is issued before this antenna's Horner
-      Geo2 nxt[NPAIR];
-      if (PIPE) {
-        const float4 g0 = sm.gs[b][0][0], g1 = sm.gs[b][0][1];
-#pragma unroll
-        for (int pp = 0; pp < NPAIR; ++pp)
-          nxt[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
-      }
+        t2_stage_issue<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
+        // (issuing the next antenna's geometry ahead of this Horner -- software pipelining --
+        // measured slower, r2p: 24.8 -> 25.1 ms)
+        const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
         Geo2 cur[NPAIR];
-        if (PIPE) {
-          const int an = aa + 1 < ga ? aa + 1 : aa;   // the last one recomputes (no branch)
-          const float4 g0 = sm.gs[b][an][0], g1 = sm.gs[b][an][1];
 #pragma unroll
-          for (int pp = 0; pp < NPAIR; ++pp) {
-            cur[pp] = nxt[pp];
-            nxt[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
-          }
-        } else {
-          const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
-#pragma unroll
-          for (int pp = 0; pp < NPAIR; ++pp)
-            cur[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
-        }
+        for (int pp = 0; pp < NPAIR; ++pp)
+          cur[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
 #pragma unroll
         for (int pp = 0; pp < NPAIR; ++pp) {
           const Geo2 &e = cur[pp];
@@ -1090,7 +1080,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
           // point-packed form (t2_horner_pp) needs the coefficient as a broadcast addend, which
           // FFMA2 cannot take (MOVs: r2m, filter 24.8 -> 26.8 ms)
           f2x h0, h1;
-          t2_horner2<P>(sm.cs[b][aa], e.x, h0, h1);
+          t2_horner2<P>(&sm.cs[b][aa * P], e.x, h0, h1);
           const float2 cv = upk(e.c), sv = upk(e.s);
           A1[2 * pp] = ffma2(bcv(cv.x), h0, A1[2 * pp]);
           A2[2 * pp] = ffma2(bcv(sv.x), h0, A2[2 * pp]);
@@ -1109,18 +1099,19 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   }
 }
 
-template <int MINB, bool RED, int NPAIR, bool PIPE = false>
+template <int MINB, bool RED, int NPAIR>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
   const T2Plan pl = *a.plan;
   __shared__ __align__(16) AdjStage sm;
+  t2_stage_init(sm);
   switch (pl.P) {
-    case 8: k2_filter_body<8, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 16: k2_filter_body<16, RED, NPAIR, PIPE>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 16: k2_filter_body<16, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1137,6 +1128,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
                                             AdjStage &sm) {
   constexpr int SPT = 2 * NPAIR;
   const int total = *s.n_items * n_splits;
+  unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
@@ -1171,14 +1163,15 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
     for (int pp = 0; pp < NPAIR; ++pp) { U[pp] = SF[pp] = Wx[pp] = Wy[pp] = Wz[pp] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
-    if (i_lo < i_hi) t2_stage_async<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
-      cp_async_wait_all();
-      __syncthreads();
+      mbar_wait(&sm.bar[b], (ph >> b) & 1u);
+      ph ^= 1u << b;
+      __syncthreads();                             // every thread is done with buffer b ^ 1
       if (i0 + kT2GA < i_hi)
-        t2_stage_async<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+        t2_stage_issue<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
         const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
@@ -1186,9 +1179,9 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
         const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
 #pragma unroll
         for (int pp = 0; pp < NPAIR; ++pp) {
-          const Geo2 e = t2_geo2<true>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);  // (cos, -sin)
+          const Geo2 e = t2_geo2<true, false>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);  // (cos, -sin)
           f2x hre, him;
-          t2_horner_pp<P>(sm.cs[b][aa], e.x, hre, him);
+          t2_horner_pp<P>(&sm.cs[b][aa * P], e.x, hre, him);
           const f2x R = ffma2(e.c, hre, fmul2(e.s, him));          // Re(E h) = c hr - s hi
           const f2x r2 = fmul2(e.r, e.r);
           const f2x Rr2 = fmul2(R, r2);
@@ -1243,6 +1236,7 @@ __global__ void __launch_bounds__(128, MINB) k2_bwd(T2Args a, T2Sorted s, int ro
                                                     int n_splits, int64_t aps, bool no_gain) {
   const T2Plan pl = *a.plan;
   __shared__ __align__(16) AdjStage sm;
+  t2_stage_init(sm);
   switch (pl.P) {
     case 8: k2_bwd_body<8, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
     case 10: k2_bwd_body<10, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
@@ -1288,7 +1282,7 @@ __device__ __forceinline__ f2x ld2(const float *p) {
   return pk(v.x, v.y);
 }
 
-template <int P, int KIND>
+template <int P, int KIND, int RP>
 __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                             bool no_gain, FwdStage &sm) {
   const int nab = (int)((a.n_a + kT2FwdAnts - 1) / kT2FwdAnts);
@@ -1338,48 +1332,58 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
       if (jn < j_hi) { pv = s.pos[jn]; pn = s.aux[jn]; }
       const int nv = (int)min((int64_t)kT2FwdTJ, j_hi - jt);
 #pragma unroll 1
-      for (int jj = 0; jj < nv; jj += 2) {
+      for (int jj = 0; jj < nv; jj += 2 * RP) {
         const float(*v)[kT2FwdTJ] = sm.v[b];
-        const Geo2 e = t2_geo2<true>(g0, g1, ld2(&v[0][jj]), ld2(&v[1][jj]), ld2(&v[2][jj]),
-                                     ld2(&v[3][jj]), kc2f, inv2f);    // (cos, -sin)
-        f2x cre, cim;
-        if (KIND == kFwdTrace) {
-          const f2x r2 = fmul2(e.r, e.r);
-          f2x gg;
-          if (no_gain) {
-            gg = bcv(1.f);
-          } else {
-            const f2x nd = ffma2(ld2(&v[6][jj]), h0x,
-                                 ffma2(ld2(&v[7][jj]), h0y, ffma2(ld2(&v[8][jj]), h0z, ld2(&v[5][jj]))));
-            const f2x ndr2 = fmul2(nd, r2);
-            const float2 gv = upk(ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f)));
-            gg = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
-          }
-          // A = w T^2 g gamma; c = A e^{-j theta} = (A cos, A (-sin))
-          const f2x A = fmul2(fmul2(ld2(&v[4][jj]), gg), fmul2(r2, bcv(kInv16Pi2f)));
-          cre = fmul2(A, e.c);
-          cim = fmul2(A, e.s);
-        } else {
-          // c = (Ar + j Ai) e^{-j theta} = (Ar cos - Ai (-sin), Ai cos + Ar (-sin))
-          const f2x Ar = ld2(&v[4][jj]), Ai = ld2(&v[5][jj]);
-          cre = ffma2(Ar, e.c, fmul2(Ai, fmul2(e.s, bcv(-1.f))));
-          cim = ffma2(Ai, e.c, fmul2(Ar, e.s));
-        }
-        // moments in record-packed pairs (lane = record): Mre[p] += v_p(x) cre, Mim[p] += v_p(x) cim,
-        // v_p = s_p T_p(x) by the plain recurrence, s = (+ + - -); no re-pairing of the records
-        const f2x x = e.x, tp = fadd2(x, x), tn = fmul2(x, bcv(-2.f));
-        Mre[0] = fadd2(Mre[0], cre);
-        Mim[0] = fadd2(Mim[0], cim);
-        Mre[1] = ffma2(x, cre, Mre[1]);
-        Mim[1] = ffma2(x, cim, Mim[1]);
-        f2x v2 = bcv(1.f), v1 = x;
+        // RP record pairs per iteration: independent geometry chains in flight (staged slots past
+        // nv hold zero-weight records)
+        f2x cre[RP], cim[RP], xr[RP];
 #pragma unroll
-        for (int p = 2; p < P; ++p) {
-          const f2x v = ffma2((p & 1) ? tp : tn, v1, v2);
-          v2 = v1;
-          v1 = v;
-          Mre[p] = ffma2(v, cre, Mre[p]);
-          Mim[p] = ffma2(v, cim, Mim[p]);
+        for (int rp = 0; rp < RP; ++rp) {
+          const int j2 = jj + 2 * rp;
+          const Geo2 e = t2_geo2<true, false>(g0, g1, ld2(&v[0][j2]), ld2(&v[1][j2]), ld2(&v[2][j2]),
+                                              ld2(&v[3][j2]), kc2f, inv2f);    // (cos, -sin)
+          if (KIND == kFwdTrace) {
+            const f2x r2 = fmul2(e.r, e.r);
+            f2x gg;
+            if (no_gain) {
+              gg = bcv(1.f);
+            } else {
+              const f2x nd = ffma2(ld2(&v[6][j2]), h0x,
+                                   ffma2(ld2(&v[7][j2]), h0y, ffma2(ld2(&v[8][j2]), h0z, ld2(&v[5][j2]))));
+              const f2x ndr2 = fmul2(nd, r2);
+              const float2 gv = upk(ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f)));
+              gg = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
+            }
+            // A = w T^2 g gamma; c = A e^{-j theta} = (A cos, A (-sin))
+            const f2x A = fmul2(fmul2(ld2(&v[4][j2]), gg), fmul2(r2, bcv(kInv16Pi2f)));
+            cre[rp] = fmul2(A, e.c);
+            cim[rp] = fmul2(A, e.s);
+          } else {
+            // c = (Ar + j Ai) e^{-j theta} = (Ar cos - Ai (-sin), Ai cos + Ar (-sin))
+            const f2x Ar = ld2(&v[4][j2]), Ai = ld2(&v[5][j2]);
+            cre[rp] = ffma2(Ar, e.c, fmul2(Ai, fmul2(e.s, bcv(-1.f))));
+            cim[rp] = ffma2(Ai, e.c, fmul2(Ar, e.s));
+          }
+          xr[rp] = e.x;
+        }
+#pragma unroll
+        for (int rp = 0; rp < RP; ++rp) {
+          // moments in record-packed pairs (lane = record): Mre[p] += v_p(x) cre, Mim[p] += v_p(x)
+          // cim, v_p = s_p T_p(x) by the plain recurrence, s = (+ + - -); no re-pairing
+          const f2x x = xr[rp], tp = fadd2(x, x), tn = fmul2(x, bcv(-2.f));
+          Mre[0] = fadd2(Mre[0], cre[rp]);
+          Mim[0] = fadd2(Mim[0], cim[rp]);
+          Mre[1] = ffma2(x, cre[rp], Mre[1]);
+          Mim[1] = ffma2(x, cim[rp], Mim[1]);
+          f2x v2 = bcv(1.f), v1 = x;
+#pragma unroll
+          for (int p = 2; p < P; ++p) {
+            const f2x vv = ffma2((p & 1) ? tp : tn, v1, v2);
+            v2 = v1;
+            v1 = vv;
+            Mre[p] = ffma2(vv, cre[rp], Mre[p]);
+            Mim[p] = ffma2(vv, cim[rp], Mim[p]);
+          }
         }
       }
     }
@@ -1397,16 +1401,16 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
   }
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kT2FwdAnts, 4) k2_fwd(T2Args a, T2Sorted s, bool no_gain) {
+template <int KIND, int RP, int MINB>
+__global__ void __launch_bounds__(kT2FwdAnts, MINB) k2_fwd(T2Args a, T2Sorted s, bool no_gain) {
   const T2Plan pl = *a.plan;
   __shared__ FwdStage sm;
   switch (pl.P) {
-    case 8: k2_fwd_body<8, KIND>(a, pl, s, no_gain, sm); break;
-    case 10: k2_fwd_body<10, KIND>(a, pl, s, no_gain, sm); break;
-    case 12: k2_fwd_body<12, KIND>(a, pl, s, no_gain, sm); break;
-    case 14: k2_fwd_body<14, KIND>(a, pl, s, no_gain, sm); break;
-    case 16: k2_fwd_body<16, KIND>(a, pl, s, no_gain, sm); break;
+    case 8: k2_fwd_body<8, KIND, RP>(a, pl, s, no_gain, sm); break;
+    case 10: k2_fwd_body<10, KIND, RP>(a, pl, s, no_gain, sm); break;
+    case 12: k2_fwd_body<12, KIND, RP>(a, pl, s, no_gain, sm); break;
+    case 14: k2_fwd_body<14, KIND, RP>(a, pl, s, no_gain, sm); break;
+    case 16: k2_fwd_body<16, KIND, RP>(a, pl, s, no_gain, sm); break;
     default: break;
   }
 }
@@ -1420,7 +1424,58 @@ __global__ void __launch_bounds__(kT2FwdAnts, 4) k2_fwd(T2Args a, T2Sorted s, bo
 // registers; fixed-order reduction: warp shuffles, then the 8 warps in order.
 constexpr int kT2OutThreads = 256;
 constexpr int kT2OutQ = 32;
-__global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *tstart,
+
+template <int P>
+__device__ __forceinline__ void t2_fout_tiles(int T, const float2 *Ms, const double *Lt,
+                                              const float (*lam)[kT2PMax], const float *xk,
+                                              double kd, double dt, double ug, double dg, int q0,
+                                              f2x (&acc)[kT2OutQ]) {
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    float2 M[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) M[p] = Ms[t * P + p];
+    const double uc = Lt[t] * kd;
+#pragma unroll 1
+    for (int k = 0; k < P; k += 2) {                // two nodes per pass: independent recurrences
+      f2x wp[2];
+      float y[2], y2[2], t0[2], t1[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float wr = 0.f, wi = 0.f;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          wr = fmaf(lam[k + h][p], M[p].x, wr);
+          wi = fmaf(lam[k + h][p], M[p].y, wi);
+        }
+        wp[h] = pk(wr, wi);
+        y[h] = (float)((uc + dt * (double)xk[k + h] - ug) / dg);
+        y2[h] = 2.f * y[h];
+        t0[h] = 1.f;
+        t1[h] = y[h];
+      }
+      for (int q = 0; q < q0; ++q) {                 // advance to T_q0 (second pass only)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float t2 = fmaf(y2[h], t1[h], -t0[h]);
+          t0[h] = t1[h];
+          t1[h] = t2;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kT2OutQ; ++q) {
+        acc[q] = ffma2(bcv(t0[1]), wp[1], ffma2(bcv(t0[0]), wp[0], acc[q]));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float t2 = fmaf(y2[h], t1[h], -t0[h]);
+          t0[h] = t1[h];
+          t1[h] = t2;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kT2OutThreads, 2) k2_fout(T2Args a, const int *tstart,
                                                          float2 *__restrict__ out) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
@@ -1468,25 +1523,14 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
       f2x acc[kT2OutQ];
 #pragma unroll
       for (int q = 0; q < kT2OutQ; ++q) acc[q] = 0ull;
-      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        float y;
-        float2 wv;
-        source(v, y, wv);
-        const float y2 = 2.f * y;
-        const f2x wp = pk(wv.x, wv.y);
-        float t0 = 1.f, t1 = y;
-        for (int q = 0; q < q0; ++q) {               // advance to T_q0 (second pass only)
-          const float t2 = fmaf(y2, t1, -t0);
-          t0 = t1;
-          t1 = t2;
-        }
-#pragma unroll
-        for (int q = 0; q < kT2OutQ; ++q) {
-          acc[q] = ffma2(bcv(t0), wp, acc[q]);
-          const float t2 = fmaf(y2, t1, -t0);
-          t0 = t1;
-          t1 = t2;
-        }
+      // thread = whole tiles (P compile-time: no index division); per tile its P node weights from
+      // the P moments, then every source through the Chebyshev recurrence in y
+      switch (P) {
+        case 8: t2_fout_tiles<8>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
+        case 10: t2_fout_tiles<10>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
+        case 12: t2_fout_tiles<12>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
+        case 14: t2_fout_tiles<14>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
+        default: t2_fout_tiles<16>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
       }
       // warp reduction (fixed xor pattern), then the warps in order
 #pragma unroll
@@ -1511,10 +1555,10 @@ __global__ void __launch_bounds__(kT2OutThreads) k2_fout(T2Args a, const int *ts
       __syncthreads();
     }
     for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
-      const float2 *cf = a.acoef + (int64_t)m * kT2PgMax;
+      const float2 *cf = a.acoef + m;                // [q][m] layout: stride n_f over q
       float re = 0.f, im = 0.f;
       for (int q = 0; q < Pg; ++q) {
-        const float2 c = cf[q], v = Mg[q];
+        const float2 c = cf[(int64_t)q * a.n_f], v = Mg[q];
         re = fmaf(c.x, v.x, fmaf(-c.y, v.y, re));
         im = fmaf(c.x, v.y, fmaf(c.y, v.x, im));
       }
@@ -1597,11 +1641,7 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     if (red) k2_filter<3, true, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
     else k2_filter<3, false, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else {
-    static int pipe = -1;
-    if (pipe < 0) { const char *e = getenv("RFR_T2PIPE"); pipe = e ? atoi(e) : 0; }
     if (red) k2_filter<5, true, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else if (pipe == 1) k2_filter<5, false, 2, true><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else if (pipe == 2) k2_filter<4, false, 2, true><<<(unsigned)(n_sms * 4), 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
     else k2_filter<5, false, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   }
   cudaError_t e = cudaGetLastError();
@@ -1635,14 +1675,15 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
   if (a.n_a <= 0) return cudaSuccess;
   {
   ProfScope prof(kProfForward, st);
+  static int rp = -1;
+  // two record pairs per iteration (r2q: forward 2.79 -> 2.67 ms at c3); RFR_T2FRP=1: one
+  if (rp < 0) { const char *e = getenv("RFR_T2FRP"); rp = (e && atoi(e) == 1) ? 1 : 2; }
   if (kind == kFwdTrace) {
-    static int occ = 0;
-    if (!occ) occ = occ_blocks((const void *)k2_fwd<kFwdTrace>, kT2FwdAnts);
-    k2_fwd<kFwdTrace><<<(unsigned)(n_sms * occ), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    if (rp == 2) k2_fwd<kFwdTrace, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else k2_fwd<kFwdTrace, 1, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
   } else {
-    static int occ = 0;
-    if (!occ) occ = occ_blocks((const void *)k2_fwd<kFwdMFAdj>, kT2FwdAnts);
-    k2_fwd<kFwdMFAdj><<<(unsigned)(n_sms * occ), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    if (rp == 2) k2_fwd<kFwdMFAdj, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else k2_fwd<kFwdMFAdj, 1, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
   }
   }
   ProfScope prof(kProfForwardOut, st);

@@ -85,7 +85,7 @@ struct T2Args {
   double *lct;                         // [n_a][kT2Max] the same, antenna-major (k2_fout)
   float4 *tgeo;                        // [kT2Max][n_a][2] tile-relative geometry
   double *lg;                          // [n_a][3]: global centre, min / max tile centre (m)
-  float2 *acoef;                       // [n_f][kT2PgMax] global a[m][q]
+  float2 *acoef;                       // global a[m][q]: [kT2PgMax][n_f] (q-major), then [n_f][kT2PgMax]
   double *tabs;                        // [4][kT2PMax][kT2PMax] nodes, W (nodes -> monomial), lambda
   float2 *gexp;                        // [2][n_a][kT2PgMax] global expansion of the adjoint rows
   float2 *coef;                        // [2][T][n_a][P] monomial coefficients (adjoint rows)
