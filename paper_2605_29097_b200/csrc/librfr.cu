@@ -148,7 +148,9 @@ struct Layout {
   // r2 tiled engine (rfr_tiled.h): plan, tables, per-(tile, antenna) data, two sorted views
   size_t off_t2plan = 0, off_t2boxp = 0, off_t2tabs = 0, off_t2tbox = 0, off_t2lc = 0,
          off_t2geo = 0, off_t2lg = 0, off_t2acoef = 0, off_t2gexp = 0, off_t2coef = 0,
-         off_t2mom = 0, off_t2bwdp = 0, off_t2lct = 0;
+         off_t2mom = 0, off_t2bwdp = 0, off_t2lct = 0, off_t2tcimg = 0, off_t2mg = 0,
+         off_t2fltp = 0;
+  int t2_flt_cap = 1;               // antenna splits the r2 filter's partial buffer holds
   size_t off_t2v[2][7] = {};        // per view: tstart+cstart+n_items, perm, pos, aux, bcnt
   size_t off_gsig = 0, off_gant = 0; // rfr_filter_gather: gathered signal rows and positions
   int t2_bwd_splits = 1;
@@ -156,6 +158,18 @@ struct Layout {
   size_t cap_cpart = 0;
   size_t cap_fwdp = 0, cap_bwdp = 0, cap_fltp = 0;
 };
+
+// antenna splits of the r2 filter sweep: enough work items (chunk of points x antenna split) for
+// ~24 per resident CTA slot (5 per SM), so the persistent grid's last round is short (equal-cost
+// items: with ~6 per slot the makespan was 7 items for 6.2 on average), at least 64 antennas per
+// split, at most `cap`, and the partials [S][n] within 1 GiB
+int t2_flt_splits(int64_t n_pts, int chunk, int64_t n_a, int cap) {
+  const int64_t items = std::max<int64_t>(1, cdiv(n_pts, chunk));
+  int64_t s = cdiv((int64_t)device_sms() * 5 * 24, items);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, 64)));
+  s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t(1) << 30) / (std::max<int64_t>(n_pts, 1) * 8)));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, cap));
+}
 
 bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) {
   if (n_s < 0 || n_a < 0 || n_q < 0 || n_f < 0) return false;
@@ -232,10 +246,15 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_t2gexp = take((size_t)2 * na1 * kT2PgMax * 8);
     L.off_t2coef = take((size_t)2 * kT2TP * na1 * 8);
     L.off_t2mom = take((size_t)kT2TP * na1 * 8);
+    L.off_t2tcimg = take(t2_tcimg_bytes(nf));
+    L.off_t2mg = take((size_t)na1 * kT2PgMax * 8);
     // backward split partials [S][5][n_s] (compacted index), S <= 16 within 1 GiB
     const int64_t ns1 = std::max<int64_t>(n_s, 1);
     L.t2_bwd_splits = (int)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t(1) << 30) / (ns1 * 20)));
     L.off_t2bwdp = take((size_t)L.t2_bwd_splits * 5 * ns1 * 4);
+    // r2 filter split partials [S][n_q] complex (S from t2_flt_splits at the smallest chunk)
+    L.t2_flt_cap = t2_flt_splits(np, kT2FltChunk, n_a, 16);
+    L.off_t2fltp = take(L.t2_flt_cap > 1 ? (size_t)L.t2_flt_cap * np * 8 : 0);
     L.off_gsig = take((size_t)na1 * nf * 8);
     L.off_gant = take((size_t)3 * na1 * 4);
     const int64_t nb = (np + kT2SortBlock - 1) / kT2SortBlock;
@@ -427,6 +446,8 @@ T2Args make_t2(const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_wo
   t.acoef = at<float2>(ws, L.off_t2acoef);
   t.tabs = at<double>(ws, L.off_t2tabs);
   t.gexp = at<float2>(ws, L.off_t2gexp);
+  t.tcimg = at<unsigned char>(ws, L.off_t2tcimg);
+  t.mg = at<float2>(ws, L.off_t2mg);
   t.coef = at<float2>(ws, L.off_t2coef);
   t.mom = at<float2>(ws, L.off_t2mom);
   t.skip = at<ChebHdr>(ws, kT2SkipOff);
@@ -695,12 +716,13 @@ static rfr_status filter_impl(const float *signal, const rfr_antennas *ants,
     pts.qx = qx; pts.qy = qy; pts.qz = qz; pts.n = n_query;
     RFR_CU(t2_plan(t, pts, v, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v.tstart, reinterpret_cast<const float2 *>(signal), nullptr, st));
-    const int S = t2_splits(n_query, t2_filter_chunk(), ants->n_ant, sp.splits);
+    const int S = t2_flt_splits(n_query, t2_filter_chunk(), ants->n_ant, L.t2_flt_cap);
     const int64_t aps = cdiv(cdiv(ants->n_ant, S), 16) * 16;
-    float2 *o = reinterpret_cast<float2 *>(S > 1 ? at<float>(ws, L.off_fltp) : M);
+    float2 *o = reinterpret_cast<float2 *>(S > 1 ? at<float>(ws, L.off_t2fltp) : M);
     RFR_CU(t2_filter(t, v, 0, o, n_query, S, aps, device_sms(), st));
-    if (S > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_fltp), S, n_query * 2, M, device_sms(), st));
+    if (S > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_t2fltp), S, n_query * 2, M, device_sms(), st));
     a.skip = t.skip;                                   // direct fallback: no-op when planned
+    a.gated = true;                                    // ... on one short persistent wave
     RFR_CU(launch_adjoint(a, kModeFlt, mono, false, sp.splits, st));
     if (sp.splits > 1)
       RFR_CU(launch_sum_splits(at<float>(ws, L.off_fltp), sp.splits, n_query * 2, M,
@@ -874,6 +896,7 @@ rfr_status rfr_backward_partial(const float *grad_signal, const rfr_samples *sam
     RFR_CU(t2_backward(t, v, 0, idx_c, n_act, n_s, at<float>(ws, L.off_t2bwdp), partials, n_s, S,
                        aps, a.no_gain, device_sms(), st));
     a.skip = t.skip;                                   // direct fallback: no-op when planned
+    a.gated = true;                                    // ... on one short persistent wave
     RFR_CU(launch_adjoint(a, kModeBwd, mono, corr, sp.splits, st));
     if (sp.splits > 1)
       RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,
@@ -1017,11 +1040,11 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     all.qx = samples->x; all.qy = samples->y; all.qz = samples->z; all.n = n_s;
     RFR_CU(t2_plan(t, all, v0, kT2PlanAdjoint, st));
     RFR_CU(t2_prep_adjoint(t, v0.tstart, a.X, a.X2, st));
-    const int Sf = t2_splits(n_s, t2_filter_chunk(), ants->n_ant, sp.splits);
+    const int Sf = t2_flt_splits(n_s, t2_filter_chunk(), ants->n_ant, L.t2_flt_cap);
     const int64_t apf = cdiv(cdiv(ants->n_ant, Sf), 16) * 16;
-    float2 *o = reinterpret_cast<float2 *>(Sf > 1 ? at<float>(ws, L.off_fltp) : mf);
+    float2 *o = reinterpret_cast<float2 *>(Sf > 1 ? at<float>(ws, L.off_t2fltp) : mf);
     RFR_CU(t2_filter(t, v0, 1, o, n_s, Sf, apf, device_sms(), st));
-    if (Sf > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_fltp), Sf, n_s * 2, mf, device_sms(), st));
+    if (Sf > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_t2fltp), Sf, n_s * 2, mf, device_sms(), st));
     Rec *rec_c = at<Rec>(ws, L.off_recc);
     int *idx_c = at<int>(ws, L.off_idxc);
     int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
@@ -1037,6 +1060,7 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     RFR_CU(t2_backward(t, v1, 0, idx_c, n_act, n_s, at<float>(ws, L.off_t2bwdp), partials, n_s,
                        Sb, apb, a.no_gain, device_sms(), st));
     a.skip = t.skip;                                   // direct fallback: no-op when planned
+    a.gated = true;                                    // ... on one short persistent wave
     RFR_CU(launch_adjoint(a, kModeBoth, mono, corr, sp.splits, st));
     if (sp.splits > 1) {
       RFR_CU(launch_sum_splits(at<float>(ws, L.off_bwdp), sp.splits, 5 * n_s, partials,

@@ -359,16 +359,17 @@ __device__ __forceinline__ void adj_accumulate(const PairBwd &g, float ec, float
 
 template <int MODE>
 __device__ __forceinline__ void adj_store(const AdjArgs &a, int64_t j, float S1, float S2,
-                                          float S3x, float S3y, float S3z) {
+                                          float S3x, float S3y, float S3z, int64_t split = -1) {
+  if (split < 0) split = blockIdx.y;                         // the launch's antenna split
   if (MODE == kModeBwd) {
-    float *P = a.out + (int64_t)blockIdx.y * 5 * a.n_s;     // [split][5][n_s]
+    float *P = a.out + split * 5 * a.n_s;                    // [split][5][n_s]
     P[j] = S1;
     P[a.n_s + j] = S2;
     P[2 * a.n_s + j] = S3x;
     P[3 * a.n_s + j] = S3y;
     P[4 * a.n_s + j] = S3z;
   } else {
-    float2 *M = reinterpret_cast<float2 *>(a.out) + (int64_t)blockIdx.y * a.n_s;
+    float2 *M = reinterpret_cast<float2 *>(a.out) + split * a.n_s;
     M[j] = make_float2(S1, S2);
   }
 }

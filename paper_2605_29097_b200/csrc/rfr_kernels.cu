@@ -484,16 +484,16 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint_s2(AdjArgs a) {
 }
 
 // Generic bin count (or unaligned rows): one buffer of kAdjGA antennas, CTA barriers, rolled Horner.
+// One (sample tile bx, antenna split by) per call.
 template <int MODE, bool MONO, bool CORR>
-__global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
-  if (a.skip && a.skip->sel) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void adjoint_generic(const AdjArgs &a, unsigned char *smem_raw,
+                                                int64_t bx, int64_t by) {
   float2 *X = reinterpret_cast<float2 *>(smem_raw);                      // [GA][n_f]
   AntD *ant = reinterpret_cast<AntD *>(smem_raw + a.smem_ant_off);       // [GA]
   const int tid = threadIdx.x;
   const int nf = a.n_f;
-  const int64_t j = (int64_t)blockIdx.x * kAdjThreads + tid;
-  const int64_t i_lo = (int64_t)blockIdx.y * a.ants_per_split;
+  const int64_t j = bx * kAdjThreads + tid;
+  const int64_t i_lo = by * a.ants_per_split;
   const int64_t i_hi = min(a.n_a, i_lo + a.ants_per_split);
   const bool no_gain = a.no_gain;
   const bool valid = j < a.n_s;
@@ -533,7 +533,23 @@ __global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
     }
   }
   if (domain) atomicOr(a.flags, 1u);
-  if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z);
+  if (valid) adj_store<MODE>(a, j, S1, S2, S3x, S3y, S3z, by);
+}
+// a.vgx > 0 (the r2 engine's direct fallback): a persistent grid walks the virtual grid
+// vgx x vgy, so the launch that returns at once when the plan applied is one short wave
+template <int MODE, bool MONO, bool CORR>
+__global__ void __launch_bounds__(kAdjThreads) k_adjoint(AdjArgs a) {
+  if (a.skip && a.skip->sel) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.vgx == 0) {
+    adjoint_generic<MODE, MONO, CORR>(a, smem_raw, blockIdx.x, blockIdx.y);
+    return;
+  }
+  const int64_t nv = (int64_t)a.vgx * a.vgy;
+  for (int64_t v = blockIdx.x; v < nv; v += gridDim.x) {
+    __syncthreads();                               // the previous virtual block's staging
+    adjoint_generic<MODE, MONO, CORR>(a, smem_raw, v % a.vgx, v / a.vgx);
+  }
 }
 
 // ================================================================================== K1' backward
@@ -804,6 +820,29 @@ static cudaError_t adj_t(const AdjArgs &a, dim3 grid, cudaStream_t st) {
   const bool al = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
   const int nf = al ? a.n_f : 0;
   const bool spec = a.n_f == 256 || a.n_f == 512 || a.n_f == 128 || a.n_f == 64;
+  if (a.gated) {
+    // the r2 engine's direct fallback: the generic kernel on a persistent grid (one short wave
+    // when the plan applied and it returns at once; the whole virtual grid when it did not)
+    auto k = k_adjoint<MODE, MONO, CORR>;
+    AdjArgs b = a;
+    b.smem_ant_off = adj_smem_ant_off(a.n_f);
+    b.vgx = grid.x;
+    b.vgy = grid.y;
+    const size_t smem = adj_smem_bytes(a.n_f);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kAdjThreads, smem) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    const unsigned g = (unsigned)std::min<int64_t>((int64_t)grid.x * grid.y, (int64_t)sms * occ);
+    k<<<g, kAdjThreads, smem, st>>>(b);
+    return counted(cudaGetLastError());
+  }
   if (MODE == kModeBwd && spec) {
     auto k = a.n_f == 256 ? k_adjoint_s2<MODE, MONO, CORR, 256>
            : a.n_f == 512 ? k_adjoint_s2<MODE, MONO, CORR, 512>
@@ -853,7 +892,7 @@ static bool use_tensor_cores() {
 cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int n_splits,
                            cudaStream_t st) {
   const size_t bneed = (size_t)a.n_a * tc_bprep_bytes_per_ant(a.n_f, mode == kModeBoth ? 2 : 1);
-  if (use_tensor_cores() && adjoint_tc_supported(a.n_f) && a.bprep && bneed <= a.bprep_cap &&
+  if (!a.gated && use_tensor_cores() && adjoint_tc_supported(a.n_f) && a.bprep && bneed <= a.bprep_cap &&
       (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
       (mode != kModeBoth || (reinterpret_cast<uintptr_t>(a.X2) & 15) == 0))
     return counted(launch_adjoint_tc(a, mode, mono, corr, n_splits, st));

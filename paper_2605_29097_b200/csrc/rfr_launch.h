@@ -99,6 +99,8 @@ struct AdjArgs {
   size_t smem_ant_off;
   unsigned int *flags;
   bool no_gain;
+  bool gated;                      // r2 fallback: generic SIMT kernel on a persistent grid
+  unsigned vgx, vgy;               // (set by launch_adjoint) virtual grid of the persistent launch
 };
 
 struct BlendBwdArgs {

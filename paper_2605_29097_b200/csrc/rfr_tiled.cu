@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(256) k2_tsetup(T2Args a, const int *tstart) {
     const double cyc = 2.0 * da * a.kc;
     float4 *g = a.tgeo + w * 2;
     g[0] = make_float4((float)(-2.0 * px), (float)(-2.0 * py), (float)(-2.0 * pz), (float)D);
-    g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), 0.f);
+    g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), (float)(1.0 / D));
   }
   __shared__ double red[256];
   red[threadIdx.x] = hm;
@@ -714,7 +714,8 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
   k2_geofix<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
   k2_tables<<<1 + (a.n_f + 127) / 128, 128, 0, st>>>(a);
   if ((e = cudaGetLastError()) == cudaSuccess) add_launches(7);
-  return e;
+  else return e;
+  return t2_tc_images(a, st);                        // fp16 images of the a table (tcgen05 GEMMs)
 }
 
 // ============================================================================ adjoint prep
@@ -887,7 +888,13 @@ cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0
     cudaError_t e = cudaFuncSetAttribute(k2_gexp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k2_gexp<<<(unsigned)a.n_a, kGexpThreads, sm, st>>>(a, X0, X1);
+  if (t2_tc_enabled()) {
+    cudaError_t e = t2_gexp_tc(a, X0, X1, st);     // tcgen05 (rfr_tc_gemm.cu)
+    if (e != cudaSuccess) return e;
+    add_launches(-1);
+  } else {
+    k2_gexp<<<(unsigned)a.n_a, kGexpThreads, sm, st>>>(a, X0, X1);
+  }
   k2_cprep<<<dim3((unsigned)a.n_a, (unsigned)(kT2Max / 128)), 128, 0, st>>>(a, tstart, X0, X1);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(2);
@@ -949,6 +956,40 @@ __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x 
   o.s = pk(s0, s1);
   o.x = ffma2(dl, bcv(inv2f), bcv(g1.z));
   o.r = r;
+  return o;
+}
+
+// One-MUFU form of the same geometry (the filter's default, RFR_T2GEO=2 selects t2_geo2): with
+// e = delta / d_a^2 (g1.w = 1 / d_a^2) the path ratio is d / d_a = sqrt(1 + e).  y = rsqrt(1 + e)
+// (MUFU), w = (1 + e) y, and one Newton step against the unrounded residual
+// rho = (1 + e) - w^2 gives sqrt(1 + e) = w + rho y / 2 to ~fp32 rounding; returned as
+// dln = (2 - 2w) - rho y = -2 (d - d_a) / d_a (2 - 2w is exact).  Replaces the rsqrt + rcp pair
+// (2 MUFU per point) by 1 MUFU and 4 more FMA-pipe operations per point pair: the filter's XU
+// load was ~0.9 of its FMA load.  Error: the residual's rounding, ~2^-26 d_a (~3e-9 m at c3,
+// below the rcp form's) -- 1e-5 rad of carrier phase.  kang = -pi 2 kc d_a (times the sign),
+// kx = -inv_t d_a: the angle and x are affine in dln.
+template <bool NEG>
+__device__ __forceinline__ Geo2 t2_geo1(const float4 &g0, const float4 &g1, f2x qx, f2x qy, f2x qz,
+                                        f2x qw, float kang, float kx) {
+  const f2x del = ffma2(bcv(g0.x), qx, ffma2(bcv(g0.y), qy, ffma2(bcv(g0.z), qz, qw)));
+  const f2x s = ffma2(del, bcv(g1.w), bcv(1.f));           // 1 + e (rsqrt input only)
+  const f2x en = fmul2(del, bcv(-g1.w));                    // -e
+  const float2 sv = upk(s);
+  const f2x y = pk(rsq_ftz(sv.x), rsq_ftz(sv.y));
+  const f2x w = fmul2(s, y);
+  const f2x rn = fadd2(ffma2(w, w, bcv(-1.f)), en);         // w^2 - (1 + e) = -rho
+  const f2x dln = ffma2(rn, y, ffma2(w, bcv(-2.f), bcv(2.f)));
+  const float sg = NEG ? -kTwoPi : kTwoPi;
+  const f2x ang = ffma2(dln, bcv(kang), bcv(g1.y * sg));
+  const float2 av = upk(ang);
+  Geo2 o;
+  float s0, c0, s1, c1;
+  sc_ftz(av.x, s0, c0);
+  sc_ftz(av.y, s1, c1);
+  o.c = pk(c0, c1);
+  o.s = pk(s0, s1);
+  o.x = ffma2(dln, bcv(kx), bcv(g1.z));
+  o.r = y;                                          // d_a / d (not 1 / d)
   return o;
 }
 
@@ -1017,7 +1058,8 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 
 // ------------------------------------------------------------------------- filter sweep
 // work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
-template <int P, bool RED, int NPAIR>
+// GM: geometry of the filter: 0 = t2_geo2 unreduced angle, 1 = t2_geo2 reduced, 2 = t2_geo1
+template <int P, int GM, int NPAIR>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
                                                int n_splits, int64_t aps, AdjStage &sm) {
@@ -1025,6 +1067,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   const int total = *s.n_items * n_splits;
   unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
+  const float kangf = (float)(-2.0 * kPi * a.kc), kxf = (float)(-pl.inv_t);   // t2_geo1
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
     const int t = t2_item_tile(s.cstart, pl.T, item);
@@ -1070,9 +1113,16 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
         // measured slower, r2p: 24.8 -> 25.1 ms)
         const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
         Geo2 cur[NPAIR];
+        if (GM == 2) {
+          const float kang = g1.x * kangf, kx = g1.x * kxf;
 #pragma unroll
-        for (int pp = 0; pp < NPAIR; ++pp)
-          cur[pp] = t2_geo2<false, RED>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
+          for (int pp = 0; pp < NPAIR; ++pp)
+            cur[pp] = t2_geo1<false>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kang, kx);
+        } else {
+#pragma unroll
+          for (int pp = 0; pp < NPAIR; ++pp)
+            cur[pp] = t2_geo2<false, GM == 1>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
+        }
 #pragma unroll
         for (int pp = 0; pp < NPAIR; ++pp) {
           const Geo2 &e = cur[pp];
@@ -1099,7 +1149,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   }
 }
 
-template <int MINB, bool RED, int NPAIR>
+template <int MINB, int GM, int NPAIR>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
@@ -1107,11 +1157,11 @@ __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int
   __shared__ __align__(16) AdjStage sm;
   t2_stage_init(sm);
   switch (pl.P) {
-    case 8: k2_filter_body<8, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 16: k2_filter_body<16, RED, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 16: k2_filter_body<16, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1425,20 +1475,20 @@ __global__ void __launch_bounds__(kT2FwdAnts, MINB) k2_fwd(T2Args a, T2Sorted s,
 constexpr int kT2OutThreads = 256;
 constexpr int kT2OutQ = 32;
 
-template <int P>
+template <int P, int QN>
 __device__ __forceinline__ void t2_fout_tiles(int T, const float2 *Ms, const double *Lt,
                                               const float (*lam)[kT2PMax], const float *xk,
-                                              double kd, double dt, double ug, double dg, int q0,
-                                              f2x (&acc)[kT2OutQ]) {
+                                              double kd, double dt, double ug, double inv_dg,
+                                              int q0, f2x (&acc)[kT2OutQ]) {
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     float2 M[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) M[p] = Ms[t * P + p];
-    const double uc = Lt[t] * kd;
+    const double yc = (Lt[t] * kd - ug) * inv_dg, yd = dt * inv_dg;
 #pragma unroll 1
     for (int k = 0; k < P; k += 2) {                // two nodes per pass: independent recurrences
       f2x wp[2];
-      float y[2], y2[2], t0[2], t1[2];
+      float y2[2], t0[2], t1[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float wr = 0.f, wi = 0.f;
@@ -1448,10 +1498,10 @@ __device__ __forceinline__ void t2_fout_tiles(int T, const float2 *Ms, const dou
           wi = fmaf(lam[k + h][p], M[p].y, wi);
         }
         wp[h] = pk(wr, wi);
-        y[h] = (float)((uc + dt * (double)xk[k + h] - ug) / dg);
-        y2[h] = 2.f * y[h];
+        const float y = (float)fma(yd, (double)xk[k + h], yc);
+        y2[h] = 2.f * y;
         t0[h] = 1.f;
-        t1[h] = y[h];
+        t1[h] = y;
       }
       for (int q = 0; q < q0; ++q) {                 // advance to T_q0 (second pass only)
 #pragma unroll
@@ -1462,7 +1512,7 @@ __device__ __forceinline__ void t2_fout_tiles(int T, const float2 *Ms, const dou
         }
       }
 #pragma unroll
-      for (int q = 0; q < kT2OutQ; ++q) {
+      for (int q = 0; q < QN; ++q) {
         acc[q] = ffma2(bcv(t0[1]), wp[1], ffma2(bcv(t0[0]), wp[0], acc[q]));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -1475,8 +1525,35 @@ __device__ __forceinline__ void t2_fout_tiles(int T, const float2 *Ms, const dou
   }
 }
 
+// sum of acc[0..32) over the warp's lanes, transposed: lane L returns the sum of acc[L] (a
+// butterfly that halves the values at every step: 31 shuffles per component instead of 160)
+__device__ __forceinline__ float2 t2_warp_sum_transpose(f2x (&acc)[kT2OutQ], int lane) {
+  float vx[kT2OutQ], vy[kT2OutQ];
+#pragma unroll
+  for (int q = 0; q < kT2OutQ; ++q) {
+    const float2 v = upk(acc[q]);
+    vx[q] = v.x;
+    vy[q] = v.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {               // n = 2 o values left; keep o of them
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const float sx = up ? vx[k] : vx[k + o], sy = up ? vy[k] : vy[k + o];
+      const float kx = up ? vx[k + o] : vx[k], ky = up ? vy[k + o] : vy[k];
+      vx[k] = kx + __shfl_xor_sync(0xffffffffu, sx, o);
+      vy[k] = ky + __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+  }
+  return make_float2(vx[0], vy[0]);
+}
+
+// mg != NULL (the tensor-core bins, t2_bins_tc): the global moments M_g go to mg[i][q] instead
+// of the bins (when a global expansion applies)
 __global__ void __launch_bounds__(kT2OutThreads, 2) k2_fout(T2Args a, const int *tstart,
-                                                         float2 *__restrict__ out) {
+                                                         float2 *__restrict__ out,
+                                                         float2 *__restrict__ mg) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
   extern __shared__ unsigned char smraw[];
@@ -1519,30 +1596,32 @@ __global__ void __launch_bounds__(kT2OutThreads, 2) k2_fout(T2Args a, const int 
   };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (Pg) {
+    const double inv_dg = 1.0 / pl.delta_g;
     for (int q0 = 0; q0 < Pg; q0 += kT2OutQ) {
       f2x acc[kT2OutQ];
 #pragma unroll
       for (int q = 0; q < kT2OutQ; ++q) acc[q] = 0ull;
-      // thread = whole tiles (P compile-time: no index division); per tile its P node weights from
-      // the P moments, then every source through the Chebyshev recurrence in y
+      // thread = whole tiles (P and the pass's moment count compile-time); per tile its P node
+      // weights from the P moments, then every source through the Chebyshev recurrence in y
+      const int qn = min(kT2OutQ, (Pg - q0 + 7) & ~7);
+#define RFR_FOUT_P(PP)                                                                          \
+  switch (qn) {                                                                                 \
+    case 8: t2_fout_tiles<PP, 8>(T, Ms, Lt, lam, xk, a.kd, dt, ug, inv_dg, q0, acc); break;     \
+    case 16: t2_fout_tiles<PP, 16>(T, Ms, Lt, lam, xk, a.kd, dt, ug, inv_dg, q0, acc); break;   \
+    case 24: t2_fout_tiles<PP, 24>(T, Ms, Lt, lam, xk, a.kd, dt, ug, inv_dg, q0, acc); break;   \
+    default: t2_fout_tiles<PP, 32>(T, Ms, Lt, lam, xk, a.kd, dt, ug, inv_dg, q0, acc); break;   \
+  }
       switch (P) {
-        case 8: t2_fout_tiles<8>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
-        case 10: t2_fout_tiles<10>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
-        case 12: t2_fout_tiles<12>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
-        case 14: t2_fout_tiles<14>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
-        default: t2_fout_tiles<16>(T, Ms, Lt, lam, xk, a.kd, dt, ug, pl.delta_g, q0, acc); break;
+        case 8: RFR_FOUT_P(8) break;
+        case 10: RFR_FOUT_P(10) break;
+        case 12: RFR_FOUT_P(12) break;
+        case 14: RFR_FOUT_P(14) break;
+        default: RFR_FOUT_P(16) break;
       }
-      // warp reduction (fixed xor pattern), then the warps in order
-#pragma unroll
-      for (int q = 0; q < kT2OutQ; ++q) {
-        float2 v = upk(acc[q]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-          v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-        }
-        if (lane == 0) red[warp][q] = v;
-      }
+#undef RFR_FOUT_P
+      // transposed warp reduction (lane q holds moment q0 + q), then the warps in order
+      const float2 wsum = t2_warp_sum_transpose(acc, lane);
+      red[warp][lane] = wsum;
       __syncthreads();
       if (threadIdx.x < kT2OutQ && q0 + (int)threadIdx.x < Pg) {
         float2 v = red[0][threadIdx.x];
@@ -1553,6 +1632,10 @@ __global__ void __launch_bounds__(kT2OutThreads, 2) k2_fout(T2Args a, const int 
         Mg[q0 + threadIdx.x] = v;
       }
       __syncthreads();
+    }
+    if (mg) {
+      if (threadIdx.x < Pg) mg[i * kT2PgMax + threadIdx.x] = Mg[threadIdx.x];
+      return;
     }
     for (int m = threadIdx.x; m < a.n_f; m += blockDim.x) {
       const float2 *cf = a.acoef + m;                // [q][m] layout: stride n_f over q
@@ -1634,15 +1717,24 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
   ProfScope prof(kProfFilter, st);
   // default: no reduction before the MUFU (r2l: filter 26.3 -> 24.8 ms at c3, rel-L2(M) 3.1e-6 ->
   // 4.5e-6 on 2048 sampled queries); RFR_T2RED=1 reduces the cycle count first
-  static int red = -1;
-  if (red < 0) { const char *e = getenv("RFR_T2RED"); red = (e && e[0] == '1') ? 1 : 0; }
+  // geometry (RFR_T2GEO): 2 = one MUFU per point (t2_geo1, default); 0 = rsqrt + rcp with the
+  // unreduced angle; 1 = rsqrt + rcp, angle reduced first (RFR_T2RED=1 is the same)
+  static int gm = -1;
+  if (gm < 0) {
+    const char *e = getenv("RFR_T2GEO"), *r = getenv("RFR_T2RED");
+    gm = e ? atoi(e) : 2;
+    if (r && r[0] == '1') gm = 1;
+    if (gm < 0 || gm > 2) gm = 2;
+  }
   const unsigned g4 = (unsigned)(n_sms * 5), g8 = (unsigned)(n_sms * 3);
   if (srt.chunk == 8 * 128) {
-    if (red) k2_filter<3, true, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else k2_filter<3, false, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    if (gm == 2) k2_filter<3, 2, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else if (gm == 1) k2_filter<3, 1, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else k2_filter<3, 0, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else {
-    if (red) k2_filter<5, true, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else k2_filter<5, false, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    if (gm == 2) k2_filter<5, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else if (gm == 1) k2_filter<5, 1, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else k2_filter<5, 0, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(1);
@@ -1694,9 +1786,11 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k2_fout<<<(unsigned)a.n_a, kT2OutThreads, sm, st>>>(a, srt.tstart, out);
+  const bool tc = t2_tc_enabled();
+  k2_fout<<<(unsigned)a.n_a, kT2OutThreads, sm, st>>>(a, srt.tstart, out, tc ? a.mg : nullptr);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(2);
+  if (e == cudaSuccess && tc) e = t2_bins_tc(a, out, st);   // M_g -> bins on tcgen05
   return e;
 }
 

@@ -90,10 +90,28 @@ struct T2Args {
   float2 *gexp;                        // [2][n_a][kT2PgMax] global expansion of the adjoint rows
   float2 *coef;                        // [2][T][n_a][P] monomial coefficients (adjoint rows)
   float2 *mom;                         // [n_a][T][P] forward moments (antenna-major)
+  unsigned char *tcimg;                // tensor-core B images of the a table (t2_tc_images):
+                                       // [cdiv(n_f, 32)][kT2GexpImg] then [cdiv(n_f, 128)][kT2BinsImg]
+  float2 *mg;                          // [n_a][kT2PgMax] global forward moments (k2_fout -> bins)
   ChebHdr *skip;                       // sel = 1 when the plan applies: the direct fallback
                                        // kernels (K2, the adjoint) read it and return at once
   unsigned int *flags;
 };
+
+// tensor-core (tcgen05) form of the two dense complex contractions against the shared a table
+// (rfr_tc_gemm.cu): the global expansion of the adjoint rows G_i = Y_i conj(a) (k2_gexp) and the
+// bins of the forward s_i = e^{-j 2 pi m' u_g} a M_g,i (the end of k2_fout).  Byte sizes of one
+// K chunk (32 bins) of the expansion's image and of one N chunk (128 bins) of the bins' image
+// (fp16 hi | lo, at the largest Pg).
+constexpr size_t kT2GexpImg = (size_t)2 * 96 * 64 * 2;
+constexpr size_t kT2BinsImg = (size_t)2 * 256 * 96 * 2;
+inline size_t t2_tcimg_bytes(int n_f) {
+  return (size_t)((n_f + 31) / 32) * kT2GexpImg + (size_t)((n_f + 127) / 128) * kT2BinsImg;
+}
+bool t2_tc_enabled();                  // RFR_T2TC=0: the SIMT contractions (A/B)
+cudaError_t t2_tc_images(const T2Args &a, cudaStream_t st);
+cudaError_t t2_gexp_tc(const T2Args &a, const float2 *X0, const float2 *X1, cudaStream_t st);
+cudaError_t t2_bins_tc(const T2Args &a, float2 *out, cudaStream_t st);
 
 // per-sweep device-time profiling (rfr_profile_enable / rfr_profile_read; ids = RFR_SWEEP_*)
 constexpr int kProfPlan = 0, kProfSort = 1, kProfPrep = 2, kProfFilter = 3, kProfBackward = 4,
