@@ -119,3 +119,20 @@ def test_workspace_planned_dims_bound_every_call():
                               None) == 2
         assert lib.rfr_filter_backward(p, sig, p, C.c_float(0.0), C.byref(a), C.byref(g), p, p, p,
                                        ns, sig, C.byref(w), None) == 2
+
+
+def test_tensor_core_kernels_issue_tcgen05_mma():
+    """The r2 engine's dense contractions (k2_gexp_tc, k2_bins_tc; rfr_tc_gemm.cu) are compiled to
+    5th-generation tensor-core MMAs (UTCHMMA, kind::f16 with A in tensor memory) for sm_100a."""
+    import shutil
+    import subprocess
+    rfr, _ = _lib()
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", rfr.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s+Function : ", sass)
+    for k in ("k2_gexp_tc", "k2_bins_tc"):
+        body = [f for f in funcs if k in f.split("\n")[0]]
+        assert body, k
+        assert "UTCHMMA" in body[0] and "UTCBAR" in body[0], k
