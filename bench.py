@@ -428,7 +428,9 @@ def run_gpu(args):
     n_pts = B[0]["n"]
     pairs = {"filter": sum(s["n"] * (s["hi"] - s["lo"]) for s in B) if has_flt else 0,
              "backward": act_bwd * n_pts * na_loc if has_bwd else 0,
-             "forward": act_fwd * n_pts * na_loc}
+             # the heatmap step's K5 (matched-filter adjoint) runs the forward sweep over every
+             # query (the samples) too, timed under the same sweep id
+             "forward": act_fwd * n_pts * na_loc + (n_pts * na_loc if heat else 0)}
     if gather:
         pairs["filter"] = sum((s["qhi"] - s["qlo"]) * prob.bundles[s["k"]].antennas.n for s in B)
     plans = {"filter": plan_flt, "backward": plan_bwd, "forward": plan_fwd}
@@ -487,6 +489,19 @@ def run_gpu(args):
             ("all-gather of the signal rows, query-sharded" if gather else "+NCCL all-reduce of M")
             + ")")
     n_active_contrib = (pairs["forward"] + pairs["backward"] + pairs["filter"]) * grid.n_freq
+    # per-pass rates in the metric's units -- N_c / t_fwd (the forward call: K1 +
+    # plan + sweep + bins), N_q N_a N_f / t_filter and N_c / t_bwd; inside the fused call the filter
+    # is its sweep time and the backward the rest of the call (plan, prep, sweep, K1')
+    sw_ms = {k: v[0] / args.steps for k, v in sweeps.items()}
+    n_q_tot = sum((s["qhi"] - s["qlo"]) for s in B) if gather else sum(s["n"] for s in B)
+    nqf = n_q_tot * (prob.bundles[0].antennas.n if gather else na_loc) * grid.n_freq
+    t_f, t_q, t_b = per_step(f_ms), per_step(q_ms), per_step(b_ms)
+    if fused:
+        t_q, t_b = sw_ms.get("filter", 0.0), per_step(b_ms) - sw_ms.get("filter", 0.0)
+    Nc_loc = Nc * share
+    per_pass = {"fwd": Nc_loc / (t_f * 1e-3) / 1e9 if t_f > 0 else None,
+                "filter": nqf / (t_q * 1e-3) / 1e9 if (has_flt and t_q > 0) else None,
+                "bwd": Nc_loc / (t_b * 1e-3) / 1e9 if (has_bwd and t_b > 0) else None}
     line = {"metric": METRIC, "value": value / 1e9, "unit": "G contributions/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -509,6 +524,7 @@ def run_gpu(args):
             "passes": {"fwd_ms": per_step(f_ms), "filter_ms": per_step(q_ms),
                        "loss_ms": per_step(l_ms), "bwd_or_fused_ms": per_step(b_ms)},
             "sweeps_ms_per_step": {k: v[0] / args.steps for k, v in sweeps.items()},
+            "per_pass_G_per_s": per_pass,
             "method": {"engine": "r2 tiled (DESIGN 5e)",
                        "plans": {k: v for k, v in (("forward", plan_fwd), ("filter", plan_flt),
                                                    ("backward", plan_bwd), ("k5", plan_k5)) if v},

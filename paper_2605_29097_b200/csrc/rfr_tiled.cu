@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(256) k2_tbox(const T2Plan *plp, T2Sorted s, fl
 
 // per (tile, antenna): centre path length L_c = dmin + dmax, half-spread dmax - dmin, and the
 // tile-relative geometry around the fp32 tile centre c_t: g0 = (-2a', |a'|^2), g1 = (d_a,
-// frac(2 d_a kc), 2 d_a - L_c, 0) with a' = a - c_t, d_a = |a'| (fp64, rounded once).  Thread =
+// frac(2 d_a kc), 2 d_a - L_c, 1 / d_a^2) with a' = a - c_t, d_a = |a'| (fp64, rounded once).  Thread =
 // (tile, antenna), antennas fastest; the per-antenna range of L_c and the global maxima by
 // order-independent atomics on the fp64 bits (positive values), so the results are deterministic.
 __global__ void __launch_bounds__(256) k2_tsetup(T2Args a, const int *tstart) {
@@ -572,7 +573,7 @@ __global__ void k2_select(T2Args a) {
 }
 
 // g1.z = (2 d_a - L_c) -> (2 d_a - L_c) inv_t: x at the antenna's tile distance (the sweeps read
-// the geometry as stored)
+// the geometry as stored; scaling it in the sweeps instead measured 2 % slower, r2v)
 __global__ void k2_geofix(T2Args a, const int *tstart) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
@@ -794,33 +795,45 @@ __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, 
   const int nrow = X1 ? 2 : 1;
   const double uc = a.lct[i * kT2Max + t] * a.kd;
   const double ug = a.lg[i * 3] * a.kd;
+  const double inv_dg = 1.0 / pl.delta_g;
+  const double yc = (uc - ug) * inv_dg, yd = pl.delta_t * inv_dg;   // y_k = yc + yd x_k
   for (int row = 0; row < nrow; ++row) {
     float Fr[P], Fi[P];
     if (Pg) {
-      // Clenshaw over q for all nodes at once, complex b packed: b_q = G_q + 2 y b_{q+1} - b_{q+2}
-      float y[P];
-      f2x b1[P], b2[P];
+      // F_k = sum_q G_q T_q(y_k) with T_q by the forward three-term recurrence, two nodes per
+      // packed register (one FFMA2 advances both) and the complex accumulation one FFMA2 per node:
+      // 3 FFMA2 per (q, node pair) against Clenshaw's 4
+      f2x y2[P / 2], t0[P / 2], t1[P / 2], acc[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) {
-        y[k] = (float)((uc + pl.delta_t * xk[k] - ug) / pl.delta_g);
-        b1[k] = 0ull;
-        b2[k] = 0ull;
+      for (int kk = 0; kk < P / 2; ++kk) {
+        const float ya = (float)fma(yd, xk[2 * kk], yc), yb = (float)fma(yd, xk[2 * kk + 1], yc);
+        y2[kk] = pk(2.f * ya, 2.f * yb);
+        t0[kk] = pk(1.f, 1.f);
+        t1[kk] = pk(ya, yb);
       }
-      for (int q = Pg - 1; q >= 1; --q) {
+      {
+        const float2 g0 = Gs[row][0];
+        const f2x g = pk(g0.x, g0.y);
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[k] = g;            // T_0 = 1
+      }
+      for (int q = 1; q < Pg; ++q) {
         const float2 gq = Gs[row][q];                // broadcast: one antenna per CTA
         const f2x g = pk(gq.x, gq.y);
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-          const f2x bn = ffma2(bcv(2.f * y[k]), b1[k], ffma2(b2[k], bcv(-1.f), g));
-          b2[k] = b1[k];
-          b1[k] = bn;
+        for (int kk = 0; kk < P / 2; ++kk) {
+          const float2 tv = upk(t1[kk]);
+          acc[2 * kk] = ffma2(bcv(tv.x), g, acc[2 * kk]);
+          acc[2 * kk + 1] = ffma2(bcv(tv.y), g, acc[2 * kk + 1]);
+          const float2 pv = upk(t0[kk]);
+          const f2x tn = ffma2(y2[kk], t1[kk], pk(-pv.x, -pv.y));
+          t0[kk] = t1[kk];
+          t1[kk] = tn;
         }
       }
-      const float2 gq0 = Gs[row][0];
-      const f2x g0 = pk(gq0.x, gq0.y);
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const float2 f = upk(ffma2(bcv(y[k]), b1[k], ffma2(b2[k], bcv(-1.f), g0)));
+        const float2 f = upk(acc[k]);
         Fr[k] = f.x;
         Fi[k] = f.y;
       }
@@ -1059,7 +1072,7 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 // ------------------------------------------------------------------------- filter sweep
 // work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
 // GM: geometry of the filter: 0 = t2_geo2 unreduced angle, 1 = t2_geo2 reduced, 2 = t2_geo1
-template <int P, int GM, int NPAIR>
+template <int P, int GM, int NPAIR, int UNR>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
                                                int n_splits, int64_t aps, AdjStage &sm) {
@@ -1107,7 +1120,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
       __syncthreads();                             // every thread is done with buffer b ^ 1
       if (i0 + kT2GA < i_hi)
         t2_stage_issue<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
-#pragma unroll 1
+#pragma unroll UNR
       for (int aa = 0; aa < ga; ++aa) {
         // (issuing the next antenna's geometry ahead of this Horner -- software pipelining --
         // measured slower, r2p: 24.8 -> 25.1 ms)
@@ -1149,7 +1162,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   }
 }
 
-template <int MINB, int GM, int NPAIR>
+template <int MINB, int GM, int NPAIR, int UNR = 1>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
@@ -1157,11 +1170,11 @@ __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int
   __shared__ __align__(16) AdjStage sm;
   t2_stage_init(sm);
   switch (pl.P) {
-    case 8: k2_filter_body<8, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 16: k2_filter_body<16, GM, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 16: k2_filter_body<16, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1698,7 +1711,10 @@ int t2_backward_chunk() {
 
 int t2_filter_chunk() {
   static int c = 0;
-  if (!c) { const char *e = getenv("RFR_T2SPT"); c = (e && atoi(e) == 8) ? 8 * 128 : kT2FltChunk; }
+  if (!c) {
+    const char *e = getenv("RFR_T2SPT");
+    c = (e && atoi(e) == 8) ? 8 * 128 : (e && atoi(e) == 6) ? 6 * 128 : kT2FltChunk;
+  }
   return c;
 }
 
@@ -1726,15 +1742,30 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     if (r && r[0] == '1') gm = 1;
     if (gm < 0 || gm > 2) gm = 2;
   }
-  const unsigned g4 = (unsigned)(n_sms * 5), g8 = (unsigned)(n_sms * 3);
+  // launch-shape variants (A/B, RFR_T2FV): m4 = 4 CTAs per SM (128 registers), u2 = the antenna
+  // loop unrolled by 2 (two antennas' independent work in one scheduling window)
+  static int fv = -1;
+  if (fv < 0) {
+    const char *e = getenv("RFR_T2FV");
+    fv = !e ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3 : 0;
+  }
+  const unsigned g5 = (unsigned)(n_sms * 5), g4 = (unsigned)(n_sms * 4), g3 = (unsigned)(n_sms * 3);
   if (srt.chunk == 8 * 128) {
-    if (gm == 2) k2_filter<3, 2, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else if (gm == 1) k2_filter<3, 1, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else k2_filter<3, 0, 4><<<g8, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    if (gm == 2) k2_filter<3, 2, 4><<<g3, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else if (gm == 1) k2_filter<3, 1, 4><<<g3, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else k2_filter<3, 0, 4><<<g3, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (srt.chunk == 6 * 128) {
+    k2_filter<4, 2, 3><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 1) {
+    k2_filter<4, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 2) {
+    k2_filter<5, 2, 2, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 3) {
+    k2_filter<4, 2, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else {
-    if (gm == 2) k2_filter<5, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else if (gm == 1) k2_filter<5, 1, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
-    else k2_filter<5, 0, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    if (gm == 2) k2_filter<5, 2, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else if (gm == 1) k2_filter<5, 1, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    else k2_filter<5, 0, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(1);
