@@ -1747,7 +1747,8 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
   static int fv = -1;
   if (fv < 0) {
     const char *e = getenv("RFR_T2FV");
-    fv = !e ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3 : 0;
+    fv = !e ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3
+       : !strcmp(e, "m6") ? 4 : 0;
   }
   const unsigned g5 = (unsigned)(n_sms * 5), g4 = (unsigned)(n_sms * 4), g3 = (unsigned)(n_sms * 3);
   if (srt.chunk == 8 * 128) {
@@ -1760,6 +1761,8 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     k2_filter<4, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 2) {
     k2_filter<5, 2, 2, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 4) {
+    k2_filter<6, 2, 2><<<(unsigned)(n_sms * 6), 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 3) {
     k2_filter<4, 2, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else {
@@ -1779,8 +1782,18 @@ cudaError_t t2_backward(const T2Args &a, const T2Sorted &srt, int row, const int
   if (a.n_a <= 0 || n_c <= 0) return cudaSuccess;
   {
     ProfScope prof(kProfBackward, st);
+    // CTAs per SM of the 2-points-per-thread form (RFR_T2BV = 4 / 5 / 6; r2w at c3: 2.63 / 2.62 /
+    // 2.56 ms, dense 15.89 / 15.59 / 15.56)
+    static int bv = -1;
+    if (bv < 0) { const char *e = getenv("RFR_T2BV"); bv = e ? atoi(e) : 6; }   // r2w: 6 fastest
     if (srt.chunk == 4 * 128)
       k2_bwd<3, 2><<<(unsigned)(n_sms * 3), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
+                                                          ants_per_split, no_gain);
+    else if (bv == 5)
+      k2_bwd<5, 1><<<(unsigned)(n_sms * 5), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
+                                                          ants_per_split, no_gain);
+    else if (bv == 6)
+      k2_bwd<6, 1><<<(unsigned)(n_sms * 6), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
                                                           ants_per_split, no_gain);
     else
       k2_bwd<4, 1><<<(unsigned)(n_sms * 4), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
@@ -1801,11 +1814,16 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
   static int rp = -1;
   // two record pairs per iteration (r2q: forward 2.79 -> 2.67 ms at c3); RFR_T2FRP=1: one
   if (rp < 0) { const char *e = getenv("RFR_T2FRP"); rp = (e && atoi(e) == 1) ? 1 : 2; }
+  // CTAs per SM (RFR_T2FWM = 3 / 4; r2w at c3: 2.674 / 2.643 ms, dense 17.41 / 17.25)
+  static int fm = -1;
+  if (fm < 0) { const char *e = getenv("RFR_T2FWM"); fm = e ? atoi(e) : 4; }
   if (kind == kFwdTrace) {
-    if (rp == 2) k2_fwd<kFwdTrace, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    if (rp == 2 && fm == 4) k2_fwd<kFwdTrace, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else if (rp == 2) k2_fwd<kFwdTrace, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else k2_fwd<kFwdTrace, 1, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
   } else {
-    if (rp == 2) k2_fwd<kFwdMFAdj, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    if (rp == 2 && fm == 4) k2_fwd<kFwdMFAdj, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else if (rp == 2) k2_fwd<kFwdMFAdj, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else k2_fwd<kFwdMFAdj, 1, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
   }
   }
