@@ -1578,18 +1578,33 @@ __global__ void __launch_bounds__(kT2OutThreads, 2) k2_fout(T2Args a, const int 
   __shared__ float xk[kT2PMax];
   __shared__ float2 red[kT2OutThreads / 32][kT2OutQ];
   __shared__ float2 Mg[kT2PgMax];
+  __shared__ unsigned char full[kT2Max];
+  __shared__ __align__(8) unsigned long long mbar;
   const int64_t i = blockIdx.x;
+  // the antenna's moments [T][P] (one contiguous row) by one bulk copy on the TMA engine, while the
+  // threads stage the tables, the tiles' occupancy and centres (coalesced)
+  const float2 *Mi = a.mom + (int64_t)i * nv;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive_expect_tx(&mbar, (unsigned)(nv * 8));
+    bulk_g2s(Ms, Mi, (unsigned)(nv * 8), &mbar);
+  }
   for (int w = threadIdx.x; w < kT2PMax * kT2PMax; w += blockDim.x)
     lam[w / kT2PMax][w % kT2PMax] = (float)a.tabs[2 * kT2PMax * kT2PMax + w];
   if (threadIdx.x < kT2PMax) xk[threadIdx.x] = (float)a.tabs[threadIdx.x];
-  // coalesced staging of the antenna's moments and tile centres (empty tiles: zero moments)
-  const float2 *Mi = a.mom + (int64_t)i * nv;
-  for (int w = threadIdx.x; w < nv; w += blockDim.x) {
-    const int t = w / P;
-    Ms[w] = tstart[t + 1] > tstart[t] ? Mi[w] : make_float2(0.f, 0.f);
+  const double lg0 = a.lg[i * 3];
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const bool f = tstart[t + 1] > tstart[t];
+    full[t] = f;
+    Lt[t] = f ? a.lct[i * kT2Max + t] : lg0;
   }
+  __syncthreads();
+  mbar_wait(&mbar, 0u);
+  // empty tiles: k2_fwd never wrote their moments -- zero them (the row may hold stale values)
   for (int t = threadIdx.x; t < T; t += blockDim.x)
-    Lt[t] = tstart[t + 1] > tstart[t] ? a.lct[i * kT2Max + t] : a.lg[i * 3];
+    if (!full[t])
+      for (int p = 0; p < P; ++p) Ms[t * P + p] = make_float2(0.f, 0.f);
   __syncthreads();
   const double ug = a.lg[i * 3] * a.kd;
   const double dt = pl.delta_t;
