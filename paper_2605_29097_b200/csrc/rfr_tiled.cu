@@ -846,15 +846,25 @@ __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, 
       }
     }
     float2 *dst = a.coef + (((int64_t)row * T + t) * a.n_a + i) * P;
+    // c_j = sum_k W[j][k] F_k in fp64, four j at a time with k inner: 8 independent DFMA chains
+    // instead of 2 (the per-j chains were latency-bound), each still summed in k order
 #pragma unroll 1
-    for (int j = 0; j < P; ++j) {
-      double cr = 0.0, ci = 0.0;
+    for (int j0 = 0; j0 < P; j0 += 4) {
+      double cr[4], ci[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) { cr[jj] = 0.0; ci[jj] = 0.0; }
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        cr = fma(W[j][k], (double)Fr[k], cr);
-        ci = fma(W[j][k], (double)Fi[k], ci);
+        const double fr = (double)Fr[k], fi = (double)Fi[k];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          cr[jj] = fma(W[j0 + jj][k], fr, cr[jj]);
+          ci[jj] = fma(W[j0 + jj][k], fi, ci[jj]);
+        }
       }
-      dst[P - 1 - j] = make_float2((float)cr, (float)ci);
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)                // P = 10, 14: the last block is half used
+        if (j0 + jj < P) dst[P - 1 - (j0 + jj)] = make_float2((float)cr[jj], (float)ci[jj]);
     }
   }
 }
