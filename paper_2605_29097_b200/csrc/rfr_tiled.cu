@@ -189,7 +189,8 @@ __device__ __forceinline__ int t2_tile_of(const T2Plan &pl, float3 q) {
 __device__ __forceinline__ float t2_centre(const float *tb, int c) { return 0.5f * (tb[c] + tb[3 + c]); }
 
 // ================================================================================= plan
-__global__ void __launch_bounds__(256) k2_box(T2Points p, float *part) {
+__global__ void __launch_bounds__(256) k2_box(T2Points p, float *part, unsigned long long *cand) {
+  if (blockIdx.x == 0 && threadIdx.x < 128) cand[threadIdx.x] = 0ull;   // k2_cand's maxima
   const int64_t n = t2_count(p);
   float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
@@ -222,11 +223,12 @@ __device__ __forceinline__ void t2_cand(int c, int L[3]) {
 }
 constexpr int kT2SubAnts = 32;
 
-// one CTA per candidate grid: max over its cells and a subsample of the antennas of the delay
-// half-spread (cell boxes bound the tight boxes from above), -> the candidate's P and cost
+// kT2CandSlices CTAs per candidate grid: max over its cells and a subsample of the antennas of the
+// delay half-spread (cell boxes bound the tight boxes from above), combined over the slices by an
+// order-independent atomicMax on the fp64 bits (non-negative); k2_pick turns it into P and a cost
+constexpr int kT2CandSlices = 4;
 __global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Args a,
-                                               int64_t n_pts_host, const int64_t *n_dev,
-                                               double *cost, int kind, int chunk) {
+                                               unsigned long long *hmax_bits) {
   __shared__ float box[6];
   __shared__ double red[256];
   if (threadIdx.x < 6) {
@@ -238,14 +240,14 @@ __global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Ar
     box[threadIdx.x] = v;
   }
   __syncthreads();
+  const int cidx = blockIdx.x % kT2Cand, slice = blockIdx.x / kT2Cand;
   int L[3];
-  t2_cand(blockIdx.x, L);
+  t2_cand(cidx, L);
   const int T = L[0] * L[1] * L[2];
-  const int64_t n = n_dev ? *n_dev : n_pts_host;
   double hmax = 0.0;
   if (T <= kT2Max && box[0] <= box[3]) {
     const int ns = (int)(a.n_a < kT2SubAnts ? a.n_a : kT2SubAnts);
-    for (int w = threadIdx.x; w < T * ns; w += blockDim.x) {
+    for (int w = slice * blockDim.x + threadIdx.x; w < T * ns; w += kT2CandSlices * blockDim.x) {
       const int t = w / ns, k = w % ns;
       const int64_t i = ns > 1 ? (int64_t)k * (a.n_a - 1) / (ns - 1) : 0;
       const int cx = t % L[0], cy = (t / L[0]) % L[1], cz = t / (L[0] * L[1]);
@@ -267,30 +269,53 @@ __global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Ar
     if ((int)threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    double c = 1e300;
-    if (T <= kT2Max && box[0] <= box[3]) {
-      const double z = 2.0 * kPi * (double)(a.n_f / 2 + 1) * red[0] * a.kd * (1.0 + 1e-6);
-      const int P = t2_select_P(z);
-      // FMA-pipe cost per (point, antenna): P Horner steps + ~10 for the geometry; partially
-      // filled work items waste ~half a chunk per tile; T P <= kT2TP (coefficient storage)
-      // FMA-pipe cost per antenna (FFMA2 units).  Adjoint sweeps (kind 0): per point P Horner
-      // steps + ~10 for the geometry, partially filled work items waste ~half a chunk per tile,
-      // plus the per-(tile, antenna) preparation; forward (kind 1): per record 1.5 P moment steps
-      // + ~12, plus per tile P virtual sources through ~32 global moments (k2_fout)
-      if (P > 0 && T * P <= kT2TP)
-        c = kind == 0 ? (double)(P + 10) * ((double)n + (double)T * chunk * 0.5) + (double)T * P * 64.0
-                      : (1.5 * P + 12.0) * (double)n + (double)T * P * 48.0;
-    }
-    cost[blockIdx.x] = c;
-  }
+  if (threadIdx.x == 0) atomicMax(hmax_bits + cidx, (unsigned long long)__double_as_longlong(red[0]));
+}
+
+// cost of a candidate grid from its delay half-spread: FMA-pipe cost per antenna (FFMA2 units).
+// Adjoint sweeps (kind 0): per point P Horner steps + ~10 for the geometry, partially filled work
+// items waste ~half a chunk per tile, plus the per-(tile, antenna) preparation; forward (kind 1):
+// per record 1.5 P moment steps + ~12, plus per tile P virtual sources through ~32 global moments
+// (k2_fout).  T P <= kT2TP (coefficient storage)
+__device__ double t2_cand_cost(int T, double hmax, const T2Args &a, int64_t n, int kind,
+                               int chunk) {
+  const double z = 2.0 * kPi * (double)(a.n_f / 2 + 1) * hmax * a.kd * (1.0 + 1e-6);
+  const int P = t2_select_P(z);
+  if (P > 0 && T * P <= kT2TP)
+    return kind == 0 ? (double)(P + 10) * ((double)n + (double)T * chunk * 0.5) + (double)T * P * 64.0
+                     : (1.5 * P + 12.0) * (double)n + (double)T * P * 48.0;
+  return 1e300;
 }
 
 // pick the cheapest candidate (ties: fewer tiles), write the box and the grid; reset scratch
-__global__ void __launch_bounds__(128) k2_pick(const float *part, int nblk, const double *cost,
+__global__ void __launch_bounds__(128) k2_pick(const float *part, int nblk,
+                                               const unsigned long long *hmax_bits, T2Args a,
                                                T2Plan *pl, int64_t n_pts_host,
-                                               const int64_t *n_dev) {
+                                               const int64_t *n_dev, int kind, int chunk) {
   __shared__ int best;
+  __shared__ double cost[kT2Cand];
+  __shared__ float bx[6];
+  if (threadIdx.x < 6) {
+    float v = threadIdx.x < 3 ? 3e38f : -3e38f;
+    for (int b = 0; b < nblk; ++b) {
+      const float u = part[b * 6 + threadIdx.x];
+      v = threadIdx.x < 3 ? fminf(v, u) : fmaxf(v, u);
+    }
+    bx[threadIdx.x] = v;
+  }
+  __syncthreads();
+  {
+    const int64_t n = n_dev ? *n_dev : n_pts_host;
+    for (int c = threadIdx.x; c < kT2Cand; c += blockDim.x) {
+      int L[3];
+      t2_cand(c, L);
+      const int T = L[0] * L[1] * L[2];
+      cost[c] = (T <= kT2Max && bx[0] <= bx[3])
+                    ? t2_cand_cost(T, __longlong_as_double((long long)hmax_bits[c]), a, n, kind, chunk)
+                    : 1e300;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     int b = -1;
     double bc = 1e300;
@@ -376,8 +401,21 @@ __global__ void __launch_bounds__(kT2Max) k2_scan(const T2Plan *plp, const int64
   const int nb = (int)((n + kT2SortBlock - 1) / kT2SortBlock);
   const int q = threadIdx.x;
   if (q < T) {
+    // 16 blocks' counts loaded before their offsets are stored: 16 loads in flight instead of a
+    // load -> store chain per block (one CTA scans every block of the sort)
     int run = 0;
-    for (int b = 0; b < nb; ++b) {
+    int b = 0;
+    for (; b + 16 <= nb; b += 16) {
+      int c[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) c[u] = s.bcnt[(int64_t)(b + u) * kT2Max + q];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        s.bcnt[(int64_t)(b + u) * kT2Max + q] = run;
+        run += c[u];
+      }
+    }
+    for (; b < nb; ++b) {
       const int c = s.bcnt[(int64_t)b * kT2Max + q];
       s.bcnt[(int64_t)b * kT2Max + q] = run;
       run += c;
@@ -470,32 +508,60 @@ __global__ void __launch_bounds__(256) k2_tbox(const T2Plan *plp, T2Sorted s, fl
 __global__ void __launch_bounds__(256) k2_tsetup(T2Args a, const int *tstart) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
-  const int64_t n = (int64_t)pl.T * a.n_a;
+  // task = (8 tiles, 32 antennas): warp = tile, lane = antenna (coalesced tile-major writes); the
+  // antenna-major copy of L_c through shared memory (64-byte runs), the per-antenna L_c range over
+  // the task's tiles reduced in shared memory before the atomics (one pair per antenna and task)
+  __shared__ double Ls[8][33];
+  const int tt = threadIdx.x >> 5, ii = threadIdx.x & 31;
+  const int ntg = (pl.T + 7) / 8;
+  const int64_t nag = (a.n_a + 31) / 32, ntask = (int64_t)ntg * nag;
   double hm = 0.0, umin = 1e300;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < n;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(w / a.n_a);
-    const int64_t i = w % a.n_a;
-    if (tstart[t + 1] == tstart[t]) continue;        // empty tile: never read
-    const double ax = a.tx_x[i], ay = a.tx_y[i], az = a.tx_z[i];
-    const float *b = a.tbox + t * 6;
-    double dmin, dmax;
-    t2_box_dist(b, ax, ay, az, dmin, dmax);
-    umin = fmin(umin, dmin);
-    const double Lc = dmin + dmax;
-    a.lc[w] = Lc;
-    a.lct[i * kT2Max + t] = Lc;
-    hm = fmax(hm, dmax - dmin);
-    unsigned long long *mm = reinterpret_cast<unsigned long long *>(a.lg + i * 3);
-    atomicMin(mm + 1, (unsigned long long)__double_as_longlong(Lc));
-    atomicMax(mm + 2, (unsigned long long)__double_as_longlong(Lc));
-    const double px = ax - (double)t2_centre(b, 0), py = ay - (double)t2_centre(b, 1),
-                 pz = az - (double)t2_centre(b, 2);
-    const double D = px * px + py * py + pz * pz, da = sqrt(D);
-    const double cyc = 2.0 * da * a.kc;
-    float4 *g = a.tgeo + w * 2;
-    g[0] = make_float4((float)(-2.0 * px), (float)(-2.0 * py), (float)(-2.0 * pz), (float)D);
-    g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), (float)(1.0 / D));
+  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+    const int tg = (int)(task / nag);
+    const int64_t ag = task % nag;
+    const int t = tg * 8 + tt;
+    const int64_t i = ag * 32 + ii;
+    double Lc = -1.0;                                // marker: empty tile / no antenna
+    if (t < pl.T && i < a.n_a && tstart[t + 1] > tstart[t]) {
+      const double ax = a.tx_x[i], ay = a.tx_y[i], az = a.tx_z[i];
+      const float *b = a.tbox + t * 6;
+      double dmin, dmax;
+      t2_box_dist(b, ax, ay, az, dmin, dmax);
+      umin = fmin(umin, dmin);
+      Lc = dmin + dmax;
+      const int64_t w = (int64_t)t * a.n_a + i;
+      a.lc[w] = Lc;
+      hm = fmax(hm, dmax - dmin);
+      const double px = ax - (double)t2_centre(b, 0), py = ay - (double)t2_centre(b, 1),
+                   pz = az - (double)t2_centre(b, 2);
+      const double D = px * px + py * py + pz * pz, da = sqrt(D);
+      const double cyc = 2.0 * da * a.kc;
+      float4 *g = a.tgeo + w * 2;
+      g[0] = make_float4((float)(-2.0 * px), (float)(-2.0 * py), (float)(-2.0 * pz), (float)D);
+      g[1] = make_float4((float)da, (float)(cyc - rint(cyc)), (float)(2.0 * da - Lc), (float)(1.0 / D));
+    }
+    Ls[tt][ii] = Lc;
+    __syncthreads();
+    {
+      const int ka = threadIdx.x >> 3, kt = threadIdx.x & 7;
+      const int64_t ia = ag * 32 + ka;
+      const double v = Ls[kt][ka];
+      if (v >= 0.0) a.lct[ia * kT2Max + tg * 8 + kt] = v;
+    }
+    if (threadIdx.x < 32) {
+      double mn = 1e300, mx = -1.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double v = Ls[k][threadIdx.x];
+        if (v >= 0.0) { mn = fmin(mn, v); mx = fmax(mx, v); }
+      }
+      if (mx >= 0.0) {
+        unsigned long long *mm = reinterpret_cast<unsigned long long *>(a.lg + (ag * 32 + threadIdx.x) * 3);
+        atomicMin(mm + 1, (unsigned long long)__double_as_longlong(mn));
+        atomicMax(mm + 2, (unsigned long long)__double_as_longlong(mx));
+      }
+    }
+    __syncthreads();
   }
   __shared__ double red[256];
   red[threadIdx.x] = hm;
@@ -696,11 +762,12 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
   cudaError_t e;
   {
   ProfScope prof(kProfPlan, st);
-  k2_box<<<kT2BoxBlocks, 256, 0, st>>>(pts, a.box_part);
-  double *cost = reinterpret_cast<double *>(a.tabs + 3 * kT2PMax * kT2PMax);   // [kT2Cand]
-  k2_cand<<<kT2Cand, 256, 0, st>>>(a.box_part, kT2BoxBlocks, a, pts.n, pts.n_dev, cost, kind,
-                                   srt.chunk);
-  k2_pick<<<1, 128, 0, st>>>(a.box_part, kT2BoxBlocks, cost, a.plan, pts.n, pts.n_dev);
+  // per-candidate maxima (fp64 bits) in the tables' scratch tail (128 slots)
+  unsigned long long *hb = reinterpret_cast<unsigned long long *>(a.tabs + 3 * kT2PMax * kT2PMax);
+  k2_box<<<kT2BoxBlocks, 256, 0, st>>>(pts, a.box_part, hb);
+  k2_cand<<<kT2Cand * kT2CandSlices, 256, 0, st>>>(a.box_part, kT2BoxBlocks, a, hb);
+  k2_pick<<<1, 128, 0, st>>>(a.box_part, kT2BoxBlocks, hb, a, a.plan, pts.n, pts.n_dev, kind,
+                             srt.chunk);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   add_launches(3);
@@ -709,7 +776,7 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
   ProfScope prof(kProfPlan, st);
   k2_tbox<<<kT2Max, 256, 0, st>>>(a.plan, srt, a.tbox);
   k2_lg_reset<<<(unsigned)std::min<int64_t>((a.n_a + 255) / 256, 1024), 256, 0, st>>>(a);
-  k2_tsetup<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
+  k2_tsetup<<<(unsigned)std::min<int64_t>((int64_t)(kT2Max / 8) * ((a.n_a + 31) / 32), 148 * 16), 256, 0, st>>>(a, srt.tstart);
   k2_gsetup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
   k2_select<<<1, 1, 0, st>>>(a);
   k2_geofix<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
