@@ -422,18 +422,29 @@ __global__ void __launch_bounds__(kT2Max) k2_scan(const T2Plan *plp, const int64
     }
     tot[q] = run;
   }
+  // exclusive scans over the tiles of the point counts and the work-item counts (warp shuffles,
+  // then the warp totals)
+  __shared__ int wsum[2][kT2Max / 32];
+  const int cnt = q < T ? tot[q] : 0, items = (cnt + s.chunk - 1) / s.chunk;
+  const int lane = q & 31, warp = q >> 5;
+  int a0 = cnt, a1 = items;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int b0 = __shfl_up_sync(0xffffffffu, a0, o), b1 = __shfl_up_sync(0xffffffffu, a1, o);
+    if (lane >= o) { a0 += b0; a1 += b1; }
+  }
+  if (lane == 31) { wsum[0][warp] = a0; wsum[1][warp] = a1; }
   __syncthreads();
-  if (q == 0) {
-    int st = 0, cs = 0;
-    for (int k = 0; k < T; ++k) {
-      s.tstart[k] = st;
-      s.cstart[k] = cs;
-      st += tot[k];
-      cs += (tot[k] + s.chunk - 1) / s.chunk;
-    }
-    s.tstart[T] = st;
-    s.cstart[T] = cs;
-    *s.n_items = cs;
+  int o0 = 0, o1 = 0;
+  for (int w = 0; w < warp; ++w) { o0 += wsum[0][w]; o1 += wsum[1][w]; }
+  if (q < T) {
+    s.tstart[q] = o0 + a0 - cnt;
+    s.cstart[q] = o1 + a1 - items;
+  }
+  if (q == T - 1 || (T == 0 && q == 0)) {
+    s.tstart[T] = T ? o0 + a0 : 0;
+    s.cstart[T] = T ? o1 + a1 : 0;
+    *s.n_items = T ? o1 + a1 : 0;
   }
 }
 
@@ -1805,7 +1816,8 @@ int t2_filter_chunk() {
   static int c = 0;
   if (!c) {
     const char *e = getenv("RFR_T2SPT");
-    c = (e && atoi(e) == 8) ? 8 * 128 : (e && atoi(e) == 6) ? 6 * 128 : kT2FltChunk;
+    c = (e && atoi(e) == 8) ? 8 * 128 : (e && atoi(e) == 6) ? 6 * 128
+      : (e && atoi(e) == 2) ? 2 * 128 : kT2FltChunk;
   }
   return c;
 }
@@ -1849,6 +1861,8 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     else k2_filter<3, 0, 4><<<g3, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (srt.chunk == 6 * 128) {
     k2_filter<4, 2, 3><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (srt.chunk == 2 * 128) {
+    k2_filter<8, 2, 1><<<(unsigned)(n_sms * 8), 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 1) {
     k2_filter<4, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 2) {
