@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "rfr_device.cuh"
@@ -126,17 +127,21 @@ __device__ __forceinline__ float rni(float v) {
   return r;
 }
 
-// truncation tail sum_{p >= P} eps_p |J_p(z)| < 1e-7 (tests/test_cheb_math.py pins the rule)
+// per-tile expansions: truncation tail sum_{p >= P} eps_p |J_p(z)| < 1e-5 -- below the per-pair
+// phase error of the sweeps' unreduced fp32 carrier angle (~2e-5 rad at c3, t2_geo1), so the
+// truncation never dominates a pair's error (DESIGN 5e, Q28; tests/test_cheb_math.py pins the rule).
+// z stays <= 4.812 (the round-1 limit): the fp32 rounding of the monomial (Horner) evaluation is
+// bounded by eps e^z sum|X|.  The global expansion (t2_select_Pg) keeps the 1e-7 rule: its error
+// enters every tile.
 __host__ __device__ inline int t2_select_P(double z) {
-  if (z <= 0.917) return 8;
-  if (z <= 1.683) return 10;
-  if (z <= 2.611) return 12;
-  if (z <= 3.663) return 14;
-  if (z <= 4.813) return 16;
+  if (z <= 1.632) return 8;
+  if (z <= 2.681) return 10;
+  if (z <= 3.866) return 12;
+  if (z <= 4.812) return 14;
   return 0;
 }
 __device__ inline int t2_select_Pg(double z) {
-  if (z <= 4.813) return 16;
+  if (z <= 4.812) return 16;
   if (z <= 7.33) return 20;
   if (z <= 10.061) return 24;
   if (z <= 12.946) return 28;
@@ -274,7 +279,8 @@ __global__ void __launch_bounds__(256) k2_cand(const float *part, int nblk, T2Ar
 
 // cost of a candidate grid from its delay half-spread: FMA-pipe cost per antenna (FFMA2 units).
 // Adjoint sweeps (kind 0): per point P Horner steps + ~10 for the geometry, partially filled work
-// items waste ~half a chunk per tile, plus the per-(tile, antenna) preparation; forward (kind 1):
+// items waste ~half a warp segment (chunk / 8) of lanes per tile (t2_item), plus the per-(tile,
+// antenna) preparation; forward (kind 1):
 // per record 1.5 P moment steps + ~12, plus per tile P virtual sources through ~32 global moments
 // (k2_fout).  T P <= kT2TP (coefficient storage)
 __device__ double t2_cand_cost(int T, double hmax, const T2Args &a, int64_t n, int kind,
@@ -282,7 +288,7 @@ __device__ double t2_cand_cost(int T, double hmax, const T2Args &a, int64_t n, i
   const double z = 2.0 * kPi * (double)(a.n_f / 2 + 1) * hmax * a.kd * (1.0 + 1e-6);
   const int P = t2_select_P(z);
   if (P > 0 && T * P <= kT2TP)
-    return kind == 0 ? (double)(P + 10) * ((double)n + (double)T * chunk * 0.5) + (double)T * P * 64.0
+    return kind == 0 ? (double)(P + 10) * ((double)n + (double)T * chunk * 0.125) + (double)T * P * 64.0
                      : (1.5 * P + 12.0) * (double)n + (double)T * P * 48.0;
   return 1e300;
 }
@@ -425,7 +431,9 @@ __global__ void __launch_bounds__(kT2Max) k2_scan(const T2Plan *plp, const int64
   // exclusive scans over the tiles of the point counts and the work-item counts (warp shuffles,
   // then the warp totals)
   __shared__ int wsum[2][kT2Max / 32];
-  const int cnt = q < T ? tot[q] : 0, items = (cnt + s.chunk - 1) / s.chunk;
+  // work units of chunk / 2 points per tile (t2_item: an item = two units)
+  const int unit = s.chunk / 2;
+  const int cnt = q < T ? tot[q] : 0, items = (cnt + unit - 1) / unit;
   const int lane = q & 31, warp = q >> 5;
   int a0 = cnt, a1 = items;
 #pragma unroll
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(kT2Max) k2_scan(const T2Plan *plp, const int64
   if (q == T - 1 || (T == 0 && q == 0)) {
     s.tstart[T] = T ? o0 + a0 : 0;
     s.cstart[T] = T ? o1 + a1 : 0;
-    *s.n_items = T ? o1 + a1 : 0;
+    *s.n_items = T ? (o1 + a1 + 1) / 2 : 0;
   }
 }
 
@@ -974,7 +982,7 @@ __global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, con
     case 10: k2_cprep_one<10>(a, pl, t, i, X0, X1, W, xk, Gs); break;
     case 12: k2_cprep_one<12>(a, pl, t, i, X0, X1, W, xk, Gs); break;
     case 14: k2_cprep_one<14>(a, pl, t, i, X0, X1, W, xk, Gs); break;
-    default: k2_cprep_one<16>(a, pl, t, i, X0, X1, W, xk, Gs); break;
+    default: break;
   }
 }
 
@@ -1102,8 +1110,8 @@ constexpr int kT2GA = 32;                         // antennas per shared-memory 
 // with two bulk copies on the TMA engine (cp.async.bulk, completion on the buffer's mbarrier)
 // while the CTA computes the previous stage.
 struct AdjStage {
-  float2 cs[2][kT2GA * kT2PMax];                  // [buffer][antenna * P + k]
-  float4 gs[2][kT2GA][2];
+  float2 cs[2][2][kT2GA * kT2PMax];               // [buffer][slot][antenna * P + k]
+  float4 gs[2][2][kT2GA][2];                      // [buffer][slot][antenna][g0, g1]
   unsigned long long bar[2];
 };
 __device__ __forceinline__ void t2_stage_init(AdjStage &sm) {
@@ -1114,14 +1122,50 @@ __device__ __forceinline__ void t2_stage_init(AdjStage &sm) {
   }
   __syncthreads();
 }
+// work item = two UNITS of srt.chunk / 2 sorted points; a unit = two warps' segments of one tile
+// (32 SPT points each, lane-contiguous) and every tile is padded to whole units (k2_scan:
+// cstart = the first unit of each tile), so an item spans at most two tiles -- one stage slot per
+// tile -- and a tile wastes on average half a warp segment of lanes instead of half a chunk
+// (c3 backward: ~270 active samples per tile in chunks of 256).  A warp whose segment lies past
+// its tile's end skips the antenna loop.
+struct T2Item {
+  int t0, t1;                                     // tiles of the item's units (-1: past the end)
+  int tw, slot;                                   // this warp's tile (-1: idle) and stage slot
+  int64_t base, end;                              // this warp's first sorted position, tile end
+  bool two;                                       // the units' tiles differ (slot 1 staged)
+};
+__device__ __forceinline__ T2Item t2_item(const T2Sorted &s, int T, int item, int seg) {
+  const int nu = s.cstart[T];
+  T2Item it;
+  it.t0 = t2_item_tile(s.cstart, T, 2 * item);
+  it.t1 = 2 * item + 1 < nu ? t2_item_tile(s.cstart, T, 2 * item + 1) : -1;
+  it.two = it.t1 >= 0 && it.t1 != it.t0;
+  const int w = (int)(threadIdx.x >> 5), h = w >> 1;
+  it.tw = h ? it.t1 : it.t0;
+  it.slot = (h && it.two) ? 1 : 0;
+  it.base = 0;
+  it.end = 0;
+  if (it.tw >= 0) {
+    it.base = s.tstart[it.tw] + (int64_t)(2 * item + h - s.cstart[it.tw]) * (2 * seg) + (w & 1) * seg;
+    it.end = s.tstart[it.tw + 1];
+    if (it.base >= it.end) it.tw = -1;
+  }
+  return it;
+}
+
 template <int P>
-__device__ __forceinline__ void t2_stage_issue(const T2Args &a, const T2Plan &pl, int row, int t,
-                                               int64_t i0, int ga, AdjStage &sm, int b) {
+__device__ __forceinline__ void t2_stage_issue(const T2Args &a, const T2Plan &pl, int row,
+                                               const T2Item &it, int64_t i0, int ga, AdjStage &sm,
+                                               int b) {
   if (threadIdx.x != 0) return;
   const unsigned bc = (unsigned)(ga * P * 8), bg = (unsigned)(ga * 32);
-  mbar_arrive_expect_tx(&sm.bar[b], bc + bg);
-  bulk_g2s(&sm.cs[b][0], a.coef + (((int64_t)row * pl.T + t) * a.n_a + i0) * P, bc, &sm.bar[b]);
-  bulk_g2s(&sm.gs[b][0][0], a.tgeo + ((int64_t)t * a.n_a + i0) * 2, bg, &sm.bar[b]);
+  mbar_arrive_expect_tx(&sm.bar[b], (bc + bg) * (it.two ? 2u : 1u));
+  bulk_g2s(&sm.cs[b][0][0], a.coef + (((int64_t)row * pl.T + it.t0) * a.n_a + i0) * P, bc, &sm.bar[b]);
+  bulk_g2s(&sm.gs[b][0][0][0], a.tgeo + ((int64_t)it.t0 * a.n_a + i0) * 2, bg, &sm.bar[b]);
+  if (it.two) {
+    bulk_g2s(&sm.cs[b][1][0], a.coef + (((int64_t)row * pl.T + it.t1) * a.n_a + i0) * P, bc, &sm.bar[b]);
+    bulk_g2s(&sm.gs[b][1][0][0], a.tgeo + ((int64_t)it.t1 * a.n_a + i0) * 2, bg, &sm.bar[b]);
+  }
 }
 
 // the same, point-packed: hre = (Re h(x0), Re h(x1)), him = (Im h(x0), Im h(x1)) -- two FFMA2
@@ -1158,7 +1202,8 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 }
 
 // ------------------------------------------------------------------------- filter sweep
-// work item = (chunk of kT2FltChunk sorted points of one tile, antenna split); thread = 4 points
+// work item = (two units of kT2FltChunk / 2 tile-sorted points, antenna split, t2_item); thread =
+// 4 points of its warp's segment (lane + 32 u)
 // GM: geometry of the filter: 0 = t2_geo2 unreduced angle, 1 = t2_geo2 reduced, 2 = t2_geo1
 template <int P, int GM, int NPAIR, int UNR>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
@@ -1169,12 +1214,12 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   const float kangf = (float)(-2.0 * kPi * a.kc), kxf = (float)(-pl.inv_t);   // t2_geo1
+  const int lane = (int)(threadIdx.x & 31);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
-    const int t = t2_item_tile(s.cstart, pl.T, item);
-    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * (SPT * 128);
-    const int64_t end = s.tstart[t + 1];
-    const float *tb = a.tbox + t * 6;
+    const T2Item it = t2_item(s, pl.T, item, 32 * SPT);
+    const int64_t base = it.base + lane, end = it.end;
+    const float *tb = a.tbox + max(it.tw, 0) * 6;
     const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
     f2x qx[NPAIR], qy[NPAIR], qz[NPAIR], qw[NPAIR];
     bool valid[SPT];
@@ -1184,7 +1229,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int u = 2 * pp + h;
-        const int64_t k = base + threadIdx.x + u * 128;
+        const int64_t k = base + u * 32;
         valid[u] = k < end;
         const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
         v4[h][0] = v.x - cx; v4[h][1] = v.y - cy; v4[h][2] = v.z - cz;
@@ -1199,7 +1244,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
     for (int u = 0; u < SPT; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
-    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
@@ -1207,12 +1252,16 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
       ph ^= 1u << b;
       __syncthreads();                             // every thread is done with buffer b ^ 1
       if (i0 + kT2GA < i_hi)
-        t2_stage_issue<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+        t2_stage_issue<P>(a, pl, row, it, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+      // the stage slot as a compile-time index in each of two copies of the antenna loop: a
+      // per-warp shared-memory base would move the loop's addressing and control off the uniform
+      // datapath (r3b: +9 instructions per antenna, filter 22.7 -> 23.2 ms)
+      auto sweep = [&](const float2 *csb, const float4 (*gsb)[2]) {
 #pragma unroll UNR
       for (int aa = 0; aa < ga; ++aa) {
         // (issuing the next antenna's geometry ahead of this Horner -- software pipelining --
         // measured slower, r2p: 24.8 -> 25.1 ms)
-        const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
+        const float4 g0 = gsb[aa][0], g1 = gsb[aa][1];
         Geo2 cur[NPAIR];
         if (GM == 2) {
           const float kang = g1.x * kangf, kx = g1.x * kxf;
@@ -1231,7 +1280,7 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
           // point-packed form (t2_horner_pp) needs the coefficient as a broadcast addend, which
           // FFMA2 cannot take (MOVs: r2m, filter 24.8 -> 26.8 ms)
           f2x h0, h1;
-          t2_horner2<P>(&sm.cs[b][aa * P], e.x, h0, h1);
+          t2_horner2<P>(&csb[aa * P], e.x, h0, h1);
           const float2 cv = upk(e.c), sv = upk(e.s);
           A1[2 * pp] = ffma2(bcv(cv.x), h0, A1[2 * pp]);
           A2[2 * pp] = ffma2(bcv(sv.x), h0, A2[2 * pp]);
@@ -1239,13 +1288,17 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
           A2[2 * pp + 1] = ffma2(bcv(sv.y), h1, A2[2 * pp + 1]);
         }
       }
+      };
+      if (it.tw < 0) continue;                     // idle warp (its segment is past the tile)
+      if (it.slot) sweep(sm.cs[b][1], sm.gs[b][1]);
+      else sweep(sm.cs[b][0], sm.gs[b][0]);
     }
     float2 *o = out + (int64_t)split * n_out;
 #pragma unroll
     for (int u = 0; u < SPT; ++u)
       if (valid[u]) {
         const float2 p1 = upk(A1[u]), p2 = upk(A2[u]);   // M = A1 + j A2
-        o[s.perm[base + threadIdx.x + u * 128]] = make_float2(p1.x - p2.y, p1.y + p2.x);
+        o[s.perm[base + u * 32]] = make_float2(p1.x - p2.y, p1.y + p2.x);
       }
   }
 }
@@ -1262,7 +1315,6 @@ __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int
     case 10: k2_filter_body<10, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     case 12: k2_filter_body<12, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     case 14: k2_filter_body<14, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 16: k2_filter_body<16, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1281,12 +1333,12 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
   const int total = *s.n_items * n_splits;
   unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
+  const int lane = (int)(threadIdx.x & 31);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
-    const int t = t2_item_tile(s.cstart, pl.T, item);
-    const int64_t base = s.tstart[t] + (int64_t)(item - s.cstart[t]) * (SPT * 128);
-    const int64_t end = s.tstart[t + 1];
-    const float *tb = a.tbox + t * 6;
+    const T2Item it = t2_item(s, pl.T, item, 32 * SPT);
+    const int64_t base = it.base + lane, end = it.end;
+    const float *tb = a.tbox + max(it.tw, 0) * 6;
     const float cx = t2_centre(tb, 0), cy = t2_centre(tb, 1), cz = t2_centre(tb, 2);
     f2x qx[NPAIR], qy[NPAIR], qz[NPAIR], qw[NPAIR], nx[NPAIR], ny[NPAIR], nz[NPAIR], nq[NPAIR];
     bool valid[SPT];
@@ -1296,7 +1348,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int u = 2 * pp + h;
-        const int64_t k = base + threadIdx.x + u * 128;
+        const int64_t k = base + u * 32;
         valid[u] = k < end;
         const float4 v = valid[u] ? s.pos[k] : make_float4(cx, cy, cz, 0.f);
         const float4 n4 = valid[u] ? s.aux[k] : make_float4(0.f, 0.f, 1.f, 0.f);
@@ -1314,7 +1366,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
     for (int pp = 0; pp < NPAIR; ++pp) { U[pp] = SF[pp] = Wx[pp] = Wy[pp] = Wz[pp] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
-    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, t, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
@@ -1322,21 +1374,24 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
       ph ^= 1u << b;
       __syncthreads();                             // every thread is done with buffer b ^ 1
       if (i0 + kT2GA < i_hi)
-        t2_stage_issue<P>(a, pl, row, t, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+        t2_stage_issue<P>(a, pl, row, it, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+      // (as in the filter; no_gain as a compile-time flag keeps its test out of the loop)
+      auto sweep = [&](auto ng, const float2 *csb, const float4 (*gsb)[2]) {
+        constexpr bool kNoGain = decltype(ng)::value;
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
-        const float4 g0 = sm.gs[b][aa][0], g1 = sm.gs[b][aa][1];
+        const float4 g0 = gsb[aa][0], g1 = gsb[aa][1];
         // -a' = g0.xyz / 2:  n.(q' - a') = n.q' + n.(g0/2)
         const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
 #pragma unroll
         for (int pp = 0; pp < NPAIR; ++pp) {
           const Geo2 e = t2_geo2<true, false>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);  // (cos, -sin)
           f2x hre, him;
-          t2_horner_pp<P>(&sm.cs[b][aa * P], e.x, hre, him);
+          t2_horner_pp<P>(&csb[aa * P], e.x, hre, him);
           const f2x R = ffma2(e.c, hre, fmul2(e.s, him));          // Re(E h) = c hr - s hi
           const f2x r2 = fmul2(e.r, e.r);
           const f2x Rr2 = fmul2(R, r2);
-          if (no_gain) {                               // E11 ablation: g = 1, dg/dn = 0
+          if (kNoGain) {                               // E11 ablation: g = 1, dg/dn = 0
             U[pp] = fadd2(U[pp], Rr2);
             continue;
           }
@@ -1354,6 +1409,15 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
           Wz[pp] = ffma2(F, h0z, Wz[pp]);
         }
       }
+      };
+      if (it.tw < 0) continue;                     // idle warp (its segment is past the tile)
+      if (no_gain) {
+        if (it.slot) sweep(std::true_type{}, sm.cs[b][1], sm.gs[b][1]);
+        else sweep(std::true_type{}, sm.cs[b][0], sm.gs[b][0]);
+      } else {
+        if (it.slot) sweep(std::false_type{}, sm.cs[b][1], sm.gs[b][1]);
+        else sweep(std::false_type{}, sm.cs[b][0], sm.gs[b][0]);
+      }
     }
     float *o = out + (int64_t)split * 5 * n_out;
 #pragma unroll
@@ -1364,7 +1428,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
       for (int h = 0; h < 2; ++h) {
         const int u = 2 * pp + h;
         if (!valid[u]) continue;
-        const int k = (int)(base + threadIdx.x + u * 128);
+        const int k = (int)(base + u * 32);
         const int64_t j = s.perm[k];                            // compacted index
         const float T = s.aux[k].w, TT = T * T;
         const float Uu = h ? Uv.y : Uv.x, SFu = h ? SFv.y : SFv.x;
@@ -1393,7 +1457,6 @@ __global__ void __launch_bounds__(128, MINB) k2_bwd(T2Args a, T2Sorted s, int ro
     case 10: k2_bwd_body<10, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
     case 12: k2_bwd_body<12, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
     case 14: k2_bwd_body<14, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
-    case 16: k2_bwd_body<16, NPAIR>(a, pl, s, row, out, n_out, n_splits, aps, no_gain, sm); break;
     default: break;
   }
 }
@@ -1561,7 +1624,6 @@ __global__ void __launch_bounds__(kT2FwdAnts, MINB) k2_fwd(T2Args a, T2Sorted s,
     case 10: k2_fwd_body<10, KIND, RP>(a, pl, s, no_gain, sm); break;
     case 12: k2_fwd_body<12, KIND, RP>(a, pl, s, no_gain, sm); break;
     case 14: k2_fwd_body<14, KIND, RP>(a, pl, s, no_gain, sm); break;
-    case 16: k2_fwd_body<16, KIND, RP>(a, pl, s, no_gain, sm); break;
     default: break;
   }
 }
@@ -1731,8 +1793,7 @@ __global__ void __launch_bounds__(kT2OutThreads, 2) k2_fout(T2Args a, const int 
         case 8: RFR_FOUT_P(8) break;
         case 10: RFR_FOUT_P(10) break;
         case 12: RFR_FOUT_P(12) break;
-        case 14: RFR_FOUT_P(14) break;
-        default: RFR_FOUT_P(16) break;
+        default: RFR_FOUT_P(14) break;
       }
 #undef RFR_FOUT_P
       // transposed warp reduction (lane q holds moment q0 + q), then the warps in order

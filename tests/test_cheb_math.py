@@ -21,6 +21,40 @@ def test_truncation_rule_bounds_the_tail(P):
         assert tail(P, z) < 1e-7, (P, z)
 
 
+# r2 engine rule (rfr_tiled.cu t2_select_P): per-tile Horner expansions, tail < 1e-5 (below the
+# ~2e-5 rad per-pair phase error of the unreduced fp32 carrier angle); global expansion t2_select_Pg
+Z_MAX_TILE = {8: 1.632, 10: 2.681, 12: 3.866, 14: 4.812}
+Z_MAX_GLOBAL = {16: 4.812, 20: 7.33, 24: 10.061, 28: 12.946, 32: 15.948, 48: 28.6}
+
+
+@pytest.mark.parametrize("P", sorted(Z_MAX_TILE))
+def test_r2_tile_rule_bounds_the_tail(P):
+    for z in np.linspace(0.0, Z_MAX_TILE[P], 60):
+        assert tail(P, z) < 1e-5, (P, z)
+    # and the rule is not looser than needed by more than the next even P
+    assert tail(P - 2, Z_MAX_TILE[P]) > 1e-5
+
+
+@pytest.mark.parametrize("P", sorted(Z_MAX_GLOBAL))
+def test_r2_global_rule_bounds_the_tail(P):
+    for z in np.linspace(0.0, Z_MAX_GLOBAL[P], 60):
+        assert tail(P, z) < 1e-7, (P, z)
+
+
+def test_r2_tile_rule_matches_device_source():
+    """the thresholds above are the ones compiled into t2_select_P / t2_select_Pg"""
+    import os
+    import re
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2605_29097_b200", "csrc",
+                            "rfr_tiled.cu")).read()
+    def rule(name):
+        body = src[src.index(name + "(double z)"):]
+        body = body[:body.index("return 0;")]
+        return {int(p): float(z) for z, p in re.findall(r"z <= ([0-9.]+)\) return (\d+);", body)}
+    assert rule("t2_select_P") == Z_MAX_TILE
+    assert rule("t2_select_Pg") == Z_MAX_GLOBAL
+
+
 @pytest.mark.parametrize("sign", [-1, 1])
 def test_jacobi_anger_expansion_matches_exponential(sign):
     """exp(sign j z x) = sum_p eps_p (sign j)^p J_p(z) T_p(x): the forward uses sign = -1, the
