@@ -69,7 +69,9 @@ def moment_ops_per_pair(sweep: str, P: int) -> int:
     return 2 * (P - 1) + (4 if sweep == "filter" else 2) if sweep != "forward" else 3 * P
 
 
-XU_PER_PAIR = 4
+# MUFU per pair: rsqrt, rcp, sin, cos; the filter's default geometry (t2_geo1: one Newton step on the FMA
+# pipe instead of the rcp) issues 3
+XU_PER_PAIR = {"filter": 3, "backward": 4, "forward": 4}
 
 
 def peaks():
@@ -444,7 +446,7 @@ def run_gpu(args):
         P = pl["P"]
         ops = lane_ops_per_pair(sw, P)
         ach = ops * pairs[sw] / (ms * 1e-3)
-        xu = XU_PER_PAIR * pairs[sw] / (ms * 1e-3)
+        xu = XU_PER_PAIR[sw] * pairs[sw] / (ms * 1e-3)
         kern = {"filter": "k2_filter", "backward": "k2_bwd", "forward": "k2_fwd"}[sw]
         roofs.append({"kernel": f"{kern}<P={P}>", "sweep": sw, "bound": "alu",
                       "achieved": ach / 1e12, "peak": peak_ops / 1e12, "unit": "T FP32 lane-ops/s",
@@ -469,7 +471,7 @@ def run_gpu(args):
                               f"{dom['lane_ops_per_pair']} lane-ops per (point, antenna) pair "
                               "(DESIGN 5e work model: pair geometry + Horner / moments + epilogue), "
                               "timed live per launch with CUDA events on the launching stream "
-                              "(rfr_profile); xu_frac: 4 MUFU per pair against 148 x 16 XU lanes")}
+                              f"(rfr_profile); xu_frac: {XU_PER_PAIR[dom['sweep']]} MUFU per pair against 148 x 16 XU lanes")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.emulate_world:
         r = oracle_sample_rates(prob, budget_s=args.ref_budget)

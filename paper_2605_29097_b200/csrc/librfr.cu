@@ -144,7 +144,7 @@ struct Layout {
          off_ccoef = 0, off_cpart = 0, off_cbadj = 0, off_recc = 0, off_ccnt = 0, off_aflag = 0,
          off_idxc = 0, off_ttile = 0, off_tbcnt = 0, off_tstart = 0, off_tperm = 0, off_tqs = 0,
          off_tbox = 0, off_tlc = 0, off_thdr = 0, off_tcoef = 0, off_tbmom = 0, off_trs = 0,
-         off_tfp = 0, off_tgeo = 0, total = 0;
+         off_tfp = 0, off_tgeo = 0, off_t2geof = 0, total = 0;
   // r2 tiled engine (rfr_tiled.h): plan, tables, per-(tile, antenna) data, two sorted views
   size_t off_t2plan = 0, off_t2boxp = 0, off_t2tabs = 0, off_t2tbox = 0, off_t2lc = 0,
          off_t2geo = 0, off_t2lg = 0, off_t2acoef = 0, off_t2gexp = 0, off_t2coef = 0,
@@ -241,6 +241,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_t2lc = take((size_t)kT2Max * na1 * 8);
     L.off_t2lct = take((size_t)kT2Max * na1 * 8);
     L.off_t2geo = take((size_t)kT2Max * na1 * 32);
+    L.off_t2geof = take((size_t)kT2Max * na1 * 32);
     L.off_t2lg = take((size_t)na1 * 3 * 8);
     L.off_t2acoef = take((size_t)2 * nf * kT2PgMax * 8);     // both layouts
     L.off_t2gexp = take((size_t)2 * na1 * kT2PgMax * 8);
@@ -442,6 +443,7 @@ T2Args make_t2(const rfr_antennas *ants, const rfr_freq_grid *grid, const rfr_wo
   t.lc = at<double>(ws, L.off_t2lc);
   t.lct = at<double>(ws, L.off_t2lct);
   t.tgeo = at<float4>(ws, L.off_t2geo);
+  t.tgeof = at<float4>(ws, L.off_t2geof);
   t.lg = at<double>(ws, L.off_t2lg);
   t.acoef = at<float2>(ws, L.off_t2acoef);
   t.tabs = at<double>(ws, L.off_t2tabs);

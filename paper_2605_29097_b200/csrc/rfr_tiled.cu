@@ -658,8 +658,12 @@ __global__ void k2_select(T2Args a) {
 }
 
 // g1.z = (2 d_a - L_c) -> (2 d_a - L_c) inv_t: x at the antenna's tile distance (the sweeps read
-// the geometry as stored; scaling it in the sweeps instead measured 2 % slower, r2v)
-__global__ void k2_geofix(T2Args a, const int *tstart) {
+// the geometry as stored; scaling it in the sweeps instead measured 2 % slower, r2v).  Adjoint
+// plans also get the filter's own image tgeof of the geometry (t2_geo1): every per-(tile, antenna)
+// product of the one-MUFU form precomputed in fp64 -- g0 = (-2a', kang = -2 pi kc d_a),
+// g1 = (kx = -inv_t d_a, 2 pi frac(2 d_a kc), x at the tile distance, 1 / d_a^2) -- three FMULs
+// per antenna iteration off the filter's FMA pipe.
+__global__ void k2_geofix(T2Args a, const int *tstart, int kind) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
   const int64_t n = (int64_t)pl.T * a.n_a;
@@ -667,8 +671,17 @@ __global__ void k2_geofix(T2Args a, const int *tstart) {
        w += (int64_t)gridDim.x * blockDim.x) {
     const int t = (int)(w / a.n_a);
     if (tstart[t + 1] == tstart[t]) continue;
-    float4 *g = a.tgeo + w * 2 + 1;
-    g->z = (float)((double)g->z * pl.inv_t);
+    float4 *g = a.tgeo + w * 2;
+    const float4 g0 = g[0];
+    float4 g1 = g[1];
+    g1.z = (float)((double)g1.z * pl.inv_t);
+    g[1].z = g1.z;
+    if (kind == kT2PlanAdjoint) {
+      const double da = (double)g1.x;
+      float4 *f = a.tgeof + w * 2;
+      f[0] = make_float4(g0.x, g0.y, g0.z, (float)(-2.0 * kPi * a.kc * da));
+      f[1] = make_float4((float)(-pl.inv_t * da), (float)((double)g1.y * (2.0 * kPi)), g1.z, g1.w);
+    }
   }
 }
 
@@ -798,7 +811,7 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
   k2_tsetup<<<(unsigned)std::min<int64_t>((int64_t)(kT2Max / 8) * ((a.n_a + 31) / 32), 148 * 16), 256, 0, st>>>(a, srt.tstart);
   k2_gsetup<<<(unsigned)((a.n_a + 255) / 256), 256, 0, st>>>(a);
   k2_select<<<1, 1, 0, st>>>(a);
-  k2_geofix<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart);
+  k2_geofix<<<(unsigned)std::min<int64_t>((kT2Max * a.n_a + 255) / 256, 148 * 16), 256, 0, st>>>(a, srt.tstart, kind);
   k2_tables<<<1 + (a.n_f + 127) / 128, 128, 0, st>>>(a);
   if ((e = cudaGetLastError()) == cudaSuccess) add_launches(7);
   else return e;
@@ -1077,9 +1090,10 @@ __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x 
 // load was ~0.9 of its FMA load.  Error: the residual's rounding, ~2^-26 d_a (~3e-9 m at c3,
 // below the rcp form's) -- 1e-5 rad of carrier phase.  kang = -pi 2 kc d_a (times the sign),
 // kx = -inv_t d_a: the angle and x are affine in dln.
-template <bool NEG>
+// g0, g1: the filter's image of the geometry (k2_geofix): g0.w = kang, g1.x = kx, g1.y = the
+// centre angle in radians.
 __device__ __forceinline__ Geo2 t2_geo1(const float4 &g0, const float4 &g1, f2x qx, f2x qy, f2x qz,
-                                        f2x qw, float kang, float kx) {
+                                        f2x qw) {
   const f2x del = ffma2(bcv(g0.x), qx, ffma2(bcv(g0.y), qy, ffma2(bcv(g0.z), qz, qw)));
   const f2x s = ffma2(del, bcv(g1.w), bcv(1.f));           // 1 + e (rsqrt input only)
   const f2x en = fmul2(del, bcv(-g1.w));                    // -e
@@ -1088,8 +1102,7 @@ __device__ __forceinline__ Geo2 t2_geo1(const float4 &g0, const float4 &g1, f2x 
   const f2x w = fmul2(s, y);
   const f2x rn = fadd2(ffma2(w, w, bcv(-1.f)), en);         // w^2 - (1 + e) = -rho
   const f2x dln = ffma2(rn, y, ffma2(w, bcv(-2.f), bcv(2.f)));
-  const float sg = NEG ? -kTwoPi : kTwoPi;
-  const f2x ang = ffma2(dln, bcv(kang), bcv(g1.y * sg));
+  const f2x ang = ffma2(dln, bcv(g0.w), bcv(g1.y));
   const float2 av = upk(ang);
   Geo2 o;
   float s0, c0, s1, c1;
@@ -1097,9 +1110,18 @@ __device__ __forceinline__ Geo2 t2_geo1(const float4 &g0, const float4 &g1, f2x 
   sc_ftz(av.y, s1, c1);
   o.c = pk(c0, c1);
   o.s = pk(s0, s1);
-  o.x = ffma2(dln, bcv(kx), bcv(g1.z));
+  o.x = ffma2(dln, bcv(g1.x), bcv(g1.z));
   o.r = y;                                          // d_a / d (not 1 / d)
   return o;
+}
+
+// the same on the shared geometry image tgeo, the per-antenna products formed in the loop (A/B:
+// RFR_T2GEO=3)
+__device__ __forceinline__ Geo2 t2_geo1m(const float4 &g0, const float4 &g1, f2x qx, f2x qy, f2x qz,
+                                         f2x qw, float kang, float kx) {
+  float4 h0 = g0, h1 = g1;
+  h0.w = kang; h1.x = kx; h1.y = g1.y * kTwoPi;
+  return t2_geo1(h0, h1, qx, qy, qz, qw);
 }
 
 constexpr int kT2GA = 32;                         // antennas per shared-memory stage
@@ -1109,12 +1131,16 @@ constexpr int kT2GA = 32;                         // antennas per shared-memory 
 // by inv_t).  Both blocks are contiguous in HBM for a run of antennas, so one thread moves a stage
 // with two bulk copies on the TMA engine (cp.async.bulk, completion on the buffer's mbarrier)
 // while the CTA computes the previous stage.
-struct AdjStage {
-  float2 cs[2][2][kT2GA * kT2PMax];               // [buffer][slot][antenna * P + k]
-  float4 gs[2][2][kT2GA][2];                      // [buffer][slot][antenna][g0, g1]
+template <int GA>
+struct AdjStageT {
+  static constexpr int kGA = GA;
+  float2 cs[2][2][GA * kT2PMax];                  // [buffer][slot][antenna * P + k]
+  float4 gs[2][2][GA][2];                         // [buffer][slot][antenna][g0, g1]
   unsigned long long bar[2];
 };
-__device__ __forceinline__ void t2_stage_init(AdjStage &sm) {
+using AdjStage = AdjStageT<kT2GA>;
+template <class Stage>
+__device__ __forceinline__ void t2_stage_init(Stage &sm) {
   if (threadIdx.x == 0) {
     mbar_init(&sm.bar[0], 1);
     mbar_init(&sm.bar[1], 1);
@@ -1153,18 +1179,18 @@ __device__ __forceinline__ T2Item t2_item(const T2Sorted &s, int T, int item, in
   return it;
 }
 
-template <int P>
+template <int P, class Stage>
 __device__ __forceinline__ void t2_stage_issue(const T2Args &a, const T2Plan &pl, int row,
-                                               const T2Item &it, int64_t i0, int ga, AdjStage &sm,
-                                               int b) {
+                                               const T2Item &it, int64_t i0, int ga, Stage &sm,
+                                               int b, const float4 *tgeo) {
   if (threadIdx.x != 0) return;
   const unsigned bc = (unsigned)(ga * P * 8), bg = (unsigned)(ga * 32);
   mbar_arrive_expect_tx(&sm.bar[b], (bc + bg) * (it.two ? 2u : 1u));
   bulk_g2s(&sm.cs[b][0][0], a.coef + (((int64_t)row * pl.T + it.t0) * a.n_a + i0) * P, bc, &sm.bar[b]);
-  bulk_g2s(&sm.gs[b][0][0][0], a.tgeo + ((int64_t)it.t0 * a.n_a + i0) * 2, bg, &sm.bar[b]);
+  bulk_g2s(&sm.gs[b][0][0][0], tgeo + ((int64_t)it.t0 * a.n_a + i0) * 2, bg, &sm.bar[b]);
   if (it.two) {
     bulk_g2s(&sm.cs[b][1][0], a.coef + (((int64_t)row * pl.T + it.t1) * a.n_a + i0) * P, bc, &sm.bar[b]);
-    bulk_g2s(&sm.gs[b][1][0][0], a.tgeo + ((int64_t)it.t1 * a.n_a + i0) * 2, bg, &sm.bar[b]);
+    bulk_g2s(&sm.gs[b][1][0][0], tgeo + ((int64_t)it.t1 * a.n_a + i0) * 2, bg, &sm.bar[b]);
   }
 }
 
@@ -1205,15 +1231,16 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 // work item = (two units of kT2FltChunk / 2 tile-sorted points, antenna split, t2_item); thread =
 // 4 points of its warp's segment (lane + 32 u)
 // GM: geometry of the filter: 0 = t2_geo2 unreduced angle, 1 = t2_geo2 reduced, 2 = t2_geo1
-template <int P, int GM, int NPAIR, int UNR>
+template <int P, int GM, int NPAIR, int UNR, int GA>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
-                                               int n_splits, int64_t aps, AdjStage &sm) {
+                                               int n_splits, int64_t aps, AdjStageT<GA> &sm) {
   constexpr int SPT = 2 * NPAIR;                   // points per thread (chunk = SPT * 128)
   const int total = *s.n_items * n_splits;
   unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
-  const float kangf = (float)(-2.0 * kPi * a.kc), kxf = (float)(-pl.inv_t);   // t2_geo1
+  const float4 *fgeo = GM == 2 ? a.tgeof : a.tgeo;  // t2_geo1 reads its own image (k2_geofix)
+  const float kangf = (float)(-2.0 * kPi * a.kc), kxf = (float)(-pl.inv_t);   // t2_geo1m
   const int lane = (int)(threadIdx.x & 31);
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int item = w / n_splits, split = w % n_splits;
@@ -1244,34 +1271,47 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
     for (int u = 0; u < SPT; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
-    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)GA, i_hi - i_lo), sm, 0, fgeo);
     int b = 0;
-    for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
-      const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
+    for (int64_t i0 = i_lo; i0 < i_hi; i0 += GA, b ^= 1) {
+      const int ga = (int)min((int64_t)GA, i_hi - i0);
       mbar_wait(&sm.bar[b], (ph >> b) & 1u);
       ph ^= 1u << b;
       __syncthreads();                             // every thread is done with buffer b ^ 1
-      if (i0 + kT2GA < i_hi)
-        t2_stage_issue<P>(a, pl, row, it, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+      if (i0 + GA < i_hi)
+        t2_stage_issue<P>(a, pl, row, it, i0 + GA, (int)min((int64_t)GA, i_hi - i0 - GA), sm, b ^ 1, fgeo);
       // the stage slot as a compile-time index in each of two copies of the antenna loop: a
       // per-warp shared-memory base would move the loop's addressing and control off the uniform
       // datapath (r3b: +9 instructions per antenna, filter 22.7 -> 23.2 ms)
       auto sweep = [&](const float2 *csb, const float4 (*gsb)[2]) {
-#pragma unroll UNR
+      // UNR == 3 (A/B, RFR_T2FV=pf): the next antenna's geometry words are loaded into the same
+      // registers as soon as this antenna's geometry has consumed them (before its Horner), so
+      // the first FFMA2 of an iteration does not wait on its own LDS
+      constexpr bool PF = UNR == 3;
+      float4 g0n = gsb[0][0], g1n = gsb[0][1];
+#pragma unroll (PF ? 1 : UNR)
       for (int aa = 0; aa < ga; ++aa) {
         // (issuing the next antenna's geometry ahead of this Horner -- software pipelining --
         // measured slower, r2p: 24.8 -> 25.1 ms)
-        const float4 g0 = gsb[aa][0], g1 = gsb[aa][1];
+        const float4 g0 = PF ? g0n : gsb[aa][0], g1 = PF ? g1n : gsb[aa][1];
         Geo2 cur[NPAIR];
         if (GM == 2) {
+#pragma unroll
+          for (int pp = 0; pp < NPAIR; ++pp)
+            cur[pp] = t2_geo1(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp]);
+        } else if (GM == 3) {
           const float kang = g1.x * kangf, kx = g1.x * kxf;
 #pragma unroll
           for (int pp = 0; pp < NPAIR; ++pp)
-            cur[pp] = t2_geo1<false>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kang, kx);
+            cur[pp] = t2_geo1m(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kang, kx);
         } else {
 #pragma unroll
           for (int pp = 0; pp < NPAIR; ++pp)
             cur[pp] = t2_geo2<false, GM == 1>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);
+        }
+        if (PF) {
+          const int an = min(aa + 1, ga - 1);
+          g0n = gsb[an][0]; g1n = gsb[an][1];
         }
 #pragma unroll
         for (int pp = 0; pp < NPAIR; ++pp) {
@@ -1303,18 +1343,18 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   }
 }
 
-template <int MINB, int GM, int NPAIR, int UNR = 1>
+template <int MINB, int GM, int NPAIR, int UNR = 1, int GA = kT2GA>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
   const T2Plan pl = *a.plan;
-  __shared__ __align__(16) AdjStage sm;
+  __shared__ __align__(16) AdjStageT<GA> sm;
   t2_stage_init(sm);
   switch (pl.P) {
-    case 8: k2_filter_body<8, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14, GM, NPAIR, UNR>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1366,7 +1406,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
     for (int pp = 0; pp < NPAIR; ++pp) { U[pp] = SF[pp] = Wx[pp] = Wy[pp] = Wz[pp] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
     __syncthreads();                               // the previous item's stages are consumed
-    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0);
+    if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0, a.tgeo);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
       const int ga = (int)min((int64_t)kT2GA, i_hi - i0);
@@ -1374,7 +1414,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
       ph ^= 1u << b;
       __syncthreads();                             // every thread is done with buffer b ^ 1
       if (i0 + kT2GA < i_hi)
-        t2_stage_issue<P>(a, pl, row, it, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1);
+        t2_stage_issue<P>(a, pl, row, it, i0 + kT2GA, (int)min((int64_t)kT2GA, i_hi - i0 - kT2GA), sm, b ^ 1, a.tgeo);
       // (as in the filter; no_gain as a compile-time flag keeps its test out of the loop)
       auto sweep = [&](auto ng, const float2 *csb, const float4 (*gsb)[2]) {
         constexpr bool kNoGain = decltype(ng)::value;
@@ -1905,15 +1945,18 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     const char *e = getenv("RFR_T2GEO"), *r = getenv("RFR_T2RED");
     gm = e ? atoi(e) : 2;
     if (r && r[0] == '1') gm = 1;
-    if (gm < 0 || gm > 2) gm = 2;
+    if (gm < 0 || gm > 3) gm = 2;
   }
-  // launch-shape variants (A/B, RFR_T2FV): m4 = 4 CTAs per SM (128 registers), u2 = the antenna
-  // loop unrolled by 2 (two antennas' independent work in one scheduling window)
+  // launch-shape variants (RFR_T2FV).  Default pf64: stages of 64 antennas (half the per-stage CTA
+  // barriers) and the next antenna's geometry words loaded before this antenna's Horner (r4c/r4d at
+  // c3: base 22.96 ms, g64 22.8, pf 22.3, pf64 22.17).  A/B: base, g64, pf; m4 = 4 CTAs per SM (128
+  // registers), u2 = the antenna loop unrolled by 2 (two antennas' independent work in one
+  // scheduling window), m6 = 6 CTAs per SM
   static int fv = -1;
   if (fv < 0) {
     const char *e = getenv("RFR_T2FV");
-    fv = !e ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3
-       : !strcmp(e, "m6") ? 4 : 0;
+    fv = !e ? 7 : !strcmp(e, "base") ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3
+       : !strcmp(e, "m6") ? 4 : !strcmp(e, "g64") ? 5 : !strcmp(e, "pf") ? 6 : !strcmp(e, "pf64") ? 7 : 0;
   }
   const unsigned g5 = (unsigned)(n_sms * 5), g4 = (unsigned)(n_sms * 4), g3 = (unsigned)(n_sms * 3);
   if (srt.chunk == 8 * 128) {
@@ -1930,6 +1973,32 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     k2_filter<5, 2, 2, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 4) {
     k2_filter<6, 2, 2><<<(unsigned)(n_sms * 6), 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 5) {
+    // stages of 64 antennas (half the per-stage CTA barriers; 40 KB of shared memory per CTA)
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k2_filter<5, 2, 2, 1, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      once = true;
+    }
+    k2_filter<5, 2, 2, 1, 64><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 6) {
+    k2_filter<5, 2, 2, 3><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 7) {
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k2_filter<5, 2, 2, 3, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      once = true;
+    }
+    k2_filter<5, 2, 2, 3, 64><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 3 && fv == 7) {
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k2_filter<5, 3, 2, 3, 64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      once = true;
+    }
+    k2_filter<5, 3, 2, 3, 64><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 3) {
+    k2_filter<5, 3, 2><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 3) {
     k2_filter<4, 2, 2, 2><<<g4, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else {

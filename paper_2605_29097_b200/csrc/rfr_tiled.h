@@ -84,6 +84,7 @@ struct T2Args {
   double *lc;                          // [kT2Max][n_a] centre path length of (tile, antenna)
   double *lct;                         // [n_a][kT2Max] the same, antenna-major (k2_fout)
   float4 *tgeo;                        // [kT2Max][n_a][2] tile-relative geometry
+  float4 *tgeof;                       // [kT2Max][n_a][2] the filter's image of it (k2_geofix)
   double *lg;                          // [n_a][3]: global centre, min / max tile centre (m)
   float2 *acoef;                       // global a[m][q]: [kT2PgMax][n_f] (q-major), then [n_f][kT2PgMax]
   double *tabs;                        // [4][kT2PMax][kT2PMax] nodes, W (nodes -> monomial), lambda
