@@ -104,6 +104,7 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr float kInv16Pi2f = 0.00633257759406206f;   // 1 / (4 pi)^2 (Q3)
+constexpr float kSqrt2f = 1.41421356237309505f;
 
 // ------------------------------------------------------------------ packed f32x2 helpers
 __device__ __forceinline__ f2x bcv(float v) { return pk(v, v); }
@@ -1042,6 +1043,7 @@ __device__ __forceinline__ int t2_item_tile(const int *cstart, int T, int item) 
 // [-1/2, 1/2]; x = (2 d_a - L_c) inv + 2 inv (d - d_a).  NEG: returns (cos, -sin).
 struct Geo2 {
   f2x c, s, x, r;                                 // cos, sin of the centre phase, x, 1/d
+  f2x dl;                                         // d - d_a (t2_geo2 only; x = g1.z + 2 inv_t dl)
 };
 // RED = false (the filter's default): no reduction of the cycle count before the MUFU (the angle
 // dl 2 pi 2 kc + 2 pi frac(2 d_a kc) in one FFMA2): |angle| <= ~2 pi (2 kc x tile spread), and
@@ -1078,6 +1080,7 @@ __device__ __forceinline__ Geo2 t2_geo2(const float4 &g0, const float4 &g1, f2x 
   o.s = pk(s0, s1);
   o.x = ffma2(dl, bcv(inv2f), bcv(g1.z));
   o.r = r;
+  o.dl = dl;
   return o;
 }
 
@@ -1112,6 +1115,7 @@ __device__ __forceinline__ Geo2 t2_geo1(const float4 &g0, const float4 &g1, f2x 
   o.s = pk(s0, s1);
   o.x = ffma2(dln, bcv(g1.x), bcv(g1.z));
   o.r = y;                                          // d_a / d (not 1 / d)
+  o.dl = dln;
   return o;
 }
 
@@ -1394,12 +1398,17 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
         const float4 n4 = valid[u] ? s.aux[k] : make_float4(0.f, 0.f, 1.f, 0.f);
         v4[h][0] = v.x - cx; v4[h][1] = v.y - cy; v4[h][2] = v.z - cz;
         v4[h][3] = fmaf(v4[h][0], v4[h][0], fmaf(v4[h][1], v4[h][1], v4[h][2] * v4[h][2]));
-        n3[h][0] = n4.x; n3[h][1] = n4.y; n3[h][2] = n4.z;
+        // the normal scaled by sqrt 2: g = 2 (n.w)^2 - 1 = (s n.w)(s n.w) - 1 without a doubling in
+        // the pair loop; F, and with it sum F and W, carry the factor sqrt 2 (removed at the store).
+        // Halved as well: n.(-a') = (n / 2).g0 with g0 = -2a' as staged (no per-antenna 0.5 g0)
+        n3[h][0] = (0.5f * kSqrt2f) * n4.x; n3[h][1] = (0.5f * kSqrt2f) * n4.y;
+        n3[h][2] = (0.5f * kSqrt2f) * n4.z;
       }
       qx[pp] = pk(v4[0][0], v4[1][0]); qy[pp] = pk(v4[0][1], v4[1][1]);
       qz[pp] = pk(v4[0][2], v4[1][2]); qw[pp] = pk(v4[0][3], v4[1][3]);
       nx[pp] = pk(n3[0][0], n3[1][0]); ny[pp] = pk(n3[0][1], n3[1][1]); nz[pp] = pk(n3[0][2], n3[1][2]);
-      nq[pp] = ffma2(nx[pp], qx[pp], ffma2(ny[pp], qy[pp], fmul2(nz[pp], qz[pp])));   // n . q'
+      const f2x nqh = ffma2(nx[pp], qx[pp], ffma2(ny[pp], qy[pp], fmul2(nz[pp], qz[pp])));
+      nq[pp] = fadd2(nqh, nqh);                                    // sqrt 2 n . q'
     }
     f2x U[NPAIR], SF[NPAIR], Wx[NPAIR], Wy[NPAIR], Wz[NPAIR];
 #pragma unroll
@@ -1421,8 +1430,8 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
 #pragma unroll 1
       for (int aa = 0; aa < ga; ++aa) {
         const float4 g0 = gsb[aa][0], g1 = gsb[aa][1];
-        // -a' = g0.xyz / 2:  n.(q' - a') = n.q' + n.(g0/2)
-        const f2x h0x = bcv(0.5f * g0.x), h0y = bcv(0.5f * g0.y), h0z = bcv(0.5f * g0.z);
+        // -a' = g0.xyz / 2:  n.(q' - a') = n.q' + (n/2).g0; W accumulates F g0 = 2 F (-a')
+        const f2x h0x = bcv(g0.x), h0y = bcv(g0.y), h0z = bcv(g0.z);
 #pragma unroll
         for (int pp = 0; pp < NPAIR; ++pp) {
           const Geo2 e = t2_geo2<true, false>(g0, g1, qx[pp], qy[pp], qz[pp], qw[pp], kc2f, inv2f);  // (cos, -sin)
@@ -1436,13 +1445,15 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
             continue;
           }
           const f2x nd = ffma2(nx[pp], h0x, ffma2(ny[pp], h0y, ffma2(nz[pp], h0z, nq[pp])));
-          const f2x ndr2 = fmul2(nd, r2);              // (n.w) / d
-          const f2x g = ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f));   // 2 (n.w)^2 - 1
+          const f2x ndr2 = fmul2(nd, r2);              // sqrt 2 (n.w) / d
+          const f2x g = ffma2(nd, ndr2, bcv(-1.f));    // 2 (n.w)^2 - 1
           const float2 gv = upk(g);
           const f2x gpos = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
-          const f2x msk = pk(gv.x > 0.f ? 1.f : 0.f, gv.y > 0.f ? 1.f : 0.f);
           U[pp] = ffma2(Rr2, gpos, U[pp]);
-          const f2x F = fmul2(fmul2(Rr2, ndr2), msk);  // R gamma 4 (n.w) / d without 4 / (4 pi)^2
+          // sqrt 2 R gamma 4 (n.w) / d without 4 / (4 pi)^2, zero where the gain is clamped (selects
+          // on the ALU pipe, no mask multiply)
+          const float2 Fm = upk(fmul2(Rr2, ndr2));
+          const f2x F = pk(gv.x > 0.f ? Fm.x : 0.f, gv.y > 0.f ? Fm.y : 0.f);
           SF[pp] = fadd2(SF[pp], F);
           Wx[pp] = ffma2(F, h0x, Wx[pp]);
           Wy[pp] = ffma2(F, h0y, Wy[pp]);
@@ -1473,13 +1484,13 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
         const float T = s.aux[k].w, TT = T * T;
         const float Uu = h ? Uv.y : Uv.x, SFu = h ? SFv.y : SFv.x;
         const float u16 = Uu * kInv16Pi2f;
-        const float f4 = 4.f * kInv16Pi2f * TT;
+        const float f4 = (4.f * kInv16Pi2f / kSqrt2f) * TT;
         o[j] = TT * u16;                                        // S1
         o[n_out + j] = T > 0.f ? 2.f * T * u16 : 0.f;           // S2
         // S3 = T^2 sum F (q' - a')
-        o[2 * n_out + j] = f4 * fmaf(h ? qxv.y : qxv.x, SFu, h ? Wxv.y : Wxv.x);
-        o[3 * n_out + j] = f4 * fmaf(h ? qyv.y : qyv.x, SFu, h ? Wyv.y : Wyv.x);
-        o[4 * n_out + j] = f4 * fmaf(h ? qzv.y : qzv.x, SFu, h ? Wzv.y : Wzv.x);
+        o[2 * n_out + j] = f4 * fmaf(h ? qxv.y : qxv.x, SFu, 0.5f * (h ? Wxv.y : Wxv.x));
+        o[3 * n_out + j] = f4 * fmaf(h ? qyv.y : qyv.x, SFu, 0.5f * (h ? Wyv.y : Wyv.x));
+        o[4 * n_out + j] = f4 * fmaf(h ? qzv.y : qzv.x, SFu, 0.5f * (h ? Wzv.y : Wzv.x));
       }
     }
   }
@@ -1571,12 +1582,16 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
         const int k = threadIdx.x;
         v[0][k] = x; v[1][k] = y; v[2][k] = z; v[3][k] = fmaf(x, x, fmaf(y, y, z * z));
         if (KIND == kFwdTrace) {
-          v[4][k] = pv.w * pn.w * pn.w;
-          v[5][k] = fmaf(pn.x, x, fmaf(pn.y, y, pn.z * z));
-          v[6][k] = pn.x; v[7][k] = pn.y; v[8][k] = pn.z;
+          // the constant of gamma folded into the weight; the normal scaled by sqrt 2 so that
+          // g = 2 (n.w)^2 - 1 = (s n.w)(s n.w) - 1 needs no doubling in the pair loop
+          v[4][k] = pv.w * pn.w * pn.w * kInv16Pi2f;
+          const float sx = kSqrt2f * pn.x, sy = kSqrt2f * pn.y, sz = kSqrt2f * pn.z;
+          v[5][k] = fmaf(sx, x, fmaf(sy, y, sz * z));
+          v[6][k] = sx; v[7][k] = sy; v[8][k] = sz;
         } else {
           v[4][k] = pv.w;                                   // K5 records: w = Re c_q, T = Im c_q
           v[5][k] = pn.w;
+          v[6][k] = -pn.w;                                  // -Im c_q (no negation in the pair loop)
         }
       }
       __syncthreads();
@@ -1590,7 +1605,7 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
         const float(*v)[kT2FwdTJ] = sm.v[b];
         // RP record pairs per iteration: independent geometry chains in flight (staged slots past
         // nv hold zero-weight records)
-        f2x cre[RP], cim[RP], xr[RP];
+        f2x cre[RP], cim[RP], xp[RP], xn[RP];       // c and +-2x
 #pragma unroll
         for (int rp = 0; rp < RP; ++rp) {
           const int j2 = jj + 2 * rp;
@@ -1604,32 +1619,37 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
             } else {
               const f2x nd = ffma2(ld2(&v[6][j2]), h0x,
                                    ffma2(ld2(&v[7][j2]), h0y, ffma2(ld2(&v[8][j2]), h0z, ld2(&v[5][j2]))));
-              const f2x ndr2 = fmul2(nd, r2);
-              const float2 gv = upk(ffma2(nd, fadd2(ndr2, ndr2), bcv(-1.f)));
+              const f2x ndr2 = fmul2(nd, r2);          // nd = sqrt 2 (n.(q - a))
+              const float2 gv = upk(ffma2(nd, ndr2, bcv(-1.f)));
               gg = pk(fmaxf(gv.x, 0.f), fmaxf(gv.y, 0.f));
             }
             // A = w T^2 g gamma; c = A e^{-j theta} = (A cos, A (-sin))
-            const f2x A = fmul2(fmul2(ld2(&v[4][j2]), gg), fmul2(r2, bcv(kInv16Pi2f)));
+            const f2x A = fmul2(fmul2(ld2(&v[4][j2]), gg), r2);
             cre[rp] = fmul2(A, e.c);
             cim[rp] = fmul2(A, e.s);
           } else {
             // c = (Ar + j Ai) e^{-j theta} = (Ar cos - Ai (-sin), Ai cos + Ar (-sin))
             const f2x Ar = ld2(&v[4][j2]), Ai = ld2(&v[5][j2]);
-            cre[rp] = ffma2(Ar, e.c, fmul2(Ai, fmul2(e.s, bcv(-1.f))));
+            cre[rp] = ffma2(Ar, e.c, fmul2(ld2(&v[6][j2]), e.s));
             cim[rp] = ffma2(Ai, e.c, fmul2(Ar, e.s));
           }
-          xr[rp] = e.x;
+          // +-2x straight from the path difference (x itself is not needed: the recurrence
+          // below runs on the doubled polynomials)
+          xp[rp] = ffma2(e.dl, bcv(2.f * inv2f), bcv(2.f * g1.z));
+          xn[rp] = ffma2(e.dl, bcv(-2.f * inv2f), bcv(-2.f * g1.z));
         }
 #pragma unroll
         for (int rp = 0; rp < RP; ++rp) {
           // moments in record-packed pairs (lane = record): Mre[p] += v_p(x) cre, Mim[p] += v_p(x)
           // cim, v_p = s_p T_p(x) by the plain recurrence, s = (+ + - -); no re-pairing
-          const f2x x = xr[rp], tp = fadd2(x, x), tn = fmul2(x, bcv(-2.f));
+          // (w_p = 2 v_p for p >= 1: w_1 = 2x, w_2 = (-2x)(2x) + 2, then the same recurrence;
+          // doubling is exact, the moments p >= 1 are halved when stored)
+          const f2x tp = xp[rp], tn = xn[rp];
           Mre[0] = fadd2(Mre[0], cre[rp]);
           Mim[0] = fadd2(Mim[0], cim[rp]);
-          Mre[1] = ffma2(x, cre[rp], Mre[1]);
-          Mim[1] = ffma2(x, cim[rp], Mim[1]);
-          f2x v2 = bcv(1.f), v1 = x;
+          Mre[1] = ffma2(tp, cre[rp], Mre[1]);
+          Mim[1] = ffma2(tp, cim[rp], Mim[1]);
+          f2x v2 = bcv(2.f), v1 = tp;
 #pragma unroll
           for (int p = 2; p < P; ++p) {
             const f2x vv = ffma2((p & 1) ? tp : tn, v1, v2);
@@ -1648,6 +1668,7 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
       for (int p = 0; p < P; ++p) {
         const float2 r = upk(Mre[p]), i2 = upk(Mim[p]);
         float2 v = make_float2(r.x + r.y, i2.x + i2.y);
+        if (p) { v.x *= 0.5f; v.y *= 0.5f; }
         if ((p >> 1) & 1) { v.x = -v.x; v.y = -v.y; }
         dst[p] = v;
       }
@@ -2050,15 +2071,20 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
   static int rp = -1;
   // two record pairs per iteration (r2q: forward 2.79 -> 2.67 ms at c3); RFR_T2FRP=1: one
   if (rp < 0) { const char *e = getenv("RFR_T2FRP"); rp = (e && atoi(e) == 1) ? 1 : 2; }
-  // CTAs per SM (RFR_T2FWM = 3 / 4; r2w at c3: 2.674 / 2.643 ms, dense 17.41 / 17.25)
+  // CTAs per SM (RFR_T2FWM = 3 / 4; r2w at c3: 2.674 / 2.643 ms, dense 17.41 / 17.25); 5 / 6: one
+  // record pair per iteration at 5 / 6 CTAs per SM (A/B)
   static int fm = -1;
   if (fm < 0) { const char *e = getenv("RFR_T2FWM"); fm = e ? atoi(e) : 4; }
   if (kind == kFwdTrace) {
-    if (rp == 2 && fm == 4) k2_fwd<kFwdTrace, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    if (fm == 5) k2_fwd<kFwdTrace, 1, 5><<<(unsigned)(n_sms * 5), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else if (fm == 6) k2_fwd<kFwdTrace, 1, 6><<<(unsigned)(n_sms * 6), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else if (rp == 2 && fm == 4) k2_fwd<kFwdTrace, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else if (rp == 2) k2_fwd<kFwdTrace, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else k2_fwd<kFwdTrace, 1, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
   } else {
-    if (rp == 2 && fm == 4) k2_fwd<kFwdMFAdj, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    if (fm == 5) k2_fwd<kFwdMFAdj, 1, 5><<<(unsigned)(n_sms * 5), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else if (fm == 6) k2_fwd<kFwdMFAdj, 1, 6><<<(unsigned)(n_sms * 6), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else if (rp == 2 && fm == 4) k2_fwd<kFwdMFAdj, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else if (rp == 2) k2_fwd<kFwdMFAdj, 2, 3><<<(unsigned)(n_sms * 3), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else k2_fwd<kFwdMFAdj, 1, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
   }
