@@ -1041,12 +1041,8 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     memset(&all, 0, sizeof(all));
     all.qx = samples->x; all.qy = samples->y; all.qz = samples->z; all.n = n_s;
     RFR_CU(t2_plan(t, all, v0, kT2PlanAdjoint, st));
-    RFR_CU(t2_prep_adjoint(t, v0.tstart, a.X, a.X2, st));
-    const int Sf = t2_flt_splits(n_s, t2_filter_chunk(), ants->n_ant, L.t2_flt_cap);
-    const int64_t apf = cdiv(cdiv(ants->n_ant, Sf), 16) * 16;
-    float2 *o = reinterpret_cast<float2 *>(Sf > 1 ? at<float>(ws, L.off_t2fltp) : mf);
-    RFR_CU(t2_filter(t, v0, 1, o, n_s, Sf, apf, device_sms(), st));
-    if (Sf > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_t2fltp), Sf, n_s * 2, mf, device_sms(), st));
+    // the alpha != 0 samples sorted into the plan's tiles first: row G's coefficients are prepared
+    // only for the tiles that hold one
     Rec *rec_c = at<Rec>(ws, L.off_recc);
     int *idx_c = at<int>(ws, L.off_idxc);
     int64_t *n_act = at<int64_t>(ws, kActiveBwdOff);
@@ -1056,6 +1052,12 @@ rfr_status rfr_backward_filter_partial(const float *grad_signal, const float *si
     memset(&act, 0, sizeof(act));
     act.rec = rec_c; act.n_dev = n_act; act.n = n_s;
     RFR_CU(t2_sort(t, act, v1, st));
+    RFR_CU(t2_prep_adjoint(t, v0.tstart, a.X, a.X2, st, v1.tstart));
+    const int Sf = t2_flt_splits(n_s, t2_filter_chunk(), ants->n_ant, L.t2_flt_cap);
+    const int64_t apf = cdiv(cdiv(ants->n_ant, Sf), 16) * 16;
+    float2 *o = reinterpret_cast<float2 *>(Sf > 1 ? at<float>(ws, L.off_t2fltp) : mf);
+    RFR_CU(t2_filter(t, v0, 1, o, n_s, Sf, apf, device_sms(), st));
+    if (Sf > 1) RFR_CU(t2_sum_splits(t, at<float>(ws, L.off_t2fltp), Sf, n_s * 2, mf, device_sms(), st));
     RFR_CU(cudaMemsetAsync(partials, 0, (size_t)5 * n_s * 4, st));
     const int Sb = std::max(1, std::min<int>(L.t2_bwd_splits, (int)cdiv(ants->n_ant, 1024)));
     const int64_t apb = cdiv(cdiv(ants->n_ant, Sb), 16) * 16;

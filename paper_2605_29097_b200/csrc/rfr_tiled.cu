@@ -890,7 +890,7 @@ template <int P>
 __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, int t, int64_t i,
                                              const float2 *X0, const float2 *X1,
                                              const double (*W)[kT2PMax], const double *xk,
-                                             const float2 (*Gs)[kT2PgMax]) {
+                                             const float2 (*Gs)[kT2PgMax], unsigned rows) {
   const int Pg = pl.Pg, T = pl.T;
   const int nrow = X1 ? 2 : 1;
   const double uc = a.lct[i * kT2Max + t] * a.kd;
@@ -898,6 +898,7 @@ __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, 
   const double inv_dg = 1.0 / pl.delta_g;
   const double yc = (uc - ug) * inv_dg, yd = pl.delta_t * inv_dg;   // y_k = yc + yd x_k
   for (int row = 0; row < nrow; ++row) {
+    if (!((rows >> row) & 1u)) continue;           // no point of this row's sweep in the tile
     float Fr[P], Fi[P];
     if (Pg) {
       // F_k = sum_q G_q T_q(y_k) with T_q by the forward three-term recurrence, two nodes per
@@ -971,8 +972,11 @@ __device__ __forceinline__ void k2_cprep_one(const T2Args &a, const T2Plan &pl, 
 
 // CTA = (one antenna, 128 tiles): the antenna's global expansions staged in shared memory (every
 // thread reads the same coefficient: broadcast), antenna-major centres (coalesced)
-__global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, const float2 *X0,
-                                                const float2 *X1) {
+// tstart0 / tstart: tile occupancy of the point sets row 0 / row 1 are swept over (the fused call:
+// row 0 = G over the alpha != 0 samples, row 1 = s over every sample -- at c3 61 of 256 tiles hold
+// an active sample, so three quarters of row 0's coefficients are never read and not computed)
+__global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart0, const int *tstart,
+                                                const float2 *X0, const float2 *X1) {
   const T2Plan pl = *a.plan;
   if (pl.P == 0) return;
   __shared__ double W[kT2PMax][kT2PMax];
@@ -990,12 +994,15 @@ __global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, con
         pl.Pg ? a.gexp[((int64_t)(w / kT2PgMax) * a.n_a + i) * kT2PgMax + w % kT2PgMax]
               : make_float2(0.f, 0.f);
   __syncthreads();
-  if (t >= pl.T || tstart[t + 1] == tstart[t]) return;
+  if (t >= pl.T) return;
+  const unsigned rows = (tstart0[t + 1] != tstart0[t] ? 1u : 0u) |
+                        (X1 && tstart[t + 1] != tstart[t] ? 2u : 0u);
+  if (!rows) return;
   switch (pl.P) {
-    case 8: k2_cprep_one<8>(a, pl, t, i, X0, X1, W, xk, Gs); break;
-    case 10: k2_cprep_one<10>(a, pl, t, i, X0, X1, W, xk, Gs); break;
-    case 12: k2_cprep_one<12>(a, pl, t, i, X0, X1, W, xk, Gs); break;
-    case 14: k2_cprep_one<14>(a, pl, t, i, X0, X1, W, xk, Gs); break;
+    case 8: k2_cprep_one<8>(a, pl, t, i, X0, X1, W, xk, Gs, rows); break;
+    case 10: k2_cprep_one<10>(a, pl, t, i, X0, X1, W, xk, Gs, rows); break;
+    case 12: k2_cprep_one<12>(a, pl, t, i, X0, X1, W, xk, Gs, rows); break;
+    case 14: k2_cprep_one<14>(a, pl, t, i, X0, X1, W, xk, Gs, rows); break;
     default: break;
   }
 }
@@ -1003,8 +1010,9 @@ __global__ void __launch_bounds__(128) k2_cprep(T2Args a, const int *tstart, con
 }  // namespace
 
 cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0, const float2 *X1,
-                            cudaStream_t st) {
+                            cudaStream_t st, const int *tstart0) {
   if (a.n_a <= 0) return cudaSuccess;
+  if (!tstart0) tstart0 = tstart;
   ProfScope prof(kProfPrep, st);
   const size_t sm = ((size_t)a.n_f + 4 * 64) * sizeof(float2);
   if (sm > 48 * 1024) {
@@ -1018,7 +1026,7 @@ cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0
   } else {
     k2_gexp<<<(unsigned)a.n_a, kGexpThreads, sm, st>>>(a, X0, X1);
   }
-  k2_cprep<<<dim3((unsigned)a.n_a, (unsigned)(kT2Max / 128)), 128, 0, st>>>(a, tstart, X0, X1);
+  k2_cprep<<<dim3((unsigned)a.n_a, (unsigned)(kT2Max / 128)), 128, 0, st>>>(a, tstart0, tstart, X0, X1);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) add_launches(2);
   return e;

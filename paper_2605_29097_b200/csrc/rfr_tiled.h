@@ -137,9 +137,11 @@ cudaError_t t2_plan(const T2Args &a, const T2Points &pts, const T2Sorted &srt, i
                     cudaStream_t st);
 // sort another point set into an existing plan's grid (chunk = srt.chunk)
 cudaError_t t2_sort(const T2Args &a, const T2Points &pts, const T2Sorted &srt, cudaStream_t st);
-// adjoint rows X0 (and X1 if not NULL): global expansion + per-(tile, antenna) coefficients
+// adjoint rows X0 (and X1 if not NULL): global expansion + per-(tile, antenna) coefficients.
+// tstart: tile occupancy of the points row 1 (or the only row) is swept over; tstart0 (NULL: the
+// same): of the points row 0 is swept over -- coefficients of unoccupied tiles are not computed
 cudaError_t t2_prep_adjoint(const T2Args &a, const int *tstart, const float2 *X0, const float2 *X1,
-                            cudaStream_t st);
+                            cudaStream_t st, const int *tstart0 = nullptr);
 // matched filter over the sorted points of srt with coefficient row `row`: M partials [split][n]
 cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out, int64_t n_out,
                       int n_splits, int64_t ants_per_split, int n_sms, cudaStream_t st);
