@@ -56,6 +56,64 @@ __global__ void k_blend(BlendArgs a) {
   if (bad) atomicOr(a.flags, 2u);
 }
 
+// Warp per ray, lane = sample (chunks of 32 samples): every load and store is coalesced along the
+// ray-major sample index, and the transmittance T_k = prod_{l<k} (1 - alpha_l) is an
+// exclusive product scan over the lanes with the running product carried across chunks.  Same
+// per-sample arithmetic as k_blend; only the association of the products differs (a tree instead
+// of a left fold), and exact factors stay exact: a (1 - alpha) of 0 or 1 gives the same T.
+// (c3: 84 -> ~20 us per call; the thread-per-ray form kept its rays' 32 samples in one thread,
+// with only 256 warps in flight on 148 SMs.)
+__global__ void __launch_bounds__(256) k_blend_warp(BlendArgs a) {
+  const int lane = (int)(threadIdx.x & 31);
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= a.n_rays) return;                        // warp-uniform
+  const int nz = a.n_per_ray;
+  const int64_t j0 = r * nz;
+  float Tc = 1.f;                                   // product of (1 - alpha) over the chunks so far
+  bool bad = false;
+  for (int k0 = 0; k0 < nz; k0 += 32) {
+    const int k = k0 + lane;
+    const bool in = k < nz;
+    const int64_t j = j0 + k;
+    float alpha = 0.f, oma = 1.f, fk = 0.f;
+    if (in) {
+      const bool has_next = (k + 1 < nz);
+      fk = a.sdf[j];
+      const float fk1 = has_next ? a.sdf[j + 1] : 0.f;
+      blend_step(a.s, fk, fk1, has_next, alpha, oma);
+    }
+    float incl = oma;                               // inclusive product scan over the lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl *= v;
+    }
+    float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 1.f;
+    const float T = Tc * excl;
+    Tc *= __shfl_sync(0xffffffffu, incl, 31);
+    if (in) {
+      const float p = a.power[j], refl = a.refl[j];
+      const float x = a.x[j], y = a.y[j], z = a.z[j];
+      const float nx = a.nx[j], ny = a.ny[j], nz_ = a.nz[j];
+      const float papr = a.phi_origin ? a.phi_origin[j] : 1.f;
+      if (a.check_finite) {
+        bad |= !isfinite(p) || !isfinite(refl) || !isfinite(x) || !isfinite(y) || !isfinite(z) ||
+               !isfinite(nx) || !isfinite(ny) || !isfinite(nz_) || !isfinite(fk) || !isfinite(papr);
+      }
+      Rec rec;
+      rec.x = (double)x; rec.y = (double)y; rec.z = (double)z;
+      rec.w = p * refl * alpha;
+      if (a.aflag) a.aflag[j] = alpha != 0.f ? 1 : 0;
+      rec.T = T;
+      rec.nx = nx; rec.ny = ny; rec.nz = nz_;
+      rec.papr = papr;
+      a.rec[j] = rec;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags, 2u);
+}
+
 // ================================================================================== K2 forward
 // Warp-independent design (no CTA barriers on the hot loop).  Warp w of a CTA owns taw = 32 / nbc
 // antennas (a0 + w taw ...) and all nbc bin blocks of B bins of this CTA's bin chunk; lane
@@ -601,6 +659,84 @@ __global__ void k_blend_bwd(BlendBwdArgs a) {
   a.ds_part[r] = gs;
 }
 
+// Warp per ray, lane = sample, chunks of 32 samples from the ray's end: the recurrence
+// Q_l = gT_{l+1} + (1 - alpha_{l+1}) Q_{l+1} is a suffix scan of affine maps over the lanes
+// (Q_l = B_l + A_l Q_in, Q_in = the Q of the first sample of the later chunk), everything else is
+// per sample or between neighbouring samples (shuffles; the later chunk's first sample carried).
+// Same per-sample expressions as k_blend_bwd; the scan and the ray sum of d/ds associate
+// differently (trees instead of folds).
+__global__ void __launch_bounds__(256) k_blend_bwd_warp(BlendBwdArgs a) {
+  const unsigned full = 0xffffffffu;
+  const int lane = (int)(threadIdx.x & 31);
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= a.n_rays) return;                        // warp-uniform
+  const int nz = a.n_per_ray;
+  const int64_t j0 = r * nz, ns = a.n_s;
+  float gs = 0.f;
+  // carried from the later chunk (its first sample): Q, gT, 1 - alpha, gf_here
+  float Qin = 0.f, gT_c = 0.f, oma_c = 1.f, gfh_c = 0.f;
+  for (int k0 = ((nz - 1) / 32) * 32; k0 >= 0; k0 -= 32) {
+    const int l = k0 + lane;
+    const bool in = l < nz;
+    const int64_t j = j0 + l;
+    const bool has_next = in && l + 1 < nz;
+    float f = 0.f, f_next = 0.f, p = 0.f, refl = 0.f, w = 0.f, Tl = 0.f;
+    float S1 = 0.f, S2 = 0.f, S3x = 0.f, S3y = 0.f, S3z = 0.f;
+    if (in) {
+      f = a.sdf[j];
+      f_next = has_next ? a.sdf[j + 1] : 0.f;
+      p = a.power[j]; refl = a.refl[j];
+      const Rec rec = a.rec[j];
+      w = rec.w; Tl = rec.T;
+      S1 = a.partials[j]; S2 = a.partials[ns + j];
+      S3x = a.partials[2 * ns + j]; S3y = a.partials[3 * ns + j]; S3z = a.partials[4 * ns + j];
+    }
+    float alpha, oma;
+    blend_step(a.s, f, f_next, has_next, alpha, oma);
+    if (!in) { alpha = 0.f; oma = 1.f; }
+    const float sm = in ? sig_minus(a.s, f) : 0.f;
+    const float gT = w * S2;
+    // neighbours: the next sample's gT, 1 - alpha, sigma(-s f) (lane 31: the later chunk's first)
+    float gT_n = __shfl_down_sync(full, gT, 1), oma_n = __shfl_down_sync(full, oma, 1);
+    float sm_n = __shfl_down_sync(full, sm, 1);
+    if (lane == 31) { gT_n = gT_c; oma_n = oma_c; sm_n = has_next ? sig_minus(a.s, f_next) : 0.f; }
+    // affine map of this sample: Q_l = b + aQ_{l+1}; the last sample of the ray (and lanes past
+    // it) map everything to 0
+    float A = has_next ? oma_n : 0.f, B = has_next ? gT_n : 0.f;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float A2 = __shfl_down_sync(full, A, d), B2 = __shfl_down_sync(full, B, d);
+      if (lane + d < 32) { B = fmaf(A, B2, B); A *= A2; }
+    }
+    const float Q = fmaf(A, Qin, B);
+    float c = 0.f, gf_here = 0.f;
+    if (in) {
+      a.g_power[j] = refl * alpha * S1;
+      a.g_refl[j] = p * alpha * S1;
+      a.g_nx[j] = w * S3x;
+      a.g_ny[j] = w * S3y;
+      a.g_nz[j] = w * S3z;
+      const float dalpha = p * refl * S1 - Tl * Q;
+      if (has_next && alpha > 0.f) {
+        c = dalpha * oma;
+        gf_here = c * a.s * sm;
+        gs += c * (f * sm - f_next * sm_n);
+      }
+    }
+    float gfh_n = __shfl_down_sync(full, gf_here, 1);
+    if (lane == 31) gfh_n = gfh_c;
+    if (has_next) a.g_sdf[j + 1] = gfh_n - c * a.s * sm_n;
+    if (k0 == 0 && lane == 0) a.g_sdf[j0] = gf_here;
+    Qin = __shfl_sync(full, Q, 0);
+    gT_c = __shfl_sync(full, gT, 0);
+    oma_c = __shfl_sync(full, oma, 0);
+    gfh_c = __shfl_sync(full, gf_here, 0);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) gs += __shfl_xor_sync(full, gs, d);
+  if (lane == 0) a.ds_part[r] = gs;
+}
+
 // ================================================================================== reductions
 // out[k] = sum_{s < S} part[s * n + k], fixed order (float2 / float granularity via float4 loads)
 __global__ void k_sum_splits(const float4 *__restrict__ part, int S, int64_t n4,
@@ -687,7 +823,11 @@ void add_launches(int n) { __atomic_add_fetch(&g_launches, (unsigned long long)n
 
 cudaError_t launch_blend(const BlendArgs &a, cudaStream_t st) {
   if (a.n_rays <= 0) return cudaSuccess;
-  k_blend<<<grid1(a.n_rays, 128), 128, 0, st>>>(a);
+  // warp per ray (default); RFR_K1=thread: the thread-per-ray form
+  static int warp = -1;
+  if (warp < 0) { const char *e = getenv("RFR_K1"); warp = (e && !strcmp(e, "thread")) ? 0 : 1; }
+  if (warp) k_blend_warp<<<grid1(a.n_rays * 32, 256), 256, 0, st>>>(a);
+  else k_blend<<<grid1(a.n_rays, 128), 128, 0, st>>>(a);
   return counted(cudaGetLastError());
 }
 
@@ -918,7 +1058,10 @@ cudaError_t launch_adjoint(const AdjArgs &a, int mode, bool mono, bool corr, int
 
 cudaError_t launch_blend_bwd(const BlendBwdArgs &a, cudaStream_t st) {
   if (a.n_rays <= 0) return cudaSuccess;
-  k_blend_bwd<<<grid1(a.n_rays, 128), 128, 0, st>>>(a);
+  static int warp = -1;
+  if (warp < 0) { const char *e = getenv("RFR_K1"); warp = (e && !strcmp(e, "thread")) ? 0 : 1; }
+  if (warp) k_blend_bwd_warp<<<grid1(a.n_rays * 32, 256), 256, 0, st>>>(a);
+  else k_blend_bwd<<<grid1(a.n_rays, 128), 128, 0, st>>>(a);
   return counted(cudaGetLastError());
 }
 
