@@ -275,6 +275,21 @@ def test_edge_one_sample_per_ray_and_many_rays():
     assert rel(c64(out), oracle.forward(S, s, A, grid)) <= TOL_SIG
 
 
+@pytest.mark.parametrize("n_per_ray", [31, 32, 33, 64, 70])
+def test_edge_long_rays_blend_scans(n_per_ray):
+    """K1 / K1' run one warp per ray in chunks of 32 samples (transmittance by a product scan, the
+    reverse recurrence Q_l = gT_{l+1} + (1 - alpha_{l+1}) Q_{l+1} by a suffix scan, both carried
+    across chunks): rays shorter than, equal to and longer than a chunk, with a ragged last chunk,
+    on dense alpha (s f ~ +-2: every sample blends), against O1 / O6 (App. A.5)."""
+    S, A, grid, s = _tiny(n_rays=9, n_per_ray=n_per_ray, n_ant=6, n_freq=24, seed=n_per_ray)
+    out, _ = gpu_forward(S, A, grid, s)
+    assert rel(c64(out), oracle.forward(S, s, A, grid)) <= TOL_SIG
+    G = (np.random.default_rng(5).standard_normal((A.n, grid.n_freq, 2)) @ [1, 1j]).astype(np.complex64)
+    g_gpu, _ = gpu_backward(G, S, A, grid, s)
+    g_ref = oracle.backward(G.astype(np.complex128), S, s, A, grid)
+    check_grads(g_gpu, g_ref, what=f"n_per_ray={n_per_ray}")
+
+
 def test_domain_and_finite_flags():
     m = rfr()
     S, A, grid, s = _tiny()

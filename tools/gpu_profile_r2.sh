@@ -24,4 +24,7 @@ for k in ${NCU_KERNELS:-k2_filter k2_bwd k2_fwd k2_fout k2_cprep}; do
     -o $OUT/$k $CMD > $OUT/ncu_$k.log 2>&1
   echo "ncu $k rc=$?" >> $OUT/ncu_$k.log
   ncu -i $OUT/$k.ncu-rep --page source --csv --print-source sass > $OUT/${k}_source.csv 2>/dev/null
+  # summaries written on the box; only the filter's report travels back (gpurun_out/ is capped at 64 MiB)
+  (python tools/ncu_summary.py $OUT/$k.ncu-rep; python tools/sass_mix.py $OUT/${k}_source.csv) > $OUT/${k}_summary.txt 2>&1
+  [ "$k" = "k2_filter" ] || rm -f $OUT/$k.ncu-rep
 done
