@@ -151,7 +151,7 @@ struct Layout {
          off_t2mom = 0, off_t2bwdp = 0, off_t2lct = 0, off_t2tcimg = 0, off_t2mg = 0,
          off_t2fltp = 0;
   int t2_flt_cap = 1;               // antenna splits the r2 filter's partial buffer holds
-  size_t off_t2v[2][7] = {};        // per view: tstart+cstart+n_items, perm, pos, aux, bcnt
+  size_t off_t2v[2][7] = {};        // per view: tstart+cstart+n_items+torder+n_occ, perm, pos, aux, bcnt
   size_t off_gsig = 0, off_gant = 0; // rfr_filter_gather: gathered signal rows and positions
   int t2_bwd_splits = 1;
   size_t cap_trs = 0, cap_tfp = 0;
@@ -165,7 +165,9 @@ struct Layout {
 // split, at most `cap`, and the partials [S][n] within 1 GiB
 int t2_flt_splits(int64_t n_pts, int chunk, int64_t n_a, int cap) {
   const int64_t items = std::max<int64_t>(1, cdiv(n_pts, chunk));
-  int64_t s = cdiv((int64_t)device_sms() * 5 * 24, items);
+  static int per_slot = -1;                         // items per resident CTA slot (A/B: RFR_T2SPL)
+  if (per_slot < 0) { const char *e = getenv("RFR_T2SPL"); per_slot = e ? std::max(1, atoi(e)) : 24; }
+  int64_t s = cdiv((int64_t)device_sms() * 5 * per_slot, items);
   s = std::min<int64_t>(s, std::max<int64_t>(1, cdiv(n_a, 64)));
   s = std::min<int64_t>(s, std::max<int64_t>(1, (int64_t(1) << 30) / (std::max<int64_t>(n_pts, 1) * 8)));
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, cap));
@@ -260,7 +262,7 @@ bool make_layout(int64_t n_s, int64_t n_a, int32_t n_f, int64_t n_q, Layout &L) 
     L.off_gant = take((size_t)3 * na1 * 4);
     const int64_t nb = (np + kT2SortBlock - 1) / kT2SortBlock;
     for (int v = 0; v < 2; ++v) {
-      L.off_t2v[v][0] = take((size_t)(2 * (kT2Max + 1) + 1) * 4);
+      L.off_t2v[v][0] = take((size_t)(3 * (kT2Max + 1) + 1) * 4);
       L.off_t2v[v][1] = take((size_t)np * 4);
       L.off_t2v[v][2] = take((size_t)np * 16);
       L.off_t2v[v][3] = take((size_t)np * 16);
@@ -462,6 +464,8 @@ T2Sorted make_view(const rfr_workspace *ws, const Layout &L, int v, int chunk) {
   s.tstart = at<int>(ws, L.off_t2v[v][0]);
   s.cstart = s.tstart + kT2Max + 1;
   s.n_items = s.cstart + kT2Max + 1;
+  s.torder = s.n_items + 1;
+  s.n_occ = s.torder + kT2Max;
   s.chunk = chunk;
   s.perm = at<int>(ws, L.off_t2v[v][1]);
   s.pos = at<float4>(ws, L.off_t2v[v][2]);

@@ -1243,7 +1243,7 @@ __device__ __forceinline__ void t2_horner2(const float2 *cs, f2x x, f2x &h0, f2x
 // work item = (two units of kT2FltChunk / 2 tile-sorted points, antenna split, t2_item); thread =
 // 4 points of its warp's segment (lane + 32 u)
 // GM: geometry of the filter: 0 = t2_geo2 unreduced angle, 1 = t2_geo2 reduced, 2 = t2_geo1
-template <int P, int GM, int NPAIR, int UNR, int GA>
+template <int P, int GM, int NPAIR, int UNR, int GA, bool DYN>
 __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                                int row, float2 *__restrict__ out, int64_t n_out,
                                                int n_splits, int64_t aps, AdjStageT<GA> &sm) {
@@ -1254,7 +1254,18 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
   const float4 *fgeo = GM == 2 ? a.tgeof : a.tgeo;  // t2_geo1 reads its own image (k2_geofix)
   const float kangf = (float)(-2.0 * kPi * a.kc), kxf = (float)(-pl.inv_t);   // t2_geo1m
   const int lane = (int)(threadIdx.x & 31);
-  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+  // DYN: work items fetched from a device counter (plan->ctr[0], zeroed before the launch) instead
+  // of the static stride -- a CTA that runs ahead takes more items; every item still writes its
+  // own outputs, so the result does not depend on who ran it
+  __shared__ int w_next;
+  int w = blockIdx.x;
+  if (DYN) {
+    if (threadIdx.x == 0) w_next = (int)atomicAdd(&a.plan->ctr[0], 1u);
+    __syncthreads();
+    w = w_next;
+    __syncthreads();                               // read before thread 0 fetches the next item
+  }
+  while (w < total) {
     const int item = w / n_splits, split = w % n_splits;
     const T2Item it = t2_item(s, pl.T, item, 32 * SPT);
     const int64_t base = it.base + lane, end = it.end;
@@ -1282,7 +1293,10 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
 #pragma unroll
     for (int u = 0; u < SPT; ++u) { A1[u] = 0ull; A2[u] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
+    if (DYN && threadIdx.x == 0) w_next = (int)atomicAdd(&a.plan->ctr[0], 1u);   // the next item
     __syncthreads();                               // the previous item's stages are consumed
+    const int wn = DYN ? w_next : w + (int)gridDim.x;
+    if (DYN && i_lo >= i_hi) __syncthreads();      // (no stage barrier below: order the read of w_next)
     if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)GA, i_hi - i_lo), sm, 0, fgeo);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += GA, b ^= 1) {
@@ -1352,10 +1366,11 @@ __device__ __forceinline__ void k2_filter_body(const T2Args &a, const T2Plan &pl
         const float2 p1 = upk(A1[u]), p2 = upk(A2[u]);   // M = A1 + j A2
         o[s.perm[base + u * 32]] = make_float2(p1.x - p2.y, p1.y + p2.x);
       }
+    w = wn;
   }
 }
 
-template <int MINB, int GM, int NPAIR, int UNR = 1, int GA = kT2GA>
+template <int MINB, int GM, int NPAIR, int UNR = 1, int GA = kT2GA, bool DYN = false>
 __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int row,
                                                        float2 *__restrict__ out, int64_t n_out,
                                                        int n_splits, int64_t aps) {
@@ -1363,10 +1378,10 @@ __global__ void __launch_bounds__(128, MINB) k2_filter(T2Args a, T2Sorted s, int
   __shared__ __align__(16) AdjStageT<GA> sm;
   t2_stage_init(sm);
   switch (pl.P) {
-    case 8: k2_filter_body<8, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 10: k2_filter_body<10, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 12: k2_filter_body<12, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
-    case 14: k2_filter_body<14, GM, NPAIR, UNR, GA>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 8: k2_filter_body<8, GM, NPAIR, UNR, GA, DYN>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 10: k2_filter_body<10, GM, NPAIR, UNR, GA, DYN>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 12: k2_filter_body<12, GM, NPAIR, UNR, GA, DYN>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
+    case 14: k2_filter_body<14, GM, NPAIR, UNR, GA, DYN>(a, pl, s, row, out, n_out, n_splits, aps, sm); break;
     default: break;
   }
 }
@@ -1386,7 +1401,18 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
   unsigned ph = 0u;                                // mbarrier phase bits of the stage buffers
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   const int lane = (int)(threadIdx.x & 31);
-  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+  // work items from the device counter plan->ctr[2] (zeroed before the launch) when there are at
+  // least 8 per CTA, else the static stride (as in the filter and the forward)
+  const bool dynf = a.dyn && total >= 8 * (int)gridDim.x;
+  __shared__ int w_next;
+  int w = blockIdx.x;
+  if (dynf) {
+    if (threadIdx.x == 0) w_next = (int)atomicAdd(&a.plan->ctr[2], 1u);
+    __syncthreads();
+    w = w_next;
+    __syncthreads();                               // read before thread 0 fetches the next item
+  }
+  while (w < total) {
     const int item = w / n_splits, split = w % n_splits;
     const T2Item it = t2_item(s, pl.T, item, 32 * SPT);
     const int64_t base = it.base + lane, end = it.end;
@@ -1422,7 +1448,10 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
 #pragma unroll
     for (int pp = 0; pp < NPAIR; ++pp) { U[pp] = SF[pp] = Wx[pp] = Wy[pp] = Wz[pp] = 0ull; }
     const int64_t i_lo = (int64_t)split * aps, i_hi = min(a.n_a, i_lo + aps);
+    if (dynf && threadIdx.x == 0) w_next = (int)atomicAdd(&a.plan->ctr[2], 1u);   // the next item
     __syncthreads();                               // the previous item's stages are consumed
+    const int wn = dynf ? w_next : w + (int)gridDim.x;
+    if (dynf && i_lo >= i_hi) __syncthreads();     // (no stage barrier below: order the read of w_next)
     if (i_lo < i_hi) t2_stage_issue<P>(a, pl, row, it, i_lo, (int)min((int64_t)kT2GA, i_hi - i_lo), sm, 0, a.tgeo);
     int b = 0;
     for (int64_t i0 = i_lo; i0 < i_hi; i0 += kT2GA, b ^= 1) {
@@ -1501,6 +1530,7 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
         o[4 * n_out + j] = f4 * fmaf(h ? qzv.y : qzv.x, SFu, 0.5f * (h ? Wzv.y : Wzv.x));
       }
     }
+    w = wn;
   }
 }
 
@@ -1555,16 +1585,58 @@ __device__ __forceinline__ f2x ld2(const float *p) {
   return pk(v.x, v.y);
 }
 
-template <int P, int KIND, int RP>
+// occupied tiles by record count, largest first (ties by tile index): the order the forward's
+// dynamic scheduler hands tiles out in (longest items first, so the sweep's tail is made of the
+// smallest tiles); 1 CTA of kT2Max threads, rank by counting
+__global__ void __launch_bounds__(kT2Max) k2_order(const T2Plan *plp, T2Sorted s) {
+  __shared__ int cnt[kT2Max];
+  const int T = plp->T, t = (int)threadIdx.x;
+  const int n = (plp->P != 0 && t < T) ? s.tstart[t + 1] - s.tstart[t] : 0;
+  cnt[t] = n;
+  __syncthreads();
+  if (n > 0) {
+    int r = 0;
+    for (int u = 0; u < T; ++u) {
+      const int m = cnt[u];
+      r += (m > n) || (m == n && u < t);
+    }
+    s.torder[r] = t;
+  }
+  const int occ = __syncthreads_count(n > 0);
+  if (t == 0) *s.n_occ = occ;
+}
+
+// DYN: work items (occupied tile in k2_order's order, antenna block) fetched from the device
+// counter plan->ctr[1] (zeroed before the launch); else the static stride over (tile, block)
+template <int P, int KIND, int RP, bool DYN>
 __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, const T2Sorted &s,
                                             bool no_gain, FwdStage &sm) {
   const int nab = (int)((a.n_a + kT2FwdAnts - 1) / kT2FwdAnts);
-  const int total = pl.T * nab;
+  // (with few items per CTA the static stride in tile order balances better -- one rank's share at
+  // N = 8, r4s: 0.51 vs 0.60 ms -- so the counter is used from 8 items per CTA on)
+  const int n_dyn = DYN ? *s.n_occ * nab : 0;
+  const bool dynf = DYN && n_dyn >= 8 * (int)gridDim.x;
+  const int total = dynf ? n_dyn : pl.T * nab;
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
-  for (int w = blockIdx.x; w < total; w += gridDim.x) {
-    const int t = w / nab, ab = w % nab;
+  __shared__ int w_next;
+  int w = blockIdx.x;
+  if (dynf) {
+    if (threadIdx.x == 0) w_next = (int)atomicAdd(&a.plan->ctr[1], 1u);
+    __syncthreads();
+    w = w_next;
+    __syncthreads();                                // read before thread 0 fetches the next item
+  }
+  while (w < total) {
+    if (dynf && threadIdx.x == 0) w_next = (int)atomicAdd(&a.plan->ctr[1], 1u);   // the next item
+    int wn = w + (int)gridDim.x;
+    const int t = dynf ? s.torder[w / nab] : w / nab, ab = w % nab;
     const int64_t j_lo = s.tstart[t], j_hi = s.tstart[t + 1];
-    if (j_hi == j_lo) continue;
+    if (j_hi == j_lo) {                             // (static stride only: DYN lists occupied tiles)
+      if (dynf) __syncthreads();
+      w = dynf ? w_next : wn;
+      if (dynf) __syncthreads();
+      continue;
+    }
     const int64_t i = (int64_t)ab * kT2FwdAnts + threadIdx.x;
     const bool ok = i < a.n_a;
     const float *tb = a.tbox + t * 6;
@@ -1603,6 +1675,7 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
         }
       }
       __syncthreads();
+      if (dynf && jt == j_lo) wn = w_next;                   // (ordered by this barrier and the item's last)
       const int64_t jn = jt + kT2FwdTJ + threadIdx.x;       // prefetch the next stage
       pv = make_float4(cx, cy, cz, 0.f);
       pn = make_float4(0.f, 0.f, 1.f, 0.f);
@@ -1681,18 +1754,19 @@ __device__ __forceinline__ void k2_fwd_body(const T2Args &a, const T2Plan &pl, c
         dst[p] = v;
       }
     }
+    w = wn;
   }
 }
 
-template <int KIND, int RP, int MINB>
+template <int KIND, int RP, int MINB, bool DYN = false>
 __global__ void __launch_bounds__(kT2FwdAnts, MINB) k2_fwd(T2Args a, T2Sorted s, bool no_gain) {
   const T2Plan pl = *a.plan;
   __shared__ FwdStage sm;
   switch (pl.P) {
-    case 8: k2_fwd_body<8, KIND, RP>(a, pl, s, no_gain, sm); break;
-    case 10: k2_fwd_body<10, KIND, RP>(a, pl, s, no_gain, sm); break;
-    case 12: k2_fwd_body<12, KIND, RP>(a, pl, s, no_gain, sm); break;
-    case 14: k2_fwd_body<14, KIND, RP>(a, pl, s, no_gain, sm); break;
+    case 8: k2_fwd_body<8, KIND, RP, DYN>(a, pl, s, no_gain, sm); break;
+    case 10: k2_fwd_body<10, KIND, RP, DYN>(a, pl, s, no_gain, sm); break;
+    case 12: k2_fwd_body<12, KIND, RP, DYN>(a, pl, s, no_gain, sm); break;
+    case 14: k2_fwd_body<14, KIND, RP, DYN>(a, pl, s, no_gain, sm); break;
     default: break;
   }
 }
@@ -1976,7 +2050,8 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     if (r && r[0] == '1') gm = 1;
     if (gm < 0 || gm > 3) gm = 2;
   }
-  // launch-shape variants (RFR_T2FV).  Default pf64: stages of 64 antennas (half the per-stage CTA
+  // launch-shape variants (RFR_T2FV).  Default dyn = pf64 with the work items fetched from a device
+  // counter instead of the static stride (r4q: 22.22 -> 21.71 ms).  pf64: stages of 64 antennas (half the per-stage CTA
   // barriers) and the next antenna's geometry words loaded before this antenna's Horner (r4c/r4d at
   // c3: base 22.96 ms, g64 22.8, pf 22.3, pf64 22.17).  A/B: base, g64, pf; m4 = 4 CTAs per SM (128
   // registers), u2 = the antenna loop unrolled by 2 (two antennas' independent work in one
@@ -1984,8 +2059,8 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
   static int fv = -1;
   if (fv < 0) {
     const char *e = getenv("RFR_T2FV");
-    fv = !e ? 7 : !strcmp(e, "base") ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3
-       : !strcmp(e, "m6") ? 4 : !strcmp(e, "g64") ? 5 : !strcmp(e, "pf") ? 6 : !strcmp(e, "pf64") ? 7 : 0;
+    fv = !e ? 8 : !strcmp(e, "base") ? 0 : !strcmp(e, "m4") ? 1 : !strcmp(e, "u2") ? 2 : !strcmp(e, "m4u2") ? 3
+       : !strcmp(e, "m6") ? 4 : !strcmp(e, "g64") ? 5 : !strcmp(e, "pf") ? 6 : !strcmp(e, "pf64") ? 7 : !strcmp(e, "dyn") ? 8 : 0;
   }
   const unsigned g5 = (unsigned)(n_sms * 5), g4 = (unsigned)(n_sms * 4), g3 = (unsigned)(n_sms * 3);
   if (srt.chunk == 8 * 128) {
@@ -2012,6 +2087,15 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
     k2_filter<5, 2, 2, 1, 64><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 6) {
     k2_filter<5, 2, 2, 3><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+  } else if (gm == 2 && fv == 8) {
+    // pf64 with the work items fetched from a device counter (A/B: RFR_T2FV=dyn)
+    static bool once = false;
+    if (!once) {
+      cudaFuncSetAttribute(k2_filter<5, 2, 2, 3, 64, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      once = true;
+    }
+    cudaMemsetAsync(reinterpret_cast<char *>(a.plan) + offsetof(T2Plan, ctr), 0, sizeof(unsigned), st);
+    k2_filter<5, 2, 2, 3, 64, true><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 7) {
     static bool once = false;
     if (!once) {
@@ -2040,10 +2124,12 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
   return e;
 }
 
-cudaError_t t2_backward(const T2Args &a, const T2Sorted &srt, int row, const int *idx,
+cudaError_t t2_backward(const T2Args &a_in, const T2Sorted &srt, int row, const int *idx,
                         const int64_t *n_dev, int64_t n_c, float *part, float *out, int64_t n_s,
                         int n_splits, int64_t ants_per_split, bool no_gain, int n_sms,
                         cudaStream_t st) {
+  T2Args a = a_in;
+  a.dyn = 0;
   if (a.n_a <= 0 || n_c <= 0) return cudaSuccess;
   {
     ProfScope prof(kProfBackward, st);
@@ -2051,6 +2137,12 @@ cudaError_t t2_backward(const T2Args &a, const T2Sorted &srt, int row, const int
     // 2.56 ms, dense 15.89 / 15.59 / 15.56)
     static int bv = -1;
     if (bv < 0) { const char *e = getenv("RFR_T2BV"); bv = e ? atoi(e) : 6; }   // r2w: 6 fastest
+    static int dyn = -1;                           // RFR_T2BDYN=0: static stride
+    if (dyn < 0) { const char *e = getenv("RFR_T2BDYN"); dyn = (e && e[0] == '0') ? 0 : 1; }
+    a.dyn = dyn;
+    if (dyn)
+      cudaMemsetAsync(reinterpret_cast<char *>(a.plan) + offsetof(T2Plan, ctr) + 2 * sizeof(unsigned),
+                      0, sizeof(unsigned), st);
     if (srt.chunk == 4 * 128)
       k2_bwd<3, 2><<<(unsigned)(n_sms * 3), 128, 0, st>>>(a, srt, row, part, n_c, n_splits,
                                                           ants_per_split, no_gain);
@@ -2083,7 +2175,22 @@ cudaError_t t2_forward(const T2Args &a, const T2Sorted &srt, int kind, bool no_g
   // record pair per iteration at 5 / 6 CTAs per SM (A/B)
   static int fm = -1;
   if (fm < 0) { const char *e = getenv("RFR_T2FWM"); fm = e ? atoi(e) : 4; }
-  if (kind == kFwdTrace) {
+  // dynamic scheduling (default; RFR_T2FDYN=0: the static stride): occupied tiles largest first,
+  // (tile, antenna block) items fetched from a device counter
+  static int dyn = -1;
+  if (dyn < 0) { const char *e = getenv("RFR_T2FDYN"); dyn = (e && e[0] == '0') ? 0 : 1; }
+  // (from 64 antenna blocks on: with fewer -- a rank's share at N = 4, 8 -- the items per CTA are too
+  // few for the counter to pay, and the plain static kernel is the faster one, r4t)
+  if (dyn && rp == 2 && fm == 4 && a.n_a >= 64 * kT2FwdAnts) {
+    k2_order<<<1, kT2Max, 0, st>>>(a.plan, srt);
+    cudaMemsetAsync(reinterpret_cast<char *>(a.plan) + offsetof(T2Plan, ctr) + sizeof(unsigned), 0,
+                    sizeof(unsigned), st);
+    if (kind == kFwdTrace)
+      k2_fwd<kFwdTrace, 2, 4, true><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    else
+      k2_fwd<kFwdMFAdj, 2, 4, true><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
+    add_launches(1);
+  } else if (kind == kFwdTrace) {
     if (fm == 5) k2_fwd<kFwdTrace, 1, 5><<<(unsigned)(n_sms * 5), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else if (fm == 6) k2_fwd<kFwdTrace, 1, 6><<<(unsigned)(n_sms * 6), kT2FwdAnts, 0, st>>>(a, srt, no_gain);
     else if (rp == 2 && fm == 4) k2_fwd<kFwdTrace, 2, 4><<<(unsigned)(n_sms * 4), kT2FwdAnts, 0, st>>>(a, srt, no_gain);

@@ -50,13 +50,17 @@ struct T2Plan {
   unsigned long long dmax_bits;        // atomicMax scratch (fp64 bits): tile half-spread (m)
   unsigned long long gmax_bits;        // global half-spread (m)
   unsigned long long umin_bits;        // atomicMin: closest (tile box, antenna) distance (m)
+  unsigned ctr[4];                     // work counters of the persistent sweeps (zeroed per launch)
 };
+static_assert(sizeof(T2Plan) <= 256, "the plan header region is 256 bytes");
 
 // a sorted view of a point set in a plan's grid (sort output)
 struct T2Sorted {
   int *tstart;                         // [kT2Max + 1] first sorted position of each tile
   int *cstart;                         // [kT2Max + 1] first work item of each tile
   int *n_items;                        // device: work items (chunks) of the sweep
+  int *torder;                         // [kT2Max] occupied tiles, most points first (k2_order)
+  int *n_occ;                          // device: occupied tiles
   int chunk;                           // points per work item
   int *perm;                           // [n] sorted position -> source index
   float4 *pos;                         // [n] sorted positions (x, y, z, w)
@@ -85,6 +89,7 @@ struct T2Args {
   double *lct;                         // [n_a][kT2Max] the same, antenna-major (k2_fout)
   float4 *tgeo;                        // [kT2Max][n_a][2] tile-relative geometry
   float4 *tgeof;                       // [kT2Max][n_a][2] the filter's image of it (k2_geofix)
+  int dyn;                             // backward sweep: work items from plan->ctr[2]
   double *lg;                          // [n_a][3]: global centre, min / max tile centre (m)
   float2 *acoef;                       // global a[m][q]: [kT2PgMax][n_f] (q-major), then [n_f][kT2PgMax]
   double *tabs;                        // [4][kT2PMax][kT2PMax] nodes, W (nodes -> monomial), lambda
