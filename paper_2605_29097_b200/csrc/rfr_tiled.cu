@@ -2095,7 +2095,9 @@ cudaError_t t2_filter(const T2Args &a, const T2Sorted &srt, int row, float2 *out
       once = true;
     }
     cudaMemsetAsync(reinterpret_cast<char *>(a.plan) + offsetof(T2Plan, ctr), 0, sizeof(unsigned), st);
-    k2_filter<5, 2, 2, 3, 64, true><<<g5, 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
+    static int cps = -1;                           // CTAs per SM of the grid (A/B: RFR_T2CPS)
+    if (cps < 0) { const char *e = getenv("RFR_T2CPS"); cps = e ? std::max(1, atoi(e)) : 5; }
+    k2_filter<5, 2, 2, 3, 64, true><<<(unsigned)(n_sms * cps), 128, 0, st>>>(a, srt, row, out, n_out, n_splits, ants_per_split);
   } else if (gm == 2 && fv == 7) {
     static bool once = false;
     if (!once) {
