@@ -1402,8 +1402,8 @@ __device__ __forceinline__ void k2_bwd_body(const T2Args &a, const T2Plan &pl, c
   const float kc2f = (float)(2.0 * a.kc), inv2f = (float)(2.0 * pl.inv_t);
   const int lane = (int)(threadIdx.x & 31);
   // work items from the device counter plan->ctr[2] (zeroed before the launch) when there are at
-  // least 8 per CTA, else the static stride (as in the filter and the forward)
-  const bool dynf = a.dyn && total >= 8 * (int)gridDim.x;
+  // least a.dyn (2; RFR_T2BDYN, r4x) per CTA, else the static stride (as in the filter and the forward)
+  const bool dynf = a.dyn > 0 && total >= a.dyn * (int)gridDim.x;
   __shared__ int w_next;
   int w = blockIdx.x;
   if (dynf) {
@@ -2140,7 +2140,7 @@ cudaError_t t2_backward(const T2Args &a_in, const T2Sorted &srt, int row, const 
     static int bv = -1;
     if (bv < 0) { const char *e = getenv("RFR_T2BV"); bv = e ? atoi(e) : 6; }   // r2w: 6 fastest
     static int dyn = -1;                           // RFR_T2BDYN=0: static stride
-    if (dyn < 0) { const char *e = getenv("RFR_T2BDYN"); dyn = (e && e[0] == '0') ? 0 : 1; }
+    if (dyn < 0) { const char *e = getenv("RFR_T2BDYN"); dyn = e ? std::max(0, atoi(e)) : 2; }
     a.dyn = dyn;
     if (dyn)
       cudaMemsetAsync(reinterpret_cast<char *>(a.plan) + offsetof(T2Plan, ctr) + 2 * sizeof(unsigned),
